@@ -1,0 +1,687 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU oracle for arXiv 1708.09746
+ * ("Faster Multiplication for Long Binary Polynomials", Chen, Cheng, Kuo, Li, Yang).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  It shares no code, header, table or constant
+ * generator with the CUDA product path (paper_1708_09746_b200/), and neither side imports the other.
+ *
+ * Citations: "P:a-b" = lines of PAPER.md (the paper's LaTeX source), with section / algorithm.
+ *
+ * Contents (SURVEY.md §8c numbering):
+ *   O2  carry-less word multiply: shift-and-xor clmul64 (or the x86 PCLMULQDQ instruction when the
+ *       CPU has it -- or_clmul_impl() says which), schoolbook, Karatsuba, single-output-word.
+ *       Definition: c_k = XOR_{i+j=k} a_i b_j.
+ *   O3  the paper's Alg. 5 step by step:
+ *         tower field TGF(2^128) (Def. of v_k P:658-665), Karatsuba per level
+ *         (sec 4.1.3), bottoming out at GF(256) log/exp tables that are
+ *         themselves derived from the bit-level recursion;
+ *         subspace vanishing polynomials s_k via s_{k+1} = s_k^2 + s_k (corollary P:718-721);
+ *         GF(2^128) = GF(2)[z]/(z^128+z^7+z^2+z+1) (sec 2.2.1) and the isomorphism
+ *         changeRepr (sec 4.3) fixed by the deterministic rule of DESIGN.md R9;
+ *         BasisCvt = Alg. 3 with VarSubs = Alg. 2, iBasisCvt (R7);
+ *         FFT_LCH = Alg. 1, iFFT (R8); pointmul; InterleavedCombine.
+ *   O4  product check modulo random irreducible degree-64 polynomials.
+ *
+ * All arithmetic is exact (GF(2) AND/XOR); no floating point anywhere.
+ */
+#include <stdint.h>
+#include <stddef.h>
+#include <stdlib.h>
+#include <string.h>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#include <cpuid.h>
+#endif
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef unsigned __int128 u128;
+
+/* ------------------------------------------------------------------------------------------ */
+/* O2: carry-less multiplication (the definition c_k = XOR_{i+j=k} a_i b_j)         */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Shift-and-xor: for every set bit i of a, add b * x^i. */
+static u128 clmul64_portable(uint64_t a, uint64_t b) {
+    u128 acc = 0;
+    for (int i = 0; i < 64; i++)
+        if ((a >> i) & 1) acc ^= ((u128)b) << i;
+    return acc;
+}
+
+#if defined(__x86_64__)
+__attribute__((target("pclmul,sse4.1")))
+static u128 clmul64_hw(uint64_t a, uint64_t b) {
+    __m128i x = _mm_set_epi64x(0, (long long)a);
+    __m128i y = _mm_set_epi64x(0, (long long)b);
+    __m128i z = _mm_clmulepi64_si128(x, y, 0x00);
+    uint64_t lo = (uint64_t)_mm_cvtsi128_si64(z);
+    uint64_t hi = (uint64_t)_mm_extract_epi64(z, 1);
+    return ((u128)hi << 64) | lo;
+}
+static int have_pclmul(void) {
+    unsigned a, b, c, d;
+    if (!__get_cpuid(1, &a, &b, &c, &d)) return 0;
+    return (c & bit_PCLMUL) != 0;
+}
+#endif
+
+static int g_use_hw = -1; /* -1 unknown, 0 portable, 1 PCLMULQDQ */
+
+static void clmul_init(void) {
+    if (g_use_hw >= 0) return;
+#if defined(__x86_64__)
+    g_use_hw = have_pclmul();
+#else
+    g_use_hw = 0;
+#endif
+}
+
+static inline u128 clmul64(uint64_t a, uint64_t b) {
+#if defined(__x86_64__)
+    if (g_use_hw == 1) return clmul64_hw(a, b);
+#endif
+    return clmul64_portable(a, b);
+}
+
+/* 1 if PCLMULQDQ is used behind clmul64, 0 if the shift-and-xor loop is. Forcing: mode 0/1. */
+int or_clmul_impl(void) { clmul_init(); return g_use_hw; }
+void or_clmul_force_portable(int portable) { clmul_init(); if (portable) g_use_hw = 0; }
+
+void or_clmul64(uint64_t a, uint64_t b, uint64_t *lo, uint64_t *hi) {
+    clmul_init();
+    u128 r = clmul64(a, b);
+    *lo = (uint64_t)r; *hi = (uint64_t)(r >> 64);
+}
+void or_clmul64_portable(uint64_t a, uint64_t b, uint64_t *lo, uint64_t *hi) {
+    u128 r = clmul64_portable(a, b);
+    *lo = (uint64_t)r; *hi = (uint64_t)(r >> 64);
+}
+
+/* Schoolbook: c (na+nb words) = XOR over all word pairs (i,j) of clmul(a_i,b_j) * x^(64(i+j)). */
+void or_mul_schoolbook(const uint64_t *a, size_t na, const uint64_t *b, size_t nb, uint64_t *c) {
+    clmul_init();
+    memset(c, 0, (na + nb) * sizeof(uint64_t));
+    for (size_t i = 0; i < na; i++) {
+        if (!a[i]) continue;
+        for (size_t j = 0; j < nb; j++) {
+            u128 p = clmul64(a[i], b[j]);
+            c[i + j] ^= (uint64_t)p;
+            c[i + j + 1] ^= (uint64_t)(p >> 64);
+        }
+    }
+}
+
+/* Karatsuba on n words (any n): a = a0 + x^(64h) a1, b likewise, h = ceil(n/2):
+ * a*b = a0b0 + x^(64h) [(a0+a1)(b0+b1) + a0b0 + a1b1] + x^(128h) a1b1.
+ * c must hold 2n words. Below 32 words it falls back to schoolbook. */
+static void kara_rec(const uint64_t *a, const uint64_t *b, size_t n, uint64_t *c, uint64_t *tmp) {
+    if (n <= 32) { or_mul_schoolbook(a, n, b, n, c); return; }
+    size_t h = (n + 1) / 2, l = n - h;          /* low part h words, high part l words (l <= h) */
+    uint64_t *sa = tmp, *sb = tmp + h, *mid = tmp + 2 * h, *rest = tmp + 4 * h;
+    kara_rec(a, b, h, c, rest);                  /* c[0, 2h)      = a0 b0 */
+    memset(c + 2 * h, 0, (2 * n - 2 * h) * sizeof(uint64_t));
+    if (l == h) {
+        kara_rec(a + h, b + h, l, c + 2 * h, rest); /* c[2h, 2n) = a1 b1 */
+    } else {
+        /* l < h: multiply the unequal high parts by schoolbook (only happens for odd n) */
+        or_mul_schoolbook(a + h, l, b + h, l, c + 2 * h);
+    }
+    for (size_t i = 0; i < h; i++) {
+        sa[i] = a[i] ^ (i < l ? a[h + i] : 0);
+        sb[i] = b[i] ^ (i < l ? b[h + i] : 0);
+    }
+    kara_rec(sa, sb, h, mid, rest);              /* mid = (a0+a1)(b0+b1), 2h words */
+    for (size_t i = 0; i < 2 * h; i++) mid[i] ^= c[i];                     /* - a0b0 */
+    for (size_t i = 0; i < 2 * l; i++) mid[i] ^= c[2 * h + i];             /* - a1b1 */
+    for (size_t i = 0; i < 2 * h; i++) c[h + i] ^= mid[i];
+}
+
+/* c (2n words) = a * b, both n words. */
+void or_mul_karatsuba(const uint64_t *a, const uint64_t *b, size_t n, uint64_t *c) {
+    clmul_init();
+    if (n == 0) return;
+    /* scratch: at each level 4h + rest; bounded by 8n + small */
+    uint64_t *tmp = (uint64_t *)calloc(8 * n + 256, sizeof(uint64_t));
+    kara_rec(a, b, n, c, tmp);
+    free(tmp);
+}
+
+/* Single output word w of a*b: c_w = XOR_{i+j=w} lo(a_i b_j) ^ XOR_{i+j=w-1} hi(a_i b_j). O(n). */
+uint64_t or_mul_word(const uint64_t *a, size_t na, const uint64_t *b, size_t nb, size_t w) {
+    clmul_init();
+    uint64_t r = 0;
+    for (size_t i = 0; i < na && i <= w; i++) {
+        size_t j = w - i;
+        if (j < nb) r ^= (uint64_t)clmul64(a[i], b[j]);
+        if (j >= 1 && j - 1 < nb) r ^= (uint64_t)(clmul64(a[i], b[j - 1]) >> 64);
+    }
+    return r;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* O3 part 1: the tower field TGF(2^(2^l)) in the basis (v_k)                    */
+/*   TGF(2^2) = GF(2)[x1]/(x1^2+x1+1);  TGF(2^(2^l)) = TGF(2^(2^(l-1)))[x_l]/(x_l^2+x_l+P)      */
+/*   with P = x_1 ... x_(l-1) = v_(2^(l-1)-1).  An element is the integer whose bit k is the     */
+/*   coordinate of v_k = prod x_(j+1)^(b_j) (Def. v_k).  Its upper half is the        */
+/*   coefficient of x_l since v_(2^(l-1)+j) = x_l v_j.                                           */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Pure recursion down to GF(2) = AND.  (a0 + a1 X)(b0 + b1 X), X^2 = X + P:
+ *   lo = a0b0 + a1b1 P,  hi = (a0+a1)(b0+b1) + a0b0   (Karatsuba, sec 4.1.3). */
+static u128 tmul_bits(u128 a, u128 b, int l) {
+    if (l == 0) return a & b & 1;
+    int h = 1 << (l - 1);
+    u128 mask = (((u128)1) << h) - 1;
+    u128 a0 = a & mask, a1 = a >> h, b0 = b & mask, b1 = b >> h;
+    u128 P = ((u128)1) << (h - 1);           /* v_(2^(l-1)-1); = 1 for l = 1 */
+    u128 p0 = tmul_bits(a0, b0, l - 1);
+    u128 p2 = tmul_bits(a1, b1, l - 1);
+    u128 p1 = tmul_bits(a0 ^ a1, b0 ^ b1, l - 1);
+    u128 lo = p0 ^ tmul_bits(p2, P, l - 1);
+    u128 hi = p1 ^ p0;
+    return lo | (hi << h);
+}
+
+/* GF(256) = TGF(2^8) log/exp tables (P:1073-1075 uses log/exp tables for the smallest fields),
+ * built from tmul_bits with the smallest generator of order 255 (SPEC S:207 rule). */
+static uint8_t g_exp[512];
+static int g_log[256];
+static int g_tables_ready = 0;
+static int g_generator = 0;
+
+static void tower_init(void) {
+    if (g_tables_ready) return;
+    for (int g = 2; g < 256; g++) {
+        int x = 1, ord = 0;
+        do { x = (int)tmul_bits((u128)x, (u128)g, 3); ord++; } while (x != 1 && ord < 300);
+        if (ord == 255) { g_generator = g; break; }
+    }
+    int x = 1;
+    for (int i = 0; i < 255; i++) {
+        g_exp[i] = (uint8_t)x; g_exp[i + 255] = (uint8_t)x;
+        g_log[x] = i;
+        x = (int)tmul_bits((u128)x, (u128)g_generator, 3);
+    }
+    g_exp[510] = g_exp[0]; g_exp[511] = g_exp[1];
+    g_log[0] = -1;
+    g_tables_ready = 1;
+}
+
+/* Tower product at level l (2^l-bit elements, l <= 7), recursion bottoming out at GF(256).
+ * Elements of a subfield are the small integers, so levels 0..3 all use the GF(256)
+ * table.  If one operand lies in the half-size subfield (b1 == 0 or a1 == 0) the recursion drops
+ * to 2 half-size products: Prop. 2 falling out of the formula. */
+static u128 tmul(u128 a, u128 b, int l) {
+    if (l <= 3) {
+        unsigned x = (unsigned)a, y = (unsigned)b;
+        if (!x || !y) return 0;
+        return g_exp[g_log[x] + g_log[y]];
+    }
+    int h = 1 << (l - 1);
+    u128 mask = (((u128)1) << h) - 1;
+    u128 a0 = a & mask, a1 = a >> h, b0 = b & mask, b1 = b >> h;
+    if (b1 == 0) return tmul(a0, b0, l - 1) | (tmul(a1, b0, l - 1) << h);
+    if (a1 == 0) return tmul(a0, b0, l - 1) | (tmul(a0, b1, l - 1) << h);
+    u128 P = ((u128)1) << (h - 1);
+    u128 p0 = tmul(a0, b0, l - 1);
+    u128 p2 = tmul(a1, b1, l - 1);
+    u128 p1 = tmul(a0 ^ a1, b0 ^ b1, l - 1);
+    u128 lo = p0 ^ tmul(p2, P, l - 1);
+    u128 hi = p1 ^ p0;
+    return lo | (hi << h);
+}
+
+static inline u128 mk(uint64_t lo, uint64_t hi) { return ((u128)hi << 64) | lo; }
+static inline void unmk(u128 x, uint64_t *out) { out[0] = (uint64_t)x; out[1] = (uint64_t)(x >> 64); }
+
+/* Exported tower multiply: a, b, r are 2-word little-endian 128-bit values. */
+void or_tower_mul(const uint64_t *a, const uint64_t *b, int level, uint64_t *r) {
+    tower_init();
+    unmk(tmul(mk(a[0], a[1]), mk(b[0], b[1]), level), r);
+}
+void or_tower_mul_bits(const uint64_t *a, const uint64_t *b, int level, uint64_t *r) {
+    unmk(tmul_bits(mk(a[0], a[1]), mk(b[0], b[1]), level), r);
+}
+int or_gf256_generator(void) { tower_init(); return g_generator; }
+
+/* ------------------------------------------------------------------------------------------ */
+/* O3 part 2: subspace vanishing polynomials s_k (Def. 2)                           */
+/*   s_0(x) = x, s_(k+1)(x) = s_k(x)^2 + s_k(x)  (recursivity corollary P:718-721),            */
+/*   i.e. s_k = s_1 applied k times with s_1(x) = x (x) x + x.                                  */
+/* ------------------------------------------------------------------------------------------ */
+static inline u128 s1(u128 x) { return tmul(x, x, 7) ^ x; }
+
+static u128 s_eval(int k, u128 x) {
+    for (int i = 0; i < k; i++) x = s1(x);
+    return x;
+}
+void or_s_eval(int k, const uint64_t *x, uint64_t *r) { tower_init(); unmk(s_eval(k, mk(x[0], x[1])), r); }
+
+/* ------------------------------------------------------------------------------------------ */
+/* O3 part 3: GF(2^128) in polynomial basis (sec 2.2.1) and changeRepr             */
+/* ------------------------------------------------------------------------------------------ */
+/* multiply by z modulo z^128 + z^7 + z^2 + z + 1 */
+static inline u128 gf128_mulz(u128 a) {
+    int carry = (int)(a >> 127);
+    a <<= 1;
+    if (carry) a ^= 0x87;
+    return a;
+}
+/* Shift-and-add: for every set bit i of b, add a * z^i mod g. */
+static u128 gf128_mul(u128 a, u128 b) {
+    u128 acc = 0;
+    for (int i = 0; i < 128; i++) {
+        if ((b >> i) & 1) acc ^= a;
+        a = gf128_mulz(a);
+    }
+    return acc;
+}
+void or_gf128_mul(const uint64_t *a, const uint64_t *b, uint64_t *r) {
+    unmk(gf128_mul(mk(a[0], a[1]), mk(b[0], b[1])), r);
+}
+
+/* Solve r^2 + r = c in GF(2^128) by Gaussian elimination on the GF(2)-linear map L(x) = x^2 + x
+ * (its kernel is {0, 1}).  Returns 0 and the numerically smaller root, or -1 if no root. */
+static int gf128_solve_as(u128 c, u128 *root) {
+    u128 col[128];
+    for (int i = 0; i < 128; i++) { u128 e = ((u128)1) << i; col[i] = gf128_mul(e, e) ^ e; }
+    /* augmented system: rows = output bits; we do elimination on columns stored as bit-vectors
+     * by transposing into row form: row r = (bits of column images at position r | rhs bit r) */
+    u128 row[128]; int rhs[128];
+    for (int r = 0; r < 128; r++) {
+        u128 v = 0;
+        for (int i = 0; i < 128; i++) if ((col[i] >> r) & 1) v |= ((u128)1) << i;
+        row[r] = v; rhs[r] = (int)((c >> r) & 1);
+    }
+    int pivcol[128]; int nr = 0;
+    for (int cidx = 0; cidx < 128 && nr < 128; cidx++) {
+        int p = -1;
+        for (int r = nr; r < 128; r++) if ((row[r] >> cidx) & 1) { p = r; break; }
+        if (p < 0) continue;
+        u128 t = row[p]; row[p] = row[nr]; row[nr] = t;
+        int tr = rhs[p]; rhs[p] = rhs[nr]; rhs[nr] = tr;
+        for (int r = 0; r < 128; r++)
+            if (r != nr && ((row[r] >> cidx) & 1)) { row[r] ^= row[nr]; rhs[r] ^= rhs[nr]; }
+        pivcol[nr] = cidx; nr++;
+    }
+    for (int r = nr; r < 128; r++) if (rhs[r]) return -1;   /* inconsistent */
+    u128 x = 0;  /* free variables = 0 */
+    for (int r = 0; r < nr; r++) if (rhs[r]) x |= ((u128)1) << pivcol[r];
+    u128 alt = x ^ 1;  /* the other root (kernel {0,1}) */
+    *root = (alt < x) ? alt : x;
+    return 0;
+}
+
+/* changeRepr (sec 4.3): Mcol[k] = image in GF(2^128) of tower basis element v_k, k < 128.
+ * Rule (R9): X_1^2+X_1 = 1, X_k^2+X_k = X_1...X_(k-1) (the defining relations P:643-650),
+ * each the numerically smaller root; v_k -> prod_{bit j of k} X_(j+1).
+ * psi_inv = Mcol (tower -> polynomial basis); psi = Mcol^(-1). */
+static u128 g_Mcol[128], g_psicol[128];
+static u128 g_X[8];
+static int g_psi_ready = 0;
+
+static int psi_init(void) {
+    if (g_psi_ready) return 0;
+    u128 prod = 1;
+    for (int k = 1; k <= 7; k++) {
+        if (gf128_solve_as(prod, &g_X[k]) != 0) return -1;
+        prod = gf128_mul(prod, g_X[k]);
+    }
+    for (int k = 0; k < 128; k++) {
+        u128 v = 1;
+        for (int j = 0; j < 7; j++) if ((k >> j) & 1) v = gf128_mul(v, g_X[j + 1]);
+        g_Mcol[k] = v;
+    }
+    /* invert M: Gauss-Jordan on [M | I] with M given by columns -> work on rows */
+    u128 A[128], B[128];
+    for (int r = 0; r < 128; r++) {
+        u128 v = 0;
+        for (int c = 0; c < 128; c++) if ((g_Mcol[c] >> r) & 1) v |= ((u128)1) << c;
+        A[r] = v; B[r] = ((u128)1) << r;
+    }
+    for (int c = 0; c < 128; c++) {
+        int p = -1;
+        for (int r = c; r < 128; r++) if ((A[r] >> c) & 1) { p = r; break; }
+        if (p < 0) return -2;
+        u128 t = A[p]; A[p] = A[c]; A[c] = t; t = B[p]; B[p] = B[c]; B[c] = t;
+        for (int r = 0; r < 128; r++)
+            if (r != c && ((A[r] >> c) & 1)) { A[r] ^= A[c]; B[r] ^= B[c]; }
+    }
+    /* now A = I, rows of B = rows of M^-1; psi column c = M^-1 e_c */
+    for (int c = 0; c < 128; c++) {
+        u128 v = 0;
+        for (int r = 0; r < 128; r++) if ((B[r] >> c) & 1) v |= ((u128)1) << r;
+        g_psicol[c] = v;
+    }
+    g_psi_ready = 1;
+    return 0;
+}
+
+static u128 apply_cols(const u128 *cols, u128 x) {
+    u128 r = 0;
+    for (int i = 0; i < 128; i++) if ((x >> i) & 1) r ^= cols[i];
+    return r;
+}
+static inline u128 psi(u128 x) { return apply_cols(g_psicol, x); }      /* poly -> tower */
+static inline u128 psi_inv(u128 x) { return apply_cols(g_Mcol, x); }   /* tower -> poly */
+
+int or_psi_init(void) { return psi_init(); }
+void or_psi(const uint64_t *x, uint64_t *r) { psi_init(); unmk(psi(mk(x[0], x[1])), r); }
+void or_psi_inv(const uint64_t *x, uint64_t *r) { psi_init(); unmk(psi_inv(mk(x[0], x[1])), r); }
+void or_psi_generator(int k, uint64_t *r) { psi_init(); unmk(g_X[k], r); }
+/* columns of psi (128 x 2 words) -- images of z^0..z^127 in the tower */
+void or_psi_columns(uint64_t *out) { psi_init(); for (int i = 0; i < 128; i++) unmk(g_psicol[i], out + 2 * i); }
+
+/* ------------------------------------------------------------------------------------------ */
+/* O3 part 4: BasisCvt (Alg. 3) via VarSubs (Alg. 2), and its inverse    */
+/* Arrays of 128-bit units (a 64-bit block occupies the low half).  XOR only.       */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Alg. 2 division by y^k' = x^(2^(l-1)) + x^(2^(l-1-K)) of one segment of len = 2^(l+sigma) words,
+ * "by repeatedly subtracting": for i = len-1 down to h, f[i-d] ^= f[i], d = h - h>>K. */
+/* optional trace of the Taylor steps (for the App. B pin): (len, K, d, xor count) per call */
+static long *g_trace = NULL; static int g_trace_n = 0, g_trace_max = 0;
+static void trace_step(size_t len, int K, size_t d, size_t xors) {
+    if (!g_trace || g_trace_n >= g_trace_max) return;
+    long *t = g_trace + 4 * g_trace_n++;
+    t[0] = (long)len; t[1] = K; t[2] = (long)d; t[3] = (long)xors;
+}
+static void taylor(u128 *f, size_t s, size_t len, int K) {
+    size_t h = len / 2, d = h - (h >> K);
+    trace_step(len, K, d, h);
+    for (size_t i = len - 1; i >= h; i--) {
+        f[s + i - d] ^= f[s + i];
+        if (i == h) break;
+    }
+}
+static void itaylor(u128 *f, size_t s, size_t len, int K) {
+    size_t h = len / 2, d = h - (h >> K);
+    for (size_t i = h; i < len; i++) f[s + i - d] ^= f[s + i];
+}
+
+static int floor_log2(int x) { int r = 0; while ((1 << (r + 1)) <= x) r++; return r; }
+
+/* CVT(f, base, m, sigma): convert the 2^m units of 2^sigma words starting at base (R4-R6). */
+static void cvt(u128 *f, size_t base, int m, int sigma) {
+    if (m <= 1) return;                                   /* deg <= 1: g = f (Alg. 3 line 1) */
+    int K = 1 << floor_log2(m - 1);                       /* largest power of two with 2^K <= deg */
+    for (int l = m; l >= K + 1; l--)                      /* VarSubs(f, y = s_K(x)) */
+        for (size_t s = 0; s < ((size_t)1 << (m + sigma)); s += ((size_t)1 << (l + sigma)))
+            taylor(f, base + s, (size_t)1 << (l + sigma), K);
+    cvt(f, base, m - K, sigma + K);                       /* BasisCvt(h(y)) over y (outer) */
+    for (size_t c = 0; c < ((size_t)1 << (m + sigma)); c += ((size_t)1 << (K + sigma)))
+        cvt(f, base + c, K, sigma);                       /* BasisCvt(q_i(x)) (inner) */
+}
+static void icvt(u128 *f, size_t base, int m, int sigma) {
+    if (m <= 1) return;
+    int K = 1 << floor_log2(m - 1);
+    for (size_t c = 0; c < ((size_t)1 << (m + sigma)); c += ((size_t)1 << (K + sigma)))
+        icvt(f, base + c, K, sigma);
+    icvt(f, base, m - K, sigma + K);
+    for (int l = K + 1; l <= m; l++)
+        for (size_t s = 0; s < ((size_t)1 << (m + sigma)); s += ((size_t)1 << (l + sigma)))
+            itaylor(f, base + s, (size_t)1 << (l + sigma), K);
+}
+
+/* Exported on arrays of n = 2^m units of `w` 64-bit words each (w = 1 or 2). */
+static void to128(const uint64_t *in, size_t n, int w, u128 *f) {
+    for (size_t i = 0; i < n; i++) f[i] = (w == 1) ? (u128)in[i] : mk(in[2 * i], in[2 * i + 1]);
+}
+static void from128(const u128 *f, size_t n, int w, uint64_t *out) {
+    for (size_t i = 0; i < n; i++) { if (w == 1) out[i] = (uint64_t)f[i]; else unmk(f[i], out + 2 * i); }
+}
+void or_basis_cvt(uint64_t *data, int m, int w) {
+    size_t n = (size_t)1 << m;
+    u128 *f = (u128 *)malloc(n * sizeof(u128));
+    to128(data, n, w, f); cvt(f, 0, m, 0); from128(f, n, w, data);
+    free(f);
+}
+/* record the Taylor steps BasisCvt performs on 2^m units: 4 longs per step; returns the count */
+int or_cvt_trace(int m, long *out, int max_steps) {
+    size_t n = (size_t)1 << m;
+    u128 *f = (u128 *)calloc(n, sizeof(u128));
+    g_trace = out; g_trace_n = 0; g_trace_max = max_steps;
+    cvt(f, 0, m, 0);
+    int cnt = g_trace_n;
+    g_trace = NULL;
+    free(f);
+    return cnt;
+}
+void or_ibasis_cvt(uint64_t *data, int m, int w) {
+    size_t n = (size_t)1 << m;
+    u128 *f = (u128 *)malloc(n * sizeof(u128));
+    to128(data, n, w, f); icvt(f, 0, m, 0); from128(f, n, w, data);
+    free(f);
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* O3 part 5: FFT_LCH (Alg. 1) at alpha = 0 over the tower, and its inverse   */
+/*   layer k = m-1 .. 0, block base b (multiple of 2^(k+1)), c = s_k(phi_v(b)):                 */
+/*     A[b+i] ^= c (x) A[b+2^k+i];  A[b+2^k+i] ^= A[b+i]      (second multiplier s_k(v_k) = 1,   */
+/*   Prop. 1).  Output i = f(phi_v(i)) (R2).                                 */
+/*   c is computed as s_k(phi_v(b)) = s_1(s_(k-1)(phi_v(b))), cached per block (SURVEY c.2 O3).  */
+/* ------------------------------------------------------------------------------------------ */
+
+/* mult[b >> (k+1)] for layer k, built bottom-up: layer 0 constants are phi_v(b) = b itself. */
+static void layer_constants(int m, int k, u128 *prev, u128 *out) {
+    size_t nb = (size_t)1 << (m - k - 1);
+    if (k == 0) { for (size_t j = 0; j < nb; j++) out[j] = (u128)(j << 1); return; }
+    /* block j of layer k has base b = j * 2^(k+1), which is block 2j of layer k-1 */
+    for (size_t j = 0; j < nb; j++) out[j] = s1(prev[2 * j]);
+}
+
+static u128 **all_constants(int m) {
+    u128 **C = (u128 **)calloc((size_t)(m > 0 ? m : 1), sizeof(u128 *));
+    for (int k = 0; k < m; k++) {
+        C[k] = (u128 *)malloc(((size_t)1 << (m - k - 1)) * sizeof(u128));
+        layer_constants(m, k, k ? C[k - 1] : NULL, C[k]);
+    }
+    return C;
+}
+static void free_constants(u128 **C, int m) { for (int k = 0; k < m; k++) free(C[k]); free(C); }
+
+static void fft(u128 *A, int m, u128 **C) {
+    for (int k = m - 1; k >= 0; k--) {
+        size_t half = (size_t)1 << k, nb = (size_t)1 << (m - k - 1);
+#pragma omp parallel for schedule(static) if (nb * half >= 4096)
+        for (size_t j = 0; j < nb; j++) {
+            size_t b = j << (k + 1);
+            u128 c = C[k][j];
+            for (size_t i = 0; i < half; i++) {
+                A[b + i] ^= tmul(A[b + half + i], c, 7);
+                A[b + half + i] ^= A[b + i];
+            }
+        }
+    }
+}
+static void ifft(u128 *A, int m, u128 **C) {
+    for (int k = 0; k < m; k++) {
+        size_t half = (size_t)1 << k, nb = (size_t)1 << (m - k - 1);
+#pragma omp parallel for schedule(static) if (nb * half >= 4096)
+        for (size_t j = 0; j < nb; j++) {
+            size_t b = j << (k + 1);
+            u128 c = C[k][j];
+            for (size_t i = 0; i < half; i++) {
+                A[b + half + i] ^= A[b + i];
+                A[b + i] ^= tmul(A[b + half + i], c, 7);
+            }
+        }
+    }
+}
+
+void or_fft(uint64_t *data, int m) {
+    tower_init();
+    size_t n = (size_t)1 << m;
+    u128 *A = (u128 *)malloc(n * sizeof(u128));
+    u128 **C = all_constants(m);
+    to128(data, n, 2, A); fft(A, m, C); from128(A, n, 2, data);
+    free_constants(C, m); free(A);
+}
+void or_ifft(uint64_t *data, int m) {
+    tower_init();
+    size_t n = (size_t)1 << m;
+    u128 *A = (u128 *)malloc(n * sizeof(u128));
+    u128 **C = all_constants(m);
+    to128(data, n, 2, A); ifft(A, m, C); from128(A, n, 2, data);
+    free_constants(C, m); free(A);
+}
+/* layer constant s_k(phi_v(b)) for block index j (b = j << (k+1)) of an m-layer FFT */
+void or_fft_constant(int m, int k, uint64_t j, uint64_t *r) {
+    tower_init();
+    u128 **C = all_constants(m);
+    unmk(C[k][j], r);
+    free_constants(C, m);
+}
+/* number of non-trivial multiplications (constant != 0 and != 1) issued by fft() on m layers
+ * with the top layer acting on nonzero upper halves: used to check the 1/2 n log n bound */
+uint64_t or_fft_mult_count(int m) {
+    tower_init();
+    u128 **C = all_constants(m);
+    uint64_t cnt = 0;
+    for (int k = 0; k < m; k++)
+        for (size_t j = 0; j < ((size_t)1 << (m - k - 1)); j++)
+            if (C[k][j] > 1) cnt += (uint64_t)1 << k;
+    free_constants(C, m);
+    return cnt;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* O3 part 6: Alg. 5 binPolyMul, w = 64                                           */
+/* ------------------------------------------------------------------------------------------ */
+static int ceil_log2_sz(size_t x) { int r = 0; while (((size_t)1 << r) < x) r++; return r; }
+
+/* Stage dump buffers (optional, may be NULL): each N x 2 words.
+ *   st_cvt_a/b : after BasisCvt + changeRepr (tower, novel basis)   -- Alg. 5 lines 3-6
+ *   st_fft_a/b : after FFT_LCH                                       -- lines 7-8
+ *   st_prod    : after pointmul                                      -- line 9
+ *   st_ifft    : after iFFT                                          -- line 10
+ *   st_icvt    : after iBasisCvt (tower)                             -- line 11
+ * c receives na+nb words (R13).  Returns 0, or a negative code on an internal
+ * assertion failure (bit 127 set, nonzero coefficient above L). */
+int or_alg5_mul(const uint64_t *a, uint64_t a_bits, const uint64_t *b, uint64_t b_bits, uint64_t *c,
+                uint64_t *st_cvt_a, uint64_t *st_cvt_b, uint64_t *st_fft_a, uint64_t *st_fft_b,
+                uint64_t *st_prod, uint64_t *st_ifft, uint64_t *st_icvt) {
+    tower_init();
+    if (psi_init() != 0) return -10;
+    size_t na = (a_bits + 63) / 64, nb = (b_bits + 63) / 64;
+    if (a_bits == 0 || b_bits == 0) { memset(c, 0, (na + nb) * sizeof(uint64_t)); return 0; }
+    size_t L = na + nb - 1;
+    int m = ceil_log2_sz(L);
+    size_t N = (size_t)1 << m;
+    u128 *A = (u128 *)calloc(N, sizeof(u128));
+    u128 *B = (u128 *)calloc(N, sizeof(u128));
+    /* Split: with w = 64 and little-endian words this is a copy; mask bits >= a_bits */
+    for (size_t j = 0; j < na; j++) {
+        uint64_t w = a[j];
+        if (j == na - 1 && (a_bits & 63)) w &= (((uint64_t)1) << (a_bits & 63)) - 1;
+        A[j] = w;
+    }
+    for (size_t j = 0; j < nb; j++) {
+        uint64_t w = b[j];
+        if (j == nb - 1 && (b_bits & 63)) w &= (((uint64_t)1) << (b_bits & 63)) - 1;
+        B[j] = w;
+    }
+    /* BasisCvt on the 64-bit blocks, before changeRepr */
+    cvt(A, 0, m, 0); cvt(B, 0, m, 0);
+    /* changeRepr */
+#pragma omp parallel for schedule(static) if (N >= 4096)
+    for (size_t i = 0; i < N; i++) { A[i] = psi(A[i]); B[i] = psi(B[i]); }
+    if (st_cvt_a) from128(A, N, 2, st_cvt_a);
+    if (st_cvt_b) from128(B, N, 2, st_cvt_b);
+    /* FFT_LCH at alpha = 0 */
+    u128 **C = all_constants(m);
+    fft(A, m, C); fft(B, m, C);
+    if (st_fft_a) from128(A, N, 2, st_fft_a);
+    if (st_fft_b) from128(B, N, 2, st_fft_b);
+    /* pointmul */
+#pragma omp parallel for schedule(static) if (N >= 4096)
+    for (size_t i = 0; i < N; i++) A[i] = tmul(A[i], B[i], 7);
+    if (st_prod) from128(A, N, 2, st_prod);
+    /* iFFT_LCH */
+    ifft(A, m, C);
+    if (st_ifft) from128(A, N, 2, st_ifft);
+    /* iBasisCvt in the tower representation */
+    icvt(A, 0, m, 0);
+    if (st_icvt) from128(A, N, 2, st_icvt);
+    /* changeRepr back */
+    int err = 0;
+#pragma omp parallel for schedule(static) if (N >= 4096)
+    for (size_t i = 0; i < N; i++) A[i] = psi_inv(A[i]);
+    for (size_t i = 0; i < N; i++) {
+        if ((A[i] >> 127) & 1) err = -1;          /* deg C_i <= 126 */
+        if (i >= L && A[i] != 0) err = -2;         /* only L product blocks */
+    }
+    /* InterleavedCombine: out[w] = lo64(C_w) ^ hi64(C_(w-1)) */
+    for (size_t w = 0; w < na + nb; w++) {
+        uint64_t v = 0;
+        if (w < N) v ^= (uint64_t)A[w];
+        if (w >= 1 && w - 1 < N) v ^= (uint64_t)(A[w - 1] >> 64);
+        c[w] = v;
+    }
+    free_constants(C, m);
+    free(A); free(B);
+    return err;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* O4: product check modulo random irreducible degree-64 polynomials (SURVEY c.2 O4)            */
+/*   p = x^64 + r(x); x^64 == r (mod p).                                                        */
+/* ------------------------------------------------------------------------------------------ */
+static uint64_t mulmod64(uint64_t x, uint64_t y, uint64_t r) {
+    u128 t = clmul64(x, y);
+    uint64_t hi = (uint64_t)(t >> 64), lo = (uint64_t)t;
+    /* t = hi x^64 + lo == hi r + lo; hi r has degree < 127; fold twice */
+    while (hi) {
+        u128 u = clmul64(hi, r);
+        lo ^= (uint64_t)u;
+        hi = (uint64_t)(u >> 64);
+    }
+    return lo;
+}
+/* polynomial gcd over GF(2) of a (deg <= 64, as u128) and p */
+static int deg128(u128 x) { int d = -1; while (x) { d++; x >>= 1; } return d; }
+static u128 pgcd(u128 a, u128 b) {
+    while (b) {
+        while (a && deg128(a) >= deg128(b)) a ^= b << (deg128(a) - deg128(b));
+        u128 t = a; a = b; b = t;
+    }
+    return a;
+}
+/* Rabin test for degree 64: x^(2^64) == x mod p, gcd(x^(2^32) - x, p) = 1. */
+int or_is_irreducible64(uint64_t r) {
+    clmul_init();
+    if (!(r & 1)) return 0;
+    uint64_t x = 2, t = x;
+    uint64_t t32 = 0;
+    for (int i = 0; i < 64; i++) { t = mulmod64(t, t, r); if (i == 31) t32 = t; }
+    if (t != x) return 0;
+    u128 p = ((u128)1 << 64) | r;
+    u128 g = pgcd((u128)(t32 ^ x), p);
+    return deg128(g) == 0;
+}
+/* residue of a polynomial of n words modulo p (Horner from the top word: r <- r x^64 + w) */
+uint64_t or_poly_mod(const uint64_t *a, size_t n, uint64_t r) {
+    clmul_init();
+    uint64_t acc = 0;
+    for (size_t i = n; i-- > 0;) acc = mulmod64(acc, r, r) ^ a[i];
+    return acc;
+}
+uint64_t or_mulmod64(uint64_t x, uint64_t y, uint64_t r) { clmul_init(); return mulmod64(x, y, r); }
+
+int or_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+void or_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
