@@ -1,0 +1,81 @@
+/*
+ * gf2x.h -- C ABI of the B200 (sm_100a) GF(2)[x] multiplier (arXiv 1708.09746, Alg. 5).
+ *
+ * Operation (§2.1 P:211-214 and Alg. 5 input/output P:886-888): given binary polynomials
+ * a(x), b(x) as bit sequences of lengths a_bits, b_bits, compute c(x) = a(x) * b(x) in GF(2)[x].
+ * The product is computed by the paper's Alg. 5: Split into 64-bit blocks, BasisCvt
+ * (Alg. 3) to the LCH novel polynomial basis, changeRepr into the tower field TGF(2^128) (§3.2),
+ * FFT_LCH (Alg. 1) at 2^m points, pointwise products, iFFT_LCH, iBasisCvt, changeRepr back and
+ * InterleavedCombine.  The result is exact and unique (no rounding).
+ *
+ * Packing (R12): little-endian 64-bit words; bit i of word j is the
+ * coefficient of x^(64 j + i).  n_x = ceil(x_bits / 64) words per operand.  The product occupies
+ * n_a + n_b words (R13); all of them are written, zero above degree a_bits+b_bits-2.
+ * Bits of a/b at positions >= a_bits/b_bits are ignored.
+ *
+ * Memory: a, b, c (and ws) are DEVICE pointers owned by the caller.  c must not overlap a or b
+ * (GF2X_EINVAL).  Calls are enqueued on `stream` and return after enqueue (no host sync in steady
+ * state); kernel faults surface at the caller's next synchronisation.  The first call on a device
+ * builds and uploads the constant tables (synchronous, once).
+ *
+ * Errors: every entry point returns a gf2x_status; detail text for the last error of the calling
+ * thread is available from gf2x_last_error().  No C++ exception crosses this boundary.
+ *
+ * Size cap: FFT size N = 2^ceil(log2(n_a + n_b - 1)) <= 2^32 (multipliers stay in TGF(2^32),
+ * §4.4); larger requests return GF2X_ETOOBIG.
+ */
+#ifndef GF2X_B200_H
+#define GF2X_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GF2X_OK = 0,
+    GF2X_EINVAL = 1,   /* bad argument: null pointer with nonzero size, aliasing, negative batch */
+    GF2X_ETOOBIG = 2,  /* N > 2^32 or the workspace cannot be represented */
+    GF2X_ENOMEM = 3,   /* device allocation failed / workspace too small */
+    GF2X_ECUDA = 4,    /* CUDA runtime error (see gf2x_last_error) */
+    GF2X_ENCCL = 5     /* NCCL error (multi-GPU entry points) */
+} gf2x_status;
+
+/* c = a * b.  `stream` is a cudaStream_t (0 = legacy default stream). */
+gf2x_status gf2x_mul(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits,
+                     uint64_t* c, void* stream);
+
+/* `batch` independent products of equal sizes, operands contiguous:
+ * a_i at a + i*n_a, b_i at b + i*n_b, c_i at c + i*(n_a+n_b).  batch == 0 is a no-op. */
+gf2x_status gf2x_mul_batched(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits,
+                             uint64_t* c, int64_t batch, void* stream);
+
+/* Workspace bytes a call with these sizes needs (0 for empty products). */
+size_t gf2x_workspace_bytes(uint64_t a_bits, uint64_t b_bits, int64_t batch);
+
+/* As gf2x_mul_batched but with a caller-provided device workspace of ws_bytes
+ * (>= gf2x_workspace_bytes, 256-byte aligned) instead of the library's per-stream cache. */
+gf2x_status gf2x_mul_ws(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits,
+                        uint64_t* c, int64_t batch, void* ws, size_t ws_bytes, void* stream);
+
+/* Number of kernels one gf2x_mul_batched call with these sizes enqueues (for launch accounting). */
+int gf2x_launch_count(uint64_t a_bits, uint64_t b_bits, int64_t batch);
+
+/* Debug / parity hook: run only the forward pipeline up to a stage and copy the FFT-domain
+ * intermediate of operand a into `out` (device, N*2 words, tower representation):
+ *   stage 1 = after BasisCvt + changeRepr, 2 = after FFT_LCH, 3 = after pointmul,
+ *   4 = after iFFT_LCH, 5 = after iBasisCvt (tower).  Returns EINVAL for other stages. */
+gf2x_status gf2x_debug_stage(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits,
+                             int stage, uint64_t* out, void* stream);
+
+const char* gf2x_status_string(gf2x_status s);
+const char* gf2x_last_error(void);      /* thread-local detail text of the last failure */
+gf2x_status gf2x_release(int device);   /* free cached workspaces and constant tables of a device */
+const char* gf2x_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GF2X_B200_H */

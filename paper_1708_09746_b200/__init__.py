@@ -1,0 +1,134 @@
+"""B200-native GF(2)[x] multiplication (arXiv 1708.09746, Alg. 5) -- thin Python binding.
+
+The binding only marshals arguments into the C ABI of include/gf2x.h (libgf2x_b200.so, built
+in-tree for sm_100a by build.py).  Every step of the multiplication runs in the library's CUDA
+kernels; there is no CPU fallback: if the shared library is missing or fails to load, importing
+the compute entry points raises.
+
+Tensors are torch.uint64 (or int64 reinterpreted) CUDA tensors holding little-endian 64-bit words,
+bit i of word j = coefficient of x^(64 j + i).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgf2x_b200.so")
+
+STATUS = {0: "GF2X_OK", 1: "GF2X_EINVAL", 2: "GF2X_ETOOBIG", 3: "GF2X_ENOMEM", 4: "GF2X_ECUDA", 5: "GF2X_ENCCL"}
+
+# every symbol include/gf2x.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "gf2x_mul", "gf2x_mul_batched", "gf2x_workspace_bytes", "gf2x_mul_ws", "gf2x_launch_count",
+    "gf2x_debug_stage", "gf2x_status_string", "gf2x_last_error", "gf2x_release", "gf2x_version",
+]
+
+
+class Gf2xError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libgf2x_b200.so (raises if it is absent: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise Gf2xError(f"{path} not built; run python -m paper_1708_09746_b200.build")
+    L = ctypes.CDLL(path)
+    u64, i64, vp, i32, sz = ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    L.gf2x_mul.argtypes = [vp, u64, vp, u64, vp, vp]
+    L.gf2x_mul_batched.argtypes = [vp, u64, vp, u64, vp, i64, vp]
+    L.gf2x_workspace_bytes.argtypes = [u64, u64, i64]
+    L.gf2x_workspace_bytes.restype = sz
+    L.gf2x_mul_ws.argtypes = [vp, u64, vp, u64, vp, i64, vp, sz, vp]
+    L.gf2x_launch_count.argtypes = [u64, u64, i64]
+    L.gf2x_debug_stage.argtypes = [vp, u64, vp, u64, i32, vp, vp]
+    L.gf2x_status_string.argtypes = [i32]
+    L.gf2x_status_string.restype = ctypes.c_char_p
+    L.gf2x_last_error.restype = ctypes.c_char_p
+    L.gf2x_release.argtypes = [i32]
+    L.gf2x_version.restype = ctypes.c_char_p
+    for name in ("gf2x_mul", "gf2x_mul_batched", "gf2x_mul_ws", "gf2x_debug_stage", "gf2x_release"):
+        getattr(L, name).restype = i32
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        detail = load().gf2x_last_error().decode()
+        raise Gf2xError(f"{STATUS.get(status, status)}: {detail}")
+
+
+def _stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    import torch
+    assert t.is_cuda and t.is_contiguous() and t.dtype in (torch.uint64, torch.int64), "need contiguous CUDA 64-bit words"
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def nwords(bits: int) -> int:
+    return (bits + 63) // 64
+
+
+def gf2x_mul(a, a_bits: int, b, b_bits: int, c=None, stream=None):
+    """c = a * b over GF(2); a, b CUDA word tensors; returns c (n_a + n_b words)."""
+    import torch
+    if c is None:
+        c = torch.empty(nwords(a_bits) + nwords(b_bits), dtype=torch.uint64, device=a.device)
+    _check(load().gf2x_mul(_ptr(a), a_bits, _ptr(b), b_bits, _ptr(c), _stream_ptr(stream)))
+    return c
+
+
+def gf2x_mul_batched(a, a_bits: int, b, b_bits: int, batch: int, c=None, stream=None):
+    """`batch` products; a is (batch, n_a) (or flat), b (batch, n_b); returns (batch, n_a + n_b)."""
+    import torch
+    n_out = nwords(a_bits) + nwords(b_bits)
+    if c is None:
+        c = torch.empty(batch, n_out, dtype=torch.uint64, device=a.device)
+    _check(load().gf2x_mul_batched(_ptr(a), a_bits, _ptr(b), b_bits, _ptr(c), batch, _stream_ptr(stream)))
+    return c
+
+
+def gf2x_workspace_bytes(a_bits: int, b_bits: int, batch: int = 1) -> int:
+    return int(load().gf2x_workspace_bytes(a_bits, b_bits, batch))
+
+
+def gf2x_mul_ws(a, a_bits: int, b, b_bits: int, c, batch: int, ws, stream=None):
+    _check(load().gf2x_mul_ws(_ptr(a), a_bits, _ptr(b), b_bits, _ptr(c), batch,
+                              ctypes.c_void_p(ws.data_ptr()), ws.numel() * ws.element_size(), _stream_ptr(stream)))
+    return c
+
+
+def gf2x_launch_count(a_bits: int, b_bits: int, batch: int = 1) -> int:
+    return int(load().gf2x_launch_count(a_bits, b_bits, batch))
+
+
+def gf2x_debug_stage(a, a_bits: int, b, b_bits: int, stage: int, stream=None):
+    """FFT-domain intermediate of operand a (tower representation) after `stage` (1..5)."""
+    import torch
+    L = (nwords(a_bits) + nwords(b_bits) - 1)
+    N = 1 << max(0, (L - 1).bit_length())
+    out = torch.empty(N, 2, dtype=torch.uint64, device=a.device)
+    _check(load().gf2x_debug_stage(_ptr(a), a_bits, _ptr(b), b_bits, stage, _ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def gf2x_release(device: int = 0):
+    _check(load().gf2x_release(device))
+
+
+def version() -> str:
+    return load().gf2x_version().decode()

@@ -1,0 +1,93 @@
+// gf2x_device.cuh -- device building blocks for the sm_100a GF(2)[x] multiplier.
+//
+// Tower elements TGF(2^128) are uint4 (four 32-bit limbs; limb L holds coordinates 32L..32L+31,
+// i.e. limb L is the TGF(2^32) coefficient of v_(32L)).
+// FFT multipliers are < 2^32 (they lie in TGF(2^32) for N <= 2^32 points), so by
+// Prop. 2 a butterfly multiplies each limb independently by the same TGF(2^32) constant.
+#pragma once
+#include <stdint.h>
+
+#define GF2X_HD __host__ __device__
+#define GF2X_INLINE __forceinline__
+
+namespace gf2x_dev {
+
+// ---------------------------------------------------------------------------------------------
+// SWAR multiplication of every small block of a 32-bit word by a generator (tower relations
+// x_1^2 = x_1 + 1, x_2^2 = x_2 + x_1).
+// ---------------------------------------------------------------------------------------------
+// each GF(4) pair (b0 + b1 x1) -> x1 (b0 + b1 x1) = b1 + (b0 + b1) x1
+GF2X_HD GF2X_INLINE uint32_t mulx1(uint32_t u) {
+    return ((u >> 1) & 0x55555555u) | ((u ^ (u << 1)) & 0xAAAAAAAAu);
+}
+// each GF(16) nibble (n0 + n1 x2) -> x2 (n0 + n1 x2) = x1 n1 + (n0 + n1) x2
+GF2X_HD GF2X_INLINE uint32_t mulx2(uint32_t u) {
+    return mulx1((u >> 2) & 0x33333333u) | ((u ^ (u << 2)) & 0xCCCCCCCCu);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Method of four Russians with 4-bit chunks (§4.3-4.4 use M4R; chunk width chosen for sm_100a:
+// a 16-entry table row spans 16 banks, so the 32 lanes of a warp never conflict).
+// Table for constant c: tab[16 t + x] = c * (x v_(4t)) = (c v_(4t)) * x, x in GF(16), t < 8.
+// ---------------------------------------------------------------------------------------------
+struct WtTables {  // M4R-8 tables of the fixed linear maps c -> c * v_(4t), t = 1..7
+    const uint32_t* wt;  // [7][4][256]
+};
+
+// Cooperative build by the 32 lanes of a warp (c warp-uniform).  Lane l writes entries
+// 16 (l/4) + 4 (l%4) + {0,1,2,3}.  Caller must __syncwarp() before use.
+__device__ GF2X_INLINE void build_tab(uint32_t* tab, uint32_t c, const uint32_t* __restrict__ wt) {
+    const int lane = threadIdx.x & 31;
+    const int t = lane >> 2, q = lane & 3;
+    uint32_t w = c;
+    if (t) {
+        const uint32_t* T = wt + (t - 1) * 1024;
+        w = __ldg(T + (c & 255)) ^ __ldg(T + 256 + ((c >> 8) & 255)) ^
+            __ldg(T + 512 + ((c >> 16) & 255)) ^ __ldg(T + 768 + (c >> 24));
+    }
+    const uint32_t w1 = mulx1(w), w2 = mulx2(w), w3 = mulx1(w2);
+    const uint32_t base = ((q & 1) ? w2 : 0u) ^ ((q & 2) ? w3 : 0u);
+    uint32_t* d = tab + 16 * t + 4 * q;
+    d[0] = base;
+    d[1] = base ^ w;
+    d[2] = base ^ w1;
+    d[3] = base ^ w ^ w1;
+}
+
+__device__ GF2X_INLINE uint32_t m4r4_word(const uint32_t* tab, uint32_t x) {
+    uint32_t r = tab[x & 15];
+    r ^= tab[16 + ((x >> 4) & 15)];
+    r ^= tab[32 + ((x >> 8) & 15)];
+    r ^= tab[48 + ((x >> 12) & 15)];
+    r ^= tab[64 + ((x >> 16) & 15)];
+    r ^= tab[80 + ((x >> 20) & 15)];
+    r ^= tab[96 + ((x >> 24) & 15)];
+    r ^= tab[112 + (x >> 28)];
+    return r;
+}
+
+__device__ GF2X_INLINE uint4 m4r4_mul(const uint32_t* tab, uint4 a) {
+    return make_uint4(m4r4_word(tab, a.x), m4r4_word(tab, a.y), m4r4_word(tab, a.z), m4r4_word(tab, a.w));
+}
+
+__device__ GF2X_INLINE uint4 xor4(uint4 a, uint4 b) {
+    return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
+}
+
+// ---------------------------------------------------------------------------------------------
+// 32x32 bit transpose: on return x[j] bit e = (old x[e]) bit j.
+// ---------------------------------------------------------------------------------------------
+GF2X_HD GF2X_INLINE void transpose32(uint32_t* x) {
+    uint32_t m = 0x0000FFFFu;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1, m ^= (m << s)) {
+#pragma unroll
+        for (int k = 0; k < 32; k = (k + s + 1) & ~s) {
+            const uint32_t t = ((x[k] >> s) ^ x[k + s]) & m;
+            x[k] ^= t << s;
+            x[k + s] ^= t;
+        }
+    }
+}
+
+}  // namespace gf2x_dev
