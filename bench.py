@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""Benchmark: GF(2)[x] multiply at the paper's headline sizes (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4b|c4a|c3|c2|c1] [--impl ours|reference]
+
+A "step" is one whole Alg. 5 multiply (every §8(a) row: Split, BasisCvt, changeRepr, FFT_LCH x2,
+pointmul, iFFT_LCH, iBasisCvt, changeRepr^-1, InterleavedCombine) of two seeded uniformly random
+operands (gf2x_synth recipe) already resident in HBM.  Time = CUDA events on the library's stream
+around exactly K steps after W warm-ups, barrier + synchronize on both sides, max over ranks.
+value = input Gbit/s = (a_bits + b_bits) * steps * n_gpus / max-rank time (whole job).
+
+Multi-GPU (torchrun, N > 1): round 1 runs one independent replica multiply per GPU (no data-path
+collective; "scaling": "weak"); the sharded FFT of SURVEY §8(e) is future work.
+
+--impl reference runs the repo's CPU oracle (oracle/, the paper's Alg. 5 step by step) on the box's
+host cores on a bounded sample of the same workload (rank 0 only) and prints the same JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from gf2x_synth import CONFIGS, DEFAULT_SEED, batch_pair, operand_pair  # noqa: E402
+
+METRIC = "ms per 2^28- and 2^29-bit GF(2)[x] multiply; input Gbit/s; % of HBM roofline"
+UNIT = "input Gbit/s"
+PAPER_GBITS = {"c4a": (2 * 2**28) / 2.302 / 1e9, "c4b": (2 * 2**29) / 4.812 / 1e9, "c3": (2 * 2**24) / 0.104 / 1e9}
+PAPER_MS = {"c4a": 2302.0, "c4b": 4812.0, "c3": 104.0}
+WORKLOAD = {
+    "c1": "single 2^16-bit x 2^16-bit GF(2)[x] multiply (FFT over 2^11 TGF(2^128) points)",
+    "c2": "4096 independent 2^14-bit x 2^14-bit multiplies (batched, 2^9 points each)",
+    "c3": "single 2^24-bit x 2^24-bit multiply (2^19 points)",
+    "c4a": "single 2^28-bit x 2^28-bit multiply (2^23 points), paper headline size",
+    "c4b": "single 2^29-bit x 2^29-bit multiply (2^24 points), paper headline size",
+}
+
+
+def rank_info():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append((time.time(), ln.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        sm, mx, reasons = [], None, set()
+        for ts, ln in self.lines:
+            if ts < t0 or ts > t1:
+                continue
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(cfg: str, sample_bits: int):
+    """The oracle (Alg. 5, plain C, OpenMP) timed on the host cores on a bounded sample."""
+    import oracle as O
+    O.build()
+    a, b = operand_pair(sample_bits, DEFAULT_SEED)
+    t0 = time.perf_counter()
+    O.alg5_mul(a, sample_bits, b, sample_bits)
+    dt = time.perf_counter() - t0
+    return {"value": round(2 * sample_bits / dt / 1e9, 6), "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+            "sample": f"one oracle Alg. 5 multiply of two 2^{sample_bits.bit_length() - 1}-bit operands "
+                      f"(same seeded recipe as {cfg}); {dt * 1e3:.1f} ms; clmul={O.clmul_impl()}"}
+
+
+def run_reference(args):
+    rank, world, _ = rank_info()
+    if rank != 0:
+        return 0
+    import oracle as O
+    O.build()
+    sample_bits = 1 << 22
+    a, b = operand_pair(sample_bits, DEFAULT_SEED)
+    for _ in range(args.warmup):
+        O.alg5_mul(a, sample_bits, b, sample_bits)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.alg5_mul(a, sample_bits, b, sample_bits)
+    dt = time.perf_counter() - t0
+    val = 2 * sample_bits * args.steps / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": WORKLOAD[args.config], "config": args.config},
+        "cpu_baseline": {"value": round(val, 6), "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+                         "sample": f"each step: one oracle Alg. 5 multiply of two 2^22-bit operands (bounded sample "
+                                   f"of {args.config}, same seeded recipe); clmul={O.clmul_impl()}"},
+        "e2e": {"value": round(val, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4b", choices=["c1", "c2", "c3", "c4a", "c4b"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_1708_09746_b200 as G
+
+    rank, world, local = rank_info()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    G.load()
+    bits, batch = CONFIGS[args.config]
+    seed = DEFAULT_SEED + 2 * rank  # each replica its own operand pair
+    if batch == 1:
+        a, b = operand_pair(bits, seed)
+    else:
+        a, b = batch_pair(bits, batch, seed)
+    n = G.nwords(bits)
+    n_out = 2 * n
+    dev = torch.device("cuda", local)
+    da = torch.from_numpy(a.reshape(-1).view(np.int64)).to(dev).view(torch.uint64)
+    db = torch.from_numpy(b.reshape(-1).view(np.int64)).to(dev).view(torch.uint64)
+    dc = torch.empty(n_out * batch, dtype=torch.uint64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if batch == 1:
+            G.gf2x_mul(da, bits, db, bits, dc, stream=stream)
+        else:
+            G.gf2x_mul_batched(da, bits, db, bits, batch, dc, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    G.profile_enable(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.time()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.time()
+    if dist:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    prof = G.profile_report()
+    G.profile_enable(False)
+    time.sleep(0.25)
+    sampler.stop()
+    clocks = sampler.summary(t_wall0 - 0.05, t_wall1 + 0.05)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    ms_step = ms / args.steps
+    in_bits = 2 * bits * batch
+    value = in_bits * world / (ms_step * 1e-3) / 1e9
+
+    # ---- end to end through the public API with pinned host buffers
+    ha = torch.from_numpy(a.reshape(-1).view(np.int64)).pin_memory()
+    hb = torch.from_numpy(b.reshape(-1).view(np.int64)).pin_memory()
+    hc = torch.empty(n_out * batch, dtype=torch.int64).pin_memory()
+    ea = torch.empty(n * batch, dtype=torch.int64, device=dev)
+    eb = torch.empty(n * batch, dtype=torch.int64, device=dev)
+    ec = torch.empty(n_out * batch, dtype=torch.int64, device=dev)
+
+    def e2e_step():
+        ea.copy_(ha, non_blocking=True)
+        eb.copy_(hb, non_blocking=True)
+        if batch == 1:
+            G.gf2x_mul(ea, bits, eb, bits, ec, stream=stream)
+        else:
+            G.gf2x_mul_batched(ea, bits, eb, bits, batch, ec, stream=stream)
+        hc.copy_(ec, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_val = in_bits * world / (e2e_ms / args.e2e_steps * 1e-3) / 1e9
+    # result check of the e2e copy against the device-resident run (both from the library)
+    assert torch.equal(hc.view(torch.int64), dc.cpu().view(torch.int64))
+
+    # ---- roofline of the dominant kernel (live CUDA-event durations over the timed region)
+    peak, peak_src = load_peaks()
+    dom = max(prof, key=lambda r: r["ms"])
+    per_launch_ms = dom["ms"] / dom["launches"]
+    per_launch_bytes = dom["bytes"] / dom["launches"]
+    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config, {}).get(dom["kernel"])
+        except Exception:
+            traffic = None
+    step_bytes = sum(r["bytes"] for r in prof) / args.steps
+    kern_ms = sum(r["ms"] for r in prof) / args.steps
+    launches = G.gf2x_launch_count(bits, bits, batch)
+
+    line = {
+        "metric": METRIC,
+        "value": round(value, 4),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": round(value / (PAPER_GBITS[args.config] * world), 2) if args.config in PAPER_GBITS else None,
+        "vs_baseline_note": "ratio to the paper's own CPU number for this workload (Table 2, Haswell E3-1245 v3, "
+                            "TGF(2^128) row): context, not the target",
+        "dtype": "u64",
+        "data": "synthetic",
+        "config": {
+            "workload": WORKLOAD[args.config], "config": args.config, "operand_bits": bits, "batch": batch,
+            "fft_points": 1 << max(0, (2 * n - 2).bit_length()), "parallelism": "replicas" if world > 1 else "single",
+            "seed": DEFAULT_SEED, "l2": "working set > 126 MB L2 (operands + 2 spectra), no flush" if bits >= 1 << 28
+            else "working set may be L2-resident (small config)",
+            "paper_ms_haswell": PAPER_MS.get(args.config),
+        },
+        "roofline": {
+            "bound": "hbm", "kernel": dom["kernel"], "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": per_launch_bytes, "ms_per_launch": round(per_launch_ms, 5),
+            "step_algorithmic_bytes": step_bytes,
+            "step_frac_of_hbm": round(step_bytes / (kern_ms * 1e-3) / 1e9 / peak, 4),
+            "b_min_frac": round(32.0 * n * batch / (ms_step * 1e-3) / 1e9 / peak, 5),
+        },
+        "kernels": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in prof],
+        "clocks": clocks,
+        "e2e": {"value": round(e2e_val, 4), "unit": UNIT, "h2d_bytes_per_step": 2 * n * 8 * batch,
+                "d2h_bytes_per_step": n_out * 8 * batch, "ms_per_step": round(e2e_ms / args.e2e_steps, 4)},
+        "gpu_launches": launches * args.steps,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config, 1 << 24 if bits >= 1 << 24 else bits)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

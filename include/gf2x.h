@@ -70,6 +70,15 @@ int gf2x_launch_count(uint64_t a_bits, uint64_t b_bits, int64_t batch);
 gf2x_status gf2x_debug_stage(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits,
                              int stage, uint64_t* out, void* stream);
 
+/* Measurement hook (bench.py): while enabled, every kernel the library enqueues from the calling
+ * thread is bracketed by CUDA events on its stream.  gf2x_profile_report synchronises those events
+ * and writes a JSON array into buf (cap bytes, NUL-terminated):
+ *   [{"kernel": name, "launches": n, "ms": total device ms, "bytes": algorithmic HBM bytes}, ...]
+ * and returns the length needed (call again with a larger buf if it exceeds cap).  Enabling or
+ * disabling clears the record. */
+gf2x_status gf2x_profile_enable(int on);
+int gf2x_profile_report(char* buf, size_t cap);
+
 const char* gf2x_status_string(gf2x_status s);
 const char* gf2x_last_error(void);      /* thread-local detail text of the last failure */
 gf2x_status gf2x_release(int device);   /* free cached workspaces and constant tables of a device */

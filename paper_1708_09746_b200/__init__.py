@@ -21,7 +21,8 @@ STATUS = {0: "GF2X_OK", 1: "GF2X_EINVAL", 2: "GF2X_ETOOBIG", 3: "GF2X_ENOMEM", 4
 # every symbol include/gf2x.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "gf2x_mul", "gf2x_mul_batched", "gf2x_workspace_bytes", "gf2x_mul_ws", "gf2x_launch_count",
-    "gf2x_debug_stage", "gf2x_status_string", "gf2x_last_error", "gf2x_release", "gf2x_version",
+    "gf2x_debug_stage", "gf2x_profile_enable", "gf2x_profile_report", "gf2x_status_string", "gf2x_last_error",
+    "gf2x_release", "gf2x_version",
 ]
 
 
@@ -53,6 +54,10 @@ def load(path: str = LIB_PATH):
     L.gf2x_last_error.restype = ctypes.c_char_p
     L.gf2x_release.argtypes = [i32]
     L.gf2x_version.restype = ctypes.c_char_p
+    L.gf2x_profile_enable.argtypes = [i32]
+    L.gf2x_profile_enable.restype = i32
+    L.gf2x_profile_report.argtypes = [ctypes.c_char_p, sz]
+    L.gf2x_profile_report.restype = i32
     for name in ("gf2x_mul", "gf2x_mul_batched", "gf2x_mul_ws", "gf2x_debug_stage", "gf2x_release"):
         getattr(L, name).restype = i32
     _lib = L
@@ -128,6 +133,20 @@ def gf2x_debug_stage(a, a_bits: int, b, b_bits: int, stage: int, stream=None):
 
 def gf2x_release(device: int = 0):
     _check(load().gf2x_release(device))
+
+
+def profile_enable(on: bool = True):
+    _check(load().gf2x_profile_enable(1 if on else 0))
+
+
+def profile_report():
+    """Per-kernel device time (CUDA events) recorded since profile_enable(True)."""
+    import json
+    L = load()
+    need = L.gf2x_profile_report(None, 0)
+    buf = ctypes.create_string_buffer(need + 16)
+    L.gf2x_profile_report(buf, len(buf))
+    return json.loads(buf.value.decode())
 
 
 def version() -> str:

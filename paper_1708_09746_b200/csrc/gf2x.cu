@@ -494,6 +494,49 @@ __global__ void __launch_bounds__(256) k_ipsi_combine(const uint4* __restrict__ 
 // =============================================================================================
 static thread_local std::string g_last_error;
 
+// ------------------------------------------------------------------------------ profiling hook
+struct ProfRec {
+    std::string name;
+    cudaEvent_t beg, end;
+    double bytes;
+};
+static thread_local bool g_prof_on = false;
+static thread_local std::vector<ProfRec> g_prof;
+static thread_local std::vector<cudaEvent_t> g_event_pool;
+
+static cudaEvent_t prof_event() {
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+static void prof_clear() {
+    for (auto& r : g_prof) {
+        g_event_pool.push_back(r.beg);
+        g_event_pool.push_back(r.end);
+    }
+    g_prof.clear();
+}
+// RAII bracket around one kernel launch
+struct ProfScope {
+    int idx = -1;
+    cudaStream_t st;
+    ProfScope(const char* name, double bytes, cudaStream_t s) : st(s) {
+        if (!g_prof_on) return;
+        ProfRec r{name, prof_event(), prof_event(), bytes};
+        cudaEventRecord(r.beg, st);
+        g_prof.push_back(r);
+        idx = (int)g_prof.size() - 1;
+    }
+    ~ProfScope() {
+        if (idx >= 0) cudaEventRecord(g_prof[idx].end, st);
+    }
+};
+
 static gf2x_status fail(gf2x_status s, const std::string& msg) {
     g_last_error = msg;
     return s;
@@ -735,6 +778,7 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
             for (int sw = 0; sw < 2; sw++) {
                 const int phaseA = (sw == 0) ? first : 1 - first;
                 const uint64_t n = phaseA ? nA : nB;
+                ProfScope ps(sizeof(T) == 8 ? "k_cvt_stream<u64>" : "k_cvt_stream<u128>", 3.0 * n * sizeof(T), st);
                 k_cvt_stream<T><<<grid_for(n, 256, sm_count, 8), 256, 0, st>>>(data, per * batch, op.lg, op.K, phaseA);
             }
         } else {
@@ -748,6 +792,7 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
             for (int i = 0; i < prm.nops; i++) prm.ops[i] = inverse ? p.ops[prm.nops - 1 - i] : p.ops[i];
             const size_t sm = ((size_t)1 << (p.c + p.R)) * sizeof(T);
             const uint64_t ntiles = (per >> (p.c + p.R)) * batch;
+            ProfScope ps(sizeof(T) == 8 ? "k_cvt_tile<u64>" : "k_cvt_tile<u128>", 2.0 * per * batch * sizeof(T), st);
             k_cvt_tile<T><<<grid_for(ntiles, 1, sm_count, 3), 256, sm, st>>>(prm);
         }
         cudaError_t e = cudaGetLastError();
@@ -773,6 +818,8 @@ static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* 
     const size_t sm = fft_smem(f, psi);
     const int occ = sm > 110 * 1024 ? 1 : (sm > 70 * 1024 ? 2 : 3);
     const int grid = grid_for(ntiles, 1, ds->sm_count, occ);
+    const double bytes = (double)P.batch * (psi ? (double)src_per * 8 : (double)P.N * 16) + (double)P.batch * P.N * 16;
+    ProfScope ps(inv ? "k_fft<inv>" : (psi ? "k_fft<psi>" : "k_fft"), bytes, st);
     if (inv) k_fft<true, false><<<grid, FFT_THREADS, sm, st>>>(prm);
     else if (psi) k_fft<false, true><<<grid, FFT_THREADS, sm, st>>>(prm);
     else k_fft<false, false><<<grid, FFT_THREADS, sm, st>>>(prm);
@@ -792,8 +839,14 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
     const int smc = ds->sm_count;
     gf2x_status s;
     // Split
-    k_prep<<<grid_for((1ull << P.ma) * P.batch, 256, smc, 8), 256, 0, st>>>(a, P.na, a_bits, P.ma, P.batch, Sa);
-    k_prep<<<grid_for((1ull << P.mb) * P.batch, 256, smc, 8), 256, 0, st>>>(b, P.nb, b_bits, P.mb, P.batch, Sb);
+    {
+        ProfScope ps("k_prep", (double)P.batch * (P.na + (1ull << P.ma)) * 8, st);
+        k_prep<<<grid_for((1ull << P.ma) * P.batch, 256, smc, 8), 256, 0, st>>>(a, P.na, a_bits, P.ma, P.batch, Sa);
+    }
+    {
+        ProfScope ps("k_prep", (double)P.batch * (P.nb + (1ull << P.mb)) * 8, st);
+        k_prep<<<grid_for((1ull << P.mb) * P.batch, 256, smc, 8), 256, 0, st>>>(b, P.nb, b_bits, P.mb, P.batch, Sb);
+    }
     // BasisCvt on 64-bit blocks
     if ((s = run_cvt<uint64_t>(P.cvt_a, Sa, P.ma, P.batch, false, smc, st)) != GF2X_OK) return s;
     if ((s = run_cvt<uint64_t>(P.cvt_b, Sb, P.mb, P.batch, false, smc, st)) != GF2X_OK) return s;
@@ -812,6 +865,7 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         const uint64_t total = P.N * P.batch;
         const uint64_t ntiles = (total + PM_THREADS * 32 - 1) / (PM_THREADS * 32);
         const size_t sm = (size_t)(2 * PM_THREADS * PM_ROW + PM_THREADS * 128) * 4;
+        ProfScope ps("k_pointmul", 48.0 * total, st);
         k_pointmul<<<grid_for(ntiles, 1, smc, 2), PM_THREADS, sm, st>>>(Wa, Wb, total);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("pointmul launch: ") + cudaGetErrorString(e));
@@ -829,6 +883,7 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
     {
         const uint64_t n_out = P.na + P.nb;
         const uint64_t total = n_out * P.batch;
+        ProfScope ps("k_ipsi_combine", 16.0 * P.N * P.batch + 8.0 * total, st);
         k_ipsi_combine<<<grid_for(total, 256, smc, 2), 256, 16 * 256 * 16, st>>>(Wa, ds->tabs, P.N, n_out, P.batch, c);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("combine launch: ") + cudaGetErrorString(e));
@@ -929,6 +984,47 @@ gf2x_status gf2x_debug_stage(const uint64_t* a, uint64_t a_bits, const uint64_t*
                              uint64_t* out, void* stream) {
     if (stage < 1 || stage > 5 || !out || a_bits == 0 || b_bits == 0) return fail(GF2X_EINVAL, "bad debug stage request");
     return mul_common(a, a_bits, b, b_bits, nullptr, 1, nullptr, 0, stream, stage, out);
+}
+
+gf2x_status gf2x_profile_enable(int on) {
+    prof_clear();
+    g_prof_on = on != 0;
+    return GF2X_OK;
+}
+
+int gf2x_profile_report(char* buf, size_t cap) {
+    // aggregate by kernel name, in first-seen order
+    std::vector<std::string> order;
+    std::map<std::string, std::pair<int, std::pair<double, double>>> agg;
+    for (auto& r : g_prof) {
+        cudaEventSynchronize(r.end);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.beg, r.end);
+        auto it = agg.find(r.name);
+        if (it == agg.end()) {
+            order.push_back(r.name);
+            agg[r.name] = {0, {0.0, 0.0}};
+        }
+        auto& a = agg[r.name];
+        a.first += 1;
+        a.second.first += ms;
+        a.second.second += r.bytes;
+    }
+    std::string out = "[";
+    for (size_t i = 0; i < order.size(); i++) {
+        auto& a = agg[order[i]];
+        char tmp[256];
+        snprintf(tmp, sizeof(tmp), "%s{\"kernel\": \"%s\", \"launches\": %d, \"ms\": %.6f, \"bytes\": %.0f}",
+                 i ? ", " : "", order[i].c_str(), a.first, a.second.first, a.second.second);
+        out += tmp;
+    }
+    out += "]";
+    if (buf && cap) {
+        size_t n = std::min(cap - 1, out.size());
+        memcpy(buf, out.data(), n);
+        buf[n] = 0;
+    }
+    return (int)out.size() + 1;
 }
 
 const char* gf2x_status_string(gf2x_status s) {
