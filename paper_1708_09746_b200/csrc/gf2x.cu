@@ -35,13 +35,12 @@ struct DevTables {
     uint4 psi64[8 * 256];    // M4R-8 of changeRepr on a 64-bit polynomial-basis block -> tower
     uint4 ipsi[16 * 256];    // M4R-8 of changeRepr^-1: 128-bit tower element -> polynomial basis
     uint32_t wt[7 * 1024];   // M4R-8 of c -> c * v_(4t), t = 1..7 (table-build helper)
-    uint32_t cloc[62 * 128]; // M4R-4 tables of the in-warp multiplier parts s_k(phi(j 2^(k+1))), k < 5
+    uint32_t cloc[63 * 128]; // M4R-4 tables of the fixed low multiplier parts s_k(phi(j 2^(k+1))), k < 6
     uint32_t S[32 * 32];     // S[k][j] = s_k(v_j): images of the basis under s_k (§4.4)
 };
 
 __constant__ uint32_t c_S[32 * 32];
 
-static const int CLOC_OFF[5] = {0, 32, 48, 56, 60};
 
 // =============================================================================================
 // Multiplier of layer k for block base b (index within one product): s_k(phi_v(b)) is GF(2)-linear
@@ -176,132 +175,7 @@ __global__ void k_cvt_stream(T* __restrict__ data, uint64_t total_units, int lg,
     }
 }
 
-// =============================================================================================
-// FFT_LCH passes (Alg. 1, α = 0): layers k in [k_lo, k_hi) of every tile with bits
-// [0,c) U [k_lo,k_hi).  Forward: k = k_hi-1 .. k_lo, butterfly  x0 ^= c*x1; x1 ^= x0.
-// Inverse: k = k_lo .. k_hi-1,  x1 ^= x0; x0 ^= c*x1.   (s_k(v_k) = 1, Prop. 1)
-// When every lane of a warp shares the multiplier (c + (k - k_lo) >= 5) the warp builds one M4R-4
-// table for it.  Otherwise (contiguous tile, k < 5) the multiplier is C_w ^ c_loc: C_w for the
-// warp's 64-element block (warp table) and c_loc from the fixed in-warp tables; by linearity
-// c*x = C_w*x ^ c_loc*x.
-// With PSI the pass reads 64-bit novel-basis blocks and applies changeRepr on load (zero above
-// n_src words: the fan-out of the top layer, falls out of the zero upper half).
-// =============================================================================================
-struct FftParams {
-    const void* src;
-    uint4* dst;
-    const DevTables* tabs;
-    uint64_t N;         // points per product (2^m)
-    uint64_t src_per;   // PSI: u64 words per pair in src (2^ms); else N
-    uint64_t batch;
-    int m, c, k_lo, k_hi;
-};
-
-#define FFT_THREADS 256
-#define FFT_WARPS (FFT_THREADS / 32)
-
-template <bool INV, bool PSI>
-__global__ void __launch_bounds__(FFT_THREADS) k_fft(FftParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int R = p.k_hi - p.k_lo;
-    const uint64_t nslots = 1ull << (p.c + R);
-    uint4* tile = reinterpret_cast<uint4*>(smem_raw);
-    uint32_t* wtab = reinterpret_cast<uint32_t*>(tile + nslots);       // FFT_WARPS x 128
-    uint32_t* cloc = wtab + FFT_WARPS * 128;                             // 62 x 128 (if needed)
-    uint4* psit = reinterpret_cast<uint4*>(cloc + ((p.c == 0 && p.k_lo == 0) ? 62 * 128 : 0));  // 8 x 256 (PSI)
-    const bool need_cloc = (p.c == 0 && p.k_lo == 0 && R > 0);
-    if (need_cloc)
-        for (int i = threadIdx.x; i < 62 * 128; i += blockDim.x) cloc[i] = p.tabs->cloc[i];
-    if (PSI)
-        for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) psit[i] = p.tabs->psi64[i];
-    __syncthreads();
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t* mytab = wtab + warp * 128;
-    const uint64_t tiles_per_pair = p.N >> (p.c + R);
-    const uint64_t ntiles = tiles_per_pair * p.batch;
-    const uint64_t nbfly = nslots >> 1;
-    const uint32_t* wt = p.tabs->wt;
-
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const uint64_t pair = t / tiles_per_pair, tt = t - pair * tiles_per_pair;
-        const uint64_t base = tile_base(tt, p.c, p.k_lo, R);
-        // ---- load
-        if (PSI) {
-            const uint64_t* src = reinterpret_cast<const uint64_t*>(p.src) + pair * p.src_per;
-            for (uint64_t s = threadIdx.x; s < nslots; s += blockDim.x) {
-                const uint64_t g = tile_index(base, s, p.c, p.k_lo);
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (g < p.src_per) {
-                    const uint64_t w = src[g];
-#pragma unroll
-                    for (int ch = 0; ch < 8; ch++) v = xor4(v, psit[ch * 256 + ((w >> (8 * ch)) & 255)]);
-                }
-                tile[s] = v;
-            }
-        } else {
-            const uint4* src = reinterpret_cast<const uint4*>(p.src) + pair * p.N;
-            for (uint64_t s = threadIdx.x; s < nslots; s += blockDim.x) tile[s] = src[tile_index(base, s, p.c, p.k_lo)];
-        }
-        __syncthreads();
-        // ---- layers
-        for (int li = 0; li < R; li++) {
-            const int k = INV ? (p.k_lo + li) : (p.k_hi - 1 - li);
-            const int kk = k - p.k_lo;
-            const bool uniform = (p.c + kk) >= 5;
-            uint32_t cached = 0xFFFFFFFFu;  // no valid table yet (multipliers are < 2^31 here)
-            const uint64_t nsets = (nbfly + 31) >> 5;
-            for (uint64_t set = warp; set < nsets; set += FFT_WARPS) {
-                const uint64_t beta = (set << 5) + lane;
-                const bool active = beta < nbfly;
-                const uint64_t col = beta & ((1ull << p.c) - 1);
-                const uint64_t rest = beta >> p.c;
-                const uint64_t row0 = (rest & ((1ull << kk) - 1)) | ((rest >> kk) << (kk + 1));
-                const uint64_t s0 = (row0 << p.c) | col, s1 = s0 | (1ull << (p.c + kk));
-                const uint64_t g0 = tile_index(base, s0, p.c, p.k_lo);  // index within the pair
-                uint32_t cst;
-                const uint32_t* tabB = nullptr;
-                if (uniform) {
-                    // all lanes share the bits > k (they differ only in col / row bits below kk)
-                    cst = layer_const(k, (uint32_t)(g0 & ~((2ull << k) - 1)));
-                } else {
-                    // k < 5 in a contiguous tile: C_w from the warp's 64-element block, c_loc fixed
-                    cst = layer_const(k, (uint32_t)(g0 & ~63ull));
-                    tabB = cloc + ((64 - (64 >> k)) + ((g0 & 63) >> (k + 1))) * 128;  // table offset 64 - 2^(6-k)
-                }
-                cst = __shfl_sync(0xFFFFFFFFu, cst, 0);   // lane 0 is always active
-                const uint32_t* tabA = mytab;
-                if (cst != cached && cst > 1) {
-                    __syncwarp();
-                    build_tab(mytab, cst, wt);
-                    __syncwarp();
-                }
-                cached = cst;
-                if (active) {
-                    uint4 x0 = tile[s0], x1 = tile[s1];
-                    if (!INV) {
-                        uint4 prod = (cst == 0) ? make_uint4(0, 0, 0, 0) : (cst == 1 ? x1 : m4r4_mul(tabA, x1));
-                        if (tabB) prod = xor4(prod, m4r4_mul(tabB, x1));
-                        x0 = xor4(x0, prod);
-                        x1 = xor4(x1, x0);
-                    } else {
-                        x1 = xor4(x1, x0);
-                        uint4 prod = (cst == 0) ? make_uint4(0, 0, 0, 0) : (cst == 1 ? x1 : m4r4_mul(tabA, x1));
-                        if (tabB) prod = xor4(prod, m4r4_mul(tabB, x1));
-                        x0 = xor4(x0, prod);
-                    }
-                    tile[s0] = x0;
-                    tile[s1] = x1;
-                }
-            }
-            __syncthreads();
-        }
-        // ---- store
-        uint4* dst = p.dst + pair * p.N;
-        for (uint64_t s = threadIdx.x; s < nslots; s += blockDim.x) dst[tile_index(base, s, p.c, p.k_lo)] = tile[s];
-        __syncthreads();
-    }
-}
+#include "fft.cuh"
 
 // =============================================================================================
 // pointmul: P[i] = A[i] (x) B[i] in TGF(2^128).  32 consecutive elements per thread are
@@ -589,13 +463,14 @@ static void host_build_tables(DevTables* T) {
             v = s1(v);
         }
     }
-    // cloc: k < 5, local block j < 2^(5-k): constant s_k(phi(j 2^(k+1))), M4R-4 table
-    for (int k = 0; k < 5; k++)
-        for (int j = 0; j < (1 << (5 - k)); j++) {
+    // cloc: fixed low parts for the bottom FFT pass: table id 2^(BOT_B-1-k) - 1 + j holds the
+    // constant s_k(phi(j 2^(k+1))) (local index bits (k, BOT_B)), k < BOT_B
+    for (int k = 0; k < BOT_B; k++)
+        for (int j = 0; j < (1 << (BOT_B - 1 - k)); j++) {
             uint32_t bb = (uint32_t)j << (k + 1), e = 0;
-            for (int i = k + 1; i < 6; i++)
+            for (int i = k + 1; i < BOT_B; i++)
                 if ((bb >> i) & 1) e ^= T->S[k * 32 + i];
-            uint32_t* tab = T->cloc + (CLOC_OFF[k] + j) * 128;
+            uint32_t* tab = T->cloc + (((1 << (BOT_B - 1 - k)) - 1) + j) * 128;
             for (int t = 0; t < 8; t++)
                 for (int x = 0; x < 16; x++) tab[16 * t + x] = (uint32_t)tower_mul((u128)e, ((u128)x) << (4 * t));
         }
@@ -618,9 +493,12 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
         if (e != cudaSuccess) { cudaFree(d); return fail(GF2X_ECUDA, cudaGetErrorString(e)); }
         CUDA_TRY(cudaDeviceGetAttribute(&st.sm_count, cudaDevAttrMultiProcessorCount, dev));
         // opt-in shared memory sizes
-        CUDA_TRY(cudaFuncSetAttribute(k_fft<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_fft<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_fft<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_fft2<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_fft2<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_fft2<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_fft2<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_fft2<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_fft2<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_tile<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_tile<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_pointmul, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -688,22 +566,26 @@ static std::vector<CvtPass> plan_cvt(int m, int unit_bytes) {
 }
 
 struct FftPass {
-    int c, k_lo, k_hi;
+    int c, k_lo, k_hi;  // direct: tile bits [0,c) U [k_lo,k_hi); bottom: c = k_lo = 0, k_hi = Rt
+    bool bottom;
+    int layers;         // bottom: layers [0, layers)
 };
-// forward order (top-down); the first pass also applies changeRepr
+// forward order (top-down); the first pass also applies changeRepr.  High layers [BOT_B, m) are
+// split evenly into direct passes of <= 6 layers; layers [0, min(m, BOT_B)) form the bottom pass.
 static std::vector<FftPass> plan_fft(int m) {
     std::vector<FftPass> v;
-    const int T_LO = 11;   // contiguous low tile: 2^11 elements (32 KB)
-    const int R_HI = 6;    // high passes: 32 contiguous x 2^6 rows (32 KB)
-    const int C_HI = 5;
+    const int H = m > BOT_B ? m - BOT_B : 0;
+    const int np = (H + 5) / 6;
     int top = m;
-    while (top > T_LO) {
-        int lo = std::max(T_LO, top - R_HI);
-        if (lo < C_HI) lo = C_HI;
-        v.push_back({C_HI, lo, top});
+    for (int i = 0; i < np; i++) {
+        const int rem = top - BOT_B;
+        const int r = (rem + (np - i) - 1) / (np - i);  // remaining layers / remaining passes
+        const int lo = top - r;
+        v.push_back({i == 0 ? 5 : 6, lo, top, false, 0});
         top = lo;
     }
-    v.push_back({0, 0, top});
+    const int rt = m < BOT_RT ? m : BOT_RT;
+    v.push_back({0, 0, rt, true, m < BOT_B ? m : BOT_B});
     return v;
 }
 
@@ -801,28 +683,29 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
     return GF2X_OK;
 }
 
-static size_t fft_smem(const FftPass& f, bool psi) {
-    size_t s = ((size_t)1 << (f.c + f.k_hi - f.k_lo)) * 16 + FFT_WARPS * 128 * 4;
-    if (f.c == 0 && f.k_lo == 0) s += 62 * 128 * 4;
-    if (psi) s += 8 * 256 * 16;
-    return s;
-}
-
 static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* src, uint64_t src_per, uint4* dst,
                               const Plan& P, DeviceState* ds, cudaStream_t st) {
     FftParams prm;
     prm.src = src; prm.dst = dst; prm.tabs = ds->tabs;
-    prm.N = P.N; prm.src_per = src_per; prm.batch = P.batch;
-    prm.m = P.m; prm.c = f.c; prm.k_lo = f.k_lo; prm.k_hi = f.k_hi;
-    const uint64_t ntiles = (P.N >> (f.c + f.k_hi - f.k_lo)) * P.batch;
-    const size_t sm = fft_smem(f, psi);
-    const int occ = sm > 110 * 1024 ? 1 : (sm > 70 * 1024 ? 2 : 3);
+    prm.src_per = src_per; prm.batch = P.batch;
+    prm.m = P.m; prm.c = f.c; prm.k_lo = f.k_lo; prm.k_hi = f.k_hi; prm.layers = f.layers;
+    const int R = f.k_hi - f.k_lo;
+    const uint64_t ntiles = (P.N >> (f.c + R)) * P.batch;
+    const size_t sm = fft2_smem(f.c, R, f.layers, psi, f.bottom);
+    const int occ = sm > 113 * 1024 ? 1 : (sm > 75 * 1024 ? 2 : 3);
     const int grid = grid_for(ntiles, 1, ds->sm_count, occ);
     const double bytes = (double)P.batch * (psi ? (double)src_per * 8 : (double)P.N * 16) + (double)P.batch * P.N * 16;
-    ProfScope ps(inv ? "k_fft<inv>" : (psi ? "k_fft<psi>" : "k_fft"), bytes, st);
-    if (inv) k_fft<true, false><<<grid, FFT_THREADS, sm, st>>>(prm);
-    else if (psi) k_fft<false, true><<<grid, FFT_THREADS, sm, st>>>(prm);
-    else k_fft<false, false><<<grid, FFT_THREADS, sm, st>>>(prm);
+    ProfScope ps(f.bottom ? (inv ? "k_fft_bottom<inv>" : (psi ? "k_fft_bottom<psi>" : "k_fft_bottom"))
+                          : (inv ? "k_fft<inv>" : (psi ? "k_fft<psi>" : "k_fft")), bytes, st);
+    if (f.bottom) {
+        if (inv) k_fft2<true, false, true><<<grid, FFT_THREADS, sm, st>>>(prm);
+        else if (psi) k_fft2<false, true, true><<<grid, FFT_THREADS, sm, st>>>(prm);
+        else k_fft2<false, false, true><<<grid, FFT_THREADS, sm, st>>>(prm);
+    } else {
+        if (inv) k_fft2<true, false, false><<<grid, FFT_THREADS, sm, st>>>(prm);
+        else if (psi) k_fft2<false, true, false><<<grid, FFT_THREADS, sm, st>>>(prm);
+        else k_fft2<false, false, false><<<grid, FFT_THREADS, sm, st>>>(prm);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("fft launch: ") + cudaGetErrorString(e));
     return GF2X_OK;
@@ -855,7 +738,10 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         const bool first = (i == 0);
         const bool only_psi = (stop_stage == 1);
         FftPass f = P.fft[i];
-        if (only_psi) { if (!first) break; f.k_lo = f.k_hi; }  // changeRepr only
+        if (only_psi) {  // changeRepr only
+            if (!first) break;
+            if (f.bottom) f.layers = 0; else f.k_lo = f.k_hi;
+        }
         if ((s = launch_fft(f, false, first, first ? (const void*)Sa : Wa, first ? (1ull << P.ma) : P.N, Wa, P, ds, st)) != GF2X_OK) return s;
         if ((s = launch_fft(f, false, first, first ? (const void*)Sb : Wb, first ? (1ull << P.mb) : P.N, Wb, P, ds, st)) != GF2X_OK) return s;
     }
