@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft2(FftParams p) {
     uint4* tile = psit + (PSI ? 8 * 256 : 0);
     const uint32_t tabs_sa = (uint32_t)__cvta_generic_to_shared(tabs);
     const uint32_t fixed_sa = (uint32_t)__cvta_generic_to_shared(fixed);
+    if (tabs_sa & 255) __trap();  // the PRMT address fusion needs 256-byte aligned tables
     if (BOTTOM)
         for (uint32_t i = threadIdx.x; i < ((1u << BOT_B) - 1) * 128; i += blockDim.x) fixed[i] = p.tabs->cloc[i];
     if (PSI)

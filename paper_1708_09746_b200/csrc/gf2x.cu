@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -77,243 +78,113 @@ __global__ void k_prep(const uint64_t* __restrict__ in, uint64_t n, uint64_t bit
     }
 }
 
-// =============================================================================================
-// Basis conversion.  One Taylor step ("op") of Alg. 2 on segments of 2^lg units, h = 2^(lg-1),
-// u = h >> K, d = h - u, is the sequential loop  for i = 2h-1 .. h: f[i-d] ^= f[i]  (R4).
-// It splits into two dependency-free sweeps ("phase A": targets [h, h+u), "phase B": targets
-// [u, h)), both f[t] ^= f[t+d]; forward runs A then B, the inverse (ascending loop) B then A.
-// =============================================================================================
-struct CvtOp {
-    int lg, K;
-};
-#define MAX_TILE_OPS 48
-struct CvtTileParams {
-    void* data;
-    uint64_t units_per_pair;  // 2^m
-    uint64_t batch;
-    int m, c, r_lo, R;        // tile bits [0,c) U [r_lo, r_lo+R)  (contiguous: c = 0, r_lo = 0)
-    int nops, inverse;
-    CvtOp ops[MAX_TILE_OPS];
-};
-
-template <typename T>
-__device__ __forceinline__ T xor_t(T a, T b);
-template <>
-__device__ __forceinline__ uint64_t xor_t<uint64_t>(uint64_t a, uint64_t b) { return a ^ b; }
-template <>
-__device__ __forceinline__ uint4 xor_t<uint4>(uint4 a, uint4 b) { return xor4(a, b); }
-
-// global index (within the pair) of tile slot s
-__device__ __forceinline__ uint64_t tile_index(uint64_t base, uint64_t s, int c, int r_lo) {
-    const uint64_t col = s & ((1ull << c) - 1), row = s >> c;
-    return base | col | (row << r_lo);
-}
-__device__ __forceinline__ uint64_t tile_slot(uint64_t g, int c, int r_lo, int R) {
-    return (g & ((1ull << c) - 1)) | (((g >> r_lo) & ((1ull << R) - 1)) << c);
-}
-// base index (within the pair) of tile t of a pair, tile bits [0,c) U [r_lo, r_lo+R)
-__device__ __forceinline__ uint64_t tile_base(uint64_t t, int c, int r_lo, int R) {
-    const int midbits = r_lo - c;
-    const uint64_t mid = t & ((1ull << midbits) - 1), hi = t >> midbits;
-    return (mid << c) | (hi << (r_lo + R));
-}
-
-template <typename T>
-__device__ void cvt_sweep(T* tile, uint64_t base, int c, int r_lo, int R, int lg, int K, int phaseA) {
-    const uint64_t h = 1ull << (lg - 1), u = h >> K, d = h - u;
-    const uint64_t nslots = 1ull << (c + R);
-    for (uint64_t s = threadIdx.x; s < nslots; s += blockDim.x) {
-        const uint64_t g = tile_index(base, s, c, r_lo);
-        const uint64_t pos = g & ((h << 1) - 1);
-        const bool tgt = phaseA ? (pos >= h && pos < h + u) : (pos >= u && pos < h);
-        if (tgt) {
-            const uint64_t src = tile_slot(g + d, c, r_lo, R);
-            tile[s] = xor_t<T>(tile[s], tile[src]);
-        }
-    }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256) k_cvt_tile(CvtTileParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* tile = reinterpret_cast<T*>(smem_raw);
-    T* data = reinterpret_cast<T*>(p.data);
-    const uint64_t nslots = 1ull << (p.c + p.R);
-    const uint64_t tiles_per_pair = p.units_per_pair >> (p.c + p.R);
-    const uint64_t ntiles = tiles_per_pair * p.batch;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const uint64_t pair = t / tiles_per_pair, tt = t - pair * tiles_per_pair;
-        const uint64_t base = tile_base(tt, p.c, p.r_lo, p.R);
-        T* dp = data + pair * p.units_per_pair;
-        for (uint64_t s = threadIdx.x; s < nslots; s += blockDim.x) tile[s] = dp[tile_index(base, s, p.c, p.r_lo)];
-        __syncthreads();
-        for (int o = 0; o < p.nops; o++) {
-            const CvtOp op = p.ops[o];
-            cvt_sweep<T>(tile, base, p.c, p.r_lo, p.R, op.lg, op.K, p.inverse ? 0 : 1);
-            __syncthreads();
-            cvt_sweep<T>(tile, base, p.c, p.r_lo, p.R, op.lg, op.K, p.inverse ? 1 : 0);
-            __syncthreads();
-        }
-        for (uint64_t s = threadIdx.x; s < nslots; s += blockDim.x) dp[tile_index(base, s, p.c, p.r_lo)] = tile[s];
-        __syncthreads();
-    }
-}
-
-// One sweep of one op over the whole array (used when the op's window does not fit a tile).
-template <typename T>
-__global__ void k_cvt_stream(T* __restrict__ data, uint64_t total_units, int lg, int K, int phaseA) {
-    const uint64_t h = 1ull << (lg - 1), u = h >> K, d = h - u;
-    const uint64_t len = h << 1;
-    // targets per segment: phase A -> u of them starting at h; phase B -> h-u starting at u
-    const uint64_t per = phaseA ? u : (h - u);
-    const uint64_t first = phaseA ? h : u;
-    const uint64_t ntgt = (total_units / len) * per;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ntgt; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t seg = i / per, j = i - seg * per;
-        const uint64_t t = seg * len + first + j;
-        data[t] = xor_t<T>(data[t], data[t + d]);
-    }
-}
-
+#include "cvt.cuh"
 #include "fft.cuh"
 
 // =============================================================================================
-// pointmul: P[i] = A[i] (x) B[i] in TGF(2^128).  32 consecutive elements per thread are
-// bit-sliced (transpose32), multiplied with the generated straight-line Karatsuba (bs_mul32 for the
-// TGF(2^32) limb products, XOR networks for the fixed constants v31, v31^2), and transposed back.
-//   a = alpha0 + alpha1 x7, alpha_i = A_2i + A_2i+1 x6 (limbs), x6^2 = x6 + v31, x7^2 = x7 + v63,
-//   v63 = v31 x6  =>  v63 (e0 + e1 x6) = v31^2 e1 + v31 (e0 + e1) x6.
+// pointmul: P[i] = A[i] (x) B[i] in TGF(2^128).  Each thread owns 32 consecutive
+// elements, bit-sliced in place in shared memory (transpose32 per limb: plane j of limb L = bit j of
+// the 32 limbs L).  With a = alpha0 + alpha1 x7, alpha_i = A_2i + A_2i+1 x6 (x6^2 = x6 + v31,
+// x7^2 = x7 + v63, v63 = v31 x6), two Karatsuba levels give nine TGF(2^32) products
+//   P0=A0B0 P1=A1B1 P01=(A0+A1)(B0+B1) P2=A2B2 P3=A3B3 P23=(A2+A3)(B2+B3)
+//   Q0=(A0+A2)(B0+B2) Q1=(A1+A3)(B1+B3) Q01=(A0+A1+A2+A3)(B0+B1+B2+B3)
+// and the result limbs
+//   R0 = P0 + v31 P1 + v31^2 (P2 + P23)        R1 = P0 + P01 + v31 P23 + v31^2 P3
+//   R2 = P0 + Q0 + v31 (P1 + Q1)               R3 = P0 + P01 + Q0 + Q01
+// Each product is one generated straight-line bit-sliced Karatsuba (bs_mul32); only one is live
+// in registers at a time.
 // =============================================================================================
-#define PM_THREADS 64
-#define PM_ROW 129   // 32 elements x 4 words + 1 pad word (conflict-free strided access)
+#define PM_THREADS 128
+#define PM_WORDS 384   // per thread: A planes 128, B planes 128, R accumulators 128
 
-__device__ __forceinline__ void load_planes(const uint32_t* rowA, int limb, uint32_t* x) {
+// in-place bit-slicing of the thread's 32 elements (limb L of element e at row[4e + L])
+__device__ __forceinline__ void slice_limb(uint32_t* row, int L) {
+    uint32_t x[32];
 #pragma unroll
-    for (int e = 0; e < 32; e++) x[e] = rowA[e * 4 + limb];
+    for (int e = 0; e < 32; e++) x[e] = row[4 * e + L];
     transpose32(x);
-}
-__device__ __forceinline__ void load_planes_sum(const uint32_t* row, int l0, int l1, uint32_t* x) {
 #pragma unroll
-    for (int e = 0; e < 32; e++) x[e] = row[e * 4 + l0] ^ row[e * 4 + l1];
-    transpose32(x);
+    for (int j = 0; j < 32; j++) row[4 * j + L] = x[j];
 }
 
-// TGF(2^64) product of bit-sliced (g0 + g1 x6)(d0 + d1 x6); operands given by loader lambdas
-template <typename LA, typename LB>
-__device__ __forceinline__ void bs_mul64(LA la, LB lb, uint32_t* r0, uint32_t* r1) {
-    uint32_t x[32], y[32], p0[32], p2[32], t[32];
-    la(0, x); lb(0, y);
-    bs_mul32(x, y, p0);
-    la(1, x); lb(1, y);
-    bs_mul32(x, y, p2);
-    la(2, x); lb(2, y);          // g0 + g1, d0 + d1
-    bs_mul32(x, y, t);           // p1
+// planes of (sum of the limbs in mask) of operand row: plane j of limb L is row[4j + L]
+__device__ __forceinline__ void load_sum(const uint32_t* row, int mask, uint32_t* x) {
 #pragma unroll
-    for (int i = 0; i < 32; i++) r1[i] = t[i] ^ p0[i];
-    bs_mul_v31(p2, t);
+    for (int j = 0; j < 32; j++) x[j] = 0;
 #pragma unroll
-    for (int i = 0; i < 32; i++) r0[i] = p0[i] ^ t[i];
+    for (int L = 0; L < 4; L++)
+        if (mask & (1 << L)) {
+#pragma unroll
+            for (int j = 0; j < 32; j++) x[j] ^= row[4 * j + L];
+        }
 }
+
+// acc limbs (mask) ^= v
+__device__ __forceinline__ void acc_add(uint32_t* acc, int mask, const uint32_t* v) {
+#pragma unroll
+    for (int L = 0; L < 4; L++)
+        if (mask & (1 << L)) {
+#pragma unroll
+            for (int j = 0; j < 32; j++) acc[4 * j + L] ^= v[j];
+        }
+}
+
+// (limb mask of the factors, limbs receiving r, limbs receiving v31 r, limbs receiving v31^2 r)
+__constant__ int c_pm_terms[9][4] = {
+    {0x1, 0xF, 0x0, 0x0},   // P0  -> R0 R1 R2 R3
+    {0x2, 0x0, 0x5, 0x0},   // P1  -> v31: R0 R2
+    {0x3, 0xA, 0x0, 0x0},   // P01 -> R1 R3
+    {0x4, 0x0, 0x0, 0x1},   // P2  -> v31^2: R0
+    {0x8, 0x0, 0x0, 0x2},   // P3  -> v31^2: R1
+    {0xC, 0x0, 0x2, 0x1},   // P23 -> v31: R1, v31^2: R0
+    {0x5, 0xC, 0x0, 0x0},   // Q0  -> R2 R3
+    {0xA, 0x0, 0x4, 0x0},   // Q1  -> v31: R2
+    {0xF, 0x8, 0x0, 0x0},   // Q01 -> R3
+};
 
 __global__ void __launch_bounds__(PM_THREADS) k_pointmul(uint4* __restrict__ A, const uint4* __restrict__ B, uint64_t total) {
-    extern __shared__ __align__(16) uint32_t pm_smem[];
-    uint32_t* sa = pm_smem;                          // PM_THREADS rows of PM_ROW
-    uint32_t* sb = sa + PM_THREADS * PM_ROW;
-    uint32_t* scr = sb + PM_THREADS * PM_ROW;        // per thread 128 words
+    extern __shared__ __align__(1024) uint32_t pm_smem[];
+    // thread t: ra = A elements (32 x 4 words), rb = B elements, acc = result; rows padded by one
+    // word per thread block of 32 elements so that the per-thread strided accesses hit distinct banks
+    uint32_t* ra = pm_smem + threadIdx.x * (PM_WORDS + 1);
+    uint32_t* rb = ra + 128;
+    uint32_t* acc = rb + 128;
     const uint64_t per_cta = PM_THREADS * 32ull;
     const uint64_t ntiles = (total + per_cta - 1) / per_cta;
-    uint32_t* rowA = sa + threadIdx.x * PM_ROW;
-    uint32_t* rowB = sb + threadIdx.x * PM_ROW;
-    uint32_t* my = scr + threadIdx.x * 128;
     for (uint64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
         const uint64_t e0 = tl * per_cta;
-        for (uint64_t i = threadIdx.x; i < per_cta; i += PM_THREADS) {
+        // coalesced load: element i of the CTA tile -> thread i/32, slot i%32
+        for (uint32_t i = threadIdx.x; i < per_cta; i += PM_THREADS) {
             const uint64_t e = e0 + i;
             uint4 va = make_uint4(0, 0, 0, 0), vb = make_uint4(0, 0, 0, 0);
             if (e < total) { va = A[e]; vb = B[e]; }
-            uint32_t* ra = sa + (i >> 5) * PM_ROW + (i & 31) * 4;
-            uint32_t* rb = sb + (i >> 5) * PM_ROW + (i & 31) * 4;
-            ra[0] = va.x; ra[1] = va.y; ra[2] = va.z; ra[3] = va.w;
-            rb[0] = vb.x; rb[1] = vb.y; rb[2] = vb.z; rb[3] = vb.w;
+            uint32_t* da = pm_smem + (i >> 5) * (PM_WORDS + 1) + (i & 31) * 4;
+            da[0] = va.x; da[1] = va.y; da[2] = va.z; da[3] = va.w;
+            da[128] = vb.x; da[129] = vb.y; da[130] = vb.z; da[131] = vb.w;
         }
         __syncthreads();
-        uint32_t h0[32], h1[32];
-        // q1 = (alpha0 + alpha1)(beta0 + beta1); limbs of alpha0+alpha1: (A0^A2, A1^A3), sum (A0^A1^A2^A3)
-        {
-            auto la = [&](int w, uint32_t* x) {
-                if (w == 0) load_planes_sum(rowA, 0, 2, x);
-                else if (w == 1) load_planes_sum(rowA, 1, 3, x);
-                else {
-#pragma unroll
-                    for (int e = 0; e < 32; e++) x[e] = rowA[e * 4] ^ rowA[e * 4 + 1] ^ rowA[e * 4 + 2] ^ rowA[e * 4 + 3];
-                    transpose32(x);
-                }
-            };
-            auto lb = [&](int w, uint32_t* x) {
-                if (w == 0) load_planes_sum(rowB, 0, 2, x);
-                else if (w == 1) load_planes_sum(rowB, 1, 3, x);
-                else {
-#pragma unroll
-                    for (int e = 0; e < 32; e++) x[e] = rowB[e * 4] ^ rowB[e * 4 + 1] ^ rowB[e * 4 + 2] ^ rowB[e * 4 + 3];
-                    transpose32(x);
-                }
-            };
-            bs_mul64(la, lb, h0, h1);
-#pragma unroll
-            for (int i = 0; i < 32; i++) { my[i] = h0[i]; my[32 + i] = h1[i]; }
+#pragma unroll 1
+        for (int L = 0; L < 4; L++) { slice_limb(ra, L); slice_limb(rb, L); }
+#pragma unroll 1
+        for (int i = 0; i < 128; i++) acc[i] = 0;
+#pragma unroll 1
+        for (int q = 0; q < 9; q++) {
+            uint32_t x[32], y[32], r[32];
+            load_sum(ra, c_pm_terms[q][0], x);
+            load_sum(rb, c_pm_terms[q][0], y);
+            bs_mul32(x, y, r);
+            acc_add(acc, c_pm_terms[q][1], r);
+            if (c_pm_terms[q][2]) { bs_mul_v31(r, x); acc_add(acc, c_pm_terms[q][2], x); }
+            if (c_pm_terms[q][3]) { bs_mul_v31sq(r, y); acc_add(acc, c_pm_terms[q][3], y); }
         }
-        // q0 = alpha0 beta0 ; hi = q1 + q0
-        {
-            auto la = [&](int w, uint32_t* x) { if (w < 2) load_planes(rowA, w, x); else load_planes_sum(rowA, 0, 1, x); };
-            auto lb = [&](int w, uint32_t* x) { if (w < 2) load_planes(rowB, w, x); else load_planes_sum(rowB, 0, 1, x); };
-            bs_mul64(la, lb, h0, h1);
-#pragma unroll
-            for (int i = 0; i < 32; i++) {
-                my[i] ^= h0[i]; my[32 + i] ^= h1[i];      // hi
-                my[64 + i] = h0[i]; my[96 + i] = h1[i];  // q0
-            }
-        }
-        // q2 = alpha1 beta1 ; lo = q0 + v63 q2
-        {
-            auto la = [&](int w, uint32_t* x) { if (w < 2) load_planes(rowA, 2 + w, x); else load_planes_sum(rowA, 2, 3, x); };
-            auto lb = [&](int w, uint32_t* x) { if (w < 2) load_planes(rowB, 2 + w, x); else load_planes_sum(rowB, 2, 3, x); };
-            bs_mul64(la, lb, h0, h1);   // q2 = (e0, e1)
-            uint32_t t[32], u[32];
-            // v63 (e0 + e1 x6) = v31^2 e1 + v31 (e0 + e1) x6
-            bs_mul_v31sq(h1, t);
-#pragma unroll
-            for (int i = 0; i < 32; i++) u[i] = h0[i] ^ h1[i];
-            bs_mul_v31(u, h1);
-#pragma unroll
-            for (int i = 0; i < 32; i++) {
-                h0[i] = my[64 + i] ^ t[i];   // lo limb 0
-                h1[i] ^= my[96 + i];         // lo limb 1
-            }
-        }
-        // write back: result limbs (lo0, lo1, hi0, hi1) -> transpose -> rowA
-        __syncwarp();
-        transpose32(h0);
-#pragma unroll
-        for (int e = 0; e < 32; e++) rowA[e * 4 + 0] = h0[e];
-        transpose32(h1);
-#pragma unroll
-        for (int e = 0; e < 32; e++) rowA[e * 4 + 1] = h1[e];
-#pragma unroll
-        for (int i = 0; i < 32; i++) h0[i] = my[i];
-        transpose32(h0);
-#pragma unroll
-        for (int e = 0; e < 32; e++) rowA[e * 4 + 2] = h0[e];
-#pragma unroll
-        for (int i = 0; i < 32; i++) h1[i] = my[32 + i];
-        transpose32(h1);
-#pragma unroll
-        for (int e = 0; e < 32; e++) rowA[e * 4 + 3] = h1[e];
+#pragma unroll 1
+        for (int L = 0; L < 4; L++) slice_limb(acc, L);   // transpose32 is an involution
         __syncthreads();
-        for (uint64_t i = threadIdx.x; i < per_cta; i += PM_THREADS) {
+        for (uint32_t i = threadIdx.x; i < per_cta; i += PM_THREADS) {
             const uint64_t e = e0 + i;
             if (e < total) {
-                const uint32_t* ra = sa + (i >> 5) * PM_ROW + (i & 31) * 4;
-                A[e] = make_uint4(ra[0], ra[1], ra[2], ra[3]);
+                const uint32_t* r = pm_smem + (i >> 5) * (PM_WORDS + 1) + 256 + (i & 31) * 4;
+                A[e] = make_uint4(r[0], r[1], r[2], r[3]);
             }
         }
         __syncthreads();
@@ -517,51 +388,61 @@ static int ceil_log2_u64(uint64_t x) {
     return r;
 }
 
-// BasisCvt schedule (Alg. 3 with the paper's largest-K split, R4-R6) as global ops
+// BasisCvt schedule (Alg. 3 with the paper's largest-K split, R4-R6) as global ops.
+// The inner conversions (windows inside [sigma, sigma+K)) and the outer one (windows inside
+// [sigma+K, sigma+m)) act on disjoint index bits, so they commute (R14); the inner ones
+// are emitted first because their windows continue where the Taylor steps end.
 static void cvt_ops(int m, int sigma, std::vector<CvtOp>& out) {
     if (m <= 1) return;
     int K = 1;
     while (2 * K <= m - 1) K *= 2;
     for (int l = m; l >= K + 1; --l) out.push_back({l + sigma, K});
-    cvt_ops(m - K, sigma + K, out);
     cvt_ops(K, sigma, out);
+    cvt_ops(m - K, sigma + K, out);
 }
 
 struct CvtPass {
     bool stream;
     int c, r_lo, R;          // tile passes
-    std::vector<CvtOp> ops;  // tile: ops in execution order; stream: 1 op
+    std::vector<CvtOp> ops;  // tile: ops in forward execution order; stream: 1 op
 };
 
-// group ops into tile passes (windows [lg-1-K, lg) inside the tile bits) or streaming ops
+// Greedy grouping of consecutive ops into tile passes: a pass holds tile bits [0,T) (contiguous)
+// or [0,cmin) U [r_lo, r_lo + T - cmin) (rows of 2^cmin contiguous units = one 32-byte sector);
+// an op whose window is wider than a tile streams through HBM.
 static std::vector<CvtPass> plan_cvt(int m, int unit_bytes) {
     std::vector<CvtOp> ops;
     cvt_ops(m, 0, ops);
-    const int T = (unit_bytes == 8) ? 13 : 12;     // 64 KB tiles
-    const int cc = (unit_bytes == 8) ? 4 : 3;      // 128 B contiguous per row
-    const int R = T - cc;
+    const int T = std::min(m, unit_bytes == 8 ? 14 : 13);  // 128 KB tiles
+    const int cmin = unit_bytes == 8 ? 2 : 1;
+    const int Rrow = T - cmin;
     std::vector<CvtPass> passes;
+    int span_lo = 0, span_hi = 0;
+    auto close = [&](CvtPass& P) {
+        if (P.stream) return;
+        if (span_hi <= T) { P.c = 0; P.r_lo = 0; P.R = T; }
+        else { P.c = cmin; P.R = Rrow; P.r_lo = std::max(cmin, std::min(span_lo, m - Rrow)); }
+    };
+    auto fits = [&](int lo, int hi) { return hi <= T || (lo >= cmin && hi - lo <= Rrow); };
     for (const CvtOp& op : ops) {
         const int wlo = op.lg - 1 - op.K, whi = op.lg;
         if (!passes.empty() && !passes.back().stream && (int)passes.back().ops.size() < MAX_TILE_OPS) {
-            CvtPass& P = passes.back();
-            bool fits = (P.c == 0) ? (whi <= P.R) : (wlo >= P.r_lo && whi <= P.r_lo + P.R);
-            if (fits) { P.ops.push_back(op); continue; }
+            const int nlo = std::min(span_lo, wlo), nhi = std::max(span_hi, whi);
+            if (fits(nlo, nhi)) {
+                passes.back().ops.push_back(op);
+                span_lo = nlo; span_hi = nhi;
+                continue;
+            }
         }
+        if (!passes.empty()) close(passes.back());
         CvtPass P;
-        if (whi <= std::min(T, m)) {
-            P.stream = false; P.c = 0; P.r_lo = 0; P.R = std::min(T, m);
-        } else if (whi - wlo <= R && wlo >= cc) {
-            P.stream = false; P.c = cc; P.R = R; P.r_lo = std::max(cc, whi - R);
-            if (P.r_lo + P.R > m) P.r_lo = m - P.R;
-            if (P.r_lo < cc) { P.stream = true; }
-        } else {
-            P.stream = true;
-        }
-        if (P.stream) { P.c = P.r_lo = P.R = 0; }
+        P.stream = !fits(wlo, whi);
+        P.c = P.r_lo = P.R = 0;
         P.ops.push_back(op);
         passes.push_back(P);
+        span_lo = wlo; span_hi = whi;
     }
+    if (!passes.empty()) close(passes.back());
     return passes;
 }
 
@@ -599,6 +480,23 @@ struct Plan {
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+static void dump_plan(const Plan& P) {
+    auto dc = [](const char* nm, const std::vector<CvtPass>& v) {
+        fprintf(stderr, "[gf2x plan] %s:", nm);
+        for (auto& p : v) {
+            if (p.stream) fprintf(stderr, " stream(%d,%d)", p.ops[0].lg - 1 - p.ops[0].K, p.ops[0].lg);
+            else fprintf(stderr, " tile{c=%d rows=[%d,%d) ops=%zu}", p.c, p.r_lo, p.r_lo + p.R, p.ops.size());
+        }
+        fprintf(stderr, "\n");
+    };
+    dc("cvt_a", P.cvt_a);
+    dc("icvt", P.icvt);
+    fprintf(stderr, "[gf2x plan] fft:");
+    for (auto& f : P.fft) fprintf(stderr, f.bottom ? " bottom{tile=%d layers=%d}" : " direct{c=%d [%d,%d)}", f.bottom ? f.k_hi : f.c,
+                                  f.bottom ? f.layers : f.k_lo, f.k_hi);
+    fprintf(stderr, "\n");
+}
+
 static gf2x_status make_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, Plan& P) {
     if (batch < 0) return fail(GF2X_EINVAL, "negative batch");
     P.na = (a_bits + 63) / 64;
@@ -620,13 +518,13 @@ static gf2x_status make_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, Pl
     P.off_wa = align256(P.off_sb + (1ull << P.mb) * P.batch * 8);
     P.off_wb = align256(P.off_wa + spec * 16);
     P.bytes = align256(P.off_wb + spec * 16);
+    if (getenv("GF2X_DEBUG_PLAN")) dump_plan(P);
     return GF2X_OK;
 }
 
 static int launches_of(const Plan& P) {
     int n = 2;  // prep a, b
-    for (auto* v : {&P.cvt_a, &P.cvt_b, &P.icvt})
-        for (auto& p : *v) n += p.stream ? 2 : 1;
+    for (auto* v : {&P.cvt_a, &P.cvt_b, &P.icvt}) n += (int)v->size();
     n += 2 * (int)P.fft.size();  // forward a, b
     n += 1;                      // pointmul
     n += (int)P.fft.size();      // inverse
@@ -654,28 +552,22 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
         const CvtPass& p = *pp;
         if (p.stream) {
             const CvtOp op = p.ops[0];
-            const uint64_t h = 1ull << (op.lg - 1), u = h >> op.K;
-            const uint64_t nA = (per * batch >> op.lg) * u, nB = (per * batch >> op.lg) * (h - u);
-            const int first = inverse ? 0 : 1;  // phaseA flag of the first sweep
-            for (int sw = 0; sw < 2; sw++) {
-                const int phaseA = (sw == 0) ? first : 1 - first;
-                const uint64_t n = phaseA ? nA : nB;
-                ProfScope ps(sizeof(T) == 8 ? "k_cvt_stream<u64>" : "k_cvt_stream<u128>", 3.0 * n * sizeof(T), st);
-                k_cvt_stream<T><<<grid_for(n, 256, sm_count, 8), 256, 0, st>>>(data, per * batch, op.lg, op.K, phaseA);
-            }
+            const uint64_t n = per * batch / 2;
+            ProfScope ps(sizeof(T) == 8 ? "k_cvt_stream<u64>" : "k_cvt_stream<u128>", 3.0 * n * sizeof(T), st);
+            k_cvt_stream<T><<<grid_for(n, 256, sm_count, 8), 256, 0, st>>>(data, per * batch, op.lg, op.K, inverse ? 1 : 0);
         } else {
             CvtTileParams prm;
             prm.data = data;
             prm.units_per_pair = per;
             prm.batch = batch;
-            prm.m = m; prm.c = p.c; prm.r_lo = p.r_lo; prm.R = p.R;
+            prm.c = p.c; prm.r_lo = p.r_lo; prm.R = p.R;
             prm.inverse = inverse ? 1 : 0;
             prm.nops = (int)p.ops.size();
             for (int i = 0; i < prm.nops; i++) prm.ops[i] = inverse ? p.ops[prm.nops - 1 - i] : p.ops[i];
             const size_t sm = ((size_t)1 << (p.c + p.R)) * sizeof(T);
             const uint64_t ntiles = (per >> (p.c + p.R)) * batch;
             ProfScope ps(sizeof(T) == 8 ? "k_cvt_tile<u64>" : "k_cvt_tile<u128>", 2.0 * per * batch * sizeof(T), st);
-            k_cvt_tile<T><<<grid_for(ntiles, 1, sm_count, 3), 256, sm, st>>>(prm);
+            k_cvt_tile<T><<<grid_for(ntiles, 1, sm_count, sm > 114 * 1024 ? 1 : 2), 512, sm, st>>>(prm);
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("cvt launch: ") + cudaGetErrorString(e));
@@ -750,9 +642,9 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
     {
         const uint64_t total = P.N * P.batch;
         const uint64_t ntiles = (total + PM_THREADS * 32 - 1) / (PM_THREADS * 32);
-        const size_t sm = (size_t)(2 * PM_THREADS * PM_ROW + PM_THREADS * 128) * 4;
+        const size_t sm = (size_t)PM_THREADS * (PM_WORDS + 1) * 4;
         ProfScope ps("k_pointmul", 48.0 * total, st);
-        k_pointmul<<<grid_for(ntiles, 1, smc, 2), PM_THREADS, sm, st>>>(Wa, Wb, total);
+        k_pointmul<<<grid_for(ntiles, 1, smc, 1), PM_THREADS, sm, st>>>(Wa, Wb, total);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("pointmul launch: ") + cudaGetErrorString(e));
     }
