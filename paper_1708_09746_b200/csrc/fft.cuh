@@ -1,14 +1,10 @@
 // fft.cuh -- FFT_LCH / iFFT_LCH passes (Alg. 1, inverse P:408), included by gf2x.cu.
 //
-// A pass handles the layers of one tile of the index space held in shared memory:
-//   * "direct" passes: tile bits [0,c) U [k_lo,k_hi), c >= 5, layers k_hi-1 .. k_lo.  All lanes of
-//     a warp work on different columns (bits < c) of the same rows, so every multiplier is
-//     warp-uniform; the 2^R - 1 distinct multipliers of the tile (one per block per layer) get one
-//     M4R-4 table each, built once per tile.
-//   * the "bottom" pass: contiguous tile bits [0,Rt), layers BOT_B-1 .. 0.  The multiplier of a
-//     block b is s_k(phi(b)) = s_k(phi(b_hi)) ^ s_k(phi(b_lo)) (s_k is GF(2)-linear, A10), b_lo =
-//     bits (k, BOT_B) of b: the first term gets a table per 2^BOT_B-element sub-block of the tile
-//     (built per tile), the second one of 2^BOT_B - 1 fixed tables shared by every tile.
+// A pass handles the layers k_hi-1 .. k_lo of tiles with index bits [0,c) U [k_lo,k_hi) (c >= 5,
+// k_lo >= BOT_B) held in shared memory.  All lanes of a warp work on different columns (bits < c)
+// of the same rows, so every multiplier is warp-uniform; the 2^R - 1 distinct multipliers of a tile
+// (one per block per layer) get one M4R-4 table each, built once per tile.  The layers below BOT_B
+// run in the fused bit-sliced bottom kernel (bottom.cuh).
 // Inside a pass the layers run in groups of up to three: each thread holds the 2^r elements of a
 // radix-2^r sub-transform in registers, so shared-memory traffic is one load/store per element per
 // group instead of per layer.
@@ -18,8 +14,7 @@
 #pragma once
 
 #define FFT_THREADS 256
-#define BOT_B 6       // bottom pass: fixed multiplier tables cover index bits [0, BOT_B)
-#define BOT_RT 10     // bottom pass tile: 2^10 contiguous elements
+#define BOT_B 6       // layers [0, BOT_B) run in the fused bit-sliced bottom kernel
 
 // ---------------------------------------------------------------------------------------------
 // shared-memory M4R-4 lookups with the table base fused into the byte-permute that extracts the
@@ -46,21 +41,6 @@ __device__ __forceinline__ uint32_t m4r4_word_sa(uint32_t tab, uint32_t x) {
     r ^= lds_off<448>(__byte_perm(o, tab, 0x7653));
     return r;
 }
-// same for two tables (hi/lo multiplier split): x * (c1 + c2)
-__device__ __forceinline__ uint32_t m4r4_word_sa2(uint32_t t1, uint32_t t2, uint32_t x) {
-    const uint32_t e = (x << 2) & 0x3C3C3C3Cu;
-    const uint32_t o = (x >> 2) & 0x3C3C3C3Cu;
-    uint32_t r = lds_off<0>(__byte_perm(e, t1, 0x7650)) ^ lds_off<0>(__byte_perm(e, t2, 0x7650));
-    r ^= lds_off<64>(__byte_perm(o, t1, 0x7650)) ^ lds_off<64>(__byte_perm(o, t2, 0x7650));
-    r ^= lds_off<128>(__byte_perm(e, t1, 0x7651)) ^ lds_off<128>(__byte_perm(e, t2, 0x7651));
-    r ^= lds_off<192>(__byte_perm(o, t1, 0x7651)) ^ lds_off<192>(__byte_perm(o, t2, 0x7651));
-    r ^= lds_off<256>(__byte_perm(e, t1, 0x7652)) ^ lds_off<256>(__byte_perm(e, t2, 0x7652));
-    r ^= lds_off<320>(__byte_perm(o, t1, 0x7652)) ^ lds_off<320>(__byte_perm(o, t2, 0x7652));
-    r ^= lds_off<384>(__byte_perm(e, t1, 0x7653)) ^ lds_off<384>(__byte_perm(e, t2, 0x7653));
-    r ^= lds_off<448>(__byte_perm(o, t1, 0x7653)) ^ lds_off<448>(__byte_perm(o, t2, 0x7653));
-    return r;
-}
-
 // Row t (16 words) of the M4R-4 table of constant c: tab[16t + x] = (c v_(4t)) * x, x in GF(16).
 // c v_(4t) = w comes from the M4R-8 tables of the fixed maps c -> c v_(4t); x = sum of x_b v_b
 // (v_0 = 1, v_1 = x1, v_2 = x2, v_3 = x1 x2) so the row is the XOR-span of w, x1 w, x2 w, x1 x2 w.
@@ -87,41 +67,28 @@ struct FftParams {
     uint64_t src_per;
     uint64_t batch;
     int m;                // N = 2^m points per product
-    int c, k_lo, k_hi;    // direct: tile bits [0,c) U [k_lo,k_hi); bottom: c = k_lo = 0, Rt = k_hi
-    int layers;           // bottom: number of layers (<= BOT_B)
+    int c, k_lo, k_hi;    // tile bits [0,c) U [k_lo,k_hi)
 };
 
 __device__ __forceinline__ uint32_t tab_addr(uint32_t base, uint32_t id) { return base + id * 512u; }
 
-template <bool INV, bool BOTTOM>
-__device__ __forceinline__ void bfly(uint4& x0, uint4& x1, uint32_t ta, uint32_t tb) {
+template <bool INV>
+__device__ __forceinline__ void bfly(uint4& x0, uint4& x1, uint32_t ta) {
     if (!INV) {
-        if (BOTTOM) {
-            x0.x ^= m4r4_word_sa2(ta, tb, x1.x); x0.y ^= m4r4_word_sa2(ta, tb, x1.y);
-            x0.z ^= m4r4_word_sa2(ta, tb, x1.z); x0.w ^= m4r4_word_sa2(ta, tb, x1.w);
-        } else {
-            x0.x ^= m4r4_word_sa(ta, x1.x); x0.y ^= m4r4_word_sa(ta, x1.y);
-            x0.z ^= m4r4_word_sa(ta, x1.z); x0.w ^= m4r4_word_sa(ta, x1.w);
-        }
+        x0.x ^= m4r4_word_sa(ta, x1.x); x0.y ^= m4r4_word_sa(ta, x1.y);
+        x0.z ^= m4r4_word_sa(ta, x1.z); x0.w ^= m4r4_word_sa(ta, x1.w);
         x1 = xor4(x1, x0);
     } else {
         x1 = xor4(x1, x0);
-        if (BOTTOM) {
-            x0.x ^= m4r4_word_sa2(ta, tb, x1.x); x0.y ^= m4r4_word_sa2(ta, tb, x1.y);
-            x0.z ^= m4r4_word_sa2(ta, tb, x1.z); x0.w ^= m4r4_word_sa2(ta, tb, x1.w);
-        } else {
-            x0.x ^= m4r4_word_sa(ta, x1.x); x0.y ^= m4r4_word_sa(ta, x1.y);
-            x0.z ^= m4r4_word_sa(ta, x1.z); x0.w ^= m4r4_word_sa(ta, x1.w);
-        }
+        x0.x ^= m4r4_word_sa(ta, x1.x); x0.y ^= m4r4_word_sa(ta, x1.y);
+        x0.z ^= m4r4_word_sa(ta, x1.z); x0.w ^= m4r4_word_sa(ta, x1.w);
     }
 }
 
 // One group of r consecutive layers [ka, ka+r) whose slot bits are [s0, s0+r).
-// Direct: table id of (layer k, slot) = 2^(R-1-kk) - 1 + (row >> (kk+1)), row = slot >> c, kk = k-k_lo.
-// Bottom: hi table id = k * nsub + (slot >> BOT_B); fixed lo id = 2^(BOT_B-1-k) - 1 + ((slot & 63) >> (k+1)).
-template <int r, bool INV, bool BOTTOM>
-__device__ __forceinline__ void fft_group(uint4* tile, uint32_t nslots, int s0, int ka, const FftParams& p,
-                                          uint32_t tabs_sa, uint32_t fixed_sa, uint32_t nsub) {
+// Table id of (layer k, slot) = 2^(R-1-kk) - 1 + (row >> (kk+1)), row = slot >> c, kk = k - k_lo.
+template <int r, bool INV>
+__device__ __forceinline__ void fft_group(uint4* tile, uint32_t nslots, int s0, int ka, const FftParams& p, uint32_t tabs_sa) {
     const uint32_t nitems = nslots >> r;
     const int R = p.k_hi - p.k_lo;
     for (uint32_t it = threadIdx.x; it < nitems; it += blockDim.x) {
@@ -132,21 +99,12 @@ __device__ __forceinline__ void fft_group(uint4* tile, uint32_t nslots, int s0, 
 #pragma unroll
         for (int li = 0; li < r; li++) {
             const int lb = INV ? li : (r - 1 - li);   // local bit of this layer
-            const int k = ka + lb;
+            const int kk = ka + lb - p.k_lo;
 #pragma unroll
             for (int j = 0; j < (1 << r); j++) {
                 if (j & (1 << lb)) continue;
-                const uint32_t slot = base | ((uint32_t)j << s0);
-                uint32_t ta, tb = 0;
-                if (BOTTOM) {
-                    ta = tab_addr(tabs_sa, (uint32_t)k * nsub + (slot >> BOT_B));
-                    tb = tab_addr(fixed_sa, ((1u << (BOT_B - 1 - k)) - 1) + ((slot & ((1u << BOT_B) - 1)) >> (k + 1)));
-                } else {
-                    const int kk = k - p.k_lo;
-                    const uint32_t row = slot >> p.c;
-                    ta = tab_addr(tabs_sa, ((1u << (R - 1 - kk)) - 1) + (row >> (kk + 1)));
-                }
-                bfly<INV, BOTTOM>(v[j], v[j | (1 << lb)], ta, tb);
+                const uint32_t row = (base | ((uint32_t)j << s0)) >> p.c;
+                bfly<INV>(v[j], v[j | (1 << lb)], tab_addr(tabs_sa, ((1u << (R - 1 - kk)) - 1) + (row >> (kk + 1))));
             }
         }
 #pragma unroll
@@ -154,32 +112,26 @@ __device__ __forceinline__ void fft_group(uint4* tile, uint32_t nslots, int s0, 
     }
 }
 
-template <bool INV, bool BOTTOM>
+template <bool INV>
 __device__ __forceinline__ void fft_group_any(int r, uint4* tile, uint32_t nslots, int s0, int ka, const FftParams& p,
-                                              uint32_t tabs_sa, uint32_t fixed_sa, uint32_t nsub) {
-    if (r == 3) fft_group<3, INV, BOTTOM>(tile, nslots, s0, ka, p, tabs_sa, fixed_sa, nsub);
-    else if (r == 2) fft_group<2, INV, BOTTOM>(tile, nslots, s0, ka, p, tabs_sa, fixed_sa, nsub);
-    else fft_group<1, INV, BOTTOM>(tile, nslots, s0, ka, p, tabs_sa, fixed_sa, nsub);
+                                              uint32_t tabs_sa) {
+    if (r == 3) fft_group<3, INV>(tile, nslots, s0, ka, p, tabs_sa);
+    else if (r == 2) fft_group<2, INV>(tile, nslots, s0, ka, p, tabs_sa);
+    else fft_group<1, INV>(tile, nslots, s0, ka, p, tabs_sa);
 }
 
-// shared memory: [tables (ntab x 512 B)] [fixed tables (bottom)] [psi table (PSI)] [tile]
-template <bool INV, bool PSI, bool BOTTOM>
+// shared memory: [tables (2^R - 1) x 512 B] [psi table (PSI)] [tile]
+template <bool INV, bool PSI>
 __global__ void __launch_bounds__(FFT_THREADS) k_fft2(FftParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const int R = p.k_hi - p.k_lo;                       // tile row bits (bottom: Rt)
+    const int R = p.k_hi - p.k_lo;
     const uint32_t nslots = 1u << (p.c + R);
-    const int nlayers = BOTTOM ? p.layers : R;
-    const uint32_t nsub = BOTTOM ? (nslots > (1u << BOT_B) ? nslots >> BOT_B : 1u) : 1u;
-    const uint32_t ntab = BOTTOM ? (uint32_t)nlayers * nsub : ((1u << R) - 1);
+    const uint32_t ntab = (1u << R) - 1;
     uint32_t* tabs = reinterpret_cast<uint32_t*>(smem_raw);
-    uint32_t* fixed = tabs + ntab * 128;
-    uint4* psit = reinterpret_cast<uint4*>(fixed + (BOTTOM ? ((1u << BOT_B) - 1) * 128 : 0));
+    uint4* psit = reinterpret_cast<uint4*>(tabs + ntab * 128);
     uint4* tile = psit + (PSI ? 8 * 256 : 0);
     const uint32_t tabs_sa = (uint32_t)__cvta_generic_to_shared(tabs);
-    const uint32_t fixed_sa = (uint32_t)__cvta_generic_to_shared(fixed);
     if (tabs_sa & 255) __trap();  // the PRMT address fusion needs 256-byte aligned tables
-    if (BOTTOM)
-        for (uint32_t i = threadIdx.x; i < ((1u << BOT_B) - 1) * 128; i += blockDim.x) fixed[i] = p.tabs->cloc[i];
     if (PSI)
         for (uint32_t i = threadIdx.x; i < 8 * 256; i += blockDim.x) psit[i] = p.tabs->psi64[i];
 
@@ -194,23 +146,14 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft2(FftParams p) {
         // base index (within the pair) of the tile: bits [c, k_lo) and >= k_hi come from tt
         const int midbits = p.k_lo - p.c;
         const uint32_t base = ((tt & ((1u << midbits) - 1)) << p.c) | ((uint32_t)((uint64_t)(tt >> midbits) << p.k_hi));
-        // ---- tables of this tile's multipliers
+        // ---- tables of this tile's multipliers: id -> (layer kk, block blk)
         for (uint32_t i = threadIdx.x; i < ntab * 8; i += blockDim.x) {
             const uint32_t id = i >> 3;
-            const int trow = i & 7;
-            uint32_t cst;
-            if (BOTTOM) {
-                const int k = (int)(id / nsub);
-                const uint32_t sub = id - (uint32_t)k * nsub;
-                cst = layer_const(k, base | (sub << BOT_B));
-            } else {
-                const int lg = 31 - __clz(id + 1);          // = R-1-kk
-                const int kk = R - 1 - lg;
-                const uint32_t blk = id + 1 - (1u << lg);
-                const int k = p.k_lo + kk;
-                cst = layer_const(k, (uint32_t)(((uint64_t)base & ~((2ull << k) - 1)) | ((uint64_t)blk << (k + 1))));
-            }
-            build_tab_row(tabs + id * 128, cst, trow, p.tabs->wt);
+            const int lg = 31 - __clz(id + 1);          // = R-1-kk
+            const int k = p.k_lo + R - 1 - lg;
+            const uint32_t blk = id + 1 - (1u << lg);
+            const uint32_t cst = layer_const(k, (uint32_t)(((uint64_t)base & ~((2ull << k) - 1)) | ((uint64_t)blk << (k + 1))));
+            build_tab_row(tabs + id * 128, cst, (int)(i & 7), p.tabs->wt);
         }
         // ---- load
         if (PSI) {
@@ -232,24 +175,20 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft2(FftParams p) {
         }
         __syncthreads();
         // ---- layers, in groups of <= 3 (forward: from the top; inverse: from the bottom)
-        const int lo = BOTTOM ? 0 : p.k_lo;
-        const int hi = lo + nlayers;
         if (!INV) {
-            int top = hi;
-            while (top > lo) {
-                const int r = (top - lo) >= 3 ? 3 : (top - lo);
+            int top = p.k_hi;
+            while (top > p.k_lo) {
+                const int r = (top - p.k_lo) >= 3 ? 3 : (top - p.k_lo);
                 const int ka = top - r;
-                const int s0 = BOTTOM ? ka : (p.c + ka - p.k_lo);
-                fft_group_any<INV, BOTTOM>(r, tile, nslots, s0, ka, p, tabs_sa, fixed_sa, nsub);
+                fft_group_any<INV>(r, tile, nslots, p.c + ka - p.k_lo, ka, p, tabs_sa);
                 __syncthreads();
                 top = ka;
             }
         } else {
-            int bot = lo;
-            while (bot < hi) {
-                const int r = (hi - bot) >= 3 ? 3 : (hi - bot);
-                const int s0 = BOTTOM ? bot : (p.c + bot - p.k_lo);
-                fft_group_any<INV, BOTTOM>(r, tile, nslots, s0, bot, p, tabs_sa, fixed_sa, nsub);
+            int bot = p.k_lo;
+            while (bot < p.k_hi) {
+                const int r = (p.k_hi - bot) >= 3 ? 3 : (p.k_hi - bot);
+                fft_group_any<INV>(r, tile, nslots, p.c + bot - p.k_lo, bot, p, tabs_sa);
                 __syncthreads();
                 bot += r;
             }
@@ -261,11 +200,8 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft2(FftParams p) {
     }
 }
 
-static size_t fft2_smem(int c, int R, int layers, bool psi, bool bottom) {
-    size_t ntab = bottom ? (size_t)layers * (((size_t)1 << (c + R)) > ((size_t)1 << BOT_B) ? ((size_t)1 << (c + R)) >> BOT_B : 1)
-                         : (((size_t)1 << R) - 1);
-    size_t s = ntab * 512;
-    if (bottom) s += (((size_t)1 << BOT_B) - 1) * 512;
+static size_t fft2_smem(int c, int R, bool psi) {
+    size_t s = (((size_t)1 << R) - 1) * 512;
     if (psi) s += 8 * 256 * 16;
     s += ((size_t)1 << (c + R)) * 16;
     return s;

@@ -3,10 +3,11 @@
 // Pipeline (Alg. 5), per product of n_a x n_b 64-bit words, N = 2^m points:
 //   k_prep          Split: copy + mask words into the conversion scratch S (u64)
 //   k_cvt_*         BasisCvt (Alg. 3 P:518-539 / Alg. 2) on 64-bit words, in place in S
-//   k_fft<psi>      changeRepr (§4.3) fused into the first FFT_LCH pass (Alg. 1)
-//   k_fft           remaining FFT_LCH layers (tiles of layers through shared memory)
-//   k_pointmul      pointmul: bit-sliced TGF(2^128) Karatsuba
-//   k_fft<inverse>  iFFT_LCH
+//   k_fft2<psi>     changeRepr (§4.3) fused into the first FFT_LCH pass (Alg. 1)
+//   k_fft2          FFT_LCH layers >= 6 (tiles of layers through shared memory, M4R-4 tables)
+//   k_bottom        FFT_LCH layers < 6 of a and b, pointmul, iFFT_LCH layers < 6,
+//                   fused and bit-sliced
+//   k_fft2<inverse> iFFT_LCH layers >= 6
 //   k_cvt_*         iBasisCvt on 128-bit tower elements
 //   k_ipsi_combine  changeRepr back + InterleavedCombine
 // Every step runs in these kernels; the host only plans passes and enqueues launches.
@@ -36,7 +37,6 @@ struct DevTables {
     uint4 psi64[8 * 256];    // M4R-8 of changeRepr on a 64-bit polynomial-basis block -> tower
     uint4 ipsi[16 * 256];    // M4R-8 of changeRepr^-1: 128-bit tower element -> polynomial basis
     uint32_t wt[7 * 1024];   // M4R-8 of c -> c * v_(4t), t = 1..7 (table-build helper)
-    uint32_t cloc[63 * 128]; // M4R-4 tables of the fixed low multiplier parts s_k(phi(j 2^(k+1))), k < 6
     uint32_t S[32 * 32];     // S[k][j] = s_k(v_j): images of the basis under s_k (§4.4)
 };
 
@@ -94,41 +94,6 @@ __global__ void k_prep(const uint64_t* __restrict__ in, uint64_t n, uint64_t bit
 // Each product is one generated straight-line bit-sliced Karatsuba (bs_mul32); only one is live
 // in registers at a time.
 // =============================================================================================
-#define PM_THREADS 128
-#define PM_WORDS 384   // per thread: A planes 128, B planes 128, R accumulators 128
-
-// in-place bit-slicing of the thread's 32 elements (limb L of element e at row[4e + L])
-__device__ __forceinline__ void slice_limb(uint32_t* row, int L) {
-    uint32_t x[32];
-#pragma unroll
-    for (int e = 0; e < 32; e++) x[e] = row[4 * e + L];
-    transpose32(x);
-#pragma unroll
-    for (int j = 0; j < 32; j++) row[4 * j + L] = x[j];
-}
-
-// planes of (sum of the limbs in mask) of operand row: plane j of limb L is row[4j + L]
-__device__ __forceinline__ void load_sum(const uint32_t* row, int mask, uint32_t* x) {
-#pragma unroll
-    for (int j = 0; j < 32; j++) x[j] = 0;
-#pragma unroll
-    for (int L = 0; L < 4; L++)
-        if (mask & (1 << L)) {
-#pragma unroll
-            for (int j = 0; j < 32; j++) x[j] ^= row[4 * j + L];
-        }
-}
-
-// acc limbs (mask) ^= v
-__device__ __forceinline__ void acc_add(uint32_t* acc, int mask, const uint32_t* v) {
-#pragma unroll
-    for (int L = 0; L < 4; L++)
-        if (mask & (1 << L)) {
-#pragma unroll
-            for (int j = 0; j < 32; j++) acc[4 * j + L] ^= v[j];
-        }
-}
-
 // (limb mask of the factors, limbs receiving r, limbs receiving v31 r, limbs receiving v31^2 r)
 __constant__ int c_pm_terms[9][4] = {
     {0x1, 0xF, 0x0, 0x0},   // P0  -> R0 R1 R2 R3
@@ -142,54 +107,7 @@ __constant__ int c_pm_terms[9][4] = {
     {0xF, 0x8, 0x0, 0x0},   // Q01 -> R3
 };
 
-__global__ void __launch_bounds__(PM_THREADS) k_pointmul(uint4* __restrict__ A, const uint4* __restrict__ B, uint64_t total) {
-    extern __shared__ __align__(1024) uint32_t pm_smem[];
-    // thread t: ra = A elements (32 x 4 words), rb = B elements, acc = result; rows padded by one
-    // word per thread block of 32 elements so that the per-thread strided accesses hit distinct banks
-    uint32_t* ra = pm_smem + threadIdx.x * (PM_WORDS + 1);
-    uint32_t* rb = ra + 128;
-    uint32_t* acc = rb + 128;
-    const uint64_t per_cta = PM_THREADS * 32ull;
-    const uint64_t ntiles = (total + per_cta - 1) / per_cta;
-    for (uint64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-        const uint64_t e0 = tl * per_cta;
-        // coalesced load: element i of the CTA tile -> thread i/32, slot i%32
-        for (uint32_t i = threadIdx.x; i < per_cta; i += PM_THREADS) {
-            const uint64_t e = e0 + i;
-            uint4 va = make_uint4(0, 0, 0, 0), vb = make_uint4(0, 0, 0, 0);
-            if (e < total) { va = A[e]; vb = B[e]; }
-            uint32_t* da = pm_smem + (i >> 5) * (PM_WORDS + 1) + (i & 31) * 4;
-            da[0] = va.x; da[1] = va.y; da[2] = va.z; da[3] = va.w;
-            da[128] = vb.x; da[129] = vb.y; da[130] = vb.z; da[131] = vb.w;
-        }
-        __syncthreads();
-#pragma unroll 1
-        for (int L = 0; L < 4; L++) { slice_limb(ra, L); slice_limb(rb, L); }
-#pragma unroll 1
-        for (int i = 0; i < 128; i++) acc[i] = 0;
-#pragma unroll 1
-        for (int q = 0; q < 9; q++) {
-            uint32_t x[32], y[32], r[32];
-            load_sum(ra, c_pm_terms[q][0], x);
-            load_sum(rb, c_pm_terms[q][0], y);
-            bs_mul32(x, y, r);
-            acc_add(acc, c_pm_terms[q][1], r);
-            if (c_pm_terms[q][2]) { bs_mul_v31(r, x); acc_add(acc, c_pm_terms[q][2], x); }
-            if (c_pm_terms[q][3]) { bs_mul_v31sq(r, y); acc_add(acc, c_pm_terms[q][3], y); }
-        }
-#pragma unroll 1
-        for (int L = 0; L < 4; L++) slice_limb(acc, L);   // transpose32 is an involution
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < per_cta; i += PM_THREADS) {
-            const uint64_t e = e0 + i;
-            if (e < total) {
-                const uint32_t* r = pm_smem + (i >> 5) * (PM_WORDS + 1) + 256 + (i & 31) * 4;
-                A[e] = make_uint4(r[0], r[1], r[2], r[3]);
-            }
-        }
-        __syncthreads();
-    }
-}
+#include "bottom.cuh"
 
 // =============================================================================================
 // changeRepr^-1 + InterleavedCombine: C_i = psi^-1(P[i]) (deg <= 126),
@@ -334,17 +252,6 @@ static void host_build_tables(DevTables* T) {
             v = s1(v);
         }
     }
-    // cloc: fixed low parts for the bottom FFT pass: table id 2^(BOT_B-1-k) - 1 + j holds the
-    // constant s_k(phi(j 2^(k+1))) (local index bits (k, BOT_B)), k < BOT_B
-    for (int k = 0; k < BOT_B; k++)
-        for (int j = 0; j < (1 << (BOT_B - 1 - k)); j++) {
-            uint32_t bb = (uint32_t)j << (k + 1), e = 0;
-            for (int i = k + 1; i < BOT_B; i++)
-                if ((bb >> i) & 1) e ^= T->S[k * 32 + i];
-            uint32_t* tab = T->cloc + (((1 << (BOT_B - 1 - k)) - 1) + j) * 128;
-            for (int t = 0; t < 8; t++)
-                for (int x = 0; x < 16; x++) tab[16 * t + x] = (uint32_t)tower_mul((u128)e, ((u128)x) << (4 * t));
-        }
 }
 
 static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
@@ -364,15 +271,12 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
         if (e != cudaSuccess) { cudaFree(d); return fail(GF2X_ECUDA, cudaGetErrorString(e)); }
         CUDA_TRY(cudaDeviceGetAttribute(&st.sm_count, cudaDevAttrMultiProcessorCount, dev));
         // opt-in shared memory sizes
-        CUDA_TRY(cudaFuncSetAttribute(k_fft2<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_fft2<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_fft2<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_fft2<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_fft2<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_fft2<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_fft2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_fft2<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_fft2<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_tile<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_tile<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_pointmul, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_ipsi_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         st.tabs = d;
     }
@@ -465,8 +369,7 @@ static std::vector<FftPass> plan_fft(int m) {
         v.push_back({i == 0 ? 5 : 6, lo, top, false, 0});
         top = lo;
     }
-    const int rt = m < BOT_RT ? m : BOT_RT;
-    v.push_back({0, 0, rt, true, m < BOT_B ? m : BOT_B});
+    v.push_back({0, 0, 0, true, m < BOT_B ? m : BOT_B});  // the fused bit-sliced bottom kernel
     return v;
 }
 
@@ -492,8 +395,10 @@ static void dump_plan(const Plan& P) {
     dc("cvt_a", P.cvt_a);
     dc("icvt", P.icvt);
     fprintf(stderr, "[gf2x plan] fft:");
-    for (auto& f : P.fft) fprintf(stderr, f.bottom ? " bottom{tile=%d layers=%d}" : " direct{c=%d [%d,%d)}", f.bottom ? f.k_hi : f.c,
-                                  f.bottom ? f.layers : f.k_lo, f.k_hi);
+    for (auto& f : P.fft) {
+        if (f.bottom) fprintf(stderr, " bottom{layers=%d}", f.layers);
+        else fprintf(stderr, " direct{c=%d [%d,%d)}", f.c, f.k_lo, f.k_hi);
+    }
     fprintf(stderr, "\n");
 }
 
@@ -525,9 +430,10 @@ static gf2x_status make_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, Pl
 static int launches_of(const Plan& P) {
     int n = 2;  // prep a, b
     for (auto* v : {&P.cvt_a, &P.cvt_b, &P.icvt}) n += (int)v->size();
-    n += 2 * (int)P.fft.size();  // forward a, b
-    n += 1;                      // pointmul
-    n += (int)P.fft.size();      // inverse
+    const int nd = (int)P.fft.size() - 1;
+    n += 2 * (nd ? nd : 1);      // forward a, b (or the changeRepr-only pass)
+    n += 1;                      // fused bottom
+    n += nd;                     // inverse
     n += 1;                      // ipsi + combine
     return n;
 }
@@ -580,24 +486,17 @@ static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* 
     FftParams prm;
     prm.src = src; prm.dst = dst; prm.tabs = ds->tabs;
     prm.src_per = src_per; prm.batch = P.batch;
-    prm.m = P.m; prm.c = f.c; prm.k_lo = f.k_lo; prm.k_hi = f.k_hi; prm.layers = f.layers;
+    prm.m = P.m; prm.c = f.c; prm.k_lo = f.k_lo; prm.k_hi = f.k_hi;
     const int R = f.k_hi - f.k_lo;
     const uint64_t ntiles = (P.N >> (f.c + R)) * P.batch;
-    const size_t sm = fft2_smem(f.c, R, f.layers, psi, f.bottom);
+    const size_t sm = fft2_smem(f.c, R, psi);
     const int occ = sm > 113 * 1024 ? 1 : (sm > 75 * 1024 ? 2 : 3);
     const int grid = grid_for(ntiles, 1, ds->sm_count, occ);
     const double bytes = (double)P.batch * (psi ? (double)src_per * 8 : (double)P.N * 16) + (double)P.batch * P.N * 16;
-    ProfScope ps(f.bottom ? (inv ? "k_fft_bottom<inv>" : (psi ? "k_fft_bottom<psi>" : "k_fft_bottom"))
-                          : (inv ? "k_fft<inv>" : (psi ? "k_fft<psi>" : "k_fft")), bytes, st);
-    if (f.bottom) {
-        if (inv) k_fft2<true, false, true><<<grid, FFT_THREADS, sm, st>>>(prm);
-        else if (psi) k_fft2<false, true, true><<<grid, FFT_THREADS, sm, st>>>(prm);
-        else k_fft2<false, false, true><<<grid, FFT_THREADS, sm, st>>>(prm);
-    } else {
-        if (inv) k_fft2<true, false, false><<<grid, FFT_THREADS, sm, st>>>(prm);
-        else if (psi) k_fft2<false, true, false><<<grid, FFT_THREADS, sm, st>>>(prm);
-        else k_fft2<false, false, false><<<grid, FFT_THREADS, sm, st>>>(prm);
-    }
+    ProfScope ps(inv ? "k_fft<inv>" : (psi ? "k_fft<psi>" : "k_fft"), bytes, st);
+    if (inv) k_fft2<true, false><<<grid, FFT_THREADS, sm, st>>>(prm);
+    else if (psi) k_fft2<false, true><<<grid, FFT_THREADS, sm, st>>>(prm);
+    else k_fft2<false, false><<<grid, FFT_THREADS, sm, st>>>(prm);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("fft launch: ") + cudaGetErrorString(e));
     return GF2X_OK;
@@ -625,32 +524,39 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
     // BasisCvt on 64-bit blocks
     if ((s = run_cvt<uint64_t>(P.cvt_a, Sa, P.ma, P.batch, false, smc, st)) != GF2X_OK) return s;
     if ((s = run_cvt<uint64_t>(P.cvt_b, Sb, P.mb, P.batch, false, smc, st)) != GF2X_OK) return s;
-    // changeRepr + FFT_LCH
-    for (size_t i = 0; i < P.fft.size(); i++) {
+    // changeRepr + FFT_LCH top layers (direct passes; the last planned pass is the bottom one)
+    const size_t ndirect = P.fft.size() - 1;
+    for (size_t i = 0; i < ndirect; i++) {
         const bool first = (i == 0);
-        const bool only_psi = (stop_stage == 1);
         FftPass f = P.fft[i];
-        if (only_psi) {  // changeRepr only
+        if (stop_stage == 1) {  // changeRepr only
             if (!first) break;
-            if (f.bottom) f.layers = 0; else f.k_lo = f.k_hi;
+            f.k_lo = f.k_hi;
         }
         if ((s = launch_fft(f, false, first, first ? (const void*)Sa : Wa, first ? (1ull << P.ma) : P.N, Wa, P, ds, st)) != GF2X_OK) return s;
         if ((s = launch_fft(f, false, first, first ? (const void*)Sb : Wb, first ? (1ull << P.mb) : P.N, Wb, P, ds, st)) != GF2X_OK) return s;
     }
-    if (stop_stage == 1 || stop_stage == 2) return GF2X_OK;
-    // pointmul
-    {
-        const uint64_t total = P.N * P.batch;
-        const uint64_t ntiles = (total + PM_THREADS * 32 - 1) / (PM_THREADS * 32);
-        const size_t sm = (size_t)PM_THREADS * (PM_WORDS + 1) * 4;
-        ProfScope ps("k_pointmul", 48.0 * total, st);
-        k_pointmul<<<grid_for(ntiles, 1, smc, 1), PM_THREADS, sm, st>>>(Wa, Wb, total);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("pointmul launch: ") + cudaGetErrorString(e));
+    if (ndirect == 0) {  // m <= BOT_B: changeRepr alone (a direct pass with no layers)
+        FftPass f{P.m < 5 ? P.m : 5, P.m, P.m, false, 0};
+        if ((s = launch_fft(f, false, true, Sa, 1ull << P.ma, Wa, P, ds, st)) != GF2X_OK) return s;
+        if ((s = launch_fft(f, false, true, Sb, 1ull << P.mb, Wb, P, ds, st)) != GF2X_OK) return s;
     }
-    if (stop_stage == 3) return GF2X_OK;
-    // iFFT_LCH (passes in reverse order)
-    for (size_t i = P.fft.size(); i-- > 0;) {
+    if (stop_stage == 1) return GF2X_OK;
+    // bottom FFT layers of a and b + pointmul + bottom iFFT layers, fused and bit-sliced
+    {
+        BottomParams bp;
+        bp.A = Wa; bp.B = Wb;
+        bp.ntiles = (P.N * P.batch + (1ull << BT_BITS) - 1) >> BT_BITS;
+        bp.m = P.m; bp.L = P.fft.back().layers;
+        bp.mode = stop_stage == 2 ? 1 : (stop_stage == 3 ? 3 : 7);
+        ProfScope ps("k_bottom", 48.0 * P.N * P.batch, st);
+        k_bottom<<<grid_for(bp.ntiles, 1, smc, 2), BT_THREADS, bottom_smem(), st>>>(bp);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("bottom launch: ") + cudaGetErrorString(e));
+    }
+    if (stop_stage == 2 || stop_stage == 3) return GF2X_OK;
+    // iFFT_LCH top layers (direct passes in reverse order)
+    for (size_t i = ndirect; i-- > 0;) {
         if ((s = launch_fft(P.fft[i], true, false, Wa, P.N, Wa, P, ds, st)) != GF2X_OK) return s;
     }
     if (stop_stage == 4) return GF2X_OK;
