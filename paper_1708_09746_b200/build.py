@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgf2x_b200.so")
 SOURCES = [os.path.join(CSRC, "gf2x.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("gf2x_device.cuh", "field_host.h", "bitslice_gen.cuh")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cuh", ".h"))] + [
     os.path.join(ROOT, "include", "gf2x.h"),
     os.path.join(HERE, "tools", "gen_bitslice.py"),
 ]

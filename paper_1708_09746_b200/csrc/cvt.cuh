@@ -42,13 +42,15 @@ __device__ __forceinline__ void cvt_phase(T* tile, uint32_t nslots, int sw0, int
             tile[t] = xor_t<T>(tile[t], tile[src]);
         }
     } else {
-        const uint32_t n = nslots >> 1;  // lines x tau, y = 0 does nothing
+        // enumerate the slots whose top window bit is 0 with the lowest slot bits fastest, so that
+        // consecutive lanes touch consecutive units (bank-conflict free); y = 0 does nothing
+        const uint32_t n = nslots >> 1;
+        const int tb = sw0 + K;                        // slot bit of the window's top bit
         const uint32_t off = (tau - 1) << sw0;
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-            const uint32_t y = i & (tau - 1);
+            const uint32_t y = (i >> sw0) & (tau - 1);
             if (!y) continue;
-            const uint32_t ln = i >> K;
-            const uint32_t t = (ln & lowm) | ((ln >> sw0) << (sw0 + K + 1)) | (y << sw0);
+            const uint32_t t = (i & ((1u << tb) - 1)) | ((i >> tb) << (tb + 1));
             tile[t] = xor_t<T>(tile[t], tile[t + off]);
         }
     }
