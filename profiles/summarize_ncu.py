@@ -1,0 +1,107 @@
+"""Summarise ncu outputs into profiles/ (tracked).
+
+python profiles/summarize_ncu.py <launches.csv> <full.ncu-rep> <tag> <config>
+writes profiles/<tag>_launches.md, profiles/<tag>_kernels.md and updates profiles/ncu_traffic.json
+(per-kernel-class DRAM bytes per launch, read by bench.py as roofline.traffic).
+"""
+import collections
+import csv
+import io
+import json
+import os
+import re
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def short(name):
+    name = name.replace("unsigned long", "u64").replace("uint4", "u128")
+    m = re.match(r"(?:void )?([A-Za-z0-9_]+)(<[^>]*>)?", name)
+    return (m.group(1) + (m.group(2) or "")) if m else name[:30]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    per = collections.OrderedDict()
+    for r in rows:
+        if "Kernel Name" in r:
+            hdr = r
+            continue
+        if not hdr or len(r) != len(hdr):
+            continue
+        d = dict(zip(hdr, r))
+        key = (d["ID"], short(d["Kernel Name"]))
+        per.setdefault(key, {})[d["Metric Name"]] = (float(d["Metric Value"].replace(",", "")), d["Metric Unit"])
+    return per
+
+
+def to_unit(v, u, target):
+    scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3, "ms": 1e3,
+             "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    return v * scale.get(u, 1.0)
+
+
+def main():
+    lpath, rep, tag, cfg = sys.argv[1:5]
+    per = launches(lpath)
+    cls = collections.OrderedDict()
+    for (i, k), m in per.items():
+        t = to_unit(*m.get("gpu__time_duration.sum", (0, "ns")), "us")
+        rb = to_unit(*m.get("dram__bytes_read.sum", (0, "byte")), "byte")
+        wb = to_unit(*m.get("dram__bytes_write.sum", (0, "byte")), "byte")
+        c = cls.setdefault(k, [0, 0.0, 0.0])
+        c[0] += 1
+        c[1] += t
+        c[2] += rb + wb
+    tot = sum(c[1] for c in cls.values())
+    out = [f"# ncu launch list, {cfg} ({tag}) -- `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+           "dram__bytes_write.sum --clock-control none` over one warm multiply (cold-cache, serialised: compare "
+           "shares, not absolutes)\n", "| kernel | launches | total us | share | DRAM bytes / launch |", "|---|---|---|---|---|"]
+    traffic = {}
+    for k, (n, t, b) in sorted(cls.items(), key=lambda kv: -kv[1][1]):
+        out.append(f"| {k} | {n} | {t:.1f} | {100 * t / tot:.1f} % | {b / n / 1e6:.1f} MB |")
+        traffic[k] = b / n
+    out.append(f"| **total** | {sum(c[0] for c in cls.values())} | {tot:.1f} | 100 % | |")
+    open(os.path.join(HERE, f"{tag}_launches.md"), "w").write("\n".join(out) + "\n")
+    tj = os.path.join(HERE, "ncu_traffic.json")
+    allt = json.load(open(tj)) if os.path.exists(tj) else {}
+    # bench.py kernel names
+    bmap = {"k_fft2<0, 1>": "k_fft<psi>", "k_fft2<0, 0>": "k_fft", "k_fft2<1, 0>": "k_fft<inv>",
+            "k_cvt_tile<u64>": "k_cvt_tile<u64>", "k_cvt_tile<u128>": "k_cvt_tile<u128>",
+            "k_cvt_stream<u64>": "k_cvt_stream<u64>", "k_cvt_stream<u128>": "k_cvt_stream<u128>"}
+    allt[cfg] = {bmap.get(k, k): v for k, v in traffic.items()}
+    json.dump(allt, open(tj, "w"), indent=1)
+    # full capture
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, data = rows[0], rows[2:]
+    keys = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "DRAM read"),
+            ("dram__bytes_write.sum", "DRAM write"), ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM %"),
+            ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+            ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe %"),
+            ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe %"),
+            ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe %"),
+            ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1/smem %"),
+            ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+            ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
+            ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+            ("launch__registers_per_thread", "regs/thread"),
+            ("smsp__inst_executed.sum", "warp instructions")]
+    keys = [(k, n) for k, n in keys if k in hdr]
+    units = dict(zip(hdr, rows[1]))
+    lines = [f"# ncu --set full, {cfg} ({tag})\n", "| kernel | grid x block | " + " | ".join(n for _, n in keys) + " |",
+             "|---|---|" + "---|" * len(keys)]
+    for r in data:
+        d = dict(zip(hdr, r))
+        vals = [f"{d[k]} {units.get(k, '')}".strip() for k, _ in keys]
+        lines.append(f"| {short(d['Kernel Name'])} | {d.get('Grid Size', '')} x {d.get('Block Size', '')} | " + " | ".join(vals) + " |")
+    open(os.path.join(HERE, f"{tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
+    print("\n".join(out))
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
