@@ -25,7 +25,8 @@
 struct BottomParams {
     uint4* A;            // spectrum of a (in: after the direct passes; out: product, after iFFT bottom)
     uint4* B;            // spectrum of b
-    uint64_t ntiles;     // ceil(batch * N / 2^11) (buffers are padded to whole tiles)
+    uint64_t total;      // batch * N elements per operand (A and B may be adjacent: never touch beyond)
+    uint64_t ntiles;     // ceil(total / 2^11)
     int m, L, mode;      // mode bit0: forward layers, bit1: pointmul, bit2: inverse layers
 };
 
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(BT_THREADS, 2) k_bottom(BottomParams p) {
             if (L + b < p.m && ((c_S[k * 32 + L + b] >> j) & 1)) v ^= POS[b];
         Pk[i] = v;
     }
-    const uint64_t total = p.ntiles << BT_BITS;   // padded; the tail of the last tile is zero
+    const uint64_t total = p.total;   // loads beyond it read 0, stores beyond it are dropped
     const int lb = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
         const uint64_t e0 = t << BT_BITS;

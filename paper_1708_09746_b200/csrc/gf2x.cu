@@ -417,21 +417,24 @@ static gf2x_status make_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, Pl
     P.cvt_b = plan_cvt(P.mb, 8);
     P.icvt = plan_cvt(P.m, 16);
     P.fft = plan_fft(P.m);
-    const uint64_t spec = P.N * P.batch + 2048;  // pad for the pointmul tile
+    // workspace: Sa | Sb (u64 blocks) and Wa | Wb (spectra) each contiguous, so that passes with
+    // equal shapes for a and b run as one launch over 2*batch products; a 2^11-element pad after Wb
+    // keeps the bottom kernel's last tile in bounds
     P.off_sa = 0;
-    P.off_sb = align256(P.off_sa + (1ull << P.ma) * P.batch * 8);
+    P.off_sb = P.off_sa + (1ull << P.ma) * P.batch * 8;
     P.off_wa = align256(P.off_sb + (1ull << P.mb) * P.batch * 8);
-    P.off_wb = align256(P.off_wa + spec * 16);
-    P.bytes = align256(P.off_wb + spec * 16);
+    P.off_wb = P.off_wa + P.N * P.batch * 16;
+    P.bytes = align256(P.off_wb + (P.N * P.batch + 2048) * 16);
     if (getenv("GF2X_DEBUG_PLAN")) dump_plan(P);
     return GF2X_OK;
 }
 
 static int launches_of(const Plan& P) {
+    const bool same = P.ma == P.mb;
     int n = 2;  // prep a, b
-    for (auto* v : {&P.cvt_a, &P.cvt_b, &P.icvt}) n += (int)v->size();
+    n += (int)P.cvt_a.size() + (int)P.cvt_b.size() + (int)P.icvt.size();
     const int nd = (int)P.fft.size() - 1;
-    n += 2 * (nd ? nd : 1);      // forward a, b (or the changeRepr-only pass)
+    n += (same ? 1 : 2) * (nd ? nd : 1);      // forward a, b (or the changeRepr-only pass)
     n += 1;                      // fused bottom
     n += nd;                     // inverse
     n += 1;                      // ipsi + combine
@@ -482,17 +485,17 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
 }
 
 static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* src, uint64_t src_per, uint4* dst,
-                              const Plan& P, DeviceState* ds, cudaStream_t st) {
+                              const Plan& P, DeviceState* ds, cudaStream_t st, int operands = 1) {
     FftParams prm;
     prm.src = src; prm.dst = dst; prm.tabs = ds->tabs;
-    prm.src_per = src_per; prm.batch = P.batch;
+    prm.src_per = src_per; prm.batch = P.batch * operands;
     prm.m = P.m; prm.c = f.c; prm.k_lo = f.k_lo; prm.k_hi = f.k_hi;
     const int R = f.k_hi - f.k_lo;
-    const uint64_t ntiles = (P.N >> (f.c + R)) * P.batch;
+    const uint64_t ntiles = (P.N >> (f.c + R)) * prm.batch;
     const size_t sm = fft2_smem(f.c, R, psi);
     const int occ = sm > 113 * 1024 ? 1 : (sm > 75 * 1024 ? 2 : 3);
     const int grid = grid_for(ntiles, 1, ds->sm_count, occ);
-    const double bytes = (double)P.batch * (psi ? (double)src_per * 8 : (double)P.N * 16) + (double)P.batch * P.N * 16;
+    const double bytes = (double)prm.batch * (psi ? (double)src_per * 8 : (double)P.N * 16) + (double)prm.batch * P.N * 16;
     ProfScope ps(inv ? "k_fft<inv>" : (psi ? "k_fft<psi>" : "k_fft"), bytes, st);
     if (inv) k_fft2<true, false><<<grid, FFT_THREADS, sm, st>>>(prm);
     else if (psi) k_fft2<false, true><<<grid, FFT_THREADS, sm, st>>>(prm);
@@ -522,8 +525,10 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         k_prep<<<grid_for((1ull << P.mb) * P.batch, 256, smc, 8), 256, 0, st>>>(b, P.nb, b_bits, P.mb, P.batch, Sb);
     }
     // BasisCvt on 64-bit blocks
+    // (one operand at a time: at the headline sizes each 64-bit block array fits the 126 MB L2 alone)
     if ((s = run_cvt<uint64_t>(P.cvt_a, Sa, P.ma, P.batch, false, smc, st)) != GF2X_OK) return s;
     if ((s = run_cvt<uint64_t>(P.cvt_b, Sb, P.mb, P.batch, false, smc, st)) != GF2X_OK) return s;
+    const bool same = (P.ma == P.mb);   // Sb | Wb directly follow Sa | Wa: one FFT launch for both
     // changeRepr + FFT_LCH top layers (direct passes; the last planned pass is the bottom one)
     const size_t ndirect = P.fft.size() - 1;
     for (size_t i = 0; i < ndirect; i++) {
@@ -533,20 +538,29 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
             if (!first) break;
             f.k_lo = f.k_hi;
         }
-        if ((s = launch_fft(f, false, first, first ? (const void*)Sa : Wa, first ? (1ull << P.ma) : P.N, Wa, P, ds, st)) != GF2X_OK) return s;
-        if ((s = launch_fft(f, false, first, first ? (const void*)Sb : Wb, first ? (1ull << P.mb) : P.N, Wb, P, ds, st)) != GF2X_OK) return s;
+        if (same) {   // Wa|Wb and Sa|Sb are contiguous: 2*batch products in one launch
+            if ((s = launch_fft(f, false, first, first ? (const void*)Sa : Wa, first ? (1ull << P.ma) : P.N, Wa, P, ds, st, 2)) != GF2X_OK) return s;
+        } else {
+            if ((s = launch_fft(f, false, first, first ? (const void*)Sa : Wa, first ? (1ull << P.ma) : P.N, Wa, P, ds, st)) != GF2X_OK) return s;
+            if ((s = launch_fft(f, false, first, first ? (const void*)Sb : Wb, first ? (1ull << P.mb) : P.N, Wb, P, ds, st)) != GF2X_OK) return s;
+        }
     }
     if (ndirect == 0) {  // m <= BOT_B: changeRepr alone (a direct pass with no layers)
         FftPass f{P.m < 5 ? P.m : 5, P.m, P.m, false, 0};
-        if ((s = launch_fft(f, false, true, Sa, 1ull << P.ma, Wa, P, ds, st)) != GF2X_OK) return s;
-        if ((s = launch_fft(f, false, true, Sb, 1ull << P.mb, Wb, P, ds, st)) != GF2X_OK) return s;
+        if (same) {
+            if ((s = launch_fft(f, false, true, Sa, 1ull << P.ma, Wa, P, ds, st, 2)) != GF2X_OK) return s;
+        } else {
+            if ((s = launch_fft(f, false, true, Sa, 1ull << P.ma, Wa, P, ds, st)) != GF2X_OK) return s;
+            if ((s = launch_fft(f, false, true, Sb, 1ull << P.mb, Wb, P, ds, st)) != GF2X_OK) return s;
+        }
     }
     if (stop_stage == 1) return GF2X_OK;
     // bottom FFT layers of a and b + pointmul + bottom iFFT layers, fused and bit-sliced
     {
         BottomParams bp;
         bp.A = Wa; bp.B = Wb;
-        bp.ntiles = (P.N * P.batch + (1ull << BT_BITS) - 1) >> BT_BITS;
+        bp.total = P.N * P.batch;
+        bp.ntiles = (bp.total + (1ull << BT_BITS) - 1) >> BT_BITS;
         bp.m = P.m; bp.L = P.fft.back().layers;
         bp.mode = stop_stage == 2 ? 1 : (stop_stage == 3 ? 3 : 7);
         ProfScope ps("k_bottom", 48.0 * P.N * P.batch, st);
