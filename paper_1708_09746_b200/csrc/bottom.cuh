@@ -22,6 +22,26 @@
 #define BT_STRIDE 33
 #define BT_REGION (4 * BT_GROUPS * BT_STRIDE)   // words per operand region
 
+// pointmul split by output limbs (limb formulas: see c_pm_terms in gf2x.cu).  Per half h, six
+// products {factor limb mask, gets r, gets v31 r, gets v31^2 r}; bit 0 = first limb of the half
+// (R0 / R2), bit 1 = second (R1 / R3).
+//   R0 = P0 + v31 P1 + v31^2 (P2 + P23)        R1 = P0 + P01 + v31 P23 + v31^2 P3
+//   R2 = P0 + Q0 + v31 (P1 + Q1)               R3 = P0 + P01 + Q0 + Q01
+__constant__ int c_pm_half[2][6][4] = {
+    {{0x1, 0x3, 0x0, 0x0},    // P0  -> R0 R1
+     {0x2, 0x0, 0x1, 0x0},    // P1  -> v31: R0
+     {0x4, 0x0, 0x0, 0x1},    // P2  -> v31^2: R0
+     {0xC, 0x0, 0x2, 0x1},    // P23 -> v31: R1, v31^2: R0
+     {0x3, 0x2, 0x0, 0x0},    // P01 -> R1
+     {0x8, 0x0, 0x0, 0x2}},   // P3  -> v31^2: R1
+    {{0x1, 0x3, 0x0, 0x0},    // P0  -> R2 R3
+     {0x5, 0x3, 0x0, 0x0},    // Q0  -> R2 R3
+     {0x2, 0x0, 0x1, 0x0},    // P1  -> v31: R2
+     {0xA, 0x0, 0x1, 0x0},    // Q1  -> v31: R2
+     {0x3, 0x2, 0x0, 0x0},    // P01 -> R3
+     {0xF, 0x2, 0x0, 0x0}},   // Q01 -> R3
+};
+
 struct BottomParams {
     uint4* A;            // spectrum of a (in: after the direct passes; out: product, after iFFT bottom)
     uint4* B;            // spectrum of b
@@ -124,8 +144,7 @@ __global__ void __launch_bounds__(BT_THREADS, 2) k_bottom(BottomParams p) {
     extern __shared__ __align__(1024) uint32_t bt_smem[];
     uint32_t* PA = bt_smem;                 // planes of A
     uint32_t* PB = PA + BT_REGION;          // planes of B
-    uint32_t* PC = PB + BT_REGION;          // product accumulators
-    uint32_t* Pk = PC + BT_REGION;          // per-layer position planes, L x 32
+    uint32_t* Pk = PB + BT_REGION;          // per-layer position planes, L x 32
     const int L = p.L;
     // P_k[j] = xor over position bits i (L+i < m) of bit j of s_k(v_(L+i)) * POS_i
     for (int i = threadIdx.x; i < L * 32; i += blockDim.x) {
@@ -156,24 +175,40 @@ __global__ void __launch_bounds__(BT_THREADS, 2) k_bottom(BottomParams p) {
         }
         uint32_t* R = PA;
         if (p.mode & 2) {
-            // zero accumulators, then the nine limb products (threads 0..63: one group each)
-            for (int i = threadIdx.x; i < BT_REGION; i += blockDim.x) PC[i] = 0;
-            __syncthreads();
-            if (threadIdx.x < BT_GROUPS) {
-                const int g = threadIdx.x;
+            // two threads per group: thread h = 0 produces result limbs R0, R1, h = 1 produces R2, R3
+            // (six TGF(2^32) products each, accumulated in registers), then both overwrite the A planes
+            const int g = threadIdx.x & (BT_GROUPS - 1), h = threadIdx.x >> 6;
+            uint32_t acc0[32], acc1[32];
+#pragma unroll
+            for (int j = 0; j < 32; j++) { acc0[j] = 0; acc1[j] = 0; }
 #pragma unroll 1
-                for (int qq = 0; qq < 9; qq++) {
-                    uint32_t x[32], y[32], r[32];
-                    bt_load_sum(PA, g, c_pm_terms[qq][0], x);
-                    bt_load_sum(PB, g, c_pm_terms[qq][0], y);
-                    bs_mul32(x, y, r);
-                    bt_acc_add(PC, g, c_pm_terms[qq][1], r);
-                    if (c_pm_terms[qq][2]) { bs_mul_v31(r, x); bt_acc_add(PC, g, c_pm_terms[qq][2], x); }
-                    if (c_pm_terms[qq][3]) { bs_mul_v31sq(r, y); bt_acc_add(PC, g, c_pm_terms[qq][3], y); }
+            for (int qq = 0; qq < 6; qq++) {
+                const int* T = c_pm_half[h][qq];
+                uint32_t x[32], y[32], r[32];
+                bt_load_sum(PA, g, T[0], x);
+                bt_load_sum(PB, g, T[0], y);
+                bs_mul32(x, y, r);
+                // T[1..3]: which of the two output limbs get r, v31 r, v31^2 r (bit 0: first, bit 1: second)
+                if (T[2]) bs_mul_v31(r, x);
+                if (T[3]) bs_mul_v31sq(r, y);
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    uint32_t a0 = acc0[j], a1 = acc1[j];
+                    if (T[1] & 1) a0 ^= r[j];
+                    if (T[1] & 2) a1 ^= r[j];
+                    if (T[2] & 1) a0 ^= x[j];
+                    if (T[2] & 2) a1 ^= x[j];
+                    if (T[3] & 1) a0 ^= y[j];
+                    if (T[3] & 2) a1 ^= y[j];
+                    acc0[j] = a0; acc1[j] = a1;
                 }
             }
+            __syncthreads();   // every thread is done reading A and B
+            uint32_t* d0 = PA + bt_block(g, 2 * h);
+            uint32_t* d1 = PA + bt_block(g, 2 * h + 1);
+#pragma unroll
+            for (int j = 0; j < 32; j++) { d0[j] = acc0[j]; d1[j] = acc1[j]; }
             __syncthreads();
-            R = PC;
         }
         if (p.mode & 4) {
             for (int k = 0; k < L; k++) {   // iFFT_LCH bottom layers, bottom-up
@@ -189,4 +224,4 @@ __global__ void __launch_bounds__(BT_THREADS, 2) k_bottom(BottomParams p) {
     }
 }
 
-static size_t bottom_smem() { return (size_t)(3 * BT_REGION + 6 * 32) * 4; }
+static size_t bottom_smem() { return (size_t)(2 * BT_REGION + 6 * 32) * 4; }
