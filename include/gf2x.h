@@ -70,6 +70,35 @@ int gf2x_launch_count(uint64_t a_bits, uint64_t b_bits, int64_t batch);
 gf2x_status gf2x_debug_stage(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits,
                              int stage, uint64_t* out, void* stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * Multi-GPU: the FFT partitioned across G = nranks ranks, one process per GPU (the
+ * decomposition is described in DESIGN.md §9).  NCCL is loaded at run time (libnccl.so.2).
+ *
+ * gf2x_comm_unique_id: on one rank, write the 128-byte NCCL unique id into id_out; the caller
+ *   distributes it (e.g. torch.distributed broadcast) and every rank calls gf2x_comm_init with it
+ *   on its own device (collective; blocks until all ranks joined).
+ * gf2x_mul_sharded: a_bits = b_bits = bits, n = ceil(bits/64) must be a power of two and
+ *   log2(2n) - log2(G) >= max(16, 12).  Rank r passes words [r n/G, (r+1) n/G) of a and b
+ *   (DEVICE, caller-owned) and receives words [r 2n/G, (r+1) 2n/G) of c.  Enqueued on `stream`
+ *   (collectives included); returns after enqueue.  EINVAL on unsupported sizes, ENCCL on NCCL
+ *   errors.  The communicator owns a workspace, freed by gf2x_comm_destroy.
+ * gf2x_mul_sharded_sim: the same algorithm with `nranks` virtual ranks in one process on the
+ *   current device (data movement between ranks = device copies); a, b full operands, c the full
+ *   2n-word product (DEVICE).  Used to check the decomposition bit-exactly on one GPU.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct gf2x_comm_s* gf2x_comm_t;
+gf2x_status gf2x_comm_unique_id(void* id_out);
+gf2x_status gf2x_comm_init(const void* nccl_unique_id, int nranks, int rank, gf2x_comm_t* out);
+gf2x_status gf2x_comm_destroy(gf2x_comm_t comm);
+gf2x_status gf2x_mul_sharded(const uint64_t* a_shard, const uint64_t* b_shard, uint64_t bits,
+                             uint64_t* c_shard, gf2x_comm_t comm, void* stream);
+gf2x_status gf2x_mul_sharded_sim(const uint64_t* a, const uint64_t* b, uint64_t bits, uint64_t* c,
+                                 int nranks, void* stream);
+/* Debug / parity hook of the simulation: the concatenated rank blocks (N tower elements, N*2 words,
+ * DEVICE) after stage 1 (forward FFT_LCH: evaluations in natural point order) or 5 (iBasisCvt). */
+gf2x_status gf2x_debug_shard_stage(const uint64_t* a, const uint64_t* b, uint64_t bits, int nranks, int stage,
+                                   uint64_t* out, void* stream);
+
 /* Measurement hook (bench.py): while enabled, every kernel the library enqueues from the calling
  * thread is bracketed by CUDA events on its stream.  gf2x_profile_report synchronises those events
  * and writes a JSON array into buf (cap bytes, NUL-terminated):

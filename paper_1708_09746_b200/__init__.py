@@ -21,7 +21,8 @@ STATUS = {0: "GF2X_OK", 1: "GF2X_EINVAL", 2: "GF2X_ETOOBIG", 3: "GF2X_ENOMEM", 4
 # every symbol include/gf2x.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "gf2x_mul", "gf2x_mul_batched", "gf2x_workspace_bytes", "gf2x_mul_ws", "gf2x_launch_count",
-    "gf2x_debug_stage", "gf2x_profile_enable", "gf2x_profile_report", "gf2x_status_string", "gf2x_last_error",
+    "gf2x_debug_stage", "gf2x_comm_unique_id", "gf2x_comm_init", "gf2x_comm_destroy", "gf2x_mul_sharded",
+    "gf2x_mul_sharded_sim", "gf2x_debug_shard_stage", "gf2x_profile_enable", "gf2x_profile_report", "gf2x_status_string", "gf2x_last_error",
     "gf2x_release", "gf2x_version",
 ]
 
@@ -54,6 +55,15 @@ def load(path: str = LIB_PATH):
     L.gf2x_last_error.restype = ctypes.c_char_p
     L.gf2x_release.argtypes = [i32]
     L.gf2x_version.restype = ctypes.c_char_p
+    L.gf2x_comm_unique_id.argtypes = [vp]
+    L.gf2x_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
+    L.gf2x_comm_destroy.argtypes = [vp]
+    L.gf2x_mul_sharded.argtypes = [vp, vp, u64, vp, vp, vp]
+    L.gf2x_mul_sharded_sim.argtypes = [vp, vp, u64, vp, i32, vp]
+    L.gf2x_debug_shard_stage.argtypes = [vp, vp, u64, i32, i32, vp, vp]
+    for name in ("gf2x_comm_unique_id", "gf2x_comm_init", "gf2x_comm_destroy", "gf2x_mul_sharded", "gf2x_mul_sharded_sim",
+                 "gf2x_debug_shard_stage"):
+        getattr(L, name).restype = i32
     L.gf2x_profile_enable.argtypes = [i32]
     L.gf2x_profile_enable.restype = i32
     L.gf2x_profile_report.argtypes = [ctypes.c_char_p, sz]
@@ -129,6 +139,87 @@ def gf2x_debug_stage(a, a_bits: int, b, b_bits: int, stage: int, stream=None):
     out = torch.empty(N, 2, dtype=torch.uint64, device=a.device)
     _check(load().gf2x_debug_stage(_ptr(a), a_bits, _ptr(b), b_bits, stage, _ptr(out), _stream_ptr(stream)))
     return out
+
+
+def gf2x_mul_sharded_sim(a, b, bits: int, nranks: int, c=None, stream=None):
+    """The multi-GPU algorithm with `nranks` virtual ranks on this device (full a, b in; full c out)."""
+    import torch
+    if c is None:
+        c = torch.empty(2 * nwords(bits), dtype=torch.uint64, device=a.device)
+    _check(load().gf2x_mul_sharded_sim(_ptr(a), _ptr(b), bits, _ptr(c), nranks, _stream_ptr(stream)))
+    return c
+
+
+def gf2x_debug_shard_stage(a, b, bits: int, nranks: int, stage: int, stream=None):
+    import torch
+    N = 2 * nwords(bits)
+    out = torch.empty(N, 2, dtype=torch.uint64, device=a.device)
+    _check(load().gf2x_debug_shard_stage(_ptr(a), _ptr(b), bits, nranks, stage, _ptr(out), _stream_ptr(stream)))
+    return out
+
+
+class Comm:
+    """NCCL communicator of the library (one rank per process/GPU).
+
+    The 128-byte unique id is created by rank 0 (`unique_id()`) and must reach every rank before
+    `Comm(uid, nranks, rank)`; `init_from_process_group` does that with a torch.distributed broadcast.
+    """
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        assert len(uid) == 128
+        self.nranks, self.rank = nranks, rank
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(uid, 128)
+        _check(load().gf2x_comm_init(buf, nranks, rank, ctypes.byref(h)))
+        self.handle = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(load().gf2x_comm_unique_id(buf))
+        return buf.raw
+
+    def mul(self, a_shard, b_shard, bits: int, c_shard=None, stream=None):
+        """Sharded product: this rank's words of a and b in, its 2n/G words of c out."""
+        import torch
+        if c_shard is None:
+            c_shard = torch.empty(2 * nwords(bits) // self.nranks, dtype=torch.uint64, device=a_shard.device)
+        _check(load().gf2x_mul_sharded(_ptr(a_shard), _ptr(b_shard), bits, _ptr(c_shard), self.handle,
+                                       _stream_ptr(stream)))
+        return c_shard
+
+    def close(self):
+        if self.handle:
+            _check(load().gf2x_comm_destroy(self.handle))
+            self.handle = None
+
+
+def broadcast_unique_id(uid_fn, rank: int, group=None) -> bytes:
+    """Rank 0 calls uid_fn() (128 bytes); every rank returns the same bytes via torch.distributed."""
+    import torch
+    import torch.distributed as dist
+    t = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        t[:] = torch.frombuffer(bytearray(uid_fn()), dtype=torch.uint8)
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        t = t.cuda()
+    dist.broadcast(t, src=0, group=group)
+    return bytes(t.cpu().tolist())
+
+
+def init_from_process_group(group=None) -> Comm:
+    import torch.distributed as dist
+    rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+    uid = broadcast_unique_id(Comm.unique_id, rank, group)
+    return Comm(uid, nranks, rank)
+
+
+def shard_words(total_words: int, nranks: int, rank: int):
+    """[lo, hi) word range of rank `rank` for an operand of total_words (block distribution)."""
+    assert total_words % nranks == 0
+    per = total_words // nranks
+    return rank * per, (rank + 1) * per
 
 
 def gf2x_release(device: int = 0):

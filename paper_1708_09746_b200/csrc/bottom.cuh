@@ -48,6 +48,8 @@ struct BottomParams {
     uint64_t total;      // batch * N elements per operand (A and B may be adjacent: never touch beyond)
     uint64_t ntiles;     // ceil(total / 2^11)
     int m, L, mode;      // mode bit0: forward layers, bit1: pointmul, bit2: inverse layers
+    IdxMap map;          // local -> global index for the multipliers (identity unless sharded;
+                         // the bottom layers and position bits are always below map.pos)
 };
 
 __device__ __forceinline__ uint32_t bt_block(int g, int lb) { return (uint32_t)((lb * BT_GROUPS + g) * BT_STRIDE); }
@@ -90,14 +92,15 @@ __device__ __forceinline__ void bt_store_block(uint4* __restrict__ dst, uint64_t
 
 // one layer k of butterflies on a plane region: warp = limb, lane = pair index
 template <bool INV>
-__device__ __forceinline__ void bt_layer(uint32_t* planes, int k, const uint32_t* Pk, uint64_t e0, int L, int m) {
+__device__ __forceinline__ void bt_layer(uint32_t* planes, int k, const uint32_t* Pk, uint64_t e0, int L, int m,
+                                         const IdxMap& map) {
     const int lb = threadIdx.x >> 5, q = threadIdx.x & 31;
     const int g0 = (q & ((1 << k) - 1)) | ((q >> k) << (k + 1));
     const int g1 = g0 | (1 << k);
     // U_k(g0): within-pair index of the group's block base with the position bits cleared
     const uint64_t N = 1ull << m;
     const uint64_t gi = (e0 + bt_elem(g0, 0, L)) & (N - 1);
-    const uint32_t U = layer_const(k, (uint32_t)gi);
+    const uint32_t U = layer_const(k, gidx(map, (uint32_t)gi));
     uint32_t c[32], x1[32], pr[32];
 #pragma unroll
     for (int j = 0; j < 32; j++) c[j] = Pk[j] ^ (((U >> j) & 1) ? 0xFFFFFFFFu : 0u);
@@ -168,8 +171,8 @@ __global__ void __launch_bounds__(BT_THREADS, 2) k_bottom(BottomParams p) {
         __syncthreads();
         if (p.mode & 1) {
             for (int k = L - 1; k >= 0; k--) {   // FFT_LCH bottom layers, top-down
-                bt_layer<false>(PA, k, Pk + k * 32, e0, L, p.m);
-                bt_layer<false>(PB, k, Pk + k * 32, e0, L, p.m);
+                bt_layer<false>(PA, k, Pk + k * 32, e0, L, p.m, p.map);
+                bt_layer<false>(PB, k, Pk + k * 32, e0, L, p.m, p.map);
                 __syncthreads();
             }
         }
@@ -212,7 +215,7 @@ __global__ void __launch_bounds__(BT_THREADS, 2) k_bottom(BottomParams p) {
         }
         if (p.mode & 4) {
             for (int k = 0; k < L; k++) {   // iFFT_LCH bottom layers, bottom-up
-                bt_layer<true>(R, k, Pk + k * 32, e0, L, p.m);
+                bt_layer<true>(R, k, Pk + k * 32, e0, L, p.m, p.map);
                 __syncthreads();
             }
         }

@@ -66,8 +66,9 @@ struct FftParams {
     const DevTables* tabs;
     uint64_t src_per;
     uint64_t batch;
-    int m;                // N = 2^m points per product
+    int m;                // N = 2^m points per product (local points for a shard)
     int c, k_lo, k_hi;    // tile bits [0,c) U [k_lo,k_hi)
+    IdxMap map;           // local -> global index for the multipliers (identity unless sharded)
 };
 
 __device__ __forceinline__ uint32_t tab_addr(uint32_t base, uint32_t id) { return base + id * 512u; }
@@ -152,7 +153,8 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft2(FftParams p) {
             const int lg = 31 - __clz(id + 1);          // = R-1-kk
             const int k = p.k_lo + R - 1 - lg;
             const uint32_t blk = id + 1 - (1u << lg);
-            const uint32_t cst = layer_const(k, (uint32_t)(((uint64_t)base & ~((2ull << k) - 1)) | ((uint64_t)blk << (k + 1))));
+            const uint32_t lb = (uint32_t)(((uint64_t)base & ~((2ull << k) - 1)) | ((uint64_t)blk << (k + 1)));
+            const uint32_t cst = layer_const(glayer(p.map, k), gidx(p.map, lb));
             build_tab_row(tabs + id * 128, cst, (int)(i & 7), p.tabs->wt);
         }
         // ---- load

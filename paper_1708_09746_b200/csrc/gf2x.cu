@@ -60,6 +60,22 @@ __device__ __forceinline__ uint32_t layer_const(int k, uint32_t b) {
 }
 
 // =============================================================================================
+// Index map from a local element index to the global index that fixes the FFT multipliers (used by
+// the sharded multiply, where a rank holds a block or a "t-sliced" part of the index space):
+//   global = (li & (2^pos - 1)) | (val << pos) | ((li >> pos) << (pos + bits)),
+// and a local layer lk maps to global layer lk (+ bits if lk >= pos).  Identity when bits = 0.
+// =============================================================================================
+struct IdxMap {
+    int pos, bits;
+    uint32_t val;
+};
+__device__ __forceinline__ uint32_t gidx(const IdxMap& M, uint32_t li) {
+    if (!M.bits) return li;
+    return (li & ((1u << M.pos) - 1)) | (M.val << M.pos) | ((li >> M.pos) << (M.pos + M.bits));
+}
+__device__ __forceinline__ int glayer(const IdxMap& M, int lk) { return lk >= M.pos ? lk + M.bits : lk; }
+
+// =============================================================================================
 // k_prep: Split.  Operand pair p occupies words [p*n, (p+1)*n) of `in`; it is copied to
 // S[p * 2^ms ...], masked to `bits`, zero-padded to 2^ms words.
 // =============================================================================================
@@ -124,8 +140,10 @@ __device__ __forceinline__ void ipsi_apply(const uint4* __restrict__ tab, uint4 
     hi = ((uint64_t)acc.w << 32) | acc.z;
 }
 
+// halo (sharded multiply): the tower element that precedes P[0] globally (rank r-1's last one), or null
 __global__ void __launch_bounds__(256) k_ipsi_combine(const uint4* __restrict__ P, const DevTables* tabs, uint64_t N,
-                                                      uint64_t n_out, uint64_t batch, uint64_t* __restrict__ out) {
+                                                      uint64_t n_out, uint64_t batch, uint64_t* __restrict__ out,
+                                                      const uint4* __restrict__ halo) {
     extern __shared__ __align__(16) uint4 itab[];
     for (int i = threadIdx.x; i < 16 * 256; i += blockDim.x) itab[i] = tabs->ipsi[i];
     __syncthreads();
@@ -142,10 +160,9 @@ __global__ void __launch_bounds__(256) k_ipsi_combine(const uint4* __restrict__ 
         if (in) {
             if (lane == 0 || w == 0) {
                 prev_hi = 0;
-                if (w >= 1 && w - 1 < N) {
-                    uint64_t l2;
-                    ipsi_apply(itab, P[pair * N + w - 1], l2, prev_hi);
-                }
+                uint64_t l2;
+                if (w >= 1 && w - 1 < N) ipsi_apply(itab, P[pair * N + w - 1], l2, prev_hi);
+                else if (w == 0 && halo) ipsi_apply(itab, *halo, l2, prev_hi);
             }
             out[i] = lo ^ prev_hi;
         }
@@ -212,6 +229,9 @@ static gf2x_status fail(gf2x_status s, const std::string& msg) {
 
 struct DeviceState {
     DevTables* tabs = nullptr;
+    DevTables* host = nullptr;   // host copy (multiplier images for host-side constants)
+    void* shard_ws = nullptr;    // simulation workspace (gf2x_mul_sharded_sim)
+    size_t shard_ws_bytes = 0;
     int sm_count = 0;
     std::map<cudaStream_t, std::pair<void*, size_t>> ws;  // per-stream workspace cache
 };
@@ -267,8 +287,8 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
         if (e != cudaSuccess) { delete h; return fail(GF2X_ENOMEM, "table allocation failed"); }
         e = cudaMemcpy(d, h, sizeof(DevTables), cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_S, h->S, sizeof(h->S));
-        delete h;
-        if (e != cudaSuccess) { cudaFree(d); return fail(GF2X_ECUDA, cudaGetErrorString(e)); }
+        if (e != cudaSuccess) { delete h; cudaFree(d); return fail(GF2X_ECUDA, cudaGetErrorString(e)); }
+        st.host = h;
         CUDA_TRY(cudaDeviceGetAttribute(&st.sm_count, cudaDevAttrMultiProcessorCount, dev));
         // opt-in shared memory sizes
         CUDA_TRY(cudaFuncSetAttribute(k_fft2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -314,9 +334,14 @@ struct CvtPass {
 // Greedy grouping of consecutive ops into tile passes: a pass holds tile bits [0,T) (contiguous)
 // or [0,cmin) U [r_lo, r_lo + T - cmin) (rows of 2^cmin contiguous units = one 32-byte sector);
 // an op whose window is wider than a tile streams through HBM.
+static std::vector<CvtPass> plan_cvt_ops(const std::vector<CvtOp>& ops, int m, int unit_bytes);
 static std::vector<CvtPass> plan_cvt(int m, int unit_bytes) {
     std::vector<CvtOp> ops;
     cvt_ops(m, 0, ops);
+    return plan_cvt_ops(ops, m, unit_bytes);
+}
+// ops: in forward execution order, windows inside [0, m)
+static std::vector<CvtPass> plan_cvt_ops(const std::vector<CvtOp>& ops, int m, int unit_bytes) {
     const int T = std::min(m, unit_bytes == 8 ? 14 : 13);  // 128 KB tiles
     const int cmin = unit_bytes == 8 ? 2 : 1;
     const int Rrow = T - cmin;
@@ -485,8 +510,9 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
 }
 
 static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* src, uint64_t src_per, uint4* dst,
-                              const Plan& P, DeviceState* ds, cudaStream_t st, int operands = 1) {
+                              const Plan& P, DeviceState* ds, cudaStream_t st, int operands = 1, IdxMap map = {0, 0, 0}) {
     FftParams prm;
+    prm.map = map;
     prm.src = src; prm.dst = dst; prm.tabs = ds->tabs;
     prm.src_per = src_per; prm.batch = P.batch * operands;
     prm.m = P.m; prm.c = f.c; prm.k_lo = f.k_lo; prm.k_hi = f.k_hi;
@@ -562,6 +588,7 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         bp.total = P.N * P.batch;
         bp.ntiles = (bp.total + (1ull << BT_BITS) - 1) >> BT_BITS;
         bp.m = P.m; bp.L = P.fft.back().layers;
+        bp.map = IdxMap{0, 0, 0};
         bp.mode = stop_stage == 2 ? 1 : (stop_stage == 3 ? 3 : 7);
         ProfScope ps("k_bottom", 48.0 * P.N * P.batch, st);
         k_bottom<<<grid_for(bp.ntiles, 1, smc, 2), BT_THREADS, bottom_smem(), st>>>(bp);
@@ -582,7 +609,7 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         const uint64_t n_out = P.na + P.nb;
         const uint64_t total = n_out * P.batch;
         ProfScope ps("k_ipsi_combine", 16.0 * P.N * P.batch + 8.0 * total, st);
-        k_ipsi_combine<<<grid_for(total, 256, smc, 2), 256, 16 * 256 * 16, st>>>(Wa, ds->tabs, P.N, n_out, P.batch, c);
+        k_ipsi_combine<<<grid_for(total, 256, smc, 2), 256, 16 * 256 * 16, st>>>(Wa, ds->tabs, P.N, n_out, P.batch, c, nullptr);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("combine launch: ") + cudaGetErrorString(e));
     }
@@ -647,6 +674,8 @@ static gf2x_status mul_common(const uint64_t* a, uint64_t a_bits, const uint64_t
     return GF2X_OK;
 }
 
+#include "shard.cuh"
+
 extern "C" {
 
 gf2x_status gf2x_mul(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c, void* stream) {
@@ -682,6 +711,118 @@ gf2x_status gf2x_debug_stage(const uint64_t* a, uint64_t a_bits, const uint64_t*
                              uint64_t* out, void* stream) {
     if (stage < 1 || stage > 5 || !out || a_bits == 0 || b_bits == 0) return fail(GF2X_EINVAL, "bad debug stage request");
     return mul_common(a, a_bits, b, b_bits, nullptr, 1, nullptr, 0, stream, stage, out);
+}
+
+gf2x_status gf2x_comm_unique_id(void* id_out) {
+    if (!id_out) return fail(GF2X_EINVAL, "null id buffer");
+    std::string err = nccl_load();
+    if (!err.empty()) return fail(GF2X_ENCCL, err);
+    nccl_uid_t id;
+    int rc = g_nccl.GetUniqueId(&id);
+    if (rc) return fail(GF2X_ENCCL, std::string("ncclGetUniqueId: ") + g_nccl.GetErrorString(rc));
+    memcpy(id_out, &id, sizeof(id));
+    return GF2X_OK;
+}
+
+gf2x_status gf2x_comm_init(const void* nccl_unique_id, int nranks, int rank, gf2x_comm_t* out) {
+    if (!nccl_unique_id || !out || nranks < 1 || rank < 0 || rank >= nranks) return fail(GF2X_EINVAL, "bad comm arguments");
+    std::string err = nccl_load();
+    if (!err.empty()) return fail(GF2X_ENCCL, err);
+    nccl_uid_t id;
+    memcpy(&id, nccl_unique_id, sizeof(id));
+    gf2x_comm_s* c = new gf2x_comm_s();
+    c->nranks = nranks;
+    c->rank = rank;
+    c->ws = nullptr;
+    c->ws_bytes = 0;
+    cudaGetDevice(&c->device);
+    int rc = g_nccl.CommInitRank(&c->comm, nranks, id, rank);
+    if (rc) {
+        delete c;
+        return fail(GF2X_ENCCL, std::string("ncclCommInitRank: ") + g_nccl.GetErrorString(rc));
+    }
+    *out = c;
+    return GF2X_OK;
+}
+
+gf2x_status gf2x_comm_destroy(gf2x_comm_t comm) {
+    if (!comm) return GF2X_OK;
+    if (comm->ws) { cudaDeviceSynchronize(); cudaFree(comm->ws); }
+    int rc = g_nccl.h ? g_nccl.CommDestroy(comm->comm) : 0;
+    delete comm;
+    if (rc) return fail(GF2X_ENCCL, std::string("ncclCommDestroy: ") + g_nccl.GetErrorString(rc));
+    return GF2X_OK;
+}
+
+static void rank_bufs(RankCtx& R, unsigned char* base, const ShardGeom& S) {
+    for (int b = 0; b < SB_COUNT; b++) R.buf[b] = base + S.off[b];
+}
+
+gf2x_status gf2x_mul_sharded(const uint64_t* a_shard, const uint64_t* b_shard, uint64_t bits, uint64_t* c_shard,
+                             gf2x_comm_t comm, void* stream) {
+    if (!comm || !a_shard || !b_shard || !c_shard) return fail(GF2X_EINVAL, "null argument");
+    int dev;
+    DeviceState* ds;
+    gf2x_status s = get_device(&dev, &ds);
+    if (s != GF2X_OK) return s;
+    ShardGeom S;
+    if ((s = shard_geom(bits, comm->nranks, S)) != GF2X_OK) return s;
+    if (comm->ws_bytes < S.bytes) {
+        if (comm->ws) { cudaDeviceSynchronize(); cudaFree(comm->ws); comm->ws = nullptr; comm->ws_bytes = 0; }
+        cudaError_t e = cudaMalloc(&comm->ws, S.bytes);
+        if (e != cudaSuccess) return fail(GF2X_ENOMEM, std::string("shard workspace: ") + cudaGetErrorString(e));
+        comm->ws_bytes = S.bytes;
+    }
+    std::vector<RankCtx> ranks(1);
+    ranks[0].r = comm->rank;
+    ranks[0].a_shard = a_shard;
+    ranks[0].b_shard = b_shard;
+    ranks[0].c_shard = c_shard;
+    rank_bufs(ranks[0], (unsigned char*)comm->ws, S);
+    ShardExec X{false, comm, reinterpret_cast<cudaStream_t>(stream), &ranks};
+    return run_sharded(S, X, ds, ds->host, bits);
+}
+
+static gf2x_status sharded_sim(const uint64_t* a, const uint64_t* b, uint64_t bits, uint64_t* c, int nranks, void* stream,
+                               int debug_stage, uint64_t* dbg) {
+    if (!a || !b || (!c && !debug_stage)) return fail(GF2X_EINVAL, "null argument");
+    int dev;
+    DeviceState* ds;
+    gf2x_status s = get_device(&dev, &ds);
+    if (s != GF2X_OK) return s;
+    ShardGeom S;
+    if ((s = shard_geom(bits, nranks, S)) != GF2X_OK) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t need = S.bytes * (size_t)nranks;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (ds->shard_ws_bytes < need) {
+            if (ds->shard_ws) { cudaDeviceSynchronize(); cudaFree(ds->shard_ws); ds->shard_ws = nullptr; ds->shard_ws_bytes = 0; }
+            cudaError_t e = cudaMalloc(&ds->shard_ws, need);
+            if (e != cudaSuccess) return fail(GF2X_ENOMEM, std::string("shard sim workspace: ") + cudaGetErrorString(e));
+            ds->shard_ws_bytes = need;
+        }
+    }
+    std::vector<RankCtx> ranks(nranks);
+    for (int r = 0; r < nranks; r++) {
+        ranks[r].r = r;
+        ranks[r].a_shard = a + r * (S.n / nranks);
+        ranks[r].b_shard = b + r * (S.n / nranks);
+        ranks[r].c_shard = c ? c + r * S.Nloc : nullptr;
+        rank_bufs(ranks[r], (unsigned char*)ds->shard_ws + r * S.bytes, S);
+    }
+    ShardExec X{true, nullptr, st, &ranks};
+    return run_sharded(S, X, ds, ds->host, bits, debug_stage, (uint4*)dbg);
+}
+
+gf2x_status gf2x_mul_sharded_sim(const uint64_t* a, const uint64_t* b, uint64_t bits, uint64_t* c, int nranks, void* stream) {
+    return sharded_sim(a, b, bits, c, nranks, stream, 0, nullptr);
+}
+
+gf2x_status gf2x_debug_shard_stage(const uint64_t* a, const uint64_t* b, uint64_t bits, int nranks, int stage, uint64_t* out,
+                                   void* stream) {
+    if ((stage != 1 && stage != 5) || !out) return fail(GF2X_EINVAL, "bad shard debug stage");
+    return sharded_sim(a, b, bits, nullptr, nranks, stream, stage, out);
 }
 
 gf2x_status gf2x_profile_enable(int on) {
@@ -750,6 +891,8 @@ gf2x_status gf2x_release(int device) {
     for (auto& kv : it->second.ws)
         if (kv.second.first) cudaFree(kv.second.first);
     if (it->second.tabs) cudaFree(it->second.tabs);
+    if (it->second.shard_ws) cudaFree(it->second.shard_ws);
+    delete it->second.host;
     g_dev.erase(it);
     cudaSetDevice(cur);
     return GF2X_OK;

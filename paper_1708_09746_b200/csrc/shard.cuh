@@ -1,0 +1,427 @@
+// shard.cuh -- the FFT partitioned across G ranks, included by gf2x.cu.
+//
+// G = 2^g ranks, operands of n = 2^p words (N = 2n points, m = p + 1), rank r owns the points
+// [r N/G, (r+1) N/G) (index bits [m-g, m) = r, "blocked"), Nloc = N/G, mloc = m - g.
+//
+// Forward.  Every rank gathers both operands and converts them (BasisCvt, redundant).  With
+// g(X) = sum_j X_(j Nloc)(x) G_j(X) (G_j = block j of the novel-basis coefficients, j < G/2 are the
+// nonzero ones) and X_(j Nloc)(alpha_r + u) = X_(j Nloc)(alpha_r) for u in V_mloc (the factors
+// s_i, i >= mloc, vanish on V_mloc and are GF(2)-linear), the evaluations at alpha_r + V_mloc are
+// those of h_r = sum_j c_(r,j) G_j with c_(r,j) = X_(j Nloc)(phi(r Nloc)) = prod_(bit i of j)
+// s_(mloc+i)(phi(r Nloc)) -- small-subfield constants.  So rank r forms h_r (k_shard_top, changeRepr
+// included) and runs the top g FFT layers' worth of work as that combination; the remaining layers,
+// pointmul and the bottom iFFT layers are local (multipliers from global indices via IdxMap).
+//
+// Inverse.  The local iFFT gives the product's h_r.  The inner iBasisCvt (index windows inside
+// [0,K), K = 16) commutes with iFFT layers >= K (they act on higher bits with multipliers that do not
+// depend on the window bits), so it runs locally first.  An all-to-all moves to the "t-sliced"
+// layout (rank = index bits [K-g, K)), where the top g iFFT layers and the outer iBasisCvt (windows in
+// [K, m)) are local; another all-to-all returns to blocked, where the top Taylor steps of level
+// l <= mloc are local and the g steps with l > mloc exchange half a block pairwise.  changeRepr^-1 +
+// InterleavedCombine need one tower element from rank r-1.
+//
+// Data movement is a list of transfers (src rank/buffer/offset -> dst rank/buffer/offset) that every
+// rank derives identically; it runs as NCCL grouped send/recv (one process per GPU) or, in the
+// single-process simulation with G virtual ranks on one device, as device-to-device copies.
+#pragma once
+#include <dlfcn.h>
+
+// ---------------------------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------------------------
+#define SHARD_MAXJ 128
+
+struct ShardTopParams {
+    const uint64_t* S;   // converted operand, n = (G/2) Nloc words
+    uint4* W;            // out: h_r, Nloc tower elements
+    const DevTables* tabs;
+    uint64_t Nloc;
+    int J;               // G/2 blocks
+    uint32_t coef[SHARD_MAXJ];
+};
+
+// W[i] = sum_j coef_j * psi(S[j Nloc + i])   (coef_j < 2^32: M4R-4 tables, psi: M4R-8 table)
+__global__ void __launch_bounds__(256) k_shard_top(ShardTopParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint32_t* tabs = reinterpret_cast<uint32_t*>(smem_raw);
+    uint4* psit = reinterpret_cast<uint4*>(tabs + p.J * 128);
+    for (int i = threadIdx.x; i < p.J * 8; i += blockDim.x) build_tab_row(tabs + (i >> 3) * 128, p.coef[i >> 3], i & 7, p.tabs->wt);
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) psit[i] = p.tabs->psi64[i];
+    __syncthreads();
+    const uint32_t tabs_sa = (uint32_t)__cvta_generic_to_shared(tabs);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.Nloc; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint4 acc = make_uint4(0, 0, 0, 0);
+        for (int j = 0; j < p.J; j++) {
+            const uint64_t w = p.S[j * p.Nloc + i];
+            uint4 v = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int ch = 0; ch < 8; ch++) v = xor4(v, psit[ch * 256 + ((w >> (8 * ch)) & 255)]);
+            const uint32_t t = tabs_sa + j * 512u;
+            acc.x ^= m4r4_word_sa(t, v.x); acc.y ^= m4r4_word_sa(t, v.y);
+            acc.z ^= m4r4_word_sa(t, v.z); acc.w ^= m4r4_word_sa(t, v.w);
+        }
+        p.W[i] = acc;
+    }
+}
+
+// blocked <-> t-sliced packing.  Element i of a blocked block goes to rank q = bits [K-g, K) of i,
+// at position j = (i & (2^(K-g)-1)) | ((i >> K) << (K-g)) of the chunk for q (chunks of Nloc/G).
+__device__ __forceinline__ uint64_t pack_src(uint64_t q, uint64_t j, int Kg, int K) {
+    return (j & ((1ull << Kg) - 1)) | (q << Kg) | ((j >> Kg) << K);
+}
+__global__ void k_pack(const uint4* __restrict__ H, uint4* __restrict__ X, uint64_t Nloc, int g, int K, int unpack) {
+    const uint64_t chunk = Nloc >> g;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < Nloc; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t q = t / chunk, j = t - q * chunk;
+        const uint64_t i = pack_src(q, j, K - g, K);
+        if (unpack) ((uint4*)H)[i] = X[t];
+        else X[t] = H[i];
+    }
+}
+
+// f[i] ^= src[i], i in [lo, hi)
+__global__ void k_xor_range(uint4* __restrict__ f, const uint4* __restrict__ src, uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < hi; i += (uint64_t)gridDim.x * blockDim.x)
+        f[i] = xor4(f[i], src[i]);
+}
+
+// ---------------------------------------------------------------------------------------------
+// NCCL, loaded at run time (no link-time dependency; whichever libnccl.so.2 the process has)
+// ---------------------------------------------------------------------------------------------
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef void* nccl_comm_t;
+struct NcclApi {
+    void* h = nullptr;
+    int (*GetUniqueId)(nccl_uid_t*);
+    int (*CommInitRank)(nccl_comm_t*, int, nccl_uid_t, int);
+    int (*CommDestroy)(nccl_comm_t);
+    int (*AllGather)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t);
+    int (*Send)(const void*, size_t, int, int, nccl_comm_t, cudaStream_t);
+    int (*Recv)(void*, size_t, int, int, nccl_comm_t, cudaStream_t);
+    int (*GroupStart)();
+    int (*GroupEnd)();
+    const char* (*GetErrorString)(int);
+};
+static const int NCCL_UINT8 = 1;   // ncclUint8 in the ncclDataType_t enum
+static NcclApi g_nccl;
+static std::string nccl_load() {
+    if (g_nccl.h) return "";
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return std::string("cannot load libnccl.so.2: ") + dlerror();
+#define NCCL_SYM(field, name)                                   \
+    *(void**)(&g_nccl.field) = dlsym(h, name);                  \
+    if (!g_nccl.field) return std::string("missing NCCL symbol ") + name;
+    NCCL_SYM(GetUniqueId, "ncclGetUniqueId");
+    NCCL_SYM(CommInitRank, "ncclCommInitRank");
+    NCCL_SYM(CommDestroy, "ncclCommDestroy");
+    NCCL_SYM(AllGather, "ncclAllGather");
+    NCCL_SYM(Send, "ncclSend");
+    NCCL_SYM(Recv, "ncclRecv");
+    NCCL_SYM(GroupStart, "ncclGroupStart");
+    NCCL_SYM(GroupEnd, "ncclGroupEnd");
+    NCCL_SYM(GetErrorString, "ncclGetErrorString");
+#undef NCCL_SYM
+    g_nccl.h = h;
+    return "";
+}
+
+struct gf2x_comm_s {
+    int nranks, rank, device;
+    nccl_comm_t comm;
+    void* ws;          // per-communicator workspace (grown on demand)
+    size_t ws_bytes;
+};
+
+// ---------------------------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------------------------
+enum ShardBuf { SB_A = 0, SB_B, SB_W, SB_T, SB_X, SB_HALO, SB_COUNT };
+
+struct RankCtx {
+    int r;
+    const uint64_t* a_shard;
+    const uint64_t* b_shard;
+    uint64_t* c_shard;
+    unsigned char* buf[SB_COUNT];
+};
+
+struct Xfer {
+    int src, dst;
+    ShardBuf sb, db;
+    size_t soff, doff, bytes;  // byte offsets
+};
+
+struct ShardGeom {
+    int G, g, m, mloc, K, p;
+    uint64_t n, N, Nloc;
+    std::vector<CvtPass> cvt_fwd, inner, outer, top_local;
+    std::vector<int> top_cross;  // levels l > mloc, ascending
+    std::vector<FftPass> fft;
+    Plan lp;                     // local plan (batch 1, N = Nloc) for the FFT launches
+    size_t off[SB_COUNT], bytes;
+};
+
+static gf2x_status shard_geom(uint64_t bits, int G, ShardGeom& S) {
+    if (G < 2 || (G & (G - 1))) return fail(GF2X_EINVAL, "nranks must be a power of two >= 2");
+    S.G = G;
+    S.g = 0;
+    while ((1 << S.g) < G) S.g++;
+    S.n = (bits + 63) / 64;
+    if (S.n == 0 || (S.n & (S.n - 1))) return fail(GF2X_EINVAL, "sharded multiply needs ceil(bits/64) a power of two");
+    S.p = ceil_log2_u64(S.n);
+    S.m = S.p + 1;
+    if (S.m > 32) return fail(GF2X_ETOOBIG, "FFT size exceeds 2^32 points");
+    S.K = 1;
+    while (2 * S.K <= S.m - 1) S.K *= 2;
+    S.mloc = S.m - S.g;
+    if (S.mloc < S.K || S.mloc < BOT_B + 6 || S.K < S.g)
+        return fail(GF2X_EINVAL, "operands too small for this many ranks (need m - log2 G >= max(K, 12))");
+    S.N = 1ull << S.m;
+    S.Nloc = S.N >> S.g;
+    S.cvt_fwd = plan_cvt(S.p, 8);
+    std::vector<CvtOp> inner, outer, top_local;
+    cvt_ops(S.K, 0, inner);
+    cvt_ops(S.m - S.K, S.K, outer);
+    for (auto& o : outer) o.lg -= S.g;   // t-sliced layout: global bits >= K sit g lower
+    for (int l = S.mloc; l >= S.K + 1; --l) top_local.push_back({l, S.K});
+    S.inner = plan_cvt_ops(inner, S.mloc, 16);
+    S.outer = plan_cvt_ops(outer, S.mloc, 16);
+    S.top_local = plan_cvt_ops(top_local, S.mloc, 16);
+    S.top_cross.clear();
+    for (int l = S.mloc + 1; l <= S.m; l++) S.top_cross.push_back(l);
+    S.fft = plan_fft(S.mloc);
+    S.lp = Plan();
+    S.lp.na = S.lp.nb = S.Nloc / 2;
+    S.lp.N = S.Nloc;
+    S.lp.batch = 1;
+    S.lp.m = S.mloc;
+    S.lp.ma = S.lp.mb = S.mloc - 1;
+    S.lp.fft = S.fft;
+    // per-rank buffers
+    size_t o = 0;
+    S.off[SB_A] = o; o = align256(o + S.n * 8);
+    S.off[SB_B] = o; o = align256(o + S.n * 8);
+    S.off[SB_W] = o; o = align256(o + (2 * S.Nloc + 2048) * 16);   // Wa | Wb | bottom pad
+    S.off[SB_T] = o; o = align256(o + S.Nloc * 16);
+    S.off[SB_X] = o; o = align256(o + S.Nloc * 16);
+    S.off[SB_HALO] = o; o = align256(o + 16);
+    S.bytes = o;
+    return GF2X_OK;
+}
+
+// s_k(phi(b)) for any b < 2^32 on the host: XOR of S[k][j] = s_k(v_j) over the set bits j of b
+// (S[k][j] = 0 for j < k, S[k][k] = s_k(v_k) = 1 by Prop. 1)
+static uint32_t host_s_eval(const DevTables* T, int k, uint64_t b) {
+    uint32_t c = 0;
+    for (int j = 0; j < 32; j++)
+        if ((b >> j) & 1) c ^= T->S[k * 32 + j];
+    return c;
+}
+
+struct ShardExec {
+    bool sim;
+    gf2x_comm_s* comm;   // NCCL mode
+    cudaStream_t st;
+    std::vector<RankCtx>* ranks;   // all ranks (sim) or the local one (NCCL)
+    gf2x_status run(const std::vector<Xfer>& xs) {
+        if (sim) {
+            for (const Xfer& x : xs) {
+                RankCtx& s = (*ranks)[x.src];
+                RankCtx& d = (*ranks)[x.dst];
+                cudaError_t e = cudaMemcpyAsync(d.buf[x.db] + x.doff, s.buf[x.sb] + x.soff, x.bytes, cudaMemcpyDeviceToDevice, st);
+                if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("shard copy: ") + cudaGetErrorString(e));
+            }
+            return GF2X_OK;
+        }
+        RankCtx& me = (*ranks)[0];
+        int rc = g_nccl.GroupStart();
+        for (const Xfer& x : xs) {
+            if (rc) break;
+            if (x.src == comm->rank && x.dst == comm->rank) {
+                cudaError_t e = cudaMemcpyAsync(me.buf[x.db] + x.doff, me.buf[x.sb] + x.soff, x.bytes, cudaMemcpyDeviceToDevice, st);
+                if (e != cudaSuccess) rc = -1;
+            } else if (x.src == comm->rank) {
+                rc = g_nccl.Send(me.buf[x.sb] + x.soff, x.bytes, NCCL_UINT8, x.dst, comm->comm, st);
+            } else if (x.dst == comm->rank) {
+                rc = g_nccl.Recv(me.buf[x.db] + x.doff, x.bytes, NCCL_UINT8, x.src, comm->comm, st);
+            }
+        }
+        int rc2 = g_nccl.GroupEnd();
+        if (rc || rc2) return fail(GF2X_ENCCL, std::string("NCCL exchange failed: ") + g_nccl.GetErrorString(rc ? rc : rc2));
+        return GF2X_OK;
+    }
+    RankCtx& local(int r) {
+        if (sim) return (*ranks)[r];
+        return (*ranks)[0];
+    }
+    bool owns(int r) const { return sim || r == comm->rank; }
+};
+
+// debug_stage (simulation only): 1 = stop after the forward FFT (copy every rank's Wa block to dbg),
+// 5 = stop after the whole iBasisCvt (copy the blocked W blocks).  dbg: N tower elements.
+static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds, const DevTables* host_tabs, uint64_t bits,
+                               int debug_stage = 0, uint4* dbg = nullptr) {
+    gf2x_status s;
+    const int G = S.G, g = S.g, smc = ds->sm_count;
+    cudaStream_t st = X.st;
+    const uint64_t Nloc = S.Nloc, chunk = Nloc >> g;
+    std::vector<int> mine;
+    for (int r = 0; r < G; r++)
+        if (X.owns(r)) mine.push_back(r);
+    auto last = [&](const char* what) -> gf2x_status {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+        return GF2X_OK;
+    };
+    // ---- gather both operands on every rank
+    if (X.sim) {   // virtual rank r's shard is at its input pointer: copy it into every rank
+        for (int q : mine) {
+            RankCtx& R = X.local(q);
+            for (int r = 0; r < G; r++) {
+                RankCtx& src = X.local(r);
+                const size_t sb = S.n / G * 8;
+                if (cudaMemcpyAsync(R.buf[SB_A] + r * sb, src.a_shard, sb, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+                    cudaMemcpyAsync(R.buf[SB_B] + r * sb, src.b_shard, sb, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                    return fail(GF2X_ECUDA, "shard gather copy failed");
+            }
+        }
+    } else {
+        RankCtx& R = X.local(X.comm->rank);
+        const size_t sb = S.n / G * 8;
+        int rc = g_nccl.GroupStart();
+        if (!rc) rc = g_nccl.AllGather(R.a_shard, R.buf[SB_A], sb, NCCL_UINT8, X.comm->comm, st);
+        if (!rc) rc = g_nccl.AllGather(R.b_shard, R.buf[SB_B], sb, NCCL_UINT8, X.comm->comm, st);
+        int rc2 = g_nccl.GroupEnd();
+        if (rc || rc2) return fail(GF2X_ENCCL, std::string("NCCL all-gather failed: ") + g_nccl.GetErrorString(rc ? rc : rc2));
+    }
+    // ---- mask, convert (redundantly), combine into h_r
+    for (int r : mine) {
+        RankCtx& R = X.local(r);
+        uint64_t* A = (uint64_t*)R.buf[SB_A];
+        uint64_t* B = (uint64_t*)R.buf[SB_B];
+        uint4* W = (uint4*)R.buf[SB_W];
+        k_prep<<<grid_for(S.n, 256, smc, 8), 256, 0, st>>>(A, S.n, bits, S.p, 1, A);
+        k_prep<<<grid_for(S.n, 256, smc, 8), 256, 0, st>>>(B, S.n, bits, S.p, 1, B);
+        if ((s = last("shard prep")) != GF2X_OK) return s;
+        if ((s = run_cvt<uint64_t>(S.cvt_fwd, A, S.p, 1, false, smc, st)) != GF2X_OK) return s;
+        if ((s = run_cvt<uint64_t>(S.cvt_fwd, B, S.p, 1, false, smc, st)) != GF2X_OK) return s;
+        ShardTopParams tp;
+        tp.tabs = ds->tabs;
+        tp.Nloc = Nloc;
+        tp.J = G / 2;
+        const uint64_t ar = (uint64_t)r * Nloc;   // alpha_r = phi(r Nloc)
+        for (int j = 0; j < tp.J; j++) {
+            gf2x_host::u128 c = 1;
+            for (int i = 0; i < g; i++)
+                if ((j >> i) & 1) c = gf2x_host::tower_mul(c, (gf2x_host::u128)host_s_eval(host_tabs, S.mloc + i, ar));
+            tp.coef[j] = (uint32_t)c;
+        }
+        const size_t sm = (size_t)tp.J * 512 + 8 * 256 * 16;
+        cudaFuncSetAttribute(k_shard_top, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        tp.S = A; tp.W = W;
+        k_shard_top<<<grid_for(Nloc, 256, smc, 2), 256, sm, st>>>(tp);
+        tp.S = B; tp.W = W + Nloc;
+        k_shard_top<<<grid_for(Nloc, 256, smc, 2), 256, sm, st>>>(tp);
+        if ((s = last("shard top")) != GF2X_OK) return s;
+        // ---- local FFT layers [6, mloc) of both operands, bottom kernel, local iFFT layers
+        const IdxMap map{S.mloc, g, (uint32_t)r};
+        const size_t nd = S.fft.size() - 1;
+        for (size_t i = 0; i < nd; i++)
+            if ((s = launch_fft(S.fft[i], false, false, W, Nloc, W, S.lp, ds, st, 2, map)) != GF2X_OK) return s;
+        BottomParams bp;
+        bp.A = W; bp.B = W + Nloc;
+        bp.total = Nloc;
+        bp.ntiles = (Nloc + (1ull << BT_BITS) - 1) >> BT_BITS;
+        bp.m = S.mloc; bp.L = S.fft.back().layers; bp.mode = debug_stage == 1 ? 1 : 7;
+        bp.map = map;
+        k_bottom<<<grid_for(bp.ntiles, 1, smc, 2), BT_THREADS, bottom_smem(), st>>>(bp);
+        if ((s = last("shard bottom")) != GF2X_OK) return s;
+        if (debug_stage == 1) {
+            cudaMemcpyAsync(dbg + r * Nloc, W, Nloc * 16, cudaMemcpyDeviceToDevice, st);
+            continue;
+        }
+        for (size_t i = nd; i-- > 0;)
+            if ((s = launch_fft(S.fft[i], true, false, W, Nloc, W, S.lp, ds, st, 1, map)) != GF2X_OK) return s;
+        // ---- inner iBasisCvt (windows in [0, K)) locally, then pack by destination rank
+        if ((s = run_cvt<uint4>(S.inner, W, S.mloc, 1, true, smc, st)) != GF2X_OK) return s;
+        k_pack<<<grid_for(Nloc, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_X], Nloc, g, S.K, 0);
+        if ((s = last("shard pack")) != GF2X_OK) return s;
+    }
+    if (debug_stage == 1) return GF2X_OK;
+    // ---- all-to-all: rank r's chunk q -> rank q's T at chunk r
+    {
+        std::vector<Xfer> xs;
+        for (int r = 0; r < G; r++)
+            for (int q = 0; q < G; q++) xs.push_back({r, q, SB_X, SB_T, q * chunk * 16, r * chunk * 16, chunk * 16});
+        if ((s = X.run(xs)) != GF2X_OK) return s;
+    }
+    // ---- t-sliced: top g iFFT layers, outer iBasisCvt
+    for (int q : mine) {
+        RankCtx& R = X.local(q);
+        uint4* T = (uint4*)R.buf[SB_T];
+        const IdxMap tmap{S.K - g, g, (uint32_t)q};
+        FftPass top{6, S.mloc - g, S.mloc, false, 0};
+        if ((s = launch_fft(top, true, false, T, Nloc, T, S.lp, ds, st, 1, tmap)) != GF2X_OK) return s;
+        if ((s = run_cvt<uint4>(S.outer, T, S.mloc, 1, true, smc, st)) != GF2X_OK) return s;
+    }
+    // ---- all-to-all back: rank q's T chunk r -> rank r's X chunk q, unpack
+    {
+        std::vector<Xfer> xs;
+        for (int q = 0; q < G; q++)
+            for (int r = 0; r < G; r++) xs.push_back({q, r, SB_T, SB_X, r * chunk * 16, q * chunk * 16, chunk * 16});
+        if ((s = X.run(xs)) != GF2X_OK) return s;
+    }
+    for (int r : mine) {
+        RankCtx& R = X.local(r);
+        uint4* W = (uint4*)R.buf[SB_W];
+        k_pack<<<grid_for(Nloc, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_X], Nloc, g, S.K, 1);
+        if ((s = last("shard unpack")) != GF2X_OK) return s;
+        if ((s = run_cvt<uint4>(S.top_local, W, S.mloc, 1, true, smc, st)) != GF2X_OK) return s;
+    }
+    // ---- top Taylor steps spanning ranks, ascending level (inverse order)
+    for (int l : S.top_cross) {
+        const int Sb = 1 << (l - S.mloc);          // blocks per segment
+        const uint64_t u = 1ull << (l - 1 - S.K);  // window unit
+        std::vector<Xfer> xs;
+        for (int base = 0; base < G; base += Sb) {
+            for (int p = 0; p < Sb / 2; p++) {
+                // phase B^-1 sources for rank base+p: t + d = t + h - u
+                xs.push_back({base + p + Sb / 2, base + p, SB_W, SB_X, 0, u * 16, (Nloc - u) * 16});
+                if (p >= 1) xs.push_back({base + p + Sb / 2 - 1, base + p, SB_W, SB_X, (Nloc - u) * 16, 0, u * 16});
+            }
+            // phase A^-1 sources: [2h-u, 2h) -> rank base + Sb/2, targets [0, u)
+            xs.push_back({base + Sb - 1, base + Sb / 2, SB_W, SB_T, (Nloc - u) * 16, 0, u * 16});
+        }
+        if ((s = X.run(xs)) != GF2X_OK) return s;
+        for (int r : mine) {
+            RankCtx& R = X.local(r);
+            uint4* W = (uint4*)R.buf[SB_W];
+            const int p = r % Sb;
+            if (p < Sb / 2) {
+                const uint64_t lo = (p == 0) ? u : 0;
+                k_xor_range<<<grid_for(Nloc - lo, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_X], lo, Nloc);
+            } else if (p == Sb / 2) {
+                k_xor_range<<<grid_for(u, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_T], 0, u);
+            }
+            if ((s = last("shard cross step")) != GF2X_OK) return s;
+        }
+    }
+    if (debug_stage == 5) {
+        for (int r : mine) cudaMemcpyAsync(dbg + r * Nloc, X.local(r).buf[SB_W], Nloc * 16, cudaMemcpyDeviceToDevice, st);
+        return GF2X_OK;
+    }
+    // ---- halo: last element of rank r-1 -> rank r; changeRepr^-1 + InterleavedCombine
+    {
+        std::vector<Xfer> xs;
+        for (int r = 1; r < G; r++) xs.push_back({r - 1, r, SB_W, SB_HALO, (Nloc - 1) * 16, 0, 16});
+        if ((s = X.run(xs)) != GF2X_OK) return s;
+    }
+    for (int r : mine) {
+        RankCtx& R = X.local(r);
+        k_ipsi_combine<<<grid_for(Nloc, 256, smc, 2), 256, 16 * 256 * 16, st>>>(
+            (const uint4*)R.buf[SB_W], ds->tabs, Nloc, Nloc, 1, R.c_shard, r ? (const uint4*)R.buf[SB_HALO] : nullptr);
+        if ((s = last("shard combine")) != GF2X_OK) return s;
+    }
+    return GF2X_OK;
+}
