@@ -133,8 +133,10 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft2(FftParams p) {
     uint4* tile = psit + (PSI ? 8 * 256 : 0);
     const uint32_t tabs_sa = (uint32_t)__cvta_generic_to_shared(tabs);
     if (tabs_sa & 255) __trap();  // the PRMT address fusion needs 256-byte aligned tables
-    if (PSI)
+    if (PSI) {
         for (uint32_t i = threadIdx.x; i < 8 * 256; i += blockDim.x) psit[i] = p.tabs->psi64[i];
+        __syncthreads();   // the first tile's load reads entries other warps wrote
+    }
 
     const uint64_t N = 1ull << p.m;
     const uint64_t tiles_per_pair = N >> (p.c + R);

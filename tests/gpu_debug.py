@@ -2,7 +2,10 @@
 
 python tests/gpu_debug.py [bits ...]
 """
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import time
 
 import numpy as np
