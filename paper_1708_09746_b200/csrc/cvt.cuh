@@ -113,3 +113,76 @@ __global__ void __launch_bounds__(256) k_cvt_stream(T* __restrict__ data, uint64
         }
     }
 }
+
+// ---------------------------------------------------------------------------------------------
+// Residue-class pass: a run of Taylor steps with one K (levels lg_hi .. lg_lo, forward order) whose
+// windows are wider than a tile.  Step lg couples f[i] with f[i + d], d = 2^(lg-1-K) (2^K - 1), so
+// every step of the run maps each residue class i mod M, M = 2^K - 1, of a 2^q-unit chunk
+// (q = lg_hi) to itself: with i = r M + c the class c is a column of rows r, and step lg is
+// "row r ^= row r + u" (u = 2^(lg-1-K)) on the rows whose position i mod 2^lg lies in [u, h).
+// A tile holds all rows of 2^C_log consecutive classes, so the whole run is one HBM pass instead
+// of one streaming pass per step.  The target at position [u, 2u) also owns the phase-A target
+// (position [h, h+u), row r + u) it reads, as in k_cvt_stream, so each step is one sweep.
+// ---------------------------------------------------------------------------------------------
+struct CvtResParams {
+    void* data;
+    uint64_t units_per_pair;  // 2^m
+    uint64_t batch;
+    int q, K, lg_hi, lg_lo, inverse;
+    int C_log, rows;          // 2^C_log classes per tile; rows = floor((2^q - 1) / M) + 1
+};
+
+template <typename T>
+__global__ void __launch_bounds__(512) k_cvt_res(CvtResParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    T* tile = reinterpret_cast<T*>(smem_raw);
+    T* data = reinterpret_cast<T*>(p.data);
+    const uint32_t M = (1u << p.K) - 1;
+    const uint32_t C = 1u << p.C_log, cmask = C - 1;
+    const uint32_t nrb = (M + C - 1) >> p.C_log;
+    const uint32_t span = 1u << p.q;                       // q <= 31
+    const uint64_t chunks = (p.units_per_pair >> p.q) * p.batch;
+    const uint64_t ntiles = chunks * nrb;
+    const uint32_t nslots = (uint32_t)p.rows << p.C_log;
+    const int nsteps = p.lg_hi - p.lg_lo + 1;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t chunk = t / nrb;
+        const uint32_t c0 = (uint32_t)(t - chunk * nrb) << p.C_log;
+        const uint32_t cn = min(C, M - c0);
+        T* dp = data + chunk * span;
+        for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
+            const uint32_t c = s & cmask, i = (s >> p.C_log) * M + c0 + c;
+            if (c < cn && i < span) tile[s] = dp[i];
+        }
+        __syncthreads();
+        for (int o = 0; o < nsteps; o++) {
+            const int lg = p.inverse ? p.lg_lo + o : p.lg_hi - o;
+            const uint32_t h = 1u << (lg - 1), u = h >> p.K, segm = (2u << (lg - 1)) - 1;
+            const uint32_t off = u << p.C_log;
+            for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
+                const uint32_t c = s & cmask, i = (s >> p.C_log) * M + c0 + c;
+                const uint32_t pos = i & segm;
+                if (c >= cn || i >= span || pos < u || pos >= h) continue;
+                if (pos < 2 * u) {   // also owns the phase-A target s + off
+                    if (!p.inverse) {
+                        const T a = xor_t<T>(tile[s + off], tile[s + 2 * off]);
+                        tile[s + off] = a;
+                        tile[s] = xor_t<T>(tile[s], a);
+                    } else {
+                        const T a = tile[s + off];
+                        tile[s] = xor_t<T>(tile[s], a);
+                        tile[s + off] = xor_t<T>(a, tile[s + 2 * off]);
+                    }
+                } else {
+                    tile[s] = xor_t<T>(tile[s], tile[s + off]);
+                }
+            }
+            __syncthreads();
+        }
+        for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
+            const uint32_t c = s & cmask, i = (s >> p.C_log) * M + c0 + c;
+            if (c < cn && i < span) dp[i] = tile[s];
+        }
+        __syncthreads();
+    }
+}

@@ -297,6 +297,8 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_tile<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_tile<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_cvt_res<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_cvt_res<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_ipsi_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         st.tabs = d;
     }
@@ -327,8 +329,10 @@ static void cvt_ops(int m, int sigma, std::vector<CvtOp>& out) {
 
 struct CvtPass {
     bool stream;
+    bool res = false;        // residue-class pass (k_cvt_res) over a run of same-K Taylor steps
     int c, r_lo, R;          // tile passes
-    std::vector<CvtOp> ops;  // tile: ops in forward execution order; stream: 1 op
+    int q = 0, C_log = 0, rows = 0;   // residue passes: chunk bits, classes per tile, rows per class
+    std::vector<CvtOp> ops;  // tile / residue: ops in forward execution order; stream: 1 op
 };
 
 // Greedy grouping of consecutive ops into tile passes: a pass holds tile bits [0,T) (contiguous)
@@ -348,14 +352,43 @@ static std::vector<CvtPass> plan_cvt_ops(const std::vector<CvtOp>& ops, int m, i
     std::vector<CvtPass> passes;
     int span_lo = 0, span_hi = 0;
     auto close = [&](CvtPass& P) {
-        if (P.stream) return;
+        if (P.stream || P.res) return;
         if (span_hi <= T) { P.c = 0; P.r_lo = 0; P.R = T; }
         else { P.c = cmin; P.R = Rrow; P.r_lo = std::max(cmin, std::min(span_lo, m - Rrow)); }
     };
     auto fits = [&](int lo, int hi) { return hi <= T || (lo >= cmin && hi - lo <= Rrow); };
-    for (const CvtOp& op : ops) {
+    for (size_t oi = 0; oi < ops.size(); oi++) {
+        const CvtOp& op = ops[oi];
         const int wlo = op.lg - 1 - op.K, whi = op.lg;
-        if (!passes.empty() && !passes.back().stream && (int)passes.back().ops.size() < MAX_TILE_OPS) {
+        if (!fits(wlo, whi) && op.lg <= 31) {
+            // a run of same-K steps at descending levels whose windows exceed a tile: one
+            // residue-class pass if the rows of a class fit shared memory (else this step streams)
+            size_t e = oi + 1;
+            while (e < ops.size() && ops[e].K == op.K && ops[e].lg == ops[e - 1].lg - 1 &&
+                   !fits(ops[e].lg - 1 - ops[e].K, ops[e].lg))
+                e++;
+            const uint64_t M = (1ull << op.K) - 1;
+            const int rows = (int)(((1ull << op.lg) - 1) / M + 1);
+            int C_log = unit_bytes == 8 ? 5 : 4;   // >= 256-byte runs per row
+            const size_t budget = 100 * 1024;
+            if ((size_t)rows * ((size_t)1 << C_log) * unit_bytes <= budget) {
+                while (C_log < 6 && (size_t)rows * ((size_t)2 << C_log) * unit_bytes <= budget) C_log++;
+                if (!passes.empty()) close(passes.back());
+                CvtPass P;
+                P.stream = false;
+                P.res = true;
+                P.c = P.r_lo = P.R = 0;
+                P.q = op.lg;
+                P.C_log = C_log;
+                P.rows = rows;
+                P.ops.assign(ops.begin() + oi, ops.begin() + e);
+                passes.push_back(P);
+                span_lo = 0; span_hi = 64;   // nothing joins a residue pass
+                oi = e - 1;
+                continue;
+            }
+        }
+        if (!passes.empty() && !passes.back().stream && !passes.back().res && (int)passes.back().ops.size() < MAX_TILE_OPS) {
             const int nlo = std::min(span_lo, wlo), nhi = std::max(span_hi, whi);
             if (fits(nlo, nhi)) {
                 passes.back().ops.push_back(op);
@@ -413,6 +446,8 @@ static void dump_plan(const Plan& P) {
         fprintf(stderr, "[gf2x plan] %s:", nm);
         for (auto& p : v) {
             if (p.stream) fprintf(stderr, " stream(%d,%d)", p.ops[0].lg - 1 - p.ops[0].K, p.ops[0].lg);
+            else if (p.res) fprintf(stderr, " res{q=%d K=%d lg=%d..%d C=%d rows=%d}", p.q, p.ops[0].K, p.ops[0].lg,
+                                    p.ops.back().lg, 1 << p.C_log, p.rows);
             else fprintf(stderr, " tile{c=%d rows=[%d,%d) ops=%zu}", p.c, p.r_lo, p.r_lo + p.R, p.ops.size());
         }
         fprintf(stderr, "\n");
@@ -484,7 +519,25 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
     if (inverse) std::reverse(order.begin(), order.end());
     for (const CvtPass* pp : order) {
         const CvtPass& p = *pp;
-        if (p.stream) {
+        if (p.res) {
+            CvtResParams prm;
+            prm.data = data;
+            prm.units_per_pair = per;
+            prm.batch = batch;
+            prm.q = p.q;
+            prm.K = p.ops[0].K;
+            prm.lg_hi = p.ops.front().lg;
+            prm.lg_lo = p.ops.back().lg;
+            prm.inverse = inverse ? 1 : 0;
+            prm.C_log = p.C_log;
+            prm.rows = p.rows;
+            const size_t sm = ((size_t)p.rows << p.C_log) * sizeof(T);
+            const uint64_t M = (1ull << prm.K) - 1;
+            const uint64_t ntiles = (per >> p.q) * batch * ((M + (1ull << p.C_log) - 1) >> p.C_log);
+            const int occ = std::max(1, (int)(200 * 1024 / (sm + 1024)));
+            ProfScope ps(sizeof(T) == 8 ? "k_cvt_res<u64>" : "k_cvt_res<u128>", 2.0 * per * batch * sizeof(T), st);
+            k_cvt_res<T><<<grid_for(ntiles, 1, sm_count, std::min(occ, 4)), 512, sm, st>>>(prm);
+        } else if (p.stream) {
             const CvtOp op = p.ops[0];
             const uint64_t n = per * batch / 2;
             ProfScope ps(sizeof(T) == 8 ? "k_cvt_stream<u64>" : "k_cvt_stream<u128>", 3.0 * n * sizeof(T), st);

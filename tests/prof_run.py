@@ -2,7 +2,10 @@
 
 python tests/prof_run.py c4a [reps]
 """
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np
 import torch
