@@ -150,9 +150,20 @@ __global__ void __launch_bounds__(512) k_cvt_res(CvtResParams p) {
         const uint32_t c0 = (uint32_t)(t - chunk * nrb) << p.C_log;
         const uint32_t cn = min(C, M - c0);
         T* dp = data + chunk * span;
-        for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
-            const uint32_t c = s & cmask, i = (s >> p.C_log) * M + c0 + c;
-            if (c < cn && i < span) tile[s] = dp[i];
+        for (uint32_t s0 = threadIdx.x; s0 < nslots; s0 += 8 * blockDim.x) {
+            T tmp[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const uint32_t s = s0 + u * blockDim.x;
+                const uint32_t c = s & cmask, i = (s >> p.C_log) * M + c0 + c;
+                if (s < nslots && c < cn && i < span) tmp[u] = dp[i];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const uint32_t s = s0 + u * blockDim.x;
+                const uint32_t c = s & cmask, i = (s >> p.C_log) * M + c0 + c;
+                if (s < nslots && c < cn && i < span) tile[s] = tmp[u];
+            }
         }
         __syncthreads();
         for (int o = 0; o < nsteps; o++) {
@@ -182,6 +193,156 @@ __global__ void __launch_bounds__(512) k_cvt_res(CvtResParams p) {
         for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
             const uint32_t c = s & cmask, i = (s >> p.C_log) * M + c0 + c;
             if (c < cn && i < span) dp[i] = tile[s];
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Register-blocked pass for a run of Taylor steps with K <= 4 (windows of <= 5 index bits) whose
+// windows lie inside R <= 8 consecutive index bits [r_lo, r_lo + R) -- e.g. a whole CVT(8) node
+// (12 steps).  XORs act on whole elements, so each 32-bit limb is independent: in a phase a thread
+// holds one limb of the 2^WB elements spanned by WB consecutive row bits [w_lo, w_lo + WB) and runs
+// every step of that phase in registers (straight-line code per (K, window offset)); phases
+// exchange data through the shared-memory tile.  A CVT(8) takes 3 phases instead of 12 steps x 2
+// shared-memory sweeps.
+//   mode 0: tile = columns (index bits [0, C), contiguous) x rows (bits [r_lo, r_lo + R)), r_lo >= C
+//   mode 1: tile = rows (bits [0, R)) x columns (bits [R, R + C)); shared rows padded by one element
+// ---------------------------------------------------------------------------------------------
+#define RB_MAX_PHASES 6
+#define RB_PAD(T) (16 / (uint32_t)sizeof(T))   // mode-1 column padding (16 B keeps bulk copies aligned)
+#define RB_MAX_OPS 48
+struct CvtRbParams {
+    void* data;
+    uint64_t units_per_pair, batch;
+    int r_lo, R, C, mode, inverse;
+    int nphase;
+    int ph_lo[RB_MAX_PHASES];    // phase window [ph_lo, ph_lo + WB) in row-bit coordinates
+    int ph_n[RB_MAX_PHASES];     // ops per phase
+    unsigned char ops[RB_MAX_OPS];   // (K index: 0 -> K=1, 1 -> K=2, 2 -> K=4) | (offset in the phase window << 2)
+};
+
+// one Taylor step with window bits [OFF, OFF + K + 1) of the WB-bit register block
+template <int WB, int K, int OFF, bool INV>
+__device__ __forceinline__ void rb_step(uint32_t* v) {
+    constexpr int T = 1 << K;
+#pragma unroll
+    for (int rest = 0; rest < (1 << WB); rest++) {
+        if ((rest >> OFF) & ((2 << K) - 1)) continue;   // enumerate the other bits only
+        auto at = [&](int y) -> uint32_t& { return v[rest | (y << OFF)]; };
+        if (!INV) {
+            at(T) ^= at(2 * T - 1);
+#pragma unroll
+            for (int y = 1; y < T; y++) at(y) ^= at(y + T - 1);
+        } else {
+#pragma unroll
+            for (int y = 1; y < T; y++) at(y) ^= at(y + T - 1);
+            at(T) ^= at(2 * T - 1);
+        }
+    }
+}
+
+template <int WB, bool INV>
+__device__ __forceinline__ void rb_dispatch(uint32_t* v, int code) {
+    const int kk = code & 3, off = code >> 2;
+    // K = 1 (2-bit windows)
+    if (kk == 0) {
+        if (off == 0) { if (WB >= 2) rb_step<WB, 1, 0, INV>(v); }
+        else if (off == 1) { if (WB >= 3) rb_step<WB, 1, (WB >= 3 ? 1 : 0), INV>(v); }
+        else if (off == 2) { if (WB >= 4) rb_step<WB, 1, (WB >= 4 ? 2 : 0), INV>(v); }
+        else if (off == 3) { if (WB >= 5) rb_step<WB, 1, (WB >= 5 ? 3 : 0), INV>(v); }
+        else { if (WB >= 6) rb_step<WB, 1, (WB >= 6 ? 4 : 0), INV>(v); }
+    } else if (kk == 1) {   // K = 2 (3-bit windows)
+        if (off == 0) { if (WB >= 3) rb_step<WB, (WB >= 3 ? 2 : 1), 0, INV>(v); }
+        else if (off == 1) { if (WB >= 4) rb_step<WB, (WB >= 4 ? 2 : 1), (WB >= 4 ? 1 : 0), INV>(v); }
+        else if (off == 2) { if (WB >= 5) rb_step<WB, (WB >= 5 ? 2 : 1), (WB >= 5 ? 2 : 0), INV>(v); }
+        else { if (WB >= 6) rb_step<WB, (WB >= 6 ? 2 : 1), (WB >= 6 ? 3 : 0), INV>(v); }
+    } else {                // K = 4 (5-bit windows)
+        if (off == 0) { if (WB >= 5) rb_step<WB, (WB >= 5 ? 4 : 1), 0, INV>(v); }
+        else { if (WB >= 6) rb_step<WB, (WB >= 6 ? 4 : 1), (WB >= 6 ? 1 : 0), INV>(v); }
+    }
+}
+
+template <typename T, int WB>
+__device__ __forceinline__ void rb_phase(uint32_t* s32, const CvtRbParams& p, int ph, int op0) {
+    constexpr int LW = sizeof(T) / 4;   // 32-bit limbs per unit
+    const int w_lo = p.ph_lo[ph];
+    const int nrest = p.R - WB;         // row bits outside the phase window
+    const uint32_t items = (uint32_t)LW << (p.C + nrest);
+    const uint32_t rowstride = p.mode ? 1u : (1u << p.C);
+    const uint32_t colstride = p.mode ? ((1u << p.R) + RB_PAD(T)) : 1u;
+    for (uint32_t it = threadIdx.x; it < items; it += blockDim.x) {
+        const uint32_t L = it % LW, rest = it / LW;
+        const uint32_t col = rest & ((1u << p.C) - 1), rr = rest >> p.C;
+        // row bits outside [w_lo, w_lo + WB): low part below w_lo, high part above
+        const uint32_t rfix = (rr & ((1u << w_lo) - 1)) | ((rr >> w_lo) << (w_lo + WB));
+        const uint32_t base = (rfix * rowstride + col * colstride) * LW + L;
+        const uint32_t jstride = (rowstride << w_lo) * LW;
+        uint32_t v[1 << WB];
+#pragma unroll
+        for (int j = 0; j < (1 << WB); j++) v[j] = s32[base + j * jstride];
+        for (int o = 0; o < p.ph_n[ph]; o++) {
+            const int code = p.ops[op0 + ((p.inverse & 1) ? p.ph_n[ph] - 1 - o : o)];
+            if (p.inverse & 1) rb_dispatch<WB, true>(v, code);
+            else rb_dispatch<WB, false>(v, code);
+        }
+#pragma unroll
+        for (int j = 0; j < (1 << WB); j++) s32[base + j * jstride] = v[j];
+    }
+}
+
+#define RB_THREADS 256
+// 2 CTAs per SM; global loads staged through registers, RB_UNR in flight per thread.  (A variant
+// with cp.async.bulk row copies issued by one warp measured 3x slower on B200: 256-byte bulk copies
+// are issue-bound.)  p.inverse bit 1 (GF2X_RB_NOPHASE, measurement only) skips the phases.
+#define RB_UNR 8
+template <typename T, int WB>
+__global__ void __launch_bounds__(RB_THREADS, 2) k_cvt_rb(CvtRbParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    T* tile = reinterpret_cast<T*>(smem_raw);
+    uint32_t* s32 = reinterpret_cast<uint32_t*>(smem_raw);
+    T* data = reinterpret_cast<T*>(p.data);
+    const uint32_t ncols = 1u << p.C, nrows = 1u << p.R, nslots = ncols << p.R;
+    const uint32_t cst = nrows + RB_PAD(T);
+    const uint64_t tiles_per_pair = p.units_per_pair >> (p.R + p.C);
+    const uint64_t ntiles = tiles_per_pair * p.batch;
+    const int midbits = p.mode ? 0 : p.r_lo - p.C;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t pair = t / tiles_per_pair;
+        const uint64_t tt = t - pair * tiles_per_pair;
+        T* dp = data + pair * p.units_per_pair;
+        uint64_t base;
+        if (p.mode) base = tt << (p.R + p.C);
+        else base = ((tt & ((1ull << midbits) - 1)) << p.C) | ((tt >> midbits) << (p.r_lo + p.R));
+        for (uint32_t s0 = threadIdx.x; s0 < nslots; s0 += RB_UNR * blockDim.x) {
+            T tmp[RB_UNR];
+            uint32_t smi[RB_UNR];
+#pragma unroll
+            for (int u = 0; u < RB_UNR; u++) {
+                const uint32_t s = s0 + u * blockDim.x;
+                uint64_t g;
+                if (p.mode) { const uint32_t row = s & (nrows - 1), col = s >> p.R; smi[u] = col * cst + row; g = base + s; }
+                else { const uint32_t col = s & (ncols - 1), row = s >> p.C; smi[u] = s; g = base + col + ((uint64_t)row << p.r_lo); }
+                if (s < nslots) tmp[u] = dp[g];
+            }
+#pragma unroll
+            for (int u = 0; u < RB_UNR; u++)
+                if (s0 + u * blockDim.x < nslots) tile[smi[u]] = tmp[u];
+        }
+        __syncthreads();
+        for (int i = 0; i < p.nphase * (p.inverse >> 1 ? 0 : 1); i++) {
+            const int ph = (p.inverse & 1) ? p.nphase - 1 - i : i;
+            int o0 = 0;
+            for (int q = 0; q < ph; q++) o0 += p.ph_n[q];
+            rb_phase<T, WB>(s32, p, ph, o0);
+            __syncthreads();
+        }
+        for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
+            uint32_t sm;
+            uint64_t g;
+            if (p.mode) { const uint32_t row = s & (nrows - 1), col = s >> p.R; sm = col * cst + row; g = base + s; }
+            else { const uint32_t col = s & (ncols - 1), row = s >> p.C; sm = s; g = base + col + ((uint64_t)row << p.r_lo); }
+            dp[g] = tile[sm];
         }
         __syncthreads();
     }

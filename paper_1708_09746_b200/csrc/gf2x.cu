@@ -297,6 +297,10 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_tile<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_tile<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+#define RB_ATTR(T, W) CUDA_TRY(cudaFuncSetAttribute(k_cvt_rb<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        RB_ATTR(uint64_t, 2); RB_ATTR(uint64_t, 3); RB_ATTR(uint64_t, 4); RB_ATTR(uint64_t, 5); RB_ATTR(uint64_t, 6);
+        RB_ATTR(uint4, 2); RB_ATTR(uint4, 3); RB_ATTR(uint4, 4); RB_ATTR(uint4, 5); RB_ATTR(uint4, 6);
+#undef RB_ATTR
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_res<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_res<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_ipsi_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -332,8 +336,67 @@ struct CvtPass {
     bool res = false;        // residue-class pass (k_cvt_res) over a run of same-K Taylor steps
     int c, r_lo, R;          // tile passes
     int q = 0, C_log = 0, rows = 0;   // residue passes: chunk bits, classes per tile, rows per class
+    bool rb = false;         // register-blocked pass (k_cvt_rb): K <= 4 steps inside 8 index bits
+    CvtRbParams rbp;         // its geometry, phases and op codes (data/sizes filled at launch)
+    int rb_wb = 0;           // phase width (bits)
     std::vector<CvtOp> ops;  // tile / residue: ops in forward execution order; stream: 1 op
 };
+
+// Try to take a run of ops starting at ops[oi] as one register-blocked pass; returns the number taken.
+static int plan_rb(const std::vector<CvtOp>& ops, size_t oi, int m, int unit_bytes, CvtPass& P) {
+    int lo = 64, hi = 0;
+    size_t e = oi;
+    for (; e < ops.size() && (int)(e - oi) < RB_MAX_OPS; e++) {
+        if (ops[e].K > 4) break;
+        const int a = ops[e].lg - 1 - ops[e].K, b = ops[e].lg;
+        const int nlo = std::min(lo, a), nhi = std::max(hi, b);
+        if (nhi - nlo > 8) break;
+        lo = nlo; hi = nhi;
+    }
+    if (e == oi) return 0;
+    const int R = hi - lo;
+    const int Cw = unit_bytes == 8 ? 5 : 4;
+    int mode, C;
+    if (lo == 0) { mode = 1; C = std::min(Cw, m - R); }
+    else if (lo >= Cw) { mode = 0; C = Cw; }
+    else return 0;
+    const int WB = std::min(6, R);
+    CvtRbParams& q = P.rbp;
+    memset(&q, 0, sizeof(q));
+    q.r_lo = lo; q.R = R; q.C = C; q.mode = mode;
+    int nph = 0, plo = 64, phi = 0, cnt = 0;
+    std::vector<std::pair<int, int>> win;   // op windows relative to lo
+    for (size_t i = oi; i < e; i++) win.push_back({ops[i].lg - 1 - ops[i].K - lo, ops[i].lg - lo});
+    size_t first = 0;
+    auto flush = [&](size_t upto) {
+        const int w_lo = std::min(plo, R - WB);
+        q.ph_lo[nph] = w_lo;
+        q.ph_n[nph] = (int)(upto - first);
+        for (size_t i = first; i < upto; i++) {
+            const int K = ops[oi + i].K;
+            const int kk = K == 1 ? 0 : (K == 2 ? 1 : 2);
+            q.ops[cnt++] = (unsigned char)(kk | ((win[i].first - w_lo) << 2));
+        }
+        nph++;
+        first = upto;
+    };
+    for (size_t i = 0; i < win.size(); i++) {
+        const int nlo = std::min(plo, win[i].first), nhi = std::max(phi, win[i].second);
+        if (nhi - nlo > WB) {
+            if (nph + 1 >= RB_MAX_PHASES) return 0;
+            flush(i);
+            plo = win[i].first; phi = win[i].second;
+        } else {
+            plo = nlo; phi = nhi;
+        }
+    }
+    flush(win.size());
+    q.nphase = nph;
+    P.stream = false; P.res = false; P.rb = true; P.rb_wb = WB;
+    P.c = P.r_lo = P.R = 0;
+    P.ops.assign(ops.begin() + oi, ops.begin() + e);
+    return (int)(e - oi);
+}
 
 // Greedy grouping of consecutive ops into tile passes: a pass holds tile bits [0,T) (contiguous)
 // or [0,cmin) U [r_lo, r_lo + T - cmin) (rows of 2^cmin contiguous units = one 32-byte sector);
@@ -352,7 +415,7 @@ static std::vector<CvtPass> plan_cvt_ops(const std::vector<CvtOp>& ops, int m, i
     std::vector<CvtPass> passes;
     int span_lo = 0, span_hi = 0;
     auto close = [&](CvtPass& P) {
-        if (P.stream || P.res) return;
+        if (P.stream || P.res || P.rb) return;
         if (span_hi <= T) { P.c = 0; P.r_lo = 0; P.R = T; }
         else { P.c = cmin; P.R = Rrow; P.r_lo = std::max(cmin, std::min(span_lo, m - Rrow)); }
     };
@@ -360,12 +423,13 @@ static std::vector<CvtPass> plan_cvt_ops(const std::vector<CvtOp>& ops, int m, i
     for (size_t oi = 0; oi < ops.size(); oi++) {
         const CvtOp& op = ops[oi];
         const int wlo = op.lg - 1 - op.K, whi = op.lg;
-        if (!fits(wlo, whi) && op.lg <= 31) {
+        const bool res8 = op.K == 8 && getenv("GF2X_RES8");   // measured no faster than tile passes
+        if ((!fits(wlo, whi) || res8) && op.lg <= 31) {
             // a run of same-K steps at descending levels whose windows exceed a tile: one
             // residue-class pass if the rows of a class fit shared memory (else this step streams)
             size_t e = oi + 1;
             while (e < ops.size() && ops[e].K == op.K && ops[e].lg == ops[e - 1].lg - 1 &&
-                   !fits(ops[e].lg - 1 - ops[e].K, ops[e].lg))
+                   (res8 || !fits(ops[e].lg - 1 - ops[e].K, ops[e].lg)))
                 e++;
             const uint64_t M = (1ull << op.K) - 1;
             const int rows = (int)(((1ull << op.lg) - 1) / M + 1);
@@ -388,7 +452,19 @@ static std::vector<CvtPass> plan_cvt_ops(const std::vector<CvtOp>& ops, int m, i
                 continue;
             }
         }
-        if (!passes.empty() && !passes.back().stream && !passes.back().res && (int)passes.back().ops.size() < MAX_TILE_OPS) {
+        if (!getenv("GF2X_NO_RB")) {
+            CvtPass P;
+            const int took = plan_rb(ops, oi, m, unit_bytes, P);
+            if (took > 0) {
+                if (!passes.empty()) close(passes.back());
+                passes.push_back(P);
+                span_lo = 0; span_hi = 64;
+                oi += took - 1;
+                continue;
+            }
+        }
+        if (!passes.empty() && !passes.back().stream && !passes.back().res && !passes.back().rb &&
+            (int)passes.back().ops.size() < MAX_TILE_OPS) {
             const int nlo = std::min(span_lo, wlo), nhi = std::max(span_hi, whi);
             if (fits(nlo, nhi)) {
                 passes.back().ops.push_back(op);
@@ -448,6 +524,8 @@ static void dump_plan(const Plan& P) {
             if (p.stream) fprintf(stderr, " stream(%d,%d)", p.ops[0].lg - 1 - p.ops[0].K, p.ops[0].lg);
             else if (p.res) fprintf(stderr, " res{q=%d K=%d lg=%d..%d C=%d rows=%d}", p.q, p.ops[0].K, p.ops[0].lg,
                                     p.ops.back().lg, 1 << p.C_log, p.rows);
+            else if (p.rb) fprintf(stderr, " rb{rows=[%d,%d) C=%d mode=%d phases=%d ops=%zu}", p.rbp.r_lo, p.rbp.r_lo + p.rbp.R,
+                                   p.rbp.C, p.rbp.mode, p.rbp.nphase, p.ops.size());
             else fprintf(stderr, " tile{c=%d rows=[%d,%d) ops=%zu}", p.c, p.r_lo, p.r_lo + p.R, p.ops.size());
         }
         fprintf(stderr, "\n");
@@ -481,7 +559,7 @@ static gf2x_status make_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, Pl
     // equal shapes for a and b run as one launch over 2*batch products; a 2^11-element pad after Wb
     // keeps the bottom kernel's last tile in bounds
     P.off_sa = 0;
-    P.off_sb = P.off_sa + (1ull << P.ma) * P.batch * 8;
+    P.off_sb = (P.off_sa + (1ull << P.ma) * P.batch * 8 + 15) & ~(size_t)15;   // 16-byte aligned (vector / bulk access)
     P.off_wa = align256(P.off_sb + (1ull << P.mb) * P.batch * 8);
     P.off_wb = P.off_wa + P.N * P.batch * 16;
     P.bytes = align256(P.off_wb + (P.N * P.batch + 2048) * 16);
@@ -490,7 +568,7 @@ static gf2x_status make_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, Pl
 }
 
 static int launches_of(const Plan& P) {
-    const bool same = P.ma == P.mb;
+    const bool same = P.ma == P.mb && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8;
     int n = 2;  // prep a, b
     n += (int)P.cvt_a.size() + (int)P.cvt_b.size() + (int)P.icvt.size();
     const int nd = (int)P.fft.size() - 1;
@@ -519,7 +597,27 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
     if (inverse) std::reverse(order.begin(), order.end());
     for (const CvtPass* pp : order) {
         const CvtPass& p = *pp;
-        if (p.res) {
+        if (p.rb) {
+            CvtRbParams prm = p.rbp;
+            prm.data = data;
+            prm.units_per_pair = per;
+            prm.batch = batch;
+            prm.inverse = (inverse ? 1 : 0) | (getenv("GF2X_RB_NOPHASE") ? 2 : 0);   // bit 1: debug, copy only
+            const size_t ncols = (size_t)1 << prm.C, nrows = (size_t)1 << prm.R;
+            const size_t bufsz = (ncols * (nrows + (prm.mode ? 16 / sizeof(T) : 0)) * sizeof(T) + 127) & ~(size_t)127;
+            const size_t sm = bufsz;
+            const uint64_t ntiles = (per >> (prm.R + prm.C)) * batch;
+            const int occ = 2;
+            ProfScope ps(sizeof(T) == 8 ? "k_cvt_rb<u64>" : "k_cvt_rb<u128>", 2.0 * per * batch * sizeof(T), st);
+            const int g = grid_for(ntiles, 1, sm_count, occ);
+            switch (p.rb_wb) {
+                case 2: k_cvt_rb<T, 2><<<g, RB_THREADS, sm, st>>>(prm); break;
+                case 3: k_cvt_rb<T, 3><<<g, RB_THREADS, sm, st>>>(prm); break;
+                case 4: k_cvt_rb<T, 4><<<g, RB_THREADS, sm, st>>>(prm); break;
+                case 5: k_cvt_rb<T, 5><<<g, RB_THREADS, sm, st>>>(prm); break;
+                default: k_cvt_rb<T, 6><<<g, RB_THREADS, sm, st>>>(prm); break;
+            }
+        } else if (p.res) {
             CvtResParams prm;
             prm.data = data;
             prm.units_per_pair = per;
@@ -607,7 +705,8 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
     // (one operand at a time: at the headline sizes each 64-bit block array fits the 126 MB L2 alone)
     if ((s = run_cvt<uint64_t>(P.cvt_a, Sa, P.ma, P.batch, false, smc, st)) != GF2X_OK) return s;
     if ((s = run_cvt<uint64_t>(P.cvt_b, Sb, P.mb, P.batch, false, smc, st)) != GF2X_OK) return s;
-    const bool same = (P.ma == P.mb);   // Sb | Wb directly follow Sa | Wa: one FFT launch for both
+    // Sb | Wb directly follow Sa | Wa: one FFT launch for both
+    const bool same = (P.ma == P.mb) && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8;
     // changeRepr + FFT_LCH top layers (direct passes; the last planned pass is the bottom one)
     const size_t ndirect = P.fft.size() - 1;
     for (size_t i = 0; i < ndirect; i++) {
