@@ -14,6 +14,7 @@
 #pragma once
 
 #define FFT_THREADS 256
+#define FFT_UNR 8
 #define BOT_B 6       // layers [0, BOT_B) run in the fused bit-sliced bottom kernel
 
 // ---------------------------------------------------------------------------------------------
@@ -122,8 +123,11 @@ __device__ __forceinline__ void fft_group_any(int r, uint4* tile, uint32_t nslot
 }
 
 // shared memory: [tables (2^R - 1) x 512 B] [psi table (PSI)] [tile]
+#ifndef FFT_MINB
+#define FFT_MINB 2
+#endif
 template <bool INV, bool PSI>
-__global__ void __launch_bounds__(FFT_THREADS) k_fft2(FftParams p) {
+__global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int R = p.k_hi - p.k_lo;
     const uint32_t nslots = 1u << (p.c + R);
@@ -173,9 +177,19 @@ __global__ void __launch_bounds__(FFT_THREADS) k_fft2(FftParams p) {
                 tile[s] = v;
             }
         } else {
+            // FFT_UNR loads per thread in flight before their shared-memory stores
             const uint4* src = reinterpret_cast<const uint4*>(p.src) + pair * N;
-            for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x)
-                tile[s] = src[base | (s & cmask) | ((s >> p.c) << p.k_lo)];
+            for (uint32_t s0 = threadIdx.x; s0 < nslots; s0 += FFT_UNR * blockDim.x) {
+                uint4 tmp[FFT_UNR];
+#pragma unroll
+                for (int u = 0; u < FFT_UNR; u++) {
+                    const uint32_t s = s0 + u * blockDim.x;
+                    if (s < nslots) tmp[u] = src[base | (s & cmask) | ((s >> p.c) << p.k_lo)];
+                }
+#pragma unroll
+                for (int u = 0; u < FFT_UNR; u++)
+                    if (s0 + u * blockDim.x < nslots) tile[s0 + u * blockDim.x] = tmp[u];
+            }
         }
         __syncthreads();
         // ---- layers, in groups of <= 3 (forward: from the top; inverse: from the bottom)

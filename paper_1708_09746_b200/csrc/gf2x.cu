@@ -500,7 +500,8 @@ static std::vector<FftPass> plan_fft(int m) {
         const int rem = top - BOT_B;
         const int r = (rem + (np - i) - 1) / (np - i);  // remaining layers / remaining passes
         const int lo = top - r;
-        v.push_back({i == 0 ? 5 : 6, lo, top, false, 0});
+        static const int cdir = getenv("GF2X_FFT_C") ? atoi(getenv("GF2X_FFT_C")) : 6;
+        v.push_back({i == 0 ? 5 : cdir, lo, top, false, 0});
         top = lo;
     }
     v.push_back({0, 0, 0, true, m < BOT_B ? m : BOT_B});  // the fused bit-sliced bottom kernel
