@@ -9,8 +9,11 @@ operands (gf2x_synth recipe) already resident in HBM.  Time = CUDA events on the
 around exactly K steps after W warm-ups, barrier + synchronize on both sides, max over ranks.
 value = input Gbit/s = (a_bits + b_bits) * steps * n_gpus / max-rank time (whole job).
 
-Multi-GPU (torchrun, N > 1): round 1 runs one independent replica multiply per GPU (no data-path
-collective; "scaling": "weak"); the sharded FFT of SURVEY §8(e) is future work.
+Multi-GPU (torchrun, N > 1): by default ONE multiply partitioned over the N ranks (SURVEY §8(e):
+gf2x_mul_sharded, NCCL all-gather + all-to-all/pairwise exchanges, top log2 N FFT layers as the
+exchange step; "scaling": "strong"; value = input bits of that multiply / max-rank time); rank 0
+checks the gathered product against its own single-GPU multiply.  --mode replicas runs one
+independent multiply per rank instead ("scaling": "weak"); batched configs always shard that way.
 
 --impl reference runs the repo's CPU oracle (oracle/, the paper's Alg. 5 step by step) on the box's
 host cores on a bounded sample of the same workload (rank 0 only) and prints the same JSON line.
@@ -48,6 +51,21 @@ WORKLOAD = {
 
 def rank_info():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def load_alu_peak():
+    """ALU-pipe peak in lane instructions/s: 148 SMs x 4 SMSPs x 16 lanes/clk (LOP3/PRMT/SHF issue every 2nd
+    cycle per SMSP, B300_MICROARCH.md "Pipe rates") x the max SM clock (MEASURED_PEAKS.json sm_max_mhz, else
+    the 1965 MHz of B200_PROFILING.md)."""
+    mhz, src = 1965.0, "derived: 148 SM x 64 lanes/clk x 1965 MHz (B200_PROFILING.md clocks.max.sm)"
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            mhz = float(json.load(open(p))["sm_max_mhz"])
+            src = f"derived: 148 SM x 64 lanes/clk x {mhz:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"
+        except Exception:
+            pass
+    return 148 * 64 * mhz * 1e6 / 1e9, src
 
 
 def load_peaks():
@@ -166,6 +184,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default=None, choices=["sharded", "replicas"],
+                    help="N > 1: one multiply partitioned over the ranks (default) or one per rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -182,7 +202,13 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     G.load()
     bits, batch = CONFIGS[args.config]
-    seed = DEFAULT_SEED + 2 * rank  # each replica its own operand pair
+    mode = args.mode or ("sharded" if world > 1 else "single")
+    if world == 1:
+        mode = "single"
+    if mode == "sharded" and batch != 1:
+        mode = "replicas"   # batched configs shard trivially: independent products per rank
+    sharded = mode == "sharded"
+    seed = DEFAULT_SEED + (0 if sharded else 2 * rank)  # replicas: each rank its own operand pair
     if batch == 1:
         a, b = operand_pair(bits, seed)
     else:
@@ -194,9 +220,18 @@ def main():
     db = torch.from_numpy(b.reshape(-1).view(np.int64)).to(dev).view(torch.uint64)
     dc = torch.empty(n_out * batch, dtype=torch.uint64, device=dev)
     stream = torch.cuda.current_stream()
+    if sharded:
+        # the FFT partitioned over the ranks (NCCL over NVLink); rank r owns words
+        # [r n/G, (r+1) n/G) of a and b and receives words [r 2n/G, (r+1) 2n/G) of c
+        comm = G.init_from_process_group()
+        lo, hi = G.shard_words(n, world, rank)
+        sa, sb = da[lo:hi].clone(), db[lo:hi].clone()
+        sc = torch.empty(n_out // world, dtype=torch.uint64, device=dev)
 
     def step():
-        if batch == 1:
+        if sharded:
+            comm.mul(sa, sb, bits, sc, stream=stream)
+        elif batch == 1:
             G.gf2x_mul(da, bits, db, bits, dc, stream=stream)
         else:
             G.gf2x_mul_batched(da, bits, db, bits, batch, dc, stream=stream)
@@ -235,20 +270,36 @@ def main():
 
     ms_step = ms / args.steps
     in_bits = 2 * bits * batch
-    value = in_bits * world / (ms_step * 1e-3) / 1e9
+    jobs = 1 if sharded else world   # multiplies the whole job completes per step
+    value = in_bits * jobs / (ms_step * 1e-3) / 1e9
+    if sharded:
+        # the partitioned product equals the single-GPU one (rank 0 recomputes it alone)
+        parts = [torch.empty_like(sc) for _ in range(world)]
+        dist.all_gather(parts, sc)
+        if rank == 0:
+            G.gf2x_mul(da, bits, db, bits, dc, stream=stream)
+            torch.cuda.synchronize()
+            assert torch.equal(torch.cat(parts).view(torch.int64), dc.view(torch.int64)), "sharded != single-GPU"
 
     # ---- end to end through the public API with pinned host buffers
-    ha = torch.from_numpy(a.reshape(-1).view(np.int64)).pin_memory()
-    hb = torch.from_numpy(b.reshape(-1).view(np.int64)).pin_memory()
-    hc = torch.empty(n_out * batch, dtype=torch.int64).pin_memory()
-    ea = torch.empty(n * batch, dtype=torch.int64, device=dev)
-    eb = torch.empty(n * batch, dtype=torch.int64, device=dev)
-    ec = torch.empty(n_out * batch, dtype=torch.int64, device=dev)
+    if sharded:   # each rank moves its own shards
+        ha = torch.from_numpy(a.reshape(-1)[lo:hi].view(np.int64)).pin_memory()
+        hb = torch.from_numpy(b.reshape(-1)[lo:hi].view(np.int64)).pin_memory()
+        hc = torch.empty(n_out // world, dtype=torch.int64).pin_memory()
+    else:
+        ha = torch.from_numpy(a.reshape(-1).view(np.int64)).pin_memory()
+        hb = torch.from_numpy(b.reshape(-1).view(np.int64)).pin_memory()
+        hc = torch.empty(n_out * batch, dtype=torch.int64).pin_memory()
+    ea = torch.empty(ha.numel(), dtype=torch.int64, device=dev)
+    eb = torch.empty(hb.numel(), dtype=torch.int64, device=dev)
+    ec = torch.empty(hc.numel(), dtype=torch.int64, device=dev)
 
     def e2e_step():
         ea.copy_(ha, non_blocking=True)
         eb.copy_(hb, non_blocking=True)
-        if batch == 1:
+        if sharded:
+            comm.mul(ea, eb, bits, ec, stream=stream)
+        elif batch == 1:
             G.gf2x_mul(ea, bits, eb, bits, ec, stream=stream)
         else:
             G.gf2x_mul_batched(ea, bits, eb, bits, batch, ec, stream=stream)
@@ -270,16 +321,19 @@ def main():
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_val = in_bits * world / (e2e_ms / args.e2e_steps * 1e-3) / 1e9
+    e2e_val = in_bits * jobs / (e2e_ms / args.e2e_steps * 1e-3) / 1e9
     # result check of the e2e copy against the device-resident run (both from the library)
-    assert torch.equal(hc.view(torch.int64), dc.cpu().view(torch.int64))
+    assert torch.equal(hc.view(torch.int64), (sc if sharded else dc).cpu().view(torch.int64))
 
     # ---- roofline of the dominant kernel (live CUDA-event durations over the timed region)
     peak, peak_src = load_peaks()
+    alu_peak, alu_src = load_alu_peak()
     dom = max(prof, key=lambda r: r["ms"])
     per_launch_ms = dom["ms"] / dom["launches"]
     per_launch_bytes = dom["bytes"] / dom["launches"]
+    per_launch_ops = dom.get("alu_ops", 0) / dom["launches"]
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+    achieved_ops = per_launch_ops / (per_launch_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -290,6 +344,8 @@ def main():
     step_bytes = sum(r["bytes"] for r in prof) / args.steps
     kern_ms = sum(r["ms"] for r in prof) / args.steps
     launches = G.gf2x_launch_count(bits, bits, batch)
+    if sharded:   # every kernel of the sharded path is bracketed by the profiling hook
+        launches = sum(r["launches"] for r in prof) // args.steps
 
     line = {
         "metric": METRIC,
@@ -300,22 +356,29 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 4),
         "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": round(value / (PAPER_GBITS[args.config] * world), 2) if args.config in PAPER_GBITS else None,
+        "scaling": "strong" if sharded else "weak",
+        "vs_baseline": round(value / (PAPER_GBITS[args.config] * jobs), 2) if args.config in PAPER_GBITS else None,
         "vs_baseline_note": "ratio to the paper's own CPU number for this workload (Table 2, Haswell E3-1245 v3, "
                             "TGF(2^128) row): context, not the target",
         "dtype": "u64",
         "data": "synthetic",
         "config": {
             "workload": WORKLOAD[args.config], "config": args.config, "operand_bits": bits, "batch": batch,
-            "fft_points": 1 << max(0, (2 * n - 2).bit_length()), "parallelism": "replicas" if world > 1 else "single",
+            "fft_points": 1 << max(0, (2 * n - 2).bit_length()),
+            "parallelism": (f"sharded FFT over {world} GPUs (NCCL)" if sharded else
+                            ("replicas" if world > 1 else "single")),
             "seed": DEFAULT_SEED, "l2": "working set > 126 MB L2 (operands + 2 spectra), no flush" if bits >= 1 << 28
             else "working set may be L2-resident (small config)",
             "paper_ms_haswell": PAPER_MS.get(args.config),
         },
-        "roofline": {
+        "roofline": ({
+            "bound": "alu", "kernel": dom["kernel"], "achieved": round(achieved_ops, 1), "peak": round(alu_peak, 1),
+            "unit": "Ginstr/s (ALU-pipe lane instructions)", "frac": round(achieved_ops / alu_peak, 4),
+            "traffic": traffic, "peak_source": alu_src, "algorithmic_alu_ops_per_launch": per_launch_ops,
+            "hbm_achieved_gbs": round(achieved, 2), "hbm_frac": round(achieved / peak, 4), "hbm_peak": peak,
+        } if per_launch_ops > 0 else {
             "bound": "hbm", "kernel": dom["kernel"], "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src}) | {
             "algorithmic_bytes_per_launch": per_launch_bytes, "ms_per_launch": round(per_launch_ms, 5),
             "step_algorithmic_bytes": step_bytes,
             "step_frac_of_hbm": round(step_bytes / (kern_ms * 1e-3) / 1e9 / peak, 4),
@@ -323,14 +386,17 @@ def main():
         },
         "kernels": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in prof],
         "clocks": clocks,
-        "e2e": {"value": round(e2e_val, 4), "unit": UNIT, "h2d_bytes_per_step": 2 * n * 8 * batch,
-                "d2h_bytes_per_step": n_out * 8 * batch, "ms_per_step": round(e2e_ms / args.e2e_steps, 4)},
+        "e2e": {"value": round(e2e_val, 4), "unit": UNIT, "h2d_bytes_per_step": (ha.numel() + hb.numel()) * 8,
+                "d2h_bytes_per_step": hc.numel() * 8, "ms_per_step": round(e2e_ms / args.e2e_steps, 4),
+                "per_rank_bytes": sharded},
         "gpu_launches": launches * args.steps,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, 1 << 24 if bits >= 1 << 24 else bits)
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if sharded:
+        comm.close()
     if dist:
         dist.destroy_process_group()
     return 0

@@ -99,10 +99,18 @@ gf2x_status gf2x_mul_sharded_sim(const uint64_t* a, const uint64_t* b, uint64_t 
 gf2x_status gf2x_debug_shard_stage(const uint64_t* a, const uint64_t* b, uint64_t bits, int nranks, int stage,
                                    uint64_t* out, void* stream);
 
+/* Host-only description of the sharded multiply's exchanges (no device work): writes JSON into buf
+ * (cap bytes, NUL-terminated) with the geometry (G, g, m, mloc, K, n, N, Nloc, per-rank buffer
+ * sizes) and every transfer list [src_rank, dst_rank, src_buf, dst_buf, src_off, dst_off, bytes]
+ * ("a2a_fwd", "a2a_back", "cross" per level of "top_cross", "halo") that every rank derives
+ * identically.  Returns the length needed, or -1 if (bits, nranks) is unsupported. */
+int gf2x_shard_plan(uint64_t bits, int nranks, char* buf, size_t cap);
+
 /* Measurement hook (bench.py): while enabled, every kernel the library enqueues from the calling
  * thread is bracketed by CUDA events on its stream.  gf2x_profile_report synchronises those events
  * and writes a JSON array into buf (cap bytes, NUL-terminated):
- *   [{"kernel": name, "launches": n, "ms": total device ms, "bytes": algorithmic HBM bytes}, ...]
+ *   [{"kernel": name, "launches": n, "ms": total device ms, "bytes": algorithmic HBM bytes,
+ *     "alu_ops": algorithmic ALU-pipe lane instructions (0 for kernels designed to be HBM-bound)}, ...]
  * and returns the length needed (call again with a larger buf if it exceeds cap).  Enabling or
  * disabling clears the record. */
 gf2x_status gf2x_profile_enable(int on);

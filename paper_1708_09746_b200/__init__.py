@@ -22,7 +22,7 @@ STATUS = {0: "GF2X_OK", 1: "GF2X_EINVAL", 2: "GF2X_ETOOBIG", 3: "GF2X_ENOMEM", 4
 EXPORTS = [
     "gf2x_mul", "gf2x_mul_batched", "gf2x_workspace_bytes", "gf2x_mul_ws", "gf2x_launch_count",
     "gf2x_debug_stage", "gf2x_comm_unique_id", "gf2x_comm_init", "gf2x_comm_destroy", "gf2x_mul_sharded",
-    "gf2x_mul_sharded_sim", "gf2x_debug_shard_stage", "gf2x_profile_enable", "gf2x_profile_report", "gf2x_status_string", "gf2x_last_error",
+    "gf2x_mul_sharded_sim", "gf2x_debug_shard_stage", "gf2x_shard_plan", "gf2x_profile_enable", "gf2x_profile_report", "gf2x_status_string", "gf2x_last_error",
     "gf2x_release", "gf2x_version",
 ]
 
@@ -64,6 +64,8 @@ def load(path: str = LIB_PATH):
     for name in ("gf2x_comm_unique_id", "gf2x_comm_init", "gf2x_comm_destroy", "gf2x_mul_sharded", "gf2x_mul_sharded_sim",
                  "gf2x_debug_shard_stage"):
         getattr(L, name).restype = i32
+    L.gf2x_shard_plan.argtypes = [u64, i32, ctypes.c_char_p, sz]
+    L.gf2x_shard_plan.restype = i32
     L.gf2x_profile_enable.argtypes = [i32]
     L.gf2x_profile_enable.restype = i32
     L.gf2x_profile_report.argtypes = [ctypes.c_char_p, sz]
@@ -220,6 +222,18 @@ def shard_words(total_words: int, nranks: int, rank: int):
     assert total_words % nranks == 0
     per = total_words // nranks
     return rank * per, (rank + 1) * per
+
+
+def gf2x_shard_plan(bits: int, nranks: int) -> dict:
+    """Host-only: geometry and exchange lists of the sharded multiply (see include/gf2x.h)."""
+    import json
+    L = load()
+    need = L.gf2x_shard_plan(bits, nranks, None, 0)
+    if need < 0:
+        raise Gf2xError(f"GF2X_EINVAL: unsupported sharded size (bits={bits}, nranks={nranks})")
+    buf = ctypes.create_string_buffer(need + 16)
+    L.gf2x_shard_plan(bits, nranks, buf, len(buf))
+    return json.loads(buf.value.decode())
 
 
 def gf2x_release(device: int = 0):

@@ -178,8 +178,14 @@ static thread_local std::string g_last_error;
 struct ProfRec {
     std::string name;
     cudaEvent_t beg, end;
-    double bytes;
+    double bytes;   // algorithmic HBM bytes of the launch
+    double ops;     // algorithmic ALU-pipe lane instructions of the launch (ALU-bound designs), else 0
 };
+// Designed ALU-pipe instructions (SASS, per lane) of the arithmetic cores, counted from cuobjdump:
+//   one bit-sliced TGF(2^32) product (bs_mul32, 32 elements): 896 LOP3
+//   one table butterfly of k_fft2 (4 limbs x (8 PRMT + 2 nibble masks + 2 shifts + 4 XOR3) + 4 XOR): 68
+#define OPS_BS_MUL32 896.0
+#define OPS_M4R_BUTTERFLY 68.0
 static thread_local bool g_prof_on = false;
 static thread_local std::vector<ProfRec> g_prof;
 static thread_local std::vector<cudaEvent_t> g_event_pool;
@@ -205,9 +211,9 @@ static void prof_clear() {
 struct ProfScope {
     int idx = -1;
     cudaStream_t st;
-    ProfScope(const char* name, double bytes, cudaStream_t s) : st(s) {
+    ProfScope(const char* name, double bytes, cudaStream_t s, double ops = 0.0) : st(s) {
         if (!g_prof_on) return;
-        ProfRec r{name, prof_event(), prof_event(), bytes};
+        ProfRec r{name, prof_event(), prof_event(), bytes, ops};
         cudaEventRecord(r.beg, st);
         g_prof.push_back(r);
         idx = (int)g_prof.size() - 1;
@@ -674,7 +680,8 @@ static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* 
     const int occ = sm > 113 * 1024 ? 1 : (sm > 75 * 1024 ? 2 : 3);
     const int grid = grid_for(ntiles, 1, ds->sm_count, occ);
     const double bytes = (double)prm.batch * (psi ? (double)src_per * 8 : (double)P.N * 16) + (double)prm.batch * P.N * 16;
-    ProfScope ps(inv ? "k_fft<inv>" : (psi ? "k_fft<psi>" : "k_fft"), bytes, st);
+    const double bfly = (double)prm.batch * (double)(P.N / 2) * R;
+    ProfScope ps(inv ? "k_fft<inv>" : (psi ? "k_fft<psi>" : "k_fft"), bytes, st, bfly * OPS_M4R_BUTTERFLY);
     if (inv) k_fft2<true, false><<<grid, FFT_THREADS, sm, st>>>(prm);
     else if (psi) k_fft2<false, true><<<grid, FFT_THREADS, sm, st>>>(prm);
     else k_fft2<false, false><<<grid, FFT_THREADS, sm, st>>>(prm);
@@ -743,7 +750,9 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         bp.m = P.m; bp.L = P.fft.back().layers;
         bp.map = IdxMap{0, 0, 0};
         bp.mode = stop_stage == 2 ? 1 : (stop_stage == 3 ? 3 : 7);
-        ProfScope ps("k_bottom", 48.0 * P.N * P.batch, st);
+        // bit-sliced products per 2^11-element tile: 2L forward + L inverse layers x 128, pointmul 768
+        const double prods = (double)bp.ntiles * (3.0 * bp.L * 128.0 + 768.0);
+        ProfScope ps("k_bottom", 48.0 * P.N * P.batch, st, prods * OPS_BS_MUL32);
         k_bottom<<<grid_for(bp.ntiles, 1, smc, 2), BT_THREADS, bottom_smem(), st>>>(bp);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("bottom launch: ") + cudaGetErrorString(e));
@@ -978,6 +987,42 @@ gf2x_status gf2x_debug_shard_stage(const uint64_t* a, const uint64_t* b, uint64_
     return sharded_sim(a, b, bits, nullptr, nranks, stream, stage, out);
 }
 
+int gf2x_shard_plan(uint64_t bits, int nranks, char* buf, size_t cap) {
+    ShardGeom S;
+    if (shard_geom(bits, nranks, S) != GF2X_OK) return -1;
+    ShardXfers X;
+    shard_xfers(S, X);
+    static const char* bn[SB_COUNT] = {"A", "B", "W", "T", "X", "HALO"};
+    auto list = [&](const std::vector<Xfer>& xs) {
+        std::string o = "[";
+        for (size_t i = 0; i < xs.size(); i++) {
+            char t[192];
+            snprintf(t, sizeof(t), "%s[%d, %d, \"%s\", \"%s\", %zu, %zu, %zu]", i ? ", " : "", xs[i].src, xs[i].dst,
+                     bn[xs[i].sb], bn[xs[i].db], xs[i].soff, xs[i].doff, xs[i].bytes);
+            o += t;
+        }
+        return o + "]";
+    };
+    char head[512];
+    snprintf(head, sizeof(head),
+             "{\"G\": %d, \"g\": %d, \"m\": %d, \"mloc\": %d, \"K\": %d, \"n\": %llu, \"N\": %llu, \"Nloc\": %llu, "
+             "\"buffers\": {\"A\": %zu, \"B\": %zu, \"W\": %zu, \"T\": %zu, \"X\": %zu, \"HALO\": %zu}, \"top_cross\": [",
+             S.G, S.g, S.m, S.mloc, S.K, (unsigned long long)S.n, (unsigned long long)S.N, (unsigned long long)S.Nloc,
+             S.off[SB_B] - S.off[SB_A], S.off[SB_W] - S.off[SB_B], S.off[SB_T] - S.off[SB_W], S.off[SB_X] - S.off[SB_T],
+             S.off[SB_HALO] - S.off[SB_X], S.bytes - S.off[SB_HALO]);
+    std::string out = head;
+    for (size_t i = 0; i < S.top_cross.size(); i++) out += (i ? ", " : "") + std::to_string(S.top_cross[i]);
+    out += "], \"a2a_fwd\": " + list(X.a2a_fwd) + ", \"a2a_back\": " + list(X.a2a_back) + ", \"cross\": [";
+    for (size_t i = 0; i < X.cross.size(); i++) out += (i ? ", " : "") + list(X.cross[i]);
+    out += "], \"halo\": " + list(X.halo) + "}";
+    if (buf && cap) {
+        const size_t n = std::min(cap - 1, out.size());
+        memcpy(buf, out.data(), n);
+        buf[n] = 0;
+    }
+    return (int)out.size() + 1;
+}
+
 gf2x_status gf2x_profile_enable(int on) {
     prof_clear();
     g_prof_on = on != 0;
@@ -988,6 +1033,7 @@ int gf2x_profile_report(char* buf, size_t cap) {
     // aggregate by kernel name, in first-seen order
     std::vector<std::string> order;
     std::map<std::string, std::pair<int, std::pair<double, double>>> agg;
+    std::map<std::string, double> aops;
     for (auto& r : g_prof) {
         cudaEventSynchronize(r.end);
         float ms = 0.f;
@@ -1001,13 +1047,14 @@ int gf2x_profile_report(char* buf, size_t cap) {
         a.first += 1;
         a.second.first += ms;
         a.second.second += r.bytes;
+        aops[r.name] += r.ops;
     }
     std::string out = "[";
     for (size_t i = 0; i < order.size(); i++) {
         auto& a = agg[order[i]];
         char tmp[256];
-        snprintf(tmp, sizeof(tmp), "%s{\"kernel\": \"%s\", \"launches\": %d, \"ms\": %.6f, \"bytes\": %.0f}",
-                 i ? ", " : "", order[i].c_str(), a.first, a.second.first, a.second.second);
+        snprintf(tmp, sizeof(tmp), "%s{\"kernel\": \"%s\", \"launches\": %d, \"ms\": %.6f, \"bytes\": %.0f, \"alu_ops\": %.0f}",
+                 i ? ", " : "", order[i].c_str(), a.first, a.second.first, a.second.second, aops[order[i]]);
         out += tmp;
     }
     out += "]";

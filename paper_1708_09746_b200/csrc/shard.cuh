@@ -258,12 +258,48 @@ struct ShardExec {
     bool owns(int r) const { return sim || r == comm->rank; }
 };
 
+// Every exchange of the sharded multiply as transfer lists (host only; every rank derives the same
+// lists from (bits, G)).  Byte offsets into the per-rank buffers of ShardGeom.
+struct ShardXfers {
+    std::vector<Xfer> a2a_fwd;                 // blocked -> t-sliced: rank r's chunk q -> rank q's T chunk r
+    std::vector<Xfer> a2a_back;                // t-sliced -> blocked: rank q's T chunk r -> rank r's X chunk q
+    std::vector<std::vector<Xfer>> cross;      // one per level in ShardGeom::top_cross (ascending)
+    std::vector<Xfer> halo;                    // last tower element of rank r-1 -> rank r
+};
+static void shard_xfers(const ShardGeom& S, ShardXfers& X) {
+    const int G = S.G;
+    const uint64_t chunk = S.Nloc >> S.g, Nloc = S.Nloc;
+    X.a2a_fwd.clear(); X.a2a_back.clear(); X.cross.clear(); X.halo.clear();
+    for (int r = 0; r < G; r++)
+        for (int q = 0; q < G; q++) X.a2a_fwd.push_back({r, q, SB_X, SB_T, q * chunk * 16, r * chunk * 16, chunk * 16});
+    for (int q = 0; q < G; q++)
+        for (int r = 0; r < G; r++) X.a2a_back.push_back({q, r, SB_T, SB_X, r * chunk * 16, q * chunk * 16, chunk * 16});
+    for (int l : S.top_cross) {
+        const int Sb = 1 << (l - S.mloc);          // blocks per segment
+        const uint64_t u = 1ull << (l - 1 - S.K);  // window unit
+        std::vector<Xfer> xs;
+        for (int base = 0; base < G; base += Sb) {
+            for (int p = 0; p < Sb / 2; p++) {
+                // phase B^-1 sources for rank base+p: t + d = t + h - u
+                xs.push_back({base + p + Sb / 2, base + p, SB_W, SB_X, 0, u * 16, (Nloc - u) * 16});
+                if (p >= 1) xs.push_back({base + p + Sb / 2 - 1, base + p, SB_W, SB_X, (Nloc - u) * 16, 0, u * 16});
+            }
+            // phase A^-1 sources: [2h-u, 2h) -> rank base + Sb/2, targets [0, u)
+            xs.push_back({base + Sb - 1, base + Sb / 2, SB_W, SB_T, (Nloc - u) * 16, 0, u * 16});
+        }
+        X.cross.push_back(xs);
+    }
+    for (int r = 1; r < G; r++) X.halo.push_back({r - 1, r, SB_W, SB_HALO, (Nloc - 1) * 16, 0, 16});
+}
+
 // debug_stage (simulation only): 1 = stop after the forward FFT (copy every rank's Wa block to dbg),
 // 5 = stop after the whole iBasisCvt (copy the blocked W blocks).  dbg: N tower elements.
 static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds, const DevTables* host_tabs, uint64_t bits,
                                int debug_stage = 0, uint4* dbg = nullptr) {
     gf2x_status s;
     const int G = S.G, g = S.g, smc = ds->sm_count;
+    ShardXfers XF;
+    shard_xfers(S, XF);
     cudaStream_t st = X.st;
     const uint64_t Nloc = S.Nloc, chunk = Nloc >> g;
     std::vector<int> mine;
@@ -301,8 +337,8 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
         uint64_t* A = (uint64_t*)R.buf[SB_A];
         uint64_t* B = (uint64_t*)R.buf[SB_B];
         uint4* W = (uint4*)R.buf[SB_W];
-        k_prep<<<grid_for(S.n, 256, smc, 8), 256, 0, st>>>(A, S.n, bits, S.p, 1, A);
-        k_prep<<<grid_for(S.n, 256, smc, 8), 256, 0, st>>>(B, S.n, bits, S.p, 1, B);
+        { ProfScope ps("k_prep", 16.0 * S.n, st); k_prep<<<grid_for(S.n, 256, smc, 8), 256, 0, st>>>(A, S.n, bits, S.p, 1, A); }
+        { ProfScope ps("k_prep", 16.0 * S.n, st); k_prep<<<grid_for(S.n, 256, smc, 8), 256, 0, st>>>(B, S.n, bits, S.p, 1, B); }
         if ((s = last("shard prep")) != GF2X_OK) return s;
         if ((s = run_cvt<uint64_t>(S.cvt_fwd, A, S.p, 1, false, smc, st)) != GF2X_OK) return s;
         if ((s = run_cvt<uint64_t>(S.cvt_fwd, B, S.p, 1, false, smc, st)) != GF2X_OK) return s;
@@ -320,9 +356,9 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
         const size_t sm = (size_t)tp.J * 512 + 8 * 256 * 16;
         cudaFuncSetAttribute(k_shard_top, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         tp.S = A; tp.W = W;
-        k_shard_top<<<grid_for(Nloc, 256, smc, 2), 256, sm, st>>>(tp);
+        { ProfScope ps("k_shard_top", 8.0 * tp.J * Nloc + 16.0 * Nloc, st); k_shard_top<<<grid_for(Nloc, 256, smc, 2), 256, sm, st>>>(tp); }
         tp.S = B; tp.W = W + Nloc;
-        k_shard_top<<<grid_for(Nloc, 256, smc, 2), 256, sm, st>>>(tp);
+        { ProfScope ps("k_shard_top", 8.0 * tp.J * Nloc + 16.0 * Nloc, st); k_shard_top<<<grid_for(Nloc, 256, smc, 2), 256, sm, st>>>(tp); }
         if ((s = last("shard top")) != GF2X_OK) return s;
         // ---- local FFT layers [6, mloc) of both operands, bottom kernel, local iFFT layers
         const IdxMap map{S.mloc, g, (uint32_t)r};
@@ -335,7 +371,11 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
         bp.ntiles = (Nloc + (1ull << BT_BITS) - 1) >> BT_BITS;
         bp.m = S.mloc; bp.L = S.fft.back().layers; bp.mode = debug_stage == 1 ? 1 : 7;
         bp.map = map;
-        k_bottom<<<grid_for(bp.ntiles, 1, smc, 2), BT_THREADS, bottom_smem(), st>>>(bp);
+        {
+            const double prods = (double)bp.ntiles * (3.0 * bp.L * 128.0 + 768.0);
+            ProfScope ps("k_bottom", 48.0 * Nloc, st, prods * OPS_BS_MUL32);
+            k_bottom<<<grid_for(bp.ntiles, 1, smc, 2), BT_THREADS, bottom_smem(), st>>>(bp);
+        }
         if ((s = last("shard bottom")) != GF2X_OK) return s;
         if (debug_stage == 1) {
             cudaMemcpyAsync(dbg + r * Nloc, W, Nloc * 16, cudaMemcpyDeviceToDevice, st);
@@ -345,17 +385,12 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
             if ((s = launch_fft(S.fft[i], true, false, W, Nloc, W, S.lp, ds, st, 1, map)) != GF2X_OK) return s;
         // ---- inner iBasisCvt (windows in [0, K)) locally, then pack by destination rank
         if ((s = run_cvt<uint4>(S.inner, W, S.mloc, 1, true, smc, st)) != GF2X_OK) return s;
-        k_pack<<<grid_for(Nloc, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_X], Nloc, g, S.K, 0);
+        { ProfScope ps("k_pack", 32.0 * Nloc, st); k_pack<<<grid_for(Nloc, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_X], Nloc, g, S.K, 0); }
         if ((s = last("shard pack")) != GF2X_OK) return s;
     }
     if (debug_stage == 1) return GF2X_OK;
     // ---- all-to-all: rank r's chunk q -> rank q's T at chunk r
-    {
-        std::vector<Xfer> xs;
-        for (int r = 0; r < G; r++)
-            for (int q = 0; q < G; q++) xs.push_back({r, q, SB_X, SB_T, q * chunk * 16, r * chunk * 16, chunk * 16});
-        if ((s = X.run(xs)) != GF2X_OK) return s;
-    }
+    if ((s = X.run(XF.a2a_fwd)) != GF2X_OK) return s;
     // ---- t-sliced: top g iFFT layers, outer iBasisCvt
     for (int q : mine) {
         RankCtx& R = X.local(q);
@@ -366,42 +401,30 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
         if ((s = run_cvt<uint4>(S.outer, T, S.mloc, 1, true, smc, st)) != GF2X_OK) return s;
     }
     // ---- all-to-all back: rank q's T chunk r -> rank r's X chunk q, unpack
-    {
-        std::vector<Xfer> xs;
-        for (int q = 0; q < G; q++)
-            for (int r = 0; r < G; r++) xs.push_back({q, r, SB_T, SB_X, r * chunk * 16, q * chunk * 16, chunk * 16});
-        if ((s = X.run(xs)) != GF2X_OK) return s;
-    }
+    if ((s = X.run(XF.a2a_back)) != GF2X_OK) return s;
     for (int r : mine) {
         RankCtx& R = X.local(r);
         uint4* W = (uint4*)R.buf[SB_W];
-        k_pack<<<grid_for(Nloc, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_X], Nloc, g, S.K, 1);
+        { ProfScope ps("k_pack", 32.0 * Nloc, st); k_pack<<<grid_for(Nloc, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_X], Nloc, g, S.K, 1); }
         if ((s = last("shard unpack")) != GF2X_OK) return s;
         if ((s = run_cvt<uint4>(S.top_local, W, S.mloc, 1, true, smc, st)) != GF2X_OK) return s;
     }
     // ---- top Taylor steps spanning ranks, ascending level (inverse order)
-    for (int l : S.top_cross) {
+    for (size_t li = 0; li < S.top_cross.size(); li++) {
+        const int l = S.top_cross[li];
         const int Sb = 1 << (l - S.mloc);          // blocks per segment
         const uint64_t u = 1ull << (l - 1 - S.K);  // window unit
-        std::vector<Xfer> xs;
-        for (int base = 0; base < G; base += Sb) {
-            for (int p = 0; p < Sb / 2; p++) {
-                // phase B^-1 sources for rank base+p: t + d = t + h - u
-                xs.push_back({base + p + Sb / 2, base + p, SB_W, SB_X, 0, u * 16, (Nloc - u) * 16});
-                if (p >= 1) xs.push_back({base + p + Sb / 2 - 1, base + p, SB_W, SB_X, (Nloc - u) * 16, 0, u * 16});
-            }
-            // phase A^-1 sources: [2h-u, 2h) -> rank base + Sb/2, targets [0, u)
-            xs.push_back({base + Sb - 1, base + Sb / 2, SB_W, SB_T, (Nloc - u) * 16, 0, u * 16});
-        }
-        if ((s = X.run(xs)) != GF2X_OK) return s;
+        if ((s = X.run(XF.cross[li])) != GF2X_OK) return s;
         for (int r : mine) {
             RankCtx& R = X.local(r);
             uint4* W = (uint4*)R.buf[SB_W];
             const int p = r % Sb;
             if (p < Sb / 2) {
                 const uint64_t lo = (p == 0) ? u : 0;
+                ProfScope ps("k_xor_range", 48.0 * (Nloc - lo), st);
                 k_xor_range<<<grid_for(Nloc - lo, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_X], lo, Nloc);
             } else if (p == Sb / 2) {
+                ProfScope ps("k_xor_range", 48.0 * u, st);
                 k_xor_range<<<grid_for(u, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_T], 0, u);
             }
             if ((s = last("shard cross step")) != GF2X_OK) return s;
@@ -412,13 +435,10 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
         return GF2X_OK;
     }
     // ---- halo: last element of rank r-1 -> rank r; changeRepr^-1 + InterleavedCombine
-    {
-        std::vector<Xfer> xs;
-        for (int r = 1; r < G; r++) xs.push_back({r - 1, r, SB_W, SB_HALO, (Nloc - 1) * 16, 0, 16});
-        if ((s = X.run(xs)) != GF2X_OK) return s;
-    }
+    if ((s = X.run(XF.halo)) != GF2X_OK) return s;
     for (int r : mine) {
         RankCtx& R = X.local(r);
+        ProfScope ps("k_ipsi_combine", 32.0 * Nloc, st);
         k_ipsi_combine<<<grid_for(Nloc, 256, smc, 2), 256, 16 * 256 * 16, st>>>(
             (const uint4*)R.buf[SB_W], ds->tabs, Nloc, Nloc, 1, R.c_shard, r ? (const uint4*)R.buf[SB_HALO] : nullptr);
         if ((s = last("shard combine")) != GF2X_OK) return s;
