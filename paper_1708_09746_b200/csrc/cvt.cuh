@@ -132,70 +132,90 @@ struct CvtResParams {
     int C_log, rows;          // 2^C_log classes per tile; rows = floor((2^q - 1) / M) + 1
 };
 
+#define RES_THREADS 256
 template <typename T>
-__global__ void __launch_bounds__(512) k_cvt_res(CvtResParams p) {
+__device__ __forceinline__ void cp_async_unit(T* dst, const T* src) {
+    if (sizeof(T) == 16) cp_async16(dst, src);
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Thread (column c = tid mod C, row lane rl = tid / C) owns rows rl, rl + RS, ... (RS = threads / C) of
+// its class; double-buffered: the next tile's rows are prefetched with cp.async during the steps.
+template <typename T>
+__global__ void __launch_bounds__(RES_THREADS, 3) k_cvt_res(CvtResParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    T* tile = reinterpret_cast<T*>(smem_raw);
     T* data = reinterpret_cast<T*>(p.data);
     const uint32_t M = (1u << p.K) - 1;
-    const uint32_t C = 1u << p.C_log, cmask = C - 1;
+    const uint32_t C = 1u << p.C_log;
     const uint32_t nrb = (M + C - 1) >> p.C_log;
     const uint32_t span = 1u << p.q;                       // q <= 31
     const uint64_t chunks = (p.units_per_pair >> p.q) * p.batch;
     const uint64_t ntiles = chunks * nrb;
     const uint32_t nslots = (uint32_t)p.rows << p.C_log;
+    const uint32_t bufsz = (nslots * (uint32_t)sizeof(T) + 127) & ~127u;
     const int nsteps = p.lg_hi - p.lg_lo + 1;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint32_t c = threadIdx.x & (C - 1), rl = threadIdx.x >> p.C_log, RS = blockDim.x >> p.C_log;
+    auto geom = [&](uint64_t t, T*& dp, uint32_t& c0, uint32_t& cn) {
         const uint64_t chunk = t / nrb;
-        const uint32_t c0 = (uint32_t)(t - chunk * nrb) << p.C_log;
-        const uint32_t cn = min(C, M - c0);
-        T* dp = data + chunk * span;
-        for (uint32_t s0 = threadIdx.x; s0 < nslots; s0 += 8 * blockDim.x) {
-            T tmp[8];
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const uint32_t s = s0 + u * blockDim.x;
-                const uint32_t c = s & cmask, i = (s >> p.C_log) * M + c0 + c;
-                if (s < nslots && c < cn && i < span) tmp[u] = dp[i];
+        c0 = (uint32_t)(t - chunk * nrb) << p.C_log;
+        cn = min(C, M - c0);
+        dp = data + chunk * span;
+    };
+    auto prefetch = [&](uint64_t t, T* buf) {
+        T* dp; uint32_t c0, cn;
+        geom(t, dp, c0, cn);
+        if (c < cn)
+            for (uint32_t r = rl; r < (uint32_t)p.rows; r += RS) {
+                const uint32_t i = r * M + c0 + c;
+                if (i < span) cp_async_unit<T>(buf + ((r << p.C_log) | c), dp + i);
             }
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const uint32_t s = s0 + u * blockDim.x;
-                const uint32_t c = s & cmask, i = (s >> p.C_log) * M + c0 + c;
-                if (s < nslots && c < cn && i < span) tile[s] = tmp[u];
-            }
-        }
+    };
+    if (blockIdx.x < ntiles) prefetch(blockIdx.x, reinterpret_cast<T*>(smem_raw));
+    cp_async_commit();
+    int k = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, k++) {
+        if (t + gridDim.x < ntiles) prefetch(t + gridDim.x, reinterpret_cast<T*>(smem_raw + ((k + 1) & 1) * bufsz));
+        cp_async_commit();
+        cp_async_wait<1>();
         __syncthreads();
+        T* tile = reinterpret_cast<T*>(smem_raw + (k & 1) * bufsz);
+        T* dp; uint32_t c0, cn;
+        geom(t, dp, c0, cn);
+        const bool colok = c < cn;
         for (int o = 0; o < nsteps; o++) {
             const int lg = p.inverse ? p.lg_lo + o : p.lg_hi - o;
             const uint32_t h = 1u << (lg - 1), u = h >> p.K, segm = (2u << (lg - 1)) - 1;
             const uint32_t off = u << p.C_log;
-            for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
-                const uint32_t c = s & cmask, i = (s >> p.C_log) * M + c0 + c;
-                const uint32_t pos = i & segm;
-                if (c >= cn || i >= span || pos < u || pos >= h) continue;
-                if (pos < 2 * u) {   // also owns the phase-A target s + off
-                    if (!p.inverse) {
-                        const T a = xor_t<T>(tile[s + off], tile[s + 2 * off]);
-                        tile[s + off] = a;
-                        tile[s] = xor_t<T>(tile[s], a);
+            if (colok)
+                for (uint32_t r = rl; r < (uint32_t)p.rows; r += RS) {
+                    const uint32_t i = r * M + c0 + c;
+                    const uint32_t pos = i & segm;
+                    if (i >= span || pos - u >= h - u) continue;   // targets: position in [u, h)
+                    const uint32_t s = (r << p.C_log) | c;
+                    if (pos < 2 * u) {   // also owns the phase-A target s + off
+                        if (!p.inverse) {
+                            const T a = xor_t<T>(tile[s + off], tile[s + 2 * off]);
+                            tile[s + off] = a;
+                            tile[s] = xor_t<T>(tile[s], a);
+                        } else {
+                            const T a = tile[s + off];
+                            tile[s] = xor_t<T>(tile[s], a);
+                            tile[s + off] = xor_t<T>(a, tile[s + 2 * off]);
+                        }
                     } else {
-                        const T a = tile[s + off];
-                        tile[s] = xor_t<T>(tile[s], a);
-                        tile[s + off] = xor_t<T>(a, tile[s + 2 * off]);
+                        tile[s] = xor_t<T>(tile[s], tile[s + off]);
                     }
-                } else {
-                    tile[s] = xor_t<T>(tile[s], tile[s + off]);
                 }
-            }
             __syncthreads();
         }
-        for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
-            const uint32_t c = s & cmask, i = (s >> p.C_log) * M + c0 + c;
-            if (c < cn && i < span) dp[i] = tile[s];
-        }
+        if (colok)
+            for (uint32_t r = rl; r < (uint32_t)p.rows; r += RS) {
+                const uint32_t i = r * M + c0 + c;
+                if (i < span) dp[i] = tile[(r << p.C_log) | c];
+            }
         __syncthreads();
     }
+    cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -291,45 +311,55 @@ __device__ __forceinline__ void rb_phase(uint32_t* s32, const CvtRbParams& p, in
     }
 }
 
-#define RB_THREADS 256
-// 2 CTAs per SM; global loads staged through registers, RB_UNR in flight per thread.  (A variant
-// with cp.async.bulk row copies issued by one warp measured 3x slower on B200: 256-byte bulk copies
-// are issue-bound.)  p.inverse bit 1 (GF2X_RB_NOPHASE, measurement only) skips the phases.
-#define RB_UNR 8
+#define RB_THREADS 128
+// Double-buffered: the next tile is prefetched with cp.async (16-byte pieces of the tile's contiguous
+// runs, straight into shared memory) while the current one runs its phases; tiles are stored from
+// shared memory with ordinary vector stores.  (A variant with cp.async.bulk row copies issued by one
+// warp measured 3x slower on B200: 256-byte bulk copies are issue-bound.)  p.inverse bit 1
+// (GF2X_RB_NOPHASE, measurement only) skips the phases.
+template <typename T>
+__device__ __forceinline__ void rb_slot(const CvtRbParams& p, uint32_t s, uint64_t base, uint32_t& sm, uint64_t& g) {
+    const uint32_t nrows = 1u << p.R, ncols = 1u << p.C;
+    if (p.mode) { const uint32_t row = s & (nrows - 1), col = s >> p.R; sm = col * (nrows + RB_PAD(T)) + row; g = base + s; }
+    else { const uint32_t col = s & (ncols - 1), row = s >> p.C; sm = s; g = base + col + ((uint64_t)row << p.r_lo); }
+}
+
 template <typename T, int WB>
-__global__ void __launch_bounds__(RB_THREADS, 2) k_cvt_rb(CvtRbParams p) {
+__global__ void __launch_bounds__(RB_THREADS, 3) k_cvt_rb(CvtRbParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    T* tile = reinterpret_cast<T*>(smem_raw);
-    uint32_t* s32 = reinterpret_cast<uint32_t*>(smem_raw);
-    T* data = reinterpret_cast<T*>(p.data);
+    constexpr uint32_t EPC = 16 / sizeof(T);   // units per 16-byte copy
     const uint32_t ncols = 1u << p.C, nrows = 1u << p.R, nslots = ncols << p.R;
-    const uint32_t cst = nrows + RB_PAD(T);
+    const uint32_t bufsz = ((ncols * (nrows + (p.mode ? RB_PAD(T) : 0)) * (uint32_t)sizeof(T)) + 127) & ~127u;
+    // (buffers are addressed from smem_raw directly so the compiler emits LDS/STS, not generic LD/ST)
+    T* data = reinterpret_cast<T*>(p.data);
     const uint64_t tiles_per_pair = p.units_per_pair >> (p.R + p.C);
     const uint64_t ntiles = tiles_per_pair * p.batch;
     const int midbits = p.mode ? 0 : p.r_lo - p.C;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const uint64_t pair = t / tiles_per_pair;
-        const uint64_t tt = t - pair * tiles_per_pair;
-        T* dp = data + pair * p.units_per_pair;
-        uint64_t base;
+    auto tile_at = [&](uint64_t t, T*& dp, uint64_t& base) {
+        const uint64_t pair = t / tiles_per_pair, tt = t - pair * tiles_per_pair;
+        dp = data + pair * p.units_per_pair;
         if (p.mode) base = tt << (p.R + p.C);
         else base = ((tt & ((1ull << midbits) - 1)) << p.C) | ((tt >> midbits) << (p.r_lo + p.R));
-        for (uint32_t s0 = threadIdx.x; s0 < nslots; s0 += RB_UNR * blockDim.x) {
-            T tmp[RB_UNR];
-            uint32_t smi[RB_UNR];
-#pragma unroll
-            for (int u = 0; u < RB_UNR; u++) {
-                const uint32_t s = s0 + u * blockDim.x;
-                uint64_t g;
-                if (p.mode) { const uint32_t row = s & (nrows - 1), col = s >> p.R; smi[u] = col * cst + row; g = base + s; }
-                else { const uint32_t col = s & (ncols - 1), row = s >> p.C; smi[u] = s; g = base + col + ((uint64_t)row << p.r_lo); }
-                if (s < nslots) tmp[u] = dp[g];
-            }
-#pragma unroll
-            for (int u = 0; u < RB_UNR; u++)
-                if (s0 + u * blockDim.x < nslots) tile[smi[u]] = tmp[u];
+    };
+    auto prefetch = [&](uint64_t t, T* buf) {
+        T* dp; uint64_t base;
+        tile_at(t, dp, base);
+        for (uint32_t s = threadIdx.x * EPC; s < nslots; s += blockDim.x * EPC) {
+            uint32_t sm; uint64_t g;
+            rb_slot<T>(p, s, base, sm, g);
+            cp_async16(buf + sm, dp + g);
         }
+    };
+    if (blockIdx.x < ntiles) prefetch(blockIdx.x, reinterpret_cast<T*>(smem_raw));
+    cp_async_commit();
+    int k = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, k++) {
+        T* buf = reinterpret_cast<T*>(smem_raw + (k & 1) * bufsz);
+        if (t + gridDim.x < ntiles) prefetch(t + gridDim.x, reinterpret_cast<T*>(smem_raw + ((k + 1) & 1) * bufsz));
+        cp_async_commit();
+        cp_async_wait<1>();   // this tile's copies (all but the newest group) have landed
         __syncthreads();
+        uint32_t* s32 = reinterpret_cast<uint32_t*>(smem_raw + (k & 1) * bufsz);
         for (int i = 0; i < p.nphase * (p.inverse >> 1 ? 0 : 1); i++) {
             const int ph = (p.inverse & 1) ? p.nphase - 1 - i : i;
             int o0 = 0;
@@ -337,13 +367,14 @@ __global__ void __launch_bounds__(RB_THREADS, 2) k_cvt_rb(CvtRbParams p) {
             rb_phase<T, WB>(s32, p, ph, o0);
             __syncthreads();
         }
-        for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
-            uint32_t sm;
-            uint64_t g;
-            if (p.mode) { const uint32_t row = s & (nrows - 1), col = s >> p.R; sm = col * cst + row; g = base + s; }
-            else { const uint32_t col = s & (ncols - 1), row = s >> p.C; sm = s; g = base + col + ((uint64_t)row << p.r_lo); }
-            dp[g] = tile[sm];
+        T* dp; uint64_t base;
+        tile_at(t, dp, base);
+        for (uint32_t s = threadIdx.x * EPC; s < nslots; s += blockDim.x * EPC) {
+            uint32_t sm; uint64_t g;
+            rb_slot<T>(p, s, base, sm, g);
+            *reinterpret_cast<uint4*>(dp + g) = *reinterpret_cast<const uint4*>(buf + sm);
         }
-        __syncthreads();
+        __syncthreads();   // the buffer is refilled by the prefetch two tiles on
     }
+    cp_async_wait<0>();
 }

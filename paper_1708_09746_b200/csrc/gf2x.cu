@@ -361,7 +361,7 @@ static int plan_rb(const std::vector<CvtOp>& ops, size_t oi, int m, int unit_byt
     }
     if (e == oi) return 0;
     const int R = hi - lo;
-    const int Cw = unit_bytes == 8 ? 5 : 4;
+    const int Cw = unit_bytes == 8 ? 4 : 3;   // 128-byte rows; 32 KB tiles (double-buffered: 3 CTAs/SM)
     int mode, C;
     if (lo == 0) { mode = 1; C = std::min(Cw, m - R); }
     else if (lo >= Cw) { mode = 0; C = Cw; }
@@ -429,7 +429,7 @@ static std::vector<CvtPass> plan_cvt_ops(const std::vector<CvtOp>& ops, int m, i
     for (size_t oi = 0; oi < ops.size(); oi++) {
         const CvtOp& op = ops[oi];
         const int wlo = op.lg - 1 - op.K, whi = op.lg;
-        const bool res8 = op.K == 8 && getenv("GF2X_RES8");   // measured no faster than tile passes
+        const bool res8 = op.K == 8 && !getenv("GF2X_NO_RES8");   // K=8 runs also as residue passes (measured faster than 2 tile passes)
         if ((!fits(wlo, whi) || res8) && op.lg <= 31) {
             // a run of same-K steps at descending levels whose windows exceed a tile: one
             // residue-class pass if the rows of a class fit shared memory (else this step streams)
@@ -439,8 +439,8 @@ static std::vector<CvtPass> plan_cvt_ops(const std::vector<CvtOp>& ops, int m, i
                 e++;
             const uint64_t M = (1ull << op.K) - 1;
             const int rows = (int)(((1ull << op.lg) - 1) / M + 1);
-            int C_log = unit_bytes == 8 ? 5 : 4;   // >= 256-byte runs per row
-            const size_t budget = 100 * 1024;
+            int C_log = unit_bytes == 8 ? 4 : 3;   // >= 128-byte runs per row
+            const size_t budget = 33 * 1024;       // per buffer (k_cvt_res is double-buffered, 3 CTAs/SM)
             if ((size_t)rows * ((size_t)1 << C_log) * unit_bytes <= budget) {
                 while (C_log < 6 && (size_t)rows * ((size_t)2 << C_log) * unit_bytes <= budget) C_log++;
                 if (!passes.empty()) close(passes.back());
@@ -577,7 +577,7 @@ static gf2x_status make_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, Pl
 static int launches_of(const Plan& P) {
     const bool same = P.ma == P.mb && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8;
     int n = 2;  // prep a, b
-    n += (int)P.cvt_a.size() + (int)P.cvt_b.size() + (int)P.icvt.size();
+    n += (int)P.cvt_a.size() + (same ? 0 : (int)P.cvt_b.size()) + (int)P.icvt.size();
     const int nd = (int)P.fft.size() - 1;
     n += (same ? 1 : 2) * (nd ? nd : 1);      // forward a, b (or the changeRepr-only pass)
     n += 1;                      // fused bottom
@@ -612,9 +612,9 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
             prm.inverse = (inverse ? 1 : 0) | (getenv("GF2X_RB_NOPHASE") ? 2 : 0);   // bit 1: debug, copy only
             const size_t ncols = (size_t)1 << prm.C, nrows = (size_t)1 << prm.R;
             const size_t bufsz = (ncols * (nrows + (prm.mode ? 16 / sizeof(T) : 0)) * sizeof(T) + 127) & ~(size_t)127;
-            const size_t sm = bufsz;
+            const size_t sm = 2 * bufsz;   // double-buffered
             const uint64_t ntiles = (per >> (prm.R + prm.C)) * batch;
-            const int occ = 2;
+            const int occ = 3;
             ProfScope ps(sizeof(T) == 8 ? "k_cvt_rb<u64>" : "k_cvt_rb<u128>", 2.0 * per * batch * sizeof(T), st);
             const int g = grid_for(ntiles, 1, sm_count, occ);
             switch (p.rb_wb) {
@@ -636,12 +636,12 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
             prm.inverse = inverse ? 1 : 0;
             prm.C_log = p.C_log;
             prm.rows = p.rows;
-            const size_t sm = ((size_t)p.rows << p.C_log) * sizeof(T);
+            const size_t sm = 2 * ((((size_t)p.rows << p.C_log) * sizeof(T) + 127) & ~(size_t)127);
             const uint64_t M = (1ull << prm.K) - 1;
             const uint64_t ntiles = (per >> p.q) * batch * ((M + (1ull << p.C_log) - 1) >> p.C_log);
             const int occ = std::max(1, (int)(200 * 1024 / (sm + 1024)));
             ProfScope ps(sizeof(T) == 8 ? "k_cvt_res<u64>" : "k_cvt_res<u128>", 2.0 * per * batch * sizeof(T), st);
-            k_cvt_res<T><<<grid_for(ntiles, 1, sm_count, std::min(occ, 4)), 512, sm, st>>>(prm);
+            k_cvt_res<T><<<grid_for(ntiles, 1, sm_count, std::min(occ, 3)), RES_THREADS, sm, st>>>(prm);
         } else if (p.stream) {
             const CvtOp op = p.ops[0];
             const uint64_t n = per * batch / 2;
@@ -711,10 +711,14 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
     }
     // BasisCvt on 64-bit blocks
     // (one operand at a time: at the headline sizes each 64-bit block array fits the 126 MB L2 alone)
-    if ((s = run_cvt<uint64_t>(P.cvt_a, Sa, P.ma, P.batch, false, smc, st)) != GF2X_OK) return s;
-    if ((s = run_cvt<uint64_t>(P.cvt_b, Sb, P.mb, P.batch, false, smc, st)) != GF2X_OK) return s;
-    // Sb | Wb directly follow Sa | Wa: one FFT launch for both
+    // Sb | Wb directly follow Sa | Wa: one launch per pass for both operands
     const bool same = (P.ma == P.mb) && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8;
+    if (same) {
+        if ((s = run_cvt<uint64_t>(P.cvt_a, Sa, P.ma, 2 * P.batch, false, smc, st)) != GF2X_OK) return s;
+    } else {
+        if ((s = run_cvt<uint64_t>(P.cvt_a, Sa, P.ma, P.batch, false, smc, st)) != GF2X_OK) return s;
+        if ((s = run_cvt<uint64_t>(P.cvt_b, Sb, P.mb, P.batch, false, smc, st)) != GF2X_OK) return s;
+    }
     // changeRepr + FFT_LCH top layers (direct passes; the last planned pass is the bottom one)
     const size_t ndirect = P.fft.size() - 1;
     for (size_t i = 0; i < ndirect; i++) {
