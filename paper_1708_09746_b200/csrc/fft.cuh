@@ -93,7 +93,8 @@ template <int r, bool INV>
 __device__ __forceinline__ void fft_group(uint4* tile, uint32_t nslots, int s0, int ka, const FftParams& p, uint32_t tabs_sa) {
     const uint32_t nitems = nslots >> r;
     const int R = p.k_hi - p.k_lo;
-    for (uint32_t it = threadIdx.x; it < nitems; it += blockDim.x) {
+    uint32_t it = threadIdx.x;
+    for (; it < nitems; it += blockDim.x) {
         const uint32_t base = (it & ((1u << s0) - 1)) | ((it >> s0) << (s0 + r));
         uint4 v[1 << r];
 #pragma unroll
