@@ -72,7 +72,15 @@ def main():
     bmap = {"k_fft2<0, 1>": "k_fft<psi>", "k_fft2<0, 0>": "k_fft", "k_fft2<1, 0>": "k_fft<inv>",
             "k_cvt_tile<u64>": "k_cvt_tile<u64>", "k_cvt_tile<u128>": "k_cvt_tile<u128>",
             "k_cvt_stream<u64>": "k_cvt_stream<u64>", "k_cvt_stream<u128>": "k_cvt_stream<u128>"}
-    allt[cfg] = {bmap.get(k, k): v for k, v in traffic.items()}
+    def bname(k):
+        if k in bmap:
+            return bmap[k]
+        m = re.match(r"(k_cvt_(?:rb|res|tile|stream))<(u64|u128)", k)
+        return f"{m.group(1)}<{m.group(2)}>" if m else k
+    agg = {}
+    for k, v in traffic.items():   # per-launch average over template variants of one bench kernel name
+        agg.setdefault(bname(k), []).append((cls[k][0], v))
+    allt[cfg] = {k: sum(n * v for n, v in lst) / sum(n for n, _ in lst) for k, lst in agg.items()}
     json.dump(allt, open(tj, "w"), indent=1)
     # full capture
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -91,13 +99,19 @@ def main():
             ("launch__registers_per_thread", "regs/thread"),
             ("smsp__inst_executed.sum", "warp instructions")]
     keys = [(k, n) for k, n in keys if k in hdr]
+    stall_cols = [(i, h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""))
+                  for i, h in enumerate(hdr) if h.startswith("smsp__average_warps_issue_stalled_")
+                  and h.endswith("_per_issue_active.ratio")]
     units = dict(zip(hdr, rows[1]))
-    lines = [f"# ncu --set full, {cfg} ({tag})\n", "| kernel | grid x block | " + " | ".join(n for _, n in keys) + " |",
-             "|---|---|" + "---|" * len(keys)]
+    lines = [f"# ncu --set full, {cfg} ({tag})\n", "| kernel | grid x block | " + " | ".join(n for _, n in keys) +
+             " | top stalls (warp-cycles per issue) |", "|---|---|" + "---|" * len(keys) + "---|"]
     for r in data:
         d = dict(zip(hdr, r))
         vals = [f"{d[k]} {units.get(k, '')}".strip() for k, _ in keys]
-        lines.append(f"| {short(d['Kernel Name'])} | {d.get('Grid Size', '')} x {d.get('Block Size', '')} | " + " | ".join(vals) + " |")
+        st = sorted(((float(r[i]), n) for i, n in stall_cols if r[i] not in ("", "n/a")), reverse=True)[:4]
+        stalls = ", ".join(f"{n} {v:.2f}" for v, n in st)
+        lines.append(f"| {short(d['Kernel Name'])} | {d.get('Grid Size', '')} x {d.get('Block Size', '')} | " +
+                     " | ".join(vals) + f" | {stalls} |")
     open(os.path.join(HERE, f"{tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
     print("\n".join(out))
     print("\n".join(lines))
