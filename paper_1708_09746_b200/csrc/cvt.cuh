@@ -133,6 +133,7 @@ struct CvtResParams {
 };
 
 #define RES_THREADS 256
+#define RES_MAXJ 18   // row slots per thread: rows <= RES_MAXJ * (RES_THREADS >> C_log) (checked by the planner)
 template <typename T>
 __device__ __forceinline__ void cp_async_unit(T* dst, const T* src) {
     if (sizeof(T) == 16) cp_async16(dst, src);
@@ -182,30 +183,45 @@ __global__ void __launch_bounds__(RES_THREADS, 3) k_cvt_res(CvtResParams p) {
         T* dp; uint32_t c0, cn;
         geom(t, dp, c0, cn);
         const bool colok = c < cn;
+        // unit index of the thread's row slot j (r = rl + j RS), span if the slot is empty
+        uint32_t ii[RES_MAXJ];
+#pragma unroll
+        for (int j = 0; j < (sizeof(T) == 8 ? RES_MAXJ : 0); j++) {
+            const uint32_t r = rl + j * RS;
+            const uint32_t i = r * M + c0 + c;
+            ii[j] = (colok && r < (uint32_t)p.rows && i < span) ? i : span;
+        }
         for (int o = 0; o < nsteps; o++) {
             const int lg = p.inverse ? p.lg_lo + o : p.lg_hi - o;
             const uint32_t h = 1u << (lg - 1), u = h >> p.K, segm = (2u << (lg - 1)) - 1;
             const uint32_t off = u << p.C_log;
-            if (colok)
-                for (uint32_t r = rl; r < (uint32_t)p.rows; r += RS) {
-                    const uint32_t i = r * M + c0 + c;
-                    const uint32_t pos = i & segm;
-                    if (i >= span || pos - u >= h - u) continue;   // targets: position in [u, h)
-                    const uint32_t s = (r << p.C_log) | c;
-                    if (pos < 2 * u) {   // also owns the phase-A target s + off
-                        if (!p.inverse) {
-                            const T a = xor_t<T>(tile[s + off], tile[s + 2 * off]);
-                            tile[s + off] = a;
-                            tile[s] = xor_t<T>(tile[s], a);
-                        } else {
-                            const T a = tile[s + off];
-                            tile[s] = xor_t<T>(tile[s], a);
-                            tile[s + off] = xor_t<T>(a, tile[s + 2 * off]);
-                        }
+            // 64-bit units: unrolled over the row slots (independent chains); 128-bit units: rolled
+            // (measured: each faster for its unit size)
+            auto slot = [&](uint32_t i, uint32_t r) {
+                const uint32_t pos = i & segm;
+                if (i >= span || pos - u >= h - u) return;   // targets: position in [u, h)
+                const uint32_t s = (r << p.C_log) | c;
+                if (pos < 2 * u) {   // also owns the phase-A target s + off
+                    if (!p.inverse) {
+                        const T a = xor_t<T>(tile[s + off], tile[s + 2 * off]);
+                        tile[s + off] = a;
+                        tile[s] = xor_t<T>(tile[s], a);
                     } else {
-                        tile[s] = xor_t<T>(tile[s], tile[s + off]);
+                        const T a = tile[s + off];
+                        tile[s] = xor_t<T>(tile[s], a);
+                        tile[s + off] = xor_t<T>(a, tile[s + 2 * off]);
                     }
+                } else {
+                    tile[s] = xor_t<T>(tile[s], tile[s + off]);
                 }
+            };
+            if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                for (int j = 0; j < RES_MAXJ; j++) slot(ii[j], rl + j * RS);
+            } else {
+                if (colok)
+                    for (uint32_t r = rl; r < (uint32_t)p.rows; r += RS) slot(r * M + c0 + c, r);
+            }
             __syncthreads();
         }
         if (colok)

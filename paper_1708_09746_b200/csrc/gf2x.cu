@@ -443,6 +443,8 @@ static std::vector<CvtPass> plan_cvt_ops(const std::vector<CvtOp>& ops, int m, i
             const size_t budget = 33 * 1024;       // per buffer (k_cvt_res is double-buffered, 3 CTAs/SM)
             if ((size_t)rows * ((size_t)1 << C_log) * unit_bytes <= budget) {
                 while (C_log < 6 && (size_t)rows * ((size_t)2 << C_log) * unit_bytes <= budget) C_log++;
+                // the kernel keeps RES_MAXJ row slots per thread (RES_THREADS / 2^C_log row lanes)
+                while (C_log > 0 && rows > RES_MAXJ * (RES_THREADS >> C_log)) C_log--;
                 if (!passes.empty()) close(passes.back());
                 CvtPass P;
                 P.stream = false;
