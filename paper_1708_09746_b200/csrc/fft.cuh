@@ -89,8 +89,9 @@ __device__ __forceinline__ void bfly(uint4& x0, uint4& x1, uint32_t ta) {
 
 // One group of r consecutive layers [ka, ka+r) whose slot bits are [s0, s0+r).
 // Table id of (layer k, slot) = 2^(R-1-kk) - 1 + (row >> (kk+1)), row = slot >> c, kk = k - k_lo.
-template <int r, bool INV>
-__device__ __forceinline__ void fft_group(uint4* tile, uint32_t nslots, int s0, int ka, const FftParams& p, uint32_t tabs_sa) {
+template <int r, bool INV, bool ZS>
+__device__ __forceinline__ void fft_group(uint4* tile, uint32_t nslots, int s0, int ka, const FftParams& p, uint32_t tabs_sa,
+                                          const uint32_t* zf) {
     const uint32_t nitems = nslots >> r;
     const int R = p.k_hi - p.k_lo;
     uint32_t it = threadIdx.x;
@@ -107,7 +108,11 @@ __device__ __forceinline__ void fft_group(uint4* tile, uint32_t nslots, int s0, 
             for (int j = 0; j < (1 << r); j++) {
                 if (j & (1 << lb)) continue;
                 const uint32_t row = (base | ((uint32_t)j << s0)) >> p.c;
-                bfly<INV>(v[j], v[j | (1 << lb)], tab_addr(tabs_sa, ((1u << (R - 1 - kk)) - 1) + (row >> (kk + 1))));
+                const uint32_t id = ((1u << (R - 1 - kk)) - 1) + (row >> (kk + 1));
+                // multiplier 0 (the block at base 0: s_k vanishes on V_k, Claim 1 P:696-701): x1 ^= x0 only
+                // (warp-uniform branch; a third of the first forward / last inverse pass)
+                if (ZS && zf[id]) v[j | (1 << lb)] = xor4(v[j | (1 << lb)], v[j]);
+                else bfly<INV>(v[j], v[j | (1 << lb)], tab_addr(tabs_sa, id));
             }
         }
 #pragma unroll
@@ -115,19 +120,20 @@ __device__ __forceinline__ void fft_group(uint4* tile, uint32_t nslots, int s0, 
     }
 }
 
-template <bool INV>
+template <bool INV, bool ZS>
 __device__ __forceinline__ void fft_group_any(int r, uint4* tile, uint32_t nslots, int s0, int ka, const FftParams& p,
-                                              uint32_t tabs_sa) {
-    if (r == 3) fft_group<3, INV>(tile, nslots, s0, ka, p, tabs_sa);
-    else if (r == 2) fft_group<2, INV>(tile, nslots, s0, ka, p, tabs_sa);
-    else fft_group<1, INV>(tile, nslots, s0, ka, p, tabs_sa);
+                                              uint32_t tabs_sa, const uint32_t* zf) {
+    if (r == 3) fft_group<3, INV, ZS>(tile, nslots, s0, ka, p, tabs_sa, zf);
+    else if (r == 2) fft_group<2, INV, ZS>(tile, nslots, s0, ka, p, tabs_sa, zf);
+    else fft_group<1, INV, ZS>(tile, nslots, s0, ka, p, tabs_sa, zf);
 }
 
 // shared memory: [tables (2^R - 1) x 512 B] [psi table (PSI)] [tile]
 #ifndef FFT_MINB
 #define FFT_MINB 2
 #endif
-template <bool INV, bool PSI>
+// ZS: the pass holds the top layer (k_hi = m), where the multiplier-0 blocks are a large share
+template <bool INV, bool PSI, bool ZS>
 __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int R = p.k_hi - p.k_lo;
@@ -138,6 +144,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     uint4* tile = psit + (PSI ? 8 * 256 : 0);
     const uint32_t tabs_sa = (uint32_t)__cvta_generic_to_shared(tabs);
     if (tabs_sa & 255) __trap();  // the PRMT address fusion needs 256-byte aligned tables
+    uint32_t* zf = reinterpret_cast<uint32_t*>(tile + nslots);   // per table: multiplier == 0
     if (PSI) {
         for (uint32_t i = threadIdx.x; i < 8 * 256; i += blockDim.x) psit[i] = p.tabs->psi64[i];
         __syncthreads();   // the first tile's load reads entries other warps wrote
@@ -163,6 +170,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             const uint32_t lb = (uint32_t)(((uint64_t)base & ~((2ull << k) - 1)) | ((uint64_t)blk << (k + 1)));
             const uint32_t cst = layer_const(glayer(p.map, k), gidx(p.map, lb));
             build_tab_row(tabs + id * 128, cst, (int)(i & 7), p.tabs->wt);
+            if ((i & 7) == 0) zf[id] = cst == 0;
         }
         // ---- load
         if (PSI) {
@@ -199,7 +207,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             while (top > p.k_lo) {
                 const int r = (top - p.k_lo) >= 3 ? 3 : (top - p.k_lo);
                 const int ka = top - r;
-                fft_group_any<INV>(r, tile, nslots, p.c + ka - p.k_lo, ka, p, tabs_sa);
+                fft_group_any<INV, ZS>(r, tile, nslots, p.c + ka - p.k_lo, ka, p, tabs_sa, zf);
                 __syncthreads();
                 top = ka;
             }
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             int bot = p.k_lo;
             while (bot < p.k_hi) {
                 const int r = (p.k_hi - bot) >= 3 ? 3 : (p.k_hi - bot);
-                fft_group_any<INV>(r, tile, nslots, p.c + bot - p.k_lo, bot, p, tabs_sa);
+                fft_group_any<INV, ZS>(r, tile, nslots, p.c + bot - p.k_lo, bot, p, tabs_sa, zf);
                 __syncthreads();
                 bot += r;
             }
@@ -223,5 +231,6 @@ static size_t fft2_smem(int c, int R, bool psi) {
     size_t s = (((size_t)1 << R) - 1) * 512;
     if (psi) s += 8 * 256 * 16;
     s += ((size_t)1 << (c + R)) * 16;
+    s += 64 * 4;   // zero-multiplier flags
     return s;
 }

@@ -297,9 +297,10 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
         st.host = h;
         CUDA_TRY(cudaDeviceGetAttribute(&st.sm_count, cudaDevAttrMultiProcessorCount, dev));
         // opt-in shared memory sizes
-        CUDA_TRY(cudaFuncSetAttribute(k_fft2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_fft2<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_fft2<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+#define FFT_ATTR(a, b, c) CUDA_TRY(cudaFuncSetAttribute(k_fft2<a, b, c>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
+        FFT_ATTR(false, false, false); FFT_ATTR(false, false, true); FFT_ATTR(false, true, false); FFT_ATTR(false, true, true);
+        FFT_ATTR(true, false, false); FFT_ATTR(true, false, true);
+#undef FFT_ATTR
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_tile<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_tile<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -684,9 +685,12 @@ static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* 
     const double bytes = (double)prm.batch * (psi ? (double)src_per * 8 : (double)P.N * 16) + (double)prm.batch * P.N * 16;
     const double bfly = (double)prm.batch * (double)(P.N / 2) * R;
     ProfScope ps(inv ? "k_fft<inv>" : (psi ? "k_fft<psi>" : "k_fft"), bytes, st, bfly * OPS_M4R_BUTTERFLY);
-    if (inv) k_fft2<true, false><<<grid, FFT_THREADS, sm, st>>>(prm);
-    else if (psi) k_fft2<false, true><<<grid, FFT_THREADS, sm, st>>>(prm);
-    else k_fft2<false, false><<<grid, FFT_THREADS, sm, st>>>(prm);
+    // passes holding the top layer skip the multiplier-0 blocks (a third of their butterflies at 6 layers);
+    // elsewhere the check costs more than it saves
+    const bool zs = f.k_hi == P.m && !map.bits;
+    if (inv) { if (zs) k_fft2<true, false, true><<<grid, FFT_THREADS, sm, st>>>(prm); else k_fft2<true, false, false><<<grid, FFT_THREADS, sm, st>>>(prm); }
+    else if (psi) { if (zs) k_fft2<false, true, true><<<grid, FFT_THREADS, sm, st>>>(prm); else k_fft2<false, true, false><<<grid, FFT_THREADS, sm, st>>>(prm); }
+    else { if (zs) k_fft2<false, false, true><<<grid, FFT_THREADS, sm, st>>>(prm); else k_fft2<false, false, false><<<grid, FFT_THREADS, sm, st>>>(prm); }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("fft launch: ") + cudaGetErrorString(e));
     return GF2X_OK;
