@@ -174,16 +174,26 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
         }
         // ---- load
         if (PSI) {
+            // FFT_UNR loads in flight per thread, then changeRepr of each word (M4R-8, 8 lookups)
             const uint64_t* src = reinterpret_cast<const uint64_t*>(p.src) + pair * p.src_per;
-            for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
-                const uint32_t g = base | (s & cmask) | ((s >> p.c) << p.k_lo);
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (g < p.src_per) {
-                    const uint64_t w = src[g];
+            for (uint32_t s0 = threadIdx.x; s0 < nslots; s0 += FFT_UNR * blockDim.x) {
+                uint64_t w[FFT_UNR];
 #pragma unroll
-                    for (int ch = 0; ch < 8; ch++) v = xor4(v, psit[ch * 256 + ((w >> (8 * ch)) & 255)]);
+                for (int u = 0; u < FFT_UNR; u++) {
+                    const uint32_t s = s0 + u * blockDim.x;
+                    const uint32_t g = base | (s & cmask) | ((s >> p.c) << p.k_lo);
+                    w[u] = (s < nslots && g < p.src_per) ? src[g] : 0ull;
                 }
-                tile[s] = v;
+#pragma unroll
+                for (int u = 0; u < FFT_UNR; u++) {
+                    const uint32_t s = s0 + u * blockDim.x;
+                    uint4 v = make_uint4(0, 0, 0, 0);
+                    if (w[u]) {
+#pragma unroll
+                        for (int ch = 0; ch < 8; ch++) v = xor4(v, psit[ch * 256 + ((w[u] >> (8 * ch)) & 255)]);
+                    }
+                    if (s < nslots) tile[s] = v;
+                }
             }
         } else {
             // FFT_UNR loads per thread in flight before their shared-memory stores
