@@ -46,6 +46,7 @@ WORKLOAD = {
     "c3": "single 2^24-bit x 2^24-bit multiply (2^19 points)",
     "c4a": "single 2^28-bit x 2^28-bit multiply (2^23 points), paper headline size",
     "c4b": "single 2^29-bit x 2^29-bit multiply (2^24 points), paper headline size",
+    "c5": "single 2^32-bit x 2^32-bit multiply (2^27 points), 2^33-bit product",
 }
 
 
@@ -180,7 +181,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c4b", choices=["c1", "c2", "c3", "c4a", "c4b"])
+    ap.add_argument("--config", default="c4b", choices=["c1", "c2", "c3", "c4a", "c4b", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")

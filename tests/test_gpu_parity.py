@@ -220,3 +220,34 @@ def test_sharded_simulation_stages_match_oracle():
         for stage, key in ((1, "fft_a"), (5, "icvt")):
             got = host(G.gf2x_debug_shard_stage(dev(a), dev(b), bits, ranks, stage)).reshape(-1, 2)
             assert np.array_equal(got, st[key]), (ranks, stage)
+
+
+# ------------------------------------------------------------------ c5: 2^32-bit operands (BASELINE configs[4])
+@pytest.fixture(scope="module")
+def c5_product():
+    bits, _ = CONFIGS["c5"]
+    a, b = operand_pair(bits)
+    da, db = dev(a), dev(b)
+    c = G.gf2x_mul(da, bits, db, bits)
+    torch.cuda.synchronize()
+    return bits, a, b, da, db, c
+
+
+def test_c5_single_gpu_sampled_words_and_mod_p(c5_product):
+    bits, a, b, _, _, c = c5_product
+    got = host(c)
+    n = len(a)
+    rng = np.random.default_rng(11)
+    for w in sorted({0, n - 1, n, 2 * n - 1} | set(int(x) for x in rng.integers(0, 2 * n, size=4))):
+        assert int(got[w]) == O.mul_word(a, b, w), w
+    assert not got[-1] >> np.uint64(63)
+    assert O.check_mod_p(a, b, got, O.random_irreducibles(2, seed=5))
+
+
+def test_c5_sharded_decomposition_8_ranks(c5_product):
+    # the configuration bench.py --gpus 8 runs (8 ranks, NCCL exchanges), here as 8 virtual ranks on one
+    # device: identical to the single-GPU product word for word
+    bits, _, _, da, db, c = c5_product
+    got = G.gf2x_mul_sharded_sim(da, db, bits, 8)
+    torch.cuda.synchronize()
+    assert torch.equal(got.view(torch.int64), c.view(torch.int64))
