@@ -139,12 +139,14 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     const int R = p.k_hi - p.k_lo;
     const uint32_t nslots = 1u << (p.c + R);
     const uint32_t ntab = (1u << R) - 1;
+    // shared memory: [tables (ntab x 512 B)] [psi table (PSI)] [zero flags, 256 B] [tile] [second tile (!PSI)]
     uint32_t* tabs = reinterpret_cast<uint32_t*>(smem_raw);
     uint4* psit = reinterpret_cast<uint4*>(tabs + ntab * 128);
-    uint4* tile = psit + (PSI ? 8 * 256 : 0);
+    uint32_t* zf = reinterpret_cast<uint32_t*>(psit + (PSI ? 8 * 256 : 0));   // per table: multiplier == 0
+    const uint32_t tile_off = (uint32_t)(ntab * 512 + (PSI ? 8 * 256 * 16 : 0) + 256);
+    uint4* tile = reinterpret_cast<uint4*>(smem_raw + tile_off);
     const uint32_t tabs_sa = (uint32_t)__cvta_generic_to_shared(tabs);
     if (tabs_sa & 255) __trap();  // the PRMT address fusion needs 256-byte aligned tables
-    uint32_t* zf = reinterpret_cast<uint32_t*>(tile + nslots);   // per table: multiplier == 0
     if (PSI) {
         for (uint32_t i = threadIdx.x; i < 8 * 256; i += blockDim.x) psit[i] = p.tabs->psi64[i];
         __syncthreads();   // the first tile's load reads entries other warps wrote
@@ -155,12 +157,37 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     const uint64_t ntiles = tiles_per_pair * p.batch;
     const uint32_t cmask = (1u << p.c) - 1;
 
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const uint64_t pair = t / tiles_per_pair;
+    const int midbits = p.k_lo - p.c;
+    // base index (within the pair) of tile t: bits [c, k_lo) and >= k_hi come from tt
+    auto tile_geom = [&](uint64_t t, uint64_t& pair, uint32_t& base) {
+        pair = t / tiles_per_pair;
         const uint32_t tt = (uint32_t)(t - pair * tiles_per_pair);
-        // base index (within the pair) of the tile: bits [c, k_lo) and >= k_hi come from tt
-        const int midbits = p.k_lo - p.c;
-        const uint32_t base = ((tt & ((1u << midbits) - 1)) << p.c) | ((uint32_t)((uint64_t)(tt >> midbits) << p.k_hi));
+        base = ((tt & ((1u << midbits) - 1)) << p.c) | ((uint32_t)((uint64_t)(tt >> midbits) << p.k_hi));
+    };
+    // non-PSI passes are double-buffered: the next tile is prefetched with cp.async during this one
+    auto prefetch = [&](uint64_t t, uint32_t off) {
+        uint64_t pair; uint32_t base;
+        tile_geom(t, pair, base);
+        const uint4* src = reinterpret_cast<const uint4*>(p.src) + pair * N;
+        uint4* buf = reinterpret_cast<uint4*>(smem_raw + off);
+        for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x)
+            cp_async16(buf + s, src + (base | (s & cmask) | ((s >> p.c) << p.k_lo)));
+    };
+    const uint32_t tbytes = nslots * 16;
+    if (!PSI) {
+        if (blockIdx.x < ntiles) prefetch(blockIdx.x, tile_off);
+        cp_async_commit();
+    }
+    int kt = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, kt++) {
+        uint64_t pair;
+        uint32_t base;
+        tile_geom(t, pair, base);
+        if (!PSI) {
+            tile = reinterpret_cast<uint4*>(smem_raw + tile_off + (kt & 1) * tbytes);
+            if (t + gridDim.x < ntiles) prefetch(t + gridDim.x, tile_off + ((kt + 1) & 1) * tbytes);
+            cp_async_commit();
+        }
         // ---- tables of this tile's multipliers: id -> (layer kk, block blk)
         for (uint32_t i = threadIdx.x; i < ntab * 8; i += blockDim.x) {
             const uint32_t id = i >> 3;
@@ -196,19 +223,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
                 }
             }
         } else {
-            // FFT_UNR loads per thread in flight before their shared-memory stores
-            const uint4* src = reinterpret_cast<const uint4*>(p.src) + pair * N;
-            for (uint32_t s0 = threadIdx.x; s0 < nslots; s0 += FFT_UNR * blockDim.x) {
-                uint4 tmp[FFT_UNR];
-#pragma unroll
-                for (int u = 0; u < FFT_UNR; u++) {
-                    const uint32_t s = s0 + u * blockDim.x;
-                    if (s < nslots) tmp[u] = src[base | (s & cmask) | ((s >> p.c) << p.k_lo)];
-                }
-#pragma unroll
-                for (int u = 0; u < FFT_UNR; u++)
-                    if (s0 + u * blockDim.x < nslots) tile[s0 + u * blockDim.x] = tmp[u];
-            }
+            cp_async_wait<1>();   // this tile's copies have landed (the next tile's may be in flight)
         }
         __syncthreads();
         // ---- layers, in groups of <= 3 (forward: from the top; inverse: from the bottom)
@@ -235,12 +250,13 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
         for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) dst[base | (s & cmask) | ((s >> p.c) << p.k_lo)] = tile[s];
         __syncthreads();
     }
+    if (!PSI) cp_async_wait<0>();
 }
 
 static size_t fft2_smem(int c, int R, bool psi) {
     size_t s = (((size_t)1 << R) - 1) * 512;
     if (psi) s += 8 * 256 * 16;
-    s += ((size_t)1 << (c + R)) * 16;
-    s += 64 * 4;   // zero-multiplier flags
+    s += 256;   // zero-multiplier flags
+    s += ((size_t)1 << (c + R)) * 16 * (psi ? 1 : 2);   // non-psi passes are double-buffered
     return s;
 }
