@@ -13,6 +13,7 @@ SOURCES = [os.path.join(CSRC, "gf2x.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cuh", ".h"))] + [
     os.path.join(ROOT, "include", "gf2x.h"),
     os.path.join(HERE, "tools", "gen_bitslice.py"),
+    os.path.join(HERE, "tools", "dump_iso.cpp"),
 ]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [*os.environ.get("GF2X_NVCC_EXTRA", "").split(), "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
@@ -29,7 +30,8 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     gen = os.path.join(HERE, "tools", "gen_bitslice.py")
     out = os.path.join(CSRC, "bitslice_gen.cuh")
-    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(gen):
+    gen_deps = [gen, os.path.join(HERE, "tools", "dump_iso.cpp"), os.path.join(CSRC, "field_host.h")]
+    if force or not os.path.exists(out) or any(os.path.getmtime(out) < os.path.getmtime(d) for d in gen_deps):
         subprocess.run([sys.executable, gen], check=True)
     if force or stale():
         cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *SOURCES, "-lcudart"]

@@ -169,6 +169,125 @@ __global__ void __launch_bounds__(256) k_ipsi_combine(const uint4* __restrict__ 
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Bit-sliced changeRepr^-1 + InterleavedCombine (used when n_out = N and N is a multiple of 4096):
+// thread t of a 128-thread CTA owns the 32 consecutive elements 32t..32t+31 of a 4096-element tile.
+// Each input limb is transposed into 32 planes (bit j of the 32 elements), the fixed 128x128 GF(2)
+// matrix of changeRepr^-1 is applied as 16 generated 32x32 XOR networks (bs_ipsi_O_L, Paar-style
+// common-pair elimination: 3457 XOR per 32 elements), and the output planes are transposed back.
+// This replaces 16 random 16-byte table lookups per element (bank-conflicted LDS.128).
+// Shared memory: limb-planar tile (4 x 4096 words, XOR-swizzled so that a thread's 32-element column
+// and a warp's 32 consecutive elements are both conflict-free) + hi64 of every element (2 x 4096 words).
+// ---------------------------------------------------------------------------------------------
+#define IB_THREADS 128
+#define IB_TILE 4096
+__device__ __forceinline__ uint32_t ib_swz(uint32_t e) { return e ^ ((e >> 5) & 31); }
+
+__global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restrict__ P, const DevTables* tabs, uint64_t N,
+                                                         uint64_t batch, uint64_t* __restrict__ out) {
+    extern __shared__ __align__(1024) uint32_t ib_smem[];
+    uint32_t* S = ib_smem;                    // [4][IB_TILE] limb planes (swizzled)
+    uint32_t* H = ib_smem + 4 * IB_TILE;      // [2][IB_TILE] hi64 halves of every element (swizzled)
+    __shared__ uint64_t halo_hi;
+    const uint64_t tiles_per_pair = N / IB_TILE;
+    const uint64_t ntiles = tiles_per_pair * batch;
+    const uint32_t t = threadIdx.x;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t pair = tile / tiles_per_pair;
+        const uint64_t w0 = (tile - pair * tiles_per_pair) * IB_TILE;   // first element / word of the tile
+        const uint4* src = P + pair * N + w0;
+        // ---- load (coalesced), limb-planar
+        for (uint32_t e = t; e < IB_TILE; e += IB_THREADS) {
+            const uint4 v = src[e];
+            const uint32_t q = ib_swz(e);
+            S[q] = v.x; S[IB_TILE + q] = v.y; S[2 * IB_TILE + q] = v.z; S[3 * IB_TILE + q] = v.w;
+        }
+        // the element before the tile (its hi64 enters the tile's first output word)
+        if (t == 0) {
+            uint64_t hi = 0;
+            if (w0 > 0) {
+                uint64_t lo;
+                const uint4 pv = src[-1];
+                uint4 acc = make_uint4(0, 0, 0, 0);
+                const uint32_t w[4] = {pv.x, pv.y, pv.z, pv.w};
+                for (int L = 0; L < 4; L++)
+                    for (int b = 0; b < 4; b++) acc = xor4(acc, tabs->ipsi[(L * 4 + b) * 256 + ((w[L] >> (8 * b)) & 255)]);
+                lo = ((uint64_t)acc.y << 32) | acc.x;
+                hi = ((uint64_t)acc.w << 32) | acc.z;
+                (void)lo;
+            }
+            halo_hi = hi;
+        }
+        __syncthreads();
+        // ---- my 32 elements: limb -> planes, in place
+        const uint32_t e0 = 32 * t;
+#pragma unroll 1
+        for (int L = 0; L < 4; L++) {
+            uint32_t x[32];
+#pragma unroll
+            for (int j = 0; j < 32; j++) x[j] = S[L * IB_TILE + ib_swz(e0 + j)];
+            transpose32(x);
+#pragma unroll
+            for (int j = 0; j < 32; j++) S[L * IB_TILE + ib_swz(e0 + j)] = x[j];
+        }
+        // ---- output limbs 2, 3 (hi64): planes -> elements, kept in H
+        {
+            uint32_t a2[32], a3[32], x[32];
+#pragma unroll
+            for (int j = 0; j < 32; j++) { a2[j] = 0; a3[j] = 0; }
+#pragma unroll
+            for (int L = 0; L < 4; L++) {
+#pragma unroll
+                for (int j = 0; j < 32; j++) x[j] = S[L * IB_TILE + ib_swz(e0 + j)];
+                if (L == 0) { bs_ipsi_2_0(x, a2); bs_ipsi_3_0(x, a3); }
+                else if (L == 1) { bs_ipsi_2_1(x, a2); bs_ipsi_3_1(x, a3); }
+                else if (L == 2) { bs_ipsi_2_2(x, a2); bs_ipsi_3_2(x, a3); }
+                else { bs_ipsi_2_3(x, a2); bs_ipsi_3_3(x, a3); }
+            }
+            transpose32(a2);
+            transpose32(a3);
+#pragma unroll
+            for (int j = 0; j < 32; j++) { H[ib_swz(e0 + j)] = a2[j]; H[IB_TILE + ib_swz(e0 + j)] = a3[j]; }
+        }
+        // ---- output limbs 0, 1 (lo64)
+        uint32_t a0[32], a1[32];
+        {
+            uint32_t x[32];
+#pragma unroll
+            for (int j = 0; j < 32; j++) { a0[j] = 0; a1[j] = 0; }
+#pragma unroll
+            for (int L = 0; L < 4; L++) {
+#pragma unroll
+                for (int j = 0; j < 32; j++) x[j] = S[L * IB_TILE + ib_swz(e0 + j)];
+                if (L == 0) { bs_ipsi_0_0(x, a0); bs_ipsi_1_0(x, a1); }
+                else if (L == 1) { bs_ipsi_0_1(x, a0); bs_ipsi_1_1(x, a1); }
+                else if (L == 2) { bs_ipsi_0_2(x, a0); bs_ipsi_1_2(x, a1); }
+                else { bs_ipsi_0_3(x, a0); bs_ipsi_1_3(x, a1); }
+            }
+            transpose32(a0);
+            transpose32(a1);
+        }
+        __syncthreads();   // H complete; every thread done with the planes
+        // ---- combine: out[w] = lo64(C_w) ^ hi64(C_(w-1)); staged limb-planar in S (limbs 0, 1)
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+            const uint32_t e = e0 + j;
+            uint32_t plo, phi;
+            if (e == 0) { plo = (uint32_t)halo_hi; phi = (uint32_t)(halo_hi >> 32); }
+            else { plo = H[ib_swz(e - 1)]; phi = H[IB_TILE + ib_swz(e - 1)]; }
+            S[ib_swz(e)] = a0[j] ^ plo;
+            S[IB_TILE + ib_swz(e)] = a1[j] ^ phi;
+        }
+        __syncthreads();
+        uint64_t* dst = out + pair * N + w0;
+        for (uint32_t e = t; e < IB_TILE; e += IB_THREADS) {
+            const uint32_t q = ib_swz(e);
+            dst[e] = ((uint64_t)S[IB_TILE + q] << 32) | S[q];
+        }
+        __syncthreads();
+    }
+}
+
 // =============================================================================================
 // Host side: tables, planning, workspace, entry points
 // =============================================================================================
@@ -311,6 +430,7 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_res<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_res<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_ipsi_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_ipsi_bs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         st.tabs = d;
     }
     *dev_out = dev;
@@ -781,8 +901,14 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
     {
         const uint64_t n_out = P.na + P.nb;
         const uint64_t total = n_out * P.batch;
-        ProfScope ps("k_ipsi_combine", 16.0 * P.N * P.batch + 8.0 * total, st);
-        k_ipsi_combine<<<grid_for(total, 256, smc, 2), 256, 16 * 256 * 16, st>>>(Wa, ds->tabs, P.N, n_out, P.batch, c, nullptr);
+        if (n_out == P.N && P.N % IB_TILE == 0 && !getenv("GF2X_NO_IPSI_BS")) {
+            ProfScope ps("k_ipsi_bs", 16.0 * P.N * P.batch + 8.0 * total, st);
+            k_ipsi_bs<<<grid_for(P.N / IB_TILE * P.batch, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(Wa, ds->tabs, P.N,
+                                                                                                           P.batch, c);
+        } else {
+            ProfScope ps("k_ipsi_combine", 16.0 * P.N * P.batch + 8.0 * total, st);
+            k_ipsi_combine<<<grid_for(total, 256, smc, 2), 256, 16 * 256 * 16, st>>>(Wa, ds->tabs, P.N, n_out, P.batch, c, nullptr);
+        }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("combine launch: ") + cudaGetErrorString(e));
     }

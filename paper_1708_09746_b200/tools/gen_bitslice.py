@@ -156,6 +156,36 @@ def emit_const(fname, const, l):
     return src, P.ops
 
 
+def ipsi_columns():
+    """Columns of changeRepr^-1 (tower v_k -> polynomial basis), from the product's field_host.h
+    (compiled and run via tools/dump_iso.cpp), so both ipsi paths share one isomorphism."""
+    import subprocess
+    import tempfile
+    src = os.path.join(HERE, "dump_iso.cpp")
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "dump_iso")
+        subprocess.run(["g++", "-O2", "-o", exe, src], check=True)
+        out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout.split()
+    cols = [int(x, 16) for x in out]
+    assert len(cols) == 128
+    return cols
+
+
+def emit_ipsi_block(o_limb, i_limb, cols):
+    """acc[i] ^= bit (32 o_limb + i) of changeRepr^-1 applied to the 32 planes of input limb i_limb."""
+    P = Prog()
+    x = [f"X{i}" for i in range(32)]
+    rows = [[j for j in range(32) if (cols[32 * i_limb + j] >> (32 * o_limb + i)) & 1] for i in range(32)]
+    r = apply_linmap(P, x, rows)
+    pre = [f"const uint32_t X{i} = x[{i}];" for i in range(32)]
+    body = pre + P.lines + [f"acc[{i}] ^= {r[i]};" for i in range(32) if r[i] != "0u"]
+    name = f"bs_ipsi_{o_limb}_{i_limb}"
+    src = (f"// changeRepr^-1 block: output limb {o_limb} <- input limb {i_limb}: {P.ops['xor']} XOR\n"
+           f"GF2X_HD GF2X_INLINE void {name}(const uint32_t* __restrict__ x, uint32_t* __restrict__ acc) {{\n  "
+           + "\n  ".join(body) + "\n}\n")
+    return src, P.ops["xor"]
+
+
 def main():
     parts = ["// GENERATED by tools/gen_bitslice.py -- do not edit.\n#pragma once\n#include <stdint.h>\n"
              "#ifndef GF2X_HD\n#define GF2X_HD\n#endif\n#ifndef GF2X_INLINE\n#define GF2X_INLINE inline\n#endif\n"]
@@ -166,9 +196,16 @@ def main():
     parts.append(s2)
     s3, _ = emit_const("bs_mul_v31sq", tmul(v31, v31, 5), 5)
     parts.append(s3)
+    cols = ipsi_columns()
+    nx = 0
+    for o in range(4):
+        for i in range(4):
+            src, n = emit_ipsi_block(o, i, cols)
+            parts.append(src)
+            nx += n
     with open(OUT, "w") as f:
         f.write("\n".join(parts))
-    print("bs_mul32 ops", ops, file=sys.stderr)
+    print("bs_mul32 ops", ops, "ipsi blocks xor", nx, file=sys.stderr)
 
 
 if __name__ == "__main__":
