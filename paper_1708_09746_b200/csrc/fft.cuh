@@ -1,10 +1,10 @@
 // fft.cuh -- FFT_LCH / iFFT_LCH passes (Alg. 1, inverse P:408), included by gf2x.cu.
 //
 // A pass handles the layers k_hi-1 .. k_lo of tiles with index bits [0,c) U [k_lo,k_hi) (c >= 5,
-// k_lo >= BOT_B) held in shared memory.  All lanes of a warp work on different columns (bits < c)
+// k_lo >= the bottom layers) held in shared memory.  All lanes of a warp work on different columns (bits < c)
 // of the same rows, so every multiplier is warp-uniform; the 2^R - 1 distinct multipliers of a tile
-// (one per block per layer) get one M4R-4 table each, built once per tile.  The layers below BOT_B
-// run in the fused bit-sliced bottom kernel (bottom.cuh).
+// (one per block per layer) get one M4R-4 table each, built once per tile.  The layers below
+// that run in the fused bit-sliced bottom kernel (bottom.cuh).
 // Inside a pass the layers run in groups of up to three: each thread holds the 2^r elements of a
 // radix-2^r sub-transform in registers, so shared-memory traffic is one load/store per element per
 // group instead of per layer.
@@ -15,7 +15,7 @@
 
 #define FFT_THREADS 256
 #define FFT_UNR 8
-#define BOT_B 6       // layers [0, BOT_B) run in the fused bit-sliced bottom kernel
+#define BOT_B_MAX 6   // at most layers [0, 6) run in the fused bit-sliced bottom kernel (planner: 5)
 
 // ---------------------------------------------------------------------------------------------
 // shared-memory M4R-4 lookups with the table base fused into the byte-permute that extracts the
@@ -139,11 +139,11 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     const int R = p.k_hi - p.k_lo;
     const uint32_t nslots = 1u << (p.c + R);
     const uint32_t ntab = (1u << R) - 1;
-    // shared memory: [tables (ntab x 512 B)] [psi table (PSI)] [zero flags, 256 B] [tile] [second tile (!PSI)]
+    // shared memory: [tables (ntab x 512 B)] [psi table (PSI)] [zero flags, 512 B] [tile] [second tile (!PSI)]
     uint32_t* tabs = reinterpret_cast<uint32_t*>(smem_raw);
     uint4* psit = reinterpret_cast<uint4*>(tabs + ntab * 128);
     uint32_t* zf = reinterpret_cast<uint32_t*>(psit + (PSI ? 8 * 256 : 0));   // per table: multiplier == 0
-    const uint32_t tile_off = (uint32_t)(ntab * 512 + (PSI ? 8 * 256 * 16 : 0) + 256);
+    const uint32_t tile_off = (uint32_t)(ntab * 512 + (PSI ? 8 * 256 * 16 : 0) + 512);
     uint4* tile = reinterpret_cast<uint4*>(smem_raw + tile_off);
     const uint32_t tabs_sa = (uint32_t)__cvta_generic_to_shared(tabs);
     if (tabs_sa & 255) __trap();  // the PRMT address fusion needs 256-byte aligned tables
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
 static size_t fft2_smem(int c, int R, bool psi) {
     size_t s = (((size_t)1 << R) - 1) * 512;
     if (psi) s += 8 * 256 * 16;
-    s += 256;   // zero-multiplier flags
+    s += 512;   // zero-multiplier flags (<= 127 tables)
     s += ((size_t)1 << (c + R)) * 16 * (psi ? 1 : 2);   // non-psi passes are double-buffered
     return s;
 }

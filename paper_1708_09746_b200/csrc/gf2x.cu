@@ -618,23 +618,36 @@ struct FftPass {
     bool bottom;
     int layers;         // bottom: layers [0, layers)
 };
-// forward order (top-down); the first pass also applies changeRepr.  High layers [BOT_B, m) are
-// split evenly into direct passes of <= 6 layers; layers [0, min(m, BOT_B)) form the bottom pass.
+// forward order (top-down); the first pass also applies changeRepr.  High layers [bot, m) are split
+// evenly into direct passes of <= 6 layers (63 M4R tables, 32 KB); layers [0, min(m, bot)) form the
+// bit-sliced bottom pass.  A table butterfly costs about half a bit-sliced one (measured), and at
+// layer 5 a 32-butterfly block still shares one multiplier per warp, so bot = 5 whenever the direct
+// layers [5, m) need no more passes than [6, m); else bot = 6 (a 7-layer pass, 127 tables, measured
+// slower than the bottom layer it saves).
+static int bot_layers(int m) {
+    if (getenv("GF2X_BOT_B")) return atoi(getenv("GF2X_BOT_B"));
+    return (m - 5 + 5) / 6 == (m - 6 + 5) / 6 ? 5 : 6;
+}
 static std::vector<FftPass> plan_fft(int m) {
     std::vector<FftPass> v;
-    const int H = m > BOT_B ? m - BOT_B : 0;
-    const int np = (H + 5) / 6;
+    const int bot = bot_layers(m);
+    static const int maxr = getenv("GF2X_MAXR") ? atoi(getenv("GF2X_MAXR")) : 6;
+    const int H = m > bot ? m - bot : 0;
+    const int np = (H + maxr - 1) / maxr;
     int top = m;
     for (int i = 0; i < np; i++) {
-        const int rem = top - BOT_B;
+        const int rem = top - bot;
         const int r = (rem + (np - i) - 1) / (np - i);  // remaining layers / remaining passes
         const int lo = top - r;
-        // 64-column tiles (double-buffered: one 160 KB CTA per SM; measured as fast as 2 CTAs of 32-column tiles)
+        // 64-column tiles (double-buffered: one 160 KB CTA per SM; measured as fast as 2 CTAs of 32-column
+        // tiles); 32 columns for the changeRepr pass and for 7-layer passes (their tables take 64 KB)
         static const int cdir = getenv("GF2X_FFT_C") ? atoi(getenv("GF2X_FFT_C")) : 6;
-        v.push_back({i == 0 ? 5 : cdir, lo, top, false, 0});
+        int c = (i == 0 || r > 6) ? 5 : cdir;
+        if (c > lo) c = lo;   // column bits must lie below the pass's layers
+        v.push_back({c, lo, top, false, 0});
         top = lo;
     }
-    v.push_back({0, 0, 0, true, m < BOT_B ? m : BOT_B});  // the fused bit-sliced bottom kernel
+    v.push_back({0, 0, 0, true, m < bot ? m : bot});  // the fused bit-sliced bottom kernel
     return v;
 }
 
@@ -862,7 +875,7 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
             if ((s = launch_fft(f, false, first, first ? (const void*)Sb : Wb, first ? (1ull << P.mb) : P.N, Wb, P, ds, st)) != GF2X_OK) return s;
         }
     }
-    if (ndirect == 0) {  // m <= BOT_B: changeRepr alone (a direct pass with no layers)
+    if (ndirect == 0) {  // m <= bot: changeRepr alone (a direct pass with no layers)
         FftPass f{P.m < 5 ? P.m : 5, P.m, P.m, false, 0};
         if (same) {
             if ((s = launch_fft(f, false, true, Sa, 1ull << P.ma, Wa, P, ds, st, 2)) != GF2X_OK) return s;

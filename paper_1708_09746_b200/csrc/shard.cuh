@@ -175,7 +175,7 @@ static gf2x_status shard_geom(uint64_t bits, int G, ShardGeom& S) {
     S.K = 1;
     while (2 * S.K <= S.m - 1) S.K *= 2;
     S.mloc = S.m - S.g;
-    if (S.mloc < S.K || S.mloc < BOT_B + 6 || S.K < S.g)
+    if (S.mloc < S.K || S.mloc < BOT_B_MAX + 6 || S.K < S.g)
         return fail(GF2X_EINVAL, "operands too small for this many ranks (need m - log2 G >= max(K, 12))");
     S.N = 1ull << S.m;
     S.Nloc = S.N >> S.g;
