@@ -76,7 +76,12 @@ def main():
         if k in bmap:
             return bmap[k]
         m = re.match(r"(k_cvt_(?:rb|res|tile|stream))<(u64|u128)", k)
-        return f"{m.group(1)}<{m.group(2)}>" if m else k
+        if m:
+            return f"{m.group(1)}<{m.group(2)}>"
+        m = re.match(r"k_fft2<(\d), (\d)", k)   # k_fft2<INV, PSI, ZS>
+        if m:
+            return "k_fft<inv>" if m.group(1) == "1" else ("k_fft<psi>" if m.group(2) == "1" else "k_fft")
+        return k
     agg = {}
     for k, v in traffic.items():   # per-launch average over template variants of one bench kernel name
         agg.setdefault(bname(k), []).append((cls[k][0], v))
