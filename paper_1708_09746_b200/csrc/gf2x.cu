@@ -11,6 +11,16 @@
 //   k_cvt_*         iBasisCvt on 128-bit tower elements
 //   k_ipsi_combine  changeRepr back + InterleavedCombine
 // Every step runs in these kernels; the host only plans passes and enqueues launches.
+//
+// Diagnostic / A-B knobs (environment, read once per process; defaults are the measured best):
+//   GF2X_DEBUG_PLAN=1    print every plan (conversion and FFT passes) to stderr
+//   GF2X_NO_RB=1         CVT(8) nodes as shared-memory tile passes instead of register-blocked passes
+//   GF2X_NO_RES8=1       K=8 Taylor runs as tile passes instead of residue-class passes
+//   GF2X_RB_NOPHASE=1    measurement only: register-blocked passes copy without converting (wrong result)
+//   GF2X_NO_IPSI_BS=1    table-driven changeRepr^-1 + combine instead of the bit-sliced kernel
+//   GF2X_FFT_C=c         column bits of the non-first FFT passes (default 6)
+//   GF2X_BOT_B=L         layers in the bit-sliced bottom kernel (default: 5 or 6 by the planner rule)
+//   GF2X_MAXR=R          maximum FFT layers per table pass (default 6)
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -342,6 +352,17 @@ struct ProfScope {
     }
 };
 
+static bool env_flag(const char* name) {
+    static std::mutex mu;
+    static std::map<std::string, bool> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(name);
+    if (it != cache.end()) return it->second;
+    const bool v = getenv(name) != nullptr;
+    cache[name] = v;
+    return v;
+}
+
 static gf2x_status fail(gf2x_status s, const std::string& msg) {
     g_last_error = msg;
     return s;
@@ -550,7 +571,7 @@ static std::vector<CvtPass> plan_cvt_ops(const std::vector<CvtOp>& ops, int m, i
     for (size_t oi = 0; oi < ops.size(); oi++) {
         const CvtOp& op = ops[oi];
         const int wlo = op.lg - 1 - op.K, whi = op.lg;
-        const bool res8 = op.K == 8 && !getenv("GF2X_NO_RES8");   // K=8 runs also as residue passes (measured faster than 2 tile passes)
+        const bool res8 = op.K == 8 && !env_flag("GF2X_NO_RES8");   // K=8 runs also as residue passes (measured faster than 2 tile passes)
         if ((!fits(wlo, whi) || res8) && op.lg <= 31) {
             // a run of same-K steps at descending levels whose windows exceed a tile: one
             // residue-class pass if the rows of a class fit shared memory (else this step streams)
@@ -581,7 +602,7 @@ static std::vector<CvtPass> plan_cvt_ops(const std::vector<CvtOp>& ops, int m, i
                 continue;
             }
         }
-        if (!getenv("GF2X_NO_RB")) {
+        if (!env_flag("GF2X_NO_RB")) {
             CvtPass P;
             const int took = plan_rb(ops, oi, m, unit_bytes, P);
             if (took > 0) {
@@ -625,7 +646,8 @@ struct FftPass {
 // layers [5, m) need no more passes than [6, m); else bot = 6 (a 7-layer pass, 127 tables, measured
 // slower than the bottom layer it saves).
 static int bot_layers(int m) {
-    if (getenv("GF2X_BOT_B")) return atoi(getenv("GF2X_BOT_B"));
+    static const int forced = getenv("GF2X_BOT_B") ? atoi(getenv("GF2X_BOT_B")) : 0;
+    if (forced) return forced;
     return (m - 5 + 5) / 6 == (m - 6 + 5) / 6 ? 5 : 6;
 }
 static std::vector<FftPass> plan_fft(int m) {
@@ -707,7 +729,7 @@ static gf2x_status make_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, Pl
     P.off_wa = align256(P.off_sb + (1ull << P.mb) * P.batch * 8);
     P.off_wb = P.off_wa + P.N * P.batch * 16;
     P.bytes = align256(P.off_wb + (P.N * P.batch + 2048) * 16);
-    if (getenv("GF2X_DEBUG_PLAN")) dump_plan(P);
+    if (env_flag("GF2X_DEBUG_PLAN")) dump_plan(P);
     return GF2X_OK;
 }
 
@@ -746,7 +768,7 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
             prm.data = data;
             prm.units_per_pair = per;
             prm.batch = batch;
-            prm.inverse = (inverse ? 1 : 0) | (getenv("GF2X_RB_NOPHASE") ? 2 : 0);   // bit 1: debug, copy only
+            prm.inverse = (inverse ? 1 : 0) | (env_flag("GF2X_RB_NOPHASE") ? 2 : 0);   // bit 1: debug, copy only
             const size_t ncols = (size_t)1 << prm.C, nrows = (size_t)1 << prm.R;
             const size_t bufsz = (ncols * (nrows + (prm.mode ? 16 / sizeof(T) : 0)) * sizeof(T) + 127) & ~(size_t)127;
             const size_t sm = 2 * bufsz;   // double-buffered
@@ -914,7 +936,7 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
     {
         const uint64_t n_out = P.na + P.nb;
         const uint64_t total = n_out * P.batch;
-        if (n_out == P.N && P.N % IB_TILE == 0 && !getenv("GF2X_NO_IPSI_BS")) {
+        if (n_out == P.N && P.N % IB_TILE == 0 && !env_flag("GF2X_NO_IPSI_BS")) {
             ProfScope ps("k_ipsi_bs", 16.0 * P.N * P.batch + 8.0 * total, st);
             k_ipsi_bs<<<grid_for(P.N / IB_TILE * P.batch, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(Wa, ds->tabs, P.N,
                                                                                                            P.batch, c);
