@@ -311,9 +311,9 @@ struct ProfRec {
     double ops;     // algorithmic ALU-pipe lane instructions of the launch (ALU-bound designs), else 0
 };
 // Designed ALU-pipe instructions (SASS, per lane) of the arithmetic cores, counted from cuobjdump:
-//   one bit-sliced TGF(2^32) product (bs_mul32, 32 elements): 896 LOP3
+//   one bit-sliced TGF(2^32) product (bs_mul32, 32 elements): 868 LOP3
 //   one table butterfly of k_fft2 (4 limbs x (8 PRMT + 2 nibble masks + 2 shifts + 4 XOR3) + 4 XOR): 68
-#define OPS_BS_MUL32 896.0
+#define OPS_BS_MUL32 868.0
 #define OPS_M4R_BUTTERFLY 68.0
 static thread_local bool g_prof_on = false;
 static thread_local std::vector<ProfRec> g_prof;
