@@ -45,12 +45,16 @@ __device__ __forceinline__ uint32_t m4r4_word_sa(uint32_t tab, uint32_t x) {
 // Row t (16 words) of the M4R-4 table of constant c: tab[16t + x] = (c v_(4t)) * x, x in GF(16).
 // c v_(4t) = w comes from the M4R-8 tables of the fixed maps c -> c v_(4t); x = sum of x_b v_b
 // (v_0 = 1, v_1 = x1, v_2 = x2, v_3 = x1 x2) so the row is the XOR-span of w, x1 w, x2 w, x1 x2 w.
+// SHARED: wt is a shared-memory copy (plain loads); else the global table (read-only cache)
+template <bool SHARED = false>
 __device__ __forceinline__ void build_tab_row(uint32_t* tab, uint32_t c, int t, const uint32_t* __restrict__ wt) {
     uint32_t w = c;
     if (t) {
         const uint32_t* T = wt + (t - 1) * 1024;
-        w = __ldg(T + (c & 255)) ^ __ldg(T + 256 + ((c >> 8) & 255)) ^ __ldg(T + 512 + ((c >> 16) & 255)) ^
-            __ldg(T + 768 + (c >> 24));
+        if (SHARED) w = T[c & 255] ^ T[256 + ((c >> 8) & 255)] ^ T[512 + ((c >> 16) & 255)] ^ T[768 + (c >> 24)];
+        else
+            w = __ldg(T + (c & 255)) ^ __ldg(T + 256 + ((c >> 8) & 255)) ^ __ldg(T + 512 + ((c >> 16) & 255)) ^
+                __ldg(T + 768 + (c >> 24));
     }
     const uint32_t w1 = mulx1(w), w2 = mulx2(w), w3 = mulx1(w2);
     uint32_t row[16];
@@ -70,6 +74,8 @@ struct FftParams {
     int m;                // N = 2^m points per product (local points for a shard)
     int c, k_lo, k_hi;    // tile bits [0,c) U [k_lo,k_hi)
     IdxMap map;           // local -> global index for the multipliers (identity unless sharded)
+    int wt_shared;        // table builds read a shared copy of the c -> c v_(4t) maps (only where the
+                          // 28 KB do not cost occupancy: the CTA holds one per SM anyway)
 };
 
 __device__ __forceinline__ uint32_t tab_addr(uint32_t base, uint32_t id) { return base + id * 512u; }
@@ -139,18 +145,22 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     const int R = p.k_hi - p.k_lo;
     const uint32_t nslots = 1u << (p.c + R);
     const uint32_t ntab = (1u << R) - 1;
-    // shared memory: [tables (ntab x 512 B)] [psi table (PSI)] [zero flags, 512 B] [tile] [second tile (!PSI)]
+    // shared memory: [tables (ntab x 512 B)] [psi table (PSI)] [zero flags, 512 B] [wt copy, 28 KB] [tile]
+    // [second tile (!PSI)]
     uint32_t* tabs = reinterpret_cast<uint32_t*>(smem_raw);
     uint4* psit = reinterpret_cast<uint4*>(tabs + ntab * 128);
     uint32_t* zf = reinterpret_cast<uint32_t*>(psit + (PSI ? 8 * 256 : 0));   // per table: multiplier == 0
-    const uint32_t tile_off = (uint32_t)(ntab * 512 + (PSI ? 8 * 256 * 16 : 0) + 512);
+    uint32_t* wts = zf + 128;                                                   // M4R-8 maps c -> c v_(4t)
+    const uint32_t tile_off = (uint32_t)(ntab * 512 + (PSI ? 8 * 256 * 16 : 0) + 512 + (p.wt_shared ? 7 * 1024 * 4 : 0));
     uint4* tile = reinterpret_cast<uint4*>(smem_raw + tile_off);
     const uint32_t tabs_sa = (uint32_t)__cvta_generic_to_shared(tabs);
     if (tabs_sa & 255) __trap();  // the PRMT address fusion needs 256-byte aligned tables
-    if (PSI) {
+    if (PSI)
         for (uint32_t i = threadIdx.x; i < 8 * 256; i += blockDim.x) psit[i] = p.tabs->psi64[i];
-        __syncthreads();   // the first tile's load reads entries other warps wrote
-    }
+    if (p.wt_shared)
+        for (uint32_t i = threadIdx.x; i < 7 * 1024 / 4; i += blockDim.x)
+            reinterpret_cast<uint4*>(wts)[i] = reinterpret_cast<const uint4*>(p.tabs->wt)[i];
+    __syncthreads();   // the first tile's table build / load reads entries other warps wrote
 
     const uint64_t N = 1ull << p.m;
     const uint64_t tiles_per_pair = N >> (p.c + R);
@@ -196,7 +206,8 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             const uint32_t blk = id + 1 - (1u << lg);
             const uint32_t lb = (uint32_t)(((uint64_t)base & ~((2ull << k) - 1)) | ((uint64_t)blk << (k + 1)));
             const uint32_t cst = layer_const(glayer(p.map, k), gidx(p.map, lb));
-            build_tab_row(tabs + id * 128, cst, (int)(i & 7), p.tabs->wt);
+            if (p.wt_shared) build_tab_row<true>(tabs + id * 128, cst, (int)(i & 7), wts);
+            else build_tab_row<false>(tabs + id * 128, cst, (int)(i & 7), p.tabs->wt);
             if ((i & 7) == 0) zf[id] = cst == 0;
         }
         // ---- load
@@ -253,10 +264,16 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     if (!PSI) cp_async_wait<0>();
 }
 
-static size_t fft2_smem(int c, int R, bool psi) {
+static size_t fft2_smem(int c, int R, bool psi, bool wt_shared) {
     size_t s = (((size_t)1 << R) - 1) * 512;
     if (psi) s += 8 * 256 * 16;
     s += 512;   // zero-multiplier flags (<= 127 tables)
+    if (wt_shared) s += 7 * 1024 * 4;   // shared copy of the M4R-8 maps c -> c v_(4t) (table builds)
     s += ((size_t)1 << (c + R)) * 16 * (psi ? 1 : 2);   // non-psi passes are double-buffered
     return s;
+}
+// the shared wt copy only where the CTA already takes a whole SM (it would otherwise halve occupancy)
+static bool fft2_wt_shared(int c, int R, bool psi) {
+    const size_t base = fft2_smem(c, R, psi, false);
+    return base > 113 * 1024 && base + 7 * 1024 * 4 <= 220 * 1024;
 }
