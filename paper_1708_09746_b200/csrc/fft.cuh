@@ -174,6 +174,12 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
         const uint32_t tt = (uint32_t)(t - pair * tiles_per_pair);
         base = ((tt & ((1u << midbits) - 1)) << p.c) | ((uint32_t)((uint64_t)(tt >> midbits) << p.k_hi));
     };
+    // Each CTA takes a contiguous run of tiles: consecutive tiles differ in the column/middle index bits
+    // [c, k_lo) first, which no multiplier of the pass depends on (layer k >= k_lo uses bits > k), so the
+    // tables are rebuilt only when the bits >= k_hi change (rarely in the upper passes).
+    const uint64_t per_cta = ntiles / gridDim.x, extra = ntiles % gridDim.x;
+    const uint64_t t_begin = blockIdx.x * per_cta + min((uint64_t)blockIdx.x, extra);
+    const uint64_t t_end = t_begin + per_cta + (blockIdx.x < extra ? 1 : 0);
     // non-PSI passes are double-buffered: the next tile is prefetched with cp.async during this one
     auto prefetch = [&](uint64_t t, uint32_t off) {
         uint64_t pair; uint32_t base;
@@ -185,20 +191,23 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     };
     const uint32_t tbytes = nslots * 16;
     if (!PSI) {
-        if (blockIdx.x < ntiles) prefetch(blockIdx.x, tile_off);
+        if (t_begin < t_end) prefetch(t_begin, tile_off);
         cp_async_commit();
     }
     int kt = 0;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, kt++) {
+    uint32_t tab_key = 0xFFFFFFFFu;
+    for (uint64_t t = t_begin; t < t_end; t++, kt++) {
         uint64_t pair;
         uint32_t base;
         tile_geom(t, pair, base);
         if (!PSI) {
             tile = reinterpret_cast<uint4*>(smem_raw + tile_off + (kt & 1) * tbytes);
-            if (t + gridDim.x < ntiles) prefetch(t + gridDim.x, tile_off + ((kt + 1) & 1) * tbytes);
+            if (t + 1 < t_end) prefetch(t + 1, tile_off + ((kt + 1) & 1) * tbytes);
             cp_async_commit();
         }
-        // ---- tables of this tile's multipliers: id -> (layer kk, block blk)
+        // ---- tables of this tile's multipliers: id -> (layer kk, block blk); they depend on base >> k_hi only
+        const uint32_t key = (uint32_t)((uint64_t)base >> p.k_hi);
+        if (key != tab_key)
         for (uint32_t i = threadIdx.x; i < ntab * 8; i += blockDim.x) {
             const uint32_t id = i >> 3;
             const int lg = 31 - __clz(id + 1);          // = R-1-kk
@@ -210,6 +219,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             else build_tab_row<false>(tabs + id * 128, cst, (int)(i & 7), p.tabs->wt);
             if ((i & 7) == 0) zf[id] = cst == 0;
         }
+        tab_key = key;
         // ---- load
         if (PSI) {
             // FFT_UNR loads in flight per thread, then changeRepr of each word (M4R-8, 8 lookups)
