@@ -76,6 +76,7 @@ struct FftParams {
     IdxMap map;           // local -> global index for the multipliers (identity unless sharded)
     int wt_shared;        // table builds read a shared copy of the c -> c v_(4t) maps (only where the
                           // 28 KB do not cost occupancy: the CTA holds one per SM anyway)
+    int db;               // non-PSI passes: double-buffered tiles (prefetch of the next tile) if they fit
 };
 
 __device__ __forceinline__ uint32_t tab_addr(uint32_t base, uint32_t id) { return base + id * 512u; }
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             cp_async16(buf + s, src + (base | (s & cmask) | ((s >> p.c) << p.k_lo)));
     };
     const uint32_t tbytes = nslots * 16;
-    if (!PSI) {
+    if (!PSI && p.db) {
         if (t_begin < t_end) prefetch(t_begin, tile_off);
         cp_async_commit();
     }
@@ -201,8 +202,12 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
         uint32_t base;
         tile_geom(t, pair, base);
         if (!PSI) {
-            tile = reinterpret_cast<uint4*>(smem_raw + tile_off + (kt & 1) * tbytes);
-            if (t + 1 < t_end) prefetch(t + 1, tile_off + ((kt + 1) & 1) * tbytes);
+            if (p.db) {
+                tile = reinterpret_cast<uint4*>(smem_raw + tile_off + (kt & 1) * tbytes);
+                if (t + 1 < t_end) prefetch(t + 1, tile_off + ((kt + 1) & 1) * tbytes);
+            } else {
+                prefetch(t, tile_off);   // single buffer: this tile's copies, waited for below
+            }
             cp_async_commit();
         }
         // ---- tables of this tile's multipliers: id -> (layer kk, block blk); they depend on base >> k_hi only
@@ -244,7 +249,8 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
                 }
             }
         } else {
-            cp_async_wait<1>();   // this tile's copies have landed (the next tile's may be in flight)
+            if (p.db) cp_async_wait<1>();   // this tile's copies have landed (the next tile's may be in flight)
+            else cp_async_wait<0>();
         }
         __syncthreads();
         // ---- layers, in groups of <= 3 (forward: from the top; inverse: from the bottom)
@@ -274,16 +280,18 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     if (!PSI) cp_async_wait<0>();
 }
 
-static size_t fft2_smem(int c, int R, bool psi, bool wt_shared) {
+static size_t fft2_smem(int c, int R, bool psi, bool wt_shared, bool db) {
     size_t s = (((size_t)1 << R) - 1) * 512;
     if (psi) s += 8 * 256 * 16;
     s += 512;   // zero-multiplier flags (<= 127 tables)
     if (wt_shared) s += 7 * 1024 * 4;   // shared copy of the M4R-8 maps c -> c v_(4t) (table builds)
-    s += ((size_t)1 << (c + R)) * 16 * (psi ? 1 : 2);   // non-psi passes are double-buffered
+    s += ((size_t)1 << (c + R)) * 16 * (db ? 2 : 1);
     return s;
 }
+// non-psi passes are double-buffered when two tiles fit
+static bool fft2_db(int c, int R, bool psi) { return !psi && fft2_smem(c, R, psi, false, true) <= 200 * 1024; }
 // the shared wt copy only where the CTA already takes a whole SM (it would otherwise halve occupancy)
 static bool fft2_wt_shared(int c, int R, bool psi) {
-    const size_t base = fft2_smem(c, R, psi, false);
+    const size_t base = fft2_smem(c, R, psi, false, fft2_db(c, R, psi));
     return base > 113 * 1024 && base + 7 * 1024 * 4 <= 220 * 1024;
 }

@@ -835,8 +835,9 @@ static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* 
     prm.m = P.m; prm.c = f.c; prm.k_lo = f.k_lo; prm.k_hi = f.k_hi;
     const int R = f.k_hi - f.k_lo;
     const uint64_t ntiles = (P.N >> (f.c + R)) * prm.batch;
+    prm.db = fft2_db(f.c, R, psi) ? 1 : 0;
     prm.wt_shared = fft2_wt_shared(f.c, R, psi) ? 1 : 0;
-    const size_t sm = fft2_smem(f.c, R, psi, prm.wt_shared != 0);
+    const size_t sm = fft2_smem(f.c, R, psi, prm.wt_shared != 0, prm.db != 0);
     const int occ = sm > 113 * 1024 ? 1 : 2;   // registers (128 x 256 threads) allow at most 2 CTAs/SM
     const int grid = grid_for(ntiles, 1, ds->sm_count, occ);
     const double bytes = (double)prm.batch * (psi ? (double)src_per * 8 : (double)P.N * 16) + (double)prm.batch * P.N * 16;
