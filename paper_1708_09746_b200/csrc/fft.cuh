@@ -293,5 +293,5 @@ static bool fft2_db(int c, int R, bool psi) { return !psi && fft2_smem(c, R, psi
 // the shared wt copy only where the CTA already takes a whole SM (it would otherwise halve occupancy)
 static bool fft2_wt_shared(int c, int R, bool psi) {
     const size_t base = fft2_smem(c, R, psi, false, fft2_db(c, R, psi));
-    return base > 113 * 1024 && base + 7 * 1024 * 4 <= 220 * 1024;
+    return base > 113 * 1024 && base + 7 * 1024 * 4 <= 200 * 1024;   // 200 KB: the opt-in set in get_device
 }

@@ -20,7 +20,7 @@
 //   GF2X_NO_IPSI_BS=1    table-driven changeRepr^-1 + combine instead of the bit-sliced kernel
 //   GF2X_FFT_C=c         column bits of the non-first FFT passes (default 6)
 //   GF2X_BOT_B=L         layers in the bit-sliced bottom kernel (default: 5 or 6 by the planner rule)
-//   GF2X_MAXR=R          maximum FFT layers per table pass (default 6)
+//   GF2X_MAXR=R          maximum FFT layers per table pass below the changeRepr pass (default 7)
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -639,30 +639,26 @@ struct FftPass {
     bool bottom;
     int layers;         // bottom: layers [0, layers)
 };
-// forward order (top-down); the first pass also applies changeRepr.  High layers [bot, m) are split
-// evenly into direct passes of <= 6 layers (63 M4R tables, 32 KB); layers [0, min(m, bot)) form the
-// bit-sliced bottom pass.  A table butterfly costs about half a bit-sliced one (measured), and at
-// layer 5 a 32-butterfly block still shares one multiplier per warp, so bot = 5 whenever the direct
-// layers [5, m) need no more passes than [6, m); else bot = 6 (a 7-layer pass, 127 tables, measured
-// slower than the bottom layer it saves).
-static int bot_layers(int m) {
-    static const int forced = getenv("GF2X_BOT_B") ? atoi(getenv("GF2X_BOT_B")) : 0;
-    if (forced) return forced;
-    return (m - 5 + 5) / 6 == (m - 6 + 5) / 6 ? 5 : 6;
-}
+// forward order (top-down); the first pass also applies changeRepr.  The high layers [bot, m) go to
+// table passes of <= 6 layers for the changeRepr pass (its 32 KB psi table) and <= 7 below it (127 M4R
+// tables, 64 KB; their tables are rebuilt only when the tile's bits >= k_hi change); layers
+// [0, min(m, bot)) form the bit-sliced bottom pass.  A table butterfly costs about half a bit-sliced one
+// (measured), so the bottom takes 5 layers unless that needs one more table pass than 6 would.
+static int fft_passes(int H, int maxr) { return H <= 0 ? 0 : (H <= 6 ? 1 : 1 + (H - 6 + maxr - 1) / maxr); }
 static std::vector<FftPass> plan_fft(int m) {
+    static const int maxr = getenv("GF2X_MAXR") ? atoi(getenv("GF2X_MAXR")) : 7;
+    static const int forced = getenv("GF2X_BOT_B") ? atoi(getenv("GF2X_BOT_B")) : 0;
+    const int bot = forced ? forced : (fft_passes(m - 5, maxr) <= fft_passes(m - 6, maxr) ? 5 : 6);
     std::vector<FftPass> v;
-    const int bot = bot_layers(m);
-    static const int maxr = getenv("GF2X_MAXR") ? atoi(getenv("GF2X_MAXR")) : 6;
     const int H = m > bot ? m - bot : 0;
-    const int np = (H + maxr - 1) / maxr;
+    const int np = fft_passes(H, maxr);
     int top = m;
     for (int i = 0; i < np; i++) {
         const int rem = top - bot;
-        const int r = (rem + (np - i) - 1) / (np - i);  // remaining layers / remaining passes
+        const int r = i == 0 ? std::min(6, rem - (np - 1)) : (rem + (np - i) - 1) / (np - i);
         const int lo = top - r;
-        // 64-column tiles (double-buffered: one 160 KB CTA per SM; measured as fast as 2 CTAs of 32-column
-        // tiles); 32 columns for the changeRepr pass and for 7-layer passes (their tables take 64 KB)
+        // 64-column tiles for 6-layer passes (double-buffered: one 160 KB CTA per SM; measured as fast as 2
+        // CTAs of 32-column tiles); 32 columns for the changeRepr pass and for 7-layer passes
         static const int cdir = getenv("GF2X_FFT_C") ? atoi(getenv("GF2X_FFT_C")) : 6;
         int c = (i == 0 || r > 6) ? 5 : cdir;
         if (c > lo) c = lo;   // column bits must lie below the pass's layers
