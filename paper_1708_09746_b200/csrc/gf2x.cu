@@ -1088,6 +1088,8 @@ gf2x_status gf2x_comm_destroy(gf2x_comm_t comm) {
 
 static void rank_bufs(RankCtx& R, unsigned char* base, const ShardGeom& S) {
     for (int b = 0; b < SB_COUNT; b++) R.buf[b] = base + S.off[b];
+    R.buf[SB_INA] = (unsigned char*)R.a_shard;
+    R.buf[SB_INB] = (unsigned char*)R.b_shard;
 }
 
 gf2x_status gf2x_mul_sharded(const uint64_t* a_shard, const uint64_t* b_shard, uint64_t bits, uint64_t* c_shard,
@@ -1162,7 +1164,7 @@ int gf2x_shard_plan(uint64_t bits, int nranks, char* buf, size_t cap) {
     if (shard_geom(bits, nranks, S) != GF2X_OK) return -1;
     ShardXfers X;
     shard_xfers(S, X);
-    static const char* bn[SB_COUNT] = {"A", "B", "W", "T", "X", "HALO"};
+    static const char* bn[SB_ALL] = {"A", "B", "W", "T", "X", "HALO", "IN_A", "IN_B"};
     auto list = [&](const std::vector<Xfer>& xs) {
         std::string o = "[";
         for (size_t i = 0; i < xs.size(); i++) {
@@ -1182,7 +1184,8 @@ int gf2x_shard_plan(uint64_t bits, int nranks, char* buf, size_t cap) {
              S.off[SB_HALO] - S.off[SB_X], S.bytes - S.off[SB_HALO]);
     std::string out = head;
     for (size_t i = 0; i < S.top_cross.size(); i++) out += (i ? ", " : "") + std::to_string(S.top_cross[i]);
-    out += "], \"a2a_fwd\": " + list(X.a2a_fwd) + ", \"a2a_back\": " + list(X.a2a_back) + ", \"cross\": [";
+    out += "], \"gather\": " + list(X.gather) + ", \"xchg\": " + list(X.xchg);
+    out += ", \"a2a_fwd\": " + list(X.a2a_fwd) + ", \"a2a_back\": " + list(X.a2a_back) + ", \"cross\": [";
     for (size_t i = 0; i < X.cross.size(); i++) out += (i ? ", " : "") + list(X.cross[i]);
     out += "], \"halo\": " + list(X.halo) + "}";
     if (buf && cap) {

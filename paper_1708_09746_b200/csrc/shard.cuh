@@ -56,6 +56,10 @@ __global__ void __launch_bounds__(256) k_shard_top(ShardTopParams p) {
             uint4 v = make_uint4(0, 0, 0, 0);
 #pragma unroll
             for (int ch = 0; ch < 8; ch++) v = xor4(v, psit[ch * 256 + ((w >> (8 * ch)) & 255)]);
+            if (j == 0) {   // c_(r,0) = X_0 = 1
+                acc = xor4(acc, v);
+                continue;
+            }
             const uint32_t t = tabs_sa + j * 512u;
             acc.x ^= m4r4_word_sa(t, v.x); acc.y ^= m4r4_word_sa(t, v.y);
             acc.z ^= m4r4_word_sa(t, v.z); acc.w ^= m4r4_word_sa(t, v.w);
@@ -136,14 +140,15 @@ struct gf2x_comm_s {
 // ---------------------------------------------------------------------------------------------
 // host orchestration
 // ---------------------------------------------------------------------------------------------
-enum ShardBuf { SB_A = 0, SB_B, SB_W, SB_T, SB_X, SB_HALO, SB_COUNT };
+// workspace buffers (SB_A..SB_HALO) and the caller's input shards (SB_INA, SB_INB: sources only)
+enum ShardBuf { SB_A = 0, SB_B, SB_W, SB_T, SB_X, SB_HALO, SB_COUNT, SB_INA = SB_COUNT, SB_INB, SB_ALL };
 
 struct RankCtx {
     int r;
     const uint64_t* a_shard;
     const uint64_t* b_shard;
     uint64_t* c_shard;
-    unsigned char* buf[SB_COUNT];
+    unsigned char* buf[SB_ALL];
 };
 
 struct Xfer {
@@ -261,6 +266,10 @@ struct ShardExec {
 // Every exchange of the sharded multiply as transfer lists (host only; every rank derives the same
 // lists from (bits, G)).  Byte offsets into the per-rank buffers of ShardGeom.
 struct ShardXfers {
+    // rank r converts operand r & 1 (0: a, 1: b): gather that operand's shards from every rank into A,
+    // then hand the converted operand to the partner rank r ^ 1 (its B)
+    std::vector<Xfer> gather;
+    std::vector<Xfer> xchg;
     std::vector<Xfer> a2a_fwd;                 // blocked -> t-sliced: rank r's chunk q -> rank q's T chunk r
     std::vector<Xfer> a2a_back;                // t-sliced -> blocked: rank q's T chunk r -> rank r's X chunk q
     std::vector<std::vector<Xfer>> cross;      // one per level in ShardGeom::top_cross (ascending)
@@ -269,7 +278,11 @@ struct ShardXfers {
 static void shard_xfers(const ShardGeom& S, ShardXfers& X) {
     const int G = S.G;
     const uint64_t chunk = S.Nloc >> S.g, Nloc = S.Nloc;
-    X.a2a_fwd.clear(); X.a2a_back.clear(); X.cross.clear(); X.halo.clear();
+    X.gather.clear(); X.xchg.clear(); X.a2a_fwd.clear(); X.a2a_back.clear(); X.cross.clear(); X.halo.clear();
+    const uint64_t sb = S.n / G * 8;   // bytes of an operand shard
+    for (int r = 0; r < G; r++)
+        for (int q = 0; q < G; q++) X.gather.push_back({q, r, (r & 1) ? SB_INB : SB_INA, SB_A, 0, q * sb, sb});
+    for (int r = 0; r < G; r++) X.xchg.push_back({r, r ^ 1, SB_A, SB_B, 0, 0, S.n * 8});
     for (int r = 0; r < G; r++)
         for (int q = 0; q < G; q++) X.a2a_fwd.push_back({r, q, SB_X, SB_T, q * chunk * 16, r * chunk * 16, chunk * 16});
     for (int q = 0; q < G; q++)
@@ -310,38 +323,23 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
         if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
         return GF2X_OK;
     };
-    // ---- gather both operands on every rank
-    if (X.sim) {   // virtual rank r's shard is at its input pointer: copy it into every rank
-        for (int q : mine) {
-            RankCtx& R = X.local(q);
-            for (int r = 0; r < G; r++) {
-                RankCtx& src = X.local(r);
-                const size_t sb = S.n / G * 8;
-                if (cudaMemcpyAsync(R.buf[SB_A] + r * sb, src.a_shard, sb, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
-                    cudaMemcpyAsync(R.buf[SB_B] + r * sb, src.b_shard, sb, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-                    return fail(GF2X_ECUDA, "shard gather copy failed");
-            }
-        }
-    } else {
-        RankCtx& R = X.local(X.comm->rank);
-        const size_t sb = S.n / G * 8;
-        int rc = g_nccl.GroupStart();
-        if (!rc) rc = g_nccl.AllGather(R.a_shard, R.buf[SB_A], sb, NCCL_UINT8, X.comm->comm, st);
-        if (!rc) rc = g_nccl.AllGather(R.b_shard, R.buf[SB_B], sb, NCCL_UINT8, X.comm->comm, st);
-        int rc2 = g_nccl.GroupEnd();
-        if (rc || rc2) return fail(GF2X_ENCCL, std::string("NCCL all-gather failed: ") + g_nccl.GetErrorString(rc ? rc : rc2));
-    }
-    // ---- mask, convert (redundantly), combine into h_r
+    // ---- gather: rank r assembles operand r & 1 (a for even ranks, b for odd ones) and converts only that
+    // one (the forward conversion is a whole-operand transform done redundantly; splitting it between
+    // partner ranks halves it), then partners swap their converted operands
+    if ((s = X.run(XF.gather)) != GF2X_OK) return s;
     for (int r : mine) {
-        RankCtx& R = X.local(r);
-        uint64_t* A = (uint64_t*)R.buf[SB_A];
-        uint64_t* B = (uint64_t*)R.buf[SB_B];
-        uint4* W = (uint4*)R.buf[SB_W];
+        uint64_t* A = (uint64_t*)X.local(r).buf[SB_A];
         { ProfScope ps("k_prep", 16.0 * S.n, st); k_prep<<<grid_for(S.n, 256, smc, 8), 256, 0, st>>>(A, S.n, bits, S.p, 1, A); }
-        { ProfScope ps("k_prep", 16.0 * S.n, st); k_prep<<<grid_for(S.n, 256, smc, 8), 256, 0, st>>>(B, S.n, bits, S.p, 1, B); }
         if ((s = last("shard prep")) != GF2X_OK) return s;
         if ((s = run_cvt<uint64_t>(S.cvt_fwd, A, S.p, 1, false, smc, st)) != GF2X_OK) return s;
-        if ((s = run_cvt<uint64_t>(S.cvt_fwd, B, S.p, 1, false, smc, st)) != GF2X_OK) return s;
+    }
+    if ((s = X.run(XF.xchg)) != GF2X_OK) return s;
+    // ---- combine into h_r (changeRepr included), local FFT
+    for (int r : mine) {
+        RankCtx& R = X.local(r);
+        uint64_t* A = (uint64_t*)R.buf[(r & 1) ? SB_B : SB_A];   // converted a
+        uint64_t* B = (uint64_t*)R.buf[(r & 1) ? SB_A : SB_B];   // converted b
+        uint4* W = (uint4*)R.buf[SB_W];
         ShardTopParams tp;
         tp.tabs = ds->tabs;
         tp.Nloc = Nloc;

@@ -65,11 +65,24 @@ def _worker(rank, world, port, bits, errq):
         uid = G.broadcast_unique_id(lambda: bytes(range(128)), rank)
         assert uid == bytes(range(128))
 
+        # ---- forward: rank r gathers operand r & 1 (a: even ranks, b: odd) into A, converts it, and swaps
+        # the converted operand with its partner r ^ 1 (into B)
+        nb = {k: v // 16 for k, v in plan["buffers"].items()}
+        n_units = plan["n"] // 2                       # 64-bit words, labelled per 16-byte unit
+        sh = n_units // world
+        lab_a = np.arange(n_units, dtype=np.int64)
+        lab_b = lab_a + (1 << 40)
+        bufs = {"IN_A": lab_a[rank * sh:(rank + 1) * sh].copy(), "IN_B": lab_b[rank * sh:(rank + 1) * sh].copy(),
+                "A": np.full(nb["A"], -1, dtype=np.int64), "B": np.full(nb["B"], -1, dtype=np.int64)}
+        _execute(plan["gather"], rank, bufs)
+        assert np.array_equal(bufs["A"][:n_units], lab_b if rank & 1 else lab_a), "gathered operand"
+        _execute(plan["xchg"], rank, bufs)
+        assert np.array_equal(bufs["B"][:n_units], lab_a if rank & 1 else lab_b), "partner's operand"
+
         g, K, Nloc = plan["g"], plan["K"], plan["Nloc"]
         assert plan["G"] == world and (1 << g) == world
         Kg = K - g
         chunk = Nloc >> g
-        nb = {k: v // 16 for k, v in plan["buffers"].items()}
         idx = np.arange(Nloc, dtype=np.int64)
         # ---- blocked -> pack -> a2a_fwd -> t-sliced
         q_of = np.arange(world, dtype=np.int64)[:, None]
