@@ -193,8 +193,10 @@ __global__ void __launch_bounds__(256) k_ipsi_combine(const uint4* __restrict__ 
 #define IB_TILE 4096
 __device__ __forceinline__ uint32_t ib_swz(uint32_t e) { return e ^ ((e >> 5) & 31); }
 
+// halo (sharded multiply, batch 1): the tower element preceding P[0] globally (rank r-1's last one), or null
 __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restrict__ P, const DevTables* tabs, uint64_t N,
-                                                         uint64_t batch, uint64_t* __restrict__ out) {
+                                                         uint64_t batch, uint64_t* __restrict__ out,
+                                                         const uint4* __restrict__ halo) {
     extern __shared__ __align__(1024) uint32_t ib_smem[];
     uint32_t* S = ib_smem;                    // [4][IB_TILE] limb planes (swizzled)
     uint32_t* H = ib_smem + 4 * IB_TILE;      // [2][IB_TILE] hi64 halves of every element (swizzled)
@@ -215,9 +217,9 @@ __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restri
         // the element before the tile (its hi64 enters the tile's first output word)
         if (t == 0) {
             uint64_t hi = 0;
-            if (w0 > 0) {
+            if (w0 > 0 || halo) {
                 uint64_t lo;
-                const uint4 pv = src[-1];
+                const uint4 pv = w0 > 0 ? src[-1] : *halo;
                 uint4 acc = make_uint4(0, 0, 0, 0);
                 const uint32_t w[4] = {pv.x, pv.y, pv.z, pv.w};
                 for (int L = 0; L < 4; L++)
@@ -937,7 +939,7 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         if (n_out == P.N && P.N % IB_TILE == 0 && !env_flag("GF2X_NO_IPSI_BS")) {
             ProfScope ps("k_ipsi_bs", 16.0 * P.N * P.batch + 8.0 * total, st);
             k_ipsi_bs<<<grid_for(P.N / IB_TILE * P.batch, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(Wa, ds->tabs, P.N,
-                                                                                                           P.batch, c);
+                                                                                                           P.batch, c, nullptr);
         } else {
             ProfScope ps("k_ipsi_combine", 16.0 * P.N * P.batch + 8.0 * total, st);
             k_ipsi_combine<<<grid_for(total, 256, smc, 2), 256, 16 * 256 * 16, st>>>(Wa, ds->tabs, P.N, n_out, P.batch, c, nullptr);
