@@ -134,6 +134,12 @@ struct CvtResParams {
 
 #define RES_THREADS 256
 #define RES_MAXJ 18   // row slots per thread: rows <= RES_MAXJ * (RES_THREADS >> C_log) (checked by the planner)
+#ifndef RES_UNROLL128
+#define RES_UNROLL128 1   // measured: 128-bit units faster unrolled over 10 slots than rolled
+#endif
+// unrolled row slots: 64-bit units (C <= 32 classes: <= 18 slots); 128-bit units use C = 8 (<= 9 slots)
+#define RES_SLOTS128 10
+#define RES_SLOTS(T) ((sizeof(T) == 8 || !RES_UNROLL128) ? RES_MAXJ : RES_SLOTS128)
 template <typename T>
 __device__ __forceinline__ void cp_async_unit(T* dst, const T* src) {
     if (sizeof(T) == 16) cp_async16(dst, src);
@@ -186,7 +192,7 @@ __global__ void __launch_bounds__(RES_THREADS, 3) k_cvt_res(CvtResParams p) {
         // unit index of the thread's row slot j (r = rl + j RS), span if the slot is empty
         uint32_t ii[RES_MAXJ];
 #pragma unroll
-        for (int j = 0; j < (sizeof(T) == 8 ? RES_MAXJ : 0); j++) {
+        for (int j = 0; j < RES_SLOTS(T); j++) {
             const uint32_t r = rl + j * RS;
             const uint32_t i = r * M + c0 + c;
             ii[j] = (colok && r < (uint32_t)p.rows && i < span) ? i : span;
@@ -215,9 +221,9 @@ __global__ void __launch_bounds__(RES_THREADS, 3) k_cvt_res(CvtResParams p) {
                     tile[s] = xor_t<T>(tile[s], tile[s + off]);
                 }
             };
-            if constexpr (sizeof(T) == 8) {
+            if (RES_UNROLL128 || sizeof(T) == 8) {
 #pragma unroll
-                for (int j = 0; j < RES_MAXJ; j++) slot(ii[j], rl + j * RS);
+                for (int j = 0; j < RES_SLOTS(T); j++) slot(ii[j], rl + j * RS);
             } else {
                 if (colok)
                     for (uint32_t r = rl; r < (uint32_t)p.rows; r += RS) slot(r * M + c0 + c, r);

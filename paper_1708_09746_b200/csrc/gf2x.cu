@@ -588,7 +588,8 @@ static std::vector<CvtPass> plan_cvt_ops(const std::vector<CvtOp>& ops, int m, i
             if ((size_t)rows * ((size_t)1 << C_log) * unit_bytes <= budget) {
                 while (C_log < 6 && (size_t)rows * ((size_t)2 << C_log) * unit_bytes <= budget) C_log++;
                 // the kernel keeps RES_MAXJ row slots per thread (RES_THREADS / 2^C_log row lanes)
-                while (C_log > 0 && rows > RES_MAXJ * (RES_THREADS >> C_log)) C_log--;
+                const int maxj = unit_bytes == 8 ? RES_MAXJ : RES_SLOTS128;
+                while (C_log > 0 && rows > maxj * (RES_THREADS >> C_log)) C_log--;
                 if (!passes.empty()) close(passes.back());
                 CvtPass P;
                 P.stream = false;
