@@ -30,6 +30,7 @@
 // kernels
 // ---------------------------------------------------------------------------------------------
 #define SHARD_MAXJ 128
+#define SHARD_MAXJ_UNR 4   // block words prefetched per point (G <= 8)
 
 struct ShardTopParams {
     const uint64_t* S;   // converted operand, n = (G/2) Nloc words
@@ -51,8 +52,11 @@ __global__ void __launch_bounds__(256) k_shard_top(ShardTopParams p) {
     const uint32_t tabs_sa = (uint32_t)__cvta_generic_to_shared(tabs);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.Nloc; i += (uint64_t)gridDim.x * blockDim.x) {
         uint4 acc = make_uint4(0, 0, 0, 0);
+        uint64_t ws[SHARD_MAXJ_UNR];   // the J block words of this point, loaded up front
+#pragma unroll
+        for (int j = 0; j < SHARD_MAXJ_UNR; j++) ws[j] = j < p.J ? p.S[j * p.Nloc + i] : 0ull;
         for (int j = 0; j < p.J; j++) {
-            const uint64_t w = p.S[j * p.Nloc + i];
+            const uint64_t w = j < SHARD_MAXJ_UNR ? ws[j] : p.S[j * p.Nloc + i];
             uint4 v = make_uint4(0, 0, 0, 0);
 #pragma unroll
             for (int ch = 0; ch < 8; ch++) v = xor4(v, psit[ch * 256 + ((w >> (8 * ch)) & 255)]);
@@ -354,9 +358,9 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
         const size_t sm = (size_t)tp.J * 512 + 8 * 256 * 16;
         cudaFuncSetAttribute(k_shard_top, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         tp.S = A; tp.W = W;
-        { ProfScope ps("k_shard_top", 8.0 * tp.J * Nloc + 16.0 * Nloc, st); k_shard_top<<<grid_for(Nloc, 256, smc, 2), 256, sm, st>>>(tp); }
+        { ProfScope ps("k_shard_top", 8.0 * tp.J * Nloc + 16.0 * Nloc, st); k_shard_top<<<grid_for(Nloc, 256, smc, 4), 256, sm, st>>>(tp); }
         tp.S = B; tp.W = W + Nloc;
-        { ProfScope ps("k_shard_top", 8.0 * tp.J * Nloc + 16.0 * Nloc, st); k_shard_top<<<grid_for(Nloc, 256, smc, 2), 256, sm, st>>>(tp); }
+        { ProfScope ps("k_shard_top", 8.0 * tp.J * Nloc + 16.0 * Nloc, st); k_shard_top<<<grid_for(Nloc, 256, smc, 4), 256, sm, st>>>(tp); }
         if ((s = last("shard top")) != GF2X_OK) return s;
         // ---- local FFT layers [6, mloc) of both operands, bottom kernel, local iFFT layers
         const IdxMap map{S.mloc, g, (uint32_t)r};
