@@ -201,13 +201,14 @@ __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restri
     uint32_t* S = ib_smem;                    // [4][IB_TILE] limb planes (swizzled)
     uint32_t* H = ib_smem + 4 * IB_TILE;      // [2][IB_TILE] hi64 halves of every element (swizzled)
     __shared__ uint64_t halo_hi;
-    const uint64_t tiles_per_pair = N / IB_TILE;
-    const uint64_t ntiles = tiles_per_pair * batch;
+    // the batch is one flat run of products (n_out = N): a tile covers IB_TILE consecutive elements, which
+    // may span several small products; an element at a product boundary has no predecessor
+    const uint64_t ntiles = N * batch / IB_TILE;
+    const uint64_t pair = 0;
     const uint32_t t = threadIdx.x;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t pair = tile / tiles_per_pair;
-        const uint64_t w0 = (tile - pair * tiles_per_pair) * IB_TILE;   // first element / word of the tile
-        const uint4* src = P + pair * N + w0;
+        const uint64_t w0 = tile * IB_TILE;   // first element / word of the tile (flat)
+        const uint4* src = P + w0;
         // ---- load (coalesced), limb-planar
         for (uint32_t e = t; e < IB_TILE; e += IB_THREADS) {
             const uint4 v = src[e];
@@ -217,9 +218,9 @@ __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restri
         // the element before the tile (its hi64 enters the tile's first output word)
         if (t == 0) {
             uint64_t hi = 0;
-            if (w0 > 0 || halo) {
+            if ((w0 & (N - 1)) != 0 || halo) {   // N is a power of two
                 uint64_t lo;
-                const uint4 pv = w0 > 0 ? src[-1] : *halo;
+                const uint4 pv = (w0 & (N - 1)) != 0 ? src[-1] : *halo;
                 uint4 acc = make_uint4(0, 0, 0, 0);
                 const uint32_t w[4] = {pv.x, pv.y, pv.z, pv.w};
                 for (int L = 0; L < 4; L++)
@@ -286,12 +287,13 @@ __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restri
             const uint32_t e = e0 + j;
             uint32_t plo, phi;
             if (e == 0) { plo = (uint32_t)halo_hi; phi = (uint32_t)(halo_hi >> 32); }
+            else if (((w0 + e) & (N - 1)) == 0) { plo = 0; phi = 0; }   // first word of a product
             else { plo = H[ib_swz(e - 1)]; phi = H[IB_TILE + ib_swz(e - 1)]; }
             S[ib_swz(e)] = a0[j] ^ plo;
             S[IB_TILE + ib_swz(e)] = a1[j] ^ phi;
         }
         __syncthreads();
-        uint64_t* dst = out + pair * N + w0;
+        uint64_t* dst = out + pair * N + w0;   // (pair = 0: flat)
         for (uint32_t e = t; e < IB_TILE; e += IB_THREADS) {
             const uint32_t q = ib_swz(e);
             dst[e] = ((uint64_t)S[IB_TILE + q] << 32) | S[q];
@@ -768,10 +770,20 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
             prm.units_per_pair = per;
             prm.batch = batch;
             prm.inverse = (inverse ? 1 : 0) | (env_flag("GF2X_RB_NOPHASE") ? 2 : 0);   // bit 1: debug, copy only
+            // a node spanning all index bits of a (small) product: the tile's columns continue into the next
+            // products (they are contiguous), up to the width the planner wanted
+            if (prm.mode == 1 && prm.R + prm.C == m) {
+                const int want = sizeof(T) == 8 ? 4 : 3;
+                while (prm.C < want && (prm.batch & 1) == 0 && prm.batch > 1) {
+                    prm.C++;
+                    prm.units_per_pair <<= 1;
+                    prm.batch >>= 1;
+                }
+            }
             const size_t ncols = (size_t)1 << prm.C, nrows = (size_t)1 << prm.R;
             const size_t bufsz = (ncols * (nrows + (prm.mode ? 16 / sizeof(T) : 0)) * sizeof(T) + 127) & ~(size_t)127;
             const size_t sm = 2 * bufsz;   // double-buffered
-            const uint64_t ntiles = (per >> (prm.R + prm.C)) * batch;
+            const uint64_t ntiles = (prm.units_per_pair >> (prm.R + prm.C)) * prm.batch;
             const int occ = 3;
             ProfScope ps(sizeof(T) == 8 ? "k_cvt_rb<u64>" : "k_cvt_rb<u128>", 2.0 * per * batch * sizeof(T), st);
             const int g = grid_for(ntiles, 1, sm_count, occ);
@@ -937,9 +949,9 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
     {
         const uint64_t n_out = P.na + P.nb;
         const uint64_t total = n_out * P.batch;
-        if (n_out == P.N && P.N % IB_TILE == 0 && !env_flag("GF2X_NO_IPSI_BS")) {
+        if (n_out == P.N && (P.N * P.batch) % IB_TILE == 0 && !env_flag("GF2X_NO_IPSI_BS")) {
             ProfScope ps("k_ipsi_bs", 16.0 * P.N * P.batch + 8.0 * total, st);
-            k_ipsi_bs<<<grid_for(P.N / IB_TILE * P.batch, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(Wa, ds->tabs, P.N,
+            k_ipsi_bs<<<grid_for(P.N * P.batch / IB_TILE, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(Wa, ds->tabs, P.N,
                                                                                                            P.batch, c, nullptr);
         } else {
             ProfScope ps("k_ipsi_combine", 16.0 * P.N * P.batch + 8.0 * total, st);
