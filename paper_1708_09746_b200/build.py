@@ -48,5 +48,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Tuning aid: the library with extra -D flags as libgf2x_b200_<name>.so (A/B timing, tests/ab_bench.py)."""
+    build()
+    path = os.path.join(HERE, f"libgf2x_b200_{name}.so")
+    cmd = [NVCC, *[f"-D{d}" for d in defines], *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", path, *SOURCES, "-lcudart"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed for variant " + name)
+    return path
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":   # --variant NAME DEF [DEF ...]
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+        sys.exit(0)
     print(build(force="--force" in sys.argv, verbose=True))

@@ -16,7 +16,11 @@
 // Planes of block (group g, limb Lb) live at word ((Lb * 64 + g) * 33 + j).
 #pragma once
 
-#define BT_THREADS 128
+#ifndef BT_TPC
+#define BT_TPC 1          // tiles per CTA (2 = one 256-thread CTA per SM whose halves share barriers: measured
+#endif                    // phase (one copy of the bs_mul32 code in the instruction caches at a time)
+#define BT_HALF 128       // threads per tile
+#define BT_THREADS (BT_HALF * BT_TPC)
 #define BT_BITS 11
 #define BT_GROUPS 64
 #define BT_STRIDE 33
@@ -91,19 +95,35 @@ __device__ __forceinline__ void bt_store_block(uint4* __restrict__ dst, uint64_t
 }
 
 // one layer k of butterflies on a plane region: warp = limb, lane = pair index
+// U_k(g0) of layer k, pair q: the multiplier of the group's block base with the position bits cleared
+__device__ __forceinline__ uint32_t bt_u(int k, int q, uint64_t e0, int L, int m, const IdxMap& map) {
+    const int g0 = (q & ((1 << k) - 1)) | ((q >> k) << (k + 1));
+    const uint64_t gi = (e0 + bt_elem(g0, 0, L)) & ((1ull << m) - 1);
+    return layer_const(k, gidx(map, (uint32_t)gi));
+}
+
+// multiplier planes of layer k for this thread's pair: c_j = P_k[j] ^ (bit j of U ? ~0 : 0)
+__device__ __forceinline__ void bt_cplanes(const uint32_t* Pk, uint32_t U, uint32_t* c) {
+#pragma unroll
+    for (int j = 0; j < 32; j++) c[j] = Pk[j] ^ (uint32_t)((int32_t)(U << (31 - j)) >> 31);
+}
+
+// CK: cache of the multiplier planes, [layer][pair][33] (written by warp 0 in the forward layers,
+// read by every warp in the inverse layers of the same tile)
 template <bool INV>
-__device__ __forceinline__ void bt_layer(uint32_t* planes, int k, const uint32_t* Pk, uint64_t e0, int L, int m,
-                                         const IdxMap& map) {
-    const int lb = threadIdx.x >> 5, q = threadIdx.x & 31;
+__device__ __forceinline__ void bt_layer(uint32_t* planes, int k, const uint32_t* Pk, const uint32_t* UC,
+                                         uint32_t* CK, int tid) {
+    const int lb = tid >> 5, q = tid & 31;
     const int g0 = (q & ((1 << k) - 1)) | ((q >> k) << (k + 1));
     const int g1 = g0 | (1 << k);
-    // U_k(g0): within-pair index of the group's block base with the position bits cleared
-    const uint64_t N = 1ull << m;
-    const uint64_t gi = (e0 + bt_elem(g0, 0, L)) & (N - 1);
-    const uint32_t U = layer_const(k, gidx(map, (uint32_t)gi));
     uint32_t c[32], x1[32], pr[32];
+    if (CK) {
+        const uint32_t* ck = CK + (k * 32 + q) * 33;
 #pragma unroll
-    for (int j = 0; j < 32; j++) c[j] = Pk[j] ^ (((U >> j) & 1) ? 0xFFFFFFFFu : 0u);
+        for (int j = 0; j < 32; j++) c[j] = ck[j];
+    } else {
+        bt_cplanes(Pk, UC[k * 32 + q], c);
+    }
     uint32_t* b0 = planes + bt_block(g0, lb);
     uint32_t* b1 = planes + bt_block(g1, lb);
 #pragma unroll
@@ -118,6 +138,36 @@ __device__ __forceinline__ void bt_layer(uint32_t* planes, int k, const uint32_t
         const uint32_t x0 = b0[j] ^ pr[j];
         b0[j] = x0;
         b1[j] = INV ? x1[j] : (x1[j] ^ x0);
+    }
+}
+
+// forward layer k on both operands with one set of multiplier planes (stored to CK by warp 0)
+__device__ __forceinline__ void bt_layer2(uint32_t* PA, uint32_t* PB, int k, const uint32_t* Pk, const uint32_t* UC,
+                                          uint32_t* CK, int tid) {
+    const int lb = tid >> 5, q = tid & 31;
+    const int g0 = (q & ((1 << k) - 1)) | ((q >> k) << (k + 1));
+    const int g1 = g0 | (1 << k);
+    uint32_t c[32], x1[32], pr[32];
+    bt_cplanes(Pk, UC[k * 32 + q], c);
+    if (CK && lb == 0) {
+        uint32_t* ck = CK + (k * 32 + q) * 33;
+#pragma unroll
+        for (int j = 0; j < 32; j++) ck[j] = c[j];
+    }
+#pragma unroll 1
+    for (int o = 0; o < 2; o++) {
+        uint32_t* planes = o ? PB : PA;
+        uint32_t* b0 = planes + bt_block(g0, lb);
+        uint32_t* b1 = planes + bt_block(g1, lb);
+#pragma unroll
+        for (int j = 0; j < 32; j++) x1[j] = b1[j];
+        bs_mul32(x1, c, pr);
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+            const uint32_t x0 = b0[j] ^ pr[j];
+            b0[j] = x0;
+            b1[j] = x1[j] ^ x0;
+        }
     }
 }
 
@@ -143,11 +193,20 @@ __device__ __forceinline__ void bt_acc_add(uint32_t* reg, int g, int mask, const
         }
 }
 
-__global__ void __launch_bounds__(BT_THREADS, 2) k_bottom(BottomParams p) {
+__global__ void __launch_bounds__(BT_THREADS, 2 / BT_TPC) k_bottom(BottomParams p) {
     extern __shared__ __align__(1024) uint32_t bt_smem[];
-    uint32_t* PA = bt_smem;                 // planes of A
-    uint32_t* PB = PA + BT_REGION;          // planes of B
-    uint32_t* Pk = PB + BT_REGION;          // per-layer position planes, L x 32
+    const int half = BT_TPC == 1 ? 0 : (int)(threadIdx.x / BT_HALF), tid = threadIdx.x % BT_HALF;
+    uint32_t* PA = bt_smem + half * 2 * BT_REGION;   // planes of A (this half's tile)
+    uint32_t* PB = PA + BT_REGION;                   // planes of B
+    uint32_t* Pk = bt_smem + BT_TPC * 2 * BT_REGION; // per-layer position planes, L x 32 (shared)
+    uint32_t* UCb = Pk + 6 * 32;                     // per tile: U_k of each (layer, pair), BT_TPC x 6 x 32
+    uint32_t* UC = UCb + half * 6 * 32;
+#ifdef BT_NO_CK
+    uint32_t* CK = nullptr;
+#else
+    // multiplier-plane cache, only when the tile runs forward and inverse layers
+    uint32_t* CK = (p.mode & 5) == 5 ? UCb + BT_TPC * 6 * 32 + half * 6 * 32 * 33 : nullptr;
+#endif
     const int L = p.L;
     // P_k[j] = xor over position bits i (L+i < m) of bit j of s_k(v_(L+i)) * POS_i
     for (int i = threadIdx.x; i < L * 32; i += blockDim.x) {
@@ -159,10 +218,13 @@ __global__ void __launch_bounds__(BT_THREADS, 2) k_bottom(BottomParams p) {
         Pk[i] = v;
     }
     const uint64_t total = p.total;   // loads beyond it read 0, stores beyond it are dropped
-    const int lb = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        const uint64_t e0 = t << BT_BITS;
+    const int lb = tid >> 5, lane = tid & 31;
+    // both halves iterate together (shared barriers); a half past the last tile loads zeros and
+    // drops its stores (e0 >= total)
+    for (uint64_t tb = (uint64_t)blockIdx.x * BT_TPC; tb < p.ntiles; tb += (uint64_t)gridDim.x * BT_TPC) {
+        const uint64_t e0 = (tb + half) << BT_BITS;
         __syncthreads();
+        for (int i = tid; i < L * 32; i += BT_HALF) UC[i] = bt_u(i >> 5, i & 31, e0, L, p.m, p.map);
         // ---- load + bit-slice both operands (warp = limb, lane = group)
         for (int g = lane; g < BT_GROUPS; g += 32) {
             bt_load_block(p.A, e0, total, g, lb, L, PA);
@@ -170,9 +232,10 @@ __global__ void __launch_bounds__(BT_THREADS, 2) k_bottom(BottomParams p) {
         }
         __syncthreads();
         if (p.mode & 1) {
-            for (int k = L - 1; k >= 0; k--) {   // FFT_LCH bottom layers, top-down
-                bt_layer<false>(PA, k, Pk + k * 32, e0, L, p.m, p.map);
-                bt_layer<false>(PB, k, Pk + k * 32, e0, L, p.m, p.map);
+            // FFT_LCH bottom layers, top-down; one set of multiplier planes per layer serves both operands
+#pragma unroll 1
+            for (int k = L - 1; k >= 0; k--) {
+                bt_layer2(PA, PB, k, Pk + k * 32, UC, CK, tid);
                 __syncthreads();
             }
         }
@@ -180,7 +243,7 @@ __global__ void __launch_bounds__(BT_THREADS, 2) k_bottom(BottomParams p) {
         if (p.mode & 2) {
             // two threads per group: thread h = 0 produces result limbs R0, R1, h = 1 produces R2, R3
             // (six TGF(2^32) products each, accumulated in registers), then both overwrite the A planes
-            const int g = threadIdx.x & (BT_GROUPS - 1), h = threadIdx.x >> 6;
+            const int g = tid & (BT_GROUPS - 1), h = tid >> 6;
             uint32_t acc0[32], acc1[32];
 #pragma unroll
             for (int j = 0; j < 32; j++) { acc0[j] = 0; acc1[j] = 0; }
@@ -215,7 +278,7 @@ __global__ void __launch_bounds__(BT_THREADS, 2) k_bottom(BottomParams p) {
         }
         if (p.mode & 4) {
             for (int k = 0; k < L; k++) {   // iFFT_LCH bottom layers, bottom-up
-                bt_layer<true>(R, k, Pk + k * 32, e0, L, p.m, p.map);
+                bt_layer<true>(R, k, Pk + k * 32, UC, CK, tid);
                 __syncthreads();
             }
         }
@@ -227,4 +290,9 @@ __global__ void __launch_bounds__(BT_THREADS, 2) k_bottom(BottomParams p) {
     }
 }
 
-static size_t bottom_smem() { return (size_t)(2 * BT_REGION + 6 * 32) * 4; }
+static size_t bottom_smem() { return (size_t)(BT_TPC * 2 * BT_REGION + 6 * 32 + BT_TPC * 6 * 32 * 34) * 4; }
+
+static int grid_for(uint64_t items, int per_block, int sm_count, int occ);
+static void bottom_launch(const BottomParams& bp, int smc, cudaStream_t st) {
+    k_bottom<<<grid_for((bp.ntiles + BT_TPC - 1) / BT_TPC, 1, smc, 2 / BT_TPC), BT_THREADS, bottom_smem(), st>>>(bp);
+}

@@ -932,7 +932,7 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         // bit-sliced products per 2^11-element tile: 2L forward + L inverse layers x 128, pointmul 768
         const double prods = (double)bp.ntiles * (3.0 * bp.L * 128.0 + 768.0);
         ProfScope ps("k_bottom", 48.0 * P.N * P.batch, st, prods * OPS_BS_MUL32);
-        k_bottom<<<grid_for(bp.ntiles, 1, smc, 2), BT_THREADS, bottom_smem(), st>>>(bp);
+        bottom_launch(bp, smc, st);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("bottom launch: ") + cudaGetErrorString(e));
     }

@@ -78,16 +78,42 @@ __device__ GF2X_INLINE uint4 xor4(uint4 a, uint4 b) {
 // 32x32 bit transpose: on return x[j] bit e = (old x[e]) bit j.
 // ---------------------------------------------------------------------------------------------
 GF2X_HD GF2X_INLINE void transpose32(uint32_t* x) {
+    // 32x32 bit transpose in place: bit j of x[k] <-> bit k of x[j].  Stage s swaps the s-bit blocks
+    // (x[k] bits [s,2s) of each 2s-block) <-> (x[k+s] bits [0,s)).  The 16- and 8-bit stages are byte
+    // permutes (PRMT, 2 per pair); the 4/2/1-bit stages are a shift + 3-input select per word (4 per pair).
+#ifdef __CUDA_ARCH__
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+        const uint32_t a = x[k], b = x[k + 16];
+        x[k] = __byte_perm(a, b, 0x5410);
+        x[k + 16] = __byte_perm(a, b, 0x7632);
+    }
+#pragma unroll
+    for (int k = 0; k < 32; k = (k + 9) & ~8) {
+        const uint32_t a = x[k], b = x[k + 8];
+        x[k] = __byte_perm(a, b, 0x6240);
+        x[k + 8] = __byte_perm(a, b, 0x7351);
+    }
+    uint32_t m = 0x0F0F0F0Fu;
+#pragma unroll
+    for (int s = 4; s > 0; s >>= 1, m ^= (m << s)) {
+#pragma unroll
+        for (int k = 0; k < 32; k = (k + s + 1) & ~s) {
+            const uint32_t a = x[k], b = x[k + s];
+            x[k] = (a & m) | ((b << s) & ~m);
+            x[k + s] = ((a >> s) & m) | (b & ~m);
+        }
+    }
+#else
     uint32_t m = 0x0000FFFFu;
-#pragma unroll
     for (int s = 16; s > 0; s >>= 1, m ^= (m << s)) {
-#pragma unroll
         for (int k = 0; k < 32; k = (k + s + 1) & ~s) {
             const uint32_t t = ((x[k] >> s) ^ x[k + s]) & m;
             x[k] ^= t << s;
             x[k + s] ^= t;
         }
     }
+#endif
 }
 
 

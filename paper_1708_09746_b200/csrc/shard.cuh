@@ -376,7 +376,7 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
         {
             const double prods = (double)bp.ntiles * (3.0 * bp.L * 128.0 + 768.0);
             ProfScope ps("k_bottom", 48.0 * Nloc, st, prods * OPS_BS_MUL32);
-            k_bottom<<<grid_for(bp.ntiles, 1, smc, 2), BT_THREADS, bottom_smem(), st>>>(bp);
+            bottom_launch(bp, smc, st);
         }
         if ((s = last("shard bottom")) != GF2X_OK) return s;
         if (debug_stage == 1) {
