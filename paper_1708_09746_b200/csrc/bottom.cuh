@@ -26,25 +26,20 @@
 #define BT_STRIDE 33
 #define BT_REGION (4 * BT_GROUPS * BT_STRIDE)   // words per operand region
 
-// pointmul split by output limbs (limb formulas: see c_pm_terms in gf2x.cu).  Per half h, six
-// products {factor limb mask, gets r, gets v31 r, gets v31^2 r}; bit 0 = first limb of the half
-// (R0 / R2), bit 1 = second (R1 / R3).
-//   R0 = P0 + v31 P1 + v31^2 (P2 + P23)        R1 = P0 + P01 + v31 P23 + v31^2 P3
-//   R2 = P0 + Q0 + v31 (P1 + Q1)               R3 = P0 + P01 + Q0 + Q01
-__constant__ int c_pm_half[2][6][4] = {
-    {{0x1, 0x3, 0x0, 0x0},    // P0  -> R0 R1
-     {0x2, 0x0, 0x1, 0x0},    // P1  -> v31: R0
-     {0x4, 0x0, 0x0, 0x1},    // P2  -> v31^2: R0
-     {0xC, 0x0, 0x2, 0x1},    // P23 -> v31: R1, v31^2: R0
-     {0x3, 0x2, 0x0, 0x0},    // P01 -> R1
-     {0x8, 0x0, 0x0, 0x2}},   // P3  -> v31^2: R1
-    {{0x1, 0x3, 0x0, 0x0},    // P0  -> R2 R3
-     {0x5, 0x3, 0x0, 0x0},    // Q0  -> R2 R3
-     {0x2, 0x0, 0x1, 0x0},    // P1  -> v31: R2
-     {0xA, 0x0, 0x1, 0x0},    // Q1  -> v31: R2
-     {0x3, 0x2, 0x0, 0x0},    // P01 -> R3
-     {0xF, 0x2, 0x0, 0x0}},   // Q01 -> R3
-};
+// pointmul on the planes: the nine TGF(2^32) products of the limb formulas (c_pm_terms in gf2x.cu)
+//   R0 = P0 + v31 P1 + v31^2 (P2 + P23)     R1 = P0 + P01 + v31 P23 + v31^2 P3
+//   R2 = P0 + v31 P1 + Q0 + v31 Q1          R3 = P0 + P01 + Q0 + Q01
+// split over the two threads of a group with the shared parts exchanged through shared memory:
+//   h = 0: P3, P1, P0, P01  -> V3 = v31^2 P3 (kept), X2 = P0 + v31 P1, X3 = P0 + P01 (exchanged)
+//   h = 1: P23, P2, Q1, Q0, Q01 -> W1 = v31 P23, W0 = v31^2 (P2 + P23) (exchanged), A = Q0 + v31 Q1,
+//          B = Q0 + Q01 (kept)
+//   then R0 = X2 + W0, R1 = X3 + W1 + V3 (h = 0) and R2 = X2 + A, R3 = X3 + B (h = 1).
+// factor limb masks per step (bit l = limb l of the sum a_l, b_l)
+__constant__ int c_pm9[2][5] = {{0x8, 0x2, 0x1, 0x3, 0}, {0xC, 0x4, 0xA, 0x5, 0xF}};
+#define BT_EX_X2 0
+#define BT_EX_X3 1
+#define BT_EX_W0 2
+#define BT_EX_W1 3
 
 struct BottomParams {
     uint4* A;            // spectrum of a (in: after the direct passes; out: product, after iFFT bottom)
@@ -201,12 +196,8 @@ __global__ void __launch_bounds__(BT_THREADS, 2 / BT_TPC) k_bottom(BottomParams 
     uint32_t* Pk = bt_smem + BT_TPC * 2 * BT_REGION; // per-layer position planes, L x 32 (shared)
     uint32_t* UCb = Pk + 6 * 32;                     // per tile: U_k of each (layer, pair), BT_TPC x 6 x 32
     uint32_t* UC = UCb + half * 6 * 32;
-#ifdef BT_NO_CK
-    uint32_t* CK = nullptr;
-#else
-    // multiplier-plane cache, only when the tile runs forward and inverse layers
-    uint32_t* CK = (p.mode & 5) == 5 ? UCb + BT_TPC * 6 * 32 + half * 6 * 32 * 33 : nullptr;
-#endif
+    uint32_t* EX = UCb + BT_TPC * 6 * 32 + half * 4 * 64 * 33;   // pointmul exchange sets, 4 x 64 x 33
+    uint32_t* CK = nullptr;   // (a multiplier-plane cache for the inverse layers measured +0.5 %: the space holds EX)
     const int L = p.L;
     // P_k[j] = xor over position bits i (L+i < m) of bit j of s_k(v_(L+i)) * POS_i
     for (int i = threadIdx.x; i < L * 32; i += blockDim.x) {
@@ -241,39 +232,66 @@ __global__ void __launch_bounds__(BT_THREADS, 2 / BT_TPC) k_bottom(BottomParams 
         }
         uint32_t* R = PA;
         if (p.mode & 2) {
-            // two threads per group: thread h = 0 produces result limbs R0, R1, h = 1 produces R2, R3
-            // (six TGF(2^32) products each, accumulated in registers), then both overwrite the A planes
             const int g = tid & (BT_GROUPS - 1), h = tid >> 6;
-            uint32_t acc0[32], acc1[32];
-#pragma unroll
-            for (int j = 0; j < 32; j++) { acc0[j] = 0; acc1[j] = 0; }
+            uint32_t* ex = EX + g * 33;   // exchange set e of group g at ex + e * 64 * 33
+            uint32_t a0[32], a1[32];
 #pragma unroll 1
-            for (int qq = 0; qq < 6; qq++) {
-                const int* T = c_pm_half[h][qq];
+            for (int st = 0; st < 4 + h; st++) {
                 uint32_t x[32], y[32], r[32];
-                bt_load_sum(PA, g, T[0], x);
-                bt_load_sum(PB, g, T[0], y);
+                const int mask = c_pm9[h][st];
+                bt_load_sum(PA, g, mask, x);
+                bt_load_sum(PB, g, mask, y);
                 bs_mul32(x, y, r);
-                // T[1..3]: which of the two output limbs get r, v31 r, v31^2 r (bit 0: first, bit 1: second)
-                if (T[2]) bs_mul_v31(r, x);
-                if (T[3]) bs_mul_v31sq(r, y);
+                switch (h * 5 + st) {
+                    case 0: bs_mul_v31sq(r, a0); break;                                   // V3
+                    case 1: bs_mul_v31(r, a1); break;                                     // v31 P1
+                    case 2:                                                               // X2, then P0
 #pragma unroll
-                for (int j = 0; j < 32; j++) {
-                    uint32_t a0 = acc0[j], a1 = acc1[j];
-                    if (T[1] & 1) a0 ^= r[j];
-                    if (T[1] & 2) a1 ^= r[j];
-                    if (T[2] & 1) a0 ^= x[j];
-                    if (T[2] & 2) a1 ^= x[j];
-                    if (T[3] & 1) a0 ^= y[j];
-                    if (T[3] & 2) a1 ^= y[j];
-                    acc0[j] = a0; acc1[j] = a1;
+                        for (int j = 0; j < 32; j++) { ex[BT_EX_X2 * 64 * 33 + j] = a1[j] ^ r[j]; a1[j] = r[j]; }
+                        break;
+                    case 3:                                                               // X3
+#pragma unroll
+                        for (int j = 0; j < 32; j++) ex[BT_EX_X3 * 64 * 33 + j] = a1[j] ^ r[j];
+                        break;
+                    case 5:                                                               // P23, W1
+                        bs_mul_v31(r, x);
+#pragma unroll
+                        for (int j = 0; j < 32; j++) { a1[j] = r[j]; ex[BT_EX_W1 * 64 * 33 + j] = x[j]; }
+                        break;
+                    case 6:                                                               // W0
+#pragma unroll
+                        for (int j = 0; j < 32; j++) a1[j] ^= r[j];
+                        bs_mul_v31sq(a1, y);
+#pragma unroll
+                        for (int j = 0; j < 32; j++) ex[BT_EX_W0 * 64 * 33 + j] = y[j];
+                        break;
+                    case 7: bs_mul_v31(r, a0); break;                                     // v31 Q1
+                    case 8:                                                               // A, B = Q0
+#pragma unroll
+                        for (int j = 0; j < 32; j++) { a0[j] ^= r[j]; a1[j] = r[j]; }
+                        break;
+                    default:                                                              // B += Q01
+#pragma unroll
+                        for (int j = 0; j < 32; j++) a1[j] ^= r[j];
+                        break;
                 }
             }
-            __syncthreads();   // every thread is done reading A and B
+            __syncthreads();   // A and B planes read, exchange sets written
             uint32_t* d0 = PA + bt_block(g, 2 * h);
             uint32_t* d1 = PA + bt_block(g, 2 * h + 1);
+            if (h == 0) {
 #pragma unroll
-            for (int j = 0; j < 32; j++) { d0[j] = acc0[j]; d1[j] = acc1[j]; }
+                for (int j = 0; j < 32; j++) {
+                    d0[j] = ex[BT_EX_X2 * 64 * 33 + j] ^ ex[BT_EX_W0 * 64 * 33 + j];
+                    d1[j] = ex[BT_EX_X3 * 64 * 33 + j] ^ ex[BT_EX_W1 * 64 * 33 + j] ^ a0[j];
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    d0[j] = ex[BT_EX_X2 * 64 * 33 + j] ^ a0[j];
+                    d1[j] = ex[BT_EX_X3 * 64 * 33 + j] ^ a1[j];
+                }
+            }
             __syncthreads();
         }
         if (p.mode & 4) {
@@ -290,7 +308,7 @@ __global__ void __launch_bounds__(BT_THREADS, 2 / BT_TPC) k_bottom(BottomParams 
     }
 }
 
-static size_t bottom_smem() { return (size_t)(BT_TPC * 2 * BT_REGION + 6 * 32 + BT_TPC * 6 * 32 * 34) * 4; }
+static size_t bottom_smem() { return (size_t)(BT_TPC * 2 * BT_REGION + 6 * 32 + BT_TPC * (6 * 32 + 4 * 64 * 33)) * 4; }
 
 static int grid_for(uint64_t items, int per_block, int sm_count, int occ);
 static void bottom_launch(const BottomParams& bp, int smc, cudaStream_t st) {

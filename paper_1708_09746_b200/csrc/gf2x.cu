@@ -647,13 +647,13 @@ struct FftPass {
 // forward order (top-down); the first pass also applies changeRepr.  The high layers [bot, m) go to
 // table passes of <= 6 layers for the changeRepr pass (its 32 KB psi table) and <= 7 below it (127 M4R
 // tables, 64 KB; their tables are rebuilt only when the tile's bits >= k_hi change); layers
-// [0, min(m, bot)) form the bit-sliced bottom pass.  A table butterfly costs about half a bit-sliced one
-// (measured), so the bottom takes 5 layers unless that needs one more table pass than 6 would.
+// [0, min(m, bot)) form the bit-sliced bottom pass: 6 layers (5 measured 0.5 % slower at c4b, 8 % at c3),
+// except for short transforms (m <= 10: one table pass either way; 5 measured 10 % faster at c2).
 static int fft_passes(int H, int maxr) { return H <= 0 ? 0 : (H <= 6 ? 1 : 1 + (H - 6 + maxr - 1) / maxr); }
 static std::vector<FftPass> plan_fft(int m) {
     static const int maxr = getenv("GF2X_MAXR") ? atoi(getenv("GF2X_MAXR")) : 7;
     static const int forced = getenv("GF2X_BOT_B") ? atoi(getenv("GF2X_BOT_B")) : 0;
-    const int bot = forced ? forced : (fft_passes(m - 5, maxr) <= fft_passes(m - 6, maxr) ? 5 : 6);
+    const int bot = forced ? forced : (m <= 10 ? 5 : 6);
     std::vector<FftPass> v;
     const int H = m > bot ? m - bot : 0;
     const int np = fft_passes(H, maxr);
@@ -930,7 +930,7 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         bp.map = IdxMap{0, 0, 0};
         bp.mode = stop_stage == 2 ? 1 : (stop_stage == 3 ? 3 : 7);
         // bit-sliced products per 2^11-element tile: 2L forward + L inverse layers x 128, pointmul 768
-        const double prods = (double)bp.ntiles * (3.0 * bp.L * 128.0 + 768.0);
+        const double prods = (double)bp.ntiles * (3.0 * bp.L * 128.0 + 576.0);
         ProfScope ps("k_bottom", 48.0 * P.N * P.batch, st, prods * OPS_BS_MUL32);
         bottom_launch(bp, smc, st);
         cudaError_t e = cudaGetLastError();

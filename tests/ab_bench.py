@@ -1,7 +1,8 @@
 """A/B kernel timing for tuning: per-kernel device ms of one config for several builds of the library.
 
-python tests/ab_bench.py CONFIG REPS LIB [LIB ...]      (run on the GPU box; alternates the libraries
-in fresh subprocesses, 3 rounds, prints the per-kernel median ms per multiply of each)
+python tests/ab_bench.py CONFIG REPS LIB[@VAR=VAL,...] [...]   (run on the GPU box; alternates the
+libraries in fresh subprocesses, 3 rounds, prints the per-kernel median ms per multiply of each; the
+optional @VAR=VAL list sets environment knobs of that run, e.g. lib.so@GF2X_BOT_B=6)
 """
 import json
 import os
@@ -41,7 +42,10 @@ if __name__ == "__main__":
     res = {l: [] for l in libs}
     for _ in range(3):
         for l in libs:
-            out = subprocess.run([sys.executable, __file__, "--child", cfg, reps, l], capture_output=True, text=True)
+            path, _, knobs = l.partition("@")
+            env = dict(os.environ, **dict(kv.split("=", 1) for kv in knobs.split(",") if kv))
+            out = subprocess.run([sys.executable, __file__, "--child", cfg, reps, path], capture_output=True, text=True,
+                                 env=env)
             if out.returncode:
                 print(out.stderr[-2000:])
                 sys.exit(1)
@@ -49,4 +53,4 @@ if __name__ == "__main__":
     for l in libs:
         ks = res[l][0].keys()
         med = {k: round(statistics.median(r[k] for r in res[l]), 4) for k in ks}
-        print(os.path.basename(l), round(sum(med.values()), 4), med)
+        print(os.path.basename(l).replace(' ', ''), round(sum(med.values()), 4), med)
