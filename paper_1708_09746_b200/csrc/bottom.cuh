@@ -217,9 +217,12 @@ __global__ void __launch_bounds__(BT_THREADS, 2 / BT_TPC) k_bottom(BottomParams 
         __syncthreads();
         for (int i = tid; i < L * 32; i += BT_HALF) UC[i] = bt_u(i >> 5, i & 31, e0, L, p.m, p.map);
         // ---- load + bit-slice both operands (warp = limb, lane = group)
-        for (int g = lane; g < BT_GROUPS; g += 32) {
-            bt_load_block(p.A, e0, total, g, lb, L, PA);
-            bt_load_block(p.B, e0, total, g, lb, L, PB);
+        // (one rolled loop: this straight-line code runs once per tile and would otherwise miss the
+        // instruction caches on every copy)
+#pragma unroll 1
+        for (int it = 0; it < 2 * BT_GROUPS / 32; it++) {
+            const int g = lane + 32 * (it >> 1);
+            bt_load_block((it & 1) ? p.B : p.A, e0, total, g, lb, L, (it & 1) ? PB : PA);
         }
         __syncthreads();
         if (p.mode & 1) {
@@ -301,9 +304,11 @@ __global__ void __launch_bounds__(BT_THREADS, 2 / BT_TPC) k_bottom(BottomParams 
             }
         }
         // ---- un-slice and store (A <- R; with mode == 1 also B <- its planes)
-        for (int g = lane; g < BT_GROUPS; g += 32) {
-            bt_store_block(p.A, e0, total, g, lb, L, R);
-            if (p.mode == 1) bt_store_block(p.B, e0, total, g, lb, L, PB);
+        const int nst = (p.mode == 1 ? 2 : 1) * BT_GROUPS / 32;
+#pragma unroll 1
+        for (int it = 0; it < nst; it++) {
+            const int g = lane + 32 * (it & 1);
+            bt_store_block((it & 2) ? p.B : p.A, e0, total, g, lb, L, (it & 2) ? PB : R);
         }
     }
 }
