@@ -74,6 +74,14 @@ def lib():
             "or_fft_constant": (None, [i32, i32, u64, _u64p]),
             "or_fft_mult_count": (u64, [i32]),
             "or_alg5_mul": (i32, [_u64p, u64, _u64p, u64, _u64p] + [_u64p] * 7),
+            "or_tower256_mul": (None, [_u64p, _u64p, _u64p]),
+            "or_gf256p_mul": (None, [_u64p, _u64p, _u64p]),
+            "or_psi256_init": (i32, []),
+            "or_psi256": (None, [_u64p, _u64p]),
+            "or_psi256_inv": (None, [_u64p, _u64p]),
+            "or_psi256_generator": (None, [i32, _u64p]),
+            "or_fft256": (None, [_u64p, i32]),
+            "or_alg5_mul_w128": (i32, [_u64p, u64, _u64p, u64, _u64p] + [_u64p] * 4),
             "or_is_irreducible64": (i32, [u64]),
             "or_poly_mod": (u64, [_u64p, sz, u64]),
             "or_mulmod64": (u64, [u64, u64, u64]),
@@ -266,6 +274,86 @@ def alg5_mul(a: np.ndarray, a_bits: int, b: np.ndarray, b_bits: int, stages: boo
         raise RuntimeError(f"oracle alg5 internal assertion failed: {err}")
     if stages:
         return c, {k: v.reshape(-1, 2) for k, v in st.items()}
+    return c
+
+
+# ---------------------------------------------------------------- O3, w = 128 (TGF(2^256))
+def _u256(x: int) -> np.ndarray:
+    return np.array([(x >> (64 * i)) & 0xFFFFFFFFFFFFFFFF for i in range(4)], dtype=np.uint64)
+
+
+def _int256(a: np.ndarray) -> int:
+    return sum(int(a[i]) << (64 * i) for i in range(4))
+
+
+def tower256_mul(a: int, b: int) -> int:
+    r = np.zeros(4, dtype=np.uint64)
+    A, B = _u256(a), _u256(b)
+    lib().or_tower256_mul(_p(A), _p(B), _p(r))
+    return _int256(r)
+
+
+def gf256p_mul(a: int, b: int) -> int:
+    """GF(2^256) = GF(2)[z]/(z^256+z^10+z^5+z^2+1), polynomial basis (R20)."""
+    r = np.zeros(4, dtype=np.uint64)
+    A, B = _u256(a), _u256(b)
+    lib().or_gf256p_mul(_p(A), _p(B), _p(r))
+    return _int256(r)
+
+
+def psi256(x: int) -> int:
+    r = np.zeros(4, dtype=np.uint64)
+    X = _u256(x)
+    lib().or_psi256(_p(X), _p(r))
+    return _int256(r)
+
+
+def psi256_inv(x: int) -> int:
+    r = np.zeros(4, dtype=np.uint64)
+    X = _u256(x)
+    lib().or_psi256_inv(_p(X), _p(r))
+    return _int256(r)
+
+
+def psi256_generator(k: int) -> int:
+    r = np.zeros(4, dtype=np.uint64)
+    lib().or_psi256_generator(k, _p(r))
+    return _int256(r)
+
+
+def fft256(g: np.ndarray) -> np.ndarray:
+    """FFT_LCH at alpha=0 on N=2^m TGF(2^256) elements given as (N,4) uint64."""
+    g = np.array(g, dtype=np.uint64, copy=True).reshape(-1, 4)
+    m = len(g).bit_length() - 1
+    assert 1 << m == len(g)
+    flat = np.ascontiguousarray(g.reshape(-1))
+    lib().or_fft256(_p(flat), m)
+    return flat.reshape(-1, 4)
+
+
+W128_STAGES = ("cvt_a", "fft_a", "prod", "icvt")
+
+
+def alg5_mul_w128(a: np.ndarray, a_bits: int, b: np.ndarray, b_bits: int, stages: bool = False):
+    """Alg. 5 with 128-bit blocks over TGF(2^256); returns c (na+nb words) or (c, stage arrays (N,4))."""
+    a = np.ascontiguousarray(a, dtype=np.uint64)
+    b = np.ascontiguousarray(b, dtype=np.uint64)
+    na, nb = (a_bits + 63) // 64, (b_bits + 63) // 64
+    assert len(a) >= na and len(b) >= nb
+    c = np.zeros(na + nb, dtype=np.uint64)
+    st = {}
+    if stages and a_bits and b_bits:
+        L = (a_bits + 127) // 128 + (b_bits + 127) // 128 - 1
+        N = 1 << max(0, (L - 1).bit_length())
+        for k in W128_STAGES:
+            st[k] = np.zeros(4 * N, dtype=np.uint64)
+    err = lib().or_alg5_mul_w128(_p(a if len(a) else np.zeros(1, np.uint64)), a_bits,
+                                 _p(b if len(b) else np.zeros(1, np.uint64)), b_bits, _p(c),
+                                 *[_nullable(st.get(k)) for k in W128_STAGES])
+    if err != 0:
+        raise RuntimeError(f"oracle alg5 (w=128) internal assertion failed: {err}")
+    if stages:
+        return c, {k: v.reshape(-1, 4) for k, v in st.items()}
     return c
 
 

@@ -21,6 +21,8 @@
  *         changeRepr (sec 4.3) fixed by the deterministic rule of DESIGN.md R9;
  *         BasisCvt = Alg. 3 with VarSubs = Alg. 2, iBasisCvt (R7);
  *         FFT_LCH = Alg. 1, iFFT (R8); pointmul; InterleavedCombine.
+ *       w = 128 variant (sec 4.2): TGF(2^256) one tower level up, GF(2^256) modulo
+ *       z^256+z^10+z^5+z^2+1 (R20) and changeRepr_256 by the same rule, Alg. 5 on 128-bit blocks.
  *   O4  product check modulo random irreducible degree-64 polynomials.
  *
  * All arithmetic is exact (GF(2) AND/XOR); no floating point anywhere.
@@ -620,6 +622,234 @@ int or_alg5_mul(const uint64_t *a, uint64_t a_bits, const uint64_t *b, uint64_t 
         if (w < N) v ^= (uint64_t)A[w];
         if (w >= 1 && w - 1 < N) v ^= (uint64_t)(A[w - 1] >> 64);
         c[w] = v;
+    }
+    free_constants(C, m);
+    free(A); free(B);
+    return err;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* O3 w = 128: Alg. 5 with 128-bit blocks over TGF(2^256) ("An initial block width of w=128 bits */
+/* is also possible and in this case the operative field is TGF(2^256)"; sec 4.2     */
+/* P:1077-1114).                                                                                */
+/*   TGF(2^256) = TGF(2^128)[x_8]/(x_8^2 + x_8 + P), P = x_1...x_7 = v_127: the tower definition */
+/*    one level up; an element is (lo, hi) = lo + hi x_8 (bit k <-> v_k, k < 256).    */
+/*   GF(2^256) in polynomial basis = GF(2)[z]/(z^256 + z^10 + z^5 + z^2 + 1) (R20: the  */
+/*   paper names no degree-256 modulus; this pentanomial is irreducible, pinned by a Rabin test). */
+/*   changeRepr_256 follows R9's rule: X_1^2+X_1 = 1, X_k^2+X_k = X_1...X_(k-1), k <= 8, each the */
+/*   numerically smaller root; v_k -> prod_{bit j of k} X_(j+1).                                 */
+/* ------------------------------------------------------------------------------------------ */
+typedef struct { u128 lo, hi; } u256;
+static inline u256 u256_xor(u256 a, u256 b) { u256 r = {a.lo ^ b.lo, a.hi ^ b.hi}; return r; }
+static inline int u256_bit(u256 a, int i) { return (int)((i < 128 ? a.lo >> i : a.hi >> (i - 128)) & 1); }
+static inline u256 u256_one(int i) {
+    u256 r = {0, 0};
+    if (i < 128) r.lo = ((u128)1) << i; else r.hi = ((u128)1) << (i - 128);
+    return r;
+}
+static inline int u256_less(u256 a, u256 b) { return a.hi != b.hi ? a.hi < b.hi : a.lo < b.lo; }
+static inline int u256_eq(u256 a, u256 b) { return a.hi == b.hi && a.lo == b.lo; }
+
+/* Karatsuba at level 8 (sec 4.1.3): lo = a0b0 + a1b1 P, hi = (a0+a1)(b0+b1) + a0b0;
+ * with one operand in TGF(2^128) it drops to two level-7 products (Prop. 2). */
+static u256 tmul256(u256 a, u256 b) {
+    u256 r;
+    if (b.hi == 0) { r.lo = tmul(a.lo, b.lo, 7); r.hi = tmul(a.hi, b.lo, 7); return r; }
+    if (a.hi == 0) { r.lo = tmul(a.lo, b.lo, 7); r.hi = tmul(a.lo, b.hi, 7); return r; }
+    const u128 P = ((u128)1) << 127;   /* v_127 */
+    u128 p0 = tmul(a.lo, b.lo, 7), p2 = tmul(a.hi, b.hi, 7), p1 = tmul(a.lo ^ a.hi, b.lo ^ b.hi, 7);
+    r.lo = p0 ^ tmul(p2, P, 7);
+    r.hi = p1 ^ p0;
+    return r;
+}
+static inline u256 mk256(const uint64_t *w) { u256 r = {mk(w[0], w[1]), mk(w[2], w[3])}; return r; }
+static inline void unmk256(u256 x, uint64_t *w) { unmk(x.lo, w); unmk(x.hi, w + 2); }
+void or_tower256_mul(const uint64_t *a, const uint64_t *b, uint64_t *r) {
+    tower_init();
+    unmk256(tmul256(mk256(a), mk256(b)), r);
+}
+
+/* GF(2^256) polynomial basis: multiply by z modulo z^256 + z^10 + z^5 + z^2 + 1, shift-and-add */
+static inline u256 gf256p_mulz(u256 a) {
+    int carry = (int)(a.hi >> 127);
+    a.hi = (a.hi << 1) | (a.lo >> 127);
+    a.lo <<= 1;
+    if (carry) a.lo ^= (u128)0x425;   /* z^10 + z^5 + z^2 + 1 */
+    return a;
+}
+static u256 gf256p_mul(u256 a, u256 b) {
+    u256 acc = {0, 0};
+    for (int i = 0; i < 256; i++) {
+        if (u256_bit(b, i)) acc = u256_xor(acc, a);
+        a = gf256p_mulz(a);
+    }
+    return acc;
+}
+void or_gf256p_mul(const uint64_t *a, const uint64_t *b, uint64_t *r) { unmk256(gf256p_mul(mk256(a), mk256(b)), r); }
+
+/* Gauss-Jordan on a 256 x 256 GF(2) system given by the images col[i] of the unit vectors:
+ * solves M x = c (returns 0 and the solution with free variables 0, or -1), used for the
+ * Artin-Schreier equations r^2 + r = c (kernel {0, 1}) and for inverting changeRepr_256. */
+static int solve256(const u256 *col, u256 c, u256 *x_out) {
+    static u256 row[256]; static int rhs[256], pivcol[256];
+    for (int r = 0; r < 256; r++) {
+        u256 v = {0, 0};
+        for (int i = 0; i < 256; i++) if (u256_bit(col[i], r)) v = u256_xor(v, u256_one(i));
+        row[r] = v; rhs[r] = u256_bit(c, r);
+    }
+    int nr = 0;
+    for (int cidx = 0; cidx < 256 && nr < 256; cidx++) {
+        int p = -1;
+        for (int r = nr; r < 256; r++) if (u256_bit(row[r], cidx)) { p = r; break; }
+        if (p < 0) continue;
+        u256 t = row[p]; row[p] = row[nr]; row[nr] = t;
+        int tr = rhs[p]; rhs[p] = rhs[nr]; rhs[nr] = tr;
+        for (int r = 0; r < 256; r++)
+            if (r != nr && u256_bit(row[r], cidx)) { row[r] = u256_xor(row[r], row[nr]); rhs[r] ^= rhs[nr]; }
+        pivcol[nr] = cidx; nr++;
+    }
+    for (int r = nr; r < 256; r++) if (rhs[r]) return -1;
+    u256 x = {0, 0};
+    for (int r = 0; r < nr; r++) if (rhs[r]) x = u256_xor(x, u256_one(pivcol[r]));
+    *x_out = x;
+    return 0;
+}
+
+static u256 g_Mcol256[256], g_psicol256[256], g_X256[9];
+static int g_psi256_ready = 0;
+static int psi256_init(void) {
+    if (g_psi256_ready) return 0;
+    static u256 asc[256];   /* L(x) = x^2 + x on the unit vectors */
+    for (int i = 0; i < 256; i++) { u256 e = u256_one(i); asc[i] = u256_xor(gf256p_mul(e, e), e); }
+    u256 prod = u256_one(0);
+    for (int k = 1; k <= 8; k++) {
+        u256 r;
+        if (solve256(asc, prod, &r) != 0) return -1;
+        u256 alt = u256_xor(r, u256_one(0));   /* the other root */
+        g_X256[k] = u256_less(alt, r) ? alt : r;
+        prod = gf256p_mul(prod, g_X256[k]);
+    }
+    for (int k = 0; k < 256; k++) {
+        u256 v = u256_one(0);
+        for (int j = 0; j < 8; j++) if ((k >> j) & 1) v = gf256p_mul(v, g_X256[j + 1]);
+        g_Mcol256[k] = v;
+    }
+    /* psi_256 = Mcol^-1: column c = the solution of M x = e_c */
+    for (int c = 0; c < 256; c++)
+        if (solve256(g_Mcol256, u256_one(c), &g_psicol256[c]) != 0) return -2;
+    g_psi256_ready = 1;
+    return 0;
+}
+static u256 apply_cols256(const u256 *cols, u256 x) {
+    u256 r = {0, 0};
+    for (int i = 0; i < 256; i++) if (u256_bit(x, i)) r = u256_xor(r, cols[i]);
+    return r;
+}
+static inline u256 psi256(u256 x) { return apply_cols256(g_psicol256, x); }      /* poly -> tower */
+static inline u256 psi256_inv(u256 x) { return apply_cols256(g_Mcol256, x); }   /* tower -> poly */
+int or_psi256_init(void) { return psi256_init(); }
+void or_psi256(const uint64_t *x, uint64_t *r) { psi256_init(); unmk256(psi256(mk256(x)), r); }
+void or_psi256_inv(const uint64_t *x, uint64_t *r) { psi256_init(); unmk256(psi256_inv(mk256(x)), r); }
+void or_psi256_generator(int k, uint64_t *r) { psi256_init(); unmk256(g_X256[k], r); }
+
+/* FFT_LCH / iFFT_LCH (Alg. 1) on TGF(2^256) elements; the multipliers are the
+ * same s_k(phi_v(b)) as at w = 64 (they lie in the subfield spanned by v_0..v_(m-1)). */
+static void fft256(u256 *A, int m, u128 **C) {
+    for (int k = m - 1; k >= 0; k--) {
+        size_t half = (size_t)1 << k, nb = (size_t)1 << (m - k - 1);
+#pragma omp parallel for schedule(static) if (nb * half >= 4096)
+        for (size_t j = 0; j < nb; j++) {
+            size_t b = j << (k + 1);
+            u256 c = {C[k][j], 0};
+            for (size_t i = 0; i < half; i++) {
+                A[b + i] = u256_xor(A[b + i], tmul256(A[b + half + i], c));
+                A[b + half + i] = u256_xor(A[b + half + i], A[b + i]);
+            }
+        }
+    }
+}
+static void ifft256(u256 *A, int m, u128 **C) {
+    for (int k = 0; k < m; k++) {
+        size_t half = (size_t)1 << k, nb = (size_t)1 << (m - k - 1);
+#pragma omp parallel for schedule(static) if (nb * half >= 4096)
+        for (size_t j = 0; j < nb; j++) {
+            size_t b = j << (k + 1);
+            u256 c = {C[k][j], 0};
+            for (size_t i = 0; i < half; i++) {
+                A[b + half + i] = u256_xor(A[b + half + i], A[b + i]);
+                A[b + i] = u256_xor(A[b + i], tmul256(A[b + half + i], c));
+            }
+        }
+    }
+}
+void or_fft256(uint64_t *data, int m) {
+    tower_init();
+    size_t n = (size_t)1 << m;
+    u256 *A = (u256 *)malloc(n * sizeof(u256));
+    u128 **C = all_constants(m);
+    for (size_t i = 0; i < n; i++) A[i] = mk256(data + 4 * i);
+    fft256(A, m, C);
+    for (size_t i = 0; i < n; i++) unmk256(A[i], data + 4 * i);
+    free_constants(C, m); free(A);
+}
+
+/* Alg. 5 with w = 128.  Stage dumps (optional, N x 4 words, tower elements): after changeRepr,
+ * after FFT_LCH (a), after pointmul, after iBasisCvt.  c receives na+nb 64-bit words. */
+int or_alg5_mul_w128(const uint64_t *a, uint64_t a_bits, const uint64_t *b, uint64_t b_bits, uint64_t *c,
+                     uint64_t *st_cvt_a, uint64_t *st_fft_a, uint64_t *st_prod, uint64_t *st_icvt) {
+    tower_init();
+    if (psi256_init() != 0) return -10;
+    size_t na = (a_bits + 63) / 64, nb = (b_bits + 63) / 64;
+    if (a_bits == 0 || b_bits == 0) { memset(c, 0, (na + nb) * sizeof(uint64_t)); return 0; }
+    size_t ma = (a_bits + 127) / 128, mb = (b_bits + 127) / 128;   /* 128-bit blocks */
+    size_t L = ma + mb - 1;
+    int m = ceil_log2_sz(L);
+    size_t N = (size_t)1 << m;
+    u128 *Fa = (u128 *)calloc(N, sizeof(u128)), *Fb = (u128 *)calloc(N, sizeof(u128));
+    /* Split into 128-bit blocks (w = 128): block j = words 2j, 2j+1; bits >= a_bits masked */
+    for (uint64_t i = 0; i < a_bits; i++) if ((a[i >> 6] >> (i & 63)) & 1) Fa[i >> 7] |= ((u128)1) << (i & 127);
+    for (uint64_t i = 0; i < b_bits; i++) if ((b[i >> 6] >> (i & 63)) & 1) Fb[i >> 7] |= ((u128)1) << (i & 127);
+    /* BasisCvt on the 128-bit blocks (XOR-only on whole blocks) */
+    cvt(Fa, 0, m, 0); cvt(Fb, 0, m, 0);
+    /* changeRepr into TGF(2^256): the block is an element of degree < 128 */
+    u256 *A = (u256 *)malloc(N * sizeof(u256)), *B = (u256 *)malloc(N * sizeof(u256));
+#pragma omp parallel for schedule(static) if (N >= 4096)
+    for (size_t i = 0; i < N; i++) {
+        u256 xa = {Fa[i], 0}, xb = {Fb[i], 0};
+        A[i] = psi256(xa); B[i] = psi256(xb);
+    }
+    free(Fa); free(Fb);
+    if (st_cvt_a) for (size_t i = 0; i < N; i++) unmk256(A[i], st_cvt_a + 4 * i);
+    u128 **C = all_constants(m);
+    fft256(A, m, C); fft256(B, m, C);
+    if (st_fft_a) for (size_t i = 0; i < N; i++) unmk256(A[i], st_fft_a + 4 * i);
+#pragma omp parallel for schedule(static) if (N >= 4096)
+    for (size_t i = 0; i < N; i++) A[i] = tmul256(A[i], B[i]);   /* pointmul P:898-899 */
+    if (st_prod) for (size_t i = 0; i < N; i++) unmk256(A[i], st_prod + 4 * i);
+    ifft256(A, m, C);
+    /* iBasisCvt in the tower representation: XOR-only on whole 256-bit units, i.e. the
+     * same network applied to the low and the high 128-bit halves */
+    u128 *Lo = (u128 *)malloc(N * sizeof(u128)), *Hi = (u128 *)malloc(N * sizeof(u128));
+    for (size_t i = 0; i < N; i++) { Lo[i] = A[i].lo; Hi[i] = A[i].hi; }
+    icvt(Lo, 0, m, 0); icvt(Hi, 0, m, 0);
+    for (size_t i = 0; i < N; i++) { A[i].lo = Lo[i]; A[i].hi = Hi[i]; }
+    free(Lo); free(Hi);
+    if (st_icvt) for (size_t i = 0; i < N; i++) unmk256(A[i], st_icvt + 4 * i);
+    /* changeRepr back */
+    int err = 0;
+#pragma omp parallel for schedule(static) if (N >= 4096)
+    for (size_t i = 0; i < N; i++) A[i] = psi256_inv(A[i]);
+    for (size_t i = 0; i < N; i++) {
+        if ((A[i].hi >> 127) & 1) err = -1;                        /* deg C_i <= 254 */
+        if (i >= L && (A[i].lo | A[i].hi) != 0) err = -2;
+    }
+    /* InterleavedCombine on 128-bit blocks: out[w] = lo128(C_w) ^ hi128(C_(w-1)) */
+    for (size_t w = 0; w < na + nb; w++) {
+        size_t blk = w >> 1;
+        u128 v = 0;
+        if (blk < N) v ^= A[blk].lo;
+        if (blk >= 1 && blk - 1 < N) v ^= A[blk - 1].hi;
+        c[w] = (w & 1) ? (uint64_t)(v >> 64) : (uint64_t)v;
     }
     free_constants(C, m);
     free(A); free(B);
