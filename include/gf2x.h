@@ -70,6 +70,22 @@ int gf2x_launch_count(uint64_t a_bits, uint64_t b_bits, int64_t batch);
 gf2x_status gf2x_debug_stage(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits,
                              int stage, uint64_t* out, void* stream);
 
+/* Block width (sec 4.2): Alg. 5 with w-bit blocks
+ * over TGF(2^(2w)).  w = 64 is gf2x_mul_batched (TGF(2^128)); w = 128 splits the operands into
+ * 128-bit blocks, converts them into TGF(2^256) = TGF(2^128)[x_8]/(x_8^2 + x_8 + v_127) through
+ * GF(2)[z]/(z^256 + z^10 + z^5 + z^2 + 1) (R20) and runs the FFT on half as many points.
+ * Same operands, output, memory and error contract as gf2x_mul_batched (the library's per-stream
+ * workspace cache is used); EINVAL for other w.  The result is the same exact product. */
+gf2x_status gf2x_mul_w(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
+                       int64_t batch, int w, void* stream);
+/* kernels one gf2x_mul_w call enqueues (0 for unsupported w) */
+int gf2x_launch_count_w(uint64_t a_bits, uint64_t b_bits, int64_t batch, int w);
+/* w = 128 debug / parity hook: operand a's TGF(2^256) spectrum (N x 4 words, DEVICE; element i =
+ * words 4i..4i+3, coordinates of v_0..v_255) after stage 1 (changeRepr), 2 (FFT_LCH), 3 (pointmul)
+ * or 5 (iBasisCvt); N = 2^ceil(log2(ceil(a_bits/128) + ceil(b_bits/128) - 1)).  EINVAL otherwise. */
+gf2x_status gf2x_debug_stage_w128(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, int stage,
+                                  uint64_t* out, void* stream);
+
 /* ---------------------------------------------------------------------------------------------
  * Multi-GPU: the FFT partitioned across G = nranks ranks, one process per GPU (the
  * decomposition is described in DESIGN.md §9).  NCCL is loaded at run time (libnccl.so.2).

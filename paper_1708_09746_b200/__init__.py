@@ -23,7 +23,7 @@ EXPORTS = [
     "gf2x_mul", "gf2x_mul_batched", "gf2x_workspace_bytes", "gf2x_mul_ws", "gf2x_launch_count",
     "gf2x_debug_stage", "gf2x_comm_unique_id", "gf2x_comm_init", "gf2x_comm_destroy", "gf2x_mul_sharded",
     "gf2x_mul_sharded_sim", "gf2x_debug_shard_stage", "gf2x_shard_plan", "gf2x_profile_enable", "gf2x_profile_report", "gf2x_status_string", "gf2x_last_error",
-    "gf2x_release", "gf2x_version",
+    "gf2x_release", "gf2x_version", "gf2x_mul_w", "gf2x_launch_count_w", "gf2x_debug_stage_w128",
 ]
 
 
@@ -50,6 +50,11 @@ def load(path: str = LIB_PATH):
     L.gf2x_mul_ws.argtypes = [vp, u64, vp, u64, vp, i64, vp, sz, vp]
     L.gf2x_launch_count.argtypes = [u64, u64, i64]
     L.gf2x_debug_stage.argtypes = [vp, u64, vp, u64, i32, vp, vp]
+    L.gf2x_mul_w.argtypes = [vp, u64, vp, u64, vp, i64, i32, vp]
+    L.gf2x_mul_w.restype = i32
+    L.gf2x_launch_count_w.argtypes = [u64, u64, i64, i32]
+    L.gf2x_debug_stage_w128.argtypes = [vp, u64, vp, u64, i32, vp, vp]
+    L.gf2x_debug_stage_w128.restype = i32
     L.gf2x_status_string.argtypes = [i32]
     L.gf2x_status_string.restype = ctypes.c_char_p
     L.gf2x_last_error.restype = ctypes.c_char_p
@@ -117,6 +122,30 @@ def gf2x_mul_batched(a, a_bits: int, b, b_bits: int, batch: int, c=None, stream=
         c = torch.empty(batch, n_out, dtype=torch.uint64, device=a.device)
     _check(load().gf2x_mul_batched(_ptr(a), a_bits, _ptr(b), b_bits, _ptr(c), batch, _stream_ptr(stream)))
     return c
+
+
+def gf2x_mul_w(a, a_bits: int, b, b_bits: int, w: int = 128, batch: int = 1, c=None, stream=None):
+    """Alg. 5 with w-bit blocks (w = 64: TGF(2^128); w = 128: TGF(2^256)); same layout as gf2x_mul_batched."""
+    import torch
+    n_out = nwords(a_bits) + nwords(b_bits)
+    if c is None:
+        c = torch.empty(batch, n_out, dtype=torch.uint64, device=a.device)
+    _check(load().gf2x_mul_w(_ptr(a), a_bits, _ptr(b), b_bits, _ptr(c), batch, w, _stream_ptr(stream)))
+    return c
+
+
+def gf2x_launch_count_w(a_bits: int, b_bits: int, batch: int = 1, w: int = 128) -> int:
+    return int(load().gf2x_launch_count_w(a_bits, b_bits, batch, w))
+
+
+def gf2x_debug_stage_w128(a, a_bits: int, b, b_bits: int, stage: int, stream=None):
+    """w = 128: operand a's TGF(2^256) spectrum (N, 4) after `stage` (1, 2, 3 or 5)."""
+    import torch
+    L = (a_bits + 127) // 128 + (b_bits + 127) // 128 - 1
+    N = 1 << max(0, (L - 1).bit_length())
+    out = torch.empty(N, 4, dtype=torch.uint64, device=a.device)
+    _check(load().gf2x_debug_stage_w128(_ptr(a), a_bits, _ptr(b), b_bits, stage, _ptr(out), _stream_ptr(stream)))
+    return out
 
 
 def gf2x_workspace_bytes(a_bits: int, b_bits: int, batch: int = 1) -> int:

@@ -46,7 +46,7 @@ struct BottomParams {
     uint4* B;            // spectrum of b
     uint64_t total;      // batch * N elements per operand (A and B may be adjacent: never touch beyond)
     uint64_t ntiles;     // ceil(total / 2^11)
-    int m, L, mode;      // mode bit0: forward layers, bit1: pointmul, bit2: inverse layers
+    int m, L, mode;      // mode bit0: forward layers (A and B), bit1: pointmul (A <- A B), bit2: inverse layers (A)
     IdxMap map;          // local -> global index for the multipliers (identity unless sharded;
                          // the bottom layers and position bits are always below map.pos)
 };
@@ -219,10 +219,12 @@ __global__ void __launch_bounds__(BT_THREADS, 2 / BT_TPC) k_bottom(BottomParams 
         // ---- load + bit-slice both operands (warp = limb, lane = group)
         // (one rolled loop: this straight-line code runs once per tile and would otherwise miss the
         // instruction caches on every copy)
+        const int nld = (p.mode & 3) ? 2 : 1;   // inverse-only tiles (mode 4) need no B
 #pragma unroll 1
-        for (int it = 0; it < 2 * BT_GROUPS / 32; it++) {
-            const int g = lane + 32 * (it >> 1);
-            bt_load_block((it & 1) ? p.B : p.A, e0, total, g, lb, L, (it & 1) ? PB : PA);
+        for (int it = 0; it < nld * BT_GROUPS / 32; it++) {
+            const int g = lane + 32 * (nld == 2 ? (it >> 1) : it);
+            const bool isb = nld == 2 && (it & 1);
+            bt_load_block(isb ? p.B : p.A, e0, total, g, lb, L, isb ? PB : PA);
         }
         __syncthreads();
         if (p.mode & 1) {

@@ -10,6 +10,7 @@
 #pragma once
 #include <stdint.h>
 #include <string.h>
+#include <utility>
 
 namespace gf2x_host {
 
@@ -166,6 +167,116 @@ static inline Isomorphism build_isomorphism() {
     }
     iso.ok = true;
     return iso;
+}
+
+
+// ----------------------------------------------------------- w = 128: GF(2^256) and changeRepr_256
+// GF(2)[z]/(z^256 + z^10 + z^5 + z^2 + 1) (R20), elements as 4 little-endian words.  The
+// w = 128 variant embeds 128-bit blocks here and maps them to TGF(2^256) =
+// TGF(2^128)[x_8]/(x_8^2 + x_8 + v_127) by the R9 rule one level up.
+struct W256 {
+    uint64_t w[4];
+};
+static inline W256 w256_zero() { W256 r; memset(&r, 0, sizeof(r)); return r; }
+static inline W256 w256_unit(int i) { W256 r = w256_zero(); r.w[i >> 6] = 1ull << (i & 63); return r; }
+static inline int w256_bit(const W256& a, int i) { return (int)((a.w[i >> 6] >> (i & 63)) & 1); }
+static inline void w256_xor(W256& a, const W256& b) { for (int i = 0; i < 4; i++) a.w[i] ^= b.w[i]; }
+static inline bool w256_less(const W256& a, const W256& b) {
+    for (int i = 3; i >= 0; i--) if (a.w[i] != b.w[i]) return a.w[i] < b.w[i];
+    return false;
+}
+
+// a * b: schoolbook over 64-bit digits into 8 words, then reduction of words 4..7 by the modulus
+static inline W256 gf256p_mul(const W256& a, const W256& b) {
+    uint64_t t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < 4; i++)
+        for (int j = 0; j < 4; j++)
+            for (int k = 0; k < 64; k++)
+                if ((b.w[j] >> k) & 1) {   // a.w[i] * z^(64 (i+j) + k)
+                    const int sh = k, dst = i + j;
+                    t[dst] ^= a.w[i] << sh;
+                    if (sh) t[dst + 1] ^= a.w[i] >> (64 - sh);
+                }
+    // z^256 = z^10 + z^5 + z^2 + 1: fold bits >= 256 from the top down
+    for (int bit = 511; bit >= 256; bit--)
+        if ((t[bit >> 6] >> (bit & 63)) & 1) {
+            t[bit >> 6] ^= 1ull << (bit & 63);
+            const int base = bit - 256;
+            const int offs[4] = {0, 2, 5, 10};
+            for (int o : offs) t[(base + o) >> 6] ^= 1ull << ((base + o) & 63);
+        }
+    W256 r;
+    for (int i = 0; i < 4; i++) r.w[i] = t[i];
+    return r;
+}
+
+// Solve M x = c over GF(2), M given by the images of the 256 unit vectors (Gauss-Jordan; free
+// variables 0).  Returns false if inconsistent.
+static inline bool w256_solve(const W256* img, const W256& c, W256* x) {
+    static W256 row[256];
+    static unsigned char rhs[256];
+    for (int r = 0; r < 256; r++) {
+        row[r] = w256_zero();
+        for (int j = 0; j < 256; j++)
+            if (w256_bit(img[j], r)) row[r].w[j >> 6] |= 1ull << (j & 63);
+        rhs[r] = (unsigned char)w256_bit(c, r);
+    }
+    int where[256];
+    for (int j = 0; j < 256; j++) where[j] = -1;
+    int r = 0;
+    for (int j = 0; j < 256 && r < 256; j++) {
+        int p = -1;
+        for (int i = r; i < 256; i++)
+            if (w256_bit(row[i], j)) { p = i; break; }
+        if (p < 0) continue;
+        std::swap(row[p], row[r]);
+        std::swap(rhs[p], rhs[r]);
+        for (int i = 0; i < 256; i++)
+            if (i != r && w256_bit(row[i], j)) { w256_xor(row[i], row[r]); rhs[i] ^= rhs[r]; }
+        where[j] = r++;
+    }
+    for (int i = r; i < 256; i++)
+        if (rhs[i]) return false;
+    *x = w256_zero();
+    for (int j = 0; j < 256; j++)
+        if (where[j] >= 0 && rhs[where[j]]) x->w[j >> 6] |= 1ull << (j & 63);
+    return true;
+}
+
+// towerToPoly[j] = image of tower basis v_j (j < 256), polyToTower[i] = image of z^i
+struct Isomorphism256 {
+    W256 towerToPoly[256];
+    W256 polyToTower[256];
+    bool ok;
+};
+static inline bool build_isomorphism256(Isomorphism256* iso) {
+    iso->ok = false;
+    static W256 as_img[256];
+    for (int j = 0; j < 256; j++) {
+        W256 e = w256_unit(j);
+        as_img[j] = gf256p_mul(e, e);
+        w256_xor(as_img[j], e);
+    }
+    W256 X[9];
+    W256 prod = w256_unit(0);
+    for (int k = 1; k <= 8; k++) {
+        W256 y;
+        if (!w256_solve(as_img, prod, &y)) return false;
+        W256 y2 = y;
+        y2.w[0] ^= 1;
+        X[k] = w256_less(y2, y) ? y2 : y;
+        prod = gf256p_mul(prod, X[k]);
+    }
+    for (int j = 0; j < 256; j++) {
+        W256 v = w256_unit(0);
+        for (int t = 0; t < 8; t++)
+            if ((j >> t) & 1) v = gf256p_mul(v, X[t + 1]);
+        iso->towerToPoly[j] = v;
+    }
+    for (int i = 0; i < 256; i++)
+        if (!w256_solve(iso->towerToPoly, w256_unit(i), &iso->polyToTower[i])) return false;
+    iso->ok = true;
+    return true;
 }
 
 }  // namespace gf2x_host

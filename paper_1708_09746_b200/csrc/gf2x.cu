@@ -380,6 +380,7 @@ static gf2x_status fail(gf2x_status s, const std::string& msg) {
 struct DeviceState {
     DevTables* tabs = nullptr;
     DevTables* host = nullptr;   // host copy (multiplier images for host-side constants)
+    struct DevTables256* tabs256 = nullptr;   // w = 128 tables (w128.cuh), built on first use
     void* shard_ws = nullptr;    // simulation workspace (gf2x_mul_sharded_sim)
     size_t shard_ws_bytes = 0;
     int sm_count = 0;
@@ -1022,6 +1023,7 @@ static gf2x_status mul_common(const uint64_t* a, uint64_t a_bits, const uint64_t
 }
 
 #include "shard.cuh"
+#include "w128.cuh"
 
 extern "C" {
 
@@ -1058,6 +1060,29 @@ gf2x_status gf2x_debug_stage(const uint64_t* a, uint64_t a_bits, const uint64_t*
                              uint64_t* out, void* stream) {
     if (stage < 1 || stage > 5 || !out || a_bits == 0 || b_bits == 0) return fail(GF2X_EINVAL, "bad debug stage request");
     return mul_common(a, a_bits, b, b_bits, nullptr, 1, nullptr, 0, stream, stage, out);
+}
+
+gf2x_status gf2x_mul_w(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c, int64_t batch,
+                       int w, void* stream) {
+    if (w == 64) return mul_common(a, a_bits, b, b_bits, c, batch, nullptr, 0, stream, 0, nullptr);
+    if (w == 128) return mul_common_w128(a, a_bits, b, b_bits, c, batch, stream, 0, nullptr);
+    return fail(GF2X_EINVAL, "block width w must be 64 or 128");
+}
+
+int gf2x_launch_count_w(uint64_t a_bits, uint64_t b_bits, int64_t batch, int w) {
+    if (w == 64) return gf2x_launch_count(a_bits, b_bits, batch);
+    if (w != 128 || batch <= 0) return 0;
+    if (a_bits == 0 || b_bits == 0) return 1;
+    PlanW128 P;
+    if (make_plan_w128(a_bits, b_bits, batch, P) != GF2X_OK) return -1;
+    return launches_of_w128(P);
+}
+
+gf2x_status gf2x_debug_stage_w128(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, int stage,
+                                  uint64_t* out, void* stream) {
+    if (stage != 1 && stage != 2 && stage != 3 && stage != 5) return fail(GF2X_EINVAL, "stage must be 1, 2, 3 or 5");
+    if (!out || a_bits == 0 || b_bits == 0) return fail(GF2X_EINVAL, "null output or empty operand");
+    return mul_common_w128(a, a_bits, b, b_bits, nullptr, 1, stream, stage, out);
 }
 
 gf2x_status gf2x_comm_unique_id(void* id_out) {
@@ -1280,12 +1305,13 @@ gf2x_status gf2x_release(int device) {
         if (kv.second.first) cudaFree(kv.second.first);
     if (it->second.tabs) cudaFree(it->second.tabs);
     if (it->second.shard_ws) cudaFree(it->second.shard_ws);
+    if (it->second.tabs256) cudaFree(it->second.tabs256);
     delete it->second.host;
     g_dev.erase(it);
     cudaSetDevice(cur);
     return GF2X_OK;
 }
 
-const char* gf2x_version(void) { return "gf2x-b200 0.1 (sm_100a, Alg. 5 TGF(2^128))"; }
+const char* gf2x_version(void) { return "gf2x-b200 0.2 (sm_100a, Alg. 5: w=64 TGF(2^128), w=128 TGF(2^256))"; }
 
 }  // extern "C"

@@ -1,0 +1,396 @@
+// w128.cuh -- Alg. 5 with 128-bit blocks over TGF(2^256) ("An initial block width
+// of w=128 bits is also possible and in this case the operative field is TGF(2^256)"; sec 4.2
+// P:1077-1114).  Included by gf2x.cu after the w = 64 pipeline.
+//
+// TGF(2^256) = TGF(2^128)[x_8]/(x_8^2 + x_8 + v_127) (the tower of P:640-652 one level up).  A spectrum
+// of N elements is stored as two planes of N uint4: the low halves (coordinates of v_0..v_127) and the
+// high halves (coefficient of x_8).  Every FFT multiplier s_k(phi_v(b)) lies in TGF(2^32), and by
+// Prop. 2 a subfield constant multiplies the two halves independently, so FFT_LCH over
+// TGF(2^256) is the w = 64 FFT kernels applied to both planes (the planes are "products" of the batch
+// with identical multipliers); likewise the XOR-only BasisCvt/iBasisCvt.  What is new:
+//   k_psi256      changeRepr 128-bit polynomial-basis block -> TGF(2^256) (M4R-4 tables, R20)
+//   k_w128_sums   a_lo + a_hi, b_lo + b_hi (Karatsuba operands)
+//   k_bottom x3   mode 2: the three TGF(2^128) products P0 = a_lo b_lo, P2 = a_hi b_hi,
+//                 P1 = (a_lo + a_hi)(b_lo + b_hi), bit-sliced (the w = 64 pointmul)
+//   k_w128_post   lo = P0 + v_127 P2, hi = P1 + P0 (Karatsuba at the x_8 level, sec 4.1.3)
+//   k_ipsi256     changeRepr^-1 to the 256-bit polynomial basis + InterleavedCombine on 128-bit blocks
+// Plane layout per operand: [lo planes of all batch products][hi planes], so each plane set is one
+// contiguous run for the bottom kernel.
+#pragma once
+
+struct DevTables256 {
+    uint4 psi[32 * 16 * 2];    // M4R-4: nibble t of a 128-bit block, value x -> image (lo, hi) in the tower
+    uint4 ipsi[64 * 16 * 2];   // M4R-4: nibble t of a tower element (t < 32: lo half), x -> polynomial (lo, hi)
+    uint4 v127[16 * 256];      // M4R-8: byte ch of a TGF(2^128) element, x -> v_127 (x) (x << 8 ch)
+};
+
+static void host_build_tables256(DevTables256* T) {
+    using namespace gf2x_host;
+    static Isomorphism256 iso;
+    build_isomorphism256(&iso);
+    auto put = [](uint4* d, const W256& v) {
+        d[0] = make_uint4((uint32_t)v.w[0], (uint32_t)(v.w[0] >> 32), (uint32_t)v.w[1], (uint32_t)(v.w[1] >> 32));
+        d[1] = make_uint4((uint32_t)v.w[2], (uint32_t)(v.w[2] >> 32), (uint32_t)v.w[3], (uint32_t)(v.w[3] >> 32));
+    };
+    for (int t = 0; t < 32; t++)
+        for (int x = 0; x < 16; x++) {
+            W256 v = w256_zero();
+            for (int b = 0; b < 4; b++)
+                if ((x >> b) & 1) w256_xor(v, iso.polyToTower[4 * t + b]);
+            put(&T->psi[(t * 16 + x) * 2], v);
+        }
+    for (int t = 0; t < 64; t++)
+        for (int x = 0; x < 16; x++) {
+            W256 v = w256_zero();
+            for (int b = 0; b < 4; b++)
+                if ((x >> b) & 1) w256_xor(v, iso.towerToPoly[4 * t + b]);
+            put(&T->ipsi[(t * 16 + x) * 2], v);
+        }
+    const u128 v127 = ((u128)1) << 127;
+    for (int ch = 0; ch < 16; ch++)
+        for (int x = 0; x < 256; x++) {
+            const u128 r = tower_mul(((u128)x) << (8 * ch), v127);
+            T->v127[ch * 256 + x] = make_uint4((uint32_t)r, (uint32_t)(r >> 32), (uint32_t)(r >> 64), (uint32_t)(r >> 96));
+        }
+}
+
+// ---------------------------------------------------------------------------------------------
+// changeRepr: element i of operand o, product p: the 128-bit block S[o][p][i] (i < s_per,
+// 0 beyond) -> planes W[o][lo/hi][p][i].  One thread per element, 32 nibble lookups of 32 B.
+// ---------------------------------------------------------------------------------------------
+#define PSI256_THREADS 256
+__global__ void __launch_bounds__(PSI256_THREADS) k_psi256(const uint4* __restrict__ S, uint64_t s_per, uint64_t N,
+                                                           uint64_t batch, int ops, const DevTables256* __restrict__ T,
+                                                           uint4* __restrict__ W) {
+    __shared__ uint4 tab[32 * 16 * 2];
+    for (int i = threadIdx.x; i < 32 * 16 * 2; i += blockDim.x) tab[i] = T->psi[i];
+    __syncthreads();
+    const uint64_t per_op = batch * N, total = per_op * ops;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t o = e / per_op, r = e - o * per_op, p = r / N, i = r - p * N;
+        uint4 lo = make_uint4(0, 0, 0, 0), hi = lo;
+        if (i < s_per) {
+            const uint4 x = S[(o * batch + p) * s_per + i];
+            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int L = 0; L < 4; L++) {
+                if (!w[L]) continue;
+#pragma unroll
+                for (int n = 0; n < 8; n++) {
+                    const uint32_t t = L * 8 + n, v = (w[L] >> (4 * n)) & 15;
+                    lo = xor4(lo, tab[(t * 16 + v) * 2]);
+                    hi = xor4(hi, tab[(t * 16 + v) * 2 + 1]);
+                }
+            }
+        }
+        uint4* d = W + o * 2 * per_op + p * N + i;
+        d[0] = lo;
+        d[per_op] = hi;
+    }
+}
+
+// Karatsuba operands: Ts = lo + hi for n elements (lo plane at P, hi plane at P + n)
+__global__ void k_w128_sums(const uint4* __restrict__ P, uint64_t n, uint4* __restrict__ Ts) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        Ts[i] = xor4(P[i], P[n + i]);
+}
+
+// x_8-level recombination: with P0 in the lo plane, P2 in the hi plane, P1 in Ts:
+//   lo = P0 + v_127 (x) P2,  hi = P1 + P0.   v_127 (x) P2 by M4R-8 (16 byte lookups).
+__global__ void __launch_bounds__(256) k_w128_post(uint4* __restrict__ P, uint64_t n, const uint4* __restrict__ Ts,
+                                                   const DevTables256* __restrict__ T) {
+    extern __shared__ uint4 v127t[];   // 16 x 256
+    for (int i = threadIdx.x; i < 16 * 256; i += blockDim.x) v127t[i] = T->v127[i];
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 p0 = P[i], p2 = P[n + i], p1 = Ts[i];
+        const uint32_t w[4] = {p2.x, p2.y, p2.z, p2.w};
+        uint4 lo = p0;
+#pragma unroll
+        for (int L = 0; L < 4; L++)
+#pragma unroll
+            for (int b = 0; b < 4; b++) lo = xor4(lo, v127t[(L * 4 + b) * 256 + ((w[L] >> (8 * b)) & 255)]);
+        P[i] = lo;
+        P[n + i] = xor4(p1, p0);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// changeRepr^-1 + InterleavedCombine on 128-bit blocks:
+//   C_i = psi256^-1(lo_i, hi_i) (degree <= 254), out block w = lo128(C_w) ^ hi128(C_(w-1)),
+// words 2w, 2w+1 of the product, w < ceil(n_out / 2) (C_i = 0 for i >= N).  A CTA covers 256 blocks
+// of one product; thread 0 also converts the element before the CTA's first block.
+// ---------------------------------------------------------------------------------------------
+#define IPSI256_THREADS 256
+__device__ __forceinline__ void ipsi256_apply(const uint4* tab, uint4 lo, uint4 hi, uint4& rlo, uint4& rhi) {
+    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    rlo = make_uint4(0, 0, 0, 0);
+    rhi = rlo;
+#pragma unroll
+    for (int L = 0; L < 8; L++) {
+        if (!w[L]) continue;
+#pragma unroll
+        for (int n = 0; n < 8; n++) {
+            const uint32_t t = L * 8 + n, v = (w[L] >> (4 * n)) & 15;
+            rlo = xor4(rlo, tab[(t * 16 + v) * 2]);
+            rhi = xor4(rhi, tab[(t * 16 + v) * 2 + 1]);
+        }
+    }
+}
+__global__ void __launch_bounds__(IPSI256_THREADS) k_ipsi256(const uint4* __restrict__ W, uint64_t N, uint64_t batch,
+                                                             uint64_t n_out, const DevTables256* __restrict__ T,
+                                                             uint64_t* __restrict__ out) {
+    extern __shared__ uint4 ib_tab[];   // 64 x 16 x 2 (32 KB)
+    __shared__ uint4 Hs[IPSI256_THREADS + 1];
+    for (int i = threadIdx.x; i < 64 * 16 * 2; i += blockDim.x) ib_tab[i] = T->ipsi[i];
+    const uint64_t nblk = (n_out + 1) / 2;
+    const uint64_t cta_per = (nblk + IPSI256_THREADS - 1) / IPSI256_THREADS;
+    const uint64_t plane = N * batch;
+    for (uint64_t cb = blockIdx.x; cb < cta_per * batch; cb += gridDim.x) {
+        const uint64_t p = cb / cta_per, w0 = (cb - p * cta_per) * IPSI256_THREADS;
+        const uint4* lo = W + p * N;
+        const uint4* hi = lo + plane;
+        __syncthreads();   // tables loaded / previous tile's Hs consumed
+        const uint64_t w = w0 + threadIdx.x;
+        uint4 clo = make_uint4(0, 0, 0, 0), chi = clo;
+        if (w < nblk && w < N) ipsi256_apply(ib_tab, lo[w], hi[w], clo, chi);
+        Hs[threadIdx.x + 1] = chi;
+        if (threadIdx.x == 0) {
+            uint4 plo = make_uint4(0, 0, 0, 0), phi = plo;
+            if (w0 >= 1 && w0 - 1 < N) ipsi256_apply(ib_tab, lo[w0 - 1], hi[w0 - 1], plo, phi);
+            Hs[0] = phi;
+        }
+        __syncthreads();
+        if (w < nblk) {
+            const uint4 v = xor4(clo, Hs[threadIdx.x]);
+            uint64_t* d = out + p * n_out + 2 * w;
+            d[0] = ((uint64_t)v.y << 32) | v.x;
+            if (2 * w + 1 < n_out) d[1] = ((uint64_t)v.w << 32) | v.z;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------ host pipeline
+struct PlanW128 {
+    uint64_t na, nb, ka, kb, N, batch;   // 64-bit words, 128-bit blocks per operand
+    int m, ma, mb;
+    std::vector<CvtPass> cvt_a, cvt_b, icvt;
+    std::vector<FftPass> fft;
+    size_t off_sa, off_sb, off_wa, off_wb, off_ta, off_tb, bytes;
+};
+
+static gf2x_status make_plan_w128(uint64_t a_bits, uint64_t b_bits, int64_t batch, PlanW128& P) {
+    P.na = (a_bits + 63) / 64;
+    P.nb = (b_bits + 63) / 64;
+    P.ka = (a_bits + 127) / 128;
+    P.kb = (b_bits + 127) / 128;
+    P.batch = (uint64_t)batch;
+    P.m = ceil_log2_u64(P.ka + P.kb - 1);
+    if (P.m > 32) return fail(GF2X_ETOOBIG, "FFT size exceeds 2^32 points");
+    P.N = 1ull << P.m;
+    P.ma = ceil_log2_u64(P.ka);
+    P.mb = ceil_log2_u64(P.kb);
+    P.cvt_a = plan_cvt(P.ma, 16);
+    P.cvt_b = plan_cvt(P.mb, 16);
+    P.icvt = plan_cvt(P.m, 16);
+    P.fft = plan_fft(P.m);
+    const uint64_t B = P.batch;
+    P.off_sa = 0;
+    P.off_sb = P.off_sa + (1ull << P.ma) * B * 16;             // Sb directly after Sa
+    P.off_wa = align256(P.off_sb + (1ull << P.mb) * B * 16);
+    P.off_wb = P.off_wa + 2 * P.N * B * 16;                    // Wb directly after Wa
+    P.off_ta = align256(P.off_wb + (2 * P.N * B + 2048) * 16);
+    P.off_tb = P.off_ta + P.N * B * 16;                        // Tb directly after Ta
+    P.bytes = align256(P.off_tb + (P.N * B + 2048) * 16);
+    return GF2X_OK;
+}
+
+static gf2x_status check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return GF2X_OK;
+}
+
+static gf2x_status get_tables256(DeviceState* ds, DevTables256** out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!ds->tabs256) {
+        DevTables256* h = new DevTables256;
+        host_build_tables256(h);
+        DevTables256* d = nullptr;
+        cudaError_t e = cudaMalloc(&d, sizeof(DevTables256));
+        if (e != cudaSuccess) { delete h; return fail(GF2X_ENOMEM, "table allocation failed"); }
+        e = cudaMemcpy(d, h, sizeof(DevTables256), cudaMemcpyHostToDevice);
+        delete h;
+        if (e != cudaSuccess) { cudaFree(d); return fail(GF2X_ECUDA, cudaGetErrorString(e)); }
+        CUDA_TRY(cudaFuncSetAttribute(k_w128_post, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        ds->tabs256 = d;
+    }
+    *out = ds->tabs256;
+    return GF2X_OK;
+}
+
+static void bottom_run(uint4* A, uint4* B, uint64_t total, int m, int L, int mode, int smc, cudaStream_t st) {
+    BottomParams bp;
+    bp.A = A; bp.B = B;
+    bp.total = total;
+    bp.ntiles = (total + (1ull << BT_BITS) - 1) >> BT_BITS;
+    bp.m = m; bp.L = L;
+    bp.map = IdxMap{0, 0, 0};
+    bp.mode = mode;
+    const double prods = (double)bp.ntiles * (((mode & 1) ? 2.0 : 0.0) * L * 128.0 + ((mode & 4) ? 1.0 : 0.0) * L * 128.0 +
+                                              ((mode & 2) ? 576.0 : 0.0));
+    const double bytes = (double)total * 16 * (((mode & 1) ? 4.0 : 0.0) + ((mode & 2) ? 3.0 : 0.0) + ((mode & 4) ? 2.0 : 0.0));
+    ProfScope ps("k_bottom", bytes, st, prods * OPS_BS_MUL32);
+    bottom_launch(bp, smc, st);
+}
+
+// stop_stage: 0 = product; 1 = after changeRepr, 2 = after FFT_LCH, 3 = after pointmul, 5 = after
+// iBasisCvt (operand a's planes left in Wa)
+static gf2x_status run_pipeline_w128(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
+                                     const PlanW128& P, void* ws, DeviceState* ds, cudaStream_t st, int stop_stage) {
+    DevTables256* T256;
+    gf2x_status s = get_tables256(ds, &T256);
+    if (s != GF2X_OK) return s;
+    unsigned char* base = reinterpret_cast<unsigned char*>(ws);
+    uint4* Sa = reinterpret_cast<uint4*>(base + P.off_sa);
+    uint4* Sb = reinterpret_cast<uint4*>(base + P.off_sb);
+    uint4* Wa = reinterpret_cast<uint4*>(base + P.off_wa);
+    uint4* Wb = reinterpret_cast<uint4*>(base + P.off_wb);
+    uint4* Ta = reinterpret_cast<uint4*>(base + P.off_ta);
+    uint4* Tb = reinterpret_cast<uint4*>(base + P.off_tb);
+    const int smc = ds->sm_count;
+    const uint64_t B = P.batch, plane = P.N * B;
+    // Split into 128-bit blocks: the words, masked, zero-padded to 2^ma blocks
+    {
+        ProfScope ps("k_prep", (double)B * (P.na + (2ull << P.ma)) * 8, st);
+        k_prep<<<grid_for((2ull << P.ma) * B, 256, smc, 8), 256, 0, st>>>(a, P.na, a_bits, P.ma + 1, B,
+                                                                           reinterpret_cast<uint64_t*>(Sa));
+    }
+    {
+        ProfScope ps("k_prep", (double)B * (P.nb + (2ull << P.mb)) * 8, st);
+        k_prep<<<grid_for((2ull << P.mb) * B, 256, smc, 8), 256, 0, st>>>(b, P.nb, b_bits, P.mb + 1, B,
+                                                                           reinterpret_cast<uint64_t*>(Sb));
+    }
+    if ((s = check_launch("prep")) != GF2X_OK) return s;
+    // BasisCvt on the 128-bit blocks (XOR-only)
+    const bool same = P.ma == P.mb;
+    if (same) {
+        if ((s = run_cvt<uint4>(P.cvt_a, Sa, P.ma, 2 * B, false, smc, st)) != GF2X_OK) return s;
+    } else {
+        if ((s = run_cvt<uint4>(P.cvt_a, Sa, P.ma, B, false, smc, st)) != GF2X_OK) return s;
+        if ((s = run_cvt<uint4>(P.cvt_b, Sb, P.mb, B, false, smc, st)) != GF2X_OK) return s;
+    }
+    // changeRepr into TGF(2^256)
+    if (same) {
+        ProfScope ps("k_psi256", 2.0 * B * ((1ull << P.ma) * 16 + P.N * 32), st);
+        k_psi256<<<grid_for(2 * plane, PSI256_THREADS, smc, 4), PSI256_THREADS, 0, st>>>(Sa, 1ull << P.ma, P.N, B, 2, T256, Wa);
+    } else {
+        ProfScope ps("k_psi256", (double)B * (((1ull << P.ma) + (1ull << P.mb)) * 16 + 2 * P.N * 32), st);
+        k_psi256<<<grid_for(plane, PSI256_THREADS, smc, 4), PSI256_THREADS, 0, st>>>(Sa, 1ull << P.ma, P.N, B, 1, T256, Wa);
+        k_psi256<<<grid_for(plane, PSI256_THREADS, smc, 4), PSI256_THREADS, 0, st>>>(Sb, 1ull << P.mb, P.N, B, 1, T256, Wb);
+    }
+    if ((s = check_launch("psi256")) != GF2X_OK) return s;
+    if (stop_stage == 1) return GF2X_OK;
+    // FFT_LCH top layers on the four plane sets (a lo/hi, b lo/hi) in one launch per pass
+    Plan Pf;
+    Pf.N = P.N; Pf.m = P.m; Pf.batch = 2 * B;
+    const size_t ndirect = P.fft.size() - 1;
+    for (size_t i = 0; i < ndirect; i++)
+        if ((s = launch_fft(P.fft[i], false, false, Wa, P.N, Wa, Pf, ds, st, 2)) != GF2X_OK) return s;
+    const int L = P.fft.back().layers;
+    bottom_run(Wa, Wb, 2 * plane, P.m, L, 1, smc, st);
+    if ((s = check_launch("bottom fwd")) != GF2X_OK) return s;
+    if (stop_stage == 2) return GF2X_OK;
+    // pointmul in TGF(2^256): Karatsuba over TGF(2^128)
+    {
+        ProfScope ps("k_w128_sums", 2.0 * plane * 48, st);
+        k_w128_sums<<<grid_for(plane, 256, smc, 8), 256, 0, st>>>(Wa, plane, Ta);
+        k_w128_sums<<<grid_for(plane, 256, smc, 8), 256, 0, st>>>(Wb, plane, Tb);
+    }
+    bottom_run(Wa, Wb, plane, P.m, L, 2, smc, st);                   // P0 = a_lo b_lo
+    bottom_run(Wa + plane, Wb + plane, plane, P.m, L, 2, smc, st);   // P2 = a_hi b_hi
+    bottom_run(Ta, Tb, plane, P.m, L, 2, smc, st);                   // P1
+    {
+        ProfScope ps("k_w128_post", (double)plane * 80, st);
+        k_w128_post<<<grid_for(plane, 256, smc, 3), 256, 64 * 1024, st>>>(Wa, plane, Ta, T256);
+    }
+    if ((s = check_launch("pointmul256")) != GF2X_OK) return s;
+    if (stop_stage == 3) return GF2X_OK;
+    // iFFT_LCH: bottom layers, then the direct passes in reverse order
+    bottom_run(Wa, Wa, 2 * plane, P.m, L, 4, smc, st);
+    for (size_t i = ndirect; i-- > 0;)
+        if ((s = launch_fft(P.fft[i], true, false, Wa, P.N, Wa, Pf, ds, st)) != GF2X_OK) return s;
+    // iBasisCvt on both planes
+    if ((s = run_cvt<uint4>(P.icvt, Wa, P.m, 2 * B, true, smc, st)) != GF2X_OK) return s;
+    if (stop_stage == 5) return GF2X_OK;
+    // changeRepr^-1 + InterleavedCombine
+    {
+        const uint64_t n_out = P.na + P.nb, nblk = (n_out + 1) / 2;
+        const uint64_t ctas = (nblk + IPSI256_THREADS - 1) / IPSI256_THREADS * B;
+        ProfScope ps("k_ipsi256", 32.0 * plane + 8.0 * n_out * B, st);
+        k_ipsi256<<<grid_for(ctas, 1, smc, 4), IPSI256_THREADS, 64 * 16 * 2 * 16, st>>>(Wa, P.N, B, n_out, T256, c);
+    }
+    return check_launch("ipsi256");
+}
+
+static gf2x_status mul_common_w128(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
+                                   int64_t batch, void* stream, int stop_stage, uint64_t* stage_out) {
+    if (batch < 0) return fail(GF2X_EINVAL, "negative batch");
+    if (batch == 0) return GF2X_OK;
+    const uint64_t na = (a_bits + 63) / 64, nb = (b_bits + 63) / 64;
+    const size_t out_bytes = (size_t)(na + nb) * 8 * (size_t)batch;
+    if (!c && out_bytes && !stop_stage) return fail(GF2X_EINVAL, "null output");
+    if ((!a && na) || (!b && nb)) return fail(GF2X_EINVAL, "null input");
+    if (c && out_bytes && ((a && overlaps(c, out_bytes, a, na * 8 * batch)) || (b && overlaps(c, out_bytes, b, nb * 8 * batch))))
+        return fail(GF2X_EINVAL, "output overlaps an input");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (a_bits == 0 || b_bits == 0) {
+        if (out_bytes && !stop_stage) CUDA_TRY(cudaMemsetAsync(c, 0, out_bytes, st));
+        return GF2X_OK;
+    }
+    int dev;
+    DeviceState* ds;
+    gf2x_status s = get_device(&dev, &ds);
+    if (s != GF2X_OK) return s;
+    PlanW128 P;
+    if ((s = make_plan_w128(a_bits, b_bits, batch, P)) != GF2X_OK) return s;
+    void* ws;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto& ent = ds->ws[st];
+        if (ent.second < P.bytes) {
+            if (ent.first) {
+                cudaStreamSynchronize(st);
+                cudaFree(ent.first);
+                ent.first = nullptr;
+                ent.second = 0;
+            }
+            void* p = nullptr;
+            cudaError_t e = cudaMalloc(&p, P.bytes);
+            if (e != cudaSuccess) return fail(GF2X_ENOMEM, std::string("workspace: ") + cudaGetErrorString(e));
+            ent.first = p;
+            ent.second = P.bytes;
+        }
+        ws = ent.first;
+    }
+    if ((s = run_pipeline_w128(a, a_bits, b, b_bits, c, P, ws, ds, st, stop_stage)) != GF2X_OK) return s;
+    if (stop_stage && stage_out) {   // (N, 4) words: element i = (lo plane i, hi plane i) of operand a, product 0
+        const unsigned char* W = reinterpret_cast<unsigned char*>(ws) + P.off_wa;
+        CUDA_TRY(cudaMemcpy2DAsync(stage_out, 32, W, 16, 16, P.N, cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(cudaMemcpy2DAsync(reinterpret_cast<unsigned char*>(stage_out) + 16, 32, W + P.N * P.batch * 16, 16, 16,
+                                   P.N, cudaMemcpyDeviceToDevice, st));
+    }
+    return GF2X_OK;
+}
+
+static int launches_of_w128(const PlanW128& P) {
+    const bool same = P.ma == P.mb;
+    int n = 2;                                                     // prep
+    n += (int)P.cvt_a.size() + (same ? 0 : (int)P.cvt_b.size());  // BasisCvt
+    n += same ? 1 : 2;                                             // psi256
+    const int nd = (int)P.fft.size() - 1;
+    n += nd;                                                       // forward passes
+    n += 1 + 2 + 3 + 1 + 1;                                        // bottom fwd, sums, 3 products, post, bottom inv
+    n += nd + (int)P.icvt.size() + 1;                              // inverse passes, iBasisCvt, ipsi256
+    return n;
+}
