@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--w", type=int, default=64, choices=[64, 128],
+                    help="Alg. 5 block width: 64 (TGF(2^128), default) or 128 (TGF(2^256), P:873-874)")
     ap.add_argument("--mode", default=None, choices=["sharded", "replicas"],
                     help="N > 1: one multiply partitioned over the ranks (default) or one per rank")
     args = ap.parse_args()
@@ -206,7 +208,7 @@ def main():
     mode = args.mode or ("sharded" if world > 1 else "single")
     if world == 1:
         mode = "single"
-    if mode == "sharded" and batch != 1:
+    if mode == "sharded" and (batch != 1 or args.w != 64):
         mode = "replicas"   # batched configs shard trivially: independent products per rank
     sharded = mode == "sharded"
     seed = DEFAULT_SEED + (0 if sharded else 2 * rank)  # replicas: each rank its own operand pair
@@ -232,6 +234,8 @@ def main():
     def step():
         if sharded:
             comm.mul(sa, sb, bits, sc, stream=stream)
+        elif args.w != 64:
+            G.gf2x_mul_w(da, bits, db, bits, args.w, batch, dc, stream=stream)
         elif batch == 1:
             G.gf2x_mul(da, bits, db, bits, dc, stream=stream)
         else:
@@ -314,6 +318,8 @@ def main():
         stream.wait_event(ev_out[k])           # step i-2's product has left EC[k]
         if sharded:
             comm.mul(EA[k], EB[k], bits, EC[k], stream=stream)
+        elif args.w != 64:
+            G.gf2x_mul_w(EA[k], bits, EB[k], bits, args.w, batch, EC[k], stream=stream)
         elif batch == 1:
             G.gf2x_mul(EA[k], bits, EB[k], bits, EC[k], stream=stream)
         else:
@@ -364,7 +370,7 @@ def main():
             traffic = None
     step_bytes = sum(r["bytes"] for r in prof) / args.steps
     kern_ms = sum(r["ms"] for r in prof) / args.steps
-    launches = G.gf2x_launch_count(bits, bits, batch)
+    launches = G.gf2x_launch_count_w(bits, bits, batch, args.w)
     if sharded:   # every kernel of the sharded path is bracketed by the profiling hook
         launches = sum(r["launches"] for r in prof) // args.steps
 
@@ -384,8 +390,9 @@ def main():
         "dtype": "u64",
         "data": "synthetic",
         "config": {
-            "workload": WORKLOAD[args.config], "config": args.config, "operand_bits": bits, "batch": batch,
-            "fft_points": 1 << max(0, (2 * n - 2).bit_length()),
+            "workload": WORKLOAD[args.config] + ("" if args.w == 64 else ", w=128 blocks over TGF(2^256)"),
+            "config": args.config, "operand_bits": bits, "batch": batch, "block_width": args.w,
+            "fft_points": 1 << max(0, (2 * n - 2).bit_length()) >> (0 if args.w == 64 else 1),
             "parallelism": (f"sharded FFT over {world} GPUs (NCCL)" if sharded else
                             ("replicas" if world > 1 else "single")),
             "seed": DEFAULT_SEED, "l2": "working set > 126 MB L2 (operands + 2 spectra), no flush" if bits >= 1 << 28
