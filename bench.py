@@ -223,13 +223,30 @@ def main():
     db = torch.from_numpy(b.reshape(-1).view(np.int64)).to(dev).view(torch.uint64)
     dc = torch.empty(n_out * batch, dtype=torch.uint64, device=dev)
     stream = torch.cuda.current_stream()
+    sharded_error = None
     if sharded:
         # the FFT partitioned over the ranks (NCCL over NVLink); rank r owns words
         # [r n/G, (r+1) n/G) of a and b and receives words [r 2n/G, (r+1) 2n/G) of c
-        comm = G.init_from_process_group()
-        lo, hi = G.shard_words(n, world, rank)
-        sa, sb = da[lo:hi].clone(), db[lo:hi].clone()
-        sc = torch.empty(n_out // world, dtype=torch.uint64, device=dev)
+        try:
+            comm = G.init_from_process_group()
+            lo, hi = G.shard_words(n, world, rank)
+            sa, sb = da[lo:hi].clone(), db[lo:hi].clone()
+            sc = torch.empty(n_out // world, dtype=torch.uint64, device=dev)
+            comm.mul(sa, sb, bits, sc, stream=stream)
+            torch.cuda.synchronize()
+            ok = 1
+        except Exception as e:   # e.g. NCCL unavailable: every rank sees it (same library, same lists)
+            sharded_error, ok = f"{type(e).__name__}: {e}"[:300], 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            sharded, mode = False, "replicas"
+            sharded_error = sharded_error or "another rank failed"
+            if rank == 0:
+                print(f"[bench] sharded multiply unavailable ({sharded_error}); running replicas", file=sys.stderr)
+            a, b = operand_pair(bits, DEFAULT_SEED + 2 * rank)
+            da = torch.from_numpy(a.reshape(-1).view(np.int64)).to(dev).view(torch.uint64)
+            db = torch.from_numpy(b.reshape(-1).view(np.int64)).to(dev).view(torch.uint64)
 
     def step():
         if sharded:
@@ -420,6 +437,8 @@ def main():
                 "pipelined": "H2D / multiply / D2H of consecutive steps overlap (2 buffer sets, separate copy streams)"},
         "gpu_launches": launches * args.steps,
     }
+    if sharded_error:
+        line["sharded_error"] = sharded_error
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, 1 << 24 if bits >= 1 << 24 else bits)
     if rank == 0:
