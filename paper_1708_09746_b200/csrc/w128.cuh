@@ -118,17 +118,18 @@ __global__ void __launch_bounds__(256) k_w128_post(uint4* __restrict__ P, uint64
 // ---------------------------------------------------------------------------------------------
 // changeRepr^-1 + InterleavedCombine on 128-bit blocks:
 //   C_i = psi256^-1(lo_i, hi_i) (degree <= 254), out block w = lo128(C_w) ^ hi128(C_(w-1)),
-// words 2w, 2w+1 of the product, w < ceil(n_out / 2) (C_i = 0 for i >= N).  A CTA covers 256 blocks
-// of one product; thread 0 also converts the element before the CTA's first block.
+// words 2w, 2w+1 of the product, w < ceil(n_out / 2) (C_i = 0 for i >= N).  A CTA iteration converts
+// the 256 elements w0-1 .. w0+254 (thread t: element w0-1+t) and writes the 255 blocks w0 .. w0+254, so
+// every thread does the same work.
 // ---------------------------------------------------------------------------------------------
 #define IPSI256_THREADS 256
+#define IPSI256_STEP (IPSI256_THREADS - 1)
 __device__ __forceinline__ void ipsi256_apply(const uint4* tab, uint4 lo, uint4 hi, uint4& rlo, uint4& rhi) {
     const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
     rlo = make_uint4(0, 0, 0, 0);
     rhi = rlo;
 #pragma unroll
     for (int L = 0; L < 8; L++) {
-        if (!w[L]) continue;
 #pragma unroll
         for (int n = 0; n < 8; n++) {
             const uint32_t t = L * 8 + n, v = (w[L] >> (4 * n)) & 15;
@@ -141,28 +142,28 @@ __global__ void __launch_bounds__(IPSI256_THREADS) k_ipsi256(const uint4* __rest
                                                              uint64_t n_out, const DevTables256* __restrict__ T,
                                                              uint64_t* __restrict__ out) {
     extern __shared__ uint4 ib_tab[];   // 64 x 16 x 2 (32 KB)
-    __shared__ uint4 Hs[IPSI256_THREADS + 1];
+    __shared__ uint4 Hs[IPSI256_THREADS];
     for (int i = threadIdx.x; i < 64 * 16 * 2; i += blockDim.x) ib_tab[i] = T->ipsi[i];
     const uint64_t nblk = (n_out + 1) / 2;
-    const uint64_t cta_per = (nblk + IPSI256_THREADS - 1) / IPSI256_THREADS;
+    const uint64_t cta_per = (nblk + IPSI256_STEP - 1) / IPSI256_STEP;
     const uint64_t plane = N * batch;
     for (uint64_t cb = blockIdx.x; cb < cta_per * batch; cb += gridDim.x) {
-        const uint64_t p = cb / cta_per, w0 = (cb - p * cta_per) * IPSI256_THREADS;
+        const uint64_t p = cb / cta_per, w0 = (cb - p * cta_per) * IPSI256_STEP;
         const uint4* lo = W + p * N;
         const uint4* hi = lo + plane;
-        __syncthreads();   // tables loaded / previous tile's Hs consumed
-        const uint64_t w = w0 + threadIdx.x;
+        __syncthreads();   // tables loaded / previous iteration's Hs consumed
+        const uint64_t e = w0 + threadIdx.x;   // element e - 1 (e = 0: none)
         uint4 clo = make_uint4(0, 0, 0, 0), chi = clo;
-        if (w < nblk && w < N) ipsi256_apply(ib_tab, lo[w], hi[w], clo, chi);
-        Hs[threadIdx.x + 1] = chi;
-        if (threadIdx.x == 0) {
-            uint4 plo = make_uint4(0, 0, 0, 0), phi = plo;
-            if (w0 >= 1 && w0 - 1 < N) ipsi256_apply(ib_tab, lo[w0 - 1], hi[w0 - 1], plo, phi);
-            Hs[0] = phi;
-        }
+        if (e >= 1 && e - 1 < N && e - 1 < nblk) ipsi256_apply(ib_tab, lo[e - 1], hi[e - 1], clo, chi);
+        // thread t < 255 writes block w = w0 + t: lo of element w (thread t + 1's clo) ^ hi of element w - 1
+        const uint64_t w = w0 + threadIdx.x;
+        const uint4 nlo = make_uint4(__shfl_down_sync(0xFFFFFFFFu, clo.x, 1), __shfl_down_sync(0xFFFFFFFFu, clo.y, 1),
+                                     __shfl_down_sync(0xFFFFFFFFu, clo.z, 1), __shfl_down_sync(0xFFFFFFFFu, clo.w, 1));
+        if ((threadIdx.x & 31) == 0) Hs[threadIdx.x] = clo;   // lane 0's clo, for lane 31 of the previous warp
         __syncthreads();
-        if (w < nblk) {
-            const uint4 v = xor4(clo, Hs[threadIdx.x]);
+        if (threadIdx.x < IPSI256_STEP && w < nblk) {
+            const uint4 lw = (threadIdx.x & 31) == 31 ? Hs[threadIdx.x + 1] : nlo;
+            const uint4 v = xor4(lw, chi);
             uint64_t* d = out + p * n_out + 2 * w;
             d[0] = ((uint64_t)v.y << 32) | v.x;
             if (2 * w + 1 < n_out) d[1] = ((uint64_t)v.w << 32) | v.z;
@@ -326,7 +327,7 @@ static gf2x_status run_pipeline_w128(const uint64_t* a, uint64_t a_bits, const u
     // changeRepr^-1 + InterleavedCombine
     {
         const uint64_t n_out = P.na + P.nb, nblk = (n_out + 1) / 2;
-        const uint64_t ctas = (nblk + IPSI256_THREADS - 1) / IPSI256_THREADS * B;
+        const uint64_t ctas = (nblk + IPSI256_STEP - 1) / IPSI256_STEP * B;
         ProfScope ps("k_ipsi256", 32.0 * plane + 8.0 * n_out * B, st);
         k_ipsi256<<<grid_for(ctas, 1, smc, 4), IPSI256_THREADS, 64 * 16 * 2 * 16, st>>>(Wa, P.N, B, n_out, T256, c);
     }
