@@ -183,7 +183,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c4b", choices=["c1", "c2", "c3", "c4a", "c4b", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--w", type=int, default=64, choices=[64, 128],
                     help="Alg. 5 block width: 64 (TGF(2^128), default) or 128 (TGF(2^256), P:873-874)")

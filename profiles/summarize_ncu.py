@@ -1,6 +1,6 @@
 """Summarise ncu outputs into profiles/ (tracked).
 
-python profiles/summarize_ncu.py <launches.csv> <full.ncu-rep> <tag> <config>
+python profiles/summarize_ncu.py <launches.csv> <full.ncu-rep> <tag> <config> ["<launch-list command>"]
 writes profiles/<tag>_launches.md, profiles/<tag>_kernels.md and updates profiles/ncu_traffic.json
 (per-kernel-class DRAM bytes per launch, read by bench.py as roofline.traffic).
 """
@@ -46,6 +46,7 @@ def to_unit(v, u, target):
 
 def main():
     lpath, rep, tag, cfg = sys.argv[1:5]
+    what = sys.argv[5] if len(sys.argv) > 5 else "one warm multiply"
     per = launches(lpath)
     cls = collections.OrderedDict()
     for (i, k), m in per.items():
@@ -58,7 +59,7 @@ def main():
         c[2] += rb + wb
     tot = sum(c[1] for c in cls.values())
     out = [f"# ncu launch list, {cfg} ({tag}) -- `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
-           "dram__bytes_write.sum --clock-control none` over one warm multiply (cold-cache, serialised: compare "
+           f"dram__bytes_write.sum --clock-control none` over {what} (cold-cache, serialised: compare "
            "shares, not absolutes)\n", "| kernel | launches | total us | share | DRAM bytes / launch |", "|---|---|---|---|---|"]
     traffic = {}
     for k, (n, t, b) in sorted(cls.items(), key=lambda kv: -kv[1][1]):
@@ -108,7 +109,8 @@ def main():
                   for i, h in enumerate(hdr) if h.startswith("smsp__average_warps_issue_stalled_")
                   and h.endswith("_per_issue_active.ratio")]
     units = dict(zip(hdr, rows[1]))
-    lines = [f"# ncu --set full, {cfg} ({tag})\n", "| kernel | grid x block | " + " | ".join(n for _, n in keys) +
+    lines = [f"# ncu --set full --clock-control none, {cfg} ({tag}): every kernel of one warm multiply "
+             "(tests/prof_run.py)\n", "| kernel | grid x block | " + " | ".join(n for _, n in keys) +
              " | top stalls (warp-cycles per issue) |", "|---|---|" + "---|" * len(keys) + "---|"]
     for r in data:
         d = dict(zip(hdr, r))
