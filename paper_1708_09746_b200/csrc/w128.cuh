@@ -8,12 +8,14 @@
 // Prop. 2 a subfield constant multiplies the two halves independently, so FFT_LCH over
 // TGF(2^256) is the w = 64 FFT kernels applied to both planes (the planes are "products" of the batch
 // with identical multipliers); likewise the XOR-only BasisCvt/iBasisCvt.  What is new:
-//   k_psi256      changeRepr 128-bit polynomial-basis block -> TGF(2^256) (M4R-4 tables, R20)
+//   k_psi256_bs   changeRepr 128-bit polynomial-basis block -> TGF(2^256), bit-sliced generated networks
+//                 (k_psi256: M4R-4 tables, for N < 2048)
 //   k_w128_sums   a_lo + a_hi, b_lo + b_hi (Karatsuba operands)
 //   k_bottom x3   mode 2: the three TGF(2^128) products P0 = a_lo b_lo, P2 = a_hi b_hi,
 //                 P1 = (a_lo + a_hi)(b_lo + b_hi), bit-sliced (the w = 64 pointmul)
 //   k_w128_post   lo = P0 + v_127 P2, hi = P1 + P0 (Karatsuba at the x_8 level, sec 4.1.3)
-//   k_ipsi256     changeRepr^-1 to the 256-bit polynomial basis + InterleavedCombine on 128-bit blocks
+//   k_ipsi256_bs  changeRepr^-1 to the 256-bit polynomial basis + InterleavedCombine on 128-bit blocks,
+//                 bit-sliced (k_ipsi256: M4R-4, for N < 2048 or ragged output lengths)
 // Plane layout per operand: [lo planes of all batch products][hi planes], so each plane set is one
 // contiguous run for the bottom kernel.
 #pragma once
@@ -118,18 +120,17 @@ __global__ void __launch_bounds__(256) k_w128_post(uint4* __restrict__ P, uint64
 // ---------------------------------------------------------------------------------------------
 // changeRepr^-1 + InterleavedCombine on 128-bit blocks:
 //   C_i = psi256^-1(lo_i, hi_i) (degree <= 254), out block w = lo128(C_w) ^ hi128(C_(w-1)),
-// words 2w, 2w+1 of the product, w < ceil(n_out / 2) (C_i = 0 for i >= N).  A CTA iteration converts
-// the 256 elements w0-1 .. w0+254 (thread t: element w0-1+t) and writes the 255 blocks w0 .. w0+254, so
-// every thread does the same work.
+// words 2w, 2w+1 of the product, w < ceil(n_out / 2) (C_i = 0 for i >= N).  A CTA covers 256 blocks
+// of one product; thread 0 also converts the element before the CTA's first block.
 // ---------------------------------------------------------------------------------------------
 #define IPSI256_THREADS 256
-#define IPSI256_STEP (IPSI256_THREADS - 1)
 __device__ __forceinline__ void ipsi256_apply(const uint4* tab, uint4 lo, uint4 hi, uint4& rlo, uint4& rhi) {
     const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
     rlo = make_uint4(0, 0, 0, 0);
     rhi = rlo;
 #pragma unroll
     for (int L = 0; L < 8; L++) {
+        if (!w[L]) continue;
 #pragma unroll
         for (int n = 0; n < 8; n++) {
             const uint32_t t = L * 8 + n, v = (w[L] >> (4 * n)) & 15;
@@ -142,31 +143,228 @@ __global__ void __launch_bounds__(IPSI256_THREADS) k_ipsi256(const uint4* __rest
                                                              uint64_t n_out, const DevTables256* __restrict__ T,
                                                              uint64_t* __restrict__ out) {
     extern __shared__ uint4 ib_tab[];   // 64 x 16 x 2 (32 KB)
-    __shared__ uint4 Hs[IPSI256_THREADS];
+    __shared__ uint4 Hs[IPSI256_THREADS + 1];
     for (int i = threadIdx.x; i < 64 * 16 * 2; i += blockDim.x) ib_tab[i] = T->ipsi[i];
     const uint64_t nblk = (n_out + 1) / 2;
-    const uint64_t cta_per = (nblk + IPSI256_STEP - 1) / IPSI256_STEP;
+    const uint64_t cta_per = (nblk + IPSI256_THREADS - 1) / IPSI256_THREADS;
     const uint64_t plane = N * batch;
     for (uint64_t cb = blockIdx.x; cb < cta_per * batch; cb += gridDim.x) {
-        const uint64_t p = cb / cta_per, w0 = (cb - p * cta_per) * IPSI256_STEP;
+        const uint64_t p = cb / cta_per, w0 = (cb - p * cta_per) * IPSI256_THREADS;
         const uint4* lo = W + p * N;
         const uint4* hi = lo + plane;
-        __syncthreads();   // tables loaded / previous iteration's Hs consumed
-        const uint64_t e = w0 + threadIdx.x;   // element e - 1 (e = 0: none)
-        uint4 clo = make_uint4(0, 0, 0, 0), chi = clo;
-        if (e >= 1 && e - 1 < N && e - 1 < nblk) ipsi256_apply(ib_tab, lo[e - 1], hi[e - 1], clo, chi);
-        // thread t < 255 writes block w = w0 + t: lo of element w (thread t + 1's clo) ^ hi of element w - 1
+        __syncthreads();   // tables loaded / previous tile's Hs consumed
         const uint64_t w = w0 + threadIdx.x;
-        const uint4 nlo = make_uint4(__shfl_down_sync(0xFFFFFFFFu, clo.x, 1), __shfl_down_sync(0xFFFFFFFFu, clo.y, 1),
-                                     __shfl_down_sync(0xFFFFFFFFu, clo.z, 1), __shfl_down_sync(0xFFFFFFFFu, clo.w, 1));
-        if ((threadIdx.x & 31) == 0) Hs[threadIdx.x] = clo;   // lane 0's clo, for lane 31 of the previous warp
+        uint4 clo = make_uint4(0, 0, 0, 0), chi = clo;
+        if (w < nblk && w < N) ipsi256_apply(ib_tab, lo[w], hi[w], clo, chi);
+        Hs[threadIdx.x + 1] = chi;
+        if (threadIdx.x == 0) {
+            uint4 plo = make_uint4(0, 0, 0, 0), phi = plo;
+            if (w0 >= 1 && w0 - 1 < N) ipsi256_apply(ib_tab, lo[w0 - 1], hi[w0 - 1], plo, phi);
+            Hs[0] = phi;
+        }
         __syncthreads();
-        if (threadIdx.x < IPSI256_STEP && w < nblk) {
-            const uint4 lw = (threadIdx.x & 31) == 31 ? Hs[threadIdx.x + 1] : nlo;
-            const uint4 v = xor4(lw, chi);
+        if (w < nblk) {
+            const uint4 v = xor4(clo, Hs[threadIdx.x]);
             uint64_t* d = out + p * n_out + 2 * w;
             d[0] = ((uint64_t)v.y << 32) | v.x;
             if (2 * w + 1 < n_out) d[1] = ((uint64_t)v.w << 32) | v.z;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Bit-sliced changeRepr / changeRepr^-1 for w = 128 (generated XOR networks of the same isomorphism,
+// tools/gen_bitslice.py + tools/dump_iso.cpp): a thread owns 32 consecutive elements of a 2048-element
+// tile, transposes each 32-bit limb into 32 planes (plane j = bit j of the 32 limbs) and runs the
+// 32 x 32 blocks of the map; output limbs are produced two at a time, transposed back and staged in
+// shared memory for the stores.  Tiles never straddle products (N % W2_TILE == 0).
+// ---------------------------------------------------------------------------------------------
+#define W2_THREADS 64
+#define W2_TILE (32 * W2_THREADS)
+__device__ __forceinline__ uint32_t w2_swz(uint32_t e) { return e ^ ((e >> 5) & 31); }
+
+// acc pair (a0, a1) = output limbs (O, O + 1) of changeRepr_256 from the 4 input limbs' planes
+__device__ __forceinline__ void psi256_block(int O, int L, const uint32_t* x, uint32_t* a0, uint32_t* a1) {
+    switch (O * 4 + L) {
+        case 0: bs_psi256_0_0(x, a0); bs_psi256_1_0(x, a1); break;
+        case 1: bs_psi256_0_1(x, a0); bs_psi256_1_1(x, a1); break;
+        case 2: bs_psi256_0_2(x, a0); bs_psi256_1_2(x, a1); break;
+        case 3: bs_psi256_0_3(x, a0); bs_psi256_1_3(x, a1); break;
+        case 8: bs_psi256_2_0(x, a0); bs_psi256_3_0(x, a1); break;
+        case 9: bs_psi256_2_1(x, a0); bs_psi256_3_1(x, a1); break;
+        case 10: bs_psi256_2_2(x, a0); bs_psi256_3_2(x, a1); break;
+        case 11: bs_psi256_2_3(x, a0); bs_psi256_3_3(x, a1); break;
+        case 16: bs_psi256_4_0(x, a0); bs_psi256_5_0(x, a1); break;
+        case 17: bs_psi256_4_1(x, a0); bs_psi256_5_1(x, a1); break;
+        case 18: bs_psi256_4_2(x, a0); bs_psi256_5_2(x, a1); break;
+        case 19: bs_psi256_4_3(x, a0); bs_psi256_5_3(x, a1); break;
+        case 24: bs_psi256_6_0(x, a0); bs_psi256_7_0(x, a1); break;
+        case 25: bs_psi256_6_1(x, a0); bs_psi256_7_1(x, a1); break;
+        case 26: bs_psi256_6_2(x, a0); bs_psi256_7_2(x, a1); break;
+        case 27: bs_psi256_6_3(x, a0); bs_psi256_7_3(x, a1); break;
+    }
+}
+__device__ __forceinline__ void ipsi256_block(int O, int L, const uint32_t* x, uint32_t* a0, uint32_t* a1) {
+    switch (O * 8 + L) {
+        case 0: bs_ipsi256_0_0(x, a0); bs_ipsi256_1_0(x, a1); break;
+        case 1: bs_ipsi256_0_1(x, a0); bs_ipsi256_1_1(x, a1); break;
+        case 2: bs_ipsi256_0_2(x, a0); bs_ipsi256_1_2(x, a1); break;
+        case 3: bs_ipsi256_0_3(x, a0); bs_ipsi256_1_3(x, a1); break;
+        case 4: bs_ipsi256_0_4(x, a0); bs_ipsi256_1_4(x, a1); break;
+        case 5: bs_ipsi256_0_5(x, a0); bs_ipsi256_1_5(x, a1); break;
+        case 6: bs_ipsi256_0_6(x, a0); bs_ipsi256_1_6(x, a1); break;
+        case 7: bs_ipsi256_0_7(x, a0); bs_ipsi256_1_7(x, a1); break;
+        case 16: bs_ipsi256_2_0(x, a0); bs_ipsi256_3_0(x, a1); break;
+        case 17: bs_ipsi256_2_1(x, a0); bs_ipsi256_3_1(x, a1); break;
+        case 18: bs_ipsi256_2_2(x, a0); bs_ipsi256_3_2(x, a1); break;
+        case 19: bs_ipsi256_2_3(x, a0); bs_ipsi256_3_3(x, a1); break;
+        case 20: bs_ipsi256_2_4(x, a0); bs_ipsi256_3_4(x, a1); break;
+        case 21: bs_ipsi256_2_5(x, a0); bs_ipsi256_3_5(x, a1); break;
+        case 22: bs_ipsi256_2_6(x, a0); bs_ipsi256_3_6(x, a1); break;
+        case 23: bs_ipsi256_2_7(x, a0); bs_ipsi256_3_7(x, a1); break;
+        case 32: bs_ipsi256_4_0(x, a0); bs_ipsi256_5_0(x, a1); break;
+        case 33: bs_ipsi256_4_1(x, a0); bs_ipsi256_5_1(x, a1); break;
+        case 34: bs_ipsi256_4_2(x, a0); bs_ipsi256_5_2(x, a1); break;
+        case 35: bs_ipsi256_4_3(x, a0); bs_ipsi256_5_3(x, a1); break;
+        case 36: bs_ipsi256_4_4(x, a0); bs_ipsi256_5_4(x, a1); break;
+        case 37: bs_ipsi256_4_5(x, a0); bs_ipsi256_5_5(x, a1); break;
+        case 38: bs_ipsi256_4_6(x, a0); bs_ipsi256_5_6(x, a1); break;
+        case 39: bs_ipsi256_4_7(x, a0); bs_ipsi256_5_7(x, a1); break;
+        case 48: bs_ipsi256_6_0(x, a0); bs_ipsi256_7_0(x, a1); break;
+        case 49: bs_ipsi256_6_1(x, a0); bs_ipsi256_7_1(x, a1); break;
+        case 50: bs_ipsi256_6_2(x, a0); bs_ipsi256_7_2(x, a1); break;
+        case 51: bs_ipsi256_6_3(x, a0); bs_ipsi256_7_3(x, a1); break;
+        case 52: bs_ipsi256_6_4(x, a0); bs_ipsi256_7_4(x, a1); break;
+        case 53: bs_ipsi256_6_5(x, a0); bs_ipsi256_7_5(x, a1); break;
+        case 54: bs_ipsi256_6_6(x, a0); bs_ipsi256_7_6(x, a1); break;
+        case 55: bs_ipsi256_6_7(x, a0); bs_ipsi256_7_7(x, a1); break;
+    }
+}
+
+// thread-own planes of input limb L -> x (in place transposed data in In)
+__device__ __forceinline__ void w2_load_planes(const uint32_t* In, int L, uint32_t e0, uint32_t* x) {
+#pragma unroll
+    for (int j = 0; j < 32; j++) x[j] = In[L * W2_TILE + w2_swz(e0 + j)];
+}
+__device__ __forceinline__ void w2_transpose_own(uint32_t* In, int nl, uint32_t e0) {
+#pragma unroll 1
+    for (int L = 0; L < nl; L++) {
+        uint32_t x[32];
+        w2_load_planes(In, L, e0, x);
+        transpose32(x);
+#pragma unroll
+        for (int j = 0; j < 32; j++) In[L * W2_TILE + w2_swz(e0 + j)] = x[j];
+    }
+}
+
+// changeRepr: S[(o batch + p) s_per + i] (0 for i >= s_per) -> W[o][lo/hi plane][p][i]
+__global__ void __launch_bounds__(W2_THREADS) k_psi256_bs(const uint4* __restrict__ S, uint64_t s_per, uint64_t N,
+                                                          uint64_t batch, int ops, uint4* __restrict__ W) {
+    extern __shared__ __align__(1024) uint32_t w2_smem[];
+    uint32_t* In = w2_smem;                  // [4][W2_TILE] limb planes
+    uint32_t* Stg = w2_smem + 4 * W2_TILE;   // [2][W2_TILE] two output limbs
+    const uint64_t per_op = batch * N, ntiles = per_op * ops / W2_TILE;
+    const uint32_t t = threadIdx.x, e0 = 32 * t;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t g0 = tile * W2_TILE, o = g0 / per_op, r0 = g0 - o * per_op, p = r0 / N, i0 = r0 - p * N;
+        const uint4* src = S + (o * batch + p) * s_per;
+        __syncthreads();   // previous tile's stores done with Stg / In
+        for (uint32_t e = t; e < W2_TILE; e += W2_THREADS) {
+            const uint64_t i = i0 + e;
+            const uint4 v = i < s_per ? src[i] : make_uint4(0, 0, 0, 0);
+            const uint32_t q = w2_swz(e);
+            In[q] = v.x; In[W2_TILE + q] = v.y; In[2 * W2_TILE + q] = v.z; In[3 * W2_TILE + q] = v.w;
+        }
+        __syncthreads();
+        w2_transpose_own(In, 4, e0);
+        uint4* dlo = W + o * 2 * per_op + p * N + i0;
+#pragma unroll 1
+        for (int O = 0; O < 8; O += 2) {
+            uint32_t a0[32], a1[32];
+#pragma unroll
+            for (int j = 0; j < 32; j++) { a0[j] = 0; a1[j] = 0; }
+#pragma unroll 1
+            for (int L = 0; L < 4; L++) {
+                uint32_t x[32];
+                w2_load_planes(In, L, e0, x);
+                psi256_block(O, L, x, a0, a1);
+            }
+            transpose32(a0);
+            transpose32(a1);
+            __syncthreads();   // previous pair's stores have read Stg
+#pragma unroll
+            for (int j = 0; j < 32; j++) { Stg[w2_swz(e0 + j)] = a0[j]; Stg[W2_TILE + w2_swz(e0 + j)] = a1[j]; }
+            __syncthreads();
+            uint32_t* d32 = reinterpret_cast<uint32_t*>(dlo + (O >= 4 ? per_op : 0)) + (O & 3);
+            for (uint32_t e = t; e < W2_TILE; e += W2_THREADS) {
+                const uint32_t q = w2_swz(e);
+                *reinterpret_cast<uint2*>(d32 + 4 * e) = make_uint2(Stg[q], Stg[W2_TILE + q]);
+            }
+        }
+    }
+}
+
+// changeRepr^-1 + InterleavedCombine: planes W (lo at W + p N, hi at + batch N) -> out (n_out = 2N words
+// per product): out block w = lo128(C_w) ^ hi128(C_(w-1)), word 2w = limbs 0,1, word 2w+1 = limbs 2,3.
+// Pairs run (4,5), (0,1), (6,7), (2,3): the hi pair of every element is staged before the lo pair that
+// needs its predecessor's.  The tile's first element takes its predecessor from Hp (thread 0, tables).
+__global__ void __launch_bounds__(W2_THREADS) k_ipsi256_bs(const uint4* __restrict__ W, uint64_t N, uint64_t batch,
+                                                           const DevTables256* __restrict__ T, uint64_t* __restrict__ out) {
+    extern __shared__ __align__(1024) uint32_t w2_smem[];
+    uint32_t* In = w2_smem;                  // [8][W2_TILE]
+    uint32_t* H = w2_smem + 8 * W2_TILE;     // [2][W2_TILE] staged hi pair
+    __shared__ uint4 Hp;                     // predecessor's C hi128 (limbs 4..7)
+    const uint64_t plane = batch * N, ntiles = plane / W2_TILE;
+    const uint32_t t = threadIdx.x, e0 = 32 * t;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t g0 = tile * W2_TILE, p = g0 / N, i0 = g0 - p * N;
+        const uint4* lo = W + g0;
+        const uint4* hi = lo + plane;
+        __syncthreads();
+        for (uint32_t e = t; e < W2_TILE; e += W2_THREADS) {
+            const uint4 a = lo[e], b = hi[e];
+            const uint32_t q = w2_swz(e);
+            In[q] = a.x; In[W2_TILE + q] = a.y; In[2 * W2_TILE + q] = a.z; In[3 * W2_TILE + q] = a.w;
+            In[4 * W2_TILE + q] = b.x; In[5 * W2_TILE + q] = b.y; In[6 * W2_TILE + q] = b.z; In[7 * W2_TILE + q] = b.w;
+        }
+        if (t == 0) {
+            uint4 rlo = make_uint4(0, 0, 0, 0), rhi = rlo;
+            if (i0 != 0) ipsi256_apply(T->ipsi, lo[-1], hi[-1], rlo, rhi);   // (L1-cached global tables)
+            Hp = rhi;
+        }
+        __syncthreads();
+        w2_transpose_own(In, 8, e0);
+        uint64_t* dst = out + p * 2 * N + 2 * i0;
+#pragma unroll 1
+        for (int k = 0; k < 4; k++) {
+            const int O = k == 0 ? 4 : (k == 1 ? 0 : (k == 2 ? 6 : 2));
+            uint32_t a0[32], a1[32];
+#pragma unroll
+            for (int j = 0; j < 32; j++) { a0[j] = 0; a1[j] = 0; }
+#pragma unroll 1
+            for (int L = 0; L < 8; L++) {
+                uint32_t x[32];
+                w2_load_planes(In, L, e0, x);
+                ipsi256_block(O, L, x, a0, a1);
+            }
+            transpose32(a0);
+            transpose32(a1);
+            if (O >= 4) {   // stage the hi pair (4,5) / (6,7)
+                __syncthreads();   // previous lo pair done reading H
+#pragma unroll
+                for (int j = 0; j < 32; j++) { H[w2_swz(e0 + j)] = a0[j]; H[W2_TILE + w2_swz(e0 + j)] = a1[j]; }
+                __syncthreads();
+            } else {        // lo pair (0,1) / (2,3): xor the predecessor's staged hi pair, write one word
+                const int hsel = O == 0 ? 0 : 2;   // limbs 4,5 (word 2w) or 6,7 (word 2w+1) of C_(w-1)
+                const uint32_t* hp = reinterpret_cast<const uint32_t*>(&Hp) + hsel;
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    const uint32_t e = e0 + j;
+                    const uint32_t p0 = e ? H[w2_swz(e - 1)] : hp[0];
+                    const uint32_t p1 = e ? H[W2_TILE + w2_swz(e - 1)] : hp[1];
+                    dst[2 * e + (O == 0 ? 0 : 1)] = ((uint64_t)(a1[j] ^ p1) << 32) | (a0[j] ^ p0);
+                }
+            }
         }
     }
 }
@@ -224,6 +422,7 @@ static gf2x_status get_tables256(DeviceState* ds, DevTables256** out) {
         delete h;
         if (e != cudaSuccess) { cudaFree(d); return fail(GF2X_ECUDA, cudaGetErrorString(e)); }
         CUDA_TRY(cudaFuncSetAttribute(k_w128_post, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_ipsi256_bs, cudaFuncAttributeMaxDynamicSharedMemorySize, 10 * W2_TILE * 4));
         ds->tabs256 = d;
     }
     *out = ds->tabs256;
@@ -281,8 +480,18 @@ static gf2x_status run_pipeline_w128(const uint64_t* a, uint64_t a_bits, const u
         if ((s = run_cvt<uint4>(P.cvt_a, Sa, P.ma, B, false, smc, st)) != GF2X_OK) return s;
         if ((s = run_cvt<uint4>(P.cvt_b, Sb, P.mb, B, false, smc, st)) != GF2X_OK) return s;
     }
-    // changeRepr into TGF(2^256)
-    if (same) {
+    // changeRepr into TGF(2^256): bit-sliced when the tiles fit the products, else M4R-4
+    const bool w2bs = P.N % W2_TILE == 0 && !env_flag("GF2X_NO_W2_BS");
+    if (w2bs) {
+        ProfScope ps("k_psi256_bs", (double)B * (((1ull << P.ma) + (1ull << P.mb)) * 16 + 2 * P.N * 32), st);
+        const size_t sm = 6 * W2_TILE * 4;
+        if (same) {
+            k_psi256_bs<<<grid_for(2 * plane / W2_TILE, 1, smc, 4), W2_THREADS, sm, st>>>(Sa, 1ull << P.ma, P.N, B, 2, Wa);
+        } else {
+            k_psi256_bs<<<grid_for(plane / W2_TILE, 1, smc, 4), W2_THREADS, sm, st>>>(Sa, 1ull << P.ma, P.N, B, 1, Wa);
+            k_psi256_bs<<<grid_for(plane / W2_TILE, 1, smc, 4), W2_THREADS, sm, st>>>(Sb, 1ull << P.mb, P.N, B, 1, Wb);
+        }
+    } else if (same) {
         ProfScope ps("k_psi256", 2.0 * B * ((1ull << P.ma) * 16 + P.N * 32), st);
         k_psi256<<<grid_for(2 * plane, PSI256_THREADS, smc, 4), PSI256_THREADS, 0, st>>>(Sa, 1ull << P.ma, P.N, B, 2, T256, Wa);
     } else {
@@ -325,9 +534,12 @@ static gf2x_status run_pipeline_w128(const uint64_t* a, uint64_t a_bits, const u
     if ((s = run_cvt<uint4>(P.icvt, Wa, P.m, 2 * B, true, smc, st)) != GF2X_OK) return s;
     if (stop_stage == 5) return GF2X_OK;
     // changeRepr^-1 + InterleavedCombine
-    {
+    if (w2bs && P.na + P.nb == 2 * P.N) {
+        ProfScope ps("k_ipsi256_bs", 32.0 * plane + 16.0 * plane, st);
+        k_ipsi256_bs<<<grid_for(plane / W2_TILE, 1, smc, 2), W2_THREADS, 10 * W2_TILE * 4, st>>>(Wa, P.N, B, T256, c);
+    } else {
         const uint64_t n_out = P.na + P.nb, nblk = (n_out + 1) / 2;
-        const uint64_t ctas = (nblk + IPSI256_STEP - 1) / IPSI256_STEP * B;
+        const uint64_t ctas = (nblk + IPSI256_THREADS - 1) / IPSI256_THREADS * B;
         ProfScope ps("k_ipsi256", 32.0 * plane + 8.0 * n_out * B, st);
         k_ipsi256<<<grid_for(ctas, 1, smc, 4), IPSI256_THREADS, 64 * 16 * 2 * 16, st>>>(Wa, P.N, B, n_out, T256, c);
     }

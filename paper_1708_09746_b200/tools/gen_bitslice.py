@@ -169,6 +169,36 @@ def emit_const(fname, const, l):
     return src, P.ops
 
 
+def iso_columns(which=None):
+    """Columns printed by tools/dump_iso.cpp (compiled from the product's field_host.h)."""
+    import subprocess
+    import tempfile
+    src = os.path.join(HERE, "dump_iso.cpp")
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "dump_iso")
+        subprocess.run(["g++", "-O2", "-o", exe, src], check=True)
+        out = subprocess.run([exe] + ([which] if which else []), check=True, capture_output=True, text=True).stdout
+    return [int(x, 16) for x in out.split()]
+
+
+def emit_linmap_block(name, o_limb, i_limb, cols):
+    """acc[i] ^= bit (32 o_limb + i) of the linear map with columns `cols` applied to the 32 planes of input
+    limb i_limb (columns 32 i_limb .. 32 i_limb + 31)."""
+    P = Prog()
+    x = [f"X{i}" for i in range(32)]
+    rows = [[j for j in range(32) if (cols[32 * i_limb + j] >> (32 * o_limb + i)) & 1] for i in range(32)]
+    r = apply_linmap(P, x, rows)
+    tail = [f"acc[{i}] ^= {r[i]};" for i in range(32) if r[i] != "0u"]
+    import re as _re
+    used = set(_re.findall(r"\bX(\d+)\b", " ".join(P.lines + tail)))
+    pre = [f"const uint32_t X{i} = x[{i}];" for i in range(32) if str(i) in used]
+    body = pre + P.lines + tail
+    src = (f"// {name}: output limb {o_limb} <- input limb {i_limb}: {P.ops['xor']} XOR\n"
+           f"GF2X_HD GF2X_INLINE void {name}_{o_limb}_{i_limb}(const uint32_t* __restrict__ x, "
+           f"uint32_t* __restrict__ acc) {{\n  " + "\n  ".join(body) + "\n}\n")
+    return src, P.ops["xor"]
+
+
 def ipsi_columns():
     """Columns of changeRepr^-1 (tower v_k -> polynomial basis), from the product's field_host.h
     (compiled and run via tools/dump_iso.cpp), so both ipsi paths share one isomorphism."""
@@ -219,6 +249,24 @@ def main():
             src, n = emit_ipsi_block(o, i, cols)
             parts.append(src)
             nx += n
+    # w = 128 (TGF(2^256)): changeRepr 128 -> 256 bits (4 x 8 blocks) and changeRepr^-1 256 -> 256 (8 x 8)
+    c256 = iso_columns("psi256")
+    assert len(c256) == 128
+    n256 = 0
+    for o in range(8):
+        for i in range(4):
+            src, n = emit_linmap_block("bs_psi256", o, i, c256)
+            parts.append(src)
+            n256 += n
+    ci256 = iso_columns("ipsi256")
+    assert len(ci256) == 256
+    ni256 = 0
+    for o in range(8):
+        for i in range(8):
+            src, n = emit_linmap_block("bs_ipsi256", o, i, ci256)
+            parts.append(src)
+            ni256 += n
+    print("psi256 xor", n256, "ipsi256 xor", ni256, file=sys.stderr)
     with open(OUT, "w") as f:
         f.write("\n".join(parts))
     print("bs_mul32 ops", ops, "ipsi blocks xor", nx, file=sys.stderr)
