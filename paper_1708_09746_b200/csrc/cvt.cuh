@@ -363,13 +363,20 @@ __global__ void __launch_bounds__(RB_THREADS, 3) k_cvt_rb(CvtRbParams p) {
         if (p.mode) base = tt << (p.R + p.C);
         else base = ((tt & ((1ull << midbits) - 1)) << p.C) | ((tt >> midbits) << (p.r_lo + p.R));
     };
+    // a thread's slots s = tid EPC + k S (S = threads EPC, a multiple of the tile's column count) advance the
+    // global pointer by a constant stride: strength-reduced 64-bit addressing in the copy loops
+    const uint32_t S = blockDim.x * EPC;
+    const uint64_t gstride = p.mode ? (uint64_t)S : ((uint64_t)(S >> p.C) << p.r_lo);
     auto prefetch = [&](uint64_t t, T* buf) {
         T* dp; uint64_t base;
         tile_at(t, dp, base);
-        for (uint32_t s = threadIdx.x * EPC; s < nslots; s += blockDim.x * EPC) {
-            uint32_t sm; uint64_t g;
-            rb_slot<T>(p, s, base, sm, g);
-            cp_async16(buf + sm, dp + g);
+        uint32_t s = threadIdx.x * EPC, sm;
+        uint64_t g;
+        rb_slot<T>(p, s, base, sm, g);
+        const T* gp = dp + g;
+        for (; s < nslots; s += S, gp += gstride) {
+            rb_slot<T>(p, s, 0, sm, g);
+            cp_async16(buf + sm, gp);
         }
     };
     if (blockIdx.x < ntiles) prefetch(blockIdx.x, reinterpret_cast<T*>(smem_raw));
@@ -391,10 +398,15 @@ __global__ void __launch_bounds__(RB_THREADS, 3) k_cvt_rb(CvtRbParams p) {
         }
         T* dp; uint64_t base;
         tile_at(t, dp, base);
-        for (uint32_t s = threadIdx.x * EPC; s < nslots; s += blockDim.x * EPC) {
-            uint32_t sm; uint64_t g;
+        {
+            uint32_t s = threadIdx.x * EPC, sm;
+            uint64_t g;
             rb_slot<T>(p, s, base, sm, g);
-            *reinterpret_cast<uint4*>(dp + g) = *reinterpret_cast<const uint4*>(buf + sm);
+            T* gp = dp + g;
+            for (; s < nslots; s += S, gp += gstride) {
+                rb_slot<T>(p, s, 0, sm, g);
+                *reinterpret_cast<uint4*>(gp) = *reinterpret_cast<const uint4*>(buf + sm);
+            }
         }
         __syncthreads();   // the buffer is refilled by the prefetch two tiles on
     }
