@@ -239,6 +239,17 @@ def main():
             sharded_error, ok = f"{type(e).__name__}: {e}"[:300], 0
         flag = torch.tensor([ok], dtype=torch.int32, device=dev)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            # the first partitioned product must equal the single-GPU one (rank 0 checks), else fall back
+            parts = [torch.empty_like(sc) for _ in range(world)]
+            dist.all_gather(parts, sc)
+            if rank == 0:
+                G.gf2x_mul(da, bits, db, bits, dc, stream=stream)
+                torch.cuda.synchronize()
+                if not torch.equal(torch.cat(parts).view(torch.int64), dc.view(torch.int64)):
+                    ok, sharded_error = 0, "sharded product differs from the single-GPU product"
+            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if int(flag.item()) == 0:
             sharded, mode = False, "replicas"
             sharded_error = sharded_error or "another rank failed"
@@ -410,7 +421,8 @@ def main():
             "workload": WORKLOAD[args.config] + ("" if args.w == 64 else ", w=128 blocks over TGF(2^256)"),
             "config": args.config, "operand_bits": bits, "batch": batch, "block_width": args.w,
             "fft_points": 1 << max(0, (2 * n - 2).bit_length()) >> (0 if args.w == 64 else 1),
-            "parallelism": (f"sharded FFT over {world} GPUs (NCCL)" if sharded else
+            "parallelism": (f"sharded FFT over {world} GPUs (" + ("peer memory: CUDA IPC over NVLink, fused pull-pack "
+                            "all-to-all, NCCL barriers" if comm.peer_memory() == 1 else "NCCL send/recv") + ")" if sharded else
                             ("replicas" if world > 1 else "single")),
             "seed": DEFAULT_SEED, "l2": "working set > 126 MB L2 (operands + 2 spectra), no flush" if bits >= 1 << 28
             else "working set may be L2-resident (small config)",

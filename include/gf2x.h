@@ -106,6 +106,12 @@ typedef struct gf2x_comm_s* gf2x_comm_t;
 gf2x_status gf2x_comm_unique_id(void* id_out);
 gf2x_status gf2x_comm_init(const void* nccl_unique_id, int nranks, int rank, gf2x_comm_t* out);
 gf2x_status gf2x_comm_destroy(gf2x_comm_t comm);
+/* Exchange path of the communicator, fixed by its first gf2x_mul_sharded (and whenever the workspace
+ * grows): 1 = peer memory (every rank's workspace mapped with CUDA IPC; the all-to-all is pulled and
+ * (un)packed by one kernel over NVLink, the other exchanges are peer copies, ordering by stream-ordered
+ * NCCL all-reduce barriers), 0 = NCCL grouped send/recv (IPC unavailable or GF2X_SHARD_NCCL=1; all ranks
+ * agree), -1 = null comm. */
+int gf2x_comm_peer_memory(gf2x_comm_t comm);
 gf2x_status gf2x_mul_sharded(const uint64_t* a_shard, const uint64_t* b_shard, uint64_t bits,
                              uint64_t* c_shard, gf2x_comm_t comm, void* stream);
 gf2x_status gf2x_mul_sharded_sim(const uint64_t* a, const uint64_t* b, uint64_t bits, uint64_t* c,

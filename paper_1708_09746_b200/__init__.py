@@ -24,6 +24,7 @@ EXPORTS = [
     "gf2x_debug_stage", "gf2x_comm_unique_id", "gf2x_comm_init", "gf2x_comm_destroy", "gf2x_mul_sharded",
     "gf2x_mul_sharded_sim", "gf2x_debug_shard_stage", "gf2x_shard_plan", "gf2x_profile_enable", "gf2x_profile_report", "gf2x_status_string", "gf2x_last_error",
     "gf2x_release", "gf2x_version", "gf2x_mul_w", "gf2x_launch_count_w", "gf2x_debug_stage_w128",
+    "gf2x_comm_peer_memory",
 ]
 
 
@@ -63,6 +64,7 @@ def load(path: str = LIB_PATH):
     L.gf2x_comm_unique_id.argtypes = [vp]
     L.gf2x_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
     L.gf2x_comm_destroy.argtypes = [vp]
+    L.gf2x_comm_peer_memory.argtypes = [vp]
     L.gf2x_mul_sharded.argtypes = [vp, vp, u64, vp, vp, vp]
     L.gf2x_mul_sharded_sim.argtypes = [vp, vp, u64, vp, i32, vp]
     L.gf2x_debug_shard_stage.argtypes = [vp, vp, u64, i32, i32, vp, vp]
@@ -218,6 +220,10 @@ class Comm:
         _check(load().gf2x_mul_sharded(_ptr(a_shard), _ptr(b_shard), bits, _ptr(c_shard), self.handle,
                                        _stream_ptr(stream)))
         return c_shard
+
+    def peer_memory(self) -> int:
+        """1: exchanges over peer memory (CUDA IPC / NVLink), 0: NCCL send/recv (see include/gf2x.h)."""
+        return int(load().gf2x_comm_peer_memory(self.handle))
 
     def close(self):
         if self.handle:

@@ -1102,12 +1102,20 @@ gf2x_status gf2x_comm_init(const void* nccl_unique_id, int nranks, int rank, gf2
     if (!err.empty()) return fail(GF2X_ENCCL, err);
     nccl_uid_t id;
     memcpy(&id, nccl_unique_id, sizeof(id));
+    if (nranks > SHARD_MAXG) return fail(GF2X_EINVAL, "at most 8 ranks");
     gf2x_comm_s* c = new gf2x_comm_s();
     c->nranks = nranks;
     c->rank = rank;
     c->ws = nullptr;
     c->ws_bytes = 0;
+    c->p2p = 0;
+    for (int r = 0; r < SHARD_MAXG; r++) c->peer_ws[r] = nullptr;
     cudaGetDevice(&c->device);
+    if (cudaMalloc(&c->d_sync, 256 + SHARD_MAXG * sizeof(cudaIpcMemHandle_t)) != cudaSuccess) {
+        delete c;
+        return fail(GF2X_ENOMEM, "comm sync buffer");
+    }
+    cudaMemset(c->d_sync, 0, 256);
     int rc = g_nccl.CommInitRank(&c->comm, nranks, id, rank);
     if (rc) {
         delete c;
@@ -1117,8 +1125,58 @@ gf2x_status gf2x_comm_init(const void* nccl_unique_id, int nranks, int rank, gf2
     return GF2X_OK;
 }
 
+static void comm_unmap_peers(gf2x_comm_s* c) {
+    for (int r = 0; r < SHARD_MAXG; r++)
+        if (c->peer_ws[r] && r != c->rank) cudaIpcCloseMemHandle(c->peer_ws[r]);
+    for (int r = 0; r < SHARD_MAXG; r++) c->peer_ws[r] = nullptr;
+    c->p2p = 0;
+}
+
+// Map every rank's workspace into this process (CUDA IPC; NVLink peer access).  Collective: the handles
+// go around with an NCCL all-gather and the outcome is agreed with an all-reduce(min), so every rank
+// takes the same exchange path.  GF2X_SHARD_NCCL=1 keeps NCCL send/recv.
+static gf2x_status comm_map_peers(gf2x_comm_s* c, cudaStream_t st) {
+    comm_unmap_peers(c);
+    const int G = c->nranks;
+    int ok = getenv("GF2X_SHARD_NCCL") ? 0 : 1;
+    cudaIpcMemHandle_t mine;
+    memset(&mine, 0, sizeof(mine));
+    if (ok && cudaIpcGetMemHandle(&mine, c->ws) != cudaSuccess) { ok = 0; cudaGetLastError(); }
+    unsigned char* dh = reinterpret_cast<unsigned char*>(c->d_sync) + 256;
+    CUDA_TRY(cudaMemcpyAsync(dh + c->rank * sizeof(mine), &mine, sizeof(mine), cudaMemcpyHostToDevice, st));
+    int rc = g_nccl.AllGather(dh + c->rank * sizeof(mine), dh, sizeof(mine), NCCL_UINT8, c->comm, st);
+    if (rc) return fail(GF2X_ENCCL, std::string("IPC handle all-gather: ") + g_nccl.GetErrorString(rc));
+    std::vector<cudaIpcMemHandle_t> hs(G);
+    CUDA_TRY(cudaMemcpyAsync(hs.data(), dh, G * sizeof(mine), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    c->peer_ws[c->rank] = c->ws;
+    for (int r = 0; r < G && ok; r++) {
+        if (r == c->rank) continue;
+        if (cudaIpcOpenMemHandle(&c->peer_ws[r], hs[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            ok = 0;
+            c->peer_ws[r] = nullptr;
+            cudaGetLastError();
+        }
+    }
+    int* dflag = c->d_sync + 1;
+    CUDA_TRY(cudaMemcpyAsync(dflag, &ok, sizeof(int), cudaMemcpyHostToDevice, st));
+    rc = g_nccl.AllReduce(dflag, dflag, 1, NCCL_INT32, NCCL_MIN, c->comm, st);
+    if (rc) return fail(GF2X_ENCCL, std::string("IPC agreement: ") + g_nccl.GetErrorString(rc));
+    int all = 0;
+    CUDA_TRY(cudaMemcpyAsync(&all, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (!all) comm_unmap_peers(c);
+    else c->p2p = 1;
+    return GF2X_OK;
+}
+
+int gf2x_comm_peer_memory(gf2x_comm_t comm) { return comm ? comm->p2p : -1; }
+
 gf2x_status gf2x_comm_destroy(gf2x_comm_t comm) {
     if (!comm) return GF2X_OK;
+    cudaDeviceSynchronize();
+    comm_unmap_peers(comm);
+    if (comm->d_sync) cudaFree(comm->d_sync);
     if (comm->ws) { cudaDeviceSynchronize(); cudaFree(comm->ws); }
     int rc = g_nccl.h ? g_nccl.CommDestroy(comm->comm) : 0;
     delete comm;
@@ -1141,11 +1199,16 @@ gf2x_status gf2x_mul_sharded(const uint64_t* a_shard, const uint64_t* b_shard, u
     if (s != GF2X_OK) return s;
     ShardGeom S;
     if ((s = shard_geom(bits, comm->nranks, S)) != GF2X_OK) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (comm->ws_bytes < S.bytes) {
-        if (comm->ws) { cudaDeviceSynchronize(); cudaFree(comm->ws); comm->ws = nullptr; comm->ws_bytes = 0; }
+        // (collective: every rank grows its workspace in the same call, the sizes depend on (bits, G) only)
+        cudaDeviceSynchronize();
+        comm_unmap_peers(comm);
+        if (comm->ws) { cudaFree(comm->ws); comm->ws = nullptr; comm->ws_bytes = 0; }
         cudaError_t e = cudaMalloc(&comm->ws, S.bytes);
         if (e != cudaSuccess) return fail(GF2X_ENOMEM, std::string("shard workspace: ") + cudaGetErrorString(e));
         comm->ws_bytes = S.bytes;
+        if ((s = comm_map_peers(comm, st)) != GF2X_OK) return s;
     }
     std::vector<RankCtx> ranks(1);
     ranks[0].r = comm->rank;
@@ -1153,8 +1216,13 @@ gf2x_status gf2x_mul_sharded(const uint64_t* a_shard, const uint64_t* b_shard, u
     ranks[0].b_shard = b_shard;
     ranks[0].c_shard = c_shard;
     rank_bufs(ranks[0], (unsigned char*)comm->ws, S);
-    ShardExec X{false, comm, reinterpret_cast<cudaStream_t>(stream), &ranks};
-    return run_sharded(S, X, ds, ds->host, bits);
+    ShardExec X{false, comm, st, &ranks};
+    X.p2p = comm->p2p != 0;
+    X.off = S.off;
+    for (int r = 0; r < comm->nranks; r++) X.peer[r] = (unsigned char*)comm->peer_ws[r];
+    if ((s = run_sharded(S, X, ds, ds->host, bits)) != GF2X_OK) return s;
+    // the next call rewrites this workspace: every peer must be done pulling from it
+    return X.p2p ? X.barrier() : GF2X_OK;
 }
 
 static gf2x_status sharded_sim(const uint64_t* a, const uint64_t* b, uint64_t bits, uint64_t* c, int nranks, void* stream,
@@ -1186,6 +1254,8 @@ static gf2x_status sharded_sim(const uint64_t* a, const uint64_t* b, uint64_t bi
         rank_bufs(ranks[r], (unsigned char*)ds->shard_ws + r * S.bytes, S);
     }
     ShardExec X{true, nullptr, st, &ranks};
+    X.p2p = getenv("GF2X_SHARD_LISTS") == nullptr;   // default: the peer-memory pulls (lists: copy engine)
+    X.off = S.off;
     return run_sharded(S, X, ds, ds->host, bits, debug_stage, (uint4*)dbg);
 }
 

@@ -29,6 +29,7 @@
 // ---------------------------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------------------------
+#define SHARD_MAXG 8       // ranks
 #define SHARD_MAXJ 128
 #define SHARD_MAXJ_UNR 4   // block words prefetched per point (G <= 8)
 
@@ -87,6 +88,33 @@ __global__ void k_pack(const uint4* __restrict__ H, uint4* __restrict__ X, uint6
     }
 }
 
+// Peer-memory all-to-all fused with the (un)packing (SURVEY §8e "exchange fused with compute"):
+//   pull-pack, rank q:   T[r chunk + j] = W_r[pack_src(q, j)]     (every rank r's blocked W)
+//   pull-unpack, rank r: W[pack_src(q, j)] = T_q[r chunk + j]     (every rank q's t-sliced T)
+// src[] are the G ranks' buffers (IPC-mapped peers over NVLink, or the virtual ranks of the simulation).
+struct PullParams {
+    const uint4* src[SHARD_MAXG];
+    uint4* dst;
+    uint64_t chunk;
+    int me, G, Kg, K;
+};
+__global__ void k_pull_pack(PullParams p) {
+    const uint64_t total = p.chunk * p.G;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(t / p.chunk);
+        const uint64_t j = t - (uint64_t)r * p.chunk;
+        p.dst[t] = p.src[r][pack_src((uint64_t)p.me, j, p.Kg, p.K)];
+    }
+}
+__global__ void k_pull_unpack(PullParams p) {
+    const uint64_t total = p.chunk * p.G;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+        const int q = (int)(t / p.chunk);
+        const uint64_t j = t - (uint64_t)q * p.chunk;
+        p.dst[pack_src((uint64_t)q, j, p.Kg, p.K)] = p.src[q][(uint64_t)p.me * p.chunk + j];
+    }
+}
+
 // f[i] ^= src[i], i in [lo, hi)
 __global__ void k_xor_range(uint4* __restrict__ f, const uint4* __restrict__ src, uint64_t lo, uint64_t hi) {
     for (uint64_t i = lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < hi; i += (uint64_t)gridDim.x * blockDim.x)
@@ -104,6 +132,7 @@ struct NcclApi {
     int (*CommInitRank)(nccl_comm_t*, int, nccl_uid_t, int);
     int (*CommDestroy)(nccl_comm_t);
     int (*AllGather)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t);
+    int (*AllReduce)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t);
     int (*Send)(const void*, size_t, int, int, nccl_comm_t, cudaStream_t);
     int (*Recv)(void*, size_t, int, int, nccl_comm_t, cudaStream_t);
     int (*GroupStart)();
@@ -111,6 +140,8 @@ struct NcclApi {
     const char* (*GetErrorString)(int);
 };
 static const int NCCL_UINT8 = 1;   // ncclUint8 in the ncclDataType_t enum
+static const int NCCL_INT32 = 2;   // ncclInt32
+static const int NCCL_SUM = 0, NCCL_MIN = 3;   // ncclRedOp_t
 static NcclApi g_nccl;
 static std::string nccl_load() {
     if (g_nccl.h) return "";
@@ -124,6 +155,7 @@ static std::string nccl_load() {
     NCCL_SYM(CommInitRank, "ncclCommInitRank");
     NCCL_SYM(CommDestroy, "ncclCommDestroy");
     NCCL_SYM(AllGather, "ncclAllGather");
+    NCCL_SYM(AllReduce, "ncclAllReduce");
     NCCL_SYM(Send, "ncclSend");
     NCCL_SYM(Recv, "ncclRecv");
     NCCL_SYM(GroupStart, "ncclGroupStart");
@@ -139,13 +171,19 @@ struct gf2x_comm_s {
     nccl_comm_t comm;
     void* ws;          // per-communicator workspace (grown on demand)
     size_t ws_bytes;
+    // peer-memory exchange: every rank's workspace mapped into this process (CUDA IPC over NVLink);
+    // p2p = 0 falls back to NCCL grouped send/recv
+    int p2p;
+    void* peer_ws[SHARD_MAXG];
+    int* d_sync;       // 1 int (stream-ordered barrier = NCCL all-reduce of it) + IPC handle staging
 };
 
 // ---------------------------------------------------------------------------------------------
 // host orchestration
 // ---------------------------------------------------------------------------------------------
 // workspace buffers (SB_A..SB_HALO) and the caller's input shards (SB_INA, SB_INB: sources only)
-enum ShardBuf { SB_A = 0, SB_B, SB_W, SB_T, SB_X, SB_HALO, SB_COUNT, SB_INA = SB_COUNT, SB_INB, SB_ALL };
+// SB_CA, SB_CB: this rank's input shards copied into the workspace (the peer-memory gather reads them)
+enum ShardBuf { SB_A = 0, SB_B, SB_W, SB_T, SB_X, SB_HALO, SB_CA, SB_CB, SB_COUNT, SB_INA = SB_COUNT, SB_INB, SB_ALL };
 
 struct RankCtx {
     int r;
@@ -215,6 +253,8 @@ static gf2x_status shard_geom(uint64_t bits, int G, ShardGeom& S) {
     S.off[SB_T] = o; o = align256(o + S.Nloc * 16);
     S.off[SB_X] = o; o = align256(o + S.Nloc * 16);
     S.off[SB_HALO] = o; o = align256(o + 16);
+    S.off[SB_CA] = o; o = align256(o + S.n / G * 8);
+    S.off[SB_CB] = o; o = align256(o + S.n / G * 8);
     S.bytes = o;
     return GF2X_OK;
 }
@@ -233,7 +273,39 @@ struct ShardExec {
     gf2x_comm_s* comm;   // NCCL mode
     cudaStream_t st;
     std::vector<RankCtx>* ranks;   // all ranks (sim) or the local one (NCCL)
+    bool p2p = false;              // pull from peer memory (sim: the virtual ranks' buffers; NCCL: IPC-mapped)
+    unsigned char* peer[SHARD_MAXG] = {};   // p2p, NCCL mode: every rank's workspace base
+    const size_t* off = nullptr;   // buffer offsets in a workspace (ShardGeom::off)
+    // pointer to rank r's buffer b (p2p)
+    unsigned char* rbuf(int r, ShardBuf b) {
+        if (sim) return (*ranks)[r].buf[b];
+        if (r == comm->rank) return (*ranks)[0].buf[b];
+        return peer[r] + off[b];
+    }
+    // stream-ordered barrier of all ranks: every rank's work enqueued before it has finished when any
+    // rank's work enqueued after it starts (NCCL all-reduce of one int); nothing to do in the simulation
+    gf2x_status barrier() {
+        if (sim) return GF2X_OK;
+        int rc = g_nccl.AllReduce(comm->d_sync, comm->d_sync, 1, NCCL_INT32, NCCL_SUM, comm->comm, st);
+        if (rc) return fail(GF2X_ENCCL, std::string("NCCL barrier: ") + g_nccl.GetErrorString(rc));
+        return GF2X_OK;
+    }
     gf2x_status run(const std::vector<Xfer>& xs) {
+        if (p2p) {   // every destination pulls its transfers from the source's memory
+            gf2x_status s = barrier();
+            if (s != GF2X_OK) return s;
+            for (const Xfer& x : xs) {
+                if (!owns(x.dst)) continue;
+                ShardBuf sb = x.sb;
+                if (!sim && sb == SB_INA) sb = SB_CA;   // peers' input shards are read from their copies
+                if (!sim && sb == SB_INB) sb = SB_CB;
+                const unsigned char* src = (sim || x.src == comm->rank) ? local(x.src).buf[sb] + x.soff
+                                                                         : rbuf(x.src, sb) + x.soff;
+                cudaError_t e = cudaMemcpyAsync(local(x.dst).buf[x.db] + x.doff, src, x.bytes, cudaMemcpyDeviceToDevice, st);
+                if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("shard pull: ") + cudaGetErrorString(e));
+            }
+            return barrier();   // the sources may be overwritten once every pull has finished
+        }
         if (sim) {
             for (const Xfer& x : xs) {
                 RankCtx& s = (*ranks)[x.src];
@@ -330,6 +402,12 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
     // ---- gather: rank r assembles operand r & 1 (a for even ranks, b for odd ones) and converts only that
     // one (the forward conversion is a whole-operand transform done redundantly; splitting it between
     // partner ranks halves it), then partners swap their converted operands
+    if (X.p2p && !X.sim)   // this rank's input shards into its workspace, where the peers pull them from
+        for (int r : mine) {
+            RankCtx& R = X.local(r);
+            CUDA_TRY(cudaMemcpyAsync(R.buf[SB_CA], R.a_shard, S.n / G * 8, cudaMemcpyDeviceToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(R.buf[SB_CB], R.b_shard, S.n / G * 8, cudaMemcpyDeviceToDevice, st));
+        }
     if ((s = X.run(XF.gather)) != GF2X_OK) return s;
     for (int r : mine) {
         uint64_t* A = (uint64_t*)X.local(r).buf[SB_A];
@@ -387,12 +465,31 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
             if ((s = launch_fft(S.fft[i], true, false, W, Nloc, W, S.lp, ds, st, 1, map)) != GF2X_OK) return s;
         // ---- inner iBasisCvt (windows in [0, K)) locally, then pack by destination rank
         if ((s = run_cvt<uint4>(S.inner, W, S.mloc, 1, true, smc, st)) != GF2X_OK) return s;
-        { ProfScope ps("k_pack", 32.0 * Nloc, st); k_pack<<<grid_for(Nloc, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_X], Nloc, g, S.K, 0); }
+        if (!X.p2p) {
+            ProfScope ps("k_pack", 32.0 * Nloc, st);
+            k_pack<<<grid_for(Nloc, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_X], Nloc, g, S.K, 0);
+        }
         if ((s = last("shard pack")) != GF2X_OK) return s;
     }
     if (debug_stage == 1) return GF2X_OK;
-    // ---- all-to-all: rank r's chunk q -> rank q's T at chunk r
-    if ((s = X.run(XF.a2a_fwd)) != GF2X_OK) return s;
+    // ---- all-to-all: rank r's chunk q -> rank q's T at chunk r (peer memory: pulled and packed in one kernel)
+    auto pull = [&](bool unpack) -> gf2x_status {
+        gf2x_status s2 = X.barrier();
+        if (s2 != GF2X_OK) return s2;
+        for (int q : mine) {
+            PullParams pp;
+            for (int r = 0; r < G; r++) pp.src[r] = (const uint4*)X.rbuf(r, unpack ? SB_T : SB_W);
+            pp.dst = (uint4*)X.local(q).buf[unpack ? SB_W : SB_T];
+            pp.chunk = chunk; pp.me = q; pp.G = G; pp.Kg = S.K - g; pp.K = S.K;
+            ProfScope ps(unpack ? "k_pull_unpack" : "k_pull_pack", 32.0 * Nloc, st);
+            if (unpack) k_pull_unpack<<<grid_for(Nloc, 256, smc, 8), 256, 0, st>>>(pp);
+            else k_pull_pack<<<grid_for(Nloc, 256, smc, 8), 256, 0, st>>>(pp);
+            if ((s2 = last("shard pull")) != GF2X_OK) return s2;
+        }
+        return X.barrier();
+    };
+    if (X.p2p) { if ((s = pull(false)) != GF2X_OK) return s; }
+    else if ((s = X.run(XF.a2a_fwd)) != GF2X_OK) return s;
     // ---- t-sliced: top g iFFT layers, outer iBasisCvt
     for (int q : mine) {
         RankCtx& R = X.local(q);
@@ -403,11 +500,15 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
         if ((s = run_cvt<uint4>(S.outer, T, S.mloc, 1, true, smc, st)) != GF2X_OK) return s;
     }
     // ---- all-to-all back: rank q's T chunk r -> rank r's X chunk q, unpack
-    if ((s = X.run(XF.a2a_back)) != GF2X_OK) return s;
+    if (X.p2p) { if ((s = pull(true)) != GF2X_OK) return s; }
+    else if ((s = X.run(XF.a2a_back)) != GF2X_OK) return s;
     for (int r : mine) {
         RankCtx& R = X.local(r);
         uint4* W = (uint4*)R.buf[SB_W];
-        { ProfScope ps("k_pack", 32.0 * Nloc, st); k_pack<<<grid_for(Nloc, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_X], Nloc, g, S.K, 1); }
+        if (!X.p2p) {
+            ProfScope ps("k_pack", 32.0 * Nloc, st);
+            k_pack<<<grid_for(Nloc, 256, smc, 8), 256, 0, st>>>(W, (uint4*)R.buf[SB_X], Nloc, g, S.K, 1);
+        }
         if ((s = last("shard unpack")) != GF2X_OK) return s;
         if ((s = run_cvt<uint4>(S.top_local, W, S.mloc, 1, true, smc, st)) != GF2X_OK) return s;
     }

@@ -206,10 +206,20 @@ def test_stream_ordering_on_side_stream():
 # ------------------------------------------------------------------ multi-GPU decomposition (one device)
 @pytest.mark.parametrize("bits,ranks", [(1 << 22, 2), (1 << 23, 4), (1 << 24, 8), (1 << 24, 2)])
 def test_sharded_simulation_exact(bits, ranks):
-    # the partitioned FFT of SURVEY §8(e) with `ranks` virtual ranks (exchanges = device copies)
+    # the partitioned FFT of SURVEY §8(e) with `ranks` virtual ranks: exchanges as peer-memory pulls (the
+    # fused pull-pack / pull-unpack all-to-all kernels read the other ranks' buffers) and, with
+    # GF2X_SHARD_LISTS=1, as the transfer lists the NCCL fallback sends (device copies)
+    import os
     a, b = operand_pair(bits, seed=bits + ranks)
+    want = O.mul_karatsuba(a, b)
     got = host(G.gf2x_mul_sharded_sim(dev(a), dev(b), bits, ranks))
-    assert np.array_equal(got, O.mul_karatsuba(a, b))
+    assert np.array_equal(got, want)
+    os.environ["GF2X_SHARD_LISTS"] = "1"
+    try:
+        got = host(G.gf2x_mul_sharded_sim(dev(a), dev(b), bits, ranks))
+    finally:
+        del os.environ["GF2X_SHARD_LISTS"]
+    assert np.array_equal(got, want)
 
 
 def test_sharded_simulation_stages_match_oracle():
