@@ -1274,7 +1274,7 @@ int gf2x_shard_plan(uint64_t bits, int nranks, char* buf, size_t cap) {
     if (shard_geom(bits, nranks, S) != GF2X_OK) return -1;
     ShardXfers X;
     shard_xfers(S, X);
-    static const char* bn[SB_ALL] = {"A", "B", "W", "T", "X", "HALO", "IN_A", "IN_B"};
+    static const char* bn[SB_ALL] = {"A", "B", "W", "T", "X", "HALO", "COPY_A", "COPY_B", "IN_A", "IN_B"};
     auto list = [&](const std::vector<Xfer>& xs) {
         std::string o = "[";
         for (size_t i = 0; i < xs.size(); i++) {
@@ -1288,10 +1288,12 @@ int gf2x_shard_plan(uint64_t bits, int nranks, char* buf, size_t cap) {
     char head[512];
     snprintf(head, sizeof(head),
              "{\"G\": %d, \"g\": %d, \"m\": %d, \"mloc\": %d, \"K\": %d, \"n\": %llu, \"N\": %llu, \"Nloc\": %llu, "
-             "\"buffers\": {\"A\": %zu, \"B\": %zu, \"W\": %zu, \"T\": %zu, \"X\": %zu, \"HALO\": %zu}, \"top_cross\": [",
+             "\"buffers\": {\"A\": %zu, \"B\": %zu, \"W\": %zu, \"T\": %zu, \"X\": %zu, \"HALO\": %zu, "
+             "\"COPY_A\": %zu, \"COPY_B\": %zu}, \"top_cross\": [",
              S.G, S.g, S.m, S.mloc, S.K, (unsigned long long)S.n, (unsigned long long)S.N, (unsigned long long)S.Nloc,
              S.off[SB_B] - S.off[SB_A], S.off[SB_W] - S.off[SB_B], S.off[SB_T] - S.off[SB_W], S.off[SB_X] - S.off[SB_T],
-             S.off[SB_HALO] - S.off[SB_X], S.bytes - S.off[SB_HALO]);
+             S.off[SB_HALO] - S.off[SB_X], S.off[SB_CA] - S.off[SB_HALO], S.off[SB_CB] - S.off[SB_CA],
+             S.bytes - S.off[SB_CB]);
     std::string out = head;
     for (size_t i = 0; i < S.top_cross.size(); i++) out += (i ? ", " : "") + std::to_string(S.top_cross[i]);
     out += "], \"gather\": " + list(X.gather) + ", \"xchg\": " + list(X.xchg);

@@ -9,7 +9,8 @@ the layouts they produce against the index maps the kernels use:
              j = (i & (2^(K-g)-1)) | ((i >> K) << (K-g))            (k_pack, shard.cuh)
   t-sliced:  rank q's local index li is global (li & (2^(K-g)-1)) | (q << (K-g)) | ((li >> (K-g)) << K)
              (IdxMap{K-g, g, q}, the multiplier index map of the top iFFT layers)
-and that the cross-rank Taylor-step and halo lists pair up and stay inside the buffers.  Also the
+and that the cross-rank Taylor-step and halo lists pair up and stay inside the buffers; the peer-memory
+all-to-all (k_pull_pack / k_pull_unpack: each rank reads every rank's buffer) is checked on the same labels.  Also the
 128-byte NCCL-id broadcast helper over a gloo process group.
 """
 import json
@@ -101,6 +102,19 @@ def _worker(rank, world, port, bits, errq):
         W = np.full(Nloc, -1, dtype=np.int64)
         W[pack_src.reshape(-1)] = bufs["X"][:Nloc]
         assert np.array_equal(W, rank * Nloc + idx), "blocked layout not restored"
+        # ---- peer-memory path (k_pull_pack / k_pull_unpack): every rank reads the other ranks' buffers
+        # (modelled by an all-gather of the buffers = what IPC mapping exposes), packing while it pulls
+        Wb = torch.from_numpy(rank * Nloc + idx)
+        allw = [torch.empty_like(Wb) for _ in range(world)]
+        dist.all_gather(allw, Wb)
+        Tp = np.concatenate([allw[r].numpy()[pack_src[rank]] for r in range(world)])   # T[r chunk + j]
+        assert np.array_equal(Tp, want_t), "pull-pack: t-sliced layout"
+        allt = [torch.empty_like(Wb) for _ in range(world)]
+        dist.all_gather(allt, torch.from_numpy(Tp))
+        Wp = np.full(Nloc, -1, dtype=np.int64)
+        for q in range(world):
+            Wp[pack_src[q]] = allt[q].numpy()[rank * chunk:(rank + 1) * chunk]
+        assert np.array_equal(Wp, rank * Nloc + idx), "pull-unpack: blocked layout"
         # ---- cross-rank Taylor steps and halo: pairing and bounds
         lists = [("cross", c) for c in plan["cross"]] + [("halo", plan["halo"])]
         for name, lst in lists:
