@@ -98,9 +98,19 @@ __device__ __forceinline__ uint32_t bt_u(int k, int q, uint64_t e0, int L, int m
 }
 
 // multiplier planes of layer k for this thread's pair: c_j = P_k[j] ^ (bit j of U ? ~0 : 0)
+__device__ __forceinline__ uint32_t prmt_sign(uint32_t x, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(x), "r"(sel));
+    return r;
+}
 __device__ __forceinline__ void bt_cplanes(const uint32_t* Pk, uint32_t U, uint32_t* c) {
+    // bit j of U replicated over the word: shift it to bit 7 of its byte, then PRMT's sign-replicate mode
+    // copies that bit into all four result bytes (selector nibble 8 | byte)
+    uint32_t us[8];
 #pragma unroll
-    for (int j = 0; j < 32; j++) c[j] = Pk[j] ^ (uint32_t)((int32_t)(U << (31 - j)) >> 31);
+    for (int k = 0; k < 8; k++) us[k] = U << k;
+#pragma unroll
+    for (int j = 0; j < 32; j++) c[j] = Pk[j] ^ prmt_sign(us[7 - (j & 7)], (8u | (uint32_t)(j >> 3)) * 0x1111u);
 }
 
 // CK: cache of the multiplier planes, [layer][pair][33] (written by warp 0 in the forward layers,
