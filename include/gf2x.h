@@ -96,8 +96,10 @@ gf2x_status gf2x_debug_stage_w128(const uint64_t* a, uint64_t a_bits, const uint
  * gf2x_mul_sharded: a_bits = b_bits = bits, n = ceil(bits/64) must be a power of two and
  *   log2(2n) - log2(G) >= max(16, 12).  Rank r passes words [r n/G, (r+1) n/G) of a and b
  *   (DEVICE, caller-owned) and receives words [r 2n/G, (r+1) 2n/G) of c.  Enqueued on `stream`
- *   (collectives included); returns after enqueue.  EINVAL on unsupported sizes, ENCCL on NCCL
- *   errors.  The communicator owns a workspace, freed by gf2x_comm_destroy.
+ *   (collectives included); returns after enqueue, except that the first call for a size (which
+ *   allocates the communicator's workspace and maps the peers' workspaces, see
+ *   gf2x_comm_peer_memory) synchronises the stream.  EINVAL on unsupported sizes, ENCCL on NCCL
+ *   errors.  The communicator owns a workspace, freed by gf2x_comm_destroy; G <= 8.
  * gf2x_mul_sharded_sim: the same algorithm with `nranks` virtual ranks in one process on the
  *   current device (data movement between ranks = device copies); a, b full operands, c the full
  *   2n-word product (DEVICE).  Used to check the decomposition bit-exactly on one GPU.

@@ -9,7 +9,9 @@
 //                   fused and bit-sliced
 //   k_fft2<inverse> iFFT_LCH layers >= 6
 //   k_cvt_*         iBasisCvt on 128-bit tower elements
-//   k_ipsi_combine  changeRepr back + InterleavedCombine
+//   k_ipsi_bs       changeRepr back + InterleavedCombine, bit-sliced
+//                   (k_ipsi_combine: table-driven fallback)
+// w = 128 (TGF(2^256)): w128.cuh.  Multi-GPU: shard.cuh.
 // Every step runs in these kernels; the host only plans passes and enqueues launches.
 //
 // Diagnostic / A-B knobs (environment, read once per process; defaults are the measured best):
@@ -21,6 +23,11 @@
 //   GF2X_FFT_C=c         column bits of the non-first FFT passes (default 6)
 //   GF2X_BOT_B=L         layers in the bit-sliced bottom kernel (default: 5 or 6 by the planner rule)
 //   GF2X_MAXR=R          maximum FFT layers per table pass below the changeRepr pass (default 7)
+//   GF2X_NO_W2_BS=1      w = 128: table-driven changeRepr_256 / changeRepr_256^-1 instead of bit-sliced
+//   GF2X_SHARD_NCCL=1    sharded multiply: NCCL send/recv instead of peer memory (read when a
+//                        communicator's workspace is allocated)
+//   GF2X_SHARD_LISTS=1   sharded simulation: run the transfer lists as copies (the NCCL path's data
+//                        movement) instead of the peer-memory pulls (read per call)
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
