@@ -51,7 +51,13 @@ struct BottomParams {
                          // the bottom layers and position bits are always below map.pos)
 };
 
-__device__ __forceinline__ uint32_t bt_block(int g, int lb) { return (uint32_t)((lb * BT_GROUPS + g) * BT_STRIDE); }
+// (group g of limb lb) -> plane block.  Blocks of groups 32..63 are stored with their low 5 bits
+// complemented: the pairs (g0, g0 + 2^k) a warp touches in layer k < 5 are 32 groups spread over both
+// halves whose low bits would otherwise coincide pairwise (a 2-way bank conflict on every plane access);
+// complementing maps the upper half onto the other 16 banks for every k at once.
+__device__ __forceinline__ uint32_t bt_block(int g, int lb) {
+    return (uint32_t)((lb * BT_GROUPS + (g ^ ((g & 32) ? 31 : 0))) * BT_STRIDE);
+}
 
 // element (within the tile) of group g at bit position p
 __device__ __forceinline__ uint32_t bt_elem(int g, int p, int L) {
