@@ -73,6 +73,43 @@ __global__ void __launch_bounds__(256) k_shard_top(ShardTopParams p) {
     }
 }
 
+// Same result with the constants folded into the changeRepr tables: T_j[ch][x] = c_j (x) psi(x << 8 ch)
+// (both maps are GF(2)-linear), so a point costs J x 8 table reads instead of J x 8 + (J-1) x 32.
+// Tables in shared memory (J x 32 KB, J <= 4), built per CTA from psi64 and the c_j M4R-4 rows.
+#define SHARD_TOP2_THREADS 512
+__global__ void __launch_bounds__(SHARD_TOP2_THREADS) k_shard_top2(ShardTopParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint4* T = reinterpret_cast<uint4*>(smem_raw);                 // [J][8 x 256]
+    uint32_t* ct = reinterpret_cast<uint32_t*>(T + p.J * 2048);     // [J][128] M4R-4 rows of c_j
+    for (int i = threadIdx.x; i < p.J * 8; i += blockDim.x) build_tab_row(ct + (i >> 3) * 128, p.coef[i >> 3], i & 7, p.tabs->wt);
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) T[i] = p.tabs->psi64[i];   // j = 0: c_0 = 1
+    __syncthreads();
+    const uint32_t ct_sa = (uint32_t)__cvta_generic_to_shared(ct);
+    for (int i = threadIdx.x; i < (p.J - 1) * 2048; i += blockDim.x) {
+        const int j = 1 + i / 2048, e = i % 2048;
+        const uint4 v = T[e];
+        const uint32_t t = ct_sa + j * 512u;
+        T[j * 2048 + e] = make_uint4(m4r4_word_sa(t, v.x), m4r4_word_sa(t, v.y), m4r4_word_sa(t, v.z), m4r4_word_sa(t, v.w));
+    }
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.Nloc; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t ws[SHARD_MAXJ_UNR];
+#pragma unroll
+        for (int j = 0; j < SHARD_MAXJ_UNR; j++) ws[j] = j < p.J ? p.S[j * p.Nloc + i] : 0ull;
+        uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int j = 0; j < SHARD_MAXJ_UNR; j++) {
+            if (j >= p.J) break;
+            const uint64_t w = ws[j];
+            if (!w) continue;
+            const uint4* tj = T + j * 2048;
+#pragma unroll
+            for (int ch = 0; ch < 8; ch++) acc = xor4(acc, tj[ch * 256 + ((w >> (8 * ch)) & 255)]);
+        }
+        p.W[i] = acc;
+    }
+}
+
 // blocked <-> t-sliced packing.  Element i of a blocked block goes to rank q = bits [K-g, K) of i,
 // at position j = (i & (2^(K-g)-1)) | ((i >> K) << (K-g)) of the chunk for q (chunks of Nloc/G).
 __device__ __forceinline__ uint64_t pack_src(uint64_t q, uint64_t j, int Kg, int K) {
@@ -433,12 +470,17 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
                 if ((j >> i) & 1) c = gf2x_host::tower_mul(c, (gf2x_host::u128)host_s_eval(host_tabs, S.mloc + i, ar));
             tp.coef[j] = (uint32_t)c;
         }
-        const size_t sm = (size_t)tp.J * 512 + 8 * 256 * 16;
-        cudaFuncSetAttribute(k_shard_top, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        tp.S = A; tp.W = W;
-        { ProfScope ps("k_shard_top", 8.0 * tp.J * Nloc + 16.0 * Nloc, st); k_shard_top<<<grid_for(Nloc, 256, smc, 4), 256, sm, st>>>(tp); }
-        tp.S = B; tp.W = W + Nloc;
-        { ProfScope ps("k_shard_top", 8.0 * tp.J * Nloc + 16.0 * Nloc, st); k_shard_top<<<grid_for(Nloc, 256, smc, 4), 256, sm, st>>>(tp); }
+        // composed tables (k_shard_top2) while J x 32 KB fits; the M4R-4 version beyond (J > 4 never at G <= 8)
+        const bool top2 = tp.J <= SHARD_MAXJ_UNR && !env_flag("GF2X_SHARD_TOP1");
+        const size_t sm = top2 ? (size_t)tp.J * (2048 * 16 + 512) : (size_t)tp.J * 512 + 8 * 256 * 16;
+        if (top2) cudaFuncSetAttribute(k_shard_top2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        else cudaFuncSetAttribute(k_shard_top, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        for (int o = 0; o < 2; o++) {
+            tp.S = o ? B : A; tp.W = W + o * Nloc;
+            ProfScope ps("k_shard_top", 8.0 * tp.J * Nloc + 16.0 * Nloc, st);
+            if (top2) k_shard_top2<<<grid_for(Nloc, SHARD_TOP2_THREADS, smc, 1), SHARD_TOP2_THREADS, sm, st>>>(tp);
+            else k_shard_top<<<grid_for(Nloc, 256, smc, 4), 256, sm, st>>>(tp);
+        }
         if ((s = last("shard top")) != GF2X_OK) return s;
         // ---- local FFT layers [6, mloc) of both operands, bottom kernel, local iFFT layers
         const IdxMap map{S.mloc, g, (uint32_t)r};
