@@ -20,7 +20,7 @@
 //   GF2X_NO_RES8=1       K=8 Taylor runs as tile passes instead of residue-class passes
 //   GF2X_RB_NOPHASE=1    measurement only: register-blocked passes copy without converting (wrong result)
 //   GF2X_NO_IPSI_BS=1    table-driven changeRepr^-1 + combine instead of the bit-sliced kernel
-//   GF2X_FFT_C=c         column bits of the non-first FFT passes (default 6)
+//   GF2X_FFT_C=c         column bits of the non-first FFT passes shorter than 6 layers (default 6)
 //   GF2X_BOT_B=L         layers in the bit-sliced bottom kernel (default: 5 or 6 by the planner rule)
 //   GF2X_MAXR=R          maximum FFT layers per table pass below the changeRepr pass (default 7)
 //   GF2X_NO_W2_BS=1      w = 128: table-driven changeRepr_256 / changeRepr_256^-1 instead of bit-sliced
@@ -670,10 +670,11 @@ static std::vector<FftPass> plan_fft(int m) {
         const int rem = top - bot;
         const int r = i == 0 ? std::min(6, rem - (np - 1)) : (rem + (np - i) - 1) / (np - i);
         const int lo = top - r;
-        // 64-column tiles for 6-layer passes (double-buffered: one 160 KB CTA per SM; measured as fast as 2
-        // CTAs of 32-column tiles); 32 columns for the changeRepr pass and for 7-layer passes
+        // 32-column tiles (2 CTAs/SM) for the changeRepr pass and passes of >= 6 layers; 64 columns (one
+        // double-buffered CTA per SM) for shorter passes (measured: c4b -1.7 %, c4a / c5 -0.3 % vs 64 columns
+        // for 6-layer passes)
         static const int cdir = getenv("GF2X_FFT_C") ? atoi(getenv("GF2X_FFT_C")) : 6;
-        int c = (i == 0 || r > 6) ? 5 : cdir;
+        int c = (i == 0 || r >= 6) ? 5 : cdir;
         if (c > lo) c = lo;   // column bits must lie below the pass's layers
         v.push_back({c, lo, top, false, 0});
         top = lo;
