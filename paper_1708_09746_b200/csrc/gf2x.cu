@@ -226,15 +226,12 @@ __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restri
         if (t == 0) {
             uint64_t hi = 0;
             if ((w0 & (N - 1)) != 0 || halo) {   // N is a power of two
-                uint64_t lo;
                 const uint4 pv = (w0 & (N - 1)) != 0 ? src[-1] : *halo;
                 uint4 acc = make_uint4(0, 0, 0, 0);
                 const uint32_t w[4] = {pv.x, pv.y, pv.z, pv.w};
                 for (int L = 0; L < 4; L++)
                     for (int b = 0; b < 4; b++) acc = xor4(acc, tabs->ipsi[(L * 4 + b) * 256 + ((w[L] >> (8 * b)) & 255)]);
-                lo = ((uint64_t)acc.y << 32) | acc.x;
-                hi = ((uint64_t)acc.w << 32) | acc.z;
-                (void)lo;
+                hi = ((uint64_t)acc.w << 32) | acc.z;   // (only the high half enters this tile)
             }
             halo_hi = hi;
         }
