@@ -74,6 +74,8 @@ def lib():
             "or_fft_constant": (None, [i32, i32, u64, _u64p]),
             "or_fft_mult_count": (u64, [i32]),
             "or_alg5_mul": (i32, [_u64p, u64, _u64p, u64, _u64p] + [_u64p] * 7),
+            "or_fft_alg4": (None, [_u64p, i32]),
+            "or_alg4_mul": (i32, [_u64p, u64, _u64p, u64, _u64p, _u64p, _u64p]),
             "or_tower256_mul": (None, [_u64p, _u64p, _u64p]),
             "or_gf256p_mul": (None, [_u64p, _u64p, _u64p]),
             "or_psi256_init": (i32, []),
@@ -272,6 +274,38 @@ def alg5_mul(a: np.ndarray, a_bits: int, b: np.ndarray, b_bits: int, stages: boo
                             *[_nullable(x) for x in args])
     if err != 0:
         raise RuntimeError(f"oracle alg5 internal assertion failed: {err}")
+    if stages:
+        return c, {k: v.reshape(-1, 2) for k, v in st.items()}
+    return c
+
+
+# ---------------------------------------------------------------- O3, Alg. 4 (sec 3.1)
+def fft_alg4(g: np.ndarray) -> np.ndarray:
+    """Alg. 4's FFT_LCH over GF(2^128) polynomial basis on N=2^m elements given as (N,2) uint64."""
+    g = np.array(g, dtype=np.uint64, copy=True).reshape(-1, 2)
+    m = len(g).bit_length() - 1
+    assert 1 << m == len(g)
+    flat = np.ascontiguousarray(g.reshape(-1))
+    lib().or_fft_alg4(_p(flat), m)
+    return flat.reshape(-1, 2)
+
+
+def alg4_mul(a: np.ndarray, a_bits: int, b: np.ndarray, b_bits: int, stages: bool = False):
+    """Alg. 4 simple binPolyMul (GF(2^128) polynomial basis, dense multipliers); c or (c, stages)."""
+    a = np.ascontiguousarray(a, dtype=np.uint64)
+    b = np.ascontiguousarray(b, dtype=np.uint64)
+    na, nb = (a_bits + 63) // 64, (b_bits + 63) // 64
+    c = np.zeros(na + nb, dtype=np.uint64)
+    st = {}
+    if stages and a_bits and b_bits:
+        L = na + nb - 1
+        N = 1 << max(0, (L - 1).bit_length())
+        st = {k: np.zeros(2 * N, dtype=np.uint64) for k in ("fft_a", "prod")}
+    err = lib().or_alg4_mul(_p(a if len(a) else np.zeros(1, np.uint64)), a_bits,
+                            _p(b if len(b) else np.zeros(1, np.uint64)), b_bits, _p(c),
+                            _nullable(st.get("fft_a")), _nullable(st.get("prod")))
+    if err != 0:
+        raise RuntimeError(f"oracle alg4 internal assertion failed: {err}")
     if stages:
         return c, {k: v.reshape(-1, 2) for k, v in st.items()}
     return c

@@ -23,6 +23,7 @@
  *         FFT_LCH = Alg. 1, iFFT (R8); pointmul; InterleavedCombine.
  *       w = 128 variant (sec 4.2): TGF(2^256) one tower level up, GF(2^256) modulo
  *       z^256+z^10+z^5+z^2+1 (R20) and changeRepr_256 by the same rule, Alg. 5 on 128-bit blocks.
+ *       Alg. 4 (sec 3.1): FFT_LCH in GF(2^128) polynomial basis, dense multipliers psi^-1(s_k).
  *   O4  product check modulo random irreducible degree-64 polynomials.
  *
  * All arithmetic is exact (GF(2) AND/XOR); no floating point anywhere.
@@ -618,6 +619,87 @@ int or_alg5_mul(const uint64_t *a, uint64_t a_bits, const uint64_t *b, uint64_t 
     }
     /* InterleavedCombine: out[w] = lo64(C_w) ^ hi64(C_(w-1)) */
     for (size_t w = 0; w < na + nb; w++) {
+        uint64_t v = 0;
+        if (w < N) v ^= (uint64_t)A[w];
+        if (w >= 1 && w - 1 < N) v ^= (uint64_t)(A[w - 1] >> 64);
+        c[w] = v;
+    }
+    free_constants(C, m);
+    free(A); free(B);
+    return err;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* O3, Alg. 4 "simple" multiplication (sec 3.1): the working field stays GF(2^128) in    */
+/* polynomial basis; FFT_LCH (Alg. 1) at the points psi^-1(phi_v(i)) with multipliers s_k computed */
+/* in the Cantor (tower) basis "and then switched to its representation in GF(2^128) with a linear */
+/* map": c = psi^-1(s_k(phi_v(b))), random-looking 128-bit elements.  No changeRepr.    */
+/* ------------------------------------------------------------------------------------------ */
+static void fft_poly(u128 *A, int m, u128 **C, int inverse) {
+    for (int kk = 0; kk < m; kk++) {
+        const int k = inverse ? kk : m - 1 - kk;
+        size_t half = (size_t)1 << k, nb = (size_t)1 << (m - k - 1);
+#pragma omp parallel for schedule(static) if (nb * half >= 4096)
+        for (size_t j = 0; j < nb; j++) {
+            size_t b = j << (k + 1);
+            u128 c = psi_inv(C[k][j]);
+            for (size_t i = 0; i < half; i++) {
+                if (!inverse) {
+                    A[b + i] ^= gf128_mul(A[b + half + i], c);
+                    A[b + half + i] ^= A[b + i];
+                } else {
+                    A[b + half + i] ^= A[b + i];
+                    A[b + i] ^= gf128_mul(A[b + half + i], c);
+                }
+            }
+        }
+    }
+}
+void or_fft_alg4(uint64_t *data, int m) {
+    tower_init();
+    psi_init();
+    size_t n = (size_t)1 << m;
+    u128 *A = (u128 *)malloc(n * sizeof(u128));
+    u128 **C = all_constants(m);
+    to128(data, n, 2, A); fft_poly(A, m, C, 0); from128(A, n, 2, data);
+    free_constants(C, m); free(A);
+}
+/* Alg. 4 binPolyMul.  Stage dumps (optional, N x 2 words): after FFT_LCH (a), after pointmul. */
+int or_alg4_mul(const uint64_t *a, uint64_t a_bits, const uint64_t *b, uint64_t b_bits, uint64_t *c,
+                uint64_t *st_fft_a, uint64_t *st_prod) {
+    tower_init();
+    if (psi_init() != 0) return -10;
+    size_t na = (a_bits + 63) / 64, nb = (b_bits + 63) / 64;
+    if (a_bits == 0 || b_bits == 0) { memset(c, 0, (na + nb) * sizeof(uint64_t)); return 0; }
+    size_t L = na + nb - 1;
+    int m = ceil_log2_sz(L);
+    size_t N = (size_t)1 << m;
+    u128 *A = (u128 *)calloc(N, sizeof(u128)), *B = (u128 *)calloc(N, sizeof(u128));
+    for (size_t j = 0; j < na; j++) {   /* Split */
+        uint64_t w = a[j];
+        if (j == na - 1 && (a_bits & 63)) w &= (((uint64_t)1) << (a_bits & 63)) - 1;
+        A[j] = w;
+    }
+    for (size_t j = 0; j < nb; j++) {
+        uint64_t w = b[j];
+        if (j == nb - 1 && (b_bits & 63)) w &= (((uint64_t)1) << (b_bits & 63)) - 1;
+        B[j] = w;
+    }
+    cvt(A, 0, m, 0); cvt(B, 0, m, 0);                       /* BasisCvt */
+    u128 **C = all_constants(m);
+    fft_poly(A, m, C, 0); fft_poly(B, m, C, 0);             /* FFT_LCH at phi_beta points */
+    if (st_fft_a) from128(A, N, 2, st_fft_a);
+#pragma omp parallel for schedule(static) if (N >= 4096)
+    for (size_t i = 0; i < N; i++) A[i] = gf128_mul(A[i], B[i]);   /* pointmul in GF(2^128) */
+    if (st_prod) from128(A, N, 2, st_prod);
+    fft_poly(A, m, C, 1);                                   /* iFFT_LCH */
+    icvt(A, 0, m, 0);                                       /* iBasisCvt */
+    int err = 0;
+    for (size_t i = 0; i < N; i++) {
+        if ((A[i] >> 127) & 1) err = -1;
+        if (i >= L && A[i] != 0) err = -2;
+    }
+    for (size_t w = 0; w < na + nb; w++) {                  /* InterleavedCombine */
         uint64_t v = 0;
         if (w < N) v ^= (uint64_t)A[w];
         if (w >= 1 && w - 1 < N) v ^= (uint64_t)(A[w - 1] >> 64);
