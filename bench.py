@@ -187,6 +187,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--w", type=int, default=64, choices=[64, 128],
                     help="Alg. 5 block width: 64 (TGF(2^128), default) or 128 (TGF(2^256), P:873-874)")
+    ap.add_argument("--alg", type=int, default=5, choices=[5, 4],
+                    help="5: Alg. 5 over the tower (default); 4: Alg. 4 in GF(2^128) polynomial basis (P:562-614)")
     ap.add_argument("--mode", default=None, choices=["sharded", "replicas"],
                     help="N > 1: one multiply partitioned over the ranks (default) or one per rank")
     args = ap.parse_args()
@@ -208,7 +210,7 @@ def main():
     mode = args.mode or ("sharded" if world > 1 else "single")
     if world == 1:
         mode = "single"
-    if mode == "sharded" and (batch != 1 or args.w != 64):
+    if mode == "sharded" and (batch != 1 or args.w != 64 or args.alg != 5):
         mode = "replicas"   # batched configs shard trivially: independent products per rank
     sharded = mode == "sharded"
     seed = DEFAULT_SEED + (0 if sharded else 2 * rank)  # replicas: each rank its own operand pair
@@ -262,6 +264,8 @@ def main():
     def step():
         if sharded:
             comm.mul(sa, sb, bits, sc, stream=stream)
+        elif args.alg == 4:
+            G.gf2x_mul_alg4(da, bits, db, bits, batch, dc, stream=stream)
         elif args.w != 64:
             G.gf2x_mul_w(da, bits, db, bits, args.w, batch, dc, stream=stream)
         elif batch == 1:
@@ -346,6 +350,8 @@ def main():
         stream.wait_event(ev_out[k])           # step i-2's product has left EC[k]
         if sharded:
             comm.mul(EA[k], EB[k], bits, EC[k], stream=stream)
+        elif args.alg == 4:
+            G.gf2x_mul_alg4(EA[k], bits, EB[k], bits, batch, EC[k], stream=stream)
         elif args.w != 64:
             G.gf2x_mul_w(EA[k], bits, EB[k], bits, args.w, batch, EC[k], stream=stream)
         elif batch == 1:
@@ -399,7 +405,7 @@ def main():
     step_bytes = sum(r["bytes"] for r in prof) / args.steps
     kern_ms = sum(r["ms"] for r in prof) / args.steps
     launches = G.gf2x_launch_count_w(bits, bits, batch, args.w)
-    if sharded:   # every kernel of the sharded path is bracketed by the profiling hook
+    if sharded or args.alg == 4:   # every kernel of the sharded path is bracketed by the profiling hook
         launches = sum(r["launches"] for r in prof) // args.steps
 
     line = {
@@ -418,8 +424,9 @@ def main():
         "dtype": "u64",
         "data": "synthetic",
         "config": {
-            "workload": WORKLOAD[args.config] + ("" if args.w == 64 else ", w=128 blocks over TGF(2^256)"),
-            "config": args.config, "operand_bits": bits, "batch": batch, "block_width": args.w,
+            "workload": WORKLOAD[args.config] + ("" if args.w == 64 else ", w=128 blocks over TGF(2^256)")
+                        + ("" if args.alg == 5 else ", Alg. 4 (GF(2^128) polynomial basis, dense multipliers)"),
+            "config": args.config, "operand_bits": bits, "batch": batch, "block_width": args.w, "algorithm": args.alg,
             "fft_points": 1 << max(0, (2 * n - 2).bit_length()) >> (0 if args.w == 64 else 1),
             "parallelism": (f"sharded FFT over {world} GPUs (" + ("peer memory: CUDA IPC over NVLink, fused pull-pack "
                             "all-to-all, NCCL barriers" if comm.peer_memory() == 1 else "NCCL send/recv") + ")" if sharded else

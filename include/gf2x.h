@@ -86,6 +86,17 @@ int gf2x_launch_count_w(uint64_t a_bits, uint64_t b_bits, int64_t batch, int w);
 gf2x_status gf2x_debug_stage_w128(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, int stage,
                                   uint64_t* out, void* stream);
 
+/* Alg. 4 (sec 3.1): the "simple" multiplication that keeps the
+ * working field GF(2^128) in polynomial basis (no changeRepr) and runs FFT_LCH with the dense multipliers
+ * psi^-1(s_k(phi_v(b))).  The same exact product as gf2x_mul_batched (same operands, output, memory and
+ * error contract); it exists as the comparison point for the tower representation and is slower.
+ * gf2x_debug_stage_alg4: operand a's spectrum (N x 2 words, polynomial basis, DEVICE) after stage 2
+ * (FFT_LCH) or 3 (pointmul); EINVAL for other stages. */
+gf2x_status gf2x_mul_alg4(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
+                          int64_t batch, void* stream);
+gf2x_status gf2x_debug_stage_alg4(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, int stage,
+                                  uint64_t* out, void* stream);
+
 /* ---------------------------------------------------------------------------------------------
  * Multi-GPU: the FFT partitioned across G = nranks ranks, one process per GPU (the
  * decomposition is described in DESIGN.md §9).  NCCL is loaded at run time (libnccl.so.2).

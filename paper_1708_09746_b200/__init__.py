@@ -24,7 +24,7 @@ EXPORTS = [
     "gf2x_debug_stage", "gf2x_comm_unique_id", "gf2x_comm_init", "gf2x_comm_destroy", "gf2x_mul_sharded",
     "gf2x_mul_sharded_sim", "gf2x_debug_shard_stage", "gf2x_shard_plan", "gf2x_profile_enable", "gf2x_profile_report", "gf2x_status_string", "gf2x_last_error",
     "gf2x_release", "gf2x_version", "gf2x_mul_w", "gf2x_launch_count_w", "gf2x_debug_stage_w128",
-    "gf2x_comm_peer_memory",
+    "gf2x_comm_peer_memory", "gf2x_mul_alg4", "gf2x_debug_stage_alg4",
 ]
 
 
@@ -56,6 +56,10 @@ def load(path: str = LIB_PATH):
     L.gf2x_launch_count_w.argtypes = [u64, u64, i64, i32]
     L.gf2x_debug_stage_w128.argtypes = [vp, u64, vp, u64, i32, vp, vp]
     L.gf2x_debug_stage_w128.restype = i32
+    L.gf2x_mul_alg4.argtypes = [vp, u64, vp, u64, vp, i64, vp]
+    L.gf2x_mul_alg4.restype = i32
+    L.gf2x_debug_stage_alg4.argtypes = [vp, u64, vp, u64, i32, vp, vp]
+    L.gf2x_debug_stage_alg4.restype = i32
     L.gf2x_status_string.argtypes = [i32]
     L.gf2x_status_string.restype = ctypes.c_char_p
     L.gf2x_last_error.restype = ctypes.c_char_p
@@ -147,6 +151,25 @@ def gf2x_debug_stage_w128(a, a_bits: int, b, b_bits: int, stage: int, stream=Non
     N = 1 << max(0, (L - 1).bit_length())
     out = torch.empty(N, 4, dtype=torch.uint64, device=a.device)
     _check(load().gf2x_debug_stage_w128(_ptr(a), a_bits, _ptr(b), b_bits, stage, _ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def gf2x_mul_alg4(a, a_bits: int, b, b_bits: int, batch: int = 1, c=None, stream=None):
+    """Alg. 4 (GF(2^128) polynomial basis, dense multipliers): the comparison variant; same layout."""
+    import torch
+    n_out = nwords(a_bits) + nwords(b_bits)
+    if c is None:
+        c = torch.empty(batch, n_out, dtype=torch.uint64, device=a.device)
+    _check(load().gf2x_mul_alg4(_ptr(a), a_bits, _ptr(b), b_bits, _ptr(c), batch, _stream_ptr(stream)))
+    return c
+
+
+def gf2x_debug_stage_alg4(a, a_bits: int, b, b_bits: int, stage: int, stream=None):
+    import torch
+    L = nwords(a_bits) + nwords(b_bits) - 1
+    N = 1 << max(0, (L - 1).bit_length())
+    out = torch.empty(N, 2, dtype=torch.uint64, device=a.device)
+    _check(load().gf2x_debug_stage_alg4(_ptr(a), a_bits, _ptr(b), b_bits, stage, _ptr(out), _stream_ptr(stream)))
     return out
 
 

@@ -385,6 +385,7 @@ struct DeviceState {
     DevTables* tabs = nullptr;
     DevTables* host = nullptr;   // host copy (multiplier images for host-side constants)
     struct DevTables256* tabs256 = nullptr;   // w = 128 tables (w128.cuh), built on first use
+    struct DevTablesA4* tabsA4 = nullptr;     // Alg. 4 tables (alg4.cuh), built on first use
     void* shard_ws = nullptr;    // simulation workspace (gf2x_mul_sharded_sim)
     size_t shard_ws_bytes = 0;
     int sm_count = 0;
@@ -975,9 +976,12 @@ static bool overlaps(const void* p, size_t pb, const void* q, size_t qb) {
     return a < b + qb && b < a + pb;
 }
 
+static gf2x_status run_pipeline_a4(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
+                                   const Plan& P, void* ws, DeviceState* ds, cudaStream_t st, int stop_stage);
+// algo: 5 = Alg. 5 (the product path), 4 = Alg. 4 (comparison variant, alg4.cuh)
 static gf2x_status mul_common(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
                               int64_t batch, void* user_ws, size_t user_ws_bytes, void* stream, int stop_stage,
-                              uint64_t* stage_out) {
+                              uint64_t* stage_out, int algo = 5) {
     if (batch < 0) return fail(GF2X_EINVAL, "negative batch");
     if (batch == 0) return GF2X_OK;
     const uint64_t na = (a_bits + 63) / 64, nb = (b_bits + 63) / 64;
@@ -1018,7 +1022,8 @@ static gf2x_status mul_common(const uint64_t* a, uint64_t a_bits, const uint64_t
         }
         ws = ent.first;
     }
-    s = run_pipeline(a, a_bits, b, b_bits, c, P, ws, ds, st, stop_stage);
+    s = algo == 4 ? run_pipeline_a4(a, a_bits, b, b_bits, c, P, ws, ds, st, stop_stage)
+                  : run_pipeline(a, a_bits, b, b_bits, c, P, ws, ds, st, stop_stage);
     if (s != GF2X_OK) return s;
     if (stop_stage && stage_out) {
         CUDA_TRY(cudaMemcpyAsync(stage_out, reinterpret_cast<unsigned char*>(ws) + P.off_wa, P.N * 16,
@@ -1029,6 +1034,7 @@ static gf2x_status mul_common(const uint64_t* a, uint64_t a_bits, const uint64_t
 
 #include "shard.cuh"
 #include "w128.cuh"
+#include "alg4.cuh"
 
 extern "C" {
 
@@ -1088,6 +1094,18 @@ gf2x_status gf2x_debug_stage_w128(const uint64_t* a, uint64_t a_bits, const uint
     if (stage != 1 && stage != 2 && stage != 3 && stage != 5) return fail(GF2X_EINVAL, "stage must be 1, 2, 3 or 5");
     if (!out || a_bits == 0 || b_bits == 0) return fail(GF2X_EINVAL, "null output or empty operand");
     return mul_common_w128(a, a_bits, b, b_bits, nullptr, 1, stream, stage, out);
+}
+
+gf2x_status gf2x_mul_alg4(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
+                          int64_t batch, void* stream) {
+    return mul_common(a, a_bits, b, b_bits, c, batch, nullptr, 0, stream, 0, nullptr, 4);
+}
+
+gf2x_status gf2x_debug_stage_alg4(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, int stage,
+                                  uint64_t* out, void* stream) {
+    if (stage != 2 && stage != 3) return fail(GF2X_EINVAL, "stage must be 2 or 3");
+    if (!out || a_bits == 0 || b_bits == 0) return fail(GF2X_EINVAL, "null output or empty operand");
+    return mul_common(a, a_bits, b, b_bits, nullptr, 1, nullptr, 0, stream, stage, out, 4);
 }
 
 gf2x_status gf2x_comm_unique_id(void* id_out) {
@@ -1383,6 +1401,7 @@ gf2x_status gf2x_release(int device) {
     if (it->second.tabs) cudaFree(it->second.tabs);
     if (it->second.shard_ws) cudaFree(it->second.shard_ws);
     if (it->second.tabs256) cudaFree(it->second.tabs256);
+    if (it->second.tabsA4) cudaFree(it->second.tabsA4);
     delete it->second.host;
     g_dev.erase(it);
     cudaSetDevice(cur);
