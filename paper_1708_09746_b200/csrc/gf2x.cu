@@ -11,7 +11,7 @@
 //   k_cvt_*         iBasisCvt on 128-bit tower elements
 //   k_ipsi_bs       changeRepr back + InterleavedCombine, bit-sliced
 //                   (k_ipsi_combine: table-driven fallback)
-// w = 128 (TGF(2^256)): w128.cuh.  Multi-GPU: shard.cuh.
+// w = 128 (TGF(2^256)): w128.cuh.  Alg. 4: alg4.cuh.  Multi-GPU: shard.cuh.
 // Every step runs in these kernels; the host only plans passes and enqueues launches.
 //
 // Diagnostic / A-B knobs (environment, read once per process; defaults are the measured best):
@@ -1408,6 +1408,6 @@ gf2x_status gf2x_release(int device) {
     return GF2X_OK;
 }
 
-const char* gf2x_version(void) { return "gf2x-b200 0.2 (sm_100a, Alg. 5: w=64 TGF(2^128), w=128 TGF(2^256))"; }
+const char* gf2x_version(void) { return "gf2x-b200 0.3 (sm_100a; Alg. 5 w=64 TGF(2^128) and w=128 TGF(2^256); Alg. 4 GF(2^128))"; }
 
 }  // extern "C"
