@@ -134,6 +134,13 @@ gf2x_status gf2x_mul_sharded_sim(const uint64_t* a, const uint64_t* b, uint64_t 
 gf2x_status gf2x_debug_shard_stage(const uint64_t* a, const uint64_t* b, uint64_t bits, int nranks, int stage,
                                    uint64_t* out, void* stream);
 
+/* Host-only description of the single-GPU plan (no device work): JSON into buf (cap bytes, NUL-terminated)
+ * with m, N, the operand conversion sizes ma/mb, workspace bytes, the table FFT passes [c, k_lo, k_hi]
+ * (forward order), the bit-sliced bottom layers, and the BasisCvt / iBasisCvt passes (kind res / rb / tile /
+ * stream, each with its Taylor steps [level, K] in forward execution order).  Returns the length needed, or
+ * -1 for empty operands / unsupported sizes. */
+int gf2x_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, char* buf, size_t cap);
+
 /* Host-only description of the sharded multiply's exchanges (no device work): writes JSON into buf
  * (cap bytes, NUL-terminated) with the geometry (G, g, m, mloc, K, n, N, Nloc, per-rank buffer
  * sizes) and every transfer list [src_rank, dst_rank, src_buf, dst_buf, src_off, dst_off, bytes]

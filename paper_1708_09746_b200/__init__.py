@@ -24,7 +24,7 @@ EXPORTS = [
     "gf2x_debug_stage", "gf2x_comm_unique_id", "gf2x_comm_init", "gf2x_comm_destroy", "gf2x_mul_sharded",
     "gf2x_mul_sharded_sim", "gf2x_debug_shard_stage", "gf2x_shard_plan", "gf2x_profile_enable", "gf2x_profile_report", "gf2x_status_string", "gf2x_last_error",
     "gf2x_release", "gf2x_version", "gf2x_mul_w", "gf2x_launch_count_w", "gf2x_debug_stage_w128",
-    "gf2x_comm_peer_memory", "gf2x_mul_alg4", "gf2x_debug_stage_alg4",
+    "gf2x_comm_peer_memory", "gf2x_mul_alg4", "gf2x_debug_stage_alg4", "gf2x_plan",
 ]
 
 
@@ -75,6 +75,8 @@ def load(path: str = LIB_PATH):
     for name in ("gf2x_comm_unique_id", "gf2x_comm_init", "gf2x_comm_destroy", "gf2x_mul_sharded", "gf2x_mul_sharded_sim",
                  "gf2x_debug_shard_stage"):
         getattr(L, name).restype = i32
+    L.gf2x_plan.argtypes = [u64, u64, i64, ctypes.c_char_p, sz]
+    L.gf2x_plan.restype = i32
     L.gf2x_shard_plan.argtypes = [u64, i32, ctypes.c_char_p, sz]
     L.gf2x_shard_plan.restype = i32
     L.gf2x_profile_enable.argtypes = [i32]
@@ -280,6 +282,18 @@ def shard_words(total_words: int, nranks: int, rank: int):
     assert total_words % nranks == 0
     per = total_words // nranks
     return rank * per, (rank + 1) * per
+
+
+def gf2x_plan(a_bits: int, b_bits: int, batch: int = 1) -> dict:
+    """Host-only: the single-GPU plan (FFT passes, bottom layers, conversion passes; see include/gf2x.h)."""
+    import json
+    L = load()
+    need = L.gf2x_plan(a_bits, b_bits, batch, None, 0)
+    if need < 0:
+        raise Gf2xError(f"GF2X_EINVAL: no plan for ({a_bits}, {b_bits}, {batch})")
+    buf = ctypes.create_string_buffer(need + 16)
+    L.gf2x_plan(a_bits, b_bits, batch, buf, len(buf))
+    return json.loads(buf.value.decode())
 
 
 def gf2x_shard_plan(bits: int, nranks: int) -> dict:

@@ -1292,6 +1292,39 @@ gf2x_status gf2x_debug_shard_stage(const uint64_t* a, const uint64_t* b, uint64_
     return sharded_sim(a, b, bits, nullptr, nranks, stream, stage, out);
 }
 
+int gf2x_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, char* buf, size_t cap) {
+    if (a_bits == 0 || b_bits == 0 || batch < 1) return -1;
+    Plan P;
+    if (make_plan(a_bits, b_bits, batch, P) != GF2X_OK) return -1;
+    auto cvt = [](const std::vector<CvtPass>& v) {
+        std::string o = "[";
+        for (size_t i = 0; i < v.size(); i++) {
+            const CvtPass& p = v[i];
+            const char* kind = p.stream ? "stream" : (p.res ? "res" : (p.rb ? "rb" : "tile"));
+            o += (i ? ", " : "");
+            o += "{\"kind\": \"" + std::string(kind) + "\", \"ops\": [";
+            for (size_t j = 0; j < p.ops.size(); j++)
+                o += (j ? ", " : "") + std::string("[") + std::to_string(p.ops[j].lg) + ", " + std::to_string(p.ops[j].K) + "]";
+            o += "]}";
+        }
+        return o + "]";
+    };
+    std::string out = "{\"m\": " + std::to_string(P.m) + ", \"N\": " + std::to_string(P.N) + ", \"ma\": " +
+                      std::to_string(P.ma) + ", \"mb\": " + std::to_string(P.mb) + ", \"workspace\": " +
+                      std::to_string(P.bytes) + ", \"fft\": [";
+    for (size_t i = 0; i + 1 < P.fft.size(); i++)
+        out += (i ? ", " : "") + std::string("[") + std::to_string(P.fft[i].c) + ", " + std::to_string(P.fft[i].k_lo) + ", " +
+               std::to_string(P.fft[i].k_hi) + "]";
+    out += "], \"bottom\": " + std::to_string(P.fft.back().layers) + ", \"cvt_a\": " + cvt(P.cvt_a) +
+           ", \"cvt_b\": " + cvt(P.cvt_b) + ", \"icvt\": " + cvt(P.icvt) + "}";
+    if (buf && cap) {
+        const size_t n = std::min(cap - 1, out.size());
+        memcpy(buf, out.data(), n);
+        buf[n] = 0;
+    }
+    return (int)out.size();
+}
+
 int gf2x_shard_plan(uint64_t bits, int nranks, char* buf, size_t cap) {
     ShardGeom S;
     if (shard_geom(bits, nranks, S) != GF2X_OK) return -1;
