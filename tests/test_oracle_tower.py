@@ -1,6 +1,8 @@
 """Pins for oracle O3 field arithmetic: the tower TGF(2^(2^l)) (§3.2), the
 vanishing polynomials s_k (Def. 2, Table 1, Prop. 1, Prop. 3
 P:796-799, Fig. 2 narrative P:833-845), and changeRepr (§4.3)."""
+import json
+import os
 import random
 
 import pytest
@@ -9,6 +11,12 @@ import oracle as O
 from oracle.brute import clmul_int
 
 R = random.Random(7)
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def golden(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
 
 
 def rnd(bits):
@@ -17,11 +25,10 @@ def rnd(bits):
 
 # ---------------------------------------------------------------- tower arithmetic
 def test_spec_small_field_examples():
-    # GF(4) 0x2*0x2 = 0x3, 0x2*0x3 = 0x1 ; GF(16) 0x2*0x8 = 0xc
-    assert O.tower_mul(2, 2, 1) == 3
-    assert O.tower_mul(2, 3, 1) == 1
-    assert O.tower_mul(2, 8, 2) == 0xC
-    assert O.tower_mul(2, 8, 2, bits_only=True) == 0xC
+    # S:175-177 (tests/golden/spec_examples.json): GF(4) 0x2*0x2 = 0x3, 0x2*0x3 = 0x1 ; GF(16) 0x2*0x8 = 0xc
+    for e in golden("spec_examples.json")["tower"]:
+        assert O.tower_mul(e["a"], e["b"], e["level"]) == e["r"]
+        assert O.tower_mul(e["a"], e["b"], e["level"], bits_only=True) == e["r"]
 
 
 @pytest.mark.parametrize("k", range(1, 8))
@@ -102,13 +109,11 @@ def s_symbolic(i):
 
 
 def test_table1():
-    # Table 1, exponent sets typed from the paper
-    table1 = {
-        0: [1], 1: [2, 1], 2: [4, 1], 3: [8, 4, 2, 1], 4: [16, 1], 5: [32, 16, 2, 1],
-        6: [64, 16, 4, 1], 7: [128, 64, 32, 16, 8, 4, 2, 1],
-    }
+    # Table 1, exponent sets typed from the paper (tests/golden/table1_s_i.json)
+    table1 = golden("table1_s_i.json")["s_i_exponents"]
+    assert len(table1) == 8
     for i, exps in table1.items():
-        assert s_symbolic(i) == sum(1 << e for e in exps)
+        assert s_symbolic(int(i)) == sum(1 << e for e in exps)
     # "minimal two terms iff i is a power of 2"
     for i in range(1, 200):
         assert (len(s_exponents(i)) == 2) == (i & (i - 1) == 0)
@@ -164,12 +169,11 @@ def test_multiplier_shortening():
 def test_fig2_multipliers():
     # Fig. 2 narrative: 16 points, degree-7 input.  Layer s_2 at alpha in {0, 0x8}:
     # {0, 0x2}; layer s_1 at {0, 0x4, 0x8, 0xc}: {0, 0x2, 0x5, 0x7}; layer s_0: {0, 0x2, ..., 0xe}.
-    m = 4
-    assert [O.fft_constant(m, 2, j) for j in range(2)] == [0, 0x2]
-    assert [O.fft_constant(m, 1, j) for j in range(4)] == [0, 0x2, 0x5, 0x7]
-    assert [O.fft_constant(m, 0, j) for j in range(8)] == list(range(0, 16, 2))
-    assert O.s_eval(1, 0x8) == 0x5
-    assert O.fft_constant(m, 3, 0) == 0               # top layer: alpha = 0 -> fan-out
+    g = golden("fig2_multipliers.json")
+    m = g["m"]
+    for k, want in g["layer_multipliers"].items():   # top layer [0]: alpha = 0 -> fan-out
+        assert [O.fft_constant(m, int(k), j) for j in range(len(want))] == want, k
+    assert O.s_eval(1, 0x8) == g["s1_of_0x8"]
 
 
 def test_multiply_count_bound():

@@ -43,13 +43,18 @@ def test_basis_cvt_is_the_definition(m):
 
 
 def test_spec_and_appendix_b_examples():
-    # x^2 -> X_2 + X_1
-    assert list(O.basis_cvt(np.array([0, 0, 1, 0], dtype=np.uint64))) == [0, 1, 1, 0]
-    # App. B: n = 16 -> 4 layers with equal XOR counts: divide by x^8+x^2 (d=6),
-    # then x^4+x on both halves (d=3), then y^2+y "4 positions apart", then x^2+x on 4 chunks.
-    tr = O.cvt_trace(4)
-    assert tr == [(16, 2, 6, 8), (8, 2, 3, 4), (8, 2, 3, 4), (16, 1, 4, 8),
-                  (4, 1, 1, 2), (4, 1, 1, 2), (4, 1, 1, 2), (4, 1, 1, 2)]
+    import json
+    import os
+    gdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    # S:349 (tests/golden/spec_examples.json): x^2 -> X_2 + X_1
+    ex = json.load(open(os.path.join(gdir, "spec_examples.json")))["basis_cvt"]
+    assert list(O.basis_cvt(np.array(ex["in"], dtype=np.uint64))) == ex["out"]
+    # App. B (tests/golden/appendix_b_schedule.json): n = 16 -> 4 layers with equal XOR counts:
+    # divide by x^8+x^2 (d=6), then x^4+x on both halves (d=3), then y^2+y "4 positions apart", then x^2+x
+    # on 4 chunks.
+    g = json.load(open(os.path.join(gdir, "appendix_b_schedule.json")))
+    tr = O.cvt_trace(g["m"])
+    assert tr == [tuple(x) for x in g["steps"]]
     layers = [8, 4 + 4, 8, 2 * 4]
     assert len(set(layers)) == 1
 
