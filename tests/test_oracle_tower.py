@@ -31,6 +31,18 @@ def test_spec_small_field_examples():
         assert O.tower_mul(e["a"], e["b"], e["level"], bits_only=True) == e["r"]
 
 
+def test_notation_example():
+    # P:668-686 (tests/golden/tower_notation.json): x_2 x_1 + x_2 + x_1 + 1 = 0xf, v_3 = x_2 x_1 = 0x8,
+    # and the 16 elements 0x00..0x0f of GF(256) are closed under the product (the subfield GF(16))
+    g = golden("tower_notation.json")
+    x1, x2 = g["generators"]["x1"], g["generators"]["x2"]
+    x2x1 = O.tower_mul(x2, x1, 2)
+    assert x2x1 == g["v"][3]
+    assert x2x1 ^ x2 ^ x1 ^ 1 == g["x2x1_plus_x2_plus_x1_plus_1"]
+    n = g["subfield_of_gf256"]
+    assert all(O.tower_mul(a, b, 3) < n for a in range(n) for b in range(n))
+
+
 @pytest.mark.parametrize("k", range(1, 8))
 def test_defining_relations(k):
     # x_k^2 + x_k = x_1 ... x_(k-1)  (= 1 for k = 1).  x_k = v_(2^(k-1)) = 1 << 2^(k-1);
