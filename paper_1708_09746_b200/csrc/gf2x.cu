@@ -21,13 +21,15 @@
 //   GF2X_RB_NOPHASE=1    measurement only: register-blocked passes copy without converting (wrong result)
 //   GF2X_NO_IPSI_BS=1    table-driven changeRepr^-1 + combine instead of the bit-sliced kernel
 //   GF2X_FFT_C=c         column bits of the non-first FFT passes shorter than 6 layers (default 6)
-//   GF2X_BOT_B=L         layers in the bit-sliced bottom kernel (default: 5 or 6 by the planner rule)
+//   GF2X_BOT_B=L         layers in the bit-sliced bottom kernel (default 6; 5 for m <= 10)
 //   GF2X_MAXR=R          maximum FFT layers per table pass below the changeRepr pass (default 7)
 //   GF2X_NO_W2_BS=1      w = 128: table-driven changeRepr_256 / changeRepr_256^-1 instead of bit-sliced
 //   GF2X_SHARD_NCCL=1    sharded multiply: NCCL send/recv instead of peer memory (read when a
 //                        communicator's workspace is allocated)
 //   GF2X_SHARD_LISTS=1   sharded simulation: run the transfer lists as copies (the NCCL path's data
 //                        movement) instead of the peer-memory pulls (read per call)
+//   GF2X_SHARD_TOP1=1    sharded forward: M4R-4 constant products after changeRepr instead of the composed
+//                        changeRepr tables (k_shard_top instead of k_shard_top2)
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
