@@ -136,7 +136,8 @@ gf2x_status gf2x_debug_shard_stage(const uint64_t* a, const uint64_t* b, uint64_
 
 /* Host-only description of the single-GPU plan (no device work): JSON into buf (cap bytes, NUL-terminated)
  * with m, N, the operand conversion sizes ma/mb, workspace bytes, the table FFT passes [c, k_lo, k_hi]
- * (forward order), the bit-sliced bottom layers, and the BasisCvt / iBasisCvt passes (kind res / rb / tile /
+ * (forward order), the bit-sliced bottom layers, trunc_j (the truncated-FFT upper part is 2^trunc_j points, -1
+ * if the product runs the full transform), and the BasisCvt / iBasisCvt passes (kind res / rb / tile /
  * stream, each with its Taylor steps [level, K] in forward execution order).  Returns the length needed, or
  * -1 for empty operands / unsupported sizes. */
 int gf2x_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, char* buf, size_t cap);

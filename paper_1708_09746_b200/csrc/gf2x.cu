@@ -980,6 +980,8 @@ static bool overlaps(const void* p, size_t pb, const void* q, size_t qb) {
 
 static gf2x_status run_pipeline_a4(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
                                    const Plan& P, void* ws, DeviceState* ds, cudaStream_t st, int stop_stage);
+static int run_trunc_if_eligible(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
+                                 const Plan& P, void* ws, DeviceState* ds, cudaStream_t st, gf2x_status* out);
 // algo: 5 = Alg. 5 (the product path), 4 = Alg. 4 (comparison variant, alg4.cuh)
 static gf2x_status mul_common(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
                               int64_t batch, void* user_ws, size_t user_ws_bytes, void* stream, int stop_stage,
@@ -1024,6 +1026,8 @@ static gf2x_status mul_common(const uint64_t* a, uint64_t a_bits, const uint64_t
         }
         ws = ent.first;
     }
+    // products just above a power of two take the truncated FFT (trunc.cuh) unless a stage is requested
+    if (algo == 5 && !stop_stage && run_trunc_if_eligible(a, a_bits, b, b_bits, c, P, ws, ds, st, &s)) return s;
     s = algo == 4 ? run_pipeline_a4(a, a_bits, b, b_bits, c, P, ws, ds, st, stop_stage)
                   : run_pipeline(a, a_bits, b, b_bits, c, P, ws, ds, st, stop_stage);
     if (s != GF2X_OK) return s;
@@ -1037,6 +1041,7 @@ static gf2x_status mul_common(const uint64_t* a, uint64_t a_bits, const uint64_t
 #include "shard.cuh"
 #include "w128.cuh"
 #include "alg4.cuh"
+#include "trunc.cuh"
 
 extern "C" {
 
@@ -1317,7 +1322,10 @@ int gf2x_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, char* buf, size_t
     for (size_t i = 0; i + 1 < P.fft.size(); i++)
         out += (i ? ", " : "") + std::string("[") + std::to_string(P.fft[i].c) + ", " + std::to_string(P.fft[i].k_lo) + ", " +
                std::to_string(P.fft[i].k_hi) + "]";
-    out += "], \"bottom\": " + std::to_string(P.fft.back().layers) + ", \"cvt_a\": " + cvt(P.cvt_a) +
+    TruncGeom TG;
+    const int tj = trunc_geom(P, TG) ? TG.j : -1;
+    out += "], \"bottom\": " + std::to_string(P.fft.back().layers) + ", \"trunc_j\": " + std::to_string(tj) +
+           ", \"cvt_a\": " + cvt(P.cvt_a) +
            ", \"cvt_b\": " + cvt(P.cvt_b) + ", \"icvt\": " + cvt(P.icvt) + "}";
     if (buf && cap) {
         const size_t n = std::min(cap - 1, out.size());

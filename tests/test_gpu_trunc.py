@@ -1,0 +1,66 @@
+"""GPU parity of the truncated FFT (trunc.cuh; R21): products whose L = n_a + n_b - 1
+blocks lie just above a power of two run an H-point multiply plus a 2^j-point one instead of an N-point one.
+The result is the exact product (oracle: Karatsuba / Alg. 5 / brute force / sampled words + mod p)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle as O  # noqa: E402
+import paper_1708_09746_b200 as G  # noqa: E402
+from gf2x_synth import operand  # noqa: E402
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x).view(np.int64).copy()).cuda().view(torch.uint64)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().view(torch.int64).numpy().view(np.uint64)
+
+
+def gpu_mul(a, ab, b, bb, profile=False):
+    if profile:
+        G.profile_enable(True)
+    c = host(G.gf2x_mul(dev(a), ab, dev(b), bb))
+    names = set()
+    if profile:
+        names = {r["kernel"] for r in G.profile_report()}
+        G.profile_enable(False)
+    return c, names
+
+
+@pytest.mark.parametrize("ab,bb", [((1 << 20) + 64, (1 << 20) + 64), ((1 << 20) + 1, (1 << 20) + 65), (1 << 20, (1 << 20) + 3000),
+                                   ((1 << 20) + 64 * 4095, (1 << 20) + 7), ((1 << 19) + 999, (1 << 21) - 64 * 100),
+                                   ((1 << 22) + 1, (1 << 22) + 1)])
+def test_truncated_products_exact(ab, bb):
+    a, b = operand(ab, seed=ab % 1000 + 1), operand(bb, seed=bb % 1000 + 2)
+    got, names = gpu_mul(a, ab, b, bb, profile=True)
+    assert "k_trunc_fold" in names   # the truncated path ran
+    assert np.array_equal(got, O.alg5_mul(a, ab, b, bb))
+
+
+def test_not_truncated_when_not_eligible():
+    ab = 1 << 20   # L = 2^15 - 1: exactly a power-of-two transform, nothing to truncate
+    a, b = operand(ab, seed=1), operand(ab, seed=2)
+    got, names = gpu_mul(a, ab, b, ab, profile=True)
+    assert "k_trunc_fold" not in names
+    assert np.array_equal(got, O.mul_karatsuba(a, b))
+
+
+def test_truncated_large_sampled_words_and_mod_p():
+    ab = (1 << 28) + 64
+    a, b = operand(ab, seed=5), operand(ab, seed=6)
+    got, names = gpu_mul(a, ab, b, ab, profile=True)
+    assert "k_trunc_fold" in names
+    n_out = len(got)
+    rng = np.random.default_rng(9)
+    for w in sorted({0, n_out // 2 - 1, n_out // 2, n_out - 3, n_out - 2, n_out - 1} |
+                    set(int(x) for x in rng.integers(0, n_out, size=12))):
+        assert int(got[w]) == O.mul_word(a, b, w), w
+    assert O.check_mod_p(a, b, got, O.random_irreducibles(3, seed=31))

@@ -77,6 +77,17 @@ def test_plan_covers_the_method(ab, bb):
     assert top == p["bottom"] == min(m, 6 if m > 10 else 5)
 
 
+def test_truncation_eligibility():
+    # L just above a power of two, both operands in the lower half: truncated with the smallest 2^j >= L - H
+    p = G.gf2x_plan((1 << 28) + 64, (1 << 28) + 64)
+    assert p["m"] == 24 and p["trunc_j"] == 12
+    p = G.gf2x_plan((1 << 28) + (1 << 23), (1 << 28) + (1 << 23))
+    assert p["trunc_j"] == 18   # L - H = 2^18 - 1
+    assert G.gf2x_plan(1 << 29, 1 << 29)["trunc_j"] == -1          # exact power of two
+    assert G.gf2x_plan((1 << 28) + 64, 1 << 10)["trunc_j"] == -1   # L <= H
+    assert G.gf2x_plan((1 << 29) + 64, 64)["trunc_j"] == -1        # an operand beyond the lower half
+
+
 def test_plan_rejects_empty():
     with pytest.raises(G.Gf2xError):
         G.gf2x_plan(0, 64)
