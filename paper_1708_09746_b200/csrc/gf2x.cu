@@ -203,16 +203,17 @@ __global__ void __launch_bounds__(256) k_ipsi_combine(const uint4* __restrict__ 
 __device__ __forceinline__ uint32_t ib_swz(uint32_t e) { return e ^ ((e >> 5) & 31); }
 
 // halo (sharded multiply, batch 1): the tower element preceding P[0] globally (rank r-1's last one), or null
+// n_write: flat output words written (N batch when n_out = N; n_out <= N for a single product)
 __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restrict__ P, const DevTables* tabs, uint64_t N,
                                                          uint64_t batch, uint64_t* __restrict__ out,
-                                                         const uint4* __restrict__ halo) {
+                                                         const uint4* __restrict__ halo, uint64_t n_write) {
     extern __shared__ __align__(1024) uint32_t ib_smem[];
     uint32_t* S = ib_smem;                    // [4][IB_TILE] limb planes (swizzled)
     uint32_t* H = ib_smem + 4 * IB_TILE;      // [2][IB_TILE] hi64 halves of every element (swizzled)
     __shared__ uint64_t halo_hi;
     // the batch is one flat run of products (n_out = N): a tile covers IB_TILE consecutive elements, which
     // may span several small products; an element at a product boundary has no predecessor
-    const uint64_t ntiles = N * batch / IB_TILE;
+    const uint64_t ntiles = (n_write + IB_TILE - 1) / IB_TILE;
     const uint64_t pair = 0;
     const uint32_t t = threadIdx.x;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restri
         uint64_t* dst = out + pair * N + w0;   // (pair = 0: flat)
         for (uint32_t e = t; e < IB_TILE; e += IB_THREADS) {
             const uint32_t q = ib_swz(e);
-            dst[e] = ((uint64_t)S[IB_TILE + q] << 32) | S[q];
+            if (w0 + e < n_write) dst[e] = ((uint64_t)S[IB_TILE + q] << 32) | S[q];
         }
         __syncthreads();
     }
@@ -958,10 +959,14 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
     {
         const uint64_t n_out = P.na + P.nb;
         const uint64_t total = n_out * P.batch;
-        if (n_out == P.N && (P.N * P.batch) % IB_TILE == 0 && !env_flag("GF2X_NO_IPSI_BS")) {
-            ProfScope ps("k_ipsi_bs", 16.0 * P.N * P.batch + 8.0 * total, st);
-            k_ipsi_bs<<<grid_for(P.N * P.batch / IB_TILE, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(Wa, ds->tabs, P.N,
-                                                                                                           P.batch, c, nullptr);
+        // bit-sliced when the output is whole tiles of the flat spectrum: n_out = N (any batch), or one
+        // product with n_out <= N (the trailing words of the last tile are not written)
+        const bool bs = (P.N * P.batch) % IB_TILE == 0 && (n_out == P.N || (P.batch == 1 && n_out < P.N));
+        if (bs && !env_flag("GF2X_NO_IPSI_BS")) {
+            const uint64_t n_write = n_out == P.N ? P.N * P.batch : n_out;
+            ProfScope ps("k_ipsi_bs", 16.0 * n_write + 8.0 * total, st);
+            k_ipsi_bs<<<grid_for((n_write + IB_TILE - 1) / IB_TILE, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(
+                Wa, ds->tabs, P.N, P.batch, c, nullptr, n_write);
         } else {
             ProfScope ps("k_ipsi_combine", 16.0 * P.N * P.batch + 8.0 * total, st);
             k_ipsi_combine<<<grid_for(total, 256, smc, 2), 256, 16 * 256 * 16, st>>>(Wa, ds->tabs, P.N, n_out, P.batch, c, nullptr);
