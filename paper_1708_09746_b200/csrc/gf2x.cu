@@ -684,12 +684,39 @@ static std::vector<FftPass> plan_fft(int m) {
     return v;
 }
 
+// A conversion of n units in a 2^(p+1) array, n <= 2^p + 2^j, done as a 2^p conversion of the lower
+// half plus a 2^j conversion of the tail and the s_p(x) = sum_{q subset p} x^(2^q) shifts (R22)
+struct CvtSplit {
+    int p = -1, j = 0;
+    std::vector<CvtPass> lo, hi;
+};
+static CvtSplit plan_cvt_split(uint64_t n, int mfull, int unit_bytes) {
+    CvtSplit S;
+    if (env_flag("GF2X_NO_CVT_SPLIT") || mfull < 16) return S;
+    const int p = mfull - 1;
+    if (n <= (1ull << p)) return S;
+    const int j = ceil_log2_u64(n - (1ull << p));
+    if (j > p - 2) return S;   // a tail above a quarter saves too little
+    S.p = p; S.j = j;
+    S.lo = plan_cvt(p, unit_bytes);
+    S.hi = plan_cvt(j, unit_bytes);
+    return S;
+}
+static int lucas_shifts(int p, uint64_t* off) {   // 2^q for q subset of p, q != p (the lower terms of s_p)
+    int n = 0;
+    for (int q = 0; q < p; q++)
+        if ((q & p) == q) off[n++] = 1ull << q;
+    return n;
+}
+
 struct Plan {
     uint64_t na, nb, N, batch;
     int m, ma, mb;
     std::vector<CvtPass> cvt_a, cvt_b, icvt;
     std::vector<FftPass> fft;
     size_t off_sa, off_sb, off_wa, off_wb, bytes;
+    // one product: BasisCvt split at 2^p + tail 2^j (R22); p < 0 = not split
+    CvtSplit sa, sb, ic;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -732,6 +759,11 @@ static gf2x_status make_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, Pl
     P.cvt_b = plan_cvt(P.mb, 8);
     P.icvt = plan_cvt(P.m, 16);
     P.fft = plan_fft(P.m);
+    if (P.batch == 1) {
+        P.sa = plan_cvt_split(P.na, P.ma, 8);
+        P.sb = plan_cvt_split(P.nb, P.mb, 8);
+        P.ic = plan_cvt_split(L, P.m, 16);
+    }
     // workspace: Sa | Sb (u64 blocks) and Wa | Wb (spectra) each contiguous, so that passes with
     // equal shapes for a and b run as one launch over 2*batch products; a 2^11-element pad after Wb
     // keeps the bottom kernel's last tile in bounds
@@ -744,10 +776,13 @@ static gf2x_status make_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, Pl
     return GF2X_OK;
 }
 
+static int launches_of_split(const CvtSplit& S, const std::vector<CvtPass>& full) {
+    return S.p < 0 ? (int)full.size() : 1 + (int)S.lo.size() + (int)S.hi.size();
+}
 static int launches_of(const Plan& P) {
-    const bool same = P.ma == P.mb && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8;
+    const bool same = P.ma == P.mb && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8 && P.sa.p < 0 && P.sb.p < 0;
     int n = 2;  // prep a, b
-    n += (int)P.cvt_a.size() + (same ? 0 : (int)P.cvt_b.size()) + (int)P.icvt.size();
+    n += launches_of_split(P.sa, P.cvt_a) + (same ? 0 : launches_of_split(P.sb, P.cvt_b)) + launches_of_split(P.ic, P.icvt);
     const int nd = (int)P.fft.size() - 1;
     n += (same ? 1 : 2) * (nd ? nd : 1);      // forward a, b (or the changeRepr-only pass)
     n += 1;                      // fused bottom
@@ -847,6 +882,54 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
     return GF2X_OK;
 }
 
+// R22 shifts: data[off_k + i] ^= data[src + i], i < n, for each offset (targets lie below src, so the
+// source is read unchanged; targets of different offsets may coincide, hence the atomics)
+struct ShiftList {
+    uint64_t off[32];
+    int n;
+};
+__device__ __forceinline__ void atomic_xor_unit(uint64_t* p, uint64_t v) { atomicXor((unsigned long long*)p, (unsigned long long)v); }
+__device__ __forceinline__ void atomic_xor_unit(uint4* p, uint4 v) {
+    unsigned long long* q = reinterpret_cast<unsigned long long*>(p);
+    const unsigned long long lo = ((unsigned long long)v.y << 32) | v.x, hi = ((unsigned long long)v.w << 32) | v.z;
+    if (lo) atomicXor(q, lo);
+    if (hi) atomicXor(q + 1, hi);
+}
+__device__ __forceinline__ bool unit_nonzero(uint64_t v) { return v != 0; }
+__device__ __forceinline__ bool unit_nonzero(uint4 v) { return (v.x | v.y | v.z | v.w) != 0; }
+template <typename T>
+__global__ void __launch_bounds__(256) k_shift_xor(T* __restrict__ data, uint64_t src, uint64_t n, ShiftList sl) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const T v = data[src + i];
+        if (!unit_nonzero(v)) continue;
+        for (int k = 0; k < sl.n; k++) atomic_xor_unit(data + sl.off[k] + i, v);
+    }
+}
+template <typename T>
+static gf2x_status launch_shift_xor(T* data, int p, uint64_t n, int smc, cudaStream_t st) {
+    ShiftList sl;
+    sl.n = lucas_shifts(p, sl.off);
+    ProfScope ps("k_shift_xor", (double)n * sizeof(T) * (1 + 2 * sl.n), st);
+    k_shift_xor<T><<<grid_for(n, 256, smc, 8), 256, 0, st>>>(data, 1ull << p, n, sl);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GF2X_OK : fail(GF2X_ECUDA, std::string("shift launch: ") + cudaGetErrorString(e));
+}
+// forward BasisCvt of one operand (n units, zero beyond) per R22: f_lo += sum_{q subset p, q != p} x^(2^q) f_hi,
+// then BasisCvt_p(f_lo) and BasisCvt_j(f_hi) in place
+static gf2x_status run_cvt_fwd_split(const CvtSplit& S, uint64_t* data, uint64_t n, int smc, cudaStream_t st) {
+    gf2x_status s;
+    if ((s = launch_shift_xor<uint64_t>(data, S.p, n - (1ull << S.p), smc, st)) != GF2X_OK) return s;
+    if ((s = run_cvt<uint64_t>(S.lo, data, S.p, 1, false, smc, st)) != GF2X_OK) return s;
+    return run_cvt<uint64_t>(S.hi, data + (1ull << S.p), S.j, 1, false, smc, st);
+}
+// inverse per R22: iBasisCvt_p(g_lo) + s_p(x) iBasisCvt_j(g_hi) (g vanishes from 2^p + 2^j up: the product's length)
+static gf2x_status run_icvt_split(const CvtSplit& S, uint4* data, int smc, cudaStream_t st) {
+    gf2x_status s;
+    if ((s = run_cvt<uint4>(S.lo, data, S.p, 1, true, smc, st)) != GF2X_OK) return s;
+    if ((s = run_cvt<uint4>(S.hi, data + (1ull << S.p), S.j, 1, true, smc, st)) != GF2X_OK) return s;
+    return launch_shift_xor<uint4>(data, S.p, 1ull << S.j, smc, st);
+}
+
 static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* src, uint64_t src_per, uint4* dst,
                               const Plan& P, DeviceState* ds, cudaStream_t st, int operands = 1, IdxMap map = {0, 0, 0}) {
     FftParams prm;
@@ -875,6 +958,13 @@ static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* 
     return GF2X_OK;
 }
 
+// BasisCvt of operand a (or b), split per R22 when planned
+static gf2x_status run_cvt_operand(const Plan& P, bool is_a, uint64_t* S, int smc, cudaStream_t st) {
+    const CvtSplit& sp = is_a ? P.sa : P.sb;
+    if (sp.p >= 0) return run_cvt_fwd_split(sp, S, is_a ? P.na : P.nb, smc, st);
+    return run_cvt<uint64_t>(is_a ? P.cvt_a : P.cvt_b, S, is_a ? P.ma : P.mb, P.batch, false, smc, st);
+}
+
 // stop_stage: 0 = full product; 1..5 = stop after that stage (debug), result left in Wa
 static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
                                 const Plan& P, void* ws, DeviceState* ds, cudaStream_t st, int stop_stage) {
@@ -898,11 +988,11 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
     // (one operand at a time: at the headline sizes each 64-bit block array fits the 126 MB L2 alone)
     // Sb | Wb directly follow Sa | Wa: one launch per pass for both operands
     const bool same = (P.ma == P.mb) && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8;
-    if (same) {
+    if (same && P.sa.p < 0 && P.sb.p < 0) {
         if ((s = run_cvt<uint64_t>(P.cvt_a, Sa, P.ma, 2 * P.batch, false, smc, st)) != GF2X_OK) return s;
     } else {
-        if ((s = run_cvt<uint64_t>(P.cvt_a, Sa, P.ma, P.batch, false, smc, st)) != GF2X_OK) return s;
-        if ((s = run_cvt<uint64_t>(P.cvt_b, Sb, P.mb, P.batch, false, smc, st)) != GF2X_OK) return s;
+        if ((s = run_cvt_operand(P, true, Sa, smc, st)) != GF2X_OK) return s;
+        if ((s = run_cvt_operand(P, false, Sb, smc, st)) != GF2X_OK) return s;
     }
     // changeRepr + FFT_LCH top layers (direct passes; the last planned pass is the bottom one)
     const size_t ndirect = P.fft.size() - 1;
@@ -952,8 +1042,10 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         if ((s = launch_fft(P.fft[i], true, false, Wa, P.N, Wa, P, ds, st)) != GF2X_OK) return s;
     }
     if (stop_stage == 4) return GF2X_OK;
-    // iBasisCvt (tower)
-    if ((s = run_cvt<uint4>(P.icvt, Wa, P.m, P.batch, true, smc, st)) != GF2X_OK) return s;
+    // iBasisCvt (tower); the novel coefficients beyond the product's length are zero (R22 split)
+    if (P.ic.p >= 0) s = run_icvt_split(P.ic, Wa, smc, st);
+    else s = run_cvt<uint4>(P.icvt, Wa, P.m, P.batch, true, smc, st);
+    if (s != GF2X_OK) return s;
     if (stop_stage == 5) return GF2X_OK;
     // changeRepr^-1 + InterleavedCombine
     {
@@ -1331,7 +1423,11 @@ int gf2x_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, char* buf, size_t
     const int tj = trunc_geom(P, TG) ? TG.j : -1;
     out += "], \"bottom\": " + std::to_string(P.fft.back().layers) + ", \"trunc_j\": " + std::to_string(tj) +
            ", \"cvt_a\": " + cvt(P.cvt_a) +
-           ", \"cvt_b\": " + cvt(P.cvt_b) + ", \"icvt\": " + cvt(P.icvt) + "}";
+           ", \"cvt_b\": " + cvt(P.cvt_b) + ", \"icvt\": " + cvt(P.icvt);
+    auto sp = [](const CvtSplit& S) {
+        return S.p < 0 ? std::string("null") : "[" + std::to_string(S.p) + ", " + std::to_string(S.j) + "]";
+    };
+    out += ", \"split\": {\"a\": " + sp(P.sa) + ", \"b\": " + sp(P.sb) + ", \"icvt\": " + sp(P.ic) + "}}";
     if (buf && cap) {
         const size_t n = std::min(cap - 1, out.size());
         memcpy(buf, out.data(), n);

@@ -88,8 +88,8 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
         ProfScope ps("k_prep", (double)(P.nb + (1ull << P.mb)) * 8, st);
         k_prep<<<grid_for(1ull << P.mb, 256, smc, 8), 256, 0, st>>>(b, P.nb, b_bits, P.mb, 1, Sb);
     }
-    if ((s = run_cvt<uint64_t>(P.cvt_a, Sa, P.ma, 1, false, smc, st)) != GF2X_OK) return s;
-    if ((s = run_cvt<uint64_t>(P.cvt_b, Sb, P.mb, 1, false, smc, st)) != GF2X_OK) return s;
+    if ((s = run_cvt_operand(P, true, Sa, smc, st)) != GF2X_OK) return s;
+    if ((s = run_cvt_operand(P, false, Sb, smc, st)) != GF2X_OK) return s;
     // sub-plans: lower part (H points, global index = local) and upper part (2^j points at H + i)
     Plan PL;
     PL.N = T.H; PL.m = T.m - 1; PL.batch = 1;
@@ -159,11 +159,17 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
         ProfScope ps("k_xor_range", 48.0 * T.U, st);
         k_xor_range<<<grid_for(T.U, 256, smc, 8), 256, 0, st>>>(Ua - 0, Wb - 0, 0, T.U);
     }
-    CUDA_TRY(cudaMemsetAsync(Ua + T.U, 0, (T.H - T.U) * 16, st));
-    if ((s = check_launch("trunc combine")) != GF2X_OK) return s;
-    // iBasisCvt on the N coefficients, changeRepr^-1 + InterleavedCombine (as the full path)
-    if ((s = run_cvt<uint4>(P.icvt, Wa, P.m, 1, true, smc, st)) != GF2X_OK) return s;
     const uint64_t n_out = P.na + P.nb;
+    if ((s = check_launch("trunc combine")) != GF2X_OK) return s;
+    // iBasisCvt on the N coefficients (or split at H, R22: only units < n_out are read afterwards), then
+    // changeRepr^-1 + InterleavedCombine (as the full path)
+    if (P.ic.p >= 0) {
+        if (n_out > T.H + T.U) CUDA_TRY(cudaMemsetAsync(Ua + T.U, 0, (n_out - T.H - T.U) * 16, st));
+        if ((s = run_icvt_split(P.ic, Wa, smc, st)) != GF2X_OK) return s;
+    } else {
+        CUDA_TRY(cudaMemsetAsync(Ua + T.U, 0, (T.H - T.U) * 16, st));
+        if ((s = run_cvt<uint4>(P.icvt, Wa, P.m, 1, true, smc, st)) != GF2X_OK) return s;
+    }
     if (n_out <= P.N && P.N % IB_TILE == 0 && !env_flag("GF2X_NO_IPSI_BS")) {
         ProfScope ps("k_ipsi_bs", 16.0 * n_out + 8.0 * n_out, st);
         k_ipsi_bs<<<grid_for((n_out + IB_TILE - 1) / IB_TILE, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(Wa, ds->tabs, P.N,
