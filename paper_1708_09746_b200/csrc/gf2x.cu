@@ -393,6 +393,11 @@ struct DeviceState {
     size_t shard_ws_bytes = 0;
     int sm_count = 0;
     std::map<cudaStream_t, std::pair<void*, size_t>> ws;  // per-stream workspace cache
+    struct Aux {
+        cudaStream_t s = nullptr;          // side stream (high priority) for independent sub-chains
+        cudaEvent_t fork = nullptr, join = nullptr;
+    };
+    std::map<cudaStream_t, Aux> aux;       // per caller stream
 };
 static std::mutex g_mu;
 static std::map<int, DeviceState> g_dev;

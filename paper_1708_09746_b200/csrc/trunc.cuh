@@ -53,6 +53,77 @@ __global__ void __launch_bounds__(256) k_psi64(const uint64_t* __restrict__ S, u
     }
 }
 
+// NL layers of Reduce in one pass: layer l (k = k_top - l) folds x[2^k, 2^(k+1)) into x[0, 2^k) times c_l.
+// Thread i < Q = 2^(k_top - NL + 1) holds x[i + u Q], u < 2^NL, in registers and folds them down to u = 0.
+// PSI: the source is the operand's novel-basis blocks S (s_per words, 0 beyond), changeRepr'ed on the fly;
+// else the source is tower elements.  Two operands per launch when src2 != nullptr.  In place is safe
+// (thread i writes x[i] and only reads it or elements at or above Q).
+struct ReduceArgs {
+    const void* src[2];
+    uint4* dst[2];
+    uint64_t s_per[2];
+    uint32_t c[5];
+};
+template <int HALF>
+__device__ __forceinline__ void reduce_level(uint4* x, uint32_t tl) {
+#pragma unroll
+    for (int u = 0; u < HALF; u++) {
+        const uint4 v = x[u + HALF];
+        x[u].x ^= m4r4_word_sa(tl, v.x); x[u].y ^= m4r4_word_sa(tl, v.y);
+        x[u].z ^= m4r4_word_sa(tl, v.z); x[u].w ^= m4r4_word_sa(tl, v.w);
+    }
+}
+template <int NL, bool PSI>
+__global__ void __launch_bounds__(256) k_trunc_reduce(ReduceArgs ra, int nops, uint64_t Q, const DevTables* __restrict__ tabs) {
+    __shared__ __align__(1024) uint32_t tab[NL * 128];
+    __shared__ uint4 psit[PSI ? 8 * 256 : 1];
+    if (threadIdx.x < 8 * NL) {
+        const int l = threadIdx.x >> 3;
+        uint32_t c = ra.c[0];
+#pragma unroll
+        for (int q = 1; q < NL; q++) c = l == q ? ra.c[q] : c;
+        build_tab_row(tab + 128 * l, c, threadIdx.x & 7, tabs->wt);
+    }
+    if (PSI)
+        for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) psit[i] = tabs->psi64[i];
+    __syncthreads();
+    const uint32_t ta = (uint32_t)__cvta_generic_to_shared(tab);
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nops * Q; e += (uint64_t)gridDim.x * blockDim.x) {
+        const int op = e >= Q;
+        const uint64_t i = e - (op ? Q : 0);
+        const void* src = op ? ra.src[1] : ra.src[0];
+        const uint64_t s_per = op ? ra.s_per[1] : ra.s_per[0];
+        uint4 x[1 << NL];
+#pragma unroll
+        for (int u = 0; u < (1 << NL); u++) {
+            const uint64_t idx = i + (uint64_t)u * Q;
+            if (PSI) {
+                const uint64_t w = idx < s_per ? reinterpret_cast<const uint64_t*>(src)[idx] : 0ull;
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (w) {
+#pragma unroll
+                    for (int ch = 0; ch < 8; ch++) v = xor4(v, psit[ch * 256 + ((w >> (8 * ch)) & 255)]);
+                }
+                x[u] = v;
+            } else {
+                x[u] = reinterpret_cast<const uint4*>(src)[idx];
+            }
+        }
+        if (NL >= 5) reduce_level<16>(x, ta + 512 * (NL - 5));
+        if (NL >= 4) reduce_level<8>(x, ta + 512 * (NL - 4));
+        if (NL >= 3) reduce_level<4>(x, ta + 512 * (NL - 3));
+        if (NL >= 2) reduce_level<2>(x, ta + 512 * (NL - 2));
+        reduce_level<1>(x, ta + 512 * (NL - 1));
+        (op ? ra.dst[1] : ra.dst[0])[i] = x[0];
+    }
+}
+template <int NL>
+static void launch_trunc_reduce(bool psi, const ReduceArgs& ra, int nops, uint64_t Q, const DevTables* tabs, int smc, cudaStream_t st) {
+    const int g = grid_for(nops * Q, 256, smc, 4);
+    if (psi) k_trunc_reduce<NL, true><<<g, 256, 0, st>>>(ra, nops, Q, tabs);
+    else k_trunc_reduce<NL, false><<<g, 256, 0, st>>>(ra, nops, Q, tabs);
+}
+
 struct TruncGeom {
     int m, j;          // N = 2^m points, upper part 2^j
     uint64_t N, H, U;  // U = 2^j
@@ -67,6 +138,23 @@ static bool trunc_geom(const Plan& P, TruncGeom& T) {
     if (j > P.m - 2) return false;
     T.m = P.m; T.j = j; T.N = P.N; T.H = H; T.U = 1ull << j;
     return true;
+}
+
+// the side stream of caller stream st (created on first use; fork / join by events, capturable)
+static DeviceState::Aux* get_aux(DeviceState* ds, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    DeviceState::Aux& a = ds->aux[st];
+    if (!a.s) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&a.s, cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess) {
+            ds->aux.erase(st);
+            return nullptr;
+        }
+    }
+    return &a;
 }
 
 static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
@@ -100,26 +188,63 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
     const IdxMap umap{T.j, T.m - T.j, (uint32_t)(T.H >> T.j)};
     uint4* Ua = Wa + T.H;   // upper scratch: H elements per operand
     uint4* Ub = Wb + T.H;
-    // upper part, forward: changeRepr of the coefficients into the scratch, Reduce to 2^j, FFT_j at H + i
-    {
-        ProfScope ps("k_psi64", 2.0 * T.H * 24, st);
-        k_psi64<<<grid_for(T.H, 256, smc, 8), 256, 0, st>>>(Sa, 1ull << P.ma, T.H, ds->tabs, Ua);
-        k_psi64<<<grid_for(T.H, 256, smc, 8), 256, 0, st>>>(Sb, 1ull << P.mb, T.H, ds->tabs, Ub);
-    }
-    if ((s = check_launch("trunc psi")) != GF2X_OK) return s;
-    auto reduce = [&](uint4* x, uint4* x2) -> gf2x_status {
-        for (int k = T.m - 2; k >= T.j; k--) {
-            const uint64_t half = 1ull << k;
-            ProfScope ps("k_trunc_fold", 48.0 * half * (x2 ? 2 : 1), st);
-            k_trunc_fold<<<grid_for(half * (x2 ? 2 : 1), 256, smc, 8), 256, 0, st>>>(x, x2, half, H->S[k * 32 + (T.m - 1)],
-                                                                                   ds->tabs);
+    // Reduce(h), k = m-2 .. j, in passes of up to 5 layers (the first one reading src / changeRepr'ing S);
+    // the result, 2^j elements per operand, lands in dst[0, 2^j)
+    auto reduce = [&](bool psi, ReduceArgs ra, int nops, cudaStream_t st) -> gf2x_status {
+        if (env_flag("GF2X_TRUNC_LAYERED")) {   // debug: one launch per layer, through the H-element scratch
+            if (psi) {
+                ProfScope ps("k_psi64", (double)nops * T.H * 24, st);
+                for (int o = 0; o < nops; o++)
+                    k_psi64<<<grid_for(T.H, 256, smc, 8), 256, 0, st>>>((const uint64_t*)ra.src[o], ra.s_per[o], T.H, ds->tabs, ra.dst[o]);
+            } else {
+                for (int o = 0; o < nops; o++) CUDA_TRY(cudaMemcpyAsync(ra.dst[o], ra.src[o], T.H * 16, cudaMemcpyDeviceToDevice, st));
+            }
+            for (int k = T.m - 2; k >= T.j; k--) {
+                const uint64_t half = 1ull << k;
+                ProfScope ps("k_trunc_fold", 48.0 * half * nops, st);
+                k_trunc_fold<<<grid_for(half * nops, 256, smc, 8), 256, 0, st>>>(ra.dst[0], nops > 1 ? ra.dst[1] : nullptr, half,
+                                                                                 H->S[k * 32 + (T.m - 1)], ds->tabs);
+            }
+            return check_launch("trunc fold");
         }
-        return check_launch("trunc fold");
+        bool first = true;
+        for (int k = T.m - 2; k >= T.j;) {
+            const int nl = std::min(5, k - T.j + 1);
+            const uint64_t Q = 1ull << (k - nl + 1);
+            for (int l = 0; l < nl; l++) ra.c[l] = H->S[(k - l) * 32 + (T.m - 1)];
+            if (!first) { ra.src[0] = ra.dst[0]; ra.src[1] = ra.dst[1]; }
+            const bool p = psi && first;
+            ProfScope ps("k_trunc_reduce", (double)nops * Q * ((p ? 8.0 : 16.0) * (1 << nl) + 16.0), st);
+            switch (nl) {
+                case 1: launch_trunc_reduce<1>(p, ra, nops, Q, ds->tabs, smc, st); break;
+                case 2: launch_trunc_reduce<2>(p, ra, nops, Q, ds->tabs, smc, st); break;
+                case 3: launch_trunc_reduce<3>(p, ra, nops, Q, ds->tabs, smc, st); break;
+                case 4: launch_trunc_reduce<4>(p, ra, nops, Q, ds->tabs, smc, st); break;
+                default: launch_trunc_reduce<5>(p, ra, nops, Q, ds->tabs, smc, st); break;
+            }
+            k -= nl;
+            first = false;
+        }
+        return check_launch("trunc reduce");
     };
-    if ((s = reduce(Ua, Ub)) != GF2X_OK) return s;
+    // upper part (on the side stream when available: its small, latency-bound launches overlap the lower
+    // part's): Reduce of the operands' (changeRepr'ed) coefficients to 2^j, FFT_j at H + i, bottom, iFFT_j
+    DeviceState::Aux* aux = env_flag("GF2X_TRUNC_SERIAL") ? nullptr : get_aux(ds, st);
+    const cudaStream_t su = aux ? aux->s : st;
+    if (aux) {
+        CUDA_TRY(cudaEventRecord(aux->fork, st));
+        CUDA_TRY(cudaStreamWaitEvent(su, aux->fork, 0));
+    }
+    {
+        ReduceArgs ra{};
+        ra.src[0] = Sa; ra.src[1] = Sb;
+        ra.s_per[0] = 1ull << P.ma; ra.s_per[1] = 1ull << P.mb;
+        ra.dst[0] = Ua; ra.dst[1] = Ub;
+        if ((s = reduce(true, ra, 2, su)) != GF2X_OK) return s;
+    }
     for (size_t i = 0; i + 1 < fu.size(); i++) {
-        if ((s = launch_fft(fu[i], false, false, Ua, T.U, Ua, PU, ds, st, 1, umap)) != GF2X_OK) return s;
-        if ((s = launch_fft(fu[i], false, false, Ub, T.U, Ub, PU, ds, st, 1, umap)) != GF2X_OK) return s;
+        if ((s = launch_fft(fu[i], false, false, Ua, T.U, Ua, PU, ds, su, 1, umap)) != GF2X_OK) return s;
+        if ((s = launch_fft(fu[i], false, false, Ub, T.U, Ub, PU, ds, su, 1, umap)) != GF2X_OK) return s;
     }
     {
         BottomParams bp;
@@ -127,11 +252,12 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
         bp.total = T.U;
         bp.ntiles = (T.U + (1ull << BT_BITS) - 1) >> BT_BITS;
         bp.m = T.j; bp.L = fu.back().layers; bp.mode = 7; bp.map = umap;
-        ProfScope ps("k_bottom", 48.0 * T.U, st, (double)bp.ntiles * (3.0 * bp.L * 128.0 + 576.0) * OPS_BS_MUL32);
-        bottom_launch(bp, smc, st);
+        ProfScope ps("k_bottom", 48.0 * T.U, su, (double)bp.ntiles * (3.0 * bp.L * 128.0 + 576.0) * OPS_BS_MUL32);
+        bottom_launch(bp, smc, su);
     }
     for (size_t i = fu.size() - 1; i-- > 0;)
-        if ((s = launch_fft(fu[i], true, false, Ua, T.U, Ua, PU, ds, st, 1, umap)) != GF2X_OK) return s;
+        if ((s = launch_fft(fu[i], true, false, Ua, T.U, Ua, PU, ds, su, 1, umap)) != GF2X_OK) return s;
+    if (aux) CUDA_TRY(cudaEventRecord(aux->join, su));
     // lower part: the H-point multiply of the full pipeline (changeRepr fused into its first pass)
     for (size_t i = 0; i + 1 < fl.size(); i++) {
         const bool first = i == 0;
@@ -152,9 +278,14 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
     }
     for (size_t i = fl.size() - 1; i-- > 0;)
         if ((s = launch_fft(fl[i], true, false, Wa, T.H, Wa, PL, ds, st)) != GF2X_OK) return s;
-    // g_hi = iFFT_j(...) + Reduce(g_lo)[0, 2^j): Reduce on a copy of g_lo (Wb's lower half is free now)
-    CUDA_TRY(cudaMemcpyAsync(Wb, Wa, T.H * 16, cudaMemcpyDeviceToDevice, st));
-    if ((s = reduce(Wb, nullptr)) != GF2X_OK) return s;
+    // g_hi = iFFT_j(...) + Reduce(g_lo)[0, 2^j): Reduce of g_lo (in Wa) into Wb (free now)
+    {
+        ReduceArgs ra{};
+        ra.src[0] = Wa;
+        ra.dst[0] = Wb;
+        if ((s = reduce(false, ra, 1, st)) != GF2X_OK) return s;
+    }
+    if (aux) CUDA_TRY(cudaStreamWaitEvent(st, aux->join, 0));
     {
         ProfScope ps("k_xor_range", 48.0 * T.U, st);
         k_xor_range<<<grid_for(T.U, 256, smc, 8), 256, 0, st>>>(Ua - 0, Wb - 0, 0, T.U);
