@@ -77,7 +77,21 @@ struct FftParams {
     int wt_shared;        // table builds read a shared copy of the c -> c v_(4t) maps (only where the
                           // 28 KB do not cost occupancy: the CTA holds one per SM anyway)
     int db;               // non-PSI passes: double-buffered tiles (prefetch of the next tile) if they fit
+    uint4* red_dst;       // c = 5, R = 6, one product (truncated FFT, trunc.cuh): the changeRepr pass (its input)
+    uint32_t red_c[6];    //   or an inverse pass (its output) also folds the tile's 6 index bits [k_lo, k_hi)
+                          //   with the Reduce constants red_c[k - k_lo] into red_dst[base | col]
 };
+
+// x[u] ^= c x[u + HALF], u < HALF (one Reduce level in registers; tl = the M4R-4 table of c)
+template <int HALF>
+__device__ __forceinline__ void reduce_level(uint4* x, uint32_t tl) {
+#pragma unroll
+    for (int u = 0; u < HALF; u++) {
+        const uint4 v = x[u + HALF];
+        x[u].x ^= m4r4_word_sa(tl, v.x); x[u].y ^= m4r4_word_sa(tl, v.y);
+        x[u].z ^= m4r4_word_sa(tl, v.z); x[u].w ^= m4r4_word_sa(tl, v.w);
+    }
+}
 
 __device__ __forceinline__ uint32_t tab_addr(uint32_t base, uint32_t id) { return base + id * 512u; }
 
@@ -161,6 +175,39 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     if (p.wt_shared)
         for (uint32_t i = threadIdx.x; i < 7 * 1024 / 4; i += blockDim.x)
             reinterpret_cast<uint4*>(wts)[i] = reinterpret_cast<const uint4*>(p.tabs->wt)[i];
+    // fused Reduce (the forward changeRepr pass: of its input tile; the last inverse pass: of its output tile):
+    // 6 tables after the tile(s), then an 8 x 32 scratch
+    uint32_t* rtab = reinterpret_cast<uint32_t*>(smem_raw + tile_off + nslots * 16 * ((!PSI && p.db) ? 2 : 1));
+    uint4* rscr = reinterpret_cast<uint4*>(rtab + 6 * 128);
+    // Reduce over slot bits [5, 11) (index bits [k_lo, k_hi)): thread (part, col) folds u = 8 part + v over v's
+    // bits, then 32 threads fold the 8 parts; the tile itself is only read
+    auto fold_tile = [&](uint32_t base) {
+        const uint32_t rt = (uint32_t)__cvta_generic_to_shared(rtab);
+        const uint32_t col = threadIdx.x & 31, part = threadIdx.x >> 5;
+        uint4 x[8];
+#pragma unroll
+        for (int v = 0; v < 8; v++) x[v] = tile[col | ((part * 8 + v) << 5)];
+        reduce_level<4>(x, rt + 512 * 2);
+        reduce_level<2>(x, rt + 512 * 1);
+        reduce_level<1>(x, rt);
+        rscr[part * 32 + col] = x[0];
+        __syncthreads();
+        if (threadIdx.x < 32) {
+#pragma unroll
+            for (int q = 0; q < 8; q++) x[q] = rscr[q * 32 + threadIdx.x];
+            reduce_level<4>(x, rt + 512 * 5);
+            reduce_level<2>(x, rt + 512 * 4);
+            reduce_level<1>(x, rt + 512 * 3);
+            p.red_dst[base | threadIdx.x] = x[0];
+        }
+    };
+    if ((PSI || INV) && p.red_dst && threadIdx.x < 48) {
+        const int l = threadIdx.x >> 3;
+        uint32_t cst = p.red_c[0];
+#pragma unroll
+        for (int q = 1; q < 6; q++) cst = l == q ? p.red_c[q] : cst;
+        build_tab_row(rtab + 128 * l, cst, threadIdx.x & 7, p.tabs->wt);
+    }
     __syncthreads();   // the first tile's table build / load reads entries other warps wrote
 
     const uint64_t N = 1ull << p.m;
@@ -253,6 +300,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             else cp_async_wait<0>();
         }
         __syncthreads();
+        if (!INV && PSI && p.red_dst) fold_tile(base);
         // ---- layers, in groups of <= 3 (forward: from the top; inverse: from the bottom)
         if (!INV) {
             int top = p.k_hi;
@@ -272,6 +320,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
                 bot += r;
             }
         }
+        if (INV && p.red_dst) fold_tile(base);
         // ---- store
         uint4* dst = p.dst + pair * N;
         for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) dst[base | (s & cmask) | ((s >> p.c) << p.k_lo)] = tile[s];
@@ -280,8 +329,9 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     if (!PSI) cp_async_wait<0>();
 }
 
-static size_t fft2_smem(int c, int R, bool psi, bool wt_shared, bool db) {
-    size_t s = (((size_t)1 << R) - 1) * 512;
+static size_t fft2_smem(int c, int R, bool psi, bool wt_shared, bool db, bool red = false) {
+    size_t s = red ? 6 * 512 + 8 * 32 * 16 : 0;
+    s += (((size_t)1 << R) - 1) * 512;
     if (psi) s += 8 * 256 * 16;
     s += 512;   // zero-multiplier flags (<= 127 tables)
     if (wt_shared) s += 7 * 1024 * 4;   // shared copy of the M4R-8 maps c -> c v_(4t) (table builds)

@@ -936,8 +936,16 @@ static gf2x_status run_icvt_split(const CvtSplit& S, uint4* data, int smc, cudaS
 }
 
 static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* src, uint64_t src_per, uint4* dst,
-                              const Plan& P, DeviceState* ds, cudaStream_t st, int operands = 1, IdxMap map = {0, 0, 0}) {
+                              const Plan& P, DeviceState* ds, cudaStream_t st, int operands = 1, IdxMap map = {0, 0, 0},
+                              uint4* red_dst = nullptr, const uint32_t* red_c = nullptr) {
     FftParams prm;
+    prm.red_dst = nullptr;
+    if (red_dst) {   // fused Reduce (trunc.cuh): the kernel's fold assumes this geometry
+        if (!(psi || inv) || f.c != 5 || f.k_hi - f.k_lo != 6 || FFT_THREADS != 256 || P.batch * operands != 1)
+            return fail(GF2X_EINVAL, "fused Reduce geometry");
+        prm.red_dst = red_dst;
+        for (int i = 0; i < 6; i++) prm.red_c[i] = red_c[i];
+    }
     prm.map = map;
     prm.src = src; prm.dst = dst; prm.tabs = ds->tabs;
     prm.src_per = src_per; prm.batch = P.batch * operands;
@@ -946,7 +954,7 @@ static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* 
     const uint64_t ntiles = (P.N >> (f.c + R)) * prm.batch;
     prm.db = fft2_db(f.c, R, psi) ? 1 : 0;
     prm.wt_shared = fft2_wt_shared(f.c, R, psi) ? 1 : 0;
-    const size_t sm = fft2_smem(f.c, R, psi, prm.wt_shared != 0, prm.db != 0);
+    const size_t sm = fft2_smem(f.c, R, psi, prm.wt_shared != 0, prm.db != 0, red_dst != nullptr);
     const int occ = sm > 113 * 1024 ? 1 : 2;   // registers (128 x 256 threads) allow at most 2 CTAs/SM
     const int grid = grid_for(ntiles, 1, ds->sm_count, occ);
     const double bytes = (double)prm.batch * (psi ? (double)src_per * 8 : (double)P.N * 16) + (double)prm.batch * P.N * 16;

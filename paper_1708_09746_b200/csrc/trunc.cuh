@@ -64,15 +64,6 @@ struct ReduceArgs {
     uint64_t s_per[2];
     uint32_t c[5];
 };
-template <int HALF>
-__device__ __forceinline__ void reduce_level(uint4* x, uint32_t tl) {
-#pragma unroll
-    for (int u = 0; u < HALF; u++) {
-        const uint4 v = x[u + HALF];
-        x[u].x ^= m4r4_word_sa(tl, v.x); x[u].y ^= m4r4_word_sa(tl, v.y);
-        x[u].z ^= m4r4_word_sa(tl, v.z); x[u].w ^= m4r4_word_sa(tl, v.w);
-    }
-}
 template <int NL, bool PSI>
 __global__ void __launch_bounds__(256) k_trunc_reduce(ReduceArgs ra, int nops, uint64_t Q, const DevTables* __restrict__ tabs) {
     __shared__ __align__(1024) uint32_t tab[NL * 128];
@@ -109,10 +100,10 @@ __global__ void __launch_bounds__(256) k_trunc_reduce(ReduceArgs ra, int nops, u
                 x[u] = reinterpret_cast<const uint4*>(src)[idx];
             }
         }
-        if (NL >= 5) reduce_level<16>(x, ta + 512 * (NL - 5));
-        if (NL >= 4) reduce_level<8>(x, ta + 512 * (NL - 4));
-        if (NL >= 3) reduce_level<4>(x, ta + 512 * (NL - 3));
-        if (NL >= 2) reduce_level<2>(x, ta + 512 * (NL - 2));
+        if constexpr (NL >= 5) reduce_level<16>(x, ta + 512 * (NL - 5));
+        if constexpr (NL >= 4) reduce_level<8>(x, ta + 512 * (NL - 4));
+        if constexpr (NL >= 3) reduce_level<4>(x, ta + 512 * (NL - 3));
+        if constexpr (NL >= 2) reduce_level<2>(x, ta + 512 * (NL - 2));
         reduce_level<1>(x, ta + 512 * (NL - 1));
         (op ? ra.dst[1] : ra.dst[0])[i] = x[0];
     }
@@ -190,7 +181,7 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
     uint4* Ub = Wb + T.H;
     // Reduce(h), k = m-2 .. j, in passes of up to 5 layers (the first one reading src / changeRepr'ing S);
     // the result, 2^j elements per operand, lands in dst[0, 2^j)
-    auto reduce = [&](bool psi, ReduceArgs ra, int nops, cudaStream_t st) -> gf2x_status {
+    auto reduce = [&](bool psi, ReduceArgs ra, int nops, cudaStream_t st, int k0) -> gf2x_status {
         if (env_flag("GF2X_TRUNC_LAYERED")) {   // debug: one launch per layer, through the H-element scratch
             if (psi) {
                 ProfScope ps("k_psi64", (double)nops * T.H * 24, st);
@@ -208,7 +199,7 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
             return check_launch("trunc fold");
         }
         bool first = true;
-        for (int k = T.m - 2; k >= T.j;) {
+        for (int k = k0; k >= T.j;) {
             const int nl = std::min(5, k - T.j + 1);
             const uint64_t Q = 1ull << (k - nl + 1);
             for (int l = 0; l < nl; l++) ra.c[l] = H->S[(k - l) * 32 + (T.m - 1)];
@@ -227,6 +218,22 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
         }
         return check_launch("trunc reduce");
     };
+    // the lower part's first pass (changeRepr + the top 6 layers) also folds its 6 index bits for Reduce
+    const bool fuse = !env_flag("GF2X_TRUNC_LAYERED") && !env_flag("GF2X_TRUNC_NOFUSE") && fl.size() > 1 && fl[0].c == 5 &&
+                      fl[0].k_hi - fl[0].k_lo == 6 && fl[0].k_hi == T.m - 1 && T.j <= fl[0].k_lo;
+    auto lower_pass = [&](size_t i) -> gf2x_status {
+        const bool first = i == 0;
+        uint32_t rc[6];
+        if (first && fuse)
+            for (int kk = 0; kk < 6; kk++) rc[kk] = H->S[(fl[0].k_lo + kk) * 32 + (T.m - 1)];
+        gf2x_status r;
+        if ((r = launch_fft(fl[i], false, first, first ? (const void*)Sa : Wa, first ? (1ull << P.ma) : T.H, Wa, PL, ds, st, 1,
+                            IdxMap{0, 0, 0}, first && fuse ? Ua : nullptr, rc)) != GF2X_OK)
+            return r;
+        return launch_fft(fl[i], false, first, first ? (const void*)Sb : Wb, first ? (1ull << P.mb) : T.H, Wb, PL, ds, st, 1,
+                          IdxMap{0, 0, 0}, first && fuse ? Ub : nullptr, rc);
+    };
+    if (fuse && (s = lower_pass(0)) != GF2X_OK) return s;
     // upper part (on the side stream when available: its small, latency-bound launches overlap the lower
     // part's): Reduce of the operands' (changeRepr'ed) coefficients to 2^j, FFT_j at H + i, bottom, iFFT_j
     DeviceState::Aux* aux = env_flag("GF2X_TRUNC_SERIAL") ? nullptr : get_aux(ds, st);
@@ -237,10 +244,10 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
     }
     {
         ReduceArgs ra{};
-        ra.src[0] = Sa; ra.src[1] = Sb;
+        ra.src[0] = fuse ? (const void*)Ua : Sa; ra.src[1] = fuse ? (const void*)Ub : Sb;
         ra.s_per[0] = 1ull << P.ma; ra.s_per[1] = 1ull << P.mb;
         ra.dst[0] = Ua; ra.dst[1] = Ub;
-        if ((s = reduce(true, ra, 2, su)) != GF2X_OK) return s;
+        if ((s = reduce(!fuse, ra, 2, su, fuse ? fl[0].k_lo - 1 : T.m - 2)) != GF2X_OK) return s;
     }
     for (size_t i = 0; i + 1 < fu.size(); i++) {
         if ((s = launch_fft(fu[i], false, false, Ua, T.U, Ua, PU, ds, su, 1, umap)) != GF2X_OK) return s;
@@ -259,13 +266,8 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
         if ((s = launch_fft(fu[i], true, false, Ua, T.U, Ua, PU, ds, su, 1, umap)) != GF2X_OK) return s;
     if (aux) CUDA_TRY(cudaEventRecord(aux->join, su));
     // lower part: the H-point multiply of the full pipeline (changeRepr fused into its first pass)
-    for (size_t i = 0; i + 1 < fl.size(); i++) {
-        const bool first = i == 0;
-        if ((s = launch_fft(fl[i], false, first, first ? (const void*)Sa : Wa, first ? (1ull << P.ma) : T.H, Wa, PL, ds, st)) != GF2X_OK)
-            return s;
-        if ((s = launch_fft(fl[i], false, first, first ? (const void*)Sb : Wb, first ? (1ull << P.mb) : T.H, Wb, PL, ds, st)) != GF2X_OK)
-            return s;
-    }
+    for (size_t i = fuse ? 1 : 0; i + 1 < fl.size(); i++)
+        if ((s = lower_pass(i)) != GF2X_OK) return s;
     if (fl.size() == 1) return fail(GF2X_EINVAL, "truncated path needs a table pass");   // (m - 1 >= 13 always has one)
     {
         BottomParams bp;
@@ -276,14 +278,18 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
         ProfScope ps("k_bottom", 48.0 * T.H, st, (double)bp.ntiles * (3.0 * bp.L * 128.0 + 576.0) * OPS_BS_MUL32);
         bottom_launch(bp, smc, st);
     }
+    // g_hi = iFFT_j(...) + Reduce(g_lo)[0, 2^j): Reduce of g_lo (in Wa) into Wb (free now); fused, the last
+    // inverse pass folds its top 6 index bits on the way out
+    uint32_t rc[6];
+    for (int kk = 0; kk < 6 && fuse; kk++) rc[kk] = H->S[(fl[0].k_lo + kk) * 32 + (T.m - 1)];
     for (size_t i = fl.size() - 1; i-- > 0;)
-        if ((s = launch_fft(fl[i], true, false, Wa, T.H, Wa, PL, ds, st)) != GF2X_OK) return s;
-    // g_hi = iFFT_j(...) + Reduce(g_lo)[0, 2^j): Reduce of g_lo (in Wa) into Wb (free now)
+        if ((s = launch_fft(fl[i], true, false, Wa, T.H, Wa, PL, ds, st, 1, IdxMap{0, 0, 0}, fuse && i == 0 ? Wb : nullptr, rc)) != GF2X_OK)
+            return s;
     {
         ReduceArgs ra{};
-        ra.src[0] = Wa;
+        ra.src[0] = fuse ? (const void*)Wb : Wa;
         ra.dst[0] = Wb;
-        if ((s = reduce(false, ra, 1, st)) != GF2X_OK) return s;
+        if ((s = reduce(false, ra, 1, st, fuse ? fl[0].k_lo - 1 : T.m - 2)) != GF2X_OK) return s;
     }
     if (aux) CUDA_TRY(cudaStreamWaitEvent(st, aux->join, 0));
     {

@@ -67,3 +67,34 @@ def test_truncated_large_sampled_words_and_mod_p():
                     set(int(x) for x in rng.integers(0, n_out, size=12))):
         assert int(got[w]) == O.mul_word(a, b, w), w
     assert O.check_mod_p(a, b, got, O.random_irreducibles(3, seed=31))
+
+
+_VARIANT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+import paper_1708_09746_b200 as G
+from gf2x_synth import operand
+ab, bb = int(sys.argv[1]), int(sys.argv[2])
+a, b = operand(ab, seed=71), operand(bb, seed=72)
+da = torch.from_numpy(a.view(np.int64)).cuda().view(torch.uint64)
+db = torch.from_numpy(b.view(np.int64)).cuda().view(torch.uint64)
+c = G.gf2x_mul(da, ab, db, bb)
+torch.cuda.synchronize()
+np.save(sys.argv[3], c.cpu().view(torch.int64).numpy())
+"""
+
+
+@pytest.mark.parametrize("env", ["GF2X_TRUNC_NOFUSE", "GF2X_TRUNC_SERIAL", "GF2X_TRUNC_LAYERED", "GF2X_NO_CVT_SPLIT"])
+def test_truncated_variants_agree(env, tmp_path):
+    # the debug / fallback variants of the truncated path (flags are read once per process: a subprocess each)
+    import os
+    import subprocess
+    import sys
+    ab = bb = (1 << 22) + 64 * 3
+    a, b = operand(ab, seed=71), operand(bb, seed=72)
+    want = O.alg5_mul(a, ab, b, bb)
+    out = tmp_path / "c.npy"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", _VARIANT, str(ab), str(bb), str(out)], cwd=root, check=True, timeout=600,
+                   env={**os.environ, env: "1"})
+    assert np.array_equal(np.load(out).view(np.uint64), want)
