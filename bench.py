@@ -184,6 +184,9 @@ def main():
     ap.add_argument("--config", default="c4b", choices=["c1", "c2", "c3", "c4a", "c4b", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--bits", type=int, default=None,
+                    help="operand size override: one multiply of two BITS-bit operands instead of --config's "
+                         "(e.g. 268435520 = 2^28 + 64, the truncated-FFT staircase, DESIGN.md §10c)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--w", type=int, default=64, choices=[64, 128],
                     help="Alg. 5 block width: 64 (TGF(2^128), default) or 128 (TGF(2^256), P:873-874)")
@@ -207,6 +210,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     G.load()
     bits, batch = CONFIGS[args.config]
+    if args.bits:
+        bits, batch = args.bits, 1
+        args.config = "custom"
+        plan = G.gf2x_plan(bits, bits)
+        WORKLOAD["custom"] = (f"single {bits}-bit x {bits}-bit multiply ({plan['N']} points"
+                              + (f", truncated FFT: H-point + 2^{plan['trunc_j']}-point multiplies" if plan["trunc_j"] >= 0 else "")
+                              + (", split BasisCvt" if any(plan["split"].values()) else "") + ")")
+        if args.mode is None and world > 1:
+            args.mode = "replicas"
     mode = args.mode or ("sharded" if world > 1 else "single")
     if world == 1:
         mode = "single"
@@ -428,6 +440,7 @@ def main():
                         + ("" if args.alg == 5 else ", Alg. 4 (GF(2^128) polynomial basis, dense multipliers)"),
             "config": args.config, "operand_bits": bits, "batch": batch, "block_width": args.w, "algorithm": args.alg,
             "fft_points": 1 << max(0, (2 * n - 2).bit_length()) >> (0 if args.w == 64 else 1),
+            **({"trunc_j": G.gf2x_plan(bits, bits)["trunc_j"]} if args.config == "custom" else {}),
             "parallelism": (f"sharded FFT over {world} GPUs (" + ("peer memory: CUDA IPC over NVLink, fused pull-pack "
                             "all-to-all, NCCL barriers" if comm.peer_memory() == 1 else "NCCL send/recv") + ")" if sharded else
                             ("replicas" if world > 1 else "single")),

@@ -1181,6 +1181,8 @@ int gf2x_launch_count(uint64_t a_bits, uint64_t b_bits, int64_t batch) {
     if (a_bits == 0 || b_bits == 0 || batch <= 0) return 0;
     Plan P;
     if (make_plan(a_bits, b_bits, batch, P) != GF2X_OK) return 0;
+    TruncGeom TG;
+    if (trunc_geom(P, TG)) return launches_of_trunc(P, TG);
     return launches_of(P);
 }
 

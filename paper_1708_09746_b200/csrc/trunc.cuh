@@ -148,6 +148,26 @@ static DeviceState::Aux* get_aux(DeviceState* ds, cudaStream_t st) {
     return &a;
 }
 
+// the lower transform's first / last pass folds Reduce's top 6 layers (k_fft2 red_dst) when its geometry fits
+static bool trunc_fuse(const std::vector<FftPass>& fl, const TruncGeom& T) {
+    return !env_flag("GF2X_TRUNC_LAYERED") && !env_flag("GF2X_TRUNC_NOFUSE") && fl.size() > 1 && fl[0].c == 5 &&
+           fl[0].k_hi - fl[0].k_lo == 6 && fl[0].k_hi == T.m - 1 && T.j <= fl[0].k_lo;
+}
+// kernel launches of one truncated multiply (the default variant)
+static int launches_of_trunc(const Plan& P, const TruncGeom& T) {
+    const std::vector<FftPass> fl = plan_fft(T.m - 1), fu = plan_fft(T.j);
+    const bool fuse = trunc_fuse(fl, T);
+    const int k0 = fuse ? fl[0].k_lo - 1 : T.m - 2;
+    const int nred = k0 >= T.j ? (k0 - T.j + 1 + 4) / 5 : 0;
+    int n = 2;                                                             // prep a, b
+    n += launches_of_split(P.sa, P.cvt_a) + launches_of_split(P.sb, P.cvt_b);
+    n += 3 * ((int)fl.size() - 1) + 1;                                     // lower: forward a, b, bottom, inverse
+    n += 3 * ((int)fu.size() - 1) + 1;                                     // upper
+    n += 2 * nred + 1;                                                     // Reduce (forward, g_lo), g_hi combine
+    n += launches_of_split(P.ic, P.icvt) + 1;                              // iBasisCvt, changeRepr^-1 + combine
+    return n;
+}
+
 static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
                                       const Plan& P, const TruncGeom& T, void* ws, DeviceState* ds, cudaStream_t st) {
     unsigned char* base = reinterpret_cast<unsigned char*>(ws);
@@ -219,8 +239,7 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
         return check_launch("trunc reduce");
     };
     // the lower part's first pass (changeRepr + the top 6 layers) also folds its 6 index bits for Reduce
-    const bool fuse = !env_flag("GF2X_TRUNC_LAYERED") && !env_flag("GF2X_TRUNC_NOFUSE") && fl.size() > 1 && fl[0].c == 5 &&
-                      fl[0].k_hi - fl[0].k_lo == 6 && fl[0].k_hi == T.m - 1 && T.j <= fl[0].k_lo;
+    const bool fuse = trunc_fuse(fl, T);
     auto lower_pass = [&](size_t i) -> gf2x_status {
         const bool first = i == 0;
         uint32_t rc[6];

@@ -90,7 +90,7 @@ def test_truncated_variants_agree(env, tmp_path):
     import os
     import subprocess
     import sys
-    ab = bb = (1 << 22) + 64 * 3
+    ab = bb = (1 << 23) + 64 * 3   # m = 19: the fused Reduce applies (j = 12 = k_lo)
     a, b = operand(ab, seed=71), operand(bb, seed=72)
     want = O.alg5_mul(a, ab, b, bb)
     out = tmp_path / "c.npy"
@@ -98,3 +98,18 @@ def test_truncated_variants_agree(env, tmp_path):
     subprocess.run([sys.executable, "-c", _VARIANT, str(ab), str(bb), str(out)], cwd=root, check=True, timeout=600,
                    env={**os.environ, env: "1"})
     assert np.array_equal(np.load(out).view(np.uint64), want)
+
+
+@pytest.mark.parametrize("bits", [(1 << 23) + 192, (1 << 24) + 64, 1 << 20, ((1 << 16) + 5) * 64])
+def test_launch_count_matches_profile(bits):
+    # gf2x_launch_count (bench.py's gpu_launches claim) = the launches the profiler records for one multiply
+    a, b = operand(bits, seed=3), operand(bits, seed=4)
+    G.gf2x_mul(dev(a), bits, dev(b), bits)
+    torch.cuda.synchronize()
+    _, _ = gpu_mul(a, bits, b, bits, profile=False)
+    G.profile_enable(True)
+    G.gf2x_mul(dev(a), bits, dev(b), bits)
+    torch.cuda.synchronize()
+    n = sum(r["launches"] for r in G.profile_report())
+    G.profile_enable(False)
+    assert n == G.gf2x_launch_count(bits, bits)
