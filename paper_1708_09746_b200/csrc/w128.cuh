@@ -308,20 +308,29 @@ __global__ void __launch_bounds__(W2_THREADS) k_psi256_bs(const uint4* __restric
 // per product): out block w = lo128(C_w) ^ hi128(C_(w-1)), word 2w = limbs 0,1, word 2w+1 = limbs 2,3.
 // Pairs run (4,5), (0,1), (6,7), (2,3): the hi pair of every element is staged before the lo pair that
 // needs its predecessor's.  The tile's first element takes its predecessor from Hp (thread 0, tables).
-__global__ void __launch_bounds__(W2_THREADS) k_ipsi256_bs(const uint4* __restrict__ W, uint64_t N, uint64_t batch,
-                                                           const DevTables256* __restrict__ T, uint64_t* __restrict__ out) {
+// 4 thread groups of W2_THREADS share one tile: group g makes output limb pair O = {4, 6, 0, 2}[g] of its 32-element
+// columns (the tile's planes are read by all four), so a CTA keeps 8 warps busy on 96 KB of shared memory
+// (the one-group form held 2 warps per CTA on 80 KB).  The hi pairs (4,5), (6,7) are staged in H for the
+// successor's lo pairs; the output words are staged limb-planar (in the plane area, free by then) and
+// written coalesced.
+#define IB2_GROUPS 4
+#define IB2_THREADS (IB2_GROUPS * W2_THREADS)
+#define IB2_SMEM (12 * W2_TILE * 4)
+__global__ void __launch_bounds__(IB2_THREADS, 1) k_ipsi256_bs(const uint4* __restrict__ W, uint64_t N, uint64_t batch,
+                                                             const DevTables256* __restrict__ T, uint64_t* __restrict__ out) {
     extern __shared__ __align__(1024) uint32_t w2_smem[];
-    uint32_t* In = w2_smem;                  // [8][W2_TILE]
-    uint32_t* H = w2_smem + 8 * W2_TILE;     // [2][W2_TILE] staged hi pair
+    uint32_t* In = w2_smem;                  // [8][W2_TILE] limb planes; afterwards [4][W2_TILE] output halves
+    uint32_t* H = w2_smem + 8 * W2_TILE;     // [4][W2_TILE] hi pairs (4,5), (6,7) of every element
     __shared__ uint4 Hp;                     // predecessor's C hi128 (limbs 4..7)
     const uint64_t plane = batch * N, ntiles = plane / W2_TILE;
-    const uint32_t t = threadIdx.x, e0 = 32 * t;
+    const uint32_t t = threadIdx.x, g = t / W2_THREADS, e0 = 32 * (t % W2_THREADS);
+    const int O = g == 0 ? 4 : (g == 1 ? 6 : (g == 2 ? 0 : 2));
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint64_t g0 = tile * W2_TILE, p = g0 / N, i0 = g0 - p * N;
         const uint4* lo = W + g0;
         const uint4* hi = lo + plane;
-        __syncthreads();
-        for (uint32_t e = t; e < W2_TILE; e += W2_THREADS) {
+        __syncthreads();   // the previous tile's output staging has been written out
+        for (uint32_t e = t; e < W2_TILE; e += IB2_THREADS) {
             const uint4 a = lo[e], b = hi[e];
             const uint32_t q = w2_swz(e);
             In[q] = a.x; In[W2_TILE + q] = a.y; In[2 * W2_TILE + q] = a.z; In[3 * W2_TILE + q] = a.w;
@@ -333,38 +342,51 @@ __global__ void __launch_bounds__(W2_THREADS) k_ipsi256_bs(const uint4* __restri
             Hp = rhi;
         }
         __syncthreads();
-        w2_transpose_own(In, 8, e0);
+        // limbs 2g, 2g + 1 of my column: elements -> planes, in place
+#pragma unroll 1
+        for (int L = 2 * (int)g; L < 2 * (int)g + 2; L++) {
+            uint32_t x[32];
+            w2_load_planes(In, L, e0, x);
+            transpose32(x);
+#pragma unroll
+            for (int j = 0; j < 32; j++) In[L * W2_TILE + w2_swz(e0 + j)] = x[j];
+        }
+        __syncthreads();
+        uint32_t a0[32], a1[32];
+#pragma unroll
+        for (int j = 0; j < 32; j++) { a0[j] = 0; a1[j] = 0; }
+#pragma unroll 1
+        for (int L = 0; L < 8; L++) {
+            uint32_t x[32];
+            w2_load_planes(In, L, e0, x);
+            ipsi256_block(O, L, x, a0, a1);
+        }
+        transpose32(a0);
+        transpose32(a1);
+        if (O >= 4) {   // hi pair -> H[(O - 4) .. (O - 3)]
+            uint32_t* h = H + (O - 4) * W2_TILE;
+#pragma unroll
+            for (int j = 0; j < 32; j++) { h[w2_swz(e0 + j)] = a0[j]; h[W2_TILE + w2_swz(e0 + j)] = a1[j]; }
+        }
+        __syncthreads();   // H complete; the planes are no longer read
+        if (O < 4) {    // word 2e (O = 0: limbs 0,1 ^ C_(e-1) limbs 4,5) or 2e + 1 (O = 2: limbs 2,3 ^ limbs 6,7)
+            const uint32_t* h = H + O * W2_TILE;
+            const uint32_t* hp = reinterpret_cast<const uint32_t*>(&Hp) + O;
+            uint32_t* o = In + O * W2_TILE;
+#pragma unroll
+            for (int j = 0; j < 32; j++) {
+                const uint32_t e = e0 + j;
+                const uint32_t p0 = e ? h[w2_swz(e - 1)] : hp[0];
+                const uint32_t p1 = e ? h[W2_TILE + w2_swz(e - 1)] : hp[1];
+                o[w2_swz(e)] = a0[j] ^ p0;
+                o[W2_TILE + w2_swz(e)] = a1[j] ^ p1;
+            }
+        }
+        __syncthreads();
         uint64_t* dst = out + p * 2 * N + 2 * i0;
-#pragma unroll 1
-        for (int k = 0; k < 4; k++) {
-            const int O = k == 0 ? 4 : (k == 1 ? 0 : (k == 2 ? 6 : 2));
-            uint32_t a0[32], a1[32];
-#pragma unroll
-            for (int j = 0; j < 32; j++) { a0[j] = 0; a1[j] = 0; }
-#pragma unroll 1
-            for (int L = 0; L < 8; L++) {
-                uint32_t x[32];
-                w2_load_planes(In, L, e0, x);
-                ipsi256_block(O, L, x, a0, a1);
-            }
-            transpose32(a0);
-            transpose32(a1);
-            if (O >= 4) {   // stage the hi pair (4,5) / (6,7)
-                __syncthreads();   // previous lo pair done reading H
-#pragma unroll
-                for (int j = 0; j < 32; j++) { H[w2_swz(e0 + j)] = a0[j]; H[W2_TILE + w2_swz(e0 + j)] = a1[j]; }
-                __syncthreads();
-            } else {        // lo pair (0,1) / (2,3): xor the predecessor's staged hi pair, write one word
-                const int hsel = O == 0 ? 0 : 2;   // limbs 4,5 (word 2w) or 6,7 (word 2w+1) of C_(w-1)
-                const uint32_t* hp = reinterpret_cast<const uint32_t*>(&Hp) + hsel;
-#pragma unroll
-                for (int j = 0; j < 32; j++) {
-                    const uint32_t e = e0 + j;
-                    const uint32_t p0 = e ? H[w2_swz(e - 1)] : hp[0];
-                    const uint32_t p1 = e ? H[W2_TILE + w2_swz(e - 1)] : hp[1];
-                    dst[2 * e + (O == 0 ? 0 : 1)] = ((uint64_t)(a1[j] ^ p1) << 32) | (a0[j] ^ p0);
-                }
-            }
+        for (uint32_t i = t; i < 2 * W2_TILE; i += IB2_THREADS) {
+            const uint32_t e = i >> 1, sel = (i & 1) * 2;
+            dst[i] = ((uint64_t)In[(sel + 1) * W2_TILE + w2_swz(e)] << 32) | In[sel * W2_TILE + w2_swz(e)];
         }
     }
 }
@@ -422,7 +444,7 @@ static gf2x_status get_tables256(DeviceState* ds, DevTables256** out) {
         delete h;
         if (e != cudaSuccess) { cudaFree(d); return fail(GF2X_ECUDA, cudaGetErrorString(e)); }
         CUDA_TRY(cudaFuncSetAttribute(k_w128_post, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_ipsi256_bs, cudaFuncAttributeMaxDynamicSharedMemorySize, 10 * W2_TILE * 4));
+        CUDA_TRY(cudaFuncSetAttribute(k_ipsi256_bs, cudaFuncAttributeMaxDynamicSharedMemorySize, IB2_SMEM));
         ds->tabs256 = d;
     }
     *out = ds->tabs256;
@@ -536,7 +558,7 @@ static gf2x_status run_pipeline_w128(const uint64_t* a, uint64_t a_bits, const u
     // changeRepr^-1 + InterleavedCombine
     if (w2bs && P.na + P.nb == 2 * P.N) {
         ProfScope ps("k_ipsi256_bs", 32.0 * plane + 16.0 * plane, st);
-        k_ipsi256_bs<<<grid_for(plane / W2_TILE, 1, smc, 2), W2_THREADS, 10 * W2_TILE * 4, st>>>(Wa, P.N, B, T256, c);
+        k_ipsi256_bs<<<grid_for(plane / W2_TILE, 1, smc, 2), IB2_THREADS, IB2_SMEM, st>>>(Wa, P.N, B, T256, c);
     } else {
         const uint64_t n_out = P.na + P.nb, nblk = (n_out + 1) / 2;
         const uint64_t ctas = (nblk + IPSI256_THREADS - 1) / IPSI256_THREADS * B;
