@@ -84,6 +84,10 @@ def lib():
             "or_psi256_generator": (None, [i32, _u64p]),
             "or_fft256": (None, [_u64p, i32]),
             "or_alg5_mul_w128": (i32, [_u64p, u64, _u64p, u64, _u64p] + [_u64p] * 4),
+            "or_frob_eval": (i32, [_u64p, u64, i32, _u64p, i32]),
+            "or_frob_columns": (None, [i32, _u64p]),
+            "or_frob_m": (i32, [u64, u64]),
+            "or_frob_mul": (i32, [_u64p, u64, _u64p, u64, _u64p]),
             "or_is_irreducible64": (i32, [u64]),
             "or_poly_mod": (u64, [_u64p, sz, u64]),
             "or_mulmod64": (u64, [u64, u64, u64]),
@@ -308,6 +312,40 @@ def alg4_mul(a: np.ndarray, a_bits: int, b: np.ndarray, b_bits: int, stages: boo
         raise RuntimeError(f"oracle alg4 internal assertion failed: {err}")
     if stages:
         return c, {k: v.reshape(-1, 2) for k, v in st.items()}
+    return c
+
+
+# ---------------------------------------------------------------- O3, App. C (Frobenius bijection)
+def frob_m(a_bits: int, b_bits: int) -> int:
+    """log2 of the number of evaluation points the Frobenius multiply uses (128 * 2^m >= a_bits + b_bits - 1)."""
+    return lib().or_frob_m(a_bits, b_bits)
+
+
+def frob_eval(a: np.ndarray, a_bits: int, m: int, stage: int = 2) -> np.ndarray:
+    """E_(beta_(m+64) + V_m)(a): 2^m tower elements as (2^m, 2) words (stage 1: after the 7-layer encoding)."""
+    a = np.ascontiguousarray(a, dtype=np.uint64)
+    out = np.zeros(2 << m, dtype=np.uint64)
+    if lib().or_frob_eval(_p(a if len(a) else np.zeros(1, np.uint64)), a_bits, m, _p(out), stage) != 0:
+        raise ValueError("frob_eval: bad size")
+    return out.reshape(-1, 2)
+
+
+def frob_columns(m: int) -> list:
+    """The encoding's 128 columns (images of the unit bits j) as Python ints."""
+    out = np.zeros(256, dtype=np.uint64)
+    lib().or_frob_columns(m, _p(out))
+    return [_int(out[2 * j:2 * j + 2]) for j in range(128)]
+
+
+def frob_mul(a: np.ndarray, a_bits: int, b: np.ndarray, b_bits: int) -> np.ndarray:
+    """App. C multiplication through the Frobenius bijection: c (na + nb words)."""
+    a = np.ascontiguousarray(a, dtype=np.uint64)
+    b = np.ascontiguousarray(b, dtype=np.uint64)
+    c = np.zeros((a_bits + 63) // 64 + (b_bits + 63) // 64, dtype=np.uint64)
+    err = lib().or_frob_mul(_p(a if len(a) else np.zeros(1, np.uint64)), a_bits,
+                            _p(b if len(b) else np.zeros(1, np.uint64)), b_bits, _p(c if len(c) else np.zeros(1, np.uint64)))
+    if err != 0:
+        raise RuntimeError(f"oracle frob internal assertion failed: {err}")
     return c
 
 

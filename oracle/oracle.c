@@ -24,6 +24,8 @@
  *       w = 128 variant (sec 4.2): TGF(2^256) one tower level up, GF(2^256) modulo
  *       z^256+z^10+z^5+z^2+1 (R20) and changeRepr_256 by the same rule, Alg. 5 on 128-bit blocks.
  *       Alg. 4 (sec 3.1): FFT_LCH in GF(2^128) polynomial basis, dense multipliers psi^-1(s_k).
+ *       App. C: multiplication through the Frobenius bijection E_(beta_(m+64) + V_m):
+ *       BasisCvt on GF(2) coefficients, the 7-layer encoding, FFT_LCH displaced by beta_(m+64), decoding.
  *   O4  product check modulo random irreducible degree-64 polynomials.
  *
  * All arithmetic is exact (GF(2) AND/XOR); no floating point anywhere.
@@ -626,6 +628,208 @@ int or_alg5_mul(const uint64_t *a, uint64_t a_bits, const uint64_t *b, uint64_t 
     }
     free_constants(C, m);
     free(A); free(B);
+    return err;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* O3, App. C: multiplication through the Frobenius bijection E_(beta_(m+64) + V_m) */
+/*   "an FFT directly on GF(2)[x] ... abandoning the Kronecker segmentation".       */
+/*   A binary polynomial of < 128 n bits (n = 2^m) is evaluated at the n points beta_(m+64) +    */
+/*   phi(i), i < n (Def. P:1502-1507): BasisCvt on its 2^(m+7) GF(2) coefficients ("proceeded    */
+/*   straightforwardly with alg. 3"), the first 7 layers of Alg. 1 with alpha =          */
+/*   beta_(m+64) keeping block 0 only ("reserve only the first 1/128 results"; the   */
+/*   "encoding"), then the normal n-point FFT_LCH with the same alpha.  The product */
+/*   has < 128 n' bits for n' = the smallest power of two with 128 n' >= L (R23), so   */
+/*   E(c) = E(a) E(b) pointwise is inverted by iFFT, decoding (the 128 x 128 map of the encoding */
+/*   is invertible: Prop. P:1515-1518) and iBasisCvt.  The Cantor basis beta_i is the tower's    */
+/*   v_i (phi(i) = i as a bit pattern), so alpha = 2^(m+64) and all arithmetic is TGF(2^128).    */
+/* ------------------------------------------------------------------------------------------ */
+/* Alg. 2/3 on GF(2) coefficients (one byte per bit): the same steps as taylor / cvt above */
+static void taylor8(uint8_t *f, size_t s, size_t len, int K) {
+    size_t h = len / 2, d = h - (h >> K);
+    for (size_t i = len - 1; i >= h; i--) {
+        f[s + i - d] ^= f[s + i];
+        if (i == h) break;
+    }
+}
+static void itaylor8(uint8_t *f, size_t s, size_t len, int K) {
+    size_t h = len / 2, d = h - (h >> K);
+    for (size_t i = h; i < len; i++) f[s + i - d] ^= f[s + i];
+}
+static void cvt8(uint8_t *f, size_t base, int m, int sigma) {
+    if (m <= 1) return;
+    int K = 1 << floor_log2(m - 1);
+    for (int l = m; l >= K + 1; l--)
+        for (size_t s = 0; s < ((size_t)1 << (m + sigma)); s += ((size_t)1 << (l + sigma)))
+            taylor8(f, base + s, (size_t)1 << (l + sigma), K);
+    cvt8(f, base, m - K, sigma + K);
+    for (size_t c = 0; c < ((size_t)1 << (m + sigma)); c += ((size_t)1 << (K + sigma))) cvt8(f, base + c, K, sigma);
+}
+static void icvt8(uint8_t *f, size_t base, int m, int sigma) {
+    if (m <= 1) return;
+    int K = 1 << floor_log2(m - 1);
+    for (size_t c = 0; c < ((size_t)1 << (m + sigma)); c += ((size_t)1 << (K + sigma))) icvt8(f, base + c, K, sigma);
+    icvt8(f, base, m - K, sigma + K);
+    for (int l = K + 1; l <= m; l++)
+        for (size_t s = 0; s < ((size_t)1 << (m + sigma)); s += ((size_t)1 << (l + sigma)))
+            itaylor8(f, base + s, (size_t)1 << (l + sigma), K);
+}
+
+/* FFT_LCH / iFFT at displacement alpha: block b of layer k multiplies by s_k(alpha + phi(b)) =
+ * s_k(alpha) + s_k(phi(b)) (s_k is linear) -- the alpha = 0 constants plus one per layer */
+static void fft_alpha(u128 *A, int m, u128 **C, const u128 *sa, int inverse) {
+    for (int kk = 0; kk < m; kk++) {
+        int k = inverse ? kk : m - 1 - kk;
+        size_t half = (size_t)1 << k, nb = (size_t)1 << (m - k - 1);
+        for (size_t j = 0; j < nb; j++) {
+            size_t b = j << (k + 1);
+            u128 c = C[k][j] ^ sa[k];
+            for (size_t i = 0; i < half; i++) {
+                if (!inverse) {
+                    A[b + i] ^= tmul(A[b + half + i], c, 7);
+                    A[b + half + i] ^= A[b + i];
+                } else {
+                    A[b + half + i] ^= A[b + i];
+                    A[b + i] ^= tmul(A[b + half + i], c, 7);
+                }
+            }
+        }
+    }
+}
+
+/* E_(alpha + V_m) of the 2^(m+7) novel-basis bits g: the first 7 layers of Alg. 1 (k = m+6 .. m) on
+ * block 0 only -- A[i] ^= s_k(alpha) A[i + 2^k], i < 2^k (the upper half belongs to the points that are
+ * not kept) -- then the n-point FFT with alpha.  stage 1: stop after the encoding. */
+static void frob_eval(const uint8_t *g, int m, u128 alpha, u128 *E, int stage) {
+    int M = m + 7;
+    size_t NB = (size_t)1 << M, n = (size_t)1 << m;
+    u128 *T = (u128 *)malloc(NB * sizeof(u128));
+    for (size_t i = 0; i < NB; i++) T[i] = g[i];
+    for (int k = M - 1; k >= m; k--) {
+        u128 c = s_eval(k, alpha);
+        for (size_t i = 0; i < ((size_t)1 << k); i++) T[i] ^= tmul(T[i + ((size_t)1 << k)], c, 7);
+    }
+    memcpy(E, T, n * sizeof(u128));
+    free(T);
+    if (stage == 1) return;
+    u128 sa[64];
+    for (int k = 0; k < m; k++) sa[k] = s_eval(k, alpha);
+    u128 **C = all_constants(m);
+    fft_alpha(E, m, C, sa, 0);
+    free_constants(C, m);
+}
+
+/* Gauss-Jordan inverse of the 128 x 128 GF(2) matrix whose column j is col[j] (rows as u128 bit sets);
+ * returns 0, or -1 if singular.  out[j] = column j of the inverse. */
+static int gf2_inverse128(const u128 *col, u128 *out) {
+    u128 rowA[128], rowI[128];
+    for (int r = 0; r < 128; r++) {
+        u128 v = 0;
+        for (int j = 0; j < 128; j++) if ((col[j] >> r) & 1) v |= (u128)1 << j;
+        rowA[r] = v; rowI[r] = (u128)1 << r;
+    }
+    for (int c = 0; c < 128; c++) {
+        int p = -1;
+        for (int r = c; r < 128; r++) if ((rowA[r] >> c) & 1) { p = r; break; }
+        if (p < 0) return -1;
+        u128 t = rowA[p]; rowA[p] = rowA[c]; rowA[c] = t;
+        t = rowI[p]; rowI[p] = rowI[c]; rowI[c] = t;
+        for (int r = 0; r < 128; r++)
+            if (r != c && ((rowA[r] >> c) & 1)) { rowA[r] ^= rowA[c]; rowI[r] ^= rowI[c]; }
+    }
+    /* rowI[r] = row r of the inverse; column j = bits j of every row */
+    for (int j = 0; j < 128; j++) {
+        u128 v = 0;
+        for (int r = 0; r < 128; r++) if ((rowI[r] >> j) & 1) v |= (u128)1 << r;
+        out[j] = v;
+    }
+    return 0;
+}
+/* apply a matrix given by columns: y = sum_j x_j col[j] */
+static u128 apply128(const u128 *col, u128 x) {
+    u128 y = 0;
+    for (int j = 0; j < 128; j++) if ((x >> j) & 1) y ^= col[j];
+    return y;
+}
+
+/* the encoding's columns: the image of the unit bit j (g[i + j n] = 1) under the 7 layers */
+static void frob_columns(int m, u128 alpha, u128 *col) {
+    u128 sk[7];
+    for (int b = 0; b < 7; b++) sk[b] = s_eval(m + b, alpha);
+    for (int j = 0; j < 128; j++) {
+        u128 c = 1;
+        for (int b = 0; b < 7; b++) if ((j >> b) & 1) c = tmul(c, sk[b], 7);
+        col[j] = c;
+    }
+}
+
+static int frob_m(uint64_t L) { int m = 0; while (((uint64_t)128 << m) < L) m++; return m; }
+
+/* E(a) at the 2^m points alpha + phi(i), alpha = beta_(m+64); a has a_bits <= 128 2^m bits.
+ * out: 2^m tower elements (2 words each).  stage 1: the encoding only. */
+int or_frob_eval(const uint64_t *a, uint64_t a_bits, int m, uint64_t *out, int stage) {
+    tower_init();
+    if (m < 0 || m > 40 || a_bits > ((uint64_t)128 << m)) return -1;
+    int M = m + 7;
+    size_t NB = (size_t)1 << M, n = (size_t)1 << m;
+    uint8_t *g = (uint8_t *)calloc(NB, 1);
+    for (uint64_t i = 0; i < a_bits; i++) g[i] = (a[i / 64] >> (i % 64)) & 1;
+    cvt8(g, 0, M, 0);
+    u128 *E = (u128 *)malloc(n * sizeof(u128));
+    frob_eval(g, m, (u128)1 << (m + 64), E, stage);
+    from128(E, n, 2, out);
+    free(E); free(g);
+    return 0;
+}
+/* the 128 columns of the encoding (2 words each), for the closed-form pin */
+void or_frob_columns(int m, uint64_t *out) { tower_init(); u128 col[128]; frob_columns(m, (u128)1 << (m + 64), col); from128(col, 128, 2, out); }
+int or_frob_m(uint64_t a_bits, uint64_t b_bits) { return a_bits && b_bits ? frob_m(a_bits + b_bits - 1) : 0; }
+
+/* c = a b (na + nb words) through E: returns 0, or -1 (singular encoding), -2 (bits above the product) */
+int or_frob_mul(const uint64_t *a, uint64_t a_bits, const uint64_t *b, uint64_t b_bits, uint64_t *c) {
+    tower_init();
+    size_t na = (a_bits + 63) / 64, nb = (b_bits + 63) / 64;
+    memset(c, 0, (na + nb) * sizeof(uint64_t));
+    if (a_bits == 0 || b_bits == 0) return 0;
+    uint64_t L = a_bits + b_bits - 1;          /* coefficients of the product */
+    int m = frob_m(L), M = m + 7;
+    size_t NB = (size_t)1 << M, n = (size_t)1 << m;
+    u128 alpha = (u128)1 << (m + 64);
+    uint8_t *g = (uint8_t *)calloc(NB, 1);
+    u128 *EA = (u128 *)malloc(n * sizeof(u128)), *EB = (u128 *)malloc(n * sizeof(u128));
+    for (uint64_t i = 0; i < a_bits; i++) g[i] = (a[i / 64] >> (i % 64)) & 1;
+    cvt8(g, 0, M, 0);
+    frob_eval(g, m, alpha, EA, 2);
+    memset(g, 0, NB);
+    for (uint64_t i = 0; i < b_bits; i++) g[i] = (b[i / 64] >> (i % 64)) & 1;
+    cvt8(g, 0, M, 0);
+    frob_eval(g, m, alpha, EB, 2);
+    /* E(c) = E(a) E(b) */
+    for (size_t i = 0; i < n; i++) EA[i] = tmul(EA[i], EB[i], 7);
+    /* iFFT with alpha */
+    u128 sa[64];
+    for (int k = 0; k < m; k++) sa[k] = s_eval(k, alpha);
+    u128 **C = all_constants(m);
+    fft_alpha(EA, m, C, sa, 1);
+    free_constants(C, m);
+    /* decoding: the 128 bits g[i + j n] of every i from the encoded element */
+    u128 col[128], inv[128];
+    frob_columns(m, alpha, col);
+    int err = 0;
+    if (gf2_inverse128(col, inv) != 0) err = -1;
+    memset(g, 0, NB);
+    for (size_t i = 0; i < n && !err; i++) {
+        u128 bits = apply128(inv, EA[i]);
+        for (int j = 0; j < 128; j++) g[i + (size_t)j * n] = (uint8_t)((bits >> j) & 1);
+    }
+    /* iBasisCvt on the 2^(m+7) GF(2) coefficients */
+    icvt8(g, 0, M, 0);
+    for (size_t i = 0; i < NB && !err; i++) {
+        if (!g[i]) continue;
+        if (i >= L) { err = -2; break; }
+        c[i / 64] |= (uint64_t)1 << (i % 64);
+    }
+    free(g); free(EA); free(EB);
     return err;
 }
 
