@@ -184,6 +184,8 @@ def main():
     ap.add_argument("--config", default="c4b", choices=["c1", "c2", "c3", "c4a", "c4b", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--graph", action="store_true",
+                    help="time replays of one step captured in a CUDA graph (launch overhead removed; for the small configs)")
     ap.add_argument("--bits", type=int, default=None,
                     help="operand size override: one multiply of two BITS-bit operands instead of --config's "
                          "(e.g. 268435520 = 2^28 + 64, the truncated-FFT staircase, DESIGN.md §10c)")
@@ -309,6 +311,31 @@ def main():
     ms = ev0.elapsed_time(ev1)
     prof = G.profile_report()
     G.profile_enable(False)
+    ms_eager = None
+    if args.graph and not sharded:
+        # one step captured on a side stream (the library plans on the host at capture time), replayed K times
+        ms_eager = ms
+        eager_stream, stream = stream, torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                step()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                graph.replay()
+            torch.cuda.synchronize()
+            t_wall0 = time.time()
+            ev0.record(stream)
+            for _ in range(args.steps):
+                graph.replay()
+            ev1.record(stream)
+        torch.cuda.synchronize()
+        t_wall1 = time.time()
+        ms = ev0.elapsed_time(ev1)
+        stream = eager_stream
     time.sleep(0.25)
     sampler.stop()
     clocks = sampler.summary(t_wall0 - 0.05, t_wall1 + 0.05)
@@ -447,6 +474,7 @@ def main():
             "seed": DEFAULT_SEED, "l2": "working set > 126 MB L2 (operands + 2 spectra), no flush" if bits >= 1 << 28
             else "working set may be L2-resident (small config)",
             "paper_ms_haswell": PAPER_MS.get(args.config),
+            **({"cuda_graph": True, "ms_per_step_eager": round(ms_eager / args.steps, 4)} if ms_eager is not None else {}),
         },
         "roofline": ({
             "bound": "alu", "kernel": dom["kernel"], "achieved": round(achieved_ops, 1), "peak": round(alu_peak, 1),
