@@ -261,6 +261,16 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
         CUDA_TRY(cudaEventRecord(aux->fork, st));
         CUDA_TRY(cudaStreamWaitEvent(su, aux->fork, 0));
     }
+    // an early error return still joins the side stream back into st (nothing of this call keeps running
+    // on the workspace after it returns control of st)
+    struct JoinGuard {
+        DeviceState::Aux* a; cudaStream_t st, su; bool recorded = false, joined = false;
+        ~JoinGuard() {
+            if (!a) return;
+            if (!recorded) cudaEventRecord(a->join, su);
+            if (!joined) cudaStreamWaitEvent(st, a->join, 0);
+        }
+    } jg{aux, st, su};
     {
         ReduceArgs ra{};
         ra.src[0] = fuse ? (const void*)Ua : Sa; ra.src[1] = fuse ? (const void*)Ub : Sb;
@@ -283,7 +293,7 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
     }
     for (size_t i = fu.size() - 1; i-- > 0;)
         if ((s = launch_fft(fu[i], true, false, Ua, T.U, Ua, PU, ds, su, 1, umap)) != GF2X_OK) return s;
-    if (aux) CUDA_TRY(cudaEventRecord(aux->join, su));
+    if (aux) { CUDA_TRY(cudaEventRecord(aux->join, su)); jg.recorded = true; }
     // lower part: the H-point multiply of the full pipeline (changeRepr fused into its first pass)
     for (size_t i = fuse ? 1 : 0; i + 1 < fl.size(); i++)
         if ((s = lower_pass(i)) != GF2X_OK) return s;
@@ -310,7 +320,7 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
         ra.dst[0] = Wb;
         if ((s = reduce(false, ra, 1, st, fuse ? fl[0].k_lo - 1 : T.m - 2)) != GF2X_OK) return s;
     }
-    if (aux) CUDA_TRY(cudaStreamWaitEvent(st, aux->join, 0));
+    if (aux) { CUDA_TRY(cudaStreamWaitEvent(st, aux->join, 0)); jg.joined = true; }
     {
         ProfScope ps("k_xor_range", 48.0 * T.U, st);
         k_xor_range<<<grid_for(T.U, 256, smc, 8), 256, 0, st>>>(Ua - 0, Wb - 0, 0, T.U);
