@@ -91,3 +91,44 @@ def test_truncation_eligibility():
 def test_plan_rejects_empty():
     with pytest.raises(G.Gf2xError):
         G.gf2x_plan(0, 64)
+
+
+def lucas_terms(p):
+    return [q for q in range(p) if (q & p) == q]
+
+
+@pytest.mark.parametrize("ab,bb", SIZES + [(((1 << 16) + 5) * 64, 3 * 64), (((1 << 16) + (1 << 14)) * 64, 64),
+                                           (((1 << 16) + (1 << 14) + 1) * 64, 64), ((1 << 22) + 64, (1 << 22) + 64)])
+def test_split_conversion_plan(ab, bb):
+    # DESIGN.md R22: one product, a conversion length n in (2^p, 2^p + 2^j] with j <= p - 2 and 2^(p+1) >= 2^16
+    # units is split into a 2^p and a 2^j conversion
+    p = G.gf2x_plan(ab, bb)
+    na, nb = (ab + 63) // 64, (bb + 63) // 64
+
+    def want(n, mfull):
+        if mfull < 16 or n <= 1 << (mfull - 1):
+            return None
+        j = max(0, (n - (1 << (mfull - 1)) - 1).bit_length())
+        return [mfull - 1, j] if j <= mfull - 3 else None
+
+    assert p["split"]["a"] == want(na, p["ma"])
+    assert p["split"]["b"] == want(nb, p["mb"])
+    assert p["split"]["icvt"] == want(na + nb - 1, p["m"])
+
+
+def test_split_fold_targets_stay_in_the_lower_half():
+    # the s_p shift terms x^(2^q), q a proper subset of p, move a tail of 2^j (j <= p - 2) to [2^q, 2^q + 2^j),
+    # below 2^p for every p (so the two conversions stay independent)
+    for p in range(15, 33):
+        for q in lucas_terms(p):
+            assert (1 << q) + (1 << (p - 2)) <= 1 << p
+
+
+@pytest.mark.parametrize("bits", [(1 << 23) + 192, (1 << 24) + 64, (1 << 28) + 64, (1 << 28) + (1 << 23)])
+def test_truncated_launch_count_is_consistent(bits):
+    # the truncated path launches fewer kernels' worth of work than the full transform but at least its lower
+    # half's passes; the count is what bench.py reports as gpu_launches (checked against the profiler on the GPU)
+    n = G.gf2x_launch_count(bits, bits)
+    p = G.gf2x_plan(bits, bits)
+    assert p["trunc_j"] >= 12
+    assert 20 <= n <= 60
