@@ -115,15 +115,31 @@ static void launch_trunc_reduce(bool psi, const ReduceArgs& ra, int nops, uint64
     else k_trunc_reduce<NL, false><<<g, 256, 0, st>>>(ra, nops, Q, tabs);
 }
 
+// an operand reaching past H: h = a_lo + a_hi on the upper half, and Reduce leaves a_hi (support < 2^j) alone,
+// so its changeRepr'ed tail is added to the reduced 2^j elements: U[i] ^= psi(S[H + i]), i < r
+__global__ void __launch_bounds__(256) k_trunc_addhi(const uint64_t* __restrict__ S, uint64_t r, const DevTables* __restrict__ tabs,
+                                                     uint4* __restrict__ U) {
+    __shared__ uint4 psit[8 * 256];
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) psit[i] = tabs->psi64[i];
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < r; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t w = S[i];
+        uint4 v = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int ch = 0; ch < 8; ch++) v = xor4(v, psit[ch * 256 + ((w >> (8 * ch)) & 255)]);
+        U[i] = xor4(U[i], v);
+    }
+}
+
 struct TruncGeom {
     int m, j;          // N = 2^m points, upper part 2^j
     uint64_t N, H, U;  // U = 2^j
 };
-// eligible: one product, both operands within the lower half, L - H <= 2^j with 12 <= j <= m - 2
+// eligible: one product, L - H <= 2^j with 12 <= j <= m - 2 (an operand longer than H has a tail of <= 2^j words)
 static bool trunc_geom(const Plan& P, TruncGeom& T) {
     if (env_flag("GF2X_NO_TRUNC") || P.batch != 1 || P.m < 14) return false;
     const uint64_t H = P.N / 2, L = P.na + P.nb - 1;
-    if (P.na > H || P.nb > H || L <= H) return false;
+    if (L <= H) return false;   // (an operand may reach past H: its tail is at most L - H <= 2^j words)
     int j = 12;
     while ((1ull << j) < L - H) j++;
     if (j > P.m - 2) return false;
@@ -164,6 +180,7 @@ static int launches_of_trunc(const Plan& P, const TruncGeom& T) {
     n += 3 * ((int)fl.size() - 1) + 1;                                     // lower: forward a, b, bottom, inverse
     n += 3 * ((int)fu.size() - 1) + 1;                                     // upper
     n += 2 * nred + 1;                                                     // Reduce (forward, g_lo), g_hi combine
+    n += (P.na > T.H) + (P.nb > T.H);                                      // operand tails past H
     n += launches_of_split(P.ic, P.icvt) + 1;                              // iBasisCvt, changeRepr^-1 + combine
     return n;
 }
@@ -277,6 +294,12 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
         ra.s_per[0] = 1ull << P.ma; ra.s_per[1] = 1ull << P.mb;
         ra.dst[0] = Ua; ra.dst[1] = Ub;
         if ((s = reduce(!fuse, ra, 2, su, fuse ? fl[0].k_lo - 1 : T.m - 2)) != GF2X_OK) return s;
+    }
+    for (int o = 0; o < 2; o++) {   // operand tails past H
+        const uint64_t n = o ? P.nb : P.na;
+        if (n <= T.H) continue;
+        ProfScope ps("k_trunc_addhi", (double)(n - T.H) * 40, su);
+        k_trunc_addhi<<<grid_for(n - T.H, 256, smc, 4), 256, 0, su>>>((o ? Sb : Sa) + T.H, n - T.H, ds->tabs, o ? Ub : Ua);
     }
     for (size_t i = 0; i + 1 < fu.size(); i++) {
         if ((s = launch_fft(fu[i], false, false, Ua, T.U, Ua, PU, ds, su, 1, umap)) != GF2X_OK) return s;

@@ -40,7 +40,10 @@ def gpu_mul(a, ab, b, bb, profile=False):
 
 @pytest.mark.parametrize("ab,bb", [((1 << 20) + 64, (1 << 20) + 64), ((1 << 20) + 1, (1 << 20) + 65), (1 << 20, (1 << 20) + 3000),
                                    ((1 << 20) + 64 * 4095, (1 << 20) + 7), ((1 << 19) + 999, (1 << 21) - 64 * 100),
-                                   ((1 << 22) + 1, (1 << 22) + 1)])
+                                   ((1 << 22) + 1, (1 << 22) + 1),
+                                   # one operand reaching past H (its tail joins the upper part unreduced)
+                                   ((1 << 20) + 128, 3000), (3000, (1 << 20) + 128), ((1 << 20) + 64 * 4000, 64 * 90 - 5),
+                                   ((1 << 22) + 64 * 3, 64 * 4000)])
 def test_truncated_products_exact(ab, bb):
     a, b = operand(ab, seed=ab % 1000 + 1), operand(bb, seed=bb % 1000 + 2)
     got, names = gpu_mul(a, ab, b, bb, profile=True)

@@ -84,8 +84,10 @@ def test_truncation_eligibility():
     p = G.gf2x_plan((1 << 28) + (1 << 23), (1 << 28) + (1 << 23))
     assert p["trunc_j"] == 18   # L - H = 2^18 - 1
     assert G.gf2x_plan(1 << 29, 1 << 29)["trunc_j"] == -1          # exact power of two
-    assert G.gf2x_plan((1 << 28) + 64, 1 << 10)["trunc_j"] == -1   # L <= H
-    assert G.gf2x_plan((1 << 29) + 64, 64)["trunc_j"] == -1        # an operand beyond the lower half
+    assert G.gf2x_plan((1 << 28) + 64, 1 << 10)["trunc_j"] == 12    # a = H + 1 words, b short
+    assert G.gf2x_plan((1 << 28) - 64 * 16, 1 << 10)["trunc_j"] == -1   # L = 2^22 - 1: L - H = 2^21 - 1, too far above H
+    assert G.gf2x_plan((1 << 29) + 64, 64)["trunc_j"] == 12        # an operand reaching past H by a short tail
+    assert G.gf2x_plan((1 << 28) + 64 * 5000, 64)["trunc_j"] == 13
 
 
 def test_plan_rejects_empty():
