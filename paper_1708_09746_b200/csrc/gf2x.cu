@@ -589,7 +589,12 @@ static std::vector<CvtPass> plan_cvt_ops(const std::vector<CvtOp>& ops, int m, i
     for (size_t oi = 0; oi < ops.size(); oi++) {
         const CvtOp& op = ops[oi];
         const int wlo = op.lg - 1 - op.K, whi = op.lg;
-        const bool res8 = op.K == 8 && !env_flag("GF2X_NO_RES8");   // K=8 runs also as residue passes (measured faster than 2 tile passes)
+        // K=8 runs also as residue passes (measured faster than 2 tile passes); a lone K=8 step that fits a tile
+        // (the top step of a 2^9-unit product) stays in the tile passes
+        bool res8 = op.K == 8 && !env_flag("GF2X_NO_RES8");
+        if (res8 && fits(wlo, whi) && !(oi + 1 < ops.size() && ops[oi + 1].K == 8 && ops[oi + 1].lg == op.lg - 1) &&
+            !env_flag("GF2X_RES8_SINGLE"))
+            res8 = false;
         if ((!fits(wlo, whi) || res8) && op.lg <= 31) {
             // a run of same-K steps at descending levels whose windows exceed a tile: one
             // residue-class pass if the rows of a class fit shared memory (else this step streams)
