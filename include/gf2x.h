@@ -97,6 +97,13 @@ gf2x_status gf2x_mul_alg4(const uint64_t* a, uint64_t a_bits, const uint64_t* b,
 gf2x_status gf2x_debug_stage_alg4(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, int stage,
                                   uint64_t* out, void* stream);
 
+/* App. C, its first step: BasisCvt (Alg. 3 P:518-539 with Alg. 2
+ * P:492-511; inverse if `inverse` != 0) on 2^M GF(2) coefficients, "proceeded straightforwardly with alg. 3"
+ * (P:1523).  words: DEVICE, caller-owned, 2^(M-6) words, coefficient t = bit t % 64 of word t / 64 (the
+ * packing of gf2x_mul's operands), converted in place; on return (stream-ordered) word bits are the
+ * novel-basis coefficients g_t with f(x) = sum_t g_t X_t(x).  6 <= M <= 40, else GF2X_EINVAL. */
+gf2x_status gf2x_basis_cvt_bits(uint64_t* words, int M, int inverse, void* stream);
+
 /* ---------------------------------------------------------------------------------------------
  * Multi-GPU: the FFT partitioned across G = nranks ranks, one process per GPU (the
  * decomposition is described in DESIGN.md §9).  NCCL is loaded at run time (libnccl.so.2).

@@ -85,6 +85,7 @@ def lib():
             "or_fft256": (None, [_u64p, i32]),
             "or_alg5_mul_w128": (i32, [_u64p, u64, _u64p, u64, _u64p] + [_u64p] * 4),
             "or_frob_eval": (i32, [_u64p, u64, i32, _u64p, i32]),
+            "or_basis_cvt_bits": (None, [_u64p, i32, i32]),
             "or_frob_columns": (None, [i32, _u64p]),
             "or_frob_m": (i32, [u64, u64]),
             "or_frob_mul": (i32, [_u64p, u64, _u64p, u64, _u64p]),
@@ -316,6 +317,14 @@ def alg4_mul(a: np.ndarray, a_bits: int, b: np.ndarray, b_bits: int, stages: boo
 
 
 # ---------------------------------------------------------------- O3, App. C (Frobenius bijection)
+def basis_cvt_bits(words: np.ndarray, M: int, inverse: bool = False) -> np.ndarray:
+    """Alg. 3 BasisCvt (or its inverse) on 2^M GF(2) coefficients packed in 2^(M-6) words; a new array."""
+    w = np.array(words, dtype=np.uint64, copy=True).reshape(-1)
+    assert M >= 6 and len(w) == 1 << (M - 6)
+    lib().or_basis_cvt_bits(_p(w), M, 1 if inverse else 0)
+    return w
+
+
 def frob_m(a_bits: int, b_bits: int) -> int:
     """log2 of the number of evaluation points the Frobenius multiply uses (128 * 2^m >= a_bits + b_bits - 1)."""
     return lib().or_frob_m(a_bits, b_bits)

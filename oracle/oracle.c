@@ -675,6 +675,17 @@ static void icvt8(uint8_t *f, size_t base, int m, int sigma) {
             itaylor8(f, base + s, (size_t)1 << (l + sigma), K);
 }
 
+/* BasisCvt / iBasisCvt on 2^M GF(2) coefficients packed little-endian in 2^(M-6) words (M >= 6), in place */
+void or_basis_cvt_bits(uint64_t *words, int M, int inverse) {
+    size_t NB = (size_t)1 << M;
+    uint8_t *g = (uint8_t *)malloc(NB);
+    for (size_t i = 0; i < NB; i++) g[i] = (words[i / 64] >> (i % 64)) & 1;
+    if (inverse) icvt8(g, 0, M, 0); else cvt8(g, 0, M, 0);
+    memset(words, 0, (NB / 64) * sizeof(uint64_t));
+    for (size_t i = 0; i < NB; i++) if (g[i]) words[i / 64] |= (uint64_t)1 << (i % 64);
+    free(g);
+}
+
 /* FFT_LCH / iFFT at displacement alpha: block b of layer k multiplies by s_k(alpha + phi(b)) =
  * s_k(alpha) + s_k(phi(b)) (s_k is linear) -- the alpha = 0 constants plus one per layer */
 static void fft_alpha(u128 *A, int m, u128 **C, const u128 *sa, int inverse) {

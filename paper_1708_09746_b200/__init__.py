@@ -24,7 +24,7 @@ EXPORTS = [
     "gf2x_debug_stage", "gf2x_comm_unique_id", "gf2x_comm_init", "gf2x_comm_destroy", "gf2x_mul_sharded",
     "gf2x_mul_sharded_sim", "gf2x_debug_shard_stage", "gf2x_shard_plan", "gf2x_profile_enable", "gf2x_profile_report", "gf2x_status_string", "gf2x_last_error",
     "gf2x_release", "gf2x_version", "gf2x_mul_w", "gf2x_launch_count_w", "gf2x_debug_stage_w128",
-    "gf2x_comm_peer_memory", "gf2x_mul_alg4", "gf2x_debug_stage_alg4", "gf2x_plan",
+    "gf2x_comm_peer_memory", "gf2x_mul_alg4", "gf2x_debug_stage_alg4", "gf2x_plan", "gf2x_basis_cvt_bits",
 ]
 
 
@@ -58,6 +58,8 @@ def load(path: str = LIB_PATH):
     L.gf2x_debug_stage_w128.restype = i32
     L.gf2x_mul_alg4.argtypes = [vp, u64, vp, u64, vp, i64, vp]
     L.gf2x_mul_alg4.restype = i32
+    L.gf2x_basis_cvt_bits.argtypes = [vp, i32, i32, vp]
+    L.gf2x_basis_cvt_bits.restype = i32
     L.gf2x_debug_stage_alg4.argtypes = [vp, u64, vp, u64, i32, vp, vp]
     L.gf2x_debug_stage_alg4.restype = i32
     L.gf2x_status_string.argtypes = [i32]
@@ -154,6 +156,12 @@ def gf2x_debug_stage_w128(a, a_bits: int, b, b_bits: int, stage: int, stream=Non
     out = torch.empty(N, 4, dtype=torch.uint64, device=a.device)
     _check(load().gf2x_debug_stage_w128(_ptr(a), a_bits, _ptr(b), b_bits, stage, _ptr(out), _stream_ptr(stream)))
     return out
+
+
+def gf2x_basis_cvt_bits(words, M: int, inverse: bool = False, stream=None):
+    """App. C's BasisCvt on 2^M GF(2) coefficients packed in a CUDA word tensor (2^(M-6) words), in place."""
+    _check(load().gf2x_basis_cvt_bits(_ptr(words), M, 1 if inverse else 0, _stream_ptr(stream)))
+    return words
 
 
 def gf2x_mul_alg4(a, a_bits: int, b, b_bits: int, batch: int = 1, c=None, stream=None):

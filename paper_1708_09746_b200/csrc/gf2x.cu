@@ -1157,6 +1157,7 @@ static gf2x_status mul_common(const uint64_t* a, uint64_t a_bits, const uint64_t
 #include "w128.cuh"
 #include "alg4.cuh"
 #include "trunc.cuh"
+#include "frob.cuh"
 
 extern "C" {
 
@@ -1230,6 +1231,15 @@ gf2x_status gf2x_debug_stage_alg4(const uint64_t* a, uint64_t a_bits, const uint
     if (stage != 2 && stage != 3) return fail(GF2X_EINVAL, "stage must be 2 or 3");
     if (!out || a_bits == 0 || b_bits == 0) return fail(GF2X_EINVAL, "null output or empty operand");
     return mul_common(a, a_bits, b, b_bits, nullptr, 1, nullptr, 0, stream, stage, out, 4);
+}
+
+gf2x_status gf2x_basis_cvt_bits(uint64_t* words, int M, int inverse, void* stream) {
+    if (!words || M < 6 || M > 40) return fail(GF2X_EINVAL, "bit-level BasisCvt needs 6 <= M <= 40 and a buffer");
+    int dev;
+    DeviceState* ds;
+    gf2x_status s = get_device(&dev, &ds);
+    if (s != GF2X_OK) return s;
+    return run_bitcvt(words, M, inverse != 0, ds->sm_count, (cudaStream_t)stream);
 }
 
 gf2x_status gf2x_comm_unique_id(void* id_out) {

@@ -134,3 +134,24 @@ def test_frobenius_order_of_alpha(m):
         if i == 64:
             assert x != alpha
     assert x == alpha
+
+
+@pytest.mark.parametrize("M", [6, 7, 9])
+def test_bit_level_basis_cvt_is_the_novel_basis_expansion(M):
+    # f(alpha) = sum_i g_i X_i(alpha) with X_i = prod_{bit k of i} s_k (Cantor-normalised novel basis),
+    # at random tower points alpha; and the inverse returns f
+    f = operand(1 << M, seed=M)
+    g = O.basis_cvt_bits(f, M)
+    assert np.array_equal(O.basis_cvt_bits(g, M, inverse=True), f)
+    for t in range(3):
+        alpha = R.getrandbits(128)
+        s = [O.s_eval(k, alpha) for k in range(M)]
+        acc = 0
+        for i in range(1 << M):
+            if (int(g[i // 64]) >> (i % 64)) & 1:
+                x = 1
+                for k in range(M):
+                    if (i >> k) & 1:
+                        x = O.tower_mul(x, s[k])
+                acc ^= x
+        assert acc == horner_bits(f, 1 << M, alpha), t
