@@ -103,6 +103,13 @@ gf2x_status gf2x_debug_stage_alg4(const uint64_t* a, uint64_t a_bits, const uint
  * packing of gf2x_mul's operands), converted in place; on return (stream-ordered) word bits are the
  * novel-basis coefficients g_t with f(x) = sum_t g_t X_t(x).  6 <= M <= 40, else GF2X_EINVAL. */
 gf2x_status gf2x_basis_cvt_bits(uint64_t* words, int M, int inverse, void* stream);
+/* App. C: c = a * b through the Frobenius bijection E_(beta_(m+64) + V_m), no Kronecker
+ * segmentation: 2^m evaluation points with 128 * 2^m >= a_bits + b_bits - 1 (R23), FFT_LCH in the
+ * polynomial basis with the displacement alpha = beta_(m+64).  Same operand / output packing and error
+ * contract as gf2x_mul (a, b, c DEVICE; c receives ceil(a_bits/64) + ceil(b_bits/64) words; a zero-length
+ * operand gives a zero product); its workspace comes from the stream-ordered allocator.  m <= 26, else
+ * GF2X_ETOOBIG.  Exact; a comparison variant of the product path (slower on B200: DESIGN.md §10d). */
+gf2x_status gf2x_mul_frob(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
  * Multi-GPU: the FFT partitioned across G = nranks ranks, one process per GPU (the

@@ -25,6 +25,7 @@ EXPORTS = [
     "gf2x_mul_sharded_sim", "gf2x_debug_shard_stage", "gf2x_shard_plan", "gf2x_profile_enable", "gf2x_profile_report", "gf2x_status_string", "gf2x_last_error",
     "gf2x_release", "gf2x_version", "gf2x_mul_w", "gf2x_launch_count_w", "gf2x_debug_stage_w128",
     "gf2x_comm_peer_memory", "gf2x_mul_alg4", "gf2x_debug_stage_alg4", "gf2x_plan", "gf2x_basis_cvt_bits",
+    "gf2x_mul_frob",
 ]
 
 
@@ -60,6 +61,8 @@ def load(path: str = LIB_PATH):
     L.gf2x_mul_alg4.restype = i32
     L.gf2x_basis_cvt_bits.argtypes = [vp, i32, i32, vp]
     L.gf2x_basis_cvt_bits.restype = i32
+    L.gf2x_mul_frob.argtypes = [vp, u64, vp, u64, vp, vp]
+    L.gf2x_mul_frob.restype = i32
     L.gf2x_debug_stage_alg4.argtypes = [vp, u64, vp, u64, i32, vp, vp]
     L.gf2x_debug_stage_alg4.restype = i32
     L.gf2x_status_string.argtypes = [i32]
@@ -156,6 +159,15 @@ def gf2x_debug_stage_w128(a, a_bits: int, b, b_bits: int, stage: int, stream=Non
     out = torch.empty(N, 4, dtype=torch.uint64, device=a.device)
     _check(load().gf2x_debug_stage_w128(_ptr(a), a_bits, _ptr(b), b_bits, stage, _ptr(out), _stream_ptr(stream)))
     return out
+
+
+def gf2x_mul_frob(a, a_bits: int, b, b_bits: int, c=None, stream=None):
+    """App. C: c = a * b through the Frobenius bijection (same packing as gf2x_mul); returns c."""
+    import torch
+    if c is None:
+        c = torch.empty(nwords(a_bits) + nwords(b_bits), dtype=torch.uint64, device=a.device)
+    _check(load().gf2x_mul_frob(_ptr(a), a_bits, _ptr(b), b_bits, _ptr(c), _stream_ptr(stream)))
+    return c
 
 
 def gf2x_basis_cvt_bits(words, M: int, inverse: bool = False, stream=None):

@@ -97,6 +97,7 @@ struct A4Params {
     const uint4* src;
     uint4* dst;
     const uint4* D;
+    const uint4* alpha;   // null, or per layer k the displacement term psi^-1(s_k(alpha)) (App. C, frob.cuh)
     uint64_t N, batch;
     int m, c, k_lo, k_hi;
 };
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(A4_THREADS) k_fft_a4(A4Params p) {
                 const uint32_t blk = id + 1 - (1u << lg);
                 const uint32_t lb = (uint32_t)(((uint64_t)base & ~((2ull << k) - 1)) | ((uint64_t)blk << (k + 1)));
                 a4u128 cc = a4_const(p.D, k, lb);
+                if (p.alpha) cc ^= a4_from(p.alpha[k]);   // s_k(alpha + phi(b)) = s_k(alpha) + s_k(phi(b))
 #pragma unroll
                 for (int i = 0; i < 4; i++) { cz[id * 4 + i] = a4_to(cc); cc = a4_mulz(cc, 1); }
             }
@@ -274,9 +276,9 @@ static std::vector<A4Pass> plan_a4(int m) {
 }
 
 static gf2x_status launch_a4(const A4Pass& f, bool inv, uint4* W, uint64_t N, int m, uint64_t batch, const DevTablesA4* T,
-                             int smc, cudaStream_t st) {
+                             int smc, cudaStream_t st, const uint4* alpha = nullptr) {
     A4Params prm;
-    prm.src = W; prm.dst = W; prm.D = T->D;
+    prm.src = W; prm.dst = W; prm.D = T->D; prm.alpha = alpha;
     prm.N = N; prm.batch = batch; prm.m = m; prm.c = f.c; prm.k_lo = f.k_lo; prm.k_hi = f.k_hi;
     const int R = f.k_hi - f.k_lo;
     const size_t sm = (((size_t)1 << R) - 1) * ((f.dense ? 512 : 16) + 4) * 16 + ((size_t)1 << (f.c + R)) * 16;

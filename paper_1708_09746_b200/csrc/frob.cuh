@@ -54,3 +54,192 @@ static gf2x_status run_bitcvt(uint64_t* G, int M, bool inverse, int smc, cudaStr
     }
     return check_launch("bit-level BasisCvt");
 }
+
+// ---------------------------------------------------------------------------------------------
+// The multiply through the Frobenius bijection E_(beta_(m+64) + V_m) (App. C; R23), in the
+// polynomial basis of GF(2^128) so that Alg. 4's dense-multiplier FFT passes serve (alg4.cuh, with the
+// displacement term psi^-1(s_k(alpha)) per layer): every evaluation is psi^-1 of the tower value, which
+// the field isomorphism carries through the products.
+//   bits of a, b -> bit-level BasisCvt (2^(m+7) coefficients) -> encoding e_i = sum_j g[i + j n] C'_j
+//   (C'_j = psi^-1 of the 7-layer columns) -> n-point FFT at alpha -> pointmul -> iFFT ->
+//   decoding (the inverse of the 128 x 128 map) -> bit scatter -> bit-level iBasisCvt -> the product bits.
+// The kernels here are the plain forms (one thread per element / word); DESIGN.md §11 has what is next.
+// ---------------------------------------------------------------------------------------------
+// constants of one m: [m] psi^-1(s_k(alpha)), [128] columns C'_j, [128] columns of the inverse map
+struct FrobConsts {
+    uint4 v[32 + 128 + 128];
+};
+#define FROB_ALPHA 0
+#define FROB_COLS 32
+#define FROB_INV 160
+
+__global__ void __launch_bounds__(256) k_frob_encode(const uint64_t* __restrict__ G, int m, const uint4* __restrict__ cols,
+                                                     uint4* __restrict__ W) {
+    __shared__ uint4 C[128];
+    if (threadIdx.x < 128) C[threadIdx.x] = cols[threadIdx.x];
+    __syncthreads();
+    const uint64_t n = 1ull << m;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint4 x = make_uint4(0, 0, 0, 0);
+        for (int j = 0; j < 128; j++) {
+            const uint64_t p = i + ((uint64_t)j << m);
+            if ((__ldg(G + (p >> 6)) >> (p & 63)) & 1) x = xor4(x, C[j]);
+        }
+        W[i] = x;
+    }
+}
+__global__ void __launch_bounds__(256) k_frob_decode(const uint4* __restrict__ E, uint64_t n, const uint4* __restrict__ inv,
+                                                     uint4* __restrict__ Dv) {
+    __shared__ uint4 C[128];
+    if (threadIdx.x < 128) C[threadIdx.x] = inv[threadIdx.x];
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 e = E[i];
+        const uint32_t w[4] = {e.x, e.y, e.z, e.w};
+        uint4 y = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int l = 0; l < 4; l++)
+            for (int b = 0; b < 32; b++)
+                if ((w[l] >> b) & 1) y = xor4(y, C[32 * l + b]);
+        Dv[i] = y;
+    }
+}
+// G[w] bit b = bit j of Dv[i] for the coefficient position p = 64 w + b = i + j n
+__global__ void __launch_bounds__(256) k_frob_scatter(const uint4* __restrict__ Dv, int m, uint64_t* __restrict__ G, uint64_t nw) {
+    const uint64_t nmask = (1ull << m) - 1;
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t v = 0;
+        for (int b = 0; b < 64; b++) {
+            const uint64_t p = (w << 6) + b, i = p & nmask;
+            const uint32_t j = (uint32_t)(p >> m);
+            const uint4 d = Dv[i];
+            const uint32_t limb = j < 32 ? d.x : (j < 64 ? d.y : (j < 96 ? d.z : d.w));
+            v |= (uint64_t)((limb >> (j & 31)) & 1) << b;
+        }
+        G[w] = v;
+    }
+}
+
+static bool gf2_inverse128_host(const gf2x_host::u128* col, gf2x_host::u128* out) {
+    using gf2x_host::u128;
+    u128 A[128], I[128];
+    for (int r = 0; r < 128; r++) {
+        u128 v = 0;
+        for (int j = 0; j < 128; j++) if ((col[j] >> r) & 1) v |= (u128)1 << j;
+        A[r] = v; I[r] = (u128)1 << r;
+    }
+    for (int c = 0; c < 128; c++) {
+        int p = -1;
+        for (int r = c; r < 128; r++) if ((A[r] >> c) & 1) { p = r; break; }
+        if (p < 0) return false;
+        std::swap(A[p], A[c]); std::swap(I[p], I[c]);
+        for (int r = 0; r < 128; r++) if (r != c && ((A[r] >> c) & 1)) { A[r] ^= A[c]; I[r] ^= I[c]; }
+    }
+    for (int j = 0; j < 128; j++) {
+        u128 v = 0;
+        for (int r = 0; r < 128; r++) if ((I[r] >> j) & 1) v |= (u128)1 << r;
+        out[j] = v;
+    }
+    return true;
+}
+
+static gf2x_status get_frob_consts(DeviceState* ds, int m, const uint4** out) {
+    using namespace gf2x_host;
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = ds->frob.find(m);
+    if (it != ds->frob.end()) { *out = it->second; return GF2X_OK; }
+    const Isomorphism iso = build_isomorphism();
+    auto to_poly = [&](u128 x) { u128 r = 0; for (int i = 0; i < 128; i++) if ((x >> i) & 1) r ^= iso.towerToPoly[i]; return r; };
+    auto to4 = [](u128 v) { return make_uint4((uint32_t)v, (uint32_t)(v >> 32), (uint32_t)(v >> 64), (uint32_t)(v >> 96)); };
+    FrobConsts h;
+    memset(&h, 0, sizeof(h));
+    const u128 alpha = (u128)1 << (m + 64);
+    u128 sk = alpha, s7[7];
+    for (int k = 0; k < m + 7; k++) {            // sk = s_k(alpha)
+        if (k < m) h.v[FROB_ALPHA + k] = to4(to_poly(sk));
+        else s7[k - m] = sk;
+        sk = s1(sk);
+    }
+    u128 colp[128], inv[128];
+    for (int j = 0; j < 128; j++) {               // C_j = prod_{bit b of j} s_(m+b)(alpha) (the 7 layers' images)
+        u128 c = 1;
+        for (int b = 0; b < 7; b++) if ((j >> b) & 1) c = tower_mul(c, s7[b]);
+        colp[j] = to_poly(c);
+        h.v[FROB_COLS + j] = to4(colp[j]);
+    }
+    if (!gf2_inverse128_host(colp, inv)) return fail(GF2X_EINVAL, "App. C encoding map is singular");
+    for (int j = 0; j < 128; j++) h.v[FROB_INV + j] = to4(inv[j]);
+    uint4* d = nullptr;
+    if (cudaMalloc(&d, sizeof(FrobConsts)) != cudaSuccess) return fail(GF2X_ENOMEM, "App. C constants");
+    if (cudaMemcpy(d, &h, sizeof(FrobConsts), cudaMemcpyHostToDevice) != cudaSuccess) { cudaFree(d); return fail(GF2X_ECUDA, "App. C constants"); }
+    ds->frob[m] = d;
+    *out = d;
+    return GF2X_OK;
+}
+
+static int frob_m_of(uint64_t L) { int m = 0; while (((uint64_t)128 << m) < L) m++; return m; }
+
+static gf2x_status run_frob_mul(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
+                                DeviceState* ds, cudaStream_t st) {
+    const uint64_t na = (a_bits + 63) / 64, nb = (b_bits + 63) / 64;
+    if (a_bits == 0 || b_bits == 0) {
+        if (na + nb) CUDA_TRY(cudaMemsetAsync(c, 0, (na + nb) * 8, st));
+        return GF2X_OK;
+    }
+    const int m = frob_m_of(a_bits + b_bits - 1), M = m + 7;
+    if (m > 26) return fail(GF2X_ETOOBIG, "App. C multiply: more than 2^26 points");
+    const uint64_t n = 1ull << m, nw = 1ull << (M - 6);
+    const uint4* K;
+    DevTablesA4* TA;
+    gf2x_status s;
+    if ((s = get_frob_consts(ds, m, &K)) != GF2X_OK) return s;
+    if ((s = get_tablesA4(ds, &TA)) != GF2X_OK) return s;
+    void* ws = nullptr;
+    const size_t bytes = 2 * nw * 8 + 2 * n * 16;
+    CUDA_TRY(cudaMallocAsync(&ws, bytes, st));
+    uint64_t* Ga = reinterpret_cast<uint64_t*>(ws);
+    uint64_t* Gb = Ga + nw;
+    uint4* Wa = reinterpret_cast<uint4*>(Gb + nw);
+    uint4* Wb = Wa + n;
+    const int smc = ds->sm_count;
+    auto body = [&]() -> gf2x_status {
+        gf2x_status r;
+        {
+            ProfScope ps("k_prep", 16.0 * nw, st);
+            k_prep<<<grid_for(nw, 256, smc, 8), 256, 0, st>>>(a, na, a_bits, M - 6, 1, Ga);
+            k_prep<<<grid_for(nw, 256, smc, 8), 256, 0, st>>>(b, nb, b_bits, M - 6, 1, Gb);
+        }
+        if ((r = run_bitcvt(Ga, M, false, smc, st)) != GF2X_OK) return r;
+        if ((r = run_bitcvt(Gb, M, false, smc, st)) != GF2X_OK) return r;
+        {
+            ProfScope ps("k_frob_encode", 2.0 * (16.0 * n + 16.0 * n), st);
+            k_frob_encode<<<grid_for(n, 256, smc, 8), 256, 0, st>>>(Ga, m, K + FROB_COLS, Wa);
+            k_frob_encode<<<grid_for(n, 256, smc, 8), 256, 0, st>>>(Gb, m, K + FROB_COLS, Wb);
+        }
+        const std::vector<A4Pass> passes = plan_a4(m);
+        for (const A4Pass& f : passes)   // Wa | Wb contiguous: both in one launch per pass
+            if ((r = launch_a4(f, false, Wa, n, m, 2, TA, smc, st, K + FROB_ALPHA)) != GF2X_OK) return r;
+        {
+            ProfScope ps("k_a4_pointmul", 48.0 * n, st);
+            k_a4_pointmul<<<grid_for(n, 128, smc, 8), 128, 0, st>>>(Wa, Wb, n);
+        }
+        for (size_t i = passes.size(); i-- > 0;)
+            if ((r = launch_a4(passes[i], true, Wa, n, m, 1, TA, smc, st, K + FROB_ALPHA)) != GF2X_OK) return r;
+        {
+            ProfScope ps("k_frob_decode", 32.0 * n, st);
+            k_frob_decode<<<grid_for(n, 256, smc, 8), 256, 0, st>>>(Wa, n, K + FROB_INV, Wb);
+        }
+        {
+            ProfScope ps("k_frob_scatter", 8.0 * nw + 16.0 * n, st);
+            k_frob_scatter<<<grid_for(nw, 256, smc, 8), 256, 0, st>>>(Wb, m, Ga, nw);
+        }
+        if ((r = run_bitcvt(Ga, M, true, smc, st)) != GF2X_OK) return r;
+        const uint64_t ncopy = std::min<uint64_t>(na + nb, nw);
+        CUDA_TRY(cudaMemcpyAsync(c, Ga, ncopy * 8, cudaMemcpyDeviceToDevice, st));
+        if (na + nb > ncopy) CUDA_TRY(cudaMemsetAsync(c + ncopy, 0, (na + nb - ncopy) * 8, st));
+        return check_launch("App. C multiply");
+    };
+    s = body();
+    cudaFreeAsync(ws, st);
+    return s;
+}

@@ -389,6 +389,7 @@ struct DeviceState {
     DevTables* host = nullptr;   // host copy (multiplier images for host-side constants)
     struct DevTables256* tabs256 = nullptr;   // w = 128 tables (w128.cuh), built on first use
     struct DevTablesA4* tabsA4 = nullptr;     // Alg. 4 tables (alg4.cuh), built on first use
+    std::map<int, uint4*> frob;               // App. C constants per m (frob.cuh), built on first use
     void* shard_ws = nullptr;    // simulation workspace (gf2x_mul_sharded_sim)
     size_t shard_ws_bytes = 0;
     int sm_count = 0;
@@ -1233,6 +1234,15 @@ gf2x_status gf2x_debug_stage_alg4(const uint64_t* a, uint64_t a_bits, const uint
     return mul_common(a, a_bits, b, b_bits, nullptr, 1, nullptr, 0, stream, stage, out, 4);
 }
 
+gf2x_status gf2x_mul_frob(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c, void* stream) {
+    if ((a_bits && !a) || (b_bits && !b) || !c) return fail(GF2X_EINVAL, "null pointer");
+    int dev;
+    DeviceState* ds;
+    gf2x_status s = get_device(&dev, &ds);
+    if (s != GF2X_OK) return s;
+    return run_frob_mul(a, a_bits, b, b_bits, c, ds, (cudaStream_t)stream);
+}
+
 gf2x_status gf2x_basis_cvt_bits(uint64_t* words, int M, int inverse, void* stream) {
     if (!words || M < 6 || M > 40) return fail(GF2X_EINVAL, "bit-level BasisCvt needs 6 <= M <= 40 and a buffer");
     int dev;
@@ -1576,6 +1586,7 @@ gf2x_status gf2x_release(int device) {
     if (it->second.shard_ws) cudaFree(it->second.shard_ws);
     if (it->second.tabs256) cudaFree(it->second.tabs256);
     if (it->second.tabsA4) cudaFree(it->second.tabsA4);
+    for (auto& f : it->second.frob) cudaFree(f.second);
     delete it->second.host;
     g_dev.erase(it);
     cudaSetDevice(cur);
