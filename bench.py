@@ -192,11 +192,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--w", type=int, default=64, choices=[64, 128],
                     help="Alg. 5 block width: 64 (TGF(2^128), default) or 128 (TGF(2^256), P:873-874)")
-    ap.add_argument("--alg", type=int, default=5, choices=[5, 4],
-                    help="5: Alg. 5 over the tower (default); 4: Alg. 4 in GF(2^128) polynomial basis (P:562-614)")
+    ap.add_argument("--alg", default="5", choices=["5", "4", "frob"],
+                    help="5: Alg. 5 over the tower (default); 4: Alg. 4 in GF(2^128) polynomial basis (P:562-614); "
+                         "frob: App. C, the Frobenius bijection (P:1485-1552; one product per step)")
     ap.add_argument("--mode", default=None, choices=["sharded", "replicas"],
                     help="N > 1: one multiply partitioned over the ranks (default) or one per rank")
     args = ap.parse_args()
+    args.alg = int(args.alg) if args.alg.isdigit() else args.alg
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
@@ -221,6 +223,9 @@ def main():
                               + (", split BasisCvt" if any(plan["split"].values()) else "") + ")")
         if args.mode is None and world > 1:
             args.mode = "replicas"
+    if args.alg == "frob" and (batch != 1 or args.w != 64):
+        print("[bench] --alg frob runs one product of 64-bit-word operands per step (no batch, w = 64)", file=sys.stderr)
+        return 2
     mode = args.mode or ("sharded" if world > 1 else "single")
     if world == 1:
         mode = "single"
@@ -278,6 +283,8 @@ def main():
     def step():
         if sharded:
             comm.mul(sa, sb, bits, sc, stream=stream)
+        elif args.alg == "frob":
+            G.gf2x_mul_frob(da, bits, db, bits, dc, stream=stream)
         elif args.alg == 4:
             G.gf2x_mul_alg4(da, bits, db, bits, batch, dc, stream=stream)
         elif args.w != 64:
@@ -389,6 +396,8 @@ def main():
         stream.wait_event(ev_out[k])           # step i-2's product has left EC[k]
         if sharded:
             comm.mul(EA[k], EB[k], bits, EC[k], stream=stream)
+        elif args.alg == "frob":
+            G.gf2x_mul_frob(EA[k], bits, EB[k], bits, EC[k], stream=stream)
         elif args.alg == 4:
             G.gf2x_mul_alg4(EA[k], bits, EB[k], bits, batch, EC[k], stream=stream)
         elif args.w != 64:
@@ -444,7 +453,7 @@ def main():
     step_bytes = sum(r["bytes"] for r in prof) / args.steps
     kern_ms = sum(r["ms"] for r in prof) / args.steps
     launches = G.gf2x_launch_count_w(bits, bits, batch, args.w)
-    if sharded or args.alg == 4:   # every kernel of the sharded path is bracketed by the profiling hook
+    if sharded or args.alg in (4, "frob"):   # every kernel of these paths is bracketed by the profiling hook
         launches = sum(r["launches"] for r in prof) // args.steps
 
     line = {
@@ -464,7 +473,8 @@ def main():
         "data": "synthetic",
         "config": {
             "workload": WORKLOAD[args.config] + ("" if args.w == 64 else ", w=128 blocks over TGF(2^256)")
-                        + ("" if args.alg == 5 else ", Alg. 4 (GF(2^128) polynomial basis, dense multipliers)"),
+                        + ("" if args.alg == 5 else (", Alg. 4 (GF(2^128) polynomial basis, dense multipliers)" if args.alg == 4
+                           else ", App. C multiply through the Frobenius bijection (no Kronecker segmentation)")),
             "config": args.config, "operand_bits": bits, "batch": batch, "block_width": args.w, "algorithm": args.alg,
             "fft_points": 1 << max(0, (2 * n - 2).bit_length()) >> (0 if args.w == 64 else 1),
             **({"trunc_j": G.gf2x_plan(bits, bits)["trunc_j"]} if args.config == "custom" else {}),
