@@ -107,7 +107,7 @@ gf2x_status gf2x_basis_cvt_bits(uint64_t* words, int M, int inverse, void* strea
  * segmentation: 2^m evaluation points with 128 * 2^m >= a_bits + b_bits - 1 (R23), FFT_LCH in the
  * polynomial basis with the displacement alpha = beta_(m+64).  Same operand / output packing and error
  * contract as gf2x_mul (a, b, c DEVICE; c receives ceil(a_bits/64) + ceil(b_bits/64) words; a zero-length
- * operand gives a zero product); its workspace comes from the stream-ordered allocator.  m <= 26, else
+ * operand gives a zero product); its workspace is the per-stream one gf2x_mul keeps.  m <= 26, else
  * GF2X_ETOOBIG.  Exact; a comparison variant of the product path (slower on B200: DESIGN.md §10d). */
 gf2x_status gf2x_mul_frob(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c, void* stream);
 

@@ -3,8 +3,8 @@
 // step of the multiply through the Frobenius bijection.  Included by gf2x.cu.
 //
 // The coefficients are packed 64 per word (bit t of the polynomial = bit t % 64 of word t / 64).  Alg. 3's
-// Taylor steps (Alg. 2, the same (lg, K) list as the word-level conversion, in the inner-first order of
-// DESIGN.md R14) act on bit positions: step (lg, K) on every segment of 2^lg bits, h = 2^(lg-1), u = h >> K,
+// Taylor steps (Alg. 2, the same (lg, K) list as the word-level conversion, in the paper's order) act on
+// bit positions: step (lg, K) on every segment of 2^lg bits, h = 2^(lg-1), u = h >> K,
 // d = h - u, "f[i - d] ^= f[i] for i = 2h-1 .. h" splits into two parallel sweeps (the targets of one sweep
 // are never its sources):
 //   sweep 1: targets [h, h + u)  (sources [2h - u, 2h));   sweep 2: targets [u, h)  (sources [h, 2h - u)),
@@ -14,17 +14,16 @@
 // forms of the word-level conversion are the next step for it.
 #pragma once
 
+// lg >= 7: only the words that hold targets are visited (ntw of every segment of 2^(lg-6) words)
 __global__ void __launch_bounds__(256) k_bitcvt_sweep(uint64_t* __restrict__ G, uint64_t nw, int lg, uint64_t d,
-                                                      uint64_t tlo, uint64_t thi, uint64_t pmask) {
-    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * blockDim.x) {
-        if (lg < 6) {   // segments inside the word: a periodic mask, sources in the same word
-            const uint64_t x = G[w];
-            G[w] = x ^ ((x >> d) & pmask);
-            continue;
-        }
-        const uint64_t len = 1ull << lg, o = (w << 6) & (len - 1);   // the word's offset in its segment
+                                                      uint64_t tlo, uint64_t thi) {
+    const uint64_t len = 1ull << lg, wps = len >> 6, tw0 = tlo >> 6, ntw = ((thi + 63) >> 6) - tw0;
+    const uint64_t total = (nw / wps) * ntw;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t seg = t / ntw, w = seg * wps + tw0 + (t - seg * ntw);
+        const uint64_t o = (w << 6) & (len - 1);   // the word's offset in its segment
         const uint64_t lo = tlo > o ? tlo - o : 0, hi = thi < o + 64 ? thi - o : 64;
-        if (thi <= o || tlo >= o + 64 || lo >= hi) continue;
+        if (lo >= hi) continue;
         const uint64_t mask = (hi >= 64 ? ~0ull : ((1ull << hi) - 1)) & ~((1ull << lo) - 1);
         const uint64_t sp = (w << 6) + d, w0 = sp >> 6;
         const int sh = (int)(sp & 63);
@@ -34,24 +33,88 @@ __global__ void __launch_bounds__(256) k_bitcvt_sweep(uint64_t* __restrict__ G, 
     }
 }
 
+// a run of steps whose segments lie inside one word (lg <= 6), applied to every word in registers
+struct InwordSweeps {
+    uint64_t pmask[64];
+    int d[64];
+    int n;
+};
+__global__ void __launch_bounds__(256) k_bitcvt_inword(uint64_t* __restrict__ G, uint64_t nw, InwordSweeps sw) {
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t x = G[w];
+        for (int k = 0; k < sw.n; k++) x ^= (x >> sw.d[k]) & sw.pmask[k];
+        G[w] = x;
+    }
+}
+
+// Alg. 3's steps in the paper's order (Taylor levels, outer conversion, inner conversions; the oracle's order)
+static void bit_ops(int m, int sigma, std::vector<CvtOp>& out) {
+    if (m <= 1) return;
+    int K = 1;
+    while (2 * K <= m - 1) K *= 2;
+    for (int l = m; l >= K + 1; --l) out.push_back({l + sigma, K});
+    bit_ops(m - K, sigma + K, out);
+    bit_ops(K, sigma, out);
+}
+
+// A step whose window [lg-1-K, lg) of index bits lies at or above bit 6 moves whole words: consecutive such
+// steps run as a word-level conversion (the planned res / rb / tile passes of the Alg. 5 path on the packed
+// words, step (lg - 6, K)); steps inside a word fuse into one in-register pass; the rest (windows across bit 6)
+// are bit sweeps.
 static gf2x_status run_bitcvt(uint64_t* G, int M, bool inverse, int smc, cudaStream_t st) {
     std::vector<CvtOp> ops;
-    cvt_ops(M, 0, ops);
-    if (inverse) std::reverse(ops.begin(), ops.end());
-    const uint64_t nw = 1ull << (M - 6);
+    bit_ops(M, 0, ops);
+    struct Group { bool words; std::vector<CvtOp> ops; };
+    std::vector<Group> groups;
     for (const CvtOp& op : ops) {
-        const uint64_t h = 1ull << (op.lg - 1), u = h >> op.K, d = h - u;
-        for (int sw = 0; sw < 2; sw++) {
-            const bool first = inverse ? sw == 1 : sw == 0;   // sweep 1 (targets [h, h+u)) or sweep 2 ([u, h))
-            const uint64_t tlo = first ? h : u, thi = first ? h + u : h;
-            uint64_t pmask = 0;
-            if (op.lg < 6)
-                for (uint64_t seg = 0; seg < 64; seg += 2 * h)
-                    for (uint64_t t = tlo; t < thi; t++) pmask |= 1ull << (seg + t);
-            ProfScope ps("k_bitcvt_sweep", 16.0 * nw, st);
-            k_bitcvt_sweep<<<grid_for(nw, 256, smc, 8), 256, 0, st>>>(G, nw, op.lg, d, tlo, thi, pmask);
+        const bool words = op.lg - 1 - op.K >= 6 && !env_flag("GF2X_BITCVT_SWEEPS");
+        if (groups.empty() || groups.back().words != words) groups.push_back({words, {}});
+        groups.back().ops.push_back(op);
+    }
+    if (inverse) std::reverse(groups.begin(), groups.end());
+    const uint64_t nw = 1ull << (M - 6);
+    InwordSweeps iw;
+    iw.n = 0;
+    auto flush = [&]() {
+        if (!iw.n) return;
+        ProfScope ps("k_bitcvt_inword", 16.0 * nw, st);
+        k_bitcvt_inword<<<grid_for(nw, 256, smc, 8), 256, 0, st>>>(G, nw, iw);
+        iw.n = 0;
+    };
+    gf2x_status s;
+    for (const Group& gr : groups) {
+        if (gr.words) {
+            flush();
+            std::vector<CvtOp> wops;
+            for (const CvtOp& op : gr.ops) wops.push_back({op.lg - 6, op.K});
+            const std::vector<CvtPass> passes = plan_cvt_ops(wops, M - 6, 8);
+            if ((s = run_cvt<uint64_t>(passes, G, M - 6, 1, inverse, smc, st)) != GF2X_OK) return s;
+            continue;
+        }
+        std::vector<CvtOp> seq = gr.ops;
+        if (inverse) std::reverse(seq.begin(), seq.end());
+        for (const CvtOp& op : seq) {
+            const uint64_t h = 1ull << (op.lg - 1), u = h >> op.K, d = h - u;
+            for (int sw = 0; sw < 2; sw++) {
+                const bool first = inverse ? sw == 1 : sw == 0;   // sweep 1 (targets [h, h+u)) or sweep 2 ([u, h))
+                const uint64_t tlo = first ? h : u, thi = first ? h + u : h;
+                if (op.lg <= 6) {   // segments inside a word: a periodic mask, sources in the same word
+                    uint64_t pmask = 0;
+                    for (uint64_t seg = 0; seg < 64; seg += 2 * h)
+                        for (uint64_t t = tlo; t < thi; t++) pmask |= 1ull << (seg + t);
+                    if (iw.n == 64) flush();
+                    iw.pmask[iw.n] = pmask;
+                    iw.d[iw.n++] = (int)d;
+                    continue;
+                }
+                flush();
+                const uint64_t ntw = ((thi + 63) >> 6) - (tlo >> 6), total = (nw >> (op.lg - 6)) * ntw;
+                ProfScope ps("k_bitcvt_sweep", 16.0 * (double)total, st);
+                k_bitcvt_sweep<<<grid_for(total, 256, smc, 8), 256, 0, st>>>(G, nw, op.lg, d, tlo, thi);
+            }
         }
     }
+    flush();
     return check_launch("bit-level BasisCvt");
 }
 
@@ -117,6 +180,49 @@ __global__ void __launch_bounds__(256) k_frob_scatter(const uint4* __restrict__ 
             v |= (uint64_t)((limb >> (j & 31)) & 1) << b;
         }
         G[w] = v;
+    }
+}
+
+// staged forms for n >= 256 (m >= 8): a CTA takes 256 consecutive i, i.e. 4 words of each of the 128 planes
+// j (word (i0 / 64 + q) + j n / 64), loaded once into shared memory
+__global__ void __launch_bounds__(256) k_frob_encode_tiled(const uint64_t* __restrict__ G, int m, const uint4* __restrict__ cols,
+                                                           uint4* __restrict__ W) {
+    __shared__ uint4 C[128];
+    __shared__ uint64_t P[128][4];
+    if (threadIdx.x < 128) C[threadIdx.x] = cols[threadIdx.x];
+    const uint64_t n = 1ull << m, wstride = n >> 6;
+    for (uint64_t blk = blockIdx.x; blk < (n >> 8); blk += gridDim.x) {
+        __syncthreads();
+        for (uint32_t t = threadIdx.x; t < 512; t += 256) {
+            const uint32_t j = t >> 2, q = t & 3;
+            P[j][q] = G[blk * 4 + q + j * wstride];
+        }
+        __syncthreads();
+        const uint32_t q = threadIdx.x >> 6, b = threadIdx.x & 63;
+        uint4 x = make_uint4(0, 0, 0, 0);
+#pragma unroll 8
+        for (int j = 0; j < 128; j++)
+            if ((P[j][q] >> b) & 1) x = xor4(x, C[j]);
+        W[blk * 256 + threadIdx.x] = x;
+    }
+}
+// a CTA takes 64 consecutive i (one word of every plane j): thread j gathers bit j of the 64 decoded vectors
+__global__ void __launch_bounds__(128) k_frob_scatter_tiled(const uint4* __restrict__ Dv, int m, uint64_t* __restrict__ G) {
+    __shared__ uint4 D[64];
+    const uint64_t n = 1ull << m, wstride = n >> 6;
+    const uint32_t j = threadIdx.x, limb = j >> 5, sh = j & 31;
+    for (uint64_t blk = blockIdx.x; blk < (n >> 6); blk += gridDim.x) {
+        __syncthreads();
+        if (threadIdx.x < 64) D[threadIdx.x] = Dv[blk * 64 + threadIdx.x];
+        __syncthreads();
+        uint64_t v = 0;
+#pragma unroll 8
+        for (int t = 0; t < 64; t++) {
+            const uint4 d = D[t];
+            const uint32_t w = limb == 0 ? d.x : (limb == 1 ? d.y : (limb == 2 ? d.z : d.w));
+            v |= (uint64_t)((w >> sh) & 1) << t;
+        }
+        G[blk + j * wstride] = v;
     }
 }
 
@@ -196,7 +302,23 @@ static gf2x_status run_frob_mul(const uint64_t* a, uint64_t a_bits, const uint64
     if ((s = get_tablesA4(ds, &TA)) != GF2X_OK) return s;
     void* ws = nullptr;
     const size_t bytes = 2 * nw * 8 + 2 * n * 16;
-    CUDA_TRY(cudaMallocAsync(&ws, bytes, st));
+    {   // the per-stream workspace of the other entry points (stream-ordered reuse)
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto& ent = ds->ws[st];
+        if (ent.second < bytes) {
+            if (ent.first) {
+                cudaStreamSynchronize(st);
+                cudaFree(ent.first);
+                ent.first = nullptr;
+                ent.second = 0;
+            }
+            void* p = nullptr;
+            if (cudaMalloc(&p, bytes) != cudaSuccess) return fail(GF2X_ENOMEM, "App. C workspace");
+            ent.first = p;
+            ent.second = bytes;
+        }
+        ws = ent.first;
+    }
     uint64_t* Ga = reinterpret_cast<uint64_t*>(ws);
     uint64_t* Gb = Ga + nw;
     uint4* Wa = reinterpret_cast<uint4*>(Gb + nw);
@@ -213,8 +335,13 @@ static gf2x_status run_frob_mul(const uint64_t* a, uint64_t a_bits, const uint64
         if ((r = run_bitcvt(Gb, M, false, smc, st)) != GF2X_OK) return r;
         {
             ProfScope ps("k_frob_encode", 2.0 * (16.0 * n + 16.0 * n), st);
-            k_frob_encode<<<grid_for(n, 256, smc, 8), 256, 0, st>>>(Ga, m, K + FROB_COLS, Wa);
-            k_frob_encode<<<grid_for(n, 256, smc, 8), 256, 0, st>>>(Gb, m, K + FROB_COLS, Wb);
+            if (m >= 8) {
+                k_frob_encode_tiled<<<grid_for(n >> 8, 1, smc, 8), 256, 0, st>>>(Ga, m, K + FROB_COLS, Wa);
+                k_frob_encode_tiled<<<grid_for(n >> 8, 1, smc, 8), 256, 0, st>>>(Gb, m, K + FROB_COLS, Wb);
+            } else {
+                k_frob_encode<<<grid_for(n, 256, smc, 8), 256, 0, st>>>(Ga, m, K + FROB_COLS, Wa);
+                k_frob_encode<<<grid_for(n, 256, smc, 8), 256, 0, st>>>(Gb, m, K + FROB_COLS, Wb);
+            }
         }
         const std::vector<A4Pass> passes = plan_a4(m);
         for (const A4Pass& f : passes)   // Wa | Wb contiguous: both in one launch per pass
@@ -231,7 +358,8 @@ static gf2x_status run_frob_mul(const uint64_t* a, uint64_t a_bits, const uint64
         }
         {
             ProfScope ps("k_frob_scatter", 8.0 * nw + 16.0 * n, st);
-            k_frob_scatter<<<grid_for(nw, 256, smc, 8), 256, 0, st>>>(Wb, m, Ga, nw);
+            if (m >= 6) k_frob_scatter_tiled<<<grid_for(n >> 6, 1, smc, 16), 128, 0, st>>>(Wb, m, Ga);
+            else k_frob_scatter<<<grid_for(nw, 256, smc, 8), 256, 0, st>>>(Wb, m, Ga, nw);
         }
         if ((r = run_bitcvt(Ga, M, true, smc, st)) != GF2X_OK) return r;
         const uint64_t ncopy = std::min<uint64_t>(na + nb, nw);
@@ -239,7 +367,5 @@ static gf2x_status run_frob_mul(const uint64_t* a, uint64_t a_bits, const uint64
         if (na + nb > ncopy) CUDA_TRY(cudaMemsetAsync(c + ncopy, 0, (na + nb - ncopy) * 8, st));
         return check_launch("App. C multiply");
     };
-    s = body();
-    cudaFreeAsync(ws, st);
-    return s;
+    return body();
 }

@@ -130,3 +130,31 @@ def test_frob_mul_c4a_sampled_and_timing():
     for w in sorted({0, 1, len(got) // 2, len(got) - 2, len(got) - 1} | set(int(x) for x in rng.integers(0, len(got), 10))):
         assert int(got[w]) == O.mul_word(a, b, w), w
     assert O.check_mod_p(a, b, got, O.random_irreducibles(3, seed=17))
+
+
+_SWEEPS_ONLY = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+import paper_1708_09746_b200 as G
+from gf2x_synth import operand
+M = int(sys.argv[1])
+f = operand(1 << M, seed=M + 500)
+d = torch.from_numpy(f.view(np.int64).copy()).cuda().view(torch.uint64)
+G.gf2x_basis_cvt_bits(d, M)
+torch.cuda.synchronize()
+np.save(sys.argv[2], d.cpu().view(torch.int64).numpy())
+"""
+
+
+@pytest.mark.parametrize("M", [9, 20])
+def test_bit_basis_cvt_sweeps_only_variant(M, tmp_path):
+    # GF2X_BITCVT_SWEEPS=1 runs every step as bit sweeps (no word-level passes): same result
+    import os
+    import subprocess
+    import sys
+    out = tmp_path / "g.npy"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", _SWEEPS_ONLY, str(M), str(out)], cwd=root, check=True, timeout=600,
+                   env={**os.environ, "GF2X_BITCVT_SWEEPS": "1"})
+    f = operand(1 << M, seed=M + 500)
+    assert np.array_equal(np.load(out).view(np.uint64), O.basis_cvt_bits(f, M))
