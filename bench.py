@@ -134,16 +134,17 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(cfg: str, sample_bits: int):
-    """The oracle (Alg. 5, plain C, OpenMP) timed on the host cores on a bounded sample."""
+def cpu_baseline(cfg: str, sample_bits: int, alg=5):
+    """The oracle (plain C, OpenMP; Alg. 5, or App. C for --alg frob) timed on the host cores on a bounded sample."""
     import oracle as O
     O.build()
     a, b = operand_pair(sample_bits, DEFAULT_SEED)
+    fn, name = (O.frob_mul, "App. C (Frobenius bijection)") if alg == "frob" else (O.alg5_mul, "Alg. 5")
     t0 = time.perf_counter()
-    O.alg5_mul(a, sample_bits, b, sample_bits)
+    fn(a, sample_bits, b, sample_bits)
     dt = time.perf_counter() - t0
     return {"value": round(2 * sample_bits / dt / 1e9, 6), "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
-            "sample": f"one oracle Alg. 5 multiply of two 2^{sample_bits.bit_length() - 1}-bit operands "
+            "sample": f"one oracle {name} multiply of two 2^{sample_bits.bit_length() - 1}-bit operands "
                       f"(same seeded recipe as {cfg}); {dt * 1e3:.1f} ms; clmul={O.clmul_impl()}"}
 
 
@@ -510,7 +511,8 @@ def main():
     if sharded_error:
         line["sharded_error"] = sharded_error
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, 1 << 24 if bits >= 1 << 24 else bits)
+        line["cpu_baseline"] = cpu_baseline(args.config, (1 << 24 if bits >= 1 << 24 else bits) if args.alg != "frob"
+                                            else min(bits, 1 << 22), args.alg)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if sharded:
