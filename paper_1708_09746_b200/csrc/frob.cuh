@@ -47,6 +47,58 @@ __global__ void __launch_bounds__(256) k_bitcvt_inword(uint64_t* __restrict__ G,
     }
 }
 
+// The inner conversion BasisCvt_C(q_i) of every 2^C-bit chunk (C <= 16: 8 KB) in one pass through shared
+// memory: the chunk's words are loaded once and all its sweeps (in-word, across bit 6 and word-aligned alike)
+// run on them with a barrier after each.
+#define BITCHUNK_MAXSW 96
+struct ChunkSweeps {
+    uint64_t pmask[BITCHUNK_MAXSW];   // lg <= 6: periodic target mask
+    uint32_t d[BITCHUNK_MAXSW], tlo[BITCHUNK_MAXSW], thi[BITCHUNK_MAXSW];
+    uint8_t lg[BITCHUNK_MAXSW];
+    int n, cw;                        // sweeps; words per chunk (2^(C-6))
+};
+__global__ void __launch_bounds__(256) k_bitcvt_chunk(uint64_t* __restrict__ G, uint64_t nchunks, ChunkSweeps sw) {
+    __shared__ uint64_t T[1024];
+    const uint32_t cw = (uint32_t)sw.cw;
+    for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        uint64_t* g = G + ch * cw;
+        __syncthreads();
+        for (uint32_t w = threadIdx.x; w < cw; w += blockDim.x) T[w] = g[w];
+        __syncthreads();
+        for (int k = 0; k < sw.n; k++) {
+            const int lg = sw.lg[k];
+            const uint32_t d = sw.d[k];
+            if (lg <= 6) {
+                const uint64_t pm = sw.pmask[k];
+                for (uint32_t w = threadIdx.x; w < cw; w += blockDim.x) { const uint64_t x = T[w]; T[w] = x ^ ((x >> d) & pm); }
+            } else {
+                const uint32_t tlo = sw.tlo[k], thi = sw.thi[k], len = 1u << lg, wps = len >> 6, tw0 = tlo >> 6;
+                const uint32_t ntw = ((thi + 63) >> 6) - tw0, total = (cw / wps) * ntw;
+                uint64_t nv[4];
+                uint32_t nwd[4];
+                int cnt = 0;
+                // read phase (all sources first: a target word may be another thread's source word)
+                for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
+                    const uint32_t seg = t / ntw, w = seg * wps + tw0 + (t - seg * ntw);
+                    const uint32_t o = (w << 6) & (len - 1);
+                    const uint32_t lo = tlo > o ? tlo - o : 0, hi = thi < o + 64 ? thi - o : 64;
+                    if (lo >= hi) continue;
+                    const uint64_t mask = (hi >= 64 ? ~0ull : ((1ull << hi) - 1)) & ~((1ull << lo) - 1);
+                    const uint32_t sp = (w << 6) + d, w0 = sp >> 6, sh = sp & 63;
+                    uint64_t src = T[w0] >> sh;
+                    if (sh && w0 + 1 < cw) src |= T[w0 + 1] << (64 - sh);
+                    nv[cnt] = T[w] ^ (src & mask);
+                    nwd[cnt++] = w;
+                }
+                __syncthreads();
+                for (int q = 0; q < cnt; q++) T[nwd[q]] = nv[q];
+            }
+            __syncthreads();
+        }
+        for (uint32_t w = threadIdx.x; w < cw; w += blockDim.x) g[w] = T[w];
+    }
+}
+
 // Alg. 3's steps in the paper's order (Taylor levels, outer conversion, inner conversions; the oracle's order)
 static void bit_ops(int m, int sigma, std::vector<CvtOp>& out) {
     if (m <= 1) return;
@@ -61,9 +113,51 @@ static void bit_ops(int m, int sigma, std::vector<CvtOp>& out) {
 // steps run as a word-level conversion (the planned res / rb / tile passes of the Alg. 5 path on the packed
 // words, step (lg - 6, K)); steps inside a word fuse into one in-register pass; the rest (windows across bit 6)
 // are bit sweeps.
+static void bit_sweeps(const CvtOp& op, bool inverse, ChunkSweeps& cs) {
+    const uint64_t h = 1ull << (op.lg - 1), u = h >> op.K, d = h - u;
+    for (int sw = 0; sw < 2; sw++) {
+        const bool first = inverse ? sw == 1 : sw == 0;
+        const uint64_t tlo = first ? h : u, thi = first ? h + u : h;
+        uint64_t pmask = 0;
+        if (op.lg <= 6)
+            for (uint64_t seg = 0; seg < 64; seg += 2 * h)
+                for (uint64_t t = tlo; t < thi; t++) pmask |= 1ull << (seg + t);
+        const int k = cs.n++;
+        cs.pmask[k] = pmask; cs.d[k] = (uint32_t)d; cs.tlo[k] = (uint32_t)tlo; cs.thi[k] = (uint32_t)thi; cs.lg[k] = (uint8_t)op.lg;
+    }
+}
+
 static gf2x_status run_bitcvt(uint64_t* G, int M, bool inverse, int smc, cudaStream_t st) {
+    // the inner conversions of the 2^C-bit chunks (C = the top level's K, or all of it for M <= 16) go to
+    // k_bitcvt_chunk; they come last in the paper's order (first when inverse)
+    int C = M;
+    if (M > 16) { C = 1; while (2 * C <= M - 1) C *= 2; }
+    const bool chunked = C >= 7 && C <= 16 && !env_flag("GF2X_BITCVT_NOCHUNK");
     std::vector<CvtOp> ops;
-    bit_ops(M, 0, ops);
+    if (chunked && C < M) {   // top Taylor levels and the outer conversion of the top node
+        for (int l = M; l >= C + 1; --l) ops.push_back({l, C});
+        bit_ops(M - C, C, ops);
+    } else if (!chunked) {
+        bit_ops(M, 0, ops);
+    }
+    auto run_chunks = [&]() -> gf2x_status {
+        std::vector<CvtOp> inner;
+        bit_ops(C, 0, inner);
+        if (inverse) std::reverse(inner.begin(), inner.end());
+        ChunkSweeps cs;
+        cs.n = 0;
+        cs.cw = 1 << (C - 6);
+        for (const CvtOp& op : inner) {
+            if (cs.n + 2 > BITCHUNK_MAXSW) return fail(GF2X_EINVAL, "bit-level chunk: too many sweeps");
+            bit_sweeps(op, inverse, cs);
+        }
+        const uint64_t nchunks = (1ull << (M - 6)) >> (C - 6);
+        ProfScope ps("k_bitcvt_chunk", 16.0 * (double)(1ull << (M - 6)), st);
+        k_bitcvt_chunk<<<grid_for(nchunks, 1, smc, 8), 256, 0, st>>>(G, nchunks, cs);
+        return check_launch("bit-level chunk");
+    };
+    gf2x_status s0;
+    if (chunked && inverse && (s0 = run_chunks()) != GF2X_OK) return s0;
     struct Group { bool words; std::vector<CvtOp> ops; };
     std::vector<Group> groups;
     for (const CvtOp& op : ops) {
@@ -115,7 +209,9 @@ static gf2x_status run_bitcvt(uint64_t* G, int M, bool inverse, int smc, cudaStr
         }
     }
     flush();
-    return check_launch("bit-level BasisCvt");
+    if ((s = check_launch("bit-level BasisCvt")) != GF2X_OK) return s;
+    if (chunked && !inverse) return run_chunks();
+    return GF2X_OK;
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -146,15 +146,16 @@ np.save(sys.argv[2], d.cpu().view(torch.int64).numpy())
 """
 
 
+@pytest.mark.parametrize("env", ["GF2X_BITCVT_SWEEPS", "GF2X_BITCVT_NOCHUNK"])
 @pytest.mark.parametrize("M", [9, 20])
-def test_bit_basis_cvt_sweeps_only_variant(M, tmp_path):
-    # GF2X_BITCVT_SWEEPS=1 runs every step as bit sweeps (no word-level passes): same result
+def test_bit_basis_cvt_sweeps_only_variant(M, env, tmp_path):
+    # GF2X_BITCVT_SWEEPS=1: no word-level passes; GF2X_BITCVT_NOCHUNK=1: no shared-memory chunk pass; same result
     import os
     import subprocess
     import sys
     out = tmp_path / "g.npy"
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     subprocess.run([sys.executable, "-c", _SWEEPS_ONLY, str(M), str(out)], cwd=root, check=True, timeout=600,
-                   env={**os.environ, "GF2X_BITCVT_SWEEPS": "1"})
+                   env={**os.environ, env: "1"})
     f = operand(1 << M, seed=M + 500)
     assert np.array_equal(np.load(out).view(np.uint64), O.basis_cvt_bits(f, M))
