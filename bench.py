@@ -134,27 +134,86 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(cfg: str, sample_bits: int, alg=5):
-    """The oracle (plain C, OpenMP; Alg. 5, or App. C for --alg frob) timed on the host cores on a bounded sample."""
+def _cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(cfg: str, bits: int, batch: int, alg=5):
+    """The oracle as it stands (plain C, OpenMP; the paper's Alg. 5 step by step, or App. C for --alg frob),
+    timed on this box's host cores (SURVEY §8(d) / BASELINE.md §3):
+      * O3 on the benched workload itself at all host cores (one run; for batched configs a bounded sample
+        of 64 of the pairs);
+      * O3 at 1 thread, median of 3, on a stated 2^22-bit size (the paper's single-core setting);
+      * O2 Karatsuba at 1 thread on 2^24-bit operands (where it finishes).
+    `value` is the all-cores figure on the benched workload."""
     import oracle as O
     O.build()
-    a, b = operand_pair(sample_bits, DEFAULT_SEED)
+    allc = O.num_threads()
     fn, name = (O.frob_mul, "App. C (Frobenius bijection)") if alg == "frob" else (O.alg5_mul, "Alg. 5")
-    t0 = time.perf_counter()
-    fn(a, sample_bits, b, sample_bits)
-    dt = time.perf_counter() - t0
-    return {"value": round(2 * sample_bits / dt / 1e9, 6), "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
-            "sample": f"one oracle {name} multiply of two 2^{sample_bits.bit_length() - 1}-bit operands "
-                      f"(same seeded recipe as {cfg}); {dt * 1e3:.1f} ms; clmul={O.clmul_impl()}"}
+    if batch == 1:
+        a, b = operand_pair(bits, DEFAULT_SEED)
+        t0 = time.perf_counter()
+        fn(a, bits, b, bits)
+        dt_all = time.perf_counter() - t0
+        all_bits, all_what = 2 * bits, f"one multiply of the benched workload ({cfg}, 2 x {bits} bits)"
+    else:
+        k = min(batch, 64)
+        A, B = batch_pair(bits, batch, DEFAULT_SEED)
+        t0 = time.perf_counter()
+        for i in range(k):
+            fn(A[i], bits, B[i], bits)
+        dt_all = time.perf_counter() - t0
+        all_bits, all_what = 2 * bits * k, f"{k} of the {batch} pairs of {cfg} (2 x {bits} bits each)"
+    val = 2 * all_bits / 2 / dt_all / 1e9
+    # 1 thread, median of 3 (the paper's Table 2 runs are single-core: P:1184-1191)
+    one_bits = min(bits, 1 << 22)
+    a1, b1 = operand_pair(one_bits, DEFAULT_SEED)
+    O.set_threads(1)
+    try:
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            fn(a1, one_bits, b1, one_bits)
+            ts.append(time.perf_counter() - t0)
+        t1 = statistics.median(ts)
+        kb = None
+        if alg != "frob":
+            kbits = min(bits, 1 << 24)
+            ak, bk = operand_pair(kbits, DEFAULT_SEED)
+            t0 = time.perf_counter()
+            O.mul_karatsuba(ak, bk)
+            kb = {"bits": kbits, "ms": round((time.perf_counter() - t0) * 1e3, 1),
+                  "value": round(2 * kbits / (time.perf_counter() - t0) / 1e9, 6)}
+    finally:
+        O.set_threads(allc)
+    return {"value": round(val, 6), "unit": UNIT, "cores": allc, "kind": "oracle",
+            "sample": f"oracle {name} (O3) at all {allc} host threads: {all_what}, {dt_all * 1e3:.1f} ms",
+            "nproc": os.cpu_count(), "cpu_model": _cpu_model(), "clmul": O.clmul_impl(),
+            "one_thread": {"bits": one_bits, "ms_median_of_3": round(t1 * 1e3, 2),
+                           "value": round(2 * one_bits / t1 / 1e9, 6), "kind": f"oracle {name} (O3), 1 thread"},
+            "karatsuba_one_thread": kb}
+
+
+REF_SAMPLE_BITS = 1 << 24   # the paper's Table 2 column 18 size (c3)
 
 
 def run_reference(args):
+    """The reference arm: the repo's CPU oracle (the paper's Alg. 5 step by step) on the host cores, each step one
+    multiply of a bounded sample (two 2^24-bit operands) of the benched workload; rank 0 only."""
     rank, world, _ = rank_info()
     if rank != 0:
         return 0
     import oracle as O
     O.build()
-    sample_bits = 1 << 22
+    bits, _ = CONFIGS[args.config]
+    sample_bits = min(bits, REF_SAMPLE_BITS)
     a, b = operand_pair(sample_bits, DEFAULT_SEED)
     for _ in range(args.warmup):
         O.alg5_mul(a, sample_bits, b, sample_bits)
@@ -169,12 +228,22 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": WORKLOAD[args.config], "config": args.config},
         "cpu_baseline": {"value": round(val, 6), "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
-                         "sample": f"each step: one oracle Alg. 5 multiply of two 2^22-bit operands (bounded sample "
-                                   f"of {args.config}, same seeded recipe); clmul={O.clmul_impl()}"},
+                         "sample": f"each step: one oracle Alg. 5 multiply of two 2^{sample_bits.bit_length() - 1}-bit "
+                                   f"operands (bounded sample of {args.config}, same seeded recipe)",
+                         "nproc": os.cpu_count(), "cpu_model": _cpu_model(), "clmul": O.clmul_impl()},
         "e2e": {"value": round(val, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def load_traffic(cfg):
+    """ncu DRAM bytes per launch (by bench kernel name) and per whole multiply, from profiles/ncu_traffic.json."""
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(tpath)).get(cfg, {})
+    except Exception:
+        return {}
 
 
 def main():
@@ -191,6 +260,8 @@ def main():
                     help="operand size override: one multiply of two BITS-bit operands instead of --config's "
                          "(e.g. 268435520 = 2^28 + 64, the truncated-FFT staircase, DESIGN.md §10c)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-companion", action="store_true",
+                    help="c4b: do not also time the 2^28-bit multiply (c4a) in the same run")
     ap.add_argument("--w", type=int, default=64, choices=[64, 128],
                     help="Alg. 5 block width: 64 (TGF(2^128), default) or 128 (TGF(2^256), P:873-874)")
     ap.add_argument("--alg", default="5", choices=["5", "4", "frob"],
@@ -233,92 +304,115 @@ def main():
     if mode == "sharded" and (batch != 1 or args.w != 64 or args.alg != 5):
         mode = "replicas"   # batched configs shard trivially: independent products per rank
     sharded = mode == "sharded"
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    def operands(nbits, nbatch, seed):
+        if nbatch == 1:
+            x, y = operand_pair(nbits, seed)
+        else:
+            x, y = batch_pair(nbits, nbatch, seed)
+        dx = torch.from_numpy(x.reshape(-1).view(np.int64)).to(dev).view(torch.uint64)
+        dy = torch.from_numpy(y.reshape(-1).view(np.int64)).to(dev).view(torch.uint64)
+        return x, y, dx, dy
+
     seed = DEFAULT_SEED + (0 if sharded else 2 * rank)  # replicas: each rank its own operand pair
-    if batch == 1:
-        a, b = operand_pair(bits, seed)
-    else:
-        a, b = batch_pair(bits, batch, seed)
+    a, b, da, db = operands(bits, batch, seed)
     n = G.nwords(bits)
     n_out = 2 * n
-    dev = torch.device("cuda", local)
-    da = torch.from_numpy(a.reshape(-1).view(np.int64)).to(dev).view(torch.uint64)
-    db = torch.from_numpy(b.reshape(-1).view(np.int64)).to(dev).view(torch.uint64)
     dc = torch.empty(n_out * batch, dtype=torch.uint64, device=dev)
-    stream = torch.cuda.current_stream()
-    sharded_error = None
+
+    def fail_line(err):
+        """A failed partitioned multiply prints a line that carries no throughput (never a replicas number)."""
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                              "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+                              "scaling": "failed", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                              "config": {"workload": WORKLOAD[args.config], "config": args.config,
+                                         "parallelism": f"sharded FFT over {world} GPUs"},
+                              "sharded_error": err, "gpu_launches": 0}), flush=True)
+        if dist:
+            dist.destroy_process_group()
+        return 1
+
     if sharded:
         # SURVEY §8(e): the FFT partitioned over the ranks (NCCL over NVLink); rank r owns words
         # [r n/G, (r+1) n/G) of a and b and receives words [r 2n/G, (r+1) 2n/G) of c
+        err = None
         try:
             comm = G.init_from_process_group()
             lo, hi = G.shard_words(n, world, rank)
             sa, sb = da[lo:hi].clone(), db[lo:hi].clone()
             sc = torch.empty(n_out // world, dtype=torch.uint64, device=dev)
             comm.mul(sa, sb, bits, sc, stream=stream)
-            torch.cuda.synchronize()
+            comm.wait(stream, timeout_s=300.0)   # NCCL async errors / a dead peer abort instead of hanging
             ok = 1
         except Exception as e:   # e.g. NCCL unavailable: every rank sees it (same library, same lists)
-            sharded_error, ok = f"{type(e).__name__}: {e}"[:300], 0
+            err, ok = f"{type(e).__name__}: {e}"[:300], 0
         flag = torch.tensor([ok], dtype=torch.int32, device=dev)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if int(flag.item()) == 1:
-            # the first partitioned product must equal the single-GPU one (rank 0 checks), else fall back
+            # the first partitioned product must equal the single-GPU one (rank 0 checks)
             parts = [torch.empty_like(sc) for _ in range(world)]
             dist.all_gather(parts, sc)
             if rank == 0:
                 G.gf2x_mul(da, bits, db, bits, dc, stream=stream)
                 torch.cuda.synchronize()
                 if not torch.equal(torch.cat(parts).view(torch.int64), dc.view(torch.int64)):
-                    ok, sharded_error = 0, "sharded product differs from the single-GPU product"
+                    ok, err = 0, "sharded product differs from the single-GPU product"
             flag = torch.tensor([ok], dtype=torch.int32, device=dev)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if int(flag.item()) == 0:
-            sharded, mode = False, "replicas"
-            sharded_error = sharded_error or "another rank failed"
-            if rank == 0:
-                print(f"[bench] sharded multiply unavailable ({sharded_error}); running replicas", file=sys.stderr)
-            a, b = operand_pair(bits, DEFAULT_SEED + 2 * rank)
-            da = torch.from_numpy(a.reshape(-1).view(np.int64)).to(dev).view(torch.uint64)
-            db = torch.from_numpy(b.reshape(-1).view(np.int64)).to(dev).view(torch.uint64)
+            return fail_line(err or "another rank failed")
 
-    def step():
-        if sharded:
-            comm.mul(sa, sb, bits, sc, stream=stream)
-        elif args.alg == "frob":
-            G.gf2x_mul_frob(da, bits, db, bits, dc, stream=stream)
-        elif args.alg == 4:
-            G.gf2x_mul_alg4(da, bits, db, bits, batch, dc, stream=stream)
-        elif args.w != 64:
-            G.gf2x_mul_w(da, bits, db, bits, args.w, batch, dc, stream=stream)
-        elif batch == 1:
-            G.gf2x_mul(da, bits, db, bits, dc, stream=stream)
-        else:
-            G.gf2x_mul_batched(da, bits, db, bits, batch, dc, stream=stream)
+    def make_step(xa, xb, xc, nbits, nbatch):
+        def step():
+            if sharded:
+                comm.mul(sa, sb, bits, sc, stream=stream)
+            elif args.alg == "frob":
+                G.gf2x_mul_frob(xa, nbits, xb, nbits, xc, stream=stream)
+            elif args.alg == 4:
+                G.gf2x_mul_alg4(xa, nbits, xb, nbits, nbatch, xc, stream=stream)
+            elif args.w != 64:
+                G.gf2x_mul_w(xa, nbits, xb, nbits, args.w, nbatch, xc, stream=stream)
+            elif nbatch == 1:
+                G.gf2x_mul(xa, nbits, xb, nbits, xc, stream=stream)
+            else:
+                G.gf2x_mul_batched(xa, nbits, xb, nbits, nbatch, xc, stream=stream)
+        return step
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
+    step = make_step(da, db, dc, bits, batch)
+
+    def timed(fn, steps):
+        """W warm-ups, then exactly `steps` calls bracketed by barrier + synchronize, CUDA events on the
+        library stream; max over ranks.  No profiling hooks inside the timed region."""
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        tw0 = time.time()
+        ev0.record(stream)
+        for _ in range(steps):
+            fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        tw1 = time.time()
+        if dist:
+            dist.barrier()
+        ms = ev0.elapsed_time(ev1)
+        if dist:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, tw0, tw1
 
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
-    G.profile_enable(True)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t_wall0 = time.time()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    t_wall1 = time.time()
-    if dist:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    prof = G.profile_report()
-    G.profile_enable(False)
+    ms, t_wall0, t_wall1 = timed(step, args.steps)
     ms_eager = None
     if args.graph and not sharded:
         # one step captured on a side stream (the library plans on the host at capture time), replayed K times
@@ -332,25 +426,11 @@ def main():
         with torch.cuda.graph(graph, stream=stream):
             step()
         with torch.cuda.stream(stream):
-            for _ in range(args.warmup):
-                graph.replay()
-            torch.cuda.synchronize()
-            t_wall0 = time.time()
-            ev0.record(stream)
-            for _ in range(args.steps):
-                graph.replay()
-            ev1.record(stream)
-        torch.cuda.synchronize()
-        t_wall1 = time.time()
-        ms = ev0.elapsed_time(ev1)
+            ms, t_wall0, t_wall1 = timed(graph.replay, args.steps)
         stream = eager_stream
     time.sleep(0.25)
     sampler.stop()
     clocks = sampler.summary(t_wall0 - 0.05, t_wall1 + 0.05)
-    if dist:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
 
     ms_step = ms / args.steps
     in_bits = 2 * bits * batch
@@ -358,12 +438,39 @@ def main():
     value = in_bits * jobs / (ms_step * 1e-3) / 1e9
     if sharded:
         # the partitioned product equals the single-GPU one (rank 0 recomputes it alone)
+        comm.check()
         parts = [torch.empty_like(sc) for _ in range(world)]
         dist.all_gather(parts, sc)
         if rank == 0:
             G.gf2x_mul(da, bits, db, bits, dc, stream=stream)
             torch.cuda.synchronize()
             assert torch.equal(torch.cat(parts).view(torch.int64), dc.view(torch.int64)), "sharded != single-GPU"
+
+    # ---- per-kernel breakdown: a separate profiled run (CUDA events around every launch), not the headline
+    nprof = max(1, min(args.steps, 10))
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    G.profile_enable(True)
+    for _ in range(nprof):
+        step()
+    torch.cuda.synchronize()
+    prof = G.profile_report()
+    G.profile_enable(False)
+
+    # ---- the 2^28-bit companion (BASELINE metric names both headline sizes): same protocol, same run
+    companion = None
+    if (args.config == "c4b" and not args.no_companion and not sharded and world == 1 and args.alg == 5
+            and args.w == 64):
+        cb, _ = CONFIGS["c4a"]
+        _, _, ca, cbb = operands(cb, 1, DEFAULT_SEED)
+        cc = torch.empty(2 * G.nwords(cb), dtype=torch.uint64, device=dev)
+        cms, _, _ = timed(make_step(ca, cbb, cc, cb, 1), args.steps)
+        cstep = cms / args.steps
+        companion = {"config": "c4a", "workload": WORKLOAD["c4a"], "operand_bits": cb, "ms_per_step": round(cstep, 4),
+                     "value": round(2 * cb / (cstep * 1e-3) / 1e9, 4), "unit": UNIT, "steps": args.steps,
+                     "paper_ms_haswell": PAPER_MS["c4a"], "gpu_launches": G.gf2x_launch_count(cb, cb, 1) * args.steps}
+        del ca, cbb, cc
 
     # ---- end to end through the public API with pinned host buffers.  Every step copies its operands
     # host -> device, multiplies, and copies the product device -> host; consecutive steps are pipelined
@@ -435,7 +542,7 @@ def main():
     assert all(torch.equal(h.view(torch.int64), ref) for h in HC)
     ha_bytes, hb_bytes, hc_bytes = ha.numel() * 8, hb.numel() * 8, n_c * 8
 
-    # ---- roofline of the dominant kernel (live CUDA-event durations over the timed region)
+    # ---- roofline of the dominant kernel (CUDA-event durations of the profiled run) and the §8(d) fractions
     peak, peak_src = load_peaks()
     alu_peak, alu_src = load_alu_peak()
     dom = max(prof, key=lambda r: r["ms"])
@@ -444,18 +551,43 @@ def main():
     per_launch_ops = dom.get("alu_ops", 0) / dom["launches"]
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
     achieved_ops = per_launch_ops / (per_launch_ms * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(args.config, {}).get(dom["kernel"])
-        except Exception:
-            traffic = None
-    step_bytes = sum(r["bytes"] for r in prof) / args.steps
-    kern_ms = sum(r["ms"] for r in prof) / args.steps
+    tr = load_traffic(args.config)
+    traffic = tr.get(dom["kernel"])
+    step_bytes = sum(r["bytes"] for r in prof) / nprof
+    kern_ms = sum(r["ms"] for r in prof) / nprof
     launches = G.gf2x_launch_count_w(bits, bits, batch, args.w)
     if sharded or args.alg in (4, "frob"):   # every kernel of these paths is bracketed by the profiling hook
-        launches = sum(r["launches"] for r in prof) // args.steps
+        launches = sum(r["launches"] for r in prof) // nprof
+    t_s = ms_step * 1e-3
+    b_min = 32.0 * n * batch                       # read both operands once, write the product once
+    b_ref = 320.0 * n * batch                      # SURVEY §8(d) 5-pass reference schedule (40 n W)
+    ncu_step = tr.get("__step_dram_bytes")
+    fractions = {
+        "of": f"HBM {peak} GB/s ({peak_src}), whole multiply (ms_per_step)",
+        "ncu_dram_bytes_per_multiply": ncu_step,
+        "ncu_dram_frac": round(ncu_step / t_s / 1e9 / peak, 4) if ncu_step else None,
+        "b_ref_bytes": b_ref, "b_ref_frac": round(b_ref / t_s / 1e9 / peak, 4),
+        "b_min_bytes": b_min, "b_min_frac": round(b_min / t_s / 1e9 / peak, 5),
+        "algorithmic_bytes_per_multiply": step_bytes,
+        "algorithmic_frac": round(step_bytes / t_s / 1e9 / peak, 4),
+    }
+    kcommon = {"kernel": dom["kernel"], "launches_per_step": dom["launches"] / nprof,
+               "algorithmic_bytes_per_launch": per_launch_bytes, "ms_per_launch": round(per_launch_ms, 5),
+               "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read.sum + "
+                                 "dram__bytes_write.sum per launch)" if traffic else None}
+    if per_launch_ops > 0:
+        roof = {"bound": "alu", "achieved": round(achieved_ops, 1), "peak": round(alu_peak, 1),
+                "unit": "Ginstr/s (ALU-pipe lane instructions)", "frac": round(achieved_ops / alu_peak, 4),
+                "traffic": traffic, "peak_source": alu_src,
+                "frac_meaning": "issue fraction of the implementation's own instruction count: the kernel's designed "
+                                "ALU-pipe instructions (SASS-counted, per launch) / its duration / the ALU-pipe peak",
+                "algorithmic_alu_ops_per_launch": per_launch_ops,
+                "hbm_achieved_gbs": round(achieved, 2), "hbm_frac": round(achieved / peak, 4), "hbm_peak": peak}
+    else:
+        roof = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src}
+    roof.update(kcommon)
+    roof["step"] = fractions
 
     line = {
         "metric": METRIC,
@@ -485,22 +617,14 @@ def main():
             "seed": DEFAULT_SEED, "l2": "working set > 126 MB L2 (operands + 2 spectra), no flush" if bits >= 1 << 28
             else "working set may be L2-resident (small config)",
             "paper_ms_haswell": PAPER_MS.get(args.config),
+            "timing": "headline: CUDA events around exactly `steps` multiplies, no profiling hooks; per-kernel "
+                      f"breakdown (`kernels`, roofline durations): a separate run of {nprof} multiplies with a CUDA "
+                      "event pair around every launch",
             **({"cuda_graph": True, "ms_per_step_eager": round(ms_eager / args.steps, 4)} if ms_eager is not None else {}),
         },
-        "roofline": ({
-            "bound": "alu", "kernel": dom["kernel"], "achieved": round(achieved_ops, 1), "peak": round(alu_peak, 1),
-            "unit": "Ginstr/s (ALU-pipe lane instructions)", "frac": round(achieved_ops / alu_peak, 4),
-            "traffic": traffic, "peak_source": alu_src, "algorithmic_alu_ops_per_launch": per_launch_ops,
-            "hbm_achieved_gbs": round(achieved, 2), "hbm_frac": round(achieved / peak, 4), "hbm_peak": peak,
-        } if per_launch_ops > 0 else {
-            "bound": "hbm", "kernel": dom["kernel"], "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src}) | {
-            "algorithmic_bytes_per_launch": per_launch_bytes, "ms_per_launch": round(per_launch_ms, 5),
-            "step_algorithmic_bytes": step_bytes,
-            "step_frac_of_hbm": round(step_bytes / (kern_ms * 1e-3) / 1e9 / peak, 4),
-            "b_min_frac": round(32.0 * n * batch / (ms_step * 1e-3) / 1e9 / peak, 5),
-        },
+        "roofline": roof,
         "kernels": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()} for r in prof],
+        "kernels_steps": nprof,
         "clocks": clocks,
         "e2e": {"value": round(e2e_val, 4), "unit": UNIT, "h2d_bytes_per_step": ha_bytes + hb_bytes,
                 "d2h_bytes_per_step": hc_bytes, "ms_per_step": round(e2e_ms / args.e2e_steps, 4),
@@ -508,11 +632,10 @@ def main():
                 "pipelined": "H2D / multiply / D2H of consecutive steps overlap (2 buffer sets, separate copy streams)"},
         "gpu_launches": launches * args.steps,
     }
-    if sharded_error:
-        line["sharded_error"] = sharded_error
+    if companion:
+        line["companion"] = companion
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, (1 << 24 if bits >= 1 << 24 else bits) if args.alg != "frob"
-                                            else min(bits, 1 << 22), args.alg)
+        line["cpu_baseline"] = cpu_baseline(args.config, bits, batch, args.alg)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if sharded:

@@ -139,6 +139,20 @@ gf2x_status gf2x_comm_destroy(gf2x_comm_t comm);
  * NCCL all-reduce barriers), 0 = NCCL grouped send/recv (IPC unavailable or GF2X_SHARD_NCCL=1; all ranks
  * agree), -1 = null comm. */
 int gf2x_comm_peer_memory(gf2x_comm_t comm);
+/* Failure surfacing.
+ * gf2x_comm_check: GF2X_OK, or GF2X_ENCCL if NCCL reports an asynchronous error on the communicator
+ *   (ncclCommGetAsyncError; e.g. a peer process died) -- the communicator is then aborted
+ *   (ncclCommAbort, which also releases NCCL kernels blocked on the dead peer) and every later call
+ *   on it returns GF2X_ENCCL.  gf2x_mul_sharded runs this check before it enqueues anything.
+ * gf2x_comm_wait: host wait for `stream` that polls the stream and the asynchronous NCCL error every
+ *   200 us; on an error, or after timeout_s seconds (<= 0: no timeout), the communicator is aborted
+ *   and GF2X_ENCCL is returned instead of hanging in cudaStreamSynchronize.  GF2X_ECUDA on a
+ *   stream fault.
+ * gf2x_comm_abort: abort the communicator now (collective peers see an error, not a hang).  The
+ *   handle must still be released with gf2x_comm_destroy. */
+gf2x_status gf2x_comm_check(gf2x_comm_t comm);
+gf2x_status gf2x_comm_wait(gf2x_comm_t comm, void* stream, double timeout_s);
+gf2x_status gf2x_comm_abort(gf2x_comm_t comm);
 gf2x_status gf2x_mul_sharded(const uint64_t* a_shard, const uint64_t* b_shard, uint64_t bits,
                              uint64_t* c_shard, gf2x_comm_t comm, void* stream);
 gf2x_status gf2x_mul_sharded_sim(const uint64_t* a, const uint64_t* b, uint64_t bits, uint64_t* c,

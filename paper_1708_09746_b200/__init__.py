@@ -25,7 +25,7 @@ EXPORTS = [
     "gf2x_mul_sharded_sim", "gf2x_debug_shard_stage", "gf2x_shard_plan", "gf2x_profile_enable", "gf2x_profile_report", "gf2x_status_string", "gf2x_last_error",
     "gf2x_release", "gf2x_version", "gf2x_mul_w", "gf2x_launch_count_w", "gf2x_debug_stage_w128",
     "gf2x_comm_peer_memory", "gf2x_mul_alg4", "gf2x_debug_stage_alg4", "gf2x_plan", "gf2x_basis_cvt_bits",
-    "gf2x_mul_frob",
+    "gf2x_mul_frob", "gf2x_comm_check", "gf2x_comm_wait", "gf2x_comm_abort",
 ]
 
 
@@ -74,11 +74,14 @@ def load(path: str = LIB_PATH):
     L.gf2x_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
     L.gf2x_comm_destroy.argtypes = [vp]
     L.gf2x_comm_peer_memory.argtypes = [vp]
+    L.gf2x_comm_check.argtypes = [vp]
+    L.gf2x_comm_wait.argtypes = [vp, vp, ctypes.c_double]
+    L.gf2x_comm_abort.argtypes = [vp]
     L.gf2x_mul_sharded.argtypes = [vp, vp, u64, vp, vp, vp]
     L.gf2x_mul_sharded_sim.argtypes = [vp, vp, u64, vp, i32, vp]
     L.gf2x_debug_shard_stage.argtypes = [vp, vp, u64, i32, i32, vp, vp]
     for name in ("gf2x_comm_unique_id", "gf2x_comm_init", "gf2x_comm_destroy", "gf2x_mul_sharded", "gf2x_mul_sharded_sim",
-                 "gf2x_debug_shard_stage"):
+                 "gf2x_debug_shard_stage", "gf2x_comm_check", "gf2x_comm_wait", "gf2x_comm_abort"):
         getattr(L, name).restype = i32
     L.gf2x_plan.argtypes = [u64, u64, i64, ctypes.c_char_p, sz]
     L.gf2x_plan.restype = i32
@@ -269,6 +272,17 @@ class Comm:
     def peer_memory(self) -> int:
         """1: exchanges over peer memory (CUDA IPC / NVLink), 0: NCCL send/recv (see include/gf2x.h)."""
         return int(load().gf2x_comm_peer_memory(self.handle))
+
+    def check(self):
+        """Raise if NCCL reports an asynchronous error (the communicator is then aborted)."""
+        _check(load().gf2x_comm_check(self.handle))
+
+    def wait(self, stream=None, timeout_s: float = 0.0):
+        """Wait for `stream` while watching for asynchronous NCCL errors; abort + raise on error or timeout."""
+        _check(load().gf2x_comm_wait(self.handle, _stream_ptr(stream), float(timeout_s)))
+
+    def abort(self):
+        _check(load().gf2x_comm_abort(self.handle))
 
     def close(self):
         if self.handle:

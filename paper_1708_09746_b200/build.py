@@ -49,7 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 def build_variant(name: str, defines: list[str]) -> str:
-    """Tuning aid: the library with extra -D flags as libgf2x_b200_<name>.so (A/B timing, tests/ab_bench.py)."""
+    """Tuning aid: the library with extra -D flags as libgf2x_b200_<name>.so (A/B timing, tools/dev/ab_bench.py)."""
     build()
     path = os.path.join(HERE, f"libgf2x_b200_{name}.so")
     cmd = [NVCC, *[f"-D{d}" for d in defines], *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", path, *SOURCES, "-lcudart"]

@@ -323,7 +323,7 @@ static gf2x_status run_pipeline_a4(const uint64_t* a, uint64_t a_bits, const uin
         if ((s = run_cvt<uint64_t>(P.cvt_b, Sb, P.mb, B, false, smc, st)) != GF2X_OK) return s;
     }
     {
-        ProfScope ps("k_a4_expand", 24.0 * P.N * B * 2, st);
+        ProfScope ps("k_a4_expand", 24.0 * P.N * B * 2, st, 0.0, 2);
         k_a4_expand<<<grid_for(P.N * B, 256, smc, 8), 256, 0, st>>>(Sa, 1ull << P.ma, P.N, B, Wa);
         k_a4_expand<<<grid_for(P.N * B, 256, smc, 8), 256, 0, st>>>(Sb, 1ull << P.mb, P.N, B, Wb);
     }

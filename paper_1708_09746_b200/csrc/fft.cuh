@@ -47,7 +47,8 @@ __device__ __forceinline__ uint32_t m4r4_word_sa(uint32_t tab, uint32_t x) {
 // (v_0 = 1, v_1 = x1, v_2 = x2, v_3 = x1 x2) so the row is the XOR-span of w, x1 w, x2 w, x1 x2 w.
 // SHARED: wt is a shared-memory copy (plain loads); else the global table (read-only cache)
 template <bool SHARED = false>
-__device__ __forceinline__ void build_tab_row(uint32_t* tab, uint32_t c, int t, const uint32_t* __restrict__ wt) {
+__device__ __forceinline__ void build_tab_row(uint32_t* tab, uint32_t c, int t, const uint32_t* __restrict__ wt,
+                                              uint32_t* kb = nullptr) {
     uint32_t w = c;
     if (t) {
         const uint32_t* T = wt + (t - 1) * 1024;
@@ -63,6 +64,45 @@ __device__ __forceinline__ void build_tab_row(uint32_t* tab, uint32_t c, int t, 
     uint4* d = reinterpret_cast<uint4*>(tab + 16 * t);
 #pragma unroll
     for (int q = 0; q < 4; q++) d[q] = make_uint4(row[4 * q], row[4 * q + 1], row[4 * q + 2], row[4 * q + 3]);
+    // small-subfield products (fft_group): K_b = c v_b, b < 8, are the entries x = 2^q of rows 0 and 1
+    if (kb && t < 2) *reinterpret_cast<uint4*>(kb + 4 * t) = make_uint4(row[1], row[2], row[4], row[8]);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Multiplication by a constant c of a small subfield (Prop. 2): when c < 2^B (B = 2, 4, 8: c in
+// GF(4), GF(16), GF(256), the tower's "small number => subfield" rule, definition of v_k P:658-687), every
+// B-bit block of a limb is multiplied by c on its own.  The multiplier shortening puts the
+// constants of layer k below 2^(m-k), so the top layers of a transform are such layers.  With
+// t_b = (u >> b) & M (bit b of every block moved to the block's lowest bit, M = 0x55.., 0x11.., 0x01..),
+//     c u = XOR_b t_b * (c v_b),
+// each integer product t_b * K_b placing K_b = c v_b < 2^B into the blocks where bit b is set: the blocks
+// are disjoint, so the integer product has no carries and equals the XOR.  IMAD runs on the FMA pipe, so
+// a GF(16) product costs 9 ALU + 4 FMA-pipe instructions and no shared-memory lookup (M4R-4: 8 LDS + 15 ALU).
+// ---------------------------------------------------------------------------------------------
+template <int B>
+__device__ __forceinline__ uint32_t smul(uint32_t u, const uint32_t* K) {
+    constexpr uint32_t M = B == 2 ? 0x55555555u : (B == 4 ? 0x11111111u : 0x01010101u);
+    uint32_t r = (u & M) * K[0];
+#pragma unroll
+    for (int b = 1; b < B; b++) r ^= ((u >> b) & M) * K[b];
+    return r;
+}
+template <int B, bool INV>
+__device__ __forceinline__ void bfly_small(uint4& x0, uint4& x1, const uint32_t* kb) {
+    uint32_t K[B];
+    if (B <= 4) {
+        const uint4 k = *reinterpret_cast<const uint4*>(kb);
+        K[0] = k.x; K[1] = k.y;
+        if (B == 4) { K[2] = k.z; K[3] = k.w; }
+    } else {
+        const uint4 k0 = *reinterpret_cast<const uint4*>(kb), k1 = *reinterpret_cast<const uint4*>(kb + 4);
+        K[0] = k0.x; K[1] = k0.y; K[2] = k0.z; K[3] = k0.w;
+        K[4 % B] = k1.x; K[5 % B] = k1.y; K[6 % B] = k1.z; K[7 % B] = k1.w;
+    }
+    if (INV) x1 = xor4(x1, x0);
+    x0.x ^= smul<B>(x1.x, K); x0.y ^= smul<B>(x1.y, K);
+    x0.z ^= smul<B>(x1.z, K); x0.w ^= smul<B>(x1.w, K);
+    if (!INV) x1 = xor4(x1, x0);
 }
 
 struct FftParams {
@@ -110,11 +150,17 @@ __device__ __forceinline__ void bfly(uint4& x0, uint4& x1, uint32_t ta) {
 
 // One group of r consecutive layers [ka, ka+r) whose slot bits are [s0, s0+r).
 // Table id of (layer k, slot) = 2^(R-1-kk) - 1 + (row >> (kk+1)), row = slot >> c, kk = k - k_lo.
+// A layer whose constants lie in GF(4) / GF(16) (/ GF(256) with FFT_SMALL_MAX 8) -- global layer kg of a
+// transform over at most 2^mg global indices has constants < 2^(mg - kg) -- multiplies by bfly_small.
+#ifndef FFT_SMALL_MAX
+#define FFT_SMALL_MAX 4
+#endif
 template <int r, bool INV, bool ZS>
 __device__ __forceinline__ void fft_group(uint4* tile, uint32_t nslots, int s0, int ka, const FftParams& p, uint32_t tabs_sa,
-                                          const uint32_t* zf) {
+                                          const uint32_t* zf, const uint32_t* kbt) {
     const uint32_t nitems = nslots >> r;
     const int R = p.k_hi - p.k_lo;
+    const int mg = p.m + p.map.bits;
     uint32_t it = threadIdx.x;
     for (; it < nitems; it += blockDim.x) {
         const uint32_t base = (it & ((1u << s0) - 1)) | ((it >> s0) << (s0 + r));
@@ -125,15 +171,30 @@ __device__ __forceinline__ void fft_group(uint4* tile, uint32_t nslots, int s0, 
         for (int li = 0; li < r; li++) {
             const int lb = INV ? li : (r - 1 - li);   // local bit of this layer
             const int kk = ka + lb - p.k_lo;
+            const int wbits = mg - glayer(p.map, ka + lb);   // the layer's constants are < 2^wbits
+            const int cls = wbits <= 2 ? 2 : (wbits <= 4 ? 4 : (wbits <= FFT_SMALL_MAX ? 8 : 0));
+            if (cls == 0) {
 #pragma unroll
-            for (int j = 0; j < (1 << r); j++) {
-                if (j & (1 << lb)) continue;
-                const uint32_t row = (base | ((uint32_t)j << s0)) >> p.c;
-                const uint32_t id = ((1u << (R - 1 - kk)) - 1) + (row >> (kk + 1));
-                // multiplier 0 (the block at base 0: s_k vanishes on V_k, Claim 1 P:696-701): x1 ^= x0 only
-                // (warp-uniform branch; a third of the first forward / last inverse pass)
-                if (ZS && zf[id]) v[j | (1 << lb)] = xor4(v[j | (1 << lb)], v[j]);
-                else bfly<INV>(v[j], v[j | (1 << lb)], tab_addr(tabs_sa, id));
+                for (int j = 0; j < (1 << r); j++) {
+                    if (j & (1 << lb)) continue;
+                    const uint32_t row = (base | ((uint32_t)j << s0)) >> p.c;
+                    const uint32_t id = ((1u << (R - 1 - kk)) - 1) + (row >> (kk + 1));
+                    // multiplier 0 (the block at base 0: s_k vanishes on V_k, Claim 1 P:696-701): x1 ^= x0 only
+                    // (warp-uniform branch; a third of the first forward / last inverse pass)
+                    if (ZS && zf[id]) v[j | (1 << lb)] = xor4(v[j | (1 << lb)], v[j]);
+                    else bfly<INV>(v[j], v[j | (1 << lb)], tab_addr(tabs_sa, id));
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < (1 << r); j++) {
+                    if (j & (1 << lb)) continue;
+                    const uint32_t row = (base | ((uint32_t)j << s0)) >> p.c;
+                    const uint32_t id = ((1u << (R - 1 - kk)) - 1) + (row >> (kk + 1));
+                    const uint32_t* kb = kbt + id * 8;
+                    if (cls == 2) bfly_small<2, INV>(v[j], v[j | (1 << lb)], kb);
+                    else if (cls == 4) bfly_small<4, INV>(v[j], v[j | (1 << lb)], kb);
+                    else bfly_small<(FFT_SMALL_MAX >= 8 ? 8 : 4), INV>(v[j], v[j | (1 << lb)], kb);
+                }
             }
         }
 #pragma unroll
@@ -143,10 +204,10 @@ __device__ __forceinline__ void fft_group(uint4* tile, uint32_t nslots, int s0, 
 
 template <bool INV, bool ZS>
 __device__ __forceinline__ void fft_group_any(int r, uint4* tile, uint32_t nslots, int s0, int ka, const FftParams& p,
-                                              uint32_t tabs_sa, const uint32_t* zf) {
-    if (r == 3) fft_group<3, INV, ZS>(tile, nslots, s0, ka, p, tabs_sa, zf);
-    else if (r == 2) fft_group<2, INV, ZS>(tile, nslots, s0, ka, p, tabs_sa, zf);
-    else fft_group<1, INV, ZS>(tile, nslots, s0, ka, p, tabs_sa, zf);
+                                              uint32_t tabs_sa, const uint32_t* zf, const uint32_t* kbt) {
+    if (r == 3) fft_group<3, INV, ZS>(tile, nslots, s0, ka, p, tabs_sa, zf, kbt);
+    else if (r == 2) fft_group<2, INV, ZS>(tile, nslots, s0, ka, p, tabs_sa, zf, kbt);
+    else fft_group<1, INV, ZS>(tile, nslots, s0, ka, p, tabs_sa, zf, kbt);
 }
 
 // shared memory: [tables (2^R - 1) x 512 B] [psi table (PSI)] [tile]
@@ -165,8 +226,9 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     uint32_t* tabs = reinterpret_cast<uint32_t*>(smem_raw);
     uint4* psit = reinterpret_cast<uint4*>(tabs + ntab * 128);
     uint32_t* zf = reinterpret_cast<uint32_t*>(psit + (PSI ? 8 * 256 : 0));   // per table: multiplier == 0
-    uint32_t* wts = zf + 128;                                                   // M4R-8 maps c -> c v_(4t)
-    const uint32_t tile_off = (uint32_t)(ntab * 512 + (PSI ? 8 * 256 * 16 : 0) + 512 + (p.wt_shared ? 7 * 1024 * 4 : 0));
+    uint32_t* kbt = zf + 128;                                                   // per table: K_b = c v_b, b < 8
+    uint32_t* wts = kbt + 128 * 8;                                              // M4R-8 maps c -> c v_(4t)
+    const uint32_t tile_off = (uint32_t)(ntab * 512 + (PSI ? 8 * 256 * 16 : 0) + 512 + 4096 + (p.wt_shared ? 7 * 1024 * 4 : 0));
     uint4* tile = reinterpret_cast<uint4*>(smem_raw + tile_off);
     const uint32_t tabs_sa = (uint32_t)__cvta_generic_to_shared(tabs);
     if (tabs_sa & 255) __trap();  // the PRMT address fusion needs 256-byte aligned tables
@@ -267,8 +329,8 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             const uint32_t blk = id + 1 - (1u << lg);
             const uint32_t lb = (uint32_t)(((uint64_t)base & ~((2ull << k) - 1)) | ((uint64_t)blk << (k + 1)));
             const uint32_t cst = layer_const(glayer(p.map, k), gidx(p.map, lb));
-            if (p.wt_shared) build_tab_row<true>(tabs + id * 128, cst, (int)(i & 7), wts);
-            else build_tab_row<false>(tabs + id * 128, cst, (int)(i & 7), p.tabs->wt);
+            if (p.wt_shared) build_tab_row<true>(tabs + id * 128, cst, (int)(i & 7), wts, kbt + id * 8);
+            else build_tab_row<false>(tabs + id * 128, cst, (int)(i & 7), p.tabs->wt, kbt + id * 8);
             if ((i & 7) == 0) zf[id] = cst == 0;
         }
         tab_key = key;
@@ -307,7 +369,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             while (top > p.k_lo) {
                 const int r = (top - p.k_lo) >= 3 ? 3 : (top - p.k_lo);
                 const int ka = top - r;
-                fft_group_any<INV, ZS>(r, tile, nslots, p.c + ka - p.k_lo, ka, p, tabs_sa, zf);
+                fft_group_any<INV, ZS>(r, tile, nslots, p.c + ka - p.k_lo, ka, p, tabs_sa, zf, kbt);
                 __syncthreads();
                 top = ka;
             }
@@ -315,7 +377,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             int bot = p.k_lo;
             while (bot < p.k_hi) {
                 const int r = (p.k_hi - bot) >= 3 ? 3 : (p.k_hi - bot);
-                fft_group_any<INV, ZS>(r, tile, nslots, p.c + bot - p.k_lo, bot, p, tabs_sa, zf);
+                fft_group_any<INV, ZS>(r, tile, nslots, p.c + bot - p.k_lo, bot, p, tabs_sa, zf, kbt);
                 __syncthreads();
                 bot += r;
             }
@@ -334,6 +396,7 @@ static size_t fft2_smem(int c, int R, bool psi, bool wt_shared, bool db, bool re
     s += (((size_t)1 << R) - 1) * 512;
     if (psi) s += 8 * 256 * 16;
     s += 512;   // zero-multiplier flags (<= 127 tables)
+    s += 4096;  // small-subfield constants K_b (<= 127 tables x 8 words)
     if (wt_shared) s += 7 * 1024 * 4;   // shared copy of the M4R-8 maps c -> c v_(4t) (table builds)
     s += ((size_t)1 << (c + R)) * 16 * (db ? 2 : 1);
     return s;

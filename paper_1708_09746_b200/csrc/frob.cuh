@@ -398,23 +398,7 @@ static gf2x_status run_frob_mul(const uint64_t* a, uint64_t a_bits, const uint64
     if ((s = get_tablesA4(ds, &TA)) != GF2X_OK) return s;
     void* ws = nullptr;
     const size_t bytes = 2 * nw * 8 + 2 * n * 16;
-    {   // the per-stream workspace of the other entry points (stream-ordered reuse)
-        std::lock_guard<std::mutex> lk(g_mu);
-        auto& ent = ds->ws[st];
-        if (ent.second < bytes) {
-            if (ent.first) {
-                cudaStreamSynchronize(st);
-                cudaFree(ent.first);
-                ent.first = nullptr;
-                ent.second = 0;
-            }
-            void* p = nullptr;
-            if (cudaMalloc(&p, bytes) != cudaSuccess) return fail(GF2X_ENOMEM, "App. C workspace");
-            ent.first = p;
-            ent.second = bytes;
-        }
-        ws = ent.first;
-    }
+    if ((s = stream_workspace(ds, st, bytes, &ws)) != GF2X_OK) return s;
     uint64_t* Ga = reinterpret_cast<uint64_t*>(ws);
     uint64_t* Gb = Ga + nw;
     uint4* Wa = reinterpret_cast<uint4*>(Gb + nw);
@@ -423,14 +407,14 @@ static gf2x_status run_frob_mul(const uint64_t* a, uint64_t a_bits, const uint64
     auto body = [&]() -> gf2x_status {
         gf2x_status r;
         {
-            ProfScope ps("k_prep", 16.0 * nw, st);
+            ProfScope ps("k_prep", 16.0 * nw, st, 0.0, 2);
             k_prep<<<grid_for(nw, 256, smc, 8), 256, 0, st>>>(a, na, a_bits, M - 6, 1, Ga);
             k_prep<<<grid_for(nw, 256, smc, 8), 256, 0, st>>>(b, nb, b_bits, M - 6, 1, Gb);
         }
         if ((r = run_bitcvt(Ga, M, false, smc, st)) != GF2X_OK) return r;
         if ((r = run_bitcvt(Gb, M, false, smc, st)) != GF2X_OK) return r;
         {
-            ProfScope ps("k_frob_encode", 2.0 * (16.0 * n + 16.0 * n), st);
+            ProfScope ps("k_frob_encode", 2.0 * (16.0 * n + 16.0 * n), st, 0.0, 2);
             if (m >= 8) {
                 k_frob_encode_tiled<<<grid_for(n >> 8, 1, smc, 8), 256, 0, st>>>(Ga, m, K + FROB_COLS, Wa);
                 k_frob_encode_tiled<<<grid_for(n >> 8, 1, smc, 8), 256, 0, st>>>(Gb, m, K + FROB_COLS, Wb);

@@ -18,7 +18,7 @@
 //   GF2X_DEBUG_PLAN=1    print every plan (conversion and FFT passes) to stderr
 //   GF2X_NO_RB=1         CVT(8) nodes as shared-memory tile passes instead of register-blocked passes
 //   GF2X_NO_RES8=1       K=8 Taylor runs as tile passes instead of residue-class passes
-//   GF2X_RB_NOPHASE=1    measurement only: register-blocked passes copy without converting (wrong result)
+//   (every flag: unset, empty or "0" = off)
 //   GF2X_NO_IPSI_BS=1    table-driven changeRepr^-1 + combine instead of the bit-sliced kernel
 //   GF2X_FFT_C=c         column bits of the non-first FFT passes shorter than 6 layers (default 6)
 //   GF2X_BOT_B=L         layers in the bit-sliced bottom kernel (default 6; 5 for m <= 10)
@@ -35,8 +35,11 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <ctype.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <map>
 #include <mutex>
 #include <string>
@@ -320,6 +323,7 @@ struct ProfRec {
     cudaEvent_t beg, end;
     double bytes;   // algorithmic HBM bytes of the launch
     double ops;     // algorithmic ALU-pipe lane instructions of the launch (ALU-bound designs), else 0
+    int launches;   // kernel launches inside the bracket
 };
 // Designed ALU-pipe instructions (SASS, per lane) of the arithmetic cores, counted from cuobjdump:
 //   one bit-sliced TGF(2^32) product (bs_mul32, 32 elements): 868 LOP3
@@ -351,9 +355,9 @@ static void prof_clear() {
 struct ProfScope {
     int idx = -1;
     cudaStream_t st;
-    ProfScope(const char* name, double bytes, cudaStream_t s, double ops = 0.0) : st(s) {
+    ProfScope(const char* name, double bytes, cudaStream_t s, double ops = 0.0, int launches = 1) : st(s) {
         if (!g_prof_on) return;
-        ProfRec r{name, prof_event(), prof_event(), bytes, ops};
+        ProfRec r{name, prof_event(), prof_event(), bytes, ops, launches};
         cudaEventRecord(r.beg, st);
         g_prof.push_back(r);
         idx = (int)g_prof.size() - 1;
@@ -369,9 +373,30 @@ static bool env_flag(const char* name) {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(name);
     if (it != cache.end()) return it->second;
-    const bool v = getenv(name) != nullptr;
+    // unset, empty, "0", "false", "no" and "off" are false; anything else is true
+    const char* e = getenv(name);
+    bool v = e != nullptr && e[0] != 0;
+    if (v) {
+        std::string t(e);
+        for (auto& ch : t) ch = (char)tolower((unsigned char)ch);
+        v = !(t == "0" || t == "false" || t == "no" || t == "off");
+    }
     cache[name] = v;
     return v;
+}
+
+// integer knob: the default unless the variable holds an integer in [lo, hi]
+static int env_int(const char* name, int dflt, int lo, int hi) {
+    const char* e = getenv(name);
+    if (!e || !e[0]) return dflt;
+    char* end = nullptr;
+    const long v = strtol(e, &end, 10);
+    return (end && *end == 0 && v >= lo && v <= hi) ? (int)v : dflt;
+}
+// per-call flag (not cached): unset, empty or "0" = off
+static bool env_flag_now(const char* name) {
+    const char* e = getenv(name);
+    return e && e[0] && !(e[0] == '0' && e[1] == 0);
 }
 
 static gf2x_status fail(gf2x_status s, const std::string& msg) {
@@ -393,7 +418,8 @@ struct DeviceState {
     void* shard_ws = nullptr;    // simulation workspace (gf2x_mul_sharded_sim)
     size_t shard_ws_bytes = 0;
     int sm_count = 0;
-    std::map<cudaStream_t, std::pair<void*, size_t>> ws;  // per-stream workspace cache
+    std::map<cudaStream_t, std::pair<void*, size_t>> ws;  // per-stream workspace cache (stream_workspace)
+    std::vector<void*> retired;            // outgrown workspaces (a captured graph may still use them)
     struct Aux {
         cudaStream_t s = nullptr;          // side stream (high priority) for independent sub-chains
         cudaEvent_t fork = nullptr, join = nullptr;
@@ -671,8 +697,8 @@ struct FftPass {
 // except for short transforms (m <= 10: one table pass either way; 5 measured 10 % faster at c2).
 static int fft_passes(int H, int maxr) { return H <= 0 ? 0 : (H <= 6 ? 1 : 1 + (H - 6 + maxr - 1) / maxr); }
 static std::vector<FftPass> plan_fft(int m) {
-    static const int maxr = getenv("GF2X_MAXR") ? atoi(getenv("GF2X_MAXR")) : 7;
-    static const int forced = getenv("GF2X_BOT_B") ? atoi(getenv("GF2X_BOT_B")) : 0;
+    static const int maxr = env_int("GF2X_MAXR", 7, 1, 7);
+    static const int forced = env_int("GF2X_BOT_B", 0, 1, BOT_B_MAX);
     const int bot = forced ? forced : (m <= 10 ? 5 : 6);
     std::vector<FftPass> v;
     const int H = m > bot ? m - bot : 0;
@@ -685,7 +711,7 @@ static std::vector<FftPass> plan_fft(int m) {
         // 32-column tiles (2 CTAs/SM) for the changeRepr pass and passes of >= 6 layers; 64 columns (one
         // double-buffered CTA per SM) for shorter passes (measured: c4b -1.7 %, c4a / c5 -0.3 % vs 64 columns
         // for 6-layer passes)
-        static const int cdir = getenv("GF2X_FFT_C") ? atoi(getenv("GF2X_FFT_C")) : 6;
+        static const int cdir = env_int("GF2X_FFT_C", 6, 5, 6);
         int c = (i == 0 || r >= 6) ? 5 : cdir;
         if (c > lo) c = lo;   // column bits must lie below the pass's layers
         v.push_back({c, lo, top, false, 0});
@@ -825,7 +851,12 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
             prm.data = data;
             prm.units_per_pair = per;
             prm.batch = batch;
-            prm.inverse = (inverse ? 1 : 0) | (env_flag("GF2X_RB_NOPHASE") ? 2 : 0);   // bit 1: debug, copy only
+#ifdef GF2X_RB_NOPHASE_BUILD
+            // measurement-only variant (build_variant with -DGF2X_RB_NOPHASE_BUILD): copy without converting
+            prm.inverse = (inverse ? 1 : 0) | 2;
+#else
+            prm.inverse = inverse ? 1 : 0;
+#endif
             // a node spanning all index bits of a (small) product: the tile's columns continue into the next
             // products (they are contiguous), up to the width the planner wanted
             if (prm.mode == 1 && prm.R + prm.C == m) {
@@ -1094,6 +1125,34 @@ static bool overlaps(const void* p, size_t pb, const void* q, size_t qb) {
     return a < b + qb && b < a + pb;
 }
 
+// Per-(device, stream) workspace cache shared by every entry point.  It only grows; a buffer it
+// outgrows is retired, not freed, because a CUDA graph captured earlier may still reference it
+// (retired buffers are freed by gf2x_release).  Growing during stream capture is an error: the
+// allocation would not be part of the graph and a later growth would leave the graph pointing at
+// a retired buffer of the wrong size -- warm up at the largest size first, or pass a workspace
+// (gf2x_mul_ws).
+static gf2x_status stream_workspace(DeviceState* ds, cudaStream_t st, size_t bytes, void** out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto& ent = ds->ws[st];
+    if (ent.second < bytes) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return fail(GF2X_ECUDA, "cudaStreamIsCapturing failed");
+        if (cs != cudaStreamCaptureStatusNone)
+            return fail(GF2X_EINVAL, "the stream's workspace must grow while the stream is being captured: run the "
+                                     "call once before capture (or use gf2x_mul_ws with a caller-owned workspace)");
+        if (ent.first) ds->retired.push_back(ent.first);
+        ent.first = nullptr;
+        ent.second = 0;
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) return fail(GF2X_ENOMEM, std::string("workspace: ") + cudaGetErrorString(e));
+        ent.first = p;
+        ent.second = bytes;
+    }
+    *out = ent.first;
+    return GF2X_OK;
+}
+
 static gf2x_status run_pipeline_a4(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
                                    const Plan& P, void* ws, DeviceState* ds, cudaStream_t st, int stop_stage);
 static int run_trunc_if_eligible(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
@@ -1125,22 +1184,7 @@ static gf2x_status mul_common(const uint64_t* a, uint64_t a_bits, const uint64_t
     if (ws) {
         if (user_ws_bytes < P.bytes) return fail(GF2X_ENOMEM, "workspace too small");
     } else {
-        std::lock_guard<std::mutex> lk(g_mu);
-        auto& ent = ds->ws[st];
-        if (ent.second < P.bytes) {
-            if (ent.first) {
-                cudaStreamSynchronize(st);
-                cudaFree(ent.first);
-                ent.first = nullptr;
-                ent.second = 0;
-            }
-            void* p = nullptr;
-            cudaError_t e = cudaMalloc(&p, P.bytes);
-            if (e != cudaSuccess) return fail(GF2X_ENOMEM, std::string("workspace: ") + cudaGetErrorString(e));
-            ent.first = p;
-            ent.second = P.bytes;
-        }
-        ws = ent.first;
+        if ((s = stream_workspace(ds, st, P.bytes, &ws)) != GF2X_OK) return s;
     }
     // products just above a power of two take the truncated FFT (trunc.cuh) unless a stage is requested
     if (algo == 5 && !stop_stage && run_trunc_if_eligible(a, a_bits, b, b_bits, c, P, ws, ds, st, &s)) return s;
@@ -1276,6 +1320,7 @@ gf2x_status gf2x_comm_init(const void* nccl_unique_id, int nranks, int rank, gf2
     c->ws = nullptr;
     c->ws_bytes = 0;
     c->p2p = 0;
+    c->aborted = 0;
     for (int r = 0; r < SHARD_MAXG; r++) c->peer_ws[r] = nullptr;
     cudaGetDevice(&c->device);
     if (cudaMalloc(&c->d_sync, 256 + SHARD_MAXG * sizeof(cudaIpcMemHandle_t)) != cudaSuccess) {
@@ -1305,7 +1350,7 @@ static void comm_unmap_peers(gf2x_comm_s* c) {
 static gf2x_status comm_map_peers(gf2x_comm_s* c, cudaStream_t st) {
     comm_unmap_peers(c);
     const int G = c->nranks;
-    int ok = getenv("GF2X_SHARD_NCCL") ? 0 : 1;
+    int ok = env_flag_now("GF2X_SHARD_NCCL") ? 0 : 1;
     cudaIpcMemHandle_t mine;
     memset(&mine, 0, sizeof(mine));
     if (ok && cudaIpcGetMemHandle(&mine, c->ws) != cudaSuccess) { ok = 0; cudaGetLastError(); }
@@ -1339,13 +1384,43 @@ static gf2x_status comm_map_peers(gf2x_comm_s* c, cudaStream_t st) {
 
 int gf2x_comm_peer_memory(gf2x_comm_t comm) { return comm ? comm->p2p : -1; }
 
+gf2x_status gf2x_comm_check(gf2x_comm_t comm) {
+    if (!comm) return fail(GF2X_EINVAL, "null communicator");
+    return comm_check(comm);
+}
+
+gf2x_status gf2x_comm_abort(gf2x_comm_t comm) {
+    if (!comm) return fail(GF2X_EINVAL, "null communicator");
+    comm_abort(comm, "gf2x_comm_abort");
+    return GF2X_OK;
+}
+
+gf2x_status gf2x_comm_wait(gf2x_comm_t comm, void* stream, double timeout_s) {
+    if (!comm) return fail(GF2X_EINVAL, "null communicator");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        gf2x_status s = comm_check(comm);
+        if (s != GF2X_OK) return s;
+        const cudaError_t q = cudaStreamQuery(st);
+        if (q == cudaSuccess) return comm_check(comm);
+        if (q != cudaErrorNotReady) return fail(GF2X_ECUDA, std::string("stream: ") + cudaGetErrorString(q));
+        const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (timeout_s > 0 && dt > timeout_s) {
+            comm_abort(comm, "gf2x_comm_wait timed out (a peer stopped participating?)");
+            return fail(GF2X_ENCCL, comm->abort_reason);
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+}
+
 gf2x_status gf2x_comm_destroy(gf2x_comm_t comm) {
     if (!comm) return GF2X_OK;
     cudaDeviceSynchronize();
     comm_unmap_peers(comm);
     if (comm->d_sync) cudaFree(comm->d_sync);
     if (comm->ws) { cudaDeviceSynchronize(); cudaFree(comm->ws); }
-    int rc = g_nccl.h ? g_nccl.CommDestroy(comm->comm) : 0;
+    int rc = (g_nccl.h && comm->comm) ? g_nccl.CommDestroy(comm->comm) : 0;   // (an aborted comm is already gone)
     delete comm;
     if (rc) return fail(GF2X_ENCCL, std::string("ncclCommDestroy: ") + g_nccl.GetErrorString(rc));
     return GF2X_OK;
@@ -1360,6 +1435,8 @@ static void rank_bufs(RankCtx& R, unsigned char* base, const ShardGeom& S) {
 gf2x_status gf2x_mul_sharded(const uint64_t* a_shard, const uint64_t* b_shard, uint64_t bits, uint64_t* c_shard,
                              gf2x_comm_t comm, void* stream) {
     if (!comm || !a_shard || !b_shard || !c_shard) return fail(GF2X_EINVAL, "null argument");
+    gf2x_status s0 = comm_check(comm);   // an earlier asynchronous NCCL failure: do not enqueue on a broken comm
+    if (s0 != GF2X_OK) return s0;
     int dev;
     DeviceState* ds;
     gf2x_status s = get_device(&dev, &ds);
@@ -1421,7 +1498,7 @@ static gf2x_status sharded_sim(const uint64_t* a, const uint64_t* b, uint64_t bi
         rank_bufs(ranks[r], (unsigned char*)ds->shard_ws + r * S.bytes, S);
     }
     ShardExec X{true, nullptr, st, &ranks};
-    X.p2p = getenv("GF2X_SHARD_LISTS") == nullptr;   // default: the peer-memory pulls (lists: copy engine)
+    X.p2p = !env_flag_now("GF2X_SHARD_LISTS");   // default: the peer-memory pulls (lists: copy engine)
     X.off = S.off;
     return run_sharded(S, X, ds, ds->host, bits, debug_stage, (uint4*)dbg);
 }
@@ -1536,7 +1613,7 @@ int gf2x_profile_report(char* buf, size_t cap) {
             agg[r.name] = {0, {0.0, 0.0}};
         }
         auto& a = agg[r.name];
-        a.first += 1;
+        a.first += r.launches;
         a.second.first += ms;
         a.second.second += r.bytes;
         aops[r.name] += r.ops;
@@ -1582,6 +1659,7 @@ gf2x_status gf2x_release(int device) {
     cudaDeviceSynchronize();
     for (auto& kv : it->second.ws)
         if (kv.second.first) cudaFree(kv.second.first);
+    for (void* p : it->second.retired) cudaFree(p);
     if (it->second.tabs) cudaFree(it->second.tabs);
     if (it->second.shard_ws) cudaFree(it->second.shard_ws);
     if (it->second.tabs256) cudaFree(it->second.tabs256);

@@ -175,6 +175,8 @@ struct NcclApi {
     int (*GroupStart)();
     int (*GroupEnd)();
     const char* (*GetErrorString)(int);
+    int (*CommGetAsyncError)(nccl_comm_t, int*);   // failure surfacing
+    int (*CommAbort)(nccl_comm_t);
 };
 static const int NCCL_UINT8 = 1;   // ncclUint8 in the ncclDataType_t enum
 static const int NCCL_INT32 = 2;   // ncclInt32
@@ -198,6 +200,8 @@ static std::string nccl_load() {
     NCCL_SYM(GroupStart, "ncclGroupStart");
     NCCL_SYM(GroupEnd, "ncclGroupEnd");
     NCCL_SYM(GetErrorString, "ncclGetErrorString");
+    NCCL_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+    NCCL_SYM(CommAbort, "ncclCommAbort");
 #undef NCCL_SYM
     g_nccl.h = h;
     return "";
@@ -213,7 +217,33 @@ struct gf2x_comm_s {
     int p2p;
     void* peer_ws[SHARD_MAXG];
     int* d_sync;       // 1 int (stream-ordered barrier = NCCL all-reduce of it) + IPC handle staging
+    int aborted;       // the NCCL communicator was aborted (async error, timeout or gf2x_comm_abort)
+    std::string abort_reason;
 };
+
+static const int NCCL_IN_PROGRESS = 7;   // ncclInProgress (non-blocking communicators): not an error
+
+static void comm_abort(gf2x_comm_s* c, const std::string& why) {
+    if (c->aborted) return;
+    c->aborted = 1;
+    c->abort_reason = why;
+    if (g_nccl.h && c->comm) g_nccl.CommAbort(c->comm);   // unblocks NCCL kernels waiting for a dead peer
+    c->comm = nullptr;
+}
+
+// ncclCommGetAsyncError: an asynchronous NCCL failure (a peer died, a network error) aborts the
+// communicator, so that the stream-ordered barriers of the exchange cannot hang forever
+static gf2x_status comm_check(gf2x_comm_s* c) {
+    if (c->aborted) return fail(GF2X_ENCCL, "communicator aborted: " + c->abort_reason);
+    int async = 0;
+    int rc = g_nccl.CommGetAsyncError(c->comm, &async);
+    if (rc || (async && async != NCCL_IN_PROGRESS)) {
+        const int e = rc ? rc : async;
+        comm_abort(c, std::string("NCCL asynchronous error: ") + g_nccl.GetErrorString(e));
+        return fail(GF2X_ENCCL, c->abort_reason);
+    }
+    return GF2X_OK;
+}
 
 // ---------------------------------------------------------------------------------------------
 // host orchestration

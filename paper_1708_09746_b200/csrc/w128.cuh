@@ -505,7 +505,7 @@ static gf2x_status run_pipeline_w128(const uint64_t* a, uint64_t a_bits, const u
     // changeRepr into TGF(2^256): bit-sliced when the tiles fit the products, else M4R-4
     const bool w2bs = P.N % W2_TILE == 0 && !env_flag("GF2X_NO_W2_BS");
     if (w2bs) {
-        ProfScope ps("k_psi256_bs", (double)B * (((1ull << P.ma) + (1ull << P.mb)) * 16 + 2 * P.N * 32), st);
+        ProfScope ps("k_psi256_bs", (double)B * (((1ull << P.ma) + (1ull << P.mb)) * 16 + 2 * P.N * 32), st, 0.0, same ? 1 : 2);
         const size_t sm = 6 * W2_TILE * 4;
         if (same) {
             k_psi256_bs<<<grid_for(2 * plane / W2_TILE, 1, smc, 4), W2_THREADS, sm, st>>>(Sa, 1ull << P.ma, P.N, B, 2, Wa);
@@ -517,7 +517,7 @@ static gf2x_status run_pipeline_w128(const uint64_t* a, uint64_t a_bits, const u
         ProfScope ps("k_psi256", 2.0 * B * ((1ull << P.ma) * 16 + P.N * 32), st);
         k_psi256<<<grid_for(2 * plane, PSI256_THREADS, smc, 4), PSI256_THREADS, 0, st>>>(Sa, 1ull << P.ma, P.N, B, 2, T256, Wa);
     } else {
-        ProfScope ps("k_psi256", (double)B * (((1ull << P.ma) + (1ull << P.mb)) * 16 + 2 * P.N * 32), st);
+        ProfScope ps("k_psi256", (double)B * (((1ull << P.ma) + (1ull << P.mb)) * 16 + 2 * P.N * 32), st, 0.0, 2);
         k_psi256<<<grid_for(plane, PSI256_THREADS, smc, 4), PSI256_THREADS, 0, st>>>(Sa, 1ull << P.ma, P.N, B, 1, T256, Wa);
         k_psi256<<<grid_for(plane, PSI256_THREADS, smc, 4), PSI256_THREADS, 0, st>>>(Sb, 1ull << P.mb, P.N, B, 1, T256, Wb);
     }
@@ -535,7 +535,7 @@ static gf2x_status run_pipeline_w128(const uint64_t* a, uint64_t a_bits, const u
     if (stop_stage == 2) return GF2X_OK;
     // pointmul in TGF(2^256): Karatsuba over TGF(2^128)
     {
-        ProfScope ps("k_w128_sums", 2.0 * plane * 48, st);
+        ProfScope ps("k_w128_sums", 2.0 * plane * 48, st, 0.0, 2);
         k_w128_sums<<<grid_for(plane, 256, smc, 8), 256, 0, st>>>(Wa, plane, Ta);
         k_w128_sums<<<grid_for(plane, 256, smc, 8), 256, 0, st>>>(Wb, plane, Tb);
     }
@@ -590,24 +590,7 @@ static gf2x_status mul_common_w128(const uint64_t* a, uint64_t a_bits, const uin
     PlanW128 P;
     if ((s = make_plan_w128(a_bits, b_bits, batch, P)) != GF2X_OK) return s;
     void* ws;
-    {
-        std::lock_guard<std::mutex> lk(g_mu);
-        auto& ent = ds->ws[st];
-        if (ent.second < P.bytes) {
-            if (ent.first) {
-                cudaStreamSynchronize(st);
-                cudaFree(ent.first);
-                ent.first = nullptr;
-                ent.second = 0;
-            }
-            void* p = nullptr;
-            cudaError_t e = cudaMalloc(&p, P.bytes);
-            if (e != cudaSuccess) return fail(GF2X_ENOMEM, std::string("workspace: ") + cudaGetErrorString(e));
-            ent.first = p;
-            ent.second = P.bytes;
-        }
-        ws = ent.first;
-    }
+    if ((s = stream_workspace(ds, st, P.bytes, &ws)) != GF2X_OK) return s;
     if ((s = run_pipeline_w128(a, a_bits, b, b_bits, c, P, ws, ds, st, stop_stage)) != GF2X_OK) return s;
     if (stop_stage && stage_out) {   // (N, 4) words: element i = (lo plane i, hi plane i) of operand a, product 0
         const unsigned char* W = reinterpret_cast<unsigned char*>(ws) + P.off_wa;

@@ -1,6 +1,6 @@
 """Summarise ncu outputs into profiles/ (tracked).
 
-python profiles/summarize_ncu.py <launches.csv> <full.ncu-rep> <tag> <config> ["<launch-list command>"]
+python profiles/summarize_ncu.py <launches.csv> <full.ncu-rep> <tag> <config> ["<launch-list command>"] [multiplies]
 writes profiles/<tag>_launches.md, profiles/<tag>_kernels.md and updates profiles/ncu_traffic.json
 (per-kernel-class DRAM bytes per launch, read by bench.py as roofline.traffic).
 """
@@ -47,6 +47,7 @@ def to_unit(v, u, target):
 def main():
     lpath, rep, tag, cfg = sys.argv[1:5]
     what = sys.argv[5] if len(sys.argv) > 5 else "one warm multiply"
+    nmul = int(sys.argv[6]) if len(sys.argv) > 6 else 1   # multiplies covered by the launch list
     per = launches(lpath)
     cls = collections.OrderedDict()
     for (i, k), m in per.items():
@@ -87,6 +88,9 @@ def main():
     for k, v in traffic.items():   # per-launch average over template variants of one bench kernel name
         agg.setdefault(bname(k), []).append((cls[k][0], v))
     allt[cfg] = {k: sum(n * v for n, v in lst) / sum(n for n, _ in lst) for k, lst in agg.items()}
+    # whole multiply: DRAM bytes and launches over all passes (SURVEY §8(d) "bytes over all passes")
+    allt[cfg]["__step_dram_bytes"] = sum(c[2] for c in cls.values()) / nmul
+    allt[cfg]["__step_launches"] = sum(c[0] for c in cls.values()) / nmul
     json.dump(allt, open(tj, "w"), indent=1)
     # full capture
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -110,7 +114,7 @@ def main():
                   and h.endswith("_per_issue_active.ratio")]
     units = dict(zip(hdr, rows[1]))
     lines = [f"# ncu --set full --clock-control none, {cfg} ({tag}): every kernel of one warm multiply "
-             "(tests/prof_run.py)\n", "| kernel | grid x block | " + " | ".join(n for _, n in keys) +
+             "(tools/dev/prof_run.py)\n", "| kernel | grid x block | " + " | ".join(n for _, n in keys) +
              " | top stalls (warp-cycles per issue) |", "|---|---|" + "---|" * len(keys) + "---|"]
     for r in data:
         d = dict(zip(hdr, r))

@@ -1,6 +1,6 @@
 """A/B kernel timing for tuning: per-kernel device ms of one config for several builds of the library.
 
-python tests/ab_bench.py CONFIG REPS LIB[@VAR=VAL,...] [...]   (run on the GPU box; alternates the
+python tools/dev/ab_bench.py CONFIG REPS LIB[@VAR=VAL,...] [...]   (run on the GPU box; alternates the
 libraries in fresh subprocesses, 3 rounds, prints the per-kernel median ms per multiply of each; the
 optional @VAR=VAL list sets environment knobs of that run, e.g. lib.so@GF2X_BOT_B=6)
 """
@@ -10,7 +10,7 @@ import statistics
 import subprocess
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 
 
 def child(cfg, reps, lib):

@@ -1,8 +1,8 @@
-"""Ad-hoc: batched multiply vs oracle, listing mismatching pairs.  python tests/gpu_batch_debug.py"""
+"""Ad-hoc: batched multiply vs oracle, listing mismatching pairs.  python tools/dev/gpu_batch_debug.py"""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 

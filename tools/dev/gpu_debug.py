@@ -1,11 +1,11 @@
 """Ad-hoc GPU debugging aid: stage-by-stage comparison of the CUDA path with the oracle.
 
-python tests/gpu_debug.py [bits ...]
+python tools/dev/gpu_debug.py [bits ...]
 """
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import time
 
 import numpy as np

@@ -1,10 +1,10 @@
 """Small workload touching every kernel, for compute-sanitizer (racecheck / memcheck / synccheck).
 
-python tests/gpu_sanitize_run.py   -- checks the products against brute force / Karatsuba."""
+python tools/dev/gpu_sanitize_run.py   -- checks the products against brute force / Karatsuba."""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 

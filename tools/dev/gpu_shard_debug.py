@@ -1,8 +1,8 @@
-"""Ad-hoc: sharded-multiply simulation vs oracle.  python tests/gpu_shard_debug.py"""
+"""Ad-hoc: sharded-multiply simulation vs oracle.  python tools/dev/gpu_shard_debug.py"""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import time
 
 import numpy as np

@@ -1,9 +1,9 @@
 """Ad-hoc: device time of the sharded decomposition simulated on one GPU (all virtual ranks in sequence),
-per-rank kernel breakdown via the profiling hook.  python tests/gpu_shard_timing.py [bits]"""
+per-rank kernel breakdown via the profiling hook.  python tools/dev/gpu_shard_timing.py [bits]"""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 

@@ -1,11 +1,11 @@
 """One warm multiply of a BASELINE config through the C ABI (for ncu launch lists / captures).
 
-python tests/prof_run.py c4a [reps]
+python tools/dev/prof_run.py c4a [reps]
 """
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 
 import numpy as np
 import torch

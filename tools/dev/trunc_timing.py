@@ -1,5 +1,5 @@
 """Dev timing (not collected by pytest): the staircase with and without the truncated FFT.
-python tests/trunc_timing.py            (run twice: plain and with GF2X_NO_TRUNC=1)"""
+python tools/dev/trunc_timing.py            (run twice: plain and with GF2X_NO_TRUNC=1)"""
 import os
 import sys
 

@@ -1,5 +1,5 @@
 """Dev timing (not collected by pytest): a long times a short operand, truncated vs full transform.
-python tests/trunc_unbalanced_timing.py   (and with GF2X_NO_TRUNC=1)"""
+python tools/dev/trunc_unbalanced_timing.py   (and with GF2X_NO_TRUNC=1)"""
 import os
 import sys
 
