@@ -74,15 +74,17 @@ def load(path: str = LIB_PATH):
     L.gf2x_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
     L.gf2x_comm_destroy.argtypes = [vp]
     L.gf2x_comm_peer_memory.argtypes = [vp]
-    L.gf2x_comm_check.argtypes = [vp]
-    L.gf2x_comm_wait.argtypes = [vp, vp, ctypes.c_double]
-    L.gf2x_comm_abort.argtypes = [vp]
+    if hasattr(L, "gf2x_comm_check"):   # (older builds, loaded by the A/B tools, lack these)
+        L.gf2x_comm_check.argtypes = [vp]
+        L.gf2x_comm_wait.argtypes = [vp, vp, ctypes.c_double]
+        L.gf2x_comm_abort.argtypes = [vp]
     L.gf2x_mul_sharded.argtypes = [vp, vp, u64, vp, vp, vp]
     L.gf2x_mul_sharded_sim.argtypes = [vp, vp, u64, vp, i32, vp]
     L.gf2x_debug_shard_stage.argtypes = [vp, vp, u64, i32, i32, vp, vp]
     for name in ("gf2x_comm_unique_id", "gf2x_comm_init", "gf2x_comm_destroy", "gf2x_mul_sharded", "gf2x_mul_sharded_sim",
                  "gf2x_debug_shard_stage", "gf2x_comm_check", "gf2x_comm_wait", "gf2x_comm_abort"):
-        getattr(L, name).restype = i32
+        if hasattr(L, name):
+            getattr(L, name).restype = i32
     L.gf2x_plan.argtypes = [u64, u64, i64, ctypes.c_char_p, sz]
     L.gf2x_plan.restype = i32
     L.gf2x_shard_plan.argtypes = [u64, i32, ctypes.c_char_p, sz]

@@ -149,9 +149,8 @@ __device__ __forceinline__ void cp_async_unit(T* dst, const T* src) {
 // Thread (column c = tid mod C, row lane rl = tid / C) owns rows rl, rl + RS, ... (RS = threads / C) of
 // its class; double-buffered: the next tile's rows are prefetched with cp.async during the steps.
 template <typename T>
-__global__ void __launch_bounds__(RES_THREADS, 3) k_cvt_res(CvtResParams p) {
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    T* data = reinterpret_cast<T*>(p.data);
+__device__ __forceinline__ void cvt_res_tiles(const CvtResParams& p, T* data, uint64_t t_first, uint64_t t_step,
+                                              unsigned char* smem_raw) {
     const uint32_t M = (1u << p.K) - 1;
     const uint32_t C = 1u << p.C_log;
     const uint32_t nrb = (M + C - 1) >> p.C_log;
@@ -177,11 +176,11 @@ __global__ void __launch_bounds__(RES_THREADS, 3) k_cvt_res(CvtResParams p) {
                 if (i < span) cp_async_unit<T>(buf + ((r << p.C_log) | c), dp + i);
             }
     };
-    if (blockIdx.x < ntiles) prefetch(blockIdx.x, reinterpret_cast<T*>(smem_raw));
+    if (t_first < ntiles) prefetch(t_first, reinterpret_cast<T*>(smem_raw));
     cp_async_commit();
     int k = 0;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, k++) {
-        if (t + gridDim.x < ntiles) prefetch(t + gridDim.x, reinterpret_cast<T*>(smem_raw + ((k + 1) & 1) * bufsz));
+    for (uint64_t t = t_first; t < ntiles; t += t_step, k++) {
+        if (t + t_step < ntiles) prefetch(t + t_step, reinterpret_cast<T*>(smem_raw + ((k + 1) & 1) * bufsz));
         cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
@@ -238,6 +237,12 @@ __global__ void __launch_bounds__(RES_THREADS, 3) k_cvt_res(CvtResParams p) {
         __syncthreads();
     }
     cp_async_wait<0>();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(RES_THREADS, 3) k_cvt_res(CvtResParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    cvt_res_tiles<T>(p, reinterpret_cast<T*>(p.data), blockIdx.x, gridDim.x, smem_raw);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -347,13 +352,12 @@ __device__ __forceinline__ void rb_slot(const CvtRbParams& p, uint32_t s, uint64
 }
 
 template <typename T, int WB>
-__global__ void __launch_bounds__(RB_THREADS, 3) k_cvt_rb(CvtRbParams p) {
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
+__device__ __forceinline__ void cvt_rb_tiles(const CvtRbParams& p, T* data, uint64_t t_first, uint64_t t_step,
+                                             unsigned char* smem_raw) {
     constexpr uint32_t EPC = 16 / sizeof(T);   // units per 16-byte copy
     const uint32_t ncols = 1u << p.C, nrows = 1u << p.R, nslots = ncols << p.R;
     const uint32_t bufsz = ((ncols * (nrows + (p.mode ? RB_PAD(T) : 0)) * (uint32_t)sizeof(T)) + 127) & ~127u;
     // (buffers are addressed from smem_raw directly so the compiler emits LDS/STS, not generic LD/ST)
-    T* data = reinterpret_cast<T*>(p.data);
     const uint64_t tiles_per_pair = p.units_per_pair >> (p.R + p.C);
     const uint64_t ntiles = tiles_per_pair * p.batch;
     const int midbits = p.mode ? 0 : p.r_lo - p.C;
@@ -379,12 +383,12 @@ __global__ void __launch_bounds__(RB_THREADS, 3) k_cvt_rb(CvtRbParams p) {
             cp_async16(buf + sm, gp);
         }
     };
-    if (blockIdx.x < ntiles) prefetch(blockIdx.x, reinterpret_cast<T*>(smem_raw));
+    if (t_first < ntiles) prefetch(t_first, reinterpret_cast<T*>(smem_raw));
     cp_async_commit();
     int k = 0;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, k++) {
+    for (uint64_t t = t_first; t < ntiles; t += t_step, k++) {
         T* buf = reinterpret_cast<T*>(smem_raw + (k & 1) * bufsz);
-        if (t + gridDim.x < ntiles) prefetch(t + gridDim.x, reinterpret_cast<T*>(smem_raw + ((k + 1) & 1) * bufsz));
+        if (t + t_step < ntiles) prefetch(t + t_step, reinterpret_cast<T*>(smem_raw + ((k + 1) & 1) * bufsz));
         cp_async_commit();
         cp_async_wait<1>();   // this tile's copies (all but the newest group) have landed
         __syncthreads();
@@ -411,4 +415,218 @@ __global__ void __launch_bounds__(RB_THREADS, 3) k_cvt_rb(CvtRbParams p) {
         __syncthreads();   // the buffer is refilled by the prefetch two tiles on
     }
     cp_async_wait<0>();
+}
+
+template <typename T, int WB>
+__global__ void __launch_bounds__(RB_THREADS, 3) k_cvt_rb(CvtRbParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    cvt_rb_tiles<T, WB>(p, reinterpret_cast<T*>(p.data), blockIdx.x, gridDim.x, smem_raw);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Top Taylor run of a conversion (k_cvt_top): the whole Taylor part of CVT(q) with K = 16 (levels
+// q .. K+1 of a 2^q-unit chunk; Alg. 3 l.531 with Alg. 2's divisions), as residue classes
+// i = r M + c (M = 2^K - 1, R17) in tiles of 2^C_log classes x all rows.
+//
+// With B = q - K row bits, write i = r 2^K + (c - r) for r <= c.  Level l (u = 2^(l-1-K), h = u 2^K) makes
+// the units at position (i mod 2^l) in [u, h + u) targets of f[t] ^= f[t + u M] -- the source is row r + u
+// of the same class.  For every class c >= 2^B - 1 + 2^(B-1) ("generic"; all but the first ~1.5 2^B of the
+// 2^K - 1 classes) the class has exactly 2^B rows, all r <= c with c - r >= u, and the position test reduces
+// to (r mod 2u) < u, i.e. bit log2(u) of r is clear.  The run on such a class is therefore
+//     for every row bit b (any order):  x[r] ^= x[r + 2^b]  for r with bit b clear,
+// the superset-sum transform over the B row bits: data-independent, its steps commute, and it is its own
+// inverse (the inverse run is the same transform).  Generic tiles run it register-blocked, <= 4 row bits per
+// phase through shared memory.  Tiles holding the first classes run Alg. 2's steps exactly, one sweep per
+// phase (A: targets [h, h+u), B: [u, h); forward A then B, inverse B then A, levels in Alg. 3's order), as
+// k_cvt_res does.  Pinned by the stage / end-to-end parity tests against the oracle's Alg. 3.
+//
+// Split can be fused into a forward run: the tile is then read from the caller's operand
+// words (pairs [0, batch0) from src0, the rest from src1; words >= nsrc read as 0, the last one masked
+// to `bits`) instead of the scratch array it writes.
+// ---------------------------------------------------------------------------------------------
+struct CvtTopParams {
+    void* data;
+    uint64_t units_per_pair, batch;   // one chunk per pair: units_per_pair = 2^q
+    int q, K, B, inverse, C_log;
+    uint32_t c_gen;                   // classes >= c_gen take the transform path
+    const uint64_t* src0;             // fused Split (T = u64, forward): operand words, or null
+    const uint64_t* src1;
+    uint64_t batch0, nsrc, bits;
+};
+#define TOP_THREADS 256
+
+template <int NB>
+__device__ __forceinline__ void top_phase(uint32_t* s32, uint32_t items, int b0, int Bt, uint32_t WC) {
+    // item = (word w of the unit, class c) fastest (contiguous words across lanes), then the row bits
+    // outside [b0, b0 + NB); the NB row bits in [b0, b0 + NB) are the register dimension
+    const uint32_t rowstride = WC;   // words per tile row
+    for (uint32_t it = threadIdx.x; it < items; it += blockDim.x) {
+        const uint32_t wc = it % WC, rest = it / WC;
+        const uint32_t r0 = (rest & ((1u << b0) - 1)) | ((rest >> b0) << (b0 + NB));
+        uint32_t* p = s32 + r0 * rowstride + wc;
+        const uint32_t js = (rowstride << b0);
+        uint32_t v[1 << NB];
+#pragma unroll
+        for (int j = 0; j < (1 << NB); j++) v[j] = p[j * js];
+#pragma unroll
+        for (int k = 0; k < NB; k++)
+#pragma unroll
+            for (int j = 0; j < (1 << NB); j++)
+                if (!(j & (1 << k))) v[j] ^= v[j | (1 << k)];
+#pragma unroll
+        for (int j = 0; j < (1 << NB); j++) p[j * js] = v[j];
+    }
+    (void)Bt;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TOP_THREADS, 2) k_cvt_top(CvtTopParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    T* data = reinterpret_cast<T*>(p.data);
+    constexpr uint32_t W = sizeof(T) / 4;   // 32-bit words per unit
+    const uint32_t M = (1u << p.K) - 1;
+    const uint32_t C = 1u << p.C_log;
+    const uint32_t nrb = (M + C - 1) >> p.C_log;
+    const uint32_t rows = (1u << p.B) + 1;
+    const uint32_t span = 1u << p.q;
+    const uint64_t ntiles = p.batch * nrb;
+    const uint32_t nslots = rows << p.C_log;
+    const uint32_t bufsz = (nslots * (uint32_t)sizeof(T) + 127) & ~127u;
+    const bool fuse = p.src0 != nullptr;   // (T = u64)
+    const uint32_t rem = (uint32_t)(p.bits & 63);
+    auto prefetch = [&](uint64_t t, T* buf) {
+        const uint64_t pair = t / nrb;
+        const uint32_t c0 = (uint32_t)(t - pair * nrb) << p.C_log;
+        T* dp = data + pair * p.units_per_pair;
+        const uint64_t* sp = fuse ? (pair < p.batch0 ? p.src0 + pair * p.nsrc : p.src1 + (pair - p.batch0) * p.nsrc) : nullptr;
+        for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
+            const uint32_t r = s >> p.C_log, c = c0 + (s & (C - 1));
+            const uint32_t i = r * M + c;
+            if (c >= M || i >= span) continue;
+            if (fuse) {
+                const uint32_t n = (uint64_t)i < p.nsrc ? 8u : 0u;   // src-size 0: zero fill (words >= nsrc)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(buf + s)),
+                             "l"(sp + (i < p.nsrc ? i : 0)), "r"(n) : "memory");
+            } else {
+                cp_async_unit<T>(buf + s, dp + i);
+            }
+        }
+    };
+    if (blockIdx.x < ntiles) prefetch(blockIdx.x, reinterpret_cast<T*>(smem_raw));
+    cp_async_commit();
+    int kb = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, kb++) {
+        if (t + gridDim.x < ntiles) prefetch(t + gridDim.x, reinterpret_cast<T*>(smem_raw + ((kb + 1) & 1) * bufsz));
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        T* tile = reinterpret_cast<T*>(smem_raw + (kb & 1) * bufsz);
+        const uint64_t pair = t / nrb;
+        const uint32_t c0 = (uint32_t)(t - pair * nrb) << p.C_log;
+        if (fuse && rem && p.nsrc && (uint32_t)((p.nsrc - 1) % M) - c0 < C) {
+            // the operand's last word lies in this tile: clear its bits >= bits (Split's mask)
+            if (threadIdx.x == 0) {
+                const uint32_t i = (uint32_t)(p.nsrc - 1);
+                uint64_t* w = reinterpret_cast<uint64_t*>(tile) + (((i / M) << p.C_log) | (i % M - c0));
+                *w &= (1ull << rem) - 1;
+            }
+            __syncthreads();
+        }
+        if (c0 >= p.c_gen) {
+            // superset-sum transform over the B row bits, <= 4 bits per phase
+            uint32_t* s32 = reinterpret_cast<uint32_t*>(tile);
+            const uint32_t WC = W << p.C_log;
+            for (int b0 = 0; b0 < p.B; b0 += 4) {
+                const int nb = min(4, p.B - b0);
+                const uint32_t items = WC << (p.B - nb);
+                if (nb == 4) top_phase<4>(s32, items, b0, p.B, WC);
+                else if (nb == 3) top_phase<3>(s32, items, b0, p.B, WC);
+                else if (nb == 2) top_phase<2>(s32, items, b0, p.B, WC);
+                else top_phase<1>(s32, items, b0, p.B, WC);
+                __syncthreads();
+            }
+        } else {
+            // Alg. 2's steps exactly: per level the phase-A sweep (targets [h, h+u)) and the phase-B sweep
+            // ([u, h)), each f[t] ^= f[t + u M] = row r + u of the class
+            const int nl = p.q - p.K;
+            for (int o = 0; o < nl; o++) {
+                const int lg = p.inverse ? p.K + 1 + o : p.q - o;
+                const uint32_t u = 1u << (lg - 1 - p.K), h = 1u << (lg - 1), segm = (lg >= 32) ? 0xFFFFFFFFu : ((1u << lg) - 1);
+                for (int ph = 0; ph < 2; ph++) {
+                    const bool A = (ph == 0) != (p.inverse != 0);
+                    const uint32_t lo = A ? h : u, len = A ? u : h - u;
+                    for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
+                        const uint32_t r = s >> p.C_log, c = c0 + (s & (C - 1));
+                        const uint32_t i = r * M + c;
+                        if (c >= M || i >= span) continue;
+                        if (((i & segm) - lo) < len) tile[s] = xor_t<T>(tile[s], tile[s + (u << p.C_log)]);
+                    }
+                    __syncthreads();
+                }
+            }
+        }
+        T* dp = data + pair * p.units_per_pair;
+        for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
+            const uint32_t r = s >> p.C_log, c = c0 + (s & (C - 1));
+            const uint32_t i = r * M + c;
+            if (c < M && i < span) dp[i] = tile[s];
+        }
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------------------------
+// CVT(16) slab pass (k_cvt_slab): the inner conversion of the top node on every 2^16-unit slab -- its
+// K = 8 Taylor run (levels 16 .. 9, residue classes mod 255, R17) and its two CVT(8) nodes (bits [0, 8) and
+// [8, 16), register-blocked, R18) -- in ONE launch instead of three HBM passes (SURVEY §8(d) P3's slab).
+// A thread-block cluster owns one slab at a time: each phase's tiles are split over the cluster's CTAs, and
+// the phases are separated by cluster barriers (barrier.cluster arrive.release / wait.acquire: the global
+// writes of one phase are visible to every CTA of the cluster in the next one; the acquire invalidates L1).
+// The slab (512 KB u64 / 1 MB u128) stays in L2 between the phases, so HBM sees one read and one write per
+// unit; the ~18 slabs in flight are far below the 126 MB L2.  Same device code as k_cvt_res / k_cvt_rb.
+// Order (Alg. 3, with R14): forward Taylor run, CVT(8) [0,8), CVT(8) [8,16); inverse reversed.
+// ---------------------------------------------------------------------------------------------
+struct CvtSlabParams {
+    void* data;
+    uint64_t nslabs;
+    CvtResParams res;     // data / units_per_pair / batch set per slab
+    CvtRbParams rb_lo;    // CVT(8) on bits [0, 8)
+    CvtRbParams rb_hi;    // CVT(8) on bits [8, 16)
+    int inverse;
+};
+#define SLAB_THREADS 256
+#define SLAB_BITS 16
+#ifndef SLAB_MINB
+#define SLAB_MINB 2
+#endif
+
+template <typename T>
+__global__ void __launch_bounds__(SLAB_THREADS, SLAB_MINB) k_cvt_slab(CvtSlabParams P) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint32_t cs, cr;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(cs));
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(cr));
+    const uint64_t ncl = gridDim.x / cs, cid = blockIdx.x / cs;
+    T* data = reinterpret_cast<T*>(P.data);
+    auto csync = [] {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    };
+    for (uint64_t sl = cid; sl < P.nslabs; sl += ncl) {
+        T* base = data + (sl << SLAB_BITS);
+        if (!P.inverse) {
+            cvt_res_tiles<T>(P.res, base, cr, cs, smem_raw);
+            csync();
+            cvt_rb_tiles<T, 6>(P.rb_lo, base, cr, cs, smem_raw);
+            csync();
+            cvt_rb_tiles<T, 6>(P.rb_hi, base, cr, cs, smem_raw);
+        } else {
+            cvt_rb_tiles<T, 6>(P.rb_hi, base, cr, cs, smem_raw);
+            csync();
+            cvt_rb_tiles<T, 6>(P.rb_lo, base, cr, cs, smem_raw);
+            csync();
+            cvt_res_tiles<T>(P.res, base, cr, cs, smem_raw);
+        }
+        csync();   // (the next slab's first phase reuses shared memory only after every CTA left this one)
+    }
 }

@@ -172,7 +172,9 @@ __device__ __forceinline__ void fft_group(uint4* tile, uint32_t nslots, int s0, 
             const int lb = INV ? li : (r - 1 - li);   // local bit of this layer
             const int kk = ka + lb - p.k_lo;
             const int wbits = mg - glayer(p.map, ka + lb);   // the layer's constants are < 2^wbits
-            const int cls = wbits <= 2 ? 2 : (wbits <= 4 ? 4 : (wbits <= FFT_SMALL_MAX ? 8 : 0));
+            // (only passes holding the top layer (ZS) have such layers in the single-GPU plans; the others keep
+            // one code path: measured 6 % slower with the class test compiled into every pass)
+            const int cls = !ZS ? 0 : (wbits <= 2 ? 2 : (wbits <= 4 ? 4 : (wbits <= FFT_SMALL_MAX ? 8 : 0)));
             if (cls == 0) {
 #pragma unroll
                 for (int j = 0; j < (1 << r); j++) {
@@ -329,8 +331,9 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             const uint32_t blk = id + 1 - (1u << lg);
             const uint32_t lb = (uint32_t)(((uint64_t)base & ~((2ull << k) - 1)) | ((uint64_t)blk << (k + 1)));
             const uint32_t cst = layer_const(glayer(p.map, k), gidx(p.map, lb));
-            if (p.wt_shared) build_tab_row<true>(tabs + id * 128, cst, (int)(i & 7), wts, kbt + id * 8);
-            else build_tab_row<false>(tabs + id * 128, cst, (int)(i & 7), p.tabs->wt, kbt + id * 8);
+            uint32_t* kbo = ZS ? kbt + id * 8 : nullptr;
+            if (p.wt_shared) build_tab_row<true>(tabs + id * 128, cst, (int)(i & 7), wts, kbo);
+            else build_tab_row<false>(tabs + id * 128, cst, (int)(i & 7), p.tabs->wt, kbo);
             if ((i & 7) == 0) zf[id] = cst == 0;
         }
         tab_key = key;

@@ -495,6 +495,10 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
 #undef RB_ATTR
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_res<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_res<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_cvt_top<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_cvt_top<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_cvt_slab<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_cvt_slab<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_ipsi_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_ipsi_bs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         st.tabs = d;
@@ -748,6 +752,7 @@ static int lucas_shifts(int p, uint64_t* off) {   // 2^q for q subset of p, q !=
 
 struct Plan {
     uint64_t na, nb, N, batch;
+    uint64_t a_bits = 0, b_bits = 0;
     int m, ma, mb;
     std::vector<CvtPass> cvt_a, cvt_b, icvt;
     std::vector<FftPass> fft;
@@ -785,6 +790,8 @@ static gf2x_status make_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, Pl
     if (batch < 0) return fail(GF2X_EINVAL, "negative batch");
     P.na = (a_bits + 63) / 64;
     P.nb = (b_bits + 63) / 64;
+    P.a_bits = a_bits;
+    P.b_bits = b_bits;
     P.batch = (uint64_t)batch;
     const uint64_t L = P.na + P.nb - 1;
     P.m = ceil_log2_u64(L);
@@ -813,13 +820,29 @@ static gf2x_status make_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, Pl
     return GF2X_OK;
 }
 
-static int launches_of_split(const CvtSplit& S, const std::vector<CvtPass>& full) {
-    return S.p < 0 ? (int)full.size() : 1 + (int)S.lo.size() + (int)S.hi.size();
+static bool slab_triple(const std::vector<CvtPass>& v, size_t i, int m);
+// launches of a planned conversion (a CVT(16) slab triple is one launch)
+static int cvt_launches(const std::vector<CvtPass>& v, int m) {
+    int n = 0;
+    for (size_t i = 0; i < v.size(); i++, n++)
+        if (slab_triple(v, i, m)) i += 2;
+    return n;
+}
+static int launches_of_split(const CvtSplit& S, const std::vector<CvtPass>& full, int mfull) {
+    return S.p < 0 ? cvt_launches(full, mfull) : 1 + cvt_launches(S.lo, S.p) + cvt_launches(S.hi, S.j);
+}
+static int top_rowbits(const CvtPass& p, int m);
+// Split fused into the first forward conversion pass: a and b convert in one launch (equal shapes, contiguous
+// scratch) and that pass is a k_cvt_top pass
+static bool split_fused(const Plan& P) {
+    const bool same = P.ma == P.mb && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8 && P.sa.p < 0 && P.sb.p < 0;
+    return same && P.a_bits == P.b_bits && !P.cvt_a.empty() && top_rowbits(P.cvt_a[0], P.ma) >= 0 && !env_flag("GF2X_NO_FUSED_SPLIT");
 }
 static int launches_of(const Plan& P) {
     const bool same = P.ma == P.mb && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8 && P.sa.p < 0 && P.sb.p < 0;
-    int n = 2;  // prep a, b
-    n += launches_of_split(P.sa, P.cvt_a) + (same ? 0 : launches_of_split(P.sb, P.cvt_b)) + launches_of_split(P.ic, P.icvt);
+    int n = split_fused(P) ? 0 : 2;  // prep a, b
+    n += launches_of_split(P.sa, P.cvt_a, P.ma) + (same ? 0 : launches_of_split(P.sb, P.cvt_b, P.mb)) +
+         launches_of_split(P.ic, P.icvt, P.m);
     const int nd = (int)P.fft.size() - 1;
     n += (same ? 1 : 2) * (nd ? nd : 1);      // forward a, b (or the changeRepr-only pass)
     n += 1;                      // fused bottom
@@ -837,15 +860,161 @@ static int grid_for(uint64_t items, int per_block, int sm_count, int occ) {
     return (int)g;
 }
 
+// A residue pass that is the whole Taylor run of the top node with K = 16 over one chunk per pair (levels
+// m .. 17) runs as k_cvt_top (generic classes as the superset-sum transform) when its rows fit a tile
+static int top_rowbits(const CvtPass& p, int m) {
+    if (!p.res || p.ops.empty() || env_flag("GF2X_NO_CVT_TOP")) return -1;
+    const int K = p.ops[0].K;
+    if (K != 16 || p.q != m || p.ops.front().lg != m || p.ops.back().lg != K + 1) return -1;
+    if ((int)p.ops.size() != m - K) return -1;
+    const int B = m - K;
+    return (B >= 1 && B <= 9) ? B : -1;
+}
+// Split fused into the first forward conversion pass (k_cvt_top reads the caller's operands)
+struct CvtSrc {
+    const uint64_t* a;
+    const uint64_t* b;
+    uint64_t batch0, n, bits;
+};
+
+template <typename T>
+static gf2x_status launch_cvt_top(const CvtPass& p, int B, T* data, int m, uint64_t batch, bool inverse, int sm_count,
+                                  cudaStream_t st, const CvtSrc* src) {
+    CvtTopParams prm;
+    memset(&prm, 0, sizeof(prm));
+    prm.data = data;
+    prm.units_per_pair = 1ull << m;
+    prm.batch = batch;
+    prm.q = m; prm.K = 16; prm.B = B; prm.inverse = inverse ? 1 : 0;
+    const size_t row_bytes = (((size_t)1 << B) + 1) * sizeof(T);   // one class, all rows
+    int C_log = 0;
+    while (C_log < 5 && row_bytes * ((size_t)2 << C_log) <= 33 * 1024) C_log++;
+    prm.C_log = C_log;
+    prm.c_gen = (1u << B) - 1 + (1u << (B - 1));
+    if (src) {
+        prm.src0 = src->a; prm.src1 = src->b; prm.batch0 = src->batch0; prm.nsrc = src->n; prm.bits = src->bits;
+    }
+    const size_t bufsz = ((row_bytes << C_log) + 127) & ~(size_t)127;
+    const size_t sm = 2 * bufsz;
+    const uint64_t M = (1ull << 16) - 1;
+    const uint64_t ntiles = batch * ((M + (1ull << C_log) - 1) >> C_log);
+    const int occ = std::max(1, std::min(3, (int)(200 * 1024 / (sm + 1024))));
+    ProfScope ps(sizeof(T) == 8 ? "k_cvt_top<u64>" : "k_cvt_top<u128>",
+                 (src ? 1.0 : 2.0) * (double)(1ull << m) * batch * sizeof(T) + (src ? (double)src->n * batch * 8 : 0.0), st);
+    k_cvt_top<T><<<grid_for(ntiles, 1, sm_count, occ), TOP_THREADS, sm, st>>>(prm);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GF2X_OK : fail(GF2X_ECUDA, std::string("cvt top launch: ") + cudaGetErrorString(e));
+}
+
+// The passes i, i+1, i+2 of a plan are one CVT(16) node on 2^16-unit slabs (its K = 8 residue run, CVT(8) on
+// bits [0, 8), CVT(8) on [8, 16)): they run as one k_cvt_slab launch
+static bool slab_triple(const std::vector<CvtPass>& v, size_t i, int m) {
+    if (i + 2 >= v.size() || m < SLAB_BITS || !env_flag("GF2X_CVT_SLAB")) return false;
+    const CvtPass &a = v[i], &b = v[i + 1], &c = v[i + 2];
+    if (!a.res || a.ops[0].K != 8 || a.q != 16 || a.ops.front().lg != 16 || a.ops.back().lg != 9 || a.ops.size() != 8)
+        return false;
+    if (!b.rb || b.rbp.r_lo != 0 || b.rbp.R != 8 || b.rbp.mode != 1 || b.rb_wb != 6) return false;
+    if (!c.rb || c.rbp.r_lo != 8 || c.rbp.R != 8 || c.rbp.mode != 0 || c.rb_wb != 6) return false;
+    return true;
+}
+static CvtResParams res_params(const CvtPass& p, void* data, uint64_t per, uint64_t batch, bool inverse) {
+    CvtResParams prm;
+    prm.data = data;
+    prm.units_per_pair = per;
+    prm.batch = batch;
+    prm.q = p.q;
+    prm.K = p.ops[0].K;
+    prm.lg_hi = p.ops.front().lg;
+    prm.lg_lo = p.ops.back().lg;
+    prm.inverse = inverse ? 1 : 0;
+    prm.C_log = p.C_log;
+    prm.rows = p.rows;
+    return prm;
+}
+static size_t res_smem(const CvtPass& p, size_t unit) { return 2 * ((((size_t)p.rows << p.C_log) * unit + 127) & ~(size_t)127); }
+static size_t rb_smem(const CvtRbParams& q, size_t unit) {
+    const size_t ncols = (size_t)1 << q.C, nrows = (size_t)1 << q.R;
+    return 2 * ((ncols * (nrows + (q.mode ? 16 / unit : 0)) * unit + 127) & ~(size_t)127);
+}
+
+template <typename T>
+static gf2x_status launch_cvt_slab(const std::vector<CvtPass>& v, size_t i, T* data, int m, uint64_t batch, bool inverse,
+                                   int sm_count, cudaStream_t st) {
+    CvtSlabParams P;
+    memset(&P, 0, sizeof(P));
+    P.data = data;
+    P.nslabs = (1ull << (m - SLAB_BITS)) * batch;
+    P.inverse = inverse ? 1 : 0;
+    P.res = res_params(v[i], data, 1ull << SLAB_BITS, 1, inverse);
+    P.rb_lo = v[i + 1].rbp;
+    P.rb_hi = v[i + 2].rbp;
+    for (CvtRbParams* q : {&P.rb_lo, &P.rb_hi}) {
+        q->units_per_pair = 1ull << SLAB_BITS;
+        q->batch = 1;
+        q->inverse = inverse ? 1 : 0;
+    }
+    const size_t sm = std::max(res_smem(v[i], sizeof(T)), std::max(rb_smem(P.rb_lo, sizeof(T)), rb_smem(P.rb_hi, sizeof(T))));
+    static const int CS = env_int("GF2X_SLAB_CLUSTER", 8, 2, 8);
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.blockDim = dim3(SLAB_THREADS);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    // as many clusters as can be resident at once (a persistent loop over the slabs)
+    static int max_cl[2] = {0, 0};
+    int& mc = max_cl[sizeof(T) == 8 ? 0 : 1];
+    if (!mc) {
+        cfg.gridDim = dim3(CS * (sm_count / CS));
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_cvt_slab<T>, &cfg) != cudaSuccess || n < 1) {
+            cudaGetLastError();
+            n = sm_count / CS;
+        }
+        mc = n;
+    }
+    const uint64_t ncl = std::min<uint64_t>(P.nslabs, (uint64_t)mc);
+    cfg.gridDim = dim3((unsigned)(ncl * CS));
+    ProfScope ps(sizeof(T) == 8 ? "k_cvt_slab<u64>" : "k_cvt_slab<u128>", 2.0 * (double)(1ull << m) * batch * sizeof(T), st);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_cvt_slab<T>, P);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return e == cudaSuccess ? GF2X_OK : fail(GF2X_ECUDA, std::string("cvt slab launch: ") + cudaGetErrorString(e));
+}
+
 template <typename T>
 static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, uint64_t batch, bool inverse,
-                           int sm_count, cudaStream_t st) {
+                           int sm_count, cudaStream_t st, const CvtSrc* src = nullptr) {
     const uint64_t per = 1ull << m;
     std::vector<const CvtPass*> order;
     for (auto& p : passes) order.push_back(&p);
     if (inverse) std::reverse(order.begin(), order.end());
-    for (const CvtPass* pp : order) {
-        const CvtPass& p = *pp;
+    for (size_t oi = 0; oi < order.size(); oi++) {
+        // three passes forming a CVT(16) node on slabs: one cluster launch (in plan order i .. i+2)
+        {
+            const size_t pi = inverse ? passes.size() - 1 - oi : oi;   // plan index of this pass
+            const size_t first = inverse ? (pi >= 2 ? pi - 2 : passes.size()) : pi;
+            if (first < passes.size() && slab_triple(passes, first, m) && !(src && oi == 0)) {
+                gf2x_status s = launch_cvt_slab<T>(passes, first, data, m, batch, inverse, sm_count, st);
+                if (s != GF2X_OK) return s;
+                oi += 2;
+                continue;
+            }
+        }
+        const CvtPass& p = *order[oi];
+        const int topB = top_rowbits(p, m);
+        if (src && oi == 0 && (topB < 0 || inverse || sizeof(T) != 8))
+            return fail(GF2X_EINVAL, "fused Split needs a top Taylor pass first");
+        if (topB >= 0) {
+            gf2x_status s = launch_cvt_top<T>(p, topB, data, m, batch, inverse, sm_count, st, oi == 0 ? src : nullptr);
+            if (s != GF2X_OK) return s;
+            continue;
+        }
         if (p.rb) {
             CvtRbParams prm = p.rbp;
             prm.data = data;
@@ -1025,20 +1194,25 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
     uint4* Wb = reinterpret_cast<uint4*>(base + P.off_wb);
     const int smc = ds->sm_count;
     gf2x_status s;
-    // Split
-    {
-        ProfScope ps("k_prep", (double)P.batch * (P.na + (1ull << P.ma)) * 8, st);
-        k_prep<<<grid_for((1ull << P.ma) * P.batch, 256, smc, 8), 256, 0, st>>>(a, P.na, a_bits, P.ma, P.batch, Sa);
-    }
-    {
-        ProfScope ps("k_prep", (double)P.batch * (P.nb + (1ull << P.mb)) * 8, st);
-        k_prep<<<grid_for((1ull << P.mb) * P.batch, 256, smc, 8), 256, 0, st>>>(b, P.nb, b_bits, P.mb, P.batch, Sb);
+    // Split (fused into the first conversion pass when that pass reads the operands itself)
+    const bool fused = split_fused(P);
+    if (!fused) {
+        {
+            ProfScope ps("k_prep", (double)P.batch * (P.na + (1ull << P.ma)) * 8, st);
+            k_prep<<<grid_for((1ull << P.ma) * P.batch, 256, smc, 8), 256, 0, st>>>(a, P.na, a_bits, P.ma, P.batch, Sa);
+        }
+        {
+            ProfScope ps("k_prep", (double)P.batch * (P.nb + (1ull << P.mb)) * 8, st);
+            k_prep<<<grid_for((1ull << P.mb) * P.batch, 256, smc, 8), 256, 0, st>>>(b, P.nb, b_bits, P.mb, P.batch, Sb);
+        }
     }
     // BasisCvt on 64-bit blocks
-    // (one operand at a time: at the headline sizes each 64-bit block array fits the 126 MB L2 alone)
     // Sb | Wb directly follow Sa | Wa: one launch per pass for both operands
     const bool same = (P.ma == P.mb) && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8;
-    if (same && P.sa.p < 0 && P.sb.p < 0) {
+    if (fused) {
+        const CvtSrc src{a, b, P.batch, P.na, a_bits};
+        if ((s = run_cvt<uint64_t>(P.cvt_a, Sa, P.ma, 2 * P.batch, false, smc, st, &src)) != GF2X_OK) return s;
+    } else if (same && P.sa.p < 0 && P.sb.p < 0) {
         if ((s = run_cvt<uint64_t>(P.cvt_a, Sa, P.ma, 2 * P.batch, false, smc, st)) != GF2X_OK) return s;
     } else {
         if ((s = run_cvt_operand(P, true, Sa, smc, st)) != GF2X_OK) return s;

@@ -176,12 +176,12 @@ static int launches_of_trunc(const Plan& P, const TruncGeom& T) {
     const int k0 = fuse ? fl[0].k_lo - 1 : T.m - 2;
     const int nred = k0 >= T.j ? (k0 - T.j + 1 + 4) / 5 : 0;
     int n = 2;                                                             // prep a, b
-    n += launches_of_split(P.sa, P.cvt_a) + launches_of_split(P.sb, P.cvt_b);
+    n += launches_of_split(P.sa, P.cvt_a, P.ma) + launches_of_split(P.sb, P.cvt_b, P.mb);
     n += 3 * ((int)fl.size() - 1) + 1;                                     // lower: forward a, b, bottom, inverse
     n += 3 * ((int)fu.size() - 1) + 1;                                     // upper
     n += 2 * nred + 1;                                                     // Reduce (forward, g_lo), g_hi combine
     n += (P.na > T.H) + (P.nb > T.H);                                      // operand tails past H
-    n += launches_of_split(P.ic, P.icvt) + 1;                              // iBasisCvt, changeRepr^-1 + combine
+    n += launches_of_split(P.ic, P.icvt, P.m) + 1;                              // iBasisCvt, changeRepr^-1 + combine
     return n;
 }
 

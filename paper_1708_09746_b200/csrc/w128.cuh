@@ -604,11 +604,11 @@ static gf2x_status mul_common_w128(const uint64_t* a, uint64_t a_bits, const uin
 static int launches_of_w128(const PlanW128& P) {
     const bool same = P.ma == P.mb;
     int n = 2;                                                     // prep
-    n += (int)P.cvt_a.size() + (same ? 0 : (int)P.cvt_b.size());  // BasisCvt
+    n += cvt_launches(P.cvt_a, P.ma) + (same ? 0 : cvt_launches(P.cvt_b, P.mb));  // BasisCvt
     n += same ? 1 : 2;                                             // psi256
     const int nd = (int)P.fft.size() - 1;
     n += nd;                                                       // forward passes
     n += 1 + 2 + 3 + 1 + 1;                                        // bottom fwd, sums, 3 products, post, bottom inv
-    n += nd + (int)P.icvt.size() + 1;                              // inverse passes, iBasisCvt, ipsi256
+    n += nd + cvt_launches(P.icvt, P.m) + 1;                       // inverse passes, iBasisCvt, ipsi256
     return n;
 }
