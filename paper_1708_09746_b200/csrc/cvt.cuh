@@ -188,45 +188,56 @@ __device__ __forceinline__ void cvt_res_tiles(const CvtResParams& p, T* data, ui
         T* dp; uint32_t c0, cn;
         geom(t, dp, c0, cn);
         const bool colok = c < cn;
-        // unit index of the thread's row slot j (r = rl + j RS), span if the slot is empty
+        // unit index of the thread's row slot j (r = rl + j RS), 0 if the slot is empty (position 0 is never a
+        // target); the slot's tile index is s0 + j RES_THREADS (RS 2^C_log = blockDim = RES_THREADS)
         uint32_t ii[RES_MAXJ];
 #pragma unroll
         for (int j = 0; j < RES_SLOTS(T); j++) {
             const uint32_t r = rl + j * RS;
             const uint32_t i = r * M + c0 + c;
-            ii[j] = (colok && r < (uint32_t)p.rows && i < span) ? i : span;
+            ii[j] = (colok && r < (uint32_t)p.rows && i < span) ? i : 0u;
         }
+        const uint32_t s0 = (rl << p.C_log) | c;
         for (int o = 0; o < nsteps; o++) {
             const int lg = p.inverse ? p.lg_lo + o : p.lg_hi - o;
             const uint32_t h = 1u << (lg - 1), u = h >> p.K, segm = (2u << (lg - 1)) - 1;
             const uint32_t off = u << p.C_log;
-            // 64-bit units: unrolled over the row slots (independent chains); 128-bit units: rolled
-            // (measured: each faster for its unit size)
-            auto slot = [&](uint32_t i, uint32_t r) {
+            // branch-light: targets are the positions [u, h); the thread of a target at [u, 2u) also owns the
+            // phase-A target s + off (position [h, h + u)), whose source is s + 2 off
+            // (measured: the single-load form below is faster for 128-bit units, the two-branch form for 64-bit)
+            auto slot = [&](uint32_t i, uint32_t s) {
                 const uint32_t pos = i & segm;
-                if (i >= span || pos - u >= h - u) return;   // targets: position in [u, h)
-                const uint32_t s = (r << p.C_log) | c;
-                if (pos < 2 * u) {   // also owns the phase-A target s + off
-                    if (!p.inverse) {
-                        const T a = xor_t<T>(tile[s + off], tile[s + 2 * off]);
-                        tile[s + off] = a;
-                        tile[s] = xor_t<T>(tile[s], a);
-                    } else {
-                        const T a = tile[s + off];
-                        tile[s] = xor_t<T>(tile[s], a);
-                        tile[s + off] = xor_t<T>(a, tile[s + 2 * off]);
+                if (sizeof(T) == 16) {
+                    const bool act = (pos - u) < (h - u);
+                    const bool isA = pos < 2 * u;
+                    if (act) {
+                        T src = tile[s + off];
+                        if (isA) {
+                            const T a = xor_t<T>(src, tile[s + 2 * off]);
+                            tile[s + off] = a;
+                            if (!p.inverse) src = a;
+                        }
+                        tile[s] = xor_t<T>(tile[s], src);
                     }
                 } else {
-                    tile[s] = xor_t<T>(tile[s], tile[s + off]);
+                    if (pos - u >= h - u) return;
+                    if (pos < 2 * u) {
+                        if (!p.inverse) {
+                            const T a = xor_t<T>(tile[s + off], tile[s + 2 * off]);
+                            tile[s + off] = a;
+                            tile[s] = xor_t<T>(tile[s], a);
+                        } else {
+                            const T a = tile[s + off];
+                            tile[s] = xor_t<T>(tile[s], a);
+                            tile[s + off] = xor_t<T>(a, tile[s + 2 * off]);
+                        }
+                    } else {
+                        tile[s] = xor_t<T>(tile[s], tile[s + off]);
+                    }
                 }
             };
-            if (RES_UNROLL128 || sizeof(T) == 8) {
 #pragma unroll
-                for (int j = 0; j < RES_SLOTS(T); j++) slot(ii[j], rl + j * RS);
-            } else {
-                if (colok)
-                    for (uint32_t r = rl; r < (uint32_t)p.rows; r += RS) slot(r * M + c0 + c, r);
-            }
+            for (int j = 0; j < RES_SLOTS(T); j++) slot(ii[j], s0 + j * RES_THREADS);
             __syncthreads();
         }
         if (colok)
@@ -421,6 +432,83 @@ template <typename T, int WB>
 __global__ void __launch_bounds__(RB_THREADS, 3) k_cvt_rb(CvtRbParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     cvt_rb_tiles<T, WB>(p, reinterpret_cast<T*>(p.data), blockIdx.x, gridDim.x, smem_raw);
+}
+
+// The same pass with the tile loads done by the TMA engine (SURVEY §8a "TMA bulk copies into smem"): one
+// thread per CTA issues, per tile, one 4-D tensor-map load (mode 0: 2^C contiguous units x 2^R rows at stride
+// 2^r_lo units; dims (units of the column run, middle bits, rows, rest)) or one 1-D bulk copy per column
+// (mode 1: the tile is 2^C contiguous runs of 2^R units, each landing after its column's shared-memory pad);
+// the copies complete on the buffer's mbarrier (transaction count = tile bytes).  Replaces 2^(R+C)/EPC
+// cp.async instructions and their address arithmetic per tile.  Stores as in k_cvt_rb.
+template <typename T, int WB>
+__global__ void __launch_bounds__(RB_THREADS, 3) k_cvt_rb_tma(CvtRbParams p, const __grid_constant__ CUtensorMap tm) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bars[2];
+    T* data = reinterpret_cast<T*>(p.data);
+    constexpr uint32_t EPC = 16 / sizeof(T);
+    const uint32_t ncols = 1u << p.C, nrows = 1u << p.R, nslots = ncols << p.R;
+    const uint32_t bufsz = ((ncols * (nrows + (p.mode ? RB_PAD(T) : 0)) * (uint32_t)sizeof(T)) + 127) & ~127u;
+    const uint64_t tiles_per_pair = p.units_per_pair >> (p.R + p.C);
+    const uint64_t ntiles = tiles_per_pair * p.batch;
+    const int midbits = p.mode ? 0 : p.r_lo - p.C;
+    const uint64_t rest_per_pair = p.units_per_pair >> (p.r_lo + p.R);
+    auto tile_at = [&](uint64_t t, T*& dp, uint64_t& base) {
+        const uint64_t pair = t / tiles_per_pair, tt = t - pair * tiles_per_pair;
+        dp = data + pair * p.units_per_pair;
+        if (p.mode) base = tt << (p.R + p.C);
+        else base = ((tt & ((1ull << midbits) - 1)) << p.C) | ((tt >> midbits) << (p.r_lo + p.R));
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto prefetch = [&](uint64_t t, int b) {   // thread 0 only
+        T* buf = reinterpret_cast<T*>(smem_raw + b * bufsz);
+        fence_proxy_async_smem();   // the buffer's earlier generic-proxy reads / writes come first
+        mbar_arrive_expect_tx(&bars[b], nslots * (uint32_t)sizeof(T));
+        const uint64_t pair = t / tiles_per_pair, tt = t - pair * tiles_per_pair;
+        if (p.mode) {
+            const T* src = data + pair * p.units_per_pair + (tt << (p.R + p.C));
+            for (uint32_t col = 0; col < ncols; col++)
+                bulk_g2s(buf + col * (nrows + RB_PAD(T)), src + ((uint64_t)col << p.R), nrows * (uint32_t)sizeof(T), &bars[b]);
+        } else {
+            tma_load_4d(buf, &tm, 0, (int)(tt & ((1ull << midbits) - 1)), 0,
+                        (int)(pair * rest_per_pair + (tt >> midbits)), &bars[b]);
+        }
+    };
+    if (threadIdx.x == 0 && blockIdx.x < ntiles) prefetch(blockIdx.x, 0);
+    const uint32_t S = blockDim.x * EPC;
+    const uint64_t gstride = p.mode ? (uint64_t)S : ((uint64_t)(S >> p.C) << p.r_lo);
+    int k = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, k++) {
+        const int b = k & 1;
+        T* buf = reinterpret_cast<T*>(smem_raw + b * bufsz);
+        if (threadIdx.x == 0 && t + gridDim.x < ntiles) prefetch(t + gridDim.x, b ^ 1);
+        mbar_wait(&bars[b], (uint32_t)(k >> 1) & 1);   // this tile has landed
+        uint32_t* s32 = reinterpret_cast<uint32_t*>(smem_raw + b * bufsz);
+        for (int i = 0; i < p.nphase; i++) {
+            const int ph = (p.inverse & 1) ? p.nphase - 1 - i : i;
+            int o0 = 0;
+            for (int q = 0; q < ph; q++) o0 += p.ph_n[q];
+            rb_phase<T, WB>(s32, p, ph, o0);
+            __syncthreads();
+        }
+        T* dp; uint64_t base;
+        tile_at(t, dp, base);
+        {
+            uint32_t s = threadIdx.x * EPC, sm;
+            uint64_t g;
+            rb_slot<T>(p, s, base, sm, g);
+            T* gp = dp + g;
+            for (; s < nslots; s += S, gp += gstride) {
+                rb_slot<T>(p, s, 0, sm, g);
+                *reinterpret_cast<uint4*>(gp) = *reinterpret_cast<const uint4*>(buf + sm);
+            }
+        }
+        __syncthreads();   // the buffer is refilled by the prefetch two tiles on
+    }
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -30,6 +30,8 @@
 //                        movement) instead of the peer-memory pulls (read per call)
 //   GF2X_SHARD_TOP1=1    sharded forward: M4R-4 constant products after changeRepr instead of the composed
 //                        changeRepr tables (k_shard_top instead of k_shard_top2)
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -146,6 +148,7 @@ __constant__ int c_pm_terms[9][4] = {
 };
 
 #include "bottom.cuh"
+#include "small.cuh"
 
 // =============================================================================================
 // changeRepr^-1 + InterleavedCombine: C_i = psi^-1(P[i]) (deg <= 126),
@@ -490,6 +493,8 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_tile<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 #define RB_ATTR(T, W) CUDA_TRY(cudaFuncSetAttribute(k_cvt_rb<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_cvt_rb_tma<uint64_t, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_cvt_rb_tma<uint4, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         RB_ATTR(uint64_t, 2); RB_ATTR(uint64_t, 3); RB_ATTR(uint64_t, 4); RB_ATTR(uint64_t, 5); RB_ATTR(uint64_t, 6);
         RB_ATTR(uint4, 2); RB_ATTR(uint4, 3); RB_ATTR(uint4, 4); RB_ATTR(uint4, 5); RB_ATTR(uint4, 6);
 #undef RB_ATTR
@@ -498,6 +503,8 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_top<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_top<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_slab<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_small<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_small<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_slab<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_ipsi_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_ipsi_bs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -838,7 +845,9 @@ static bool split_fused(const Plan& P) {
     const bool same = P.ma == P.mb && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8 && P.sa.p < 0 && P.sb.p < 0;
     return same && P.a_bits == P.b_bits && !P.cvt_a.empty() && top_rowbits(P.cvt_a[0], P.ma) >= 0 && !env_flag("GF2X_NO_FUSED_SPLIT");
 }
+static int small_cluster(const Plan& P);
 static int launches_of(const Plan& P) {
+    if (small_cluster(P)) return 1;
     const bool same = P.ma == P.mb && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8 && P.sa.p < 0 && P.sb.p < 0;
     int n = split_fused(P) ? 0 : 2;  // prep a, b
     n += launches_of_split(P.sa, P.cvt_a, P.ma) + (same ? 0 : launches_of_split(P.sb, P.cvt_b, P.mb)) +
@@ -987,6 +996,45 @@ static gf2x_status launch_cvt_slab(const std::vector<CvtPass>& v, size_t i, T* d
     return e == cudaSuccess ? GF2X_OK : fail(GF2X_ECUDA, std::string("cvt slab launch: ") + cudaGetErrorString(e));
 }
 
+// ------------------------------------------------------------------------------ TMA tensor maps (k_cvt_rb_tma)
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+static bool rb_tma_enabled() { return !env_flag("GF2X_NO_RB_TMA"); }   // measured 5 % faster (c4b)
+// mode 0: dims (column run of 2^C units, middle bits [C, r_lo), rows [r_lo, r_lo + R), the rest incl. pairs),
+// box (2^C units, 1, 2^R, 1); units as 64-bit elements (u128: 2 per unit).  Mode 1 uses 1-D bulk copies.
+template <typename T>
+static bool make_rb_tmap(const CvtRbParams& q, CUtensorMap* tm) {
+    memset(tm, 0, sizeof(*tm));
+    if (q.mode) return true;
+    auto fn = tmap_encode_fn();
+    if (!fn) return false;
+    const uint64_t EU = sizeof(T) / 8;
+    const uint64_t total = q.units_per_pair * q.batch;
+    cuuint64_t dims[4] = {((cuuint64_t)1 << q.C) * EU, (cuuint64_t)1 << (q.r_lo - q.C), (cuuint64_t)1 << q.R,
+                          (cuuint64_t)(total >> (q.r_lo + q.R))};
+    cuuint64_t strides[3] = {((cuuint64_t)1 << q.C) * sizeof(T), ((cuuint64_t)1 << q.r_lo) * sizeof(T),
+                             ((cuuint64_t)1 << (q.r_lo + q.R)) * sizeof(T)};
+    cuuint32_t box[4] = {(cuuint32_t)(((cuuint64_t)1 << q.C) * EU), 1, (cuuint32_t)1 << q.R, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    if (box[0] > 256 || box[2] > 256) return false;
+    CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, q.data, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 template <typename T>
 static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, uint64_t batch, bool inverse,
                            int sm_count, cudaStream_t st, const CvtSrc* src = nullptr) {
@@ -1043,6 +1091,13 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
             const int occ = 3;
             ProfScope ps(sizeof(T) == 8 ? "k_cvt_rb<u64>" : "k_cvt_rb<u128>", 2.0 * per * batch * sizeof(T), st);
             const int g = grid_for(ntiles, 1, sm_count, occ);
+            CUtensorMap tm;
+            if (rb_tma_enabled() && p.rb_wb == 6 && make_rb_tmap<T>(prm, &tm)) {
+                k_cvt_rb_tma<T, 6><<<g, RB_THREADS, sm, st>>>(prm, tm);
+                cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("cvt rb tma launch: ") + cudaGetErrorString(e));
+                continue;
+            }
             switch (p.rb_wb) {
                 case 2: k_cvt_rb<T, 2><<<g, RB_THREADS, sm, st>>>(prm); break;
                 case 3: k_cvt_rb<T, 3><<<g, RB_THREADS, sm, st>>>(prm); break;
@@ -1327,6 +1382,68 @@ static gf2x_status stream_workspace(DeviceState* ds, cudaStream_t st, size_t byt
     return GF2X_OK;
 }
 
+// ------------------------------------------------------------------------------ the fused small-N kernel
+// 0: not used; else the cluster size of k_small (small.cuh): products of N = 2^m points, 5 <= m <= 11
+static int small_cluster(const Plan& P) {
+    if (P.m < 5 || P.m > 11 || env_flag("GF2X_NO_SMALL")) return 0;
+    std::vector<CvtOp> oa, ob, oi;
+    cvt_ops(P.ma, 0, oa);
+    cvt_ops(P.mb, 0, ob);
+    cvt_ops(P.m, 0, oi);
+    if (oa.size() > SM_MAX_OPS || ob.size() > SM_MAX_OPS || oi.size() > SM_MAX_OPS) return 0;
+    if (P.batch == 1 && P.m >= 7) return 4;   // one product: its limbs on four CTAs
+    // batches keep the multi-pass path: one CTA per 2^9-point product measured 1.12 ms at c2 against 0.56
+    // (per-butterfly constants and M4R-4 changeRepr^-1 lookups cost more than the bit-sliced bottom kernel);
+    // GF2X_SMALL_BATCH=1 selects it (tested)
+    if (P.batch > 1 && env_flag("GF2X_SMALL_BATCH")) return small_layout(P.m, 1).total * 4 <= 200 * 1024 ? 1 : (P.m >= 7 ? 4 : 0);
+    return 0;
+}
+
+static gf2x_status run_small(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
+                             const Plan& P, int CL, DeviceState* ds, cudaStream_t st) {
+    SmallParams sp;
+    memset(&sp, 0, sizeof(sp));
+    sp.a = a; sp.b = b; sp.c = c;
+    sp.na = P.na; sp.nb = P.nb; sp.a_bits = a_bits; sp.b_bits = b_bits; sp.batch = P.batch;
+    sp.m = P.m; sp.ma = P.ma; sp.mb = P.mb;
+    std::vector<CvtOp> oa, ob, oi;
+    cvt_ops(P.ma, 0, oa);
+    cvt_ops(P.mb, 0, ob);
+    cvt_ops(P.m, 0, oi);
+    sp.nops_a = (int)oa.size(); sp.nops_b = (int)ob.size(); sp.nops_i = (int)oi.size();
+    for (size_t i = 0; i < oa.size(); i++) sp.ops_a[i] = oa[i];
+    for (size_t i = 0; i < ob.size(); i++) sp.ops_b[i] = ob[i];
+    for (size_t i = 0; i < oi.size(); i++) sp.ops_i[i] = oi[i];
+    sp.tabs = ds->tabs;
+    const size_t sm = (size_t)small_layout(P.m, CL).total * 4;
+    const double bytes = (double)P.batch * 8.0 * (P.na + P.nb + P.na + P.nb);
+    ProfScope ps(CL == 1 ? "k_small<1>" : "k_small<4>", bytes, st);
+    cudaError_t e;
+    if (CL == 1) {
+        const int occ = std::max(1, (int)(220 * 1024 / (sm + 1024)));
+        k_small<1><<<grid_for(P.batch, 1, ds->sm_count, occ), SM_THREADS, sm, st>>>(sp);
+        e = cudaGetLastError();
+    } else {
+        cudaLaunchConfig_t cfg;
+        memset(&cfg, 0, sizeof(cfg));
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 4;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cfg.blockDim = dim3(SM_THREADS);
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = st;
+        const uint64_t ncl = std::min<uint64_t>(P.batch, (uint64_t)(ds->sm_count / 4) * std::max(1, (int)(220 * 1024 / (sm + 1024))));
+        cfg.gridDim = dim3((unsigned)(4 * ncl));
+        e = cudaLaunchKernelEx(&cfg, k_small<4>, sp);
+        if (e == cudaSuccess) e = cudaGetLastError();
+    }
+    return e == cudaSuccess ? GF2X_OK : fail(GF2X_ECUDA, std::string("small launch: ") + cudaGetErrorString(e));
+}
+
 static gf2x_status run_pipeline_a4(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
                                    const Plan& P, void* ws, DeviceState* ds, cudaStream_t st, int stop_stage);
 static int run_trunc_if_eligible(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
@@ -1354,6 +1471,11 @@ static gf2x_status mul_common(const uint64_t* a, uint64_t a_bits, const uint64_t
     if (s != GF2X_OK) return s;
     Plan P;
     if ((s = make_plan(a_bits, b_bits, batch, P)) != GF2X_OK) return s;
+    // products of at most 2^11 points: the fused single-kernel pipeline (no workspace)
+    if (algo == 5 && !stop_stage) {
+        const int CL = small_cluster(P);
+        if (CL) return run_small(a, a_bits, b, b_bits, c, P, CL, ds, st);
+    }
     void* ws = user_ws;
     if (ws) {
         if (user_ws_bytes < P.bytes) return fail(GF2X_ENOMEM, "workspace too small");

@@ -1,0 +1,346 @@
+// small.cuh -- the whole Alg. 5 multiply of a product with N = 2^m <= 2^11 points in ONE kernel
+// (SURVEY §7 step 3 / §3 call stack (4): "one fused kernel per product, the pipeline in shared memory"),
+// included by gf2x.cu.
+//
+// A product runs on a cluster of CL CTAs (CL = 4 for a single product: CTA r owns limb r of both spectra;
+// CL = 1 for batches: one persistent CTA per product at a time, all four limbs).  Limbs are independent in
+// every step except pointmul and changeRepr^-1 (Prop. 2: the FFT multipliers lie in TGF(2^32) and
+// multiply each 32-bit limb on its own; BasisCvt is XOR only), so the cluster exchanges data twice, through
+// distributed shared memory:
+//   1 Split + pad          -> SA, SB (u64, zero-extended to N)
+//   2 BasisCvt (Alg. 3 / Alg. 2)        -> in place on SA, SB (every CTA; Taylor steps as phase-A / phase-B sweeps)
+//   3 changeRepr psi        -> my limbs of A, B (M4R-8 lookups of the product's psi tables)
+//   4 FFT_LCH x2 (Alg. 1)     -> layers m-1 .. 0 on my limbs; multipliers s_k(phi(b)) < 2^(m-k) lie in
+//                                          GF(2^16) (multiplier shortening P:802-815), multiplied by integer
+//                                          products of the bits of each block (smul, fft.cuh)
+//   5 pointmul              -> bit-sliced: 32 elements per plane word, the nine TGF(2^32) products of
+//                                          the limb Karatsuba (bs_mul32) one per thread, combined per result limb
+//   6 iFFT_LCH           -> layers 0 .. m-1 on my limbs of the product
+//   7 iBasisCvt                 -> on my limbs (u32 units, reversed schedule, B then A)
+//   8 changeRepr^-1 + combine -> every CTA a quarter of the output words (M4R-4, word-planar tables)
+#pragma once
+
+#define SM_THREADS 256
+#define SM_MAX_OPS 48
+
+struct SmallParams {
+    const uint64_t* a;
+    const uint64_t* b;
+    uint64_t* c;
+    uint64_t na, nb, a_bits, b_bits, batch;
+    int m, ma, mb;
+    int nops_a, nops_b, nops_i;
+    CvtOp ops_a[SM_MAX_OPS], ops_b[SM_MAX_OPS], ops_i[SM_MAX_OPS];
+    const DevTables* tabs;
+};
+
+// shared-memory layout (32-bit words), per CTA; N = 2^m, LPC = 4 / CL limbs, G = N / 32 groups, GC = G / CL
+struct SmallLayout {
+    uint32_t sa, sb, al, bl, ptab, itab, pl, pr, total;
+};
+__host__ __device__ inline SmallLayout small_layout(int m, int CL) {
+    SmallLayout L;
+    const uint32_t N = 1u << m, LPC = 4 / CL, GC = (N >> 5) / CL;
+    L.sa = 0;
+    L.sb = L.sa + 2 * N;
+    L.al = L.sb + 2 * N;                 // [LPC][N]
+    L.bl = L.al + LPC * N;
+    L.ptab = L.bl + LPC * N;             // psi: CL = 1: uint4 M4R-8 (8 x 256 x 4 words); CL = 4: my limb (8 x 256)
+    L.itab = L.ptab + (CL == 1 ? 8 * 256 * 4 : 8 * 256);   // psi^-1: M4R-4 word-planar [4 limbs][32 nibbles][16]
+    L.pl = L.itab + 4 * 32 * 16;         // planes of A, B: [operand 2][limb 4][GC][33]
+    L.pr = L.pl + 2 * 4 * GC * 33;       // the nine products: [GC][9][33]
+    L.total = L.pr + GC * 9 * 33;
+    return L;
+}
+
+// ---- small-subfield constants: K_b = c v_b (tower basis v_b = prod of x_(i+1) over the bits i of b)
+// SWAR products by the generators on 2-, 4-, 8- and 16-bit blocks (x_k^2 = x_k + x_1 ... x_(k-1))
+__device__ __forceinline__ uint32_t sm_mulx3(uint32_t u) {   // bytes: (n0 + n1 x3) x3 = n1 x1x2 + (n0 + n1) x3
+    const uint32_t hi = (u >> 4) & 0x0F0F0F0Fu;
+    return mulx1(mulx2(hi)) | ((u ^ (u << 4)) & 0xF0F0F0F0u);
+}
+__device__ __forceinline__ uint32_t sm_mulx4(uint32_t u) {   // halves: (w0 + w1 x4) x4 = w1 x1x2x3 + (w0 + w1) x4
+    const uint32_t hi = (u >> 8) & 0x00FF00FFu;
+    return mulx1(mulx2(sm_mulx3(hi))) | ((u ^ (u << 8)) & 0xFF00FF00u);
+}
+// x0 ^= c x1 for a limb, c < 2^W: XOR over the bits b of every W-bit block of the integer products t_b K_b
+template <int W>
+__device__ __forceinline__ uint32_t sm_smul(uint32_t u, const uint32_t* K) {
+    constexpr uint32_t M = W == 2 ? 0x55555555u : (W == 4 ? 0x11111111u : (W == 8 ? 0x01010101u : 0x00010001u));
+    uint32_t r = (u & M) * K[0];
+#pragma unroll
+    for (int b = 1; b < W; b++) r ^= ((u >> b) & M) * K[b];
+    return r;
+}
+template <int W>
+__device__ __forceinline__ void sm_consts(uint32_t c, uint32_t* K) {
+    K[0] = c;
+    K[1] = mulx1(c);
+    if constexpr (W > 2) {
+        K[2] = mulx2(c);
+        K[3] = mulx1(K[2]);
+    }
+    if constexpr (W > 4) {
+#pragma unroll
+        for (int b = 0; b < 4; b++) K[4 + b] = sm_mulx3(K[b]);
+    }
+    if constexpr (W > 8) {
+#pragma unroll
+        for (int b = 0; b < 8; b++) K[8 + b] = sm_mulx4(K[b]);
+    }
+}
+
+// Alg. 2 step (lg, K) on units of type T in s[0, 2^mm) as two sweeps, A (targets [h, h+u)) and B ([u, h)),
+// source = target + d; forward A then B, inverse B then A (R4 / R7)
+template <typename T>
+__device__ __forceinline__ void sm_sweep(T* s, int mm, int lg, int K, bool A, int tid, int nthr) {
+    const uint32_t h = 1u << (lg - 1), u = h >> K, d = h - u;
+    const uint32_t nseg = 1u << (mm - lg);
+    if (A) {
+        const uint32_t n = nseg * u;
+        for (uint32_t it = tid; it < n; it += nthr) {
+            const uint32_t seg = it / u, j = it - seg * u;
+            const uint32_t t = (seg << lg) + h + j;
+            s[t] ^= s[t + d];
+        }
+    } else {
+        const uint32_t n = nseg * h;
+        for (uint32_t it = tid; it < n; it += nthr) {
+            const uint32_t seg = it >> (lg - 1), j = it & (h - 1);
+            if (j < u) continue;
+            const uint32_t t = (seg << lg) + j;
+            s[t] ^= s[t + d];
+        }
+    }
+}
+
+template <int CL>
+__device__ __forceinline__ uint32_t* sm_peer(uint32_t* p, int rank) {
+    if (CL == 1) return p;
+    uint32_t* r;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(p), "r"(rank));
+    return r;
+}
+template <int CL>
+__device__ __forceinline__ void sm_sync() {
+    if (CL == 1) __syncthreads();
+    else asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// one FFT layer k on my limbs of A (and B): forward x0 ^= c x1, x1 ^= x0; inverse x1 ^= x0, x0 ^= c x1
+template <int W, bool INV>
+__device__ __forceinline__ void sm_layer(uint32_t* A, uint32_t* B, int nops, int m, int k, int LPC, uint32_t N) {
+    const uint32_t half = N >> 1;
+    for (uint32_t it = threadIdx.x; it < half; it += blockDim.x) {
+        const uint32_t blk = it >> k, off = it & ((1u << k) - 1);
+        const uint32_t i0 = (blk << (k + 1)) | off, i1 = i0 | (1u << k);
+        const uint32_t cst = layer_const(k, blk << (k + 1));
+        uint32_t K[W];
+        sm_consts<W>(cst, K);
+        for (int o = 0; o < nops; o++) {
+            uint32_t* X = o ? B : A;
+            for (int l = 0; l < LPC; l++) {
+                uint32_t* x = X + l * N;
+                uint32_t x0 = x[i0], x1 = x[i1];
+                if (INV) x1 ^= x0;
+                x0 ^= sm_smul<W>(x1, K);
+                if (!INV) x1 ^= x0;
+                x[i0] = x0;
+                x[i1] = x1;
+            }
+        }
+    }
+}
+template <bool INV>
+__device__ __forceinline__ void sm_fft(uint32_t* A, uint32_t* B, int nops, int m, int LPC, uint32_t N) {
+    for (int s = 0; s < m; s++) {
+        const int k = INV ? s : m - 1 - s;
+        const int w = m - k;   // the layer's multipliers are < 2^w
+        if (w <= 2) sm_layer<2, INV>(A, B, nops, m, k, LPC, N);
+        else if (w <= 4) sm_layer<4, INV>(A, B, nops, m, k, LPC, N);
+        else if (w <= 8) sm_layer<8, INV>(A, B, nops, m, k, LPC, N);
+        else sm_layer<16, INV>(A, B, nops, m, k, LPC, N);
+        __syncthreads();
+    }
+}
+
+template <int CL>
+__global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
+    extern __shared__ __align__(1024) uint32_t sm[];
+    const int m = p.m;
+    const uint32_t N = 1u << m, LPC = 4 / CL, G = N >> 5, GC = G / CL;
+    const SmallLayout Ly = small_layout(m, CL);
+    uint64_t* SA = reinterpret_cast<uint64_t*>(sm + Ly.sa);
+    uint64_t* SB = reinterpret_cast<uint64_t*>(sm + Ly.sb);
+    uint32_t* AL = sm + Ly.al;
+    uint32_t* BL = sm + Ly.bl;
+    uint32_t* ptab = sm + Ly.ptab;
+    uint32_t* itab = sm + Ly.itab;
+    uint32_t* PL = sm + Ly.pl;
+    uint32_t* PR = sm + Ly.pr;
+    uint32_t rank = 0;
+    if (CL > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const uint32_t l0 = rank * LPC;   // my first limb
+    // ---- tables (once per CTA): psi (M4R-8: my limbs), psi^-1 (M4R-4, word-planar: entry (o, t, x) = limb o of
+    // psi^-1(x << 4t) = limb o of the M4R-8 entry of byte t/2 with x in its nibble t&1)
+    if (CL == 1) {
+        for (int i = tid; i < 8 * 256; i += nthr) reinterpret_cast<uint4*>(ptab)[i] = p.tabs->psi64[i];
+    } else {
+        for (int i = tid; i < 8 * 256; i += nthr) ptab[i] = reinterpret_cast<const uint32_t*>(p.tabs->psi64 + i)[l0];
+    }
+    for (int i = tid; i < 4 * 32 * 16; i += nthr) {
+        const int o = i >> 9, t = (i >> 4) & 31, x = i & 15;
+        itab[i] = reinterpret_cast<const uint32_t*>(p.tabs->ipsi + (t >> 1) * 256 + (x << (4 * (t & 1))))[o];
+    }
+    const uint64_t n_out = p.na + p.nb;
+    const uint64_t pstep = CL == 1 ? gridDim.x : gridDim.x / CL;
+    for (uint64_t pr = CL == 1 ? blockIdx.x : blockIdx.x / CL; pr < p.batch; pr += pstep) {
+        const uint64_t* a = p.a + pr * p.na;
+        const uint64_t* b = p.b + pr * p.nb;
+        __syncthreads();   // (tables; the previous product's last reads of SA .. PR)
+        // ---- 1 Split + pad
+        const uint32_t ra = (uint32_t)(p.a_bits & 63), rb = (uint32_t)(p.b_bits & 63);
+        for (uint32_t i = tid; i < N; i += nthr) {
+            uint64_t x = i < p.na ? a[i] : 0ull, y = i < p.nb ? b[i] : 0ull;
+            if (i == p.na - 1 && ra) x &= (1ull << ra) - 1;
+            if (i == p.nb - 1 && rb) y &= (1ull << rb) - 1;
+            SA[i] = x;
+            SB[i] = y;
+        }
+        __syncthreads();
+        // ---- 2 BasisCvt of both operands (every CTA of the cluster: a few thousand XORs)
+        for (int o = 0; o < max(p.nops_a, p.nops_b); o++)
+            for (int ph = 0; ph < 2; ph++) {
+                if (o < p.nops_a) sm_sweep<uint64_t>(SA, p.ma, p.ops_a[o].lg, p.ops_a[o].K, ph == 0, tid, nthr);
+                if (o < p.nops_b) sm_sweep<uint64_t>(SB, p.mb, p.ops_b[o].lg, p.ops_b[o].K, ph == 0, tid, nthr);
+                __syncthreads();
+            }
+        // ---- 3 changeRepr: my limbs of psi(SA[i]), psi(SB[i])
+        for (uint32_t i = tid; i < N; i += nthr) {
+            const uint64_t x = SA[i], y = SB[i];
+            for (uint32_t l = 0; l < LPC; l++) {
+                uint32_t va = 0, vb = 0;
+#pragma unroll
+                for (int ch = 0; ch < 8; ch++) {
+                    const uint32_t ia = (uint32_t)(x >> (8 * ch)) & 255, ib = (uint32_t)(y >> (8 * ch)) & 255;
+                    if (CL == 1) {
+                        va ^= ptab[(ch * 256 + ia) * 4 + l];
+                        vb ^= ptab[(ch * 256 + ib) * 4 + l];
+                    } else {
+                        va ^= ptab[ch * 256 + ia];
+                        vb ^= ptab[ch * 256 + ib];
+                    }
+                }
+                AL[l * N + i] = va;
+                BL[l * N + i] = vb;
+            }
+        }
+        __syncthreads();
+        // ---- 4 FFT_LCH of both spectra, my limbs
+        sm_fft<false>(AL, BL, 2, m, LPC, N);
+        sm_sync<CL>();   // every limb of A and B complete (pointmul reads them from every CTA)
+        // ---- 5 pointmul, bit-sliced: my GC groups of 32 consecutive elements
+        const uint32_t g0 = rank * GC;
+        for (uint32_t it = tid; it < GC * 8; it += nthr) {   // (group, limb, operand): transpose into planes
+            const uint32_t g = it >> 3, l = (it >> 1) & 3, o = it & 1;
+            const uint32_t* src = sm_peer<CL>((o ? BL : AL) + (l % LPC) * N, l / LPC) + ((g0 + g) << 5);
+            uint32_t x[32];
+#pragma unroll
+            for (int j = 0; j < 32; j++) x[j] = src[j];
+            transpose32(x);
+            uint32_t* d = PL + ((o * 4 + l) * GC + g) * 33;
+#pragma unroll
+            for (int j = 0; j < 32; j++) d[j] = x[j];
+        }
+        __syncthreads();
+        for (uint32_t it = tid; it < GC * 9; it += nthr) {   // (group, product): one bs_mul32 each
+            const uint32_t g = it / 9, q = it - g * 9;
+            const int mask = c_pm_terms[q][0];
+            uint32_t x[32], y[32], r[32];
+#pragma unroll
+            for (int j = 0; j < 32; j++) { x[j] = 0; y[j] = 0; }
+#pragma unroll
+            for (int l = 0; l < 4; l++)
+                if (mask & (1 << l)) {
+                    const uint32_t* pa = PL + ((0 * 4 + l) * GC + g) * 33;
+                    const uint32_t* pb = PL + ((1 * 4 + l) * GC + g) * 33;
+#pragma unroll
+                    for (int j = 0; j < 32; j++) { x[j] ^= pa[j]; y[j] ^= pb[j]; }
+                }
+            bs_mul32(x, y, r);
+            uint32_t* d = PR + (g * 9 + q) * 33;
+#pragma unroll
+            for (int j = 0; j < 32; j++) d[j] = r[j];
+        }
+        __syncthreads();
+        for (uint32_t it = tid; it < GC * 4; it += nthr) {   // (group, result limb): R_L = sum of its terms
+            const uint32_t g = it >> 2, L = it & 3;
+            uint32_t acc[32], s1[32], s2[32], t[32];
+#pragma unroll
+            for (int j = 0; j < 32; j++) { acc[j] = 0; s1[j] = 0; s2[j] = 0; }
+#pragma unroll 1
+            for (int q = 0; q < 9; q++) {
+                const uint32_t* src = PR + (g * 9 + q) * 33;
+                const bool r0 = (c_pm_terms[q][1] >> L) & 1, r1 = (c_pm_terms[q][2] >> L) & 1, r2 = (c_pm_terms[q][3] >> L) & 1;
+                if (r0) { for (int j = 0; j < 32; j++) acc[j] ^= src[j]; }
+                if (r1) { for (int j = 0; j < 32; j++) s1[j] ^= src[j]; }
+                if (r2) { for (int j = 0; j < 32; j++) s2[j] ^= src[j]; }
+            }
+            bs_mul_v31(s1, t);
+#pragma unroll
+            for (int j = 0; j < 32; j++) acc[j] ^= t[j];
+            bs_mul_v31sq(s2, t);
+#pragma unroll
+            for (int j = 0; j < 32; j++) acc[j] ^= t[j];
+            transpose32(acc);
+            uint32_t* dst = sm_peer<CL>(AL + (L % LPC) * N, L / LPC) + ((g0 + g) << 5);
+#pragma unroll
+            for (int j = 0; j < 32; j++) dst[j] = acc[j];
+        }
+        sm_sync<CL>();   // every result limb delivered
+        // ---- 6 iFFT_LCH, my limbs of the product
+        sm_fft<true>(AL, BL, 1, m, LPC, N);
+        // ---- 7 iBasisCvt, my limbs (u32 units; XOR acts limb-wise)
+        for (int o = p.nops_i - 1; o >= 0; o--)
+            for (int ph = 0; ph < 2; ph++) {
+                for (uint32_t l = 0; l < LPC; l++)
+                    sm_sweep<uint32_t>(AL + l * N, m, p.ops_i[o].lg, p.ops_i[o].K, ph == 1, tid, nthr);
+                __syncthreads();
+            }
+        sm_sync<CL>();   // every limb of the product converted
+        // ---- 8 changeRepr^-1 + InterleavedCombine: out[w] = lo64(C_w) ^ hi64(C_(w-1)), C_i = 0 for i >= N
+        const uint32_t* Lp[4];
+#pragma unroll
+        for (int l = 0; l < 4; l++) Lp[l] = sm_peer<CL>(AL + (l % LPC) * N, l / LPC);
+        uint64_t* cout = p.c + pr * n_out;
+        const uint32_t wpc = (uint32_t)((n_out + CL - 1) / CL);
+        for (uint32_t w = rank * wpc + tid; w < min((uint64_t)(rank + 1) * wpc, n_out); w += nthr) {
+            uint32_t lo0 = 0, lo1 = 0, hi2 = 0, hi3 = 0;
+            if (w < N) {
+                uint32_t v[4];
+#pragma unroll
+                for (int l = 0; l < 4; l++) v[l] = Lp[l][w];
+#pragma unroll
+                for (int t = 0; t < 32; t++) {
+                    const uint32_t x = (v[t >> 3] >> (4 * (t & 7))) & 15;
+                    lo0 ^= itab[(0 * 32 + t) * 16 + x];
+                    lo1 ^= itab[(1 * 32 + t) * 16 + x];
+                }
+            }
+            if (w >= 1 && w - 1 < N) {
+                uint32_t v[4];
+#pragma unroll
+                for (int l = 0; l < 4; l++) v[l] = Lp[l][w - 1];
+#pragma unroll
+                for (int t = 0; t < 32; t++) {
+                    const uint32_t x = (v[t >> 3] >> (4 * (t & 7))) & 15;
+                    hi2 ^= itab[(2 * 32 + t) * 16 + x];
+                    hi3 ^= itab[(3 * 32 + t) * 16 + x];
+                }
+            }
+            cout[w] = ((uint64_t)(lo1 ^ hi3) << 32) | (lo0 ^ hi2);
+        }
+        sm_sync<CL>();   // (peers are done reading my limbs before they are overwritten / I exit)
+    }
+}

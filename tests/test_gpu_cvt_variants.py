@@ -4,7 +4,8 @@ process), against the oracle's Alg. 5 / Karatsuba on the same seeded operands:
     superset-sum transform over the row bits, tests/test_cvt_top_reading.py) -- checks it actually ran;
   * GF2X_NO_CVT_TOP=1: the plain residue pass + k_prep;
   * GF2X_CVT_SLAB=1: the CVT(16) slab pass on thread-block clusters (measured slower; kept opt-in);
-  * GF2X_NO_FUSED_SPLIT=1: k_cvt_top without the fused Split."""
+  * GF2X_NO_FUSED_SPLIT=1: k_cvt_top without the fused Split;
+  * GF2X_NO_RB_TMA=1: the register-blocked passes with cp.async tile loads instead of TMA (k_cvt_rb_tma)."""
 import json
 import os
 import subprocess
@@ -55,7 +56,8 @@ def run_variant(env, sizes, tmp_path):
     return {int(k): v for k, v in json.load(open(out)).items()}
 
 
-@pytest.mark.parametrize("env", [{}, {"GF2X_NO_CVT_TOP": "1"}, {"GF2X_CVT_SLAB": "1"}, {"GF2X_NO_FUSED_SPLIT": "1"}])
+@pytest.mark.parametrize("env", [{}, {"GF2X_NO_CVT_TOP": "1"}, {"GF2X_CVT_SLAB": "1"}, {"GF2X_NO_FUSED_SPLIT": "1"},
+                                 {"GF2X_NO_RB_TMA": "1"}])
 def test_cvt_variants_exact(env, tmp_path):
     res = run_variant(env, SIZES + BIG, tmp_path)
     for bits in SIZES + BIG:
