@@ -43,29 +43,26 @@ __device__ __forceinline__ uint32_t m4r4_word_sa(uint32_t tab, uint32_t x) {
     return r;
 }
 // Row t (16 words) of the M4R-4 table of constant c: tab[16t + x] = (c v_(4t)) * x, x in GF(16).
-// c v_(4t) = w comes from the M4R-8 tables of the fixed maps c -> c v_(4t); x = sum of x_b v_b
-// (v_0 = 1, v_1 = x1, v_2 = x2, v_3 = x1 x2) so the row is the XOR-span of w, x1 w, x2 w, x1 x2 w.
-// SHARED: wt is a shared-memory copy (plain loads); else the global table (read-only cache)
+// c v_(4t) = w by SWAR products with the generators x3, x4, x5 (gf2x_device.cuh mul_v4t; no table
+// lookups), and x = sum of x_b v_b (v_0 = 1, v_1 = x1, v_2 = x2, v_3 = x1 x2) so the row is the XOR-span of
+// w, x1 w, x2 w, x1 x2 w.  The row's four 16-byte stores are rotated by (t >> 1): the 8 threads of a table
+// (rows t = 0..7, 64 B apart) then cover all 32 banks in every store instruction (they hit 8 of them with
+// 4-way conflicts in order).  (wt / SHARED: kept for the callers' signatures, unused.)
 template <bool SHARED = false>
 __device__ __forceinline__ void build_tab_row(uint32_t* tab, uint32_t c, int t, const uint32_t* __restrict__ wt,
                                               uint32_t* kb = nullptr) {
-    uint32_t w = c;
-    if (t) {
-        const uint32_t* T = wt + (t - 1) * 1024;
-        if (SHARED) w = T[c & 255] ^ T[256 + ((c >> 8) & 255)] ^ T[512 + ((c >> 16) & 255)] ^ T[768 + (c >> 24)];
-        else
-            w = __ldg(T + (c & 255)) ^ __ldg(T + 256 + ((c >> 8) & 255)) ^ __ldg(T + 512 + ((c >> 16) & 255)) ^
-                __ldg(T + 768 + (c >> 24));
-    }
+    (void)wt;
+    const uint32_t w = mul_v4t(c, t);
     const uint32_t w1 = mulx1(w), w2 = mulx2(w), w3 = mulx1(w2);
-    uint32_t row[16];
-#pragma unroll
-    for (int x = 0; x < 16; x++) row[x] = ((x & 1) ? w : 0u) ^ ((x & 2) ? w1 : 0u) ^ ((x & 4) ? w2 : 0u) ^ ((x & 8) ? w3 : 0u);
     uint4* d = reinterpret_cast<uint4*>(tab + 16 * t);
 #pragma unroll
-    for (int q = 0; q < 4; q++) d[q] = make_uint4(row[4 * q], row[4 * q + 1], row[4 * q + 2], row[4 * q + 3]);
+    for (int q = 0; q < 4; q++) {
+        const int qq = (q + (t >> 1)) & 3;   // entries 4 qq .. 4 qq + 3
+        const uint32_t base = ((qq & 1) ? w2 : 0u) ^ ((qq & 2) ? w3 : 0u);
+        d[qq] = make_uint4(base, base ^ w, base ^ w1, base ^ w ^ w1);
+    }
     // small-subfield products (fft_group): K_b = c v_b, b < 8, are the entries x = 2^q of rows 0 and 1
-    if (kb && t < 2) *reinterpret_cast<uint4*>(kb + 4 * t) = make_uint4(row[1], row[2], row[4], row[8]);
+    if (kb && t < 2) *reinterpret_cast<uint4*>(kb + 4 * t) = make_uint4(w, w1, w2, w3);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -408,6 +405,6 @@ static size_t fft2_smem(int c, int R, bool psi, bool wt_shared, bool db, bool re
 static bool fft2_db(int c, int R, bool psi) { return !psi && fft2_smem(c, R, psi, false, true) <= 200 * 1024; }
 // the shared wt copy only where the CTA already takes a whole SM (it would otherwise halve occupancy)
 static bool fft2_wt_shared(int c, int R, bool psi) {
-    const size_t base = fft2_smem(c, R, psi, false, fft2_db(c, R, psi));
-    return base > 113 * 1024 && base + 7 * 1024 * 4 <= 200 * 1024;   // 200 KB: the opt-in set in get_device
+    (void)c; (void)R; (void)psi;
+    return false;   // the table rows are built by SWAR products (build_tab_row): no c -> c v_(4t) maps needed
 }

@@ -25,6 +25,26 @@ GF2X_HD GF2X_INLINE uint32_t mulx2(uint32_t u) {
     return mulx1((u >> 2) & 0x33333333u) | ((u ^ (u << 2)) & 0xCCCCCCCCu);
 }
 
+// each byte (m0 + m1 x3) -> x3 (m0 + m1 x3) = m1 x1x2 + (m0 + m1) x3   (x3^2 = x3 + x1 x2)
+GF2X_HD GF2X_INLINE uint32_t mulx3(uint32_t u) {
+    return mulx1(mulx2((u >> 4) & 0x0F0F0F0Fu)) | ((u ^ (u << 4)) & 0xF0F0F0F0u);
+}
+// each 16-bit half (w0 + w1 x4) -> w1 x1x2x3 + (w0 + w1) x4   (x4^2 = x4 + x1 x2 x3)
+GF2X_HD GF2X_INLINE uint32_t mulx4(uint32_t u) {
+    return mulx1(mulx2(mulx3((u >> 8) & 0x00FF00FFu))) | ((u ^ (u << 8)) & 0xFF00FF00u);
+}
+// a TGF(2^32) element (h0 + h1 x5) -> h1 x1x2x3x4 + (h0 + h1) x5   (x5^2 = x5 + x1 x2 x3 x4)
+GF2X_HD GF2X_INLINE uint32_t mulx5(uint32_t u) {
+    return mulx1(mulx2(mulx3(mulx4(u >> 16)))) | ((u ^ (u << 16)) & 0xFFFF0000u);
+}
+// c v_(4t), t < 8: v_4 = x3, v_8 = x4, v_16 = x5 (the basis v_k = prod of x_(j+1) over the bits j of k)
+GF2X_HD GF2X_INLINE uint32_t mul_v4t(uint32_t c, int t) {
+    if (t & 1) c = mulx3(c);
+    if (t & 2) c = mulx4(c);
+    if (t & 4) c = mulx5(c);
+    return c;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Method of four Russians with 4-bit chunks (§4.3-4.4 use M4R; chunk width chosen for sm_100a:
 // a 16-entry table row spans 16 banks, so the 32 lanes of a warp never conflict).

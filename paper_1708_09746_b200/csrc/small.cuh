@@ -36,7 +36,7 @@ struct SmallParams {
 
 // shared-memory layout (32-bit words), per CTA; N = 2^m, LPC = 4 / CL limbs, G = N / 32 groups, GC = G / CL
 struct SmallLayout {
-    uint32_t sa, sb, al, bl, ptab, itab, pl, pr, total;
+    uint32_t sa, sb, al, bl, ptab, itab, pl, pr, kd, total;
 };
 __host__ __device__ inline SmallLayout small_layout(int m, int CL) {
     SmallLayout L;
@@ -49,20 +49,14 @@ __host__ __device__ inline SmallLayout small_layout(int m, int CL) {
     L.itab = L.ptab + (CL == 1 ? 8 * 256 * 4 : 8 * 256);   // psi^-1: M4R-4 word-planar [4 limbs][32 nibbles][16]
     L.pl = L.itab + 4 * 32 * 16;         // planes of A, B: [operand 2][limb 4][GC][33]
     L.pr = L.pl + 2 * 4 * GC * 33;       // the nine products: [GC][9][33]
-    L.total = L.pr + GC * 9 * 33;
+    L.kd = L.pr + GC * 9 * 33;           // FFT constant deltas KD[layer < 9][2][16]
+    L.total = L.kd + 9 * 2 * 16;
     return L;
 }
 
 // ---- small-subfield constants: K_b = c v_b (tower basis v_b = prod of x_(i+1) over the bits i of b)
 // SWAR products by the generators on 2-, 4-, 8- and 16-bit blocks (x_k^2 = x_k + x_1 ... x_(k-1))
-__device__ __forceinline__ uint32_t sm_mulx3(uint32_t u) {   // bytes: (n0 + n1 x3) x3 = n1 x1x2 + (n0 + n1) x3
-    const uint32_t hi = (u >> 4) & 0x0F0F0F0Fu;
-    return mulx1(mulx2(hi)) | ((u ^ (u << 4)) & 0xF0F0F0F0u);
-}
-__device__ __forceinline__ uint32_t sm_mulx4(uint32_t u) {   // halves: (w0 + w1 x4) x4 = w1 x1x2x3 + (w0 + w1) x4
-    const uint32_t hi = (u >> 8) & 0x00FF00FFu;
-    return mulx1(mulx2(sm_mulx3(hi))) | ((u ^ (u << 8)) & 0xFF00FF00u);
-}
+// (mulx3 / mulx4 on bytes / 16-bit halves: gf2x_device.cuh)
 // x0 ^= c x1 for a limb, c < 2^W: XOR over the bits b of every W-bit block of the integer products t_b K_b
 template <int W>
 __device__ __forceinline__ uint32_t sm_smul(uint32_t u, const uint32_t* K) {
@@ -82,11 +76,11 @@ __device__ __forceinline__ void sm_consts(uint32_t c, uint32_t* K) {
     }
     if constexpr (W > 4) {
 #pragma unroll
-        for (int b = 0; b < 4; b++) K[4 + b] = sm_mulx3(K[b]);
+        for (int b = 0; b < 4; b++) K[4 + b] = mulx3(K[b]);
     }
     if constexpr (W > 8) {
 #pragma unroll
-        for (int b = 0; b < 8; b++) K[8 + b] = sm_mulx4(K[b]);
+        for (int b = 0; b < 8; b++) K[8 + b] = mulx4(K[b]);
     }
 }
 
@@ -127,16 +121,34 @@ __device__ __forceinline__ void sm_sync() {
     else asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// one FFT layer k on my limbs of A (and B): forward x0 ^= c x1, x1 ^= x0; inverse x1 ^= x0, x0 ^= c x1
+// one FFT layer k on my limbs of A (and B): forward x0 ^= c x1, x1 ^= x0; inverse x1 ^= x0, x0 ^= c x1.
+// Thread t takes the butterflies it = t + 256 j: their block bases are b_0 | j 2^9 (b_0 < 2^9), so by the
+// linearity of s_k and of c -> c v_b the constants are K(j) = K(0) ^ [j & 1] KD[k][0] ^ [j & 2] KD[k][1] with
+// KD[k][i][b] = s_k(v_(9+i)) v_b (layers k <= 8; built once per CTA): one full constant per thread and layer.
+#define SM_KD_LAYERS 9
 template <int W, bool INV>
-__device__ __forceinline__ void sm_layer(uint32_t* A, uint32_t* B, int nops, int m, int k, int LPC, uint32_t N) {
+__device__ __forceinline__ void sm_layer(uint32_t* A, uint32_t* B, int nops, int m, int k, int LPC, uint32_t N,
+                                         const uint32_t* KD) {
     const uint32_t half = N >> 1;
-    for (uint32_t it = threadIdx.x; it < half; it += blockDim.x) {
+    uint32_t K0[W];
+    bool have = false;
+    for (uint32_t it = threadIdx.x, j = 0; it < half; it += blockDim.x, j++) {
         const uint32_t blk = it >> k, off = it & ((1u << k) - 1);
         const uint32_t i0 = (blk << (k + 1)) | off, i1 = i0 | (1u << k);
-        const uint32_t cst = layer_const(k, blk << (k + 1));
         uint32_t K[W];
-        sm_consts<W>(cst, K);
+        if (blockDim.x == 256 && k < SM_KD_LAYERS && have) {
+#pragma unroll
+            for (int b = 0; b < W; b++)
+                K[b] = K0[b] ^ ((j & 1) ? KD[(k * 2 + 0) * 16 + b] : 0u) ^ ((j & 2) ? KD[(k * 2 + 1) * 16 + b] : 0u);
+        } else {
+            const uint32_t cst = layer_const(k, blk << (k + 1));
+            sm_consts<W>(cst, K);
+            if (j == 0) {
+#pragma unroll
+                for (int b = 0; b < W; b++) K0[b] = K[b];
+                have = true;
+            }
+        }
         for (int o = 0; o < nops; o++) {
             uint32_t* X = o ? B : A;
             for (int l = 0; l < LPC; l++) {
@@ -152,14 +164,14 @@ __device__ __forceinline__ void sm_layer(uint32_t* A, uint32_t* B, int nops, int
     }
 }
 template <bool INV>
-__device__ __forceinline__ void sm_fft(uint32_t* A, uint32_t* B, int nops, int m, int LPC, uint32_t N) {
+__device__ __forceinline__ void sm_fft(uint32_t* A, uint32_t* B, int nops, int m, int LPC, uint32_t N, const uint32_t* KD) {
     for (int s = 0; s < m; s++) {
         const int k = INV ? s : m - 1 - s;
         const int w = m - k;   // the layer's multipliers are < 2^w
-        if (w <= 2) sm_layer<2, INV>(A, B, nops, m, k, LPC, N);
-        else if (w <= 4) sm_layer<4, INV>(A, B, nops, m, k, LPC, N);
-        else if (w <= 8) sm_layer<8, INV>(A, B, nops, m, k, LPC, N);
-        else sm_layer<16, INV>(A, B, nops, m, k, LPC, N);
+        if (w <= 2) sm_layer<2, INV>(A, B, nops, m, k, LPC, N, KD);
+        else if (w <= 4) sm_layer<4, INV>(A, B, nops, m, k, LPC, N, KD);
+        else if (w <= 8) sm_layer<8, INV>(A, B, nops, m, k, LPC, N, KD);
+        else sm_layer<16, INV>(A, B, nops, m, k, LPC, N, KD);
         __syncthreads();
     }
 }
@@ -178,6 +190,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
     uint32_t* itab = sm + Ly.itab;
     uint32_t* PL = sm + Ly.pl;
     uint32_t* PR = sm + Ly.pr;
+    uint32_t* KD = sm + Ly.kd;
     uint32_t rank = 0;
     if (CL > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
     const int tid = threadIdx.x, nthr = blockDim.x;
@@ -192,6 +205,13 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
     for (int i = tid; i < 4 * 32 * 16; i += nthr) {
         const int o = i >> 9, t = (i >> 4) & 31, x = i & 15;
         itab[i] = reinterpret_cast<const uint32_t*>(p.tabs->ipsi + (t >> 1) * 256 + (x << (4 * (t & 1))))[o];
+    }
+    if (tid < SM_KD_LAYERS * 2) {   // KD[k][i] = s_k(v_(9+i)) v_b, b < 16
+        const int k = tid >> 1, i = tid & 1;
+        uint32_t K[16];
+        sm_consts<16>(k < 9 + i ? c_S[k * 32 + 9 + i] : 0u, K);
+#pragma unroll
+        for (int b = 0; b < 16; b++) KD[tid * 16 + b] = K[b];
     }
     const uint64_t n_out = p.na + p.nb;
     const uint64_t pstep = CL == 1 ? gridDim.x : gridDim.x / CL;
@@ -238,7 +258,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
         }
         __syncthreads();
         // ---- 4 FFT_LCH of both spectra, my limbs
-        sm_fft<false>(AL, BL, 2, m, LPC, N);
+        sm_fft<false>(AL, BL, 2, m, LPC, N, KD);
         sm_sync<CL>();   // every limb of A and B complete (pointmul reads them from every CTA)
         // ---- 5 pointmul, bit-sliced: my GC groups of 32 consecutive elements
         const uint32_t g0 = rank * GC;
@@ -300,7 +320,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
         }
         sm_sync<CL>();   // every result limb delivered
         // ---- 6 iFFT_LCH, my limbs of the product
-        sm_fft<true>(AL, BL, 1, m, LPC, N);
+        sm_fft<true>(AL, BL, 1, m, LPC, N, KD);
         // ---- 7 iBasisCvt, my limbs (u32 units; XOR acts limb-wise)
         for (int o = p.nops_i - 1; o >= 0; o--)
             for (int ph = 0; ph < 2; ph++) {
