@@ -478,6 +478,12 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
     if ((s = X.run(XF.gather)) != GF2X_OK) return s;
     for (int r : mine) {
         uint64_t* A = (uint64_t*)X.local(r).buf[SB_A];
+        if (!S.cvt_fwd.empty() && top_rowbits(S.cvt_fwd[0], S.p) >= 0 && !env_flag("GF2X_NO_FUSED_SPLIT")) {
+            // Split (the mask of the last word) fused into the top Taylor pass, in place (k_cvt_top)
+            const CvtSrc src{A, A, 1, S.n, bits};
+            if ((s = run_cvt<uint64_t>(S.cvt_fwd, A, S.p, 1, false, smc, st, &src)) != GF2X_OK) return s;
+            continue;
+        }
         { ProfScope ps("k_prep", 16.0 * S.n, st); k_prep<<<grid_for(S.n, 256, smc, 8), 256, 0, st>>>(A, S.n, bits, S.p, 1, A); }
         if ((s = last("shard prep")) != GF2X_OK) return s;
         if ((s = run_cvt<uint64_t>(S.cvt_fwd, A, S.p, 1, false, smc, st)) != GF2X_OK) return s;

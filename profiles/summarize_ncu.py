@@ -77,7 +77,7 @@ def main():
     def bname(k):
         if k in bmap:
             return bmap[k]
-        m = re.match(r"(k_cvt_(?:rb|res|tile|stream))<(u64|u128)", k)
+        m = re.match(r"(k_cvt_(?:rb|res|tile|stream|top|slab))(?:_tma)?<(u64|u128)", k)
         if m:
             return f"{m.group(1)}<{m.group(2)}>"
         m = re.match(r"k_fft2<(\d), (\d)", k)   # k_fft2<INV, PSI, ZS>
