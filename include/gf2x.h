@@ -151,6 +151,17 @@ int gf2x_comm_peer_memory(gf2x_comm_t comm);
  * gf2x_comm_abort: abort the communicator now (collective peers see an error, not a hang).  The
  *   handle must still be released with gf2x_comm_destroy. */
 gf2x_status gf2x_comm_check(gf2x_comm_t comm);
+/* Host-mode communicator (no NCCL): the ranks' synchronisation goes through two caller-supplied HOST callbacks,
+ * e.g. a torch.distributed gloo group.  `barrier(user)` returns when every rank has called it; `allgather(in,
+ * out, bytes, user)` gathers `bytes` from every rank into out[rank * bytes].  Both return 0 on success.  All
+ * exchanges of gf2x_mul_sharded are then peer-memory pulls of CUDA-IPC-mapped workspaces (GF2X_ECUDA when the
+ * mapping fails, e.g. no peer access), each preceded by cudaStreamSynchronize + barrier; the ranks may share one
+ * GPU (no kernel ever waits on another rank's kernel).  Meant for tests and hosts without NCCL; slower than the
+ * stream-ordered NCCL barriers of gf2x_comm_init.  Callbacks are invoked from the calling thread only. */
+typedef int (*gf2x_host_barrier_fn)(void* user);
+typedef int (*gf2x_host_allgather_fn)(const void* in, void* out, size_t bytes, void* user);
+gf2x_status gf2x_comm_init_host(int nranks, int rank, gf2x_host_barrier_fn barrier, gf2x_host_allgather_fn allgather,
+                                void* user, gf2x_comm_t* out);
 gf2x_status gf2x_comm_wait(gf2x_comm_t comm, void* stream, double timeout_s);
 gf2x_status gf2x_comm_abort(gf2x_comm_t comm);
 gf2x_status gf2x_mul_sharded(const uint64_t* a_shard, const uint64_t* b_shard, uint64_t bits,

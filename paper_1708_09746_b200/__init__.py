@@ -25,7 +25,7 @@ EXPORTS = [
     "gf2x_mul_sharded_sim", "gf2x_debug_shard_stage", "gf2x_shard_plan", "gf2x_profile_enable", "gf2x_profile_report", "gf2x_status_string", "gf2x_last_error",
     "gf2x_release", "gf2x_version", "gf2x_mul_w", "gf2x_launch_count_w", "gf2x_debug_stage_w128",
     "gf2x_comm_peer_memory", "gf2x_mul_alg4", "gf2x_debug_stage_alg4", "gf2x_plan", "gf2x_basis_cvt_bits",
-    "gf2x_mul_frob", "gf2x_comm_check", "gf2x_comm_wait", "gf2x_comm_abort",
+    "gf2x_mul_frob", "gf2x_comm_check", "gf2x_comm_wait", "gf2x_comm_abort", "gf2x_comm_init_host",
 ]
 
 
@@ -74,6 +74,9 @@ def load(path: str = LIB_PATH):
     L.gf2x_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
     L.gf2x_comm_destroy.argtypes = [vp]
     L.gf2x_comm_peer_memory.argtypes = [vp]
+    if hasattr(L, "gf2x_comm_init_host"):
+        L.gf2x_comm_init_host.argtypes = [i32, i32, vp, vp, vp, ctypes.POINTER(vp)]
+        L.gf2x_comm_init_host.restype = i32
     if hasattr(L, "gf2x_comm_check"):   # (older builds, loaded by the A/B tools, lack these)
         L.gf2x_comm_check.argtypes = [vp]
         L.gf2x_comm_wait.argtypes = [vp, vp, ctypes.c_double]
@@ -255,6 +258,42 @@ class Comm:
         buf = ctypes.create_string_buffer(uid, 128)
         _check(load().gf2x_comm_init(buf, nranks, rank, ctypes.byref(h)))
         self.handle = h
+
+    @classmethod
+    def from_host_group(cls, group=None):
+        """Host-mode communicator (gf2x_comm_init_host): barriers and the IPC-handle exchange through a
+        torch.distributed group (e.g. gloo), exchanges as peer-memory pulls; the ranks may share a GPU."""
+        import torch
+        import torch.distributed as dist
+        self = cls.__new__(cls)
+        self.nranks, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        BAR = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
+        AG = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+
+        def _barrier(_user):
+            try:
+                dist.barrier(group=group)
+                return 0
+            except Exception:
+                return 1
+
+        def _allgather(src, dst, nbytes, _user):
+            try:
+                t = torch.frombuffer(bytearray(ctypes.string_at(src, nbytes)), dtype=torch.uint8)
+                outs = [torch.empty_like(t) for _ in range(self.nranks)]
+                dist.all_gather(outs, t, group=group)
+                buf = b"".join(bytes(o.tolist()) for o in outs)
+                ctypes.memmove(dst, buf, len(buf))
+                return 0
+            except Exception:
+                return 1
+
+        self._cbs = (BAR(_barrier), AG(_allgather))   # kept alive as long as the communicator
+        h = ctypes.c_void_p()
+        _check(load().gf2x_comm_init_host(self.nranks, self.rank, ctypes.cast(self._cbs[0], ctypes.c_void_p),
+                                          ctypes.cast(self._cbs[1], ctypes.c_void_p), None, ctypes.byref(h)))
+        self.handle = h
+        return self
 
     @staticmethod
     def unique_id() -> bytes:

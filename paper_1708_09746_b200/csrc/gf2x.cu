@@ -225,11 +225,18 @@ __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restri
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint64_t w0 = tile * IB_TILE;   // first element / word of the tile (flat)
         const uint4* src = P + w0;
-        // ---- load (coalesced), limb-planar
-        for (uint32_t e = t; e < IB_TILE; e += IB_THREADS) {
-            const uint4 v = src[e];
-            const uint32_t q = ib_swz(e);
-            S[q] = v.x; S[IB_TILE + q] = v.y; S[2 * IB_TILE + q] = v.z; S[3 * IB_TILE + q] = v.w;
+        // ---- load (coalesced), limb-planar; 16 loads in flight per thread (the tile is not prefetched: a second
+        // 64 KB buffer would halve the occupancy)
+#pragma unroll 1
+        for (uint32_t e0 = t; e0 < IB_TILE; e0 += 16 * IB_THREADS) {
+            uint4 v[16];
+#pragma unroll
+            for (int u = 0; u < 16; u++) v[u] = src[e0 + u * IB_THREADS];
+#pragma unroll
+            for (int u = 0; u < 16; u++) {
+                const uint32_t q = ib_swz(e0 + u * IB_THREADS);
+                S[q] = v[u].x; S[IB_TILE + q] = v[u].y; S[2 * IB_TILE + q] = v[u].z; S[3 * IB_TILE + q] = v[u].w;
+            }
         }
         // the element before the tile (its hi64 enters the tile's first output word)
         if (t == 0) {
@@ -1633,6 +1640,32 @@ gf2x_status gf2x_comm_init(const void* nccl_unique_id, int nranks, int rank, gf2
     return GF2X_OK;
 }
 
+gf2x_status gf2x_comm_init_host(int nranks, int rank, gf2x_host_barrier_fn barrier, gf2x_host_allgather_fn allgather,
+                                void* user, gf2x_comm_t* out) {
+    if (!out || !barrier || !allgather || nranks < 1 || rank < 0 || rank >= nranks) return fail(GF2X_EINVAL, "bad comm arguments");
+    if (nranks > SHARD_MAXG) return fail(GF2X_EINVAL, "at most 8 ranks");
+    gf2x_comm_s* c = new gf2x_comm_s();
+    c->nranks = nranks;
+    c->rank = rank;
+    c->comm = nullptr;
+    c->ws = nullptr;
+    c->ws_bytes = 0;
+    c->p2p = 0;
+    c->aborted = 0;
+    c->host = 1;
+    c->hbar = barrier;
+    c->hag = allgather;
+    c->huser = user;
+    for (int r = 0; r < SHARD_MAXG; r++) c->peer_ws[r] = nullptr;
+    cudaGetDevice(&c->device);
+    if (cudaMalloc(&c->d_sync, 256 + SHARD_MAXG * sizeof(cudaIpcMemHandle_t)) != cudaSuccess) {
+        delete c;
+        return fail(GF2X_ENOMEM, "comm sync buffer");
+    }
+    *out = c;
+    return GF2X_OK;
+}
+
 static void comm_unmap_peers(gf2x_comm_s* c) {
     for (int r = 0; r < SHARD_MAXG; r++)
         if (c->peer_ws[r] && r != c->rank) cudaIpcCloseMemHandle(c->peer_ws[r]);
@@ -1643,7 +1676,38 @@ static void comm_unmap_peers(gf2x_comm_s* c) {
 // Map every rank's workspace into this process (CUDA IPC; NVLink peer access).  Collective: the handles
 // go around with an NCCL all-gather and the outcome is agreed with an all-reduce(min), so every rank
 // takes the same exchange path.  GF2X_SHARD_NCCL=1 keeps NCCL send/recv.
+static gf2x_status comm_map_peers_host(gf2x_comm_s* c, cudaStream_t st) {
+    comm_unmap_peers(c);
+    const int G = c->nranks;
+    CUDA_TRY(cudaStreamSynchronize(st));
+    cudaIpcMemHandle_t mine;
+    memset(&mine, 0, sizeof(mine));
+    int ok = cudaIpcGetMemHandle(&mine, c->ws) == cudaSuccess ? 1 : 0;
+    if (!ok) cudaGetLastError();
+    std::vector<cudaIpcMemHandle_t> hs(G);
+    if (c->hag(&mine, hs.data(), sizeof(mine), c->huser) != 0) return fail(GF2X_ENCCL, "host all-gather callback failed");
+    c->peer_ws[c->rank] = c->ws;
+    for (int r = 0; r < G && ok; r++) {
+        if (r == c->rank) continue;
+        if (cudaIpcOpenMemHandle(&c->peer_ws[r], hs[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            ok = 0;
+            c->peer_ws[r] = nullptr;
+            cudaGetLastError();
+        }
+    }
+    std::vector<int> oks(G);
+    if (c->hag(&ok, oks.data(), sizeof(int), c->huser) != 0) return fail(GF2X_ENCCL, "host all-gather callback failed");
+    for (int r = 0; r < G; r++) ok = std::min(ok, oks[r]);
+    if (!ok) {
+        comm_unmap_peers(c);
+        return fail(GF2X_ECUDA, "host-mode communicator: CUDA IPC mapping of the peers' workspaces failed");
+    }
+    c->p2p = 1;
+    return GF2X_OK;
+}
+
 static gf2x_status comm_map_peers(gf2x_comm_s* c, cudaStream_t st) {
+    if (c->host) return comm_map_peers_host(c, st);
     comm_unmap_peers(c);
     const int G = c->nranks;
     int ok = env_flag_now("GF2X_SHARD_NCCL") ? 0 : 1;

@@ -219,6 +219,12 @@ struct gf2x_comm_s {
     int* d_sync;       // 1 int (stream-ordered barrier = NCCL all-reduce of it) + IPC handle staging
     int aborted;       // the NCCL communicator was aborted (async error, timeout or gf2x_comm_abort)
     std::string abort_reason;
+    // host mode (gf2x_comm_init_host): no NCCL; barriers and the IPC-handle exchange go through the caller's
+    // host callbacks (e.g. a torch.distributed gloo group), every exchange is a peer-memory pull
+    int host = 0;
+    gf2x_host_barrier_fn hbar = nullptr;
+    gf2x_host_allgather_fn hag = nullptr;
+    void* huser = nullptr;
 };
 
 static const int NCCL_IN_PROGRESS = 7;   // ncclInProgress (non-blocking communicators): not an error
@@ -235,6 +241,7 @@ static void comm_abort(gf2x_comm_s* c, const std::string& why) {
 // communicator, so that the stream-ordered barriers of the exchange cannot hang forever
 static gf2x_status comm_check(gf2x_comm_s* c) {
     if (c->aborted) return fail(GF2X_ENCCL, "communicator aborted: " + c->abort_reason);
+    if (c->host) return GF2X_OK;
     int async = 0;
     int rc = g_nccl.CommGetAsyncError(c->comm, &async);
     if (rc || (async && async != NCCL_IN_PROGRESS)) {
@@ -353,6 +360,11 @@ struct ShardExec {
     // rank's work enqueued after it starts (NCCL all-reduce of one int); nothing to do in the simulation
     gf2x_status barrier() {
         if (sim) return GF2X_OK;
+        if (comm->host) {   // host barrier: this rank's enqueued work is complete, then the caller's barrier
+            CUDA_TRY(cudaStreamSynchronize(st));
+            if (comm->hbar(comm->huser) != 0) return fail(GF2X_ENCCL, "host barrier callback failed");
+            return GF2X_OK;
+        }
         int rc = g_nccl.AllReduce(comm->d_sync, comm->d_sync, 1, NCCL_INT32, NCCL_SUM, comm->comm, st);
         if (rc) return fail(GF2X_ENCCL, std::string("NCCL barrier: ") + g_nccl.GetErrorString(rc));
         return GF2X_OK;
@@ -383,6 +395,7 @@ struct ShardExec {
             return GF2X_OK;
         }
         RankCtx& me = (*ranks)[0];
+        if (comm->host) return fail(GF2X_EINVAL, "host-mode communicator: peer-memory exchanges only");
         int rc = g_nccl.GroupStart();
         for (const Xfer& x : xs) {
             if (rc) break;
