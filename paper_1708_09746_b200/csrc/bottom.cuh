@@ -119,9 +119,19 @@ __device__ __forceinline__ void bt_cplanes(const uint32_t* Pk, uint32_t U, uint3
     for (int j = 0; j < 32; j++) c[j] = Pk[j] ^ prmt_sign(us[7 - (j & 7)], (8u | (uint32_t)(j >> 3)) * 0x1111u);
 }
 
+// x * c for 32 bit-sliced TGF(2^32) elements x and multiplier planes c whose planes >= W are zero (the layer's
+// multipliers are < 2^W, multiplier shortening P:802-815): for W = 8 / 16 each 8- / 16-bit block of x is
+// multiplied by c on its own (Prop. 2) -- 4 x 110 / 2 x 375 gates instead of 1229
+template <int W>
+__device__ __forceinline__ void bs_mul_w(const uint32_t* x, const uint32_t* c, uint32_t* r) {
+    if (W == 8) { bs_mul8(x, c, r); bs_mul8(x + 8, c, r + 8); bs_mul8(x + 16, c, r + 16); bs_mul8(x + 24, c, r + 24); }
+    else if (W == 16) { bs_mul16(x, c, r); bs_mul16(x + 16, c, r + 16); }
+    else bs_mul32(x, c, r);
+}
+
 // CK: cache of the multiplier planes, [layer][pair][33] (written by warp 0 in the forward layers,
 // read by every warp in the inverse layers of the same tile)
-template <bool INV>
+template <bool INV, int W = 32>
 __device__ __forceinline__ void bt_layer(uint32_t* planes, int k, const uint32_t* Pk, const uint32_t* UC,
                                          uint32_t* CK, int tid) {
     const int lb = tid >> 5, q = tid & 31;
@@ -143,7 +153,7 @@ __device__ __forceinline__ void bt_layer(uint32_t* planes, int k, const uint32_t
 #pragma unroll
         for (int j = 0; j < 32; j++) x1[j] ^= b0[j];
     }
-    bs_mul32(x1, c, pr);
+    bs_mul_w<W>(x1, c, pr);
 #pragma unroll
     for (int j = 0; j < 32; j++) {
         const uint32_t x0 = b0[j] ^ pr[j];
@@ -153,6 +163,7 @@ __device__ __forceinline__ void bt_layer(uint32_t* planes, int k, const uint32_t
 }
 
 // forward layer k on both operands with one set of multiplier planes (stored to CK by warp 0)
+template <int W = 32>
 __device__ __forceinline__ void bt_layer2(uint32_t* PA, uint32_t* PB, int k, const uint32_t* Pk, const uint32_t* UC,
                                           uint32_t* CK, int tid) {
     const int lb = tid >> 5, q = tid & 31;
@@ -172,7 +183,7 @@ __device__ __forceinline__ void bt_layer2(uint32_t* PA, uint32_t* PB, int k, con
         uint32_t* b1 = planes + bt_block(g1, lb);
 #pragma unroll
         for (int j = 0; j < 32; j++) x1[j] = b1[j];
-        bs_mul32(x1, c, pr);
+        bs_mul_w<W>(x1, c, pr);
 #pragma unroll
         for (int j = 0; j < 32; j++) {
             const uint32_t x0 = b0[j] ^ pr[j];
@@ -204,6 +215,9 @@ __device__ __forceinline__ void bt_acc_add(uint32_t* reg, int g, int mask, const
         }
 }
 
+// SUBW: some layer's multipliers lie below 2^16 (small transforms): per-layer width dispatch to bs_mul_w (a
+// separate instantiation: compiled into the plain kernel the dispatch cost the headline c4b 2 %)
+template <bool SUBW>
 __global__ void __launch_bounds__(BT_THREADS, 2 / BT_TPC) k_bottom(BottomParams p) {
     extern __shared__ __align__(1024) uint32_t bt_smem[];
     const int half = BT_TPC == 1 ? 0 : (int)(threadIdx.x / BT_HALF), tid = threadIdx.x % BT_HALF;
@@ -247,7 +261,10 @@ __global__ void __launch_bounds__(BT_THREADS, 2 / BT_TPC) k_bottom(BottomParams 
             // FFT_LCH bottom layers, top-down; one set of multiplier planes per layer serves both operands
 #pragma unroll 1
             for (int k = L - 1; k >= 0; k--) {
-                bt_layer2(PA, PB, k, Pk + k * 32, UC, CK, tid);
+                const int wc = p.m + p.map.bits - k;   // the layer's multipliers are < 2^wc
+                if (SUBW && wc <= 8) bt_layer2<8>(PA, PB, k, Pk + k * 32, UC, CK, tid);
+                else if (SUBW && wc <= 16) bt_layer2<16>(PA, PB, k, Pk + k * 32, UC, CK, tid);
+                else bt_layer2<32>(PA, PB, k, Pk + k * 32, UC, CK, tid);
                 __syncthreads();
             }
         }
@@ -317,7 +334,10 @@ __global__ void __launch_bounds__(BT_THREADS, 2 / BT_TPC) k_bottom(BottomParams 
         }
         if (p.mode & 4) {
             for (int k = 0; k < L; k++) {   // iFFT_LCH bottom layers, bottom-up
-                bt_layer<true>(R, k, Pk + k * 32, UC, CK, tid);
+                const int wc = p.m + p.map.bits - k;
+                if (SUBW && wc <= 8) bt_layer<true, 8>(R, k, Pk + k * 32, UC, CK, tid);
+                else if (SUBW && wc <= 16) bt_layer<true, 16>(R, k, Pk + k * 32, UC, CK, tid);
+                else bt_layer<true, 32>(R, k, Pk + k * 32, UC, CK, tid);
                 __syncthreads();
             }
         }
@@ -335,5 +355,8 @@ static size_t bottom_smem() { return (size_t)(BT_TPC * 2 * BT_REGION + 6 * 32 + 
 
 static int grid_for(uint64_t items, int per_block, int sm_count, int occ);
 static void bottom_launch(const BottomParams& bp, int smc, cudaStream_t st) {
-    k_bottom<<<grid_for((bp.ntiles + BT_TPC - 1) / BT_TPC, 1, smc, 2 / BT_TPC), BT_THREADS, bottom_smem(), st>>>(bp);
+    const bool subw = bp.m + bp.map.bits - (bp.L - 1) <= 16;   // the lowest layer's multipliers are < 2^16
+    const int g = grid_for((bp.ntiles + BT_TPC - 1) / BT_TPC, 1, smc, 2 / BT_TPC);
+    if (subw) k_bottom<true><<<g, BT_THREADS, bottom_smem(), st>>>(bp);
+    else k_bottom<false><<<g, BT_THREADS, bottom_smem(), st>>>(bp);
 }

@@ -339,6 +339,20 @@ struct ProfRec {
 //   one bit-sliced TGF(2^32) product (bs_mul32, 32 elements): 868 LOP3
 //   one table butterfly of k_fft2 (4 limbs x (8 PRMT + 2 nibble masks + 2 shifts + 4 XOR3) + 4 XOR): 68
 #define OPS_BS_MUL32 868.0
+//   the same product by a multiplier below 2^16 / 2^8 (bs_mul_w: 2 x bs_mul16 / 4 x bs_mul8): 2 x 259 / 4 x 80 LOP3
+#define OPS_BS_MUL16 518.0
+#define OPS_BS_MUL8 320.0
+// designed ALU-pipe instructions of one k_bottom launch: per 2^11-element tile, 2 (forward) + 1 (inverse) x 128
+// products per layer at the layer's multiplier width, 576 general products of the pointmul
+static double bottom_alu_ops(const BottomParams& bp) {
+    double per_tile = (bp.mode & 2) ? 576.0 * OPS_BS_MUL32 : 0.0;
+    const double nl = ((bp.mode & 1) ? 2.0 : 0.0) + ((bp.mode & 4) ? 1.0 : 0.0);
+    for (int k = 0; k < bp.L; k++) {
+        const int wc = bp.m + bp.map.bits - k;
+        per_tile += nl * 128.0 * (wc <= 8 ? OPS_BS_MUL8 : (wc <= 16 ? OPS_BS_MUL16 : OPS_BS_MUL32));
+    }
+    return (double)bp.ntiles * per_tile;
+}
 #define OPS_M4R_BUTTERFLY 68.0
 static thread_local bool g_prof_on = false;
 static thread_local std::vector<ProfRec> g_prof;
@@ -498,7 +512,8 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
 #undef FFT_ATTR
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_tile<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_tile<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_bottom<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_bottom<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 #define RB_ATTR(T, W) CUDA_TRY(cudaFuncSetAttribute(k_cvt_rb<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_rb_tma<uint64_t, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_rb_tma<uint4, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1315,9 +1330,7 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         bp.m = P.m; bp.L = P.fft.back().layers;
         bp.map = IdxMap{0, 0, 0};
         bp.mode = stop_stage == 2 ? 1 : (stop_stage == 3 ? 3 : 7);
-        // bit-sliced products per 2^11-element tile: 2L forward + L inverse layers x 128, pointmul 768
-        const double prods = (double)bp.ntiles * (3.0 * bp.L * 128.0 + 576.0);
-        ProfScope ps("k_bottom", 48.0 * P.N * P.batch, st, prods * OPS_BS_MUL32);
+        ProfScope ps("k_bottom", 48.0 * P.N * P.batch, st, bottom_alu_ops(bp));
         bottom_launch(bp, smc, st);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("bottom launch: ") + cudaGetErrorString(e));

@@ -543,8 +543,7 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
         bp.m = S.mloc; bp.L = S.fft.back().layers; bp.mode = debug_stage == 1 ? 1 : 7;
         bp.map = map;
         {
-            const double prods = (double)bp.ntiles * (3.0 * bp.L * 128.0 + 576.0);
-            ProfScope ps("k_bottom", 48.0 * Nloc, st, prods * OPS_BS_MUL32);
+            ProfScope ps("k_bottom", 48.0 * Nloc, st, bottom_alu_ops(bp));
             bottom_launch(bp, smc, st);
         }
         if ((s = last("shard bottom")) != GF2X_OK) return s;

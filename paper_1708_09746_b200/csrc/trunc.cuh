@@ -311,7 +311,7 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
         bp.total = T.U;
         bp.ntiles = (T.U + (1ull << BT_BITS) - 1) >> BT_BITS;
         bp.m = T.j; bp.L = fu.back().layers; bp.mode = 7; bp.map = umap;
-        ProfScope ps("k_bottom", 48.0 * T.U, su, (double)bp.ntiles * (3.0 * bp.L * 128.0 + 576.0) * OPS_BS_MUL32);
+        ProfScope ps("k_bottom", 48.0 * T.U, su, bottom_alu_ops(bp));
         bottom_launch(bp, smc, su);
     }
     for (size_t i = fu.size() - 1; i-- > 0;)
@@ -327,7 +327,7 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
         bp.total = T.H;
         bp.ntiles = (T.H + (1ull << BT_BITS) - 1) >> BT_BITS;
         bp.m = T.m - 1; bp.L = fl.back().layers; bp.mode = 7; bp.map = IdxMap{0, 0, 0};
-        ProfScope ps("k_bottom", 48.0 * T.H, st, (double)bp.ntiles * (3.0 * bp.L * 128.0 + 576.0) * OPS_BS_MUL32);
+        ProfScope ps("k_bottom", 48.0 * T.H, st, bottom_alu_ops(bp));
         bottom_launch(bp, smc, st);
     }
     // g_hi = iFFT_j(...) + Reduce(g_lo)[0, 2^j): Reduce of g_lo (in Wa) into Wb (free now); fused, the last

@@ -459,10 +459,8 @@ static void bottom_run(uint4* A, uint4* B, uint64_t total, int m, int L, int mod
     bp.m = m; bp.L = L;
     bp.map = IdxMap{0, 0, 0};
     bp.mode = mode;
-    const double prods = (double)bp.ntiles * (((mode & 1) ? 2.0 : 0.0) * L * 128.0 + ((mode & 4) ? 1.0 : 0.0) * L * 128.0 +
-                                              ((mode & 2) ? 576.0 : 0.0));
     const double bytes = (double)total * 16 * (((mode & 1) ? 4.0 : 0.0) + ((mode & 2) ? 3.0 : 0.0) + ((mode & 4) ? 2.0 : 0.0));
-    ProfScope ps("k_bottom", bytes, st, prods * OPS_BS_MUL32);
+    ProfScope ps("k_bottom", bytes, st, bottom_alu_ops(bp));
     bottom_launch(bp, smc, st);
 }
 

@@ -237,6 +237,13 @@ def main():
              "#ifndef GF2X_HD\n#define GF2X_HD\n#endif\n#ifndef GF2X_INLINE\n#define GF2X_INLINE inline\n#endif\n"]
     s, ops = emit_mul("bs_mul32", 5)
     parts.append(s)
+    # products by a multiplier of a subfield (k_bottom layers whose multipliers are < 2^16 / < 2^8: Prop. 2,
+    # each 16- / 8-bit block of the other factor is multiplied on its own)
+    s16, ops16 = emit_mul("bs_mul16", 4)
+    parts.append(s16)
+    s8, ops8 = emit_mul("bs_mul8", 3)
+    parts.append(s8)
+    print("bs_mul16 ops", ops16, "bs_mul8 ops", ops8, file=sys.stderr)
     v31 = 1 << 31
     s2, _ = emit_const("bs_mul_v31", v31, 5)
     parts.append(s2)

@@ -80,6 +80,8 @@ def main():
         m = re.match(r"(k_cvt_(?:rb|res|tile|stream|top|slab))(?:_tma)?<(u64|u128)", k)
         if m:
             return f"{m.group(1)}<{m.group(2)}>"
+        if k.startswith("k_bottom"):
+            return "k_bottom"
         m = re.match(r"k_fft2<(\d), (\d)", k)   # k_fft2<INV, PSI, ZS>
         if m:
             return "k_fft<inv>" if m.group(1) == "1" else ("k_fft<psi>" if m.group(2) == "1" else "k_fft")

@@ -19,19 +19,25 @@ KERNEL = r'''
 #define GF2X_HD __device__
 #define GF2X_INLINE __forceinline__
 #include "bitslice_gen.cuh"
-__global__ void k(const uint32_t* a, const uint32_t* b, uint32_t* r) {
-    uint32_t x[32], y[32], z[32];
-    for (int i = 0; i < 32; i++) { x[i] = a[threadIdx.x * 32 + i]; y[i] = b[threadIdx.x * 32 + i]; }
-    bs_mul32(x, y, z);
-    for (int i = 0; i < 32; i++) r[threadIdx.x * 32 + i] = z[i];
+#define KER(NAME, N)                                                                          \
+__global__ void k_##NAME(const uint32_t* a, const uint32_t* b, uint32_t* r) {                  \
+    uint32_t x[N], y[N], z[N];                                                                 \
+    for (int i = 0; i < N; i++) { x[i] = a[threadIdx.x * 32 + i]; y[i] = b[threadIdx.x * 32 + i]; } \
+    NAME(x, y, z);                                                                             \
+    for (int i = 0; i < N; i++) r[threadIdx.x * 32 + i] = z[i];                                \
 }
+KER(bs_mul32, 32)
+KER(bs_mul16, 16)
+KER(bs_mul8, 8)
 '''
 
 
 @pytest.mark.skipif(not (os.path.exists(NVCC) and shutil.which("cuobjdump")), reason="needs nvcc and cuobjdump")
-def test_bs_mul32_lop3_count_matches_roofline_constant():
+def test_bs_mul_lop3_counts_match_roofline_constants():
     src = open(os.path.join(CSRC, "gf2x.cu")).read()
-    ops = float(re.search(r"#define OPS_BS_MUL32 ([0-9.]+)", src).group(1))
+    want = {"bs_mul32": float(re.search(r"#define OPS_BS_MUL32 ([0-9.]+)", src).group(1)),
+            "bs_mul16": float(re.search(r"#define OPS_BS_MUL16 ([0-9.]+)", src).group(1)) / 2,
+            "bs_mul8": float(re.search(r"#define OPS_BS_MUL8 ([0-9.]+)", src).group(1)) / 4}
     with tempfile.TemporaryDirectory() as d:
         cu = os.path.join(d, "k.cu")
         open(cu, "w").write(KERNEL)
@@ -39,5 +45,11 @@ def test_bs_mul32_lop3_count_matches_roofline_constant():
         subprocess.run([NVCC, "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-cubin", "-I", CSRC, "-o", cubin, cu],
                        check=True, capture_output=True)
         sass = subprocess.run(["cuobjdump", "-sass", cubin], check=True, capture_output=True, text=True).stdout
-    lop3 = len(re.findall(r"\bLOP3\.LUT\b", sass))
-    assert lop3 == ops, (lop3, ops)
+    counts, fn = {}, None
+    for ln in sass.splitlines():
+        m = re.search(r"Function : _Z\d+k_(bs_mul\d+)", ln)
+        if m:
+            fn = m.group(1)
+        elif fn and re.search(r"\bLOP3\.LUT\b", ln):
+            counts[fn] = counts.get(fn, 0) + 1
+    assert counts == want, (counts, want)
