@@ -69,8 +69,16 @@ __global__ void __launch_bounds__(256) k_bitcvt_chunk(uint64_t* __restrict__ G, 
             const int lg = sw.lg[k];
             const uint32_t d = sw.d[k];
             if (lg <= 6) {
-                const uint64_t pm = sw.pmask[k];
-                for (uint32_t w = threadIdx.x; w < cw; w += blockDim.x) { const uint64_t x = T[w]; T[w] = x ^ ((x >> d) & pm); }
+                // a run of consecutive in-word sweeps: each thread applies all of them to its own words in
+                // registers (no word is read by another thread), with one barrier after the run
+                int k1 = k + 1;
+                while (k1 < sw.n && sw.lg[k1] <= 6) k1++;
+                for (uint32_t w = threadIdx.x; w < cw; w += blockDim.x) {
+                    uint64_t x = T[w];
+                    for (int q = k; q < k1; q++) x ^= (x >> sw.d[q]) & sw.pmask[q];
+                    T[w] = x;
+                }
+                k = k1 - 1;
             } else {
                 const uint32_t tlo = sw.tlo[k], thi = sw.thi[k], len = 1u << lg, wps = len >> 6, tw0 = tlo >> 6;
                 const uint32_t ntw = ((thi + 63) >> 6) - tw0, total = (cw / wps) * ntw;
