@@ -151,6 +151,12 @@ int gf2x_comm_peer_memory(gf2x_comm_t comm);
  * gf2x_comm_abort: abort the communicator now (collective peers see an error, not a hang).  The
  *   handle must still be released with gf2x_comm_destroy. */
 gf2x_status gf2x_comm_check(gf2x_comm_t comm);
+/* Experiment (not on the product path): changeRepr^-1 of n tower elements P (16 bytes each, device)
+ * into out (n x 16 bytes, device) as a tcgen05.mma kind::i8 product of 0/1 bytes with the accumulator in TMEM,
+ * 128 elements per MMA tile.  lbo / sbo: the shared-memory descriptors' core-matrix offsets in bytes (0: the
+ * canonical no-swizzle K-major values 128 / 1024).  Profiled as "k_ipsi_tc". */
+gf2x_status gf2x_experiment_ipsi_tc(const void* P, uint64_t n, void* out, uint32_t lbo, uint32_t sbo, void* stream);
+
 /* Host-mode communicator (no NCCL): the ranks' synchronisation goes through two caller-supplied HOST callbacks,
  * e.g. a torch.distributed gloo group.  `barrier(user)` returns when every rank has called it; `allgather(in,
  * out, bytes, user)` gathers `bytes` from every rank into out[rank * bytes].  Both return 0 on success.  All

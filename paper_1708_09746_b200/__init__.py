@@ -26,6 +26,7 @@ EXPORTS = [
     "gf2x_release", "gf2x_version", "gf2x_mul_w", "gf2x_launch_count_w", "gf2x_debug_stage_w128",
     "gf2x_comm_peer_memory", "gf2x_mul_alg4", "gf2x_debug_stage_alg4", "gf2x_plan", "gf2x_basis_cvt_bits",
     "gf2x_mul_frob", "gf2x_comm_check", "gf2x_comm_wait", "gf2x_comm_abort", "gf2x_comm_init_host",
+    "gf2x_experiment_ipsi_tc",
 ]
 
 
@@ -74,6 +75,9 @@ def load(path: str = LIB_PATH):
     L.gf2x_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
     L.gf2x_comm_destroy.argtypes = [vp]
     L.gf2x_comm_peer_memory.argtypes = [vp]
+    if hasattr(L, "gf2x_experiment_ipsi_tc"):
+        L.gf2x_experiment_ipsi_tc.argtypes = [vp, u64, vp, ctypes.c_uint32, ctypes.c_uint32, vp]
+        L.gf2x_experiment_ipsi_tc.restype = i32
     if hasattr(L, "gf2x_comm_init_host"):
         L.gf2x_comm_init_host.argtypes = [i32, i32, vp, vp, vp, ctypes.POINTER(vp)]
         L.gf2x_comm_init_host.restype = i32
@@ -241,6 +245,15 @@ def gf2x_debug_shard_stage(a, b, bits: int, nranks: int, stage: int, stream=None
     N = 2 * nwords(bits)
     out = torch.empty(N, 2, dtype=torch.uint64, device=a.device)
     _check(load().gf2x_debug_shard_stage(_ptr(a), _ptr(b), bits, nranks, stage, _ptr(out), _stream_ptr(stream)))
+    return out
+
+
+def experiment_ipsi_tc(P, lbo: int = 0, sbo: int = 0, stream=None):
+    """changeRepr^-1 of the tower elements P ((n, 2) uint64 / 16 bytes each, device) on the tensor cores
+    (tcgen05.mma kind::i8, TMEM accumulator): the DESIGN.md §7 experiment.  Returns (n, 2) uint64."""
+    import torch
+    out = torch.empty_like(P)
+    _check(load().gf2x_experiment_ipsi_tc(_ptr(P), P.shape[0], _ptr(out), lbo, sbo, _stream_ptr(stream)))
     return out
 
 

@@ -149,6 +149,7 @@ __constant__ int c_pm_terms[9][4] = {
 
 #include "bottom.cuh"
 #include "small.cuh"
+#include "tc_experiment.cuh"
 
 // =============================================================================================
 // changeRepr^-1 + InterleavedCombine: C_i = psi^-1(P[i]) (deg <= 126),
@@ -1756,6 +1757,20 @@ static gf2x_status comm_map_peers(gf2x_comm_s* c, cudaStream_t st) {
 }
 
 int gf2x_comm_peer_memory(gf2x_comm_t comm) { return comm ? comm->p2p : -1; }
+
+gf2x_status gf2x_experiment_ipsi_tc(const void* P, uint64_t n, void* out, uint32_t lbo, uint32_t sbo, void* stream) {
+    if (!P || !out) return fail(GF2X_EINVAL, "null argument");
+    int dev;
+    DeviceState* ds;
+    gf2x_status s = get_device(&dev, &ds);
+    if (s != GF2X_OK) return s;
+    const uint64_t ntiles = (n + 127) >> 7;
+    ProfScope ps("k_ipsi_tc", 32.0 * n, (cudaStream_t)stream);
+    k_ipsi_tc<<<grid_for(ntiles, 1, ds->sm_count, env_int("GF2X_TC_OCC", 4, 1, 4)), TC_THREADS, 0, (cudaStream_t)stream>>>(
+        (const uint4*)P, n, ds->tabs, (uint4*)out, lbo ? lbo : 128, sbo ? sbo : 1024);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GF2X_OK : fail(GF2X_ECUDA, std::string("ipsi tc launch: ") + cudaGetErrorString(e));
+}
 
 gf2x_status gf2x_comm_check(gf2x_comm_t comm) {
     if (!comm) return fail(GF2X_EINVAL, "null communicator");
