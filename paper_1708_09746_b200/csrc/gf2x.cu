@@ -528,6 +528,9 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_slab<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_small<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_small<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_small<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_small<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_small<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_slab<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_ipsi_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_ipsi_bs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1412,16 +1415,46 @@ static int small_cluster(const Plan& P) {
     cvt_ops(P.mb, 0, ob);
     cvt_ops(P.m, 0, oi);
     if (oa.size() > SM_MAX_OPS || ob.size() > SM_MAX_OPS || oi.size() > SM_MAX_OPS) return 0;
-    if (P.batch == 1 && P.m >= 7) return 4;   // one product: its limbs on four CTAs
+    if (P.batch == 1 && P.m >= 7) {   // one product: its limbs on four CTAs, with m >= 9 (8) also its points on
+        // four (two) segments: 16 (8) CTAs; GF2X_SMALL_CL = 4 / 8 / 16 caps the cluster
+        const int cap = env_int("GF2X_SMALL_CL", 16, 4, 16);
+        if (cap >= 16 && P.m >= 9) return 16;
+        if (cap >= 8 && P.m >= 8) return 8;
+        return 4;
+    }
     // batches keep the multi-pass path: one CTA per 2^9-point product measured 1.12 ms at c2 against 0.56
     // (per-butterfly constants and M4R-4 changeRepr^-1 lookups cost more than the bit-sliced bottom kernel);
     // GF2X_SMALL_BATCH=1 selects it (tested)
-    if (P.batch > 1 && env_flag("GF2X_SMALL_BATCH")) return small_layout(P.m, 1).total * 4 <= 200 * 1024 ? 1 : (P.m >= 7 ? 4 : 0);
+    if (P.batch > 1 && env_flag_now("GF2X_SMALL_BATCH")) return small_layout(P.m, 1).total * 4 <= 200 * 1024 ? 1 : (P.m >= 7 ? 4 : 0);
     return 0;
 }
 
 static gf2x_status run_small(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
                              const Plan& P, int CL, DeviceState* ds, cudaStream_t st) {
+    if (CL == 16) {   // a 16-CTA cluster is non-portable: fall back to 8 where the device cannot hold one
+        static int ok16[64];   // per device: 0 unknown, 1 yes, 2 no
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 64 && ok16[dev] == 0) {
+            cudaLaunchConfig_t q;
+            memset(&q, 0, sizeof(q));
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 16;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            q.attrs = at;
+            q.numAttrs = 1;
+            q.blockDim = dim3(SM_THREADS);
+            q.gridDim = dim3(16);
+            q.dynamicSmemBytes = (size_t)small_layout(P.m, 16, true).total * 4;
+            int ncl = 0;
+            const cudaError_t qe = cudaOccupancyMaxActiveClusters(&ncl, k_small<16>, &q);
+            if (qe != cudaSuccess) cudaGetLastError();
+            ok16[dev] = (qe == cudaSuccess && ncl >= 1) ? 1 : 2;
+        }
+        if (dev >= 64 || ok16[dev] != 1) CL = 8;
+    }
     SmallParams sp;
     memset(&sp, 0, sizeof(sp));
     sp.a = a; sp.b = b; sp.c = c;
@@ -1436,9 +1469,27 @@ static gf2x_status run_small(const uint64_t* a, uint64_t a_bits, const uint64_t*
     for (size_t i = 0; i < ob.size(); i++) sp.ops_b[i] = ob[i];
     for (size_t i = 0; i < oi.size(); i++) sp.ops_i[i] = oi[i];
     sp.tabs = ds->tabs;
-    const size_t sm = (size_t)small_layout(P.m, CL).total * 4;
+    // segmented conversions (small.cuh sm_conv_op): op list idx of 2^mm units -> mode, top-run and low-block lengths
+    auto seg_cvt = [&](int mm, int idx) {
+        sp.cmode[idx] = 0; sp.ntop[idx] = 0; sp.nlow[idx] = 0;
+        const int QB = small_qb(CL);
+        if (QB == 0 || mm <= 1 || env_flag_now("GF2X_SMALL_NO_SEGCVT")) return;
+        if (mm <= P.m - QB) { if (idx < 2) sp.cmode[idx] = 2; return; }
+        int K = 1;
+        while (2 * K <= mm - 1) K *= 2;   // (cvt_ops' split)
+        if (K > P.m - QB) return;
+        std::vector<CvtOp> low;
+        cvt_ops(K, 0, low);
+        sp.cmode[idx] = 1; sp.ntop[idx] = mm - K; sp.nlow[idx] = (int)low.size();
+    };
+    seg_cvt(P.ma, 0);
+    seg_cvt(P.mb, 1);
+    seg_cvt(P.m, 2);
+    // the segment's FFT constants precomputed per CTA when they fit (GF2X_SMALL_NO_KT=1: per layer and thread)
+    sp.kt = !env_flag_now("GF2X_SMALL_NO_KT") && (size_t)small_layout(P.m, CL, true).total * 4 <= 220 * 1024;
+    const size_t sm = (size_t)small_layout(P.m, CL, sp.kt != 0).total * 4;
     const double bytes = (double)P.batch * 8.0 * (P.na + P.nb + P.na + P.nb);
-    ProfScope ps(CL == 1 ? "k_small<1>" : "k_small<4>", bytes, st);
+    ProfScope ps(CL == 1 ? "k_small<1>" : (CL == 4 ? "k_small<4>" : (CL == 8 ? "k_small<8>" : "k_small<16>")), bytes, st);
     cudaError_t e;
     if (CL == 1) {
         const int occ = std::max(1, (int)(220 * 1024 / (sm + 1024)));
@@ -1449,7 +1500,7 @@ static gf2x_status run_small(const uint64_t* a, uint64_t a_bits, const uint64_t*
         memset(&cfg, 0, sizeof(cfg));
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 4;
+        attr[0].val.clusterDim.x = CL;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
@@ -1457,9 +1508,9 @@ static gf2x_status run_small(const uint64_t* a, uint64_t a_bits, const uint64_t*
         cfg.blockDim = dim3(SM_THREADS);
         cfg.dynamicSmemBytes = sm;
         cfg.stream = st;
-        const uint64_t ncl = std::min<uint64_t>(P.batch, (uint64_t)(ds->sm_count / 4) * std::max(1, (int)(220 * 1024 / (sm + 1024))));
-        cfg.gridDim = dim3((unsigned)(4 * ncl));
-        e = cudaLaunchKernelEx(&cfg, k_small<4>, sp);
+        const uint64_t ncl = std::min<uint64_t>(P.batch, (uint64_t)(ds->sm_count / CL) * std::max(1, (int)(220 * 1024 / (sm + 1024))));
+        cfg.gridDim = dim3((unsigned)(CL * ncl));
+        e = cudaLaunchKernelEx(&cfg, CL == 4 ? k_small<4> : (CL == 8 ? k_small<8> : k_small<16>), sp);
         if (e == cudaSuccess) e = cudaGetLastError();
     }
     return e == cudaSuccess ? GF2X_OK : fail(GF2X_ECUDA, std::string("small launch: ") + cudaGetErrorString(e));
