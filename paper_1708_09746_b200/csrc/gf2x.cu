@@ -440,6 +440,7 @@ struct DeviceState {
     struct DevTables256* tabs256 = nullptr;   // w = 128 tables (w128.cuh), built on first use
     struct DevTablesA4* tabsA4 = nullptr;     // Alg. 4 tables (alg4.cuh), built on first use
     std::map<int, uint4*> frob;               // App. C constants per m (frob.cuh), built on first use
+    std::map<int, uint32_t*> small_kt;        // k_small FFT constants per (m, segments) (get_small_kt)
     void* shard_ws = nullptr;    // simulation workspace (gf2x_mul_sharded_sim)
     size_t shard_ws_bytes = 0;
     int sm_count = 0;
@@ -1429,6 +1430,46 @@ static int small_cluster(const Plan& P) {
     return 0;
 }
 
+// The FFT constants of k_small (small.cuh KT) for 2^m points cut into 2^QB segments, every segment's table
+// (ktw words each, 16-byte multiples): K_b = c v_b for each local layer and block, c = s_k(block base) the XOR
+// of S[k][j] over the base's bits (layer_const), computed on the host once per device and (m, QB) like the
+// App. C constants (frob.cuh); the kernel copies its segment's table with cp.async instead of building it.
+static gf2x_status get_small_kt(DeviceState* ds, int m, int QB, const uint32_t** out, uint32_t* ktw) {
+    const int mloc = m - QB;
+    *ktw = (kt_off(m, mloc, mloc) + 3) & ~3u;
+    std::lock_guard<std::mutex> lk(g_mu);
+    const int key = m * 4 + QB;
+    auto it = ds->small_kt.find(key);
+    if (it != ds->small_kt.end()) { *out = it->second; return GF2X_OK; }
+    const uint32_t seg = 1u << mloc, QC = 1u << QB;
+    std::vector<uint32_t> h((size_t)QC * *ktw, 0u);
+    for (uint32_t q = 0; q < QC; q++)
+        for (int k = 0; k < mloc; k++) {
+            const int W = sm_width(m - k);
+            for (uint32_t blk = 0; blk < (seg >> (k + 1)); blk++) {
+                uint32_t bb = (q * seg + (blk << (k + 1))) >> (k + 1), cst = 0;
+                for (int j = k + 1; bb; bb >>= 1, j++)
+                    if (bb & 1) cst ^= ds->host->S[k * 32 + j];
+                uint32_t K[16];
+                if (W == 2) sm_consts<2>(cst, K);
+                else if (W == 4) sm_consts<4>(cst, K);
+                else if (W == 8) sm_consts<8>(cst, K);
+                else sm_consts<16>(cst, K);
+                uint32_t* d = h.data() + (size_t)q * *ktw + kt_off(m, mloc, k) + blk * W;
+                for (int b = 0; b < W; b++) d[b] = K[b];
+            }
+        }
+    uint32_t* d = nullptr;
+    if (cudaMalloc(&d, h.size() * 4) != cudaSuccess) return fail(GF2X_ENOMEM, "k_small constants");
+    if (cudaMemcpy(d, h.data(), h.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return fail(GF2X_ECUDA, "k_small constants");
+    }
+    ds->small_kt[key] = d;
+    *out = d;
+    return GF2X_OK;
+}
+
 static gf2x_status run_small(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
                              const Plan& P, int CL, DeviceState* ds, cudaStream_t st) {
     if (CL == 16) {   // a 16-CTA cluster is non-portable: fall back to 8 where the device cannot hold one
@@ -1469,24 +1510,29 @@ static gf2x_status run_small(const uint64_t* a, uint64_t a_bits, const uint64_t*
     for (size_t i = 0; i < ob.size(); i++) sp.ops_b[i] = ob[i];
     for (size_t i = 0; i < oi.size(); i++) sp.ops_i[i] = oi[i];
     sp.tabs = ds->tabs;
-    // segmented conversions (small.cuh sm_conv_op): op list idx of 2^mm units -> mode, top-run and low-block lengths
+    // split conversions (small.cuh sm_conv_op / sm_low_block): op list idx of 2^mm units -> top-run and
+    // low-block lengths and the low block's window bits K (split only when the windows fit a point segment)
     auto seg_cvt = [&](int mm, int idx) {
-        sp.cmode[idx] = 0; sp.ntop[idx] = 0; sp.nlow[idx] = 0;
-        const int QB = small_qb(CL);
-        if (QB == 0 || mm <= 1 || env_flag_now("GF2X_SMALL_NO_SEGCVT")) return;
-        if (mm <= P.m - QB) { if (idx < 2) sp.cmode[idx] = 2; return; }
+        sp.split[idx] = 0; sp.ntop[idx] = 0; sp.nlow[idx] = 0; sp.kw[idx] = 0;
+        if (mm <= 2 || env_flag_now("GF2X_SMALL_NO_SEGCVT")) return;
         int K = 1;
         while (2 * K <= mm - 1) K *= 2;   // (cvt_ops' split)
-        if (K > P.m - QB) return;
+        if (K > P.m - small_qb(CL)) return;
         std::vector<CvtOp> low;
         cvt_ops(K, 0, low);
-        sp.cmode[idx] = 1; sp.ntop[idx] = mm - K; sp.nlow[idx] = (int)low.size();
+        sp.split[idx] = 1; sp.ntop[idx] = mm - K; sp.nlow[idx] = (int)low.size(); sp.kw[idx] = K;
     };
     seg_cvt(P.ma, 0);
     seg_cvt(P.mb, 1);
     seg_cvt(P.m, 2);
     // the segment's FFT constants precomputed per CTA when they fit (GF2X_SMALL_NO_KT=1: per layer and thread)
     sp.kt = !env_flag_now("GF2X_SMALL_NO_KT") && (size_t)small_layout(P.m, CL, true).total * 4 <= 220 * 1024;
+    sp.ktg = nullptr;
+    sp.ktw = 0;
+    if (sp.kt && !env_flag_now("GF2X_SMALL_KT_BUILD")) {   // (GF2X_SMALL_KT_BUILD=1: every CTA builds its table)
+        gf2x_status ks = get_small_kt(ds, P.m, small_qb(CL), &sp.ktg, &sp.ktw);
+        if (ks != GF2X_OK) return ks;
+    }
     const size_t sm = (size_t)small_layout(P.m, CL, sp.kt != 0).total * 4;
     const double bytes = (double)P.batch * 8.0 * (P.na + P.nb + P.na + P.nb);
     ProfScope ps(CL == 1 ? "k_small<1>" : (CL == 4 ? "k_small<4>" : (CL == 8 ? "k_small<8>" : "k_small<16>")), bytes, st);
@@ -2113,3 +2159,10 @@ gf2x_status gf2x_release(int device) {
 const char* gf2x_version(void) { return "gf2x-b200 0.3 (sm_100a; Alg. 5 w=64 TGF(2^128) and w=128 TGF(2^256); Alg. 4 GF(2^128))"; }
 
 }  // extern "C"
+
+#ifdef SM_TRACE
+// (SM_TRACE builds only: the phase timestamps of the last k_small launch, 16 CTAs x 16 points)
+extern "C" int gf2x_debug_small_trace(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, g_sm_trace, sizeof(g_sm_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif

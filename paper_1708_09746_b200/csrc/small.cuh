@@ -33,9 +33,11 @@ struct SmallParams {
     int m, ma, mb;
     int nops_a, nops_b, nops_i;
     int kt;   // 1: the FFT constants of the CTA's segment precomputed once into shared memory (KT)
-    // segmented conversions (CL >= 8; sm_conv_op): per op list (a, b, inverse) the mode (0: every op on the
-    // whole array, 1: split, 2: the list lies inside segment 0) and the lengths of its top run and low block
-    int cmode[3], ntop[3], nlow[3];
+    const uint32_t* ktg;   // (kt) the per-device copy of every segment's KT (get_small_kt): copied, not computed
+    uint32_t ktw;          // its words per segment
+    // split conversions (sm_conv_op): per op list (a, b, inverse) split[i] = 1: top run + high block
+    // CTA-wide, low block (windows of 2^kw[i] units) warp by warp, on my segment only; 0: every op CTA-wide
+    int split[3], ntop[3], nlow[3], kw[3];
     CvtOp ops_a[SM_MAX_OPS], ops_b[SM_MAX_OPS], ops_i[SM_MAX_OPS];
     const DevTables* tabs;
 };
@@ -87,7 +89,7 @@ __device__ __forceinline__ uint32_t sm_smul(uint32_t u, const uint32_t* K) {
     return r;
 }
 template <int W>
-__device__ __forceinline__ void sm_consts(uint32_t c, uint32_t* K) {
+__host__ __device__ __forceinline__ void sm_consts(uint32_t c, uint32_t* K) {
     K[0] = c;
     K[1] = mulx1(c);
     if constexpr (W > 2) {
@@ -115,18 +117,13 @@ __device__ __forceinline__ void sm_kt_store(uint32_t c, uint32_t* d) {
 // BasisCvt's op list for 2^mm units (cvt_ops, gf2x.cu) is [top run: levels mm .. K+1 with K] [low block: the
 // list for 2^K units, levels <= K] [high block: the list for the bits [K, mm), units of 2^K words].  The high
 // block acts on the index bits >= K identically for every offset below 2^K, the low block inside every aligned
-// 2^K window identically, so the two commute (Kronecker factors).  With point segments of 2^mloc >= 2^K units
-// each CTA runs the top run and the high block on the whole array (few ops) and the low block (most ops) on its
-// own segment only; the inverse runs the inverted low block on its segment first, then the rest on the whole
-// (gathered) array.  Step s of the forward schedule -> op index, and whether it runs segment-locally.
-__device__ __forceinline__ int sm_conv_op(int s, int mode, int ntop, int nlow, int nops, bool& local) {
-    local = mode == 2;
-    if (mode != 1) return s;
-    const int nhigh = nops - ntop - nlow;
-    if (s < ntop) return s;
-    if (s < ntop + nhigh) return ntop + nlow + (s - ntop);
-    local = true;
-    return ntop + (s - ntop - nhigh);
+// 2^K window identically, so the two commute (Kronecker factors).  So the forward runs the top run and the
+// high block CTA-wide (few ops, a barrier per sweep) and then the low block (most ops) window by window, one
+// warp per window (__syncwarp between sweeps), only on the windows of my point segment; the inverse runs the
+// inverted low block window by window first, then the rest CTA-wide on the whole (gathered) array.
+// Step s of the CTA-wide forward schedule (split lists: top run, then high block) -> op index.
+__device__ __forceinline__ int sm_conv_op(int s, int split, int ntop, int nlow) {
+    return (!split || s < ntop) ? s : s + nlow;
 }
 
 // Alg. 2 step (lg, K) on units of type T in s[0, 2^mm) as two sweeps, A (targets [h, h+u)) and B ([u, h)),
@@ -134,25 +131,68 @@ __device__ __forceinline__ int sm_conv_op(int s, int mode, int ntop, int nlow, i
 template <typename T>
 __device__ __forceinline__ void sm_sweep(T* s, int mm, int lg, int K, bool A, int tid, int nthr) {
     const uint32_t h = 1u << (lg - 1), u = h >> K, d = h - u;
-    const uint32_t nseg = 1u << (mm - lg);
-    if (A) {
-        const uint32_t n = nseg * u, lu = lg - 1 - K;   // u = 2^lu
-        for (uint32_t it = tid; it < n; it += nthr) {
-            const uint32_t seg = it >> lu, j = it & (u - 1);
-            const uint32_t t = (seg << lg) + h + j;
-            s[t] ^= s[t + d];
+    const uint32_t nseg = 1u << (mm - lg), lu = lg - 1 - K;   // u = 2^lu
+    const uint32_t n = A ? nseg * u : nseg * h;
+    // four targets per thread at a time: all loads first (a phase's targets and sources are disjoint and every
+    // target is written once, so the loads of a batch may run ahead of its stores)
+    for (uint32_t b0 = tid; b0 < n; b0 += 4 * nthr) {
+        T v[4];
+        uint32_t t[4];
+        bool ok[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const uint32_t it = b0 + c * nthr;
+            uint32_t seg, j;
+            if (A) {
+                seg = it >> lu; j = it & (u - 1);
+                t[c] = (seg << lg) + h + j;
+                ok[c] = it < n;
+            } else {
+                seg = it >> (lg - 1); j = it & (h - 1);
+                t[c] = (seg << lg) + j;
+                ok[c] = it < n && j >= u;
+            }
+            if (ok[c]) v[c] = s[t[c]] ^ s[t[c] + d];
         }
-    } else {
-        const uint32_t n = nseg * h;
-        for (uint32_t it = tid; it < n; it += nthr) {
-            const uint32_t seg = it >> (lg - 1), j = it & (h - 1);
-            if (j < u) continue;
-            const uint32_t t = (seg << lg) + j;
-            s[t] ^= s[t + d];
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+            if (ok[c]) s[t[c]] = v[c];
+    }
+}
+
+// the low block (ops [ntop, ntop + nlow)) of a split list on the windows of 2^kw units in [lo, hi), a warp per
+// window; INV: the inverted ops in reverse order
+template <typename T, bool INV>
+__device__ __forceinline__ void sm_low_block(T* S, uint32_t lo, uint32_t hi, int kw, const CvtOp* ops, int ntop,
+                                             int nlow, uint32_t nitems_before, uint32_t stride) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t nwin = hi > lo ? (hi - lo) >> kw : 0;
+    for (uint32_t it = warp; it < nitems_before + nwin; it += stride) {
+        if (it < nitems_before) continue;
+        T* w = S + lo + ((it - nitems_before) << kw);
+        for (int j = 0; j < nlow; j++) {
+            const CvtOp op = ops[ntop + (INV ? nlow - 1 - j : j)];
+            sm_sweep<T>(w, kw, op.lg, op.K, !INV, lane, 32);
+            __syncwarp();
+            sm_sweep<T>(w, kw, op.lg, op.K, INV, lane, 32);
+            __syncwarp();
         }
     }
 }
 
+// 32 x 32 bit transpose across a warp: lane j holds word j (row j) in, column j out (bit i = bit j of word i)
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t v, uint32_t lane) {
+#pragma unroll
+    for (int sh = 16; sh >= 1; sh >>= 1) {
+        const uint32_t M = sh == 16 ? 0x0000FFFFu : (sh == 8 ? 0x00FF00FFu : (sh == 4 ? 0x0F0F0F0Fu : (sh == 2 ? 0x33333333u : 0x55555555u)));
+        const uint32_t t = __shfl_xor_sync(0xffffffffu, v, sh);
+        v = (lane & sh) ? ((v & ~M) | ((t & ~M) >> sh)) : ((v & M) | ((t & M) << sh));
+    }
+    return v;
+}
+__device__ __forceinline__ void sm_cp4(uint32_t* dst, const uint32_t* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 template <int CL>
 __device__ __forceinline__ uint32_t* sm_peer(uint32_t* p, int rank) {
     if (CL == 1) return p;
@@ -179,7 +219,8 @@ __device__ __forceinline__ void sm_sync() {
 #define SM_KD_LAYERS 9
 template <int W, bool INV>
 __device__ __forceinline__ void sm_layer(uint32_t* A, uint32_t* B, int nops, int m, int k, int LPC, uint32_t N,
-                                         const uint32_t* KD, uint32_t seg, uint32_t base, const uint32_t* KTk) {
+                                         const uint32_t* KD, uint32_t seg, uint32_t base, const uint32_t* KTk,
+                                         int dsh) {
     const uint32_t half = seg >> 1;   // butterflies of the segment [base, base + seg)
     uint32_t K0[W];
     bool have = false;
@@ -216,20 +257,22 @@ __device__ __forceinline__ void sm_layer(uint32_t* A, uint32_t* B, int nops, int
             uint32_t* X = o ? B : A;
             for (int l = 0; l < LPC; l++) {
                 uint32_t* x = X + l * N;
-                uint32_t x0 = x[i0], x1 = x[i1];
+                const uint32_t j0 = i0 + dsh, j1 = i1 + dsh;   // (data of the segment at base + dsh)
+                uint32_t x0 = x[j0], x1 = x[j1];
                 if (INV) x1 ^= x0;
                 x0 ^= sm_smul<W>(x1, K);
                 if (!INV) x1 ^= x0;
-                x[i0] = x0;
-                x[i1] = x1;
+                x[j0] = x0;
+                x[j1] = x1;
             }
         }
     }
 }
-// layers [0, mloc) on the segment [base, base + 2^mloc) (mloc = m, base = 0: the whole transform)
+// layers [0, mloc) on the segment [base, base + 2^mloc) (mloc = m, base = 0: the whole transform), its data
+// stored at base + dsh
 template <bool INV>
 __device__ __forceinline__ void sm_fft(uint32_t* A, uint32_t* B, int nops, int m, int LPC, uint32_t N, const uint32_t* KD,
-                                       int mloc, uint32_t base, const uint32_t* KT) {
+                                       int mloc, uint32_t base, const uint32_t* KT, int dsh) {
     const uint32_t seg = 1u << mloc;
     // layer k's KT entries start at kt_off(k): walked incrementally (up for the inverse, down for the forward)
     uint32_t kto = INV ? 0u : kt_off(m, mloc, mloc - 1);
@@ -239,10 +282,10 @@ __device__ __forceinline__ void sm_fft(uint32_t* A, uint32_t* B, int nops, int m
         const uint32_t* KTk = KT ? KT + kto : nullptr;
         if (INV) kto += (seg >> (k + 1)) * (uint32_t)sm_width(w);
         else if (k > 0) kto -= (seg >> k) * (uint32_t)sm_width(w + 1);
-        if (w <= 2) sm_layer<2, INV>(A, B, nops, m, k, LPC, N, KD, seg, base, KTk);
-        else if (w <= 4) sm_layer<4, INV>(A, B, nops, m, k, LPC, N, KD, seg, base, KTk);
-        else if (w <= 8) sm_layer<8, INV>(A, B, nops, m, k, LPC, N, KD, seg, base, KTk);
-        else sm_layer<16, INV>(A, B, nops, m, k, LPC, N, KD, seg, base, KTk);
+        if (w <= 2) sm_layer<2, INV>(A, B, nops, m, k, LPC, N, KD, seg, base, KTk, dsh);
+        else if (w <= 4) sm_layer<4, INV>(A, B, nops, m, k, LPC, N, KD, seg, base, KTk, dsh);
+        else if (w <= 8) sm_layer<8, INV>(A, B, nops, m, k, LPC, N, KD, seg, base, KTk, dsh);
+        else sm_layer<16, INV>(A, B, nops, m, k, LPC, N, KD, seg, base, KTk, dsh);
         __syncthreads();
     }
 }
@@ -253,9 +296,14 @@ __device__ __forceinline__ void sm_fft(uint32_t* A, uint32_t* B, int nops, int m
 //   y0;  y1 ^ y0;  z2 = (y2 ^ y0) ^ C (y3 ^ y1);  (y3 ^ y1) ^ z2
 // inverse (layers m-2, m-1):
 //   y0;  y1 ^ y0;  (y2 ^ C (y3 ^ y2)) ^ y0;  (y3 ^ y2) ^ (y1 ^ y0)
-// (QC = 2: layer m-1 only, y0; y1 ^ y0 both ways).  Every CTA reads the other segments' values over DSMEM
-// into registers, the cluster barrier orders all reads before any write, then each writes its own segment.
+// (QC = 2: layer m-1 only, y0; y1 ^ y0 both ways).  Every CTA reads the other segments' values over DSMEM.
+// Double-buffered: segment s's canonical region is [s seg, (s+1) seg) of its limb arrays, its working region
+// (where its FFT layers run, between the two cross steps) the region of segment (s+1) mod QC of the SAME
+// arrays (free then: each CTA only holds its own segment).  The forward cross reads canonical regions and
+// writes the working one, the inverse reads working regions and writes the canonical one, so no CTA ever
+// writes a region a peer is reading and one cluster barrier (inputs complete) suffices.
 #define SM_CROSS_MAXP 4
+__host__ __device__ inline uint32_t sm_wreg(uint32_t s, int QC) { return (s + 1) & (uint32_t)(QC - 1); }
 template <int CL, bool INV>
 __device__ __forceinline__ void sm_cross(uint32_t* A, uint32_t* B, int nops, int m, uint32_t q, uint32_t l0,
                                          uint32_t N) {
@@ -269,7 +317,7 @@ __device__ __forceinline__ void sm_cross(uint32_t* A, uint32_t* B, int nops, int
         uint32_t* X = o ? B : A;
         const uint32_t* src[QC];
 #pragma unroll
-        for (int s = 0; s < QC; s++) src[s] = sm_limb<CL>(X, l0, s, N) + s * seg;
+        for (int s = 0; s < QC; s++) src[s] = sm_limb<CL>(X, l0, s, N) + (INV ? sm_wreg(s, QC) : s) * seg;
 #pragma unroll
         for (int pi = 0; pi < SM_CROSS_MAXP; pi++) {
             const uint32_t i = threadIdx.x + pi * blockDim.x;
@@ -291,9 +339,8 @@ __device__ __forceinline__ void sm_cross(uint32_t* A, uint32_t* B, int nops, int
             out[o][pi] = r;
         }
     }
-    sm_sync<CL>();   // every read of the old values done
     for (int o = 0; o < nops; o++) {
-        uint32_t* X = (o ? B : A) + q * seg;
+        uint32_t* X = (o ? B : A) + (INV ? q : sm_wreg(q, QC)) * seg;
 #pragma unroll
         for (int pi = 0; pi < SM_CROSS_MAXP; pi++) {
             const uint32_t i = threadIdx.x + pi * blockDim.x;
@@ -304,9 +351,24 @@ __device__ __forceinline__ void sm_cross(uint32_t* A, uint32_t* B, int nops, int
     __syncthreads();
 }
 
+// SM_TRACE builds (tools/dev/small_trace.py): %globaltimer of thread 0 of every CTA at the phase ends
+#ifdef SM_TRACE
+__device__ unsigned long long g_sm_trace[16][16];
+#define SM_T(i)                                                                                              \
+    do {                                                                                                     \
+        if (threadIdx.x == 0 && blockIdx.x < 16) {                                                           \
+            unsigned long long t_;                                                                           \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                           \
+            g_sm_trace[blockIdx.x][i] = t_;                                                                  \
+        }                                                                                                    \
+    } while (0)
+#else
+#define SM_T(i) do {} while (0)
+#endif
 template <int CL>
 __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
     extern __shared__ __align__(1024) uint32_t sm[];
+    SM_T(0);
     const int m = p.m;
     constexpr int QC = CL >= 8 ? CL / 4 : 1;   // segments of the points
     constexpr int QB = QC == 4 ? 2 : (QC == 2 ? 1 : 0);
@@ -328,25 +390,33 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
     const uint32_t l0 = CL >= 4 ? (rank & 3) : 0;   // my first limb
     const uint32_t q = CL >= 4 ? (rank >> 2) : 0;    // my segment of the points
     const uint32_t seg = N >> QB, sbase = q * seg;
+    // with segments, the FFT data lives in the working region between the cross steps (sm_cross)
+    const int dsh = QB ? (int)(sm_wreg(q, QC) * seg) - (int)sbase : 0;
     // ---- tables (once per CTA): psi (M4R-8: my limbs), psi^-1 (M4R-4, word-planar: entry (o, t, x) = limb o of
     // psi^-1(x << 4t) = limb o of the M4R-8 entry of byte t/2 with x in its nibble t&1)
+    // (asynchronous copies: they complete under the constant builds, Split and BasisCvt; waited before psi)
     if (CL == 1) {
-        for (int i = tid; i < 8 * 256; i += nthr) reinterpret_cast<uint4*>(ptab)[i] = p.tabs->psi64[i];
+        for (int i = tid; i < 8 * 256; i += nthr) cp_async16(reinterpret_cast<uint4*>(ptab) + i, p.tabs->psi64 + i);
     } else {
-        for (int i = tid; i < 8 * 256; i += nthr) ptab[i] = reinterpret_cast<const uint32_t*>(p.tabs->psi64 + i)[l0];
+        for (int i = tid; i < 8 * 256; i += nthr) sm_cp4(ptab + i, reinterpret_cast<const uint32_t*>(p.tabs->psi64 + i) + l0);
     }
     for (int i = tid; i < 4 * 32 * 16; i += nthr) {
         const int o = i >> 9, t = (i >> 4) & 31, x = i & 15;
-        itab[i] = reinterpret_cast<const uint32_t*>(p.tabs->ipsi + (t >> 1) * 256 + (x << (4 * (t & 1))))[o];
+        sm_cp4(itab + i, reinterpret_cast<const uint32_t*>(p.tabs->ipsi + (t >> 1) * 256 + (x << (4 * (t & 1)))) + o);
     }
-    if (tid < SM_KD_LAYERS * 2) {   // KD[k][i] = s_k(v_(9+i)) v_b, b < 16
+    cp_async_commit();
+    if (!KT && tid < SM_KD_LAYERS * 2) {   // KD[k][i] = s_k(v_(9+i)) v_b, b < 16 (without KT only)
         const int k = tid >> 1, i = tid & 1;
         uint32_t K[16];
         sm_consts<16>(k < 9 + i ? c_S[k * 32 + 9 + i] : 0u, K);
 #pragma unroll
         for (int b = 0; b < 16; b++) KD[tid * 16 + b] = K[b];
     }
-    if (KT) {   // the segment's FFT constants, once per CTA: layer k has 2^(mloc-k-1) blocks of sm_width(m-k) words
+    if (KT && p.ktg) {   // the segment's FFT constants: copied from the per-device table (asynchronously)
+        const uint4* src = reinterpret_cast<const uint4*>(p.ktg + (size_t)q * p.ktw);
+        for (uint32_t i = tid; i < (p.ktw >> 2); i += nthr) cp_async16(reinterpret_cast<uint4*>(KT) + i, src + i);
+        cp_async_commit();
+    } else if (KT) {   // ... or built once per CTA: layer k has 2^(mloc-k-1) blocks of sm_width(m-k) words
         const int mloc = m - QB;
         for (uint32_t i = tid; i < seg - 1; i += nthr) {
             int k = 0;
@@ -367,33 +437,52 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
         const uint64_t* a = p.a + pr * p.na;
         const uint64_t* b = p.b + pr * p.nb;
         __syncthreads();   // (tables; the previous product's last reads of SA .. PR)
-        // ---- 1 Split + pad
+        SM_T(1);
+        // ---- 1 Split + pad (asynchronous copies; the last word of an operand with a partial top word masked)
         const uint32_t ra = (uint32_t)(p.a_bits & 63), rb = (uint32_t)(p.b_bits & 63);
         for (uint32_t i = tid; i < N; i += nthr) {
-            uint64_t x = i < p.na ? a[i] : 0ull, y = i < p.nb ? b[i] : 0ull;
-            if (i == p.na - 1 && ra) x &= (1ull << ra) - 1;
-            if (i == p.nb - 1 && rb) y &= (1ull << rb) - 1;
-            SA[i] = x;
-            SB[i] = y;
+            if (i >= p.na) SA[i] = 0ull;
+            else if (i == p.na - 1 && ra) SA[i] = a[i] & ((1ull << ra) - 1);
+            else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(SA + i)), "l"(a + i) : "memory");
+            if (i >= p.nb) SB[i] = 0ull;
+            else if (i == p.nb - 1 && rb) SB[i] = b[i] & ((1ull << rb) - 1);
+            else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(SB + i)), "l"(b + i) : "memory");
         }
+        cp_async_commit();
+        cp_async_wait<0>();   // (also the tables, on the first product)
         __syncthreads();
+        SM_T(2);
         // ---- 2 BasisCvt of both operands (every CTA of the cluster; with segments the low block on my segment only)
-        for (int o = 0; o < max(p.nops_a, p.nops_b); o++)
-            for (int ph = 0; ph < 2; ph++) {
+        {
+            // CTA-wide steps (a CTA whose segment lies past an operand skips it: its part stays zero)
+            const int na_cta = p.split[0] ? p.nops_a - p.nlow[0] : p.nops_a;
+            const int nb_cta = p.split[1] ? p.nops_b - p.nlow[1] : p.nops_b;
+            for (int o = 0; o < max(na_cta, nb_cta); o++)
+                for (int ph = 0; ph < 2; ph++) {
 #pragma unroll
-                for (int x = 0; x < 2; x++) {
-                    if (o >= (x ? p.nops_b : p.nops_a)) continue;
-                    bool local;
-                    const int oi = sm_conv_op(o, p.cmode[x], p.ntop[x], p.nlow[x], x ? p.nops_b : p.nops_a, local);
-                    const CvtOp op = x ? p.ops_b[oi] : p.ops_a[oi];
-                    uint64_t* S = x ? SB : SA;
-                    const int mm = x ? p.mb : p.ma;
-                    if (!local) sm_sweep<uint64_t>(S, mm, op.lg, op.K, ph == 0, tid, nthr);
-                    else if (p.cmode[x] == 2) { if (q == 0) sm_sweep<uint64_t>(S, mm, op.lg, op.K, ph == 0, tid, nthr); }
-                    else if ((sbase >> mm) == 0) sm_sweep<uint64_t>(S + sbase, m - QB, op.lg, op.K, ph == 0, tid, nthr);
+                    for (int x = 0; x < 2; x++) {
+                        const int mm = x ? p.mb : p.ma;
+                        if (o >= (x ? nb_cta : na_cta) || (sbase >> mm) != 0) continue;
+                        const int oi = sm_conv_op(o, p.split[x], p.ntop[x], p.nlow[x]);
+                        const CvtOp op = x ? p.ops_b[oi] : p.ops_a[oi];
+                        sm_sweep<uint64_t>(x ? SB : SA, mm, op.lg, op.K, ph == 0, tid, nthr);
+                    }
+                    __syncthreads();
                 }
-                __syncthreads();
+            // the low blocks, window by window on my segment's part of each operand
+            uint32_t before = 0;
+#pragma unroll
+            for (int x = 0; x < 2; x++) {
+                if (!p.split[x]) continue;
+                const uint32_t ext = 1u << (x ? p.mb : p.ma);
+                const uint32_t lo = QB ? sbase : 0u, hi = min(lo + seg, ext);
+                sm_low_block<uint64_t, false>(x ? SB : SA, lo, hi, p.kw[x], x ? p.ops_b : p.ops_a, p.ntop[x], p.nlow[x],
+                                              before, nthr >> 5);
+                before += hi > lo ? (hi - lo) >> p.kw[x] : 0;
             }
+            __syncthreads();
+        }
+            SM_T(3);
         // ---- 3 changeRepr: my limbs of psi(SA[i]), psi(SB[i]), i in my segment
         for (uint32_t i = sbase + tid; i < sbase + seg; i += nthr) {
             const uint64_t x = SA[i], y = SB[i];
@@ -415,27 +504,26 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
             }
         }
         __syncthreads();
+        SM_T(4);
         // ---- 4 FFT_LCH of both spectra, my limbs (with segments: the top QB layers across them first)
         if constexpr (QB > 0) sm_cross<CL, false>(AL, BL, 2, m, q, l0, N);
-        sm_fft<false>(AL, BL, 2, m, LPC, N, KD, m - QB, sbase, KT);
+        SM_T(5);
+        sm_fft<false>(AL, BL, 2, m, LPC, N, KD, m - QB, sbase, KT, dsh);
         sm_sync<CL>();   // every limb of A and B complete (pointmul reads them from every CTA)
+        SM_T(6);
         // ---- 5 pointmul, bit-sliced: my GC groups of 32 consecutive elements
         const uint32_t g0 = rank * GC;
-        for (uint32_t it = tid; it < GC * 8; it += nthr) {   // (group, limb, operand): transpose into planes
+        const uint32_t lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
+        for (uint32_t it = warp; it < GC * 8; it += nwarp) {   // (group, limb, operand): a warp transposes into planes
             const uint32_t g = it >> 3, l = (it >> 1) & 3, o = it & 1;
-            const uint32_t* src = sm_limb<CL>(o ? BL : AL, l, q, N) + ((g0 + g) << 5);
-            uint32_t x[32];
-#pragma unroll
-            for (int j = 0; j < 32; j++) x[j] = src[j];
-            transpose32(x);
-            uint32_t* d = PL + ((o * 4 + l) * GC + g) * 33;
-#pragma unroll
-            for (int j = 0; j < 32; j++) d[j] = x[j];
+            const uint32_t* src = sm_limb<CL>(o ? BL : AL, l, q, N) + (int)((g0 + g) << 5) + dsh;
+            PL[((o * 4 + l) * GC + g) * 33 + lane] = warp_transpose32(src[lane], lane);
         }
         __syncthreads();
+        SM_T(7);
         for (uint32_t it = tid; it < GC * 9; it += nthr) {   // (group, product): one bs_mul32 each
-            const uint32_t g = it / 9, q = it - g * 9;
-            const int mask = c_pm_terms[q][0];
+            const uint32_t g = it / 9, qq = it - g * 9;
+            const int mask = c_pm_terms[qq][0];
             uint32_t x[32], y[32], r[32];
 #pragma unroll
             for (int j = 0; j < 32; j++) { x[j] = 0; y[j] = 0; }
@@ -448,20 +536,21 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
                     for (int j = 0; j < 32; j++) { x[j] ^= pa[j]; y[j] ^= pb[j]; }
                 }
             bs_mul32(x, y, r);
-            uint32_t* d = PR + (g * 9 + q) * 33;
+            uint32_t* d = PR + (g * 9 + qq) * 33;
 #pragma unroll
             for (int j = 0; j < 32; j++) d[j] = r[j];
         }
         __syncthreads();
+        SM_T(8);
         for (uint32_t it = tid; it < GC * 4; it += nthr) {   // (group, result limb): R_L = sum of its terms
             const uint32_t g = it >> 2, L = it & 3;
             uint32_t acc[32], s1[32], s2[32], t[32];
 #pragma unroll
             for (int j = 0; j < 32; j++) { acc[j] = 0; s1[j] = 0; s2[j] = 0; }
 #pragma unroll 1
-            for (int q = 0; q < 9; q++) {
-                const uint32_t* src = PR + (g * 9 + q) * 33;
-                const bool r0 = (c_pm_terms[q][1] >> L) & 1, r1 = (c_pm_terms[q][2] >> L) & 1, r2 = (c_pm_terms[q][3] >> L) & 1;
+            for (int t9 = 0; t9 < 9; t9++) {
+                const uint32_t* src = PR + (g * 9 + t9) * 33;
+                const bool r0 = (c_pm_terms[t9][1] >> L) & 1, r1 = (c_pm_terms[t9][2] >> L) & 1, r2 = (c_pm_terms[t9][3] >> L) & 1;
                 if (r0) { for (int j = 0; j < 32; j++) acc[j] ^= src[j]; }
                 if (r1) { for (int j = 0; j < 32; j++) s1[j] ^= src[j]; }
                 if (r2) { for (int j = 0; j < 32; j++) s2[j] ^= src[j]; }
@@ -470,38 +559,43 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
 #pragma unroll
             for (int j = 0; j < 32; j++) acc[j] ^= t[j];
             bs_mul_v31sq(s2, t);
+            uint32_t* sc = PL + it * 33;   // (the operand planes are dead: the products have read them)
 #pragma unroll
-            for (int j = 0; j < 32; j++) acc[j] ^= t[j];
-            transpose32(acc);
-            uint32_t* dst = sm_limb<CL>(AL, L, q, N) + ((g0 + g) << 5);
-#pragma unroll
-            for (int j = 0; j < 32; j++) dst[j] = acc[j];
+            for (int j = 0; j < 32; j++) sc[j] = acc[j] ^ t[j];
+        }
+        __syncthreads();
+        for (uint32_t it = warp; it < GC * 4; it += nwarp) {   // back to elements: a warp transpose per item
+            const uint32_t g = it >> 2, L = it & 3;
+            uint32_t* dst = sm_limb<CL>(AL, L, q, N) + (int)((g0 + g) << 5) + dsh;
+            dst[lane] = warp_transpose32(PL[it * 33 + lane], lane);
         }
         sm_sync<CL>();   // every result limb delivered
+        SM_T(9);
         // ---- 6 iFFT_LCH, my limbs of the product (with segments: the top QB layers across them last, then
         // every CTA gathers its limb whole for iBasisCvt)
-        sm_fft<true>(AL, BL, 1, m, LPC, N, KD, m - QB, sbase, KT);
+        sm_fft<true>(AL, BL, 1, m, LPC, N, KD, m - QB, sbase, KT, dsh);
+        SM_T(10);
         // ---- 7 iBasisCvt, my limbs (u32 units; XOR acts limb-wise); segmented (cmode[2] == 1): the inverted low
         // block on my segment, then the gather, then the inverted high block and top run on the whole limb
         int o_hi = p.nops_i - 1;
+        if constexpr (QB > 0) sm_cross<CL, true>(AL, BL, 1, m, q, l0, N);
+        if (p.split[2]) {   // the inverted low block, window by window on my segment (every limb I hold)
+            for (uint32_t l = 0; l < LPC; l++)
+                sm_low_block<uint32_t, true>(AL + l * N, sbase, sbase + seg, p.kw[2], p.ops_i, p.ntop[2], p.nlow[2],
+                                             l * (seg >> p.kw[2]), nthr >> 5);
+            __syncthreads();
+        }
         if constexpr (QB > 0) {
-            sm_cross<CL, true>(AL, BL, 1, m, q, l0, N);
-            if (p.cmode[2] == 1) {
-                const int lo = p.ntop[2], hi = p.ntop[2] + p.nlow[2];
-                for (int o = hi - 1; o >= lo; o--)
-                    for (int ph = 0; ph < 2; ph++) {
-                        sm_sweep<uint32_t>(AL + sbase, m - QB, p.ops_i[o].lg, p.ops_i[o].K, ph == 1, tid, nthr);
-                        __syncthreads();
-                    }
-            }
             sm_sync<CL>();   // every segment final
+            SM_T(11);
             for (uint32_t i = tid; i < N; i += nthr)
                 if ((i >> (m - QB)) != q) AL[i] = sm_limb<CL>(AL, l0, i >> (m - QB), N)[i];
             __syncthreads();
+            SM_T(12);
         }
         for (int s = 0; s <= o_hi; s++) {
-            int o = o_hi - s;   // reversed forward order; segmented: high block reversed, then top run reversed
-            if (p.cmode[2] == 1) {
+            int o = o_hi - s;   // reversed forward order; split: high block reversed, then top run reversed
+            if (p.split[2]) {
                 const int nhigh = p.nops_i - p.ntop[2] - p.nlow[2];
                 if (s < nhigh) o = p.nops_i - 1 - s;
                 else if (s < nhigh + p.ntop[2]) o = p.ntop[2] - 1 - (s - nhigh);
@@ -514,6 +608,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
             }
         }
         sm_sync<CL>();   // every limb of the product converted
+        SM_T(13);
         // ---- 8 changeRepr^-1 + InterleavedCombine: out[w] = lo64(C_w) ^ hi64(C_(w-1)), C_i = 0 for i >= N
         const uint32_t* Lp[4];
 #pragma unroll
@@ -546,6 +641,8 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
             }
             cout[w] = ((uint64_t)(lo1 ^ hi3) << 32) | (lo0 ^ hi2);
         }
+        SM_T(14);
         sm_sync<CL>();   // (peers are done reading my limbs before they are overwritten / I exit)
+        SM_T(15);
     }
 }

@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(TC_THREADS, 4) k_ipsi_tc(const uint4* __restri
     __shared__ __align__(1024) unsigned char B[128 * 128];
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint32_t tmem_base;
-    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
     // canonical K-major, no swizzle: core matrix (row block rb = r / 8, k block kb = k / 16) at (rb * 8 + kb) * 128
     // bytes, its row r % 8 at + 16 (r % 8), byte k % 16
     auto off = [](uint32_t r, uint32_t k) { return (((r >> 3) * 8 + (k >> 4)) << 7) + ((r & 7) << 4) + (k & 15); };

@@ -1,7 +1,8 @@
-"""Host check of the segmented conversion schedule of k_small (csrc/small.cuh sm_conv_op, gf2x.cu seg_cvt):
-BasisCvt's op list for 2^mm units is [top run][low block: levels <= K][high block: bits >= K], and the kernel
-runs the low block AFTER the high block, on each 2^mloc-unit point segment separately (the two blocks commute:
-Kronecker factors); the inverse runs the inverted low block on its segment BEFORE the rest.  The schedule is
+"""Host check of the split conversion schedule of k_small (csrc/small.cuh sm_conv_op / sm_low_block, gf2x.cu
+seg_cvt): BasisCvt's op list for 2^mm units is [top run][low block: levels <= K][high block: bits >= K], and
+the kernel runs the low block AFTER the high block, window (2^K units) by window and on each 2^mloc-unit point
+segment separately (the two blocks commute: Kronecker factors); the inverse runs the inverted low block on its
+segment BEFORE the rest.  The schedule is
 executed here with plain sweeps (the kernel's sm_sweep, restated) over the planner's op list (cvt_ops,
 restated) and compared with the oracle's Alg. 3 BasisCvt / iBasisCvt on random data, segment by segment
 (so a wrong op list, sweep or reordering fails against the oracle, not against itself)."""
@@ -38,30 +39,21 @@ def sweep(s, off, mm, lg, K, A):
             s[b + u: b + h] ^= s[b + u + d: b + h + d]
 
 
-def seg_info(mm, m, QB):
-    """(mode, ntop, nlow) as gf2x.cu's seg_cvt."""
-    if mm <= m - QB:
-        return 2, 0, 0
+def split_info(mm, m, QB):
+    """(split, ntop, nlow, K) as gf2x.cu's seg_cvt."""
     K = 1
     while 2 * K <= mm - 1:
         K *= 2
-    if K > m - QB:
-        return 0, 0, 0
-    return 1, mm - K, len(cvt_ops(K))
+    if mm <= 2 or K > m - QB:
+        return 0, 0, 0, 0
+    return 1, mm - K, len(cvt_ops(K)), K
 
 
-def fwd_schedule(ops, mode, ntop, nlow):
-    """sm_conv_op: step -> (op index, local)."""
-    if mode != 1:
-        return [(i, mode == 2) for i in range(len(ops))]
-    nhigh = len(ops) - ntop - nlow
-    order = [(i, False) for i in range(ntop)] + [(ntop + nlow + i, False) for i in range(nhigh)]
-    return order + [(ntop + i, True) for i in range(nlow)]
-
-
-@pytest.mark.parametrize("m,QB", [(11, 2), (10, 2), (11, 1), (9, 1), (8, 1), (9, 2), (7, 1)])
+@pytest.mark.parametrize("m,QB", [(11, 2), (10, 2), (11, 1), (9, 1), (8, 1), (9, 2), (7, 1), (11, 0), (9, 0), (6, 0)])
 @pytest.mark.parametrize("mm_off", [0, 1, 2])
 def test_forward_segments_match_oracle(m, QB, mm_off):
+    """Every CTA q: CTA-wide steps (top run, then high block; all ops if not split) on the whole operand unless
+    its segment lies past it, then the low block window by window on its segment's part of the operand."""
     mm = m - mm_off   # operand of 2^mm words zero-extended to 2^m
     N, mloc = 1 << m, m - QB
     f = np.zeros(N, np.uint64)
@@ -69,45 +61,50 @@ def test_forward_segments_match_oracle(m, QB, mm_off):
     want = np.zeros(N, np.uint64)
     want[: 1 << mm] = O.basis_cvt(f[: 1 << mm])
     ops = cvt_ops(mm)
-    mode, ntop, nlow = seg_info(mm, m, QB)
-    for q in range(1 << QB):   # every CTA's view: its own segment must come out right
+    split, ntop, nlow, K = split_info(mm, m, QB)
+    cta_ops = list(range(ntop)) + list(range(ntop + nlow, len(ops))) if split else list(range(len(ops)))
+    for q in range(1 << QB):
         s = f.copy()
         sbase = q << mloc
-        for oi, local in fwd_schedule(ops, mode, ntop, nlow):
-            lg, K = ops[oi]
-            for A in (True, False):
-                if not local:
-                    sweep(s, 0, mm, lg, K, A)
-                elif mode == 2:
-                    if q == 0:
-                        sweep(s, 0, mm, lg, K, A)
-                elif (sbase >> mm) == 0:
-                    sweep(s, sbase, mloc, lg, K, A)
-        assert np.array_equal(s[sbase: sbase + (1 << mloc)], want[sbase: sbase + (1 << mloc)]), (q, mode)
+        if sbase < (1 << mm):
+            for oi in cta_ops:
+                lg, Kop = ops[oi]
+                for A in (True, False):
+                    sweep(s, 0, mm, lg, Kop, A)
+            if split:
+                lo = sbase
+                hi = min(lo + (1 << mloc), 1 << mm)
+                for w in range(lo, hi, 1 << K):
+                    for oi in range(ntop, ntop + nlow):
+                        lg, Kop = ops[oi]
+                        for A in (True, False):
+                            sweep(s, w, K, lg, Kop, A)
+        assert np.array_equal(s[sbase: sbase + (1 << mloc)], want[sbase: sbase + (1 << mloc)]), (q, split)
 
 
-@pytest.mark.parametrize("m,QB", [(11, 2), (10, 2), (11, 1), (9, 1), (8, 1), (9, 2)])
+@pytest.mark.parametrize("m,QB", [(11, 2), (10, 2), (11, 1), (9, 1), (8, 1), (9, 2), (11, 0), (7, 0)])
 def test_inverse_segments_match_oracle(m, QB):
     N, mloc = 1 << m, m - QB
     g = splitmix64(77 + m, N)
     want = O.ibasis_cvt(g)
     ops = cvt_ops(m)
-    mode, ntop, nlow = seg_info(m, m, QB)
-    # every CTA inverts the low block on its own segment, then the array is gathered
+    mode, ntop, nlow, K = split_info(m, m, QB)
+    # every CTA inverts the low block window by window on its own segment, then the array is gathered
     s = g.copy()
     if mode == 1:
         for q in range(1 << QB):
-            for oi in range(ntop + nlow - 1, ntop - 1, -1):
-                lg, K = ops[oi]
-                for A in (False, True):
-                    sweep(s, q << mloc, mloc, lg, K, A)
+            for w in range(q << mloc, (q + 1) << mloc, 1 << K):
+                for oi in range(ntop + nlow - 1, ntop - 1, -1):
+                    lg, Kop = ops[oi]
+                    for A in (False, True):
+                        sweep(s, w, K, lg, Kop, A)
         nhigh = len(ops) - ntop - nlow
         rest = [len(ops) - 1 - i for i in range(nhigh)] + [ntop - 1 - i for i in range(ntop)]
     else:
         rest = list(range(len(ops) - 1, -1, -1))
     for oi in rest:
-        lg, K = ops[oi]
+        lg, Kop = ops[oi]
         for A in (False, True):
-            sweep(s, 0, m, lg, K, A)
+            sweep(s, 0, m, lg, Kop, A)
     assert np.array_equal(s, want), mode
 

@@ -17,6 +17,7 @@ VARIANTS = {
     "cl16_noseg": {"GF2X_SMALL_CL": "16", "GF2X_SMALL_NO_SEGCVT": "1"},
     "cl16_nokt": {"GF2X_SMALL_CL": "16", "GF2X_SMALL_NO_KT": "1"},
     "cl8_noseg": {"GF2X_SMALL_CL": "8", "GF2X_SMALL_NO_SEGCVT": "1"},
+    "cl16_ktbuild": {"GF2X_SMALL_CL": "16", "GF2X_SMALL_KT_BUILD": "1"},
 }
 KNOBS = sorted({k for v in VARIANTS.values() for k in v})
 bits = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 16
@@ -26,6 +27,7 @@ if batch == 1:
 else:
     a, b = batch_pair(bits, batch)
     VARIANTS = {"batch_small": {"GF2X_SMALL_BATCH": "1"}, "batch_small_nokt": {"GF2X_SMALL_BATCH": "1", "GF2X_SMALL_NO_KT": "1"},
+                "batch_small_ktbuild": {"GF2X_SMALL_BATCH": "1", "GF2X_SMALL_KT_BUILD": "1"},
                 "multipass": {}}
     KNOBS = sorted({k for v in VARIANTS.values() for k in v})
 da = torch.from_numpy(a.reshape(-1).view(np.int64)).cuda().view(torch.uint64)
