@@ -68,8 +68,8 @@ __host__ __device__ inline SmallLayout small_layout(int m, int CL, bool kt = fal
     L.ptab = L.bl + LPC * N;             // psi: CL = 1: uint4 M4R-8 (8 x 256 x 4 words); CL = 4: my limb (8 x 256)
     L.itab = L.ptab + (CL == 1 ? 8 * 256 * 4 : 8 * 256);   // psi^-1: M4R-4 word-planar [4 limbs][32 nibbles][16]
     L.pl = L.itab + 4 * 32 * 16;         // planes of A, B: [operand 2][limb 4][GC][33]
-    L.pr = L.pl + 2 * 4 * GC * 33;       // the nine products: [GC][9][33]
-    L.kd = L.pr + GC * 9 * 33;           // FFT constant deltas KD[layer < 9][2][16]
+    L.pr = L.pl + 2 * 4 * GC * 33;       // the nine products P and v31 P, v31^2 P: [GC][9][3][33]
+    L.kd = L.pr + GC * 27 * 33;          // FFT constant deltas KD[layer < 9][2][16]
     L.kt = (L.kd + 9 * 2 * 16 + 3) & ~3u;   // (kt) the segment's FFT constants (16-byte aligned)
     const int mloc = m - small_qb(CL);
     L.total = L.kt + (kt ? kt_off(m, mloc, mloc) : 0u);
@@ -160,21 +160,86 @@ __device__ __forceinline__ void sm_sweep(T* s, int mm, int lg, int K, bool A, in
     }
 }
 
+// Alg. 2 step (LG, K) on 16 units held in registers (compile-time indices): sweeps A / B as sm_sweep
+template <typename T, int LG, int K, bool A>
+__device__ __forceinline__ void reg_sweep16(T* v) {
+    constexpr int h = 1 << (LG - 1), u = h >> K, d = h - u, nseg = 1 << (4 - LG);
+#pragma unroll
+    for (int sg = 0; sg < nseg; sg++) {
+        if (A) {
+#pragma unroll
+            for (int j = 0; j < u; j++) v[sg * 2 * h + h + j] ^= v[sg * 2 * h + h + j + d];
+        } else {
+#pragma unroll
+            for (int j = u; j < h; j++) v[sg * 2 * h + j] ^= v[sg * 2 * h + j + d];
+        }
+    }
+}
+template <typename T, int LG, int K, bool INV>
+__device__ __forceinline__ void reg_step16(T* v) {
+    reg_sweep16<T, LG, K, !INV>(v);
+    reg_sweep16<T, LG, K, INV>(v);
+}
+// BasisCvt of 16 units in registers: cvt_ops(4) = (4,2) (3,2) (2,1) (4,1); INV: its inverse
+template <typename T, bool INV>
+__device__ __forceinline__ void cvt16_regs(T* v) {
+    if (!INV) {
+        reg_step16<T, 4, 2, false>(v); reg_step16<T, 3, 2, false>(v); reg_step16<T, 2, 1, false>(v); reg_step16<T, 4, 1, false>(v);
+    } else {
+        reg_step16<T, 4, 1, true>(v); reg_step16<T, 2, 1, true>(v); reg_step16<T, 3, 2, true>(v); reg_step16<T, 4, 2, true>(v);
+    }
+}
+// cvt16_regs on the 16 units w[off + i * str], i < 16
+template <typename T, bool INV>
+__device__ __forceinline__ void cvt16_pass(T* w, uint32_t off, uint32_t str) {
+    T v[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) v[i] = w[off + i * str];
+    cvt16_regs<T, INV>(v);
+#pragma unroll
+    for (int i = 0; i < 16; i++) w[off + i * str] = v[i];
+}
+
 // the low block (ops [ntop, ntop + nlow)) of a split list on the windows of 2^kw units in [lo, hi), a warp per
-// window; INV: the inverted ops in reverse order
+// window; INV: the inverted ops in reverse order.  Windows of 16 units (kw = 4: the block is cvt_ops(4)) run
+// as one register pass per window; windows of 256 (kw = 8: cvt_ops(8) = [the 4 steps of levels 8..5]
+// [cvt_ops(4) on bits 0..3][cvt_ops(4) on bits 4..7], the last two commuting Kronecker factors) as 4 swept
+// steps and two register passes (16 units contiguous, then 16 units at stride 16)
 template <typename T, bool INV>
 __device__ __forceinline__ void sm_low_block(T* S, uint32_t lo, uint32_t hi, int kw, const CvtOp* ops, int ntop,
                                              int nlow, uint32_t nitems_before, uint32_t stride) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t nwin = hi > lo ? (hi - lo) >> kw : 0;
+    if (kw == 4) {   // a thread per 16-unit window (items counted in warps of 32 windows)
+        const uint32_t nw32 = (nwin + 31) >> 5;
+        for (uint32_t it = warp; it < nitems_before + nw32; it += stride) {
+            if (it < nitems_before) continue;
+            const uint32_t win = ((it - nitems_before) << 5) + lane;
+            if (win < nwin) cvt16_pass<T, INV>(S + lo + (win << 4), 0, 1);
+        }
+        return;
+    }
     for (uint32_t it = warp; it < nitems_before + nwin; it += stride) {
         if (it < nitems_before) continue;
         T* w = S + lo + ((it - nitems_before) << kw);
-        for (int j = 0; j < nlow; j++) {
-            const CvtOp op = ops[ntop + (INV ? nlow - 1 - j : j)];
+        const int nsw = kw == 8 ? 4 : nlow;   // swept steps (kw = 8: the top run of cvt_ops(8))
+        if (kw == 8 && INV) {
+            if (lane < 16) cvt16_pass<T, true>(w, lane, 16);
+            __syncwarp();
+            if (lane < 16) cvt16_pass<T, true>(w, lane << 4, 1);
+            __syncwarp();
+        }
+        for (int j = 0; j < nsw; j++) {
+            const CvtOp op = ops[ntop + (INV ? nsw - 1 - j : j)];
             sm_sweep<T>(w, kw, op.lg, op.K, !INV, lane, 32);
             __syncwarp();
             sm_sweep<T>(w, kw, op.lg, op.K, INV, lane, 32);
+            __syncwarp();
+        }
+        if (kw == 8 && !INV) {
+            if (lane < 16) cvt16_pass<T, false>(w, lane << 4, 1);
+            __syncwarp();
+            if (lane < 16) cvt16_pass<T, false>(w, lane, 16);
             __syncwarp();
         }
     }
@@ -269,7 +334,7 @@ __device__ __forceinline__ void sm_layer(uint32_t* A, uint32_t* B, int nops, int
     }
 }
 // layers [0, mloc) on the segment [base, base + 2^mloc) (mloc = m, base = 0: the whole transform), its data
-// stored at base + dsh
+// stored at base + dsh (radix-4 layer pairs with one barrier each measured slower: 39.2 against 32.8 us at c1)
 template <bool INV>
 __device__ __forceinline__ void sm_fft(uint32_t* A, uint32_t* B, int nops, int m, int LPC, uint32_t N, const uint32_t* KD,
                                        int mloc, uint32_t base, const uint32_t* KT, int dsh) {
@@ -478,7 +543,8 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
                 const uint32_t lo = QB ? sbase : 0u, hi = min(lo + seg, ext);
                 sm_low_block<uint64_t, false>(x ? SB : SA, lo, hi, p.kw[x], x ? p.ops_b : p.ops_a, p.ntop[x], p.nlow[x],
                                               before, nthr >> 5);
-                before += hi > lo ? (hi - lo) >> p.kw[x] : 0;
+                const uint32_t nw = hi > lo ? (hi - lo) >> p.kw[x] : 0;
+                before += p.kw[x] == 4 ? (nw + 31) >> 5 : nw;   // (sm_low_block's work items)
             }
             __syncthreads();
         }
@@ -536,38 +602,37 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
                     for (int j = 0; j < 32; j++) { x[j] ^= pa[j]; y[j] ^= pb[j]; }
                 }
             bs_mul32(x, y, r);
-            uint32_t* d = PR + (g * 9 + qq) * 33;
+            uint32_t* d = PR + (g * 9 + qq) * 3 * 33;
 #pragma unroll
             for (int j = 0; j < 32; j++) d[j] = r[j];
+            // the product scaled by the Karatsuba constants where a result limb takes it so (combine below)
+            if (c_pm_terms[qq][2]) {
+                bs_mul_v31(r, x);
+#pragma unroll
+                for (int j = 0; j < 32; j++) d[33 + j] = x[j];
+            }
+            if (c_pm_terms[qq][3]) {
+                bs_mul_v31sq(r, x);
+#pragma unroll
+                for (int j = 0; j < 32; j++) d[66 + j] = x[j];
+            }
         }
         __syncthreads();
         SM_T(8);
-        for (uint32_t it = tid; it < GC * 4; it += nthr) {   // (group, result limb): R_L = sum of its terms
+        // (group, result limb): R_L = sum of its terms P, v31 P, v31^2 P (c_pm_terms), a warp per item with lane j
+        // on plane j, then a warp transpose back to elements
+        for (uint32_t it = warp; it < GC * 4; it += nwarp) {
             const uint32_t g = it >> 2, L = it & 3;
-            uint32_t acc[32], s1[32], s2[32], t[32];
+            uint32_t acc = 0;
 #pragma unroll
-            for (int j = 0; j < 32; j++) { acc[j] = 0; s1[j] = 0; s2[j] = 0; }
-#pragma unroll 1
             for (int t9 = 0; t9 < 9; t9++) {
-                const uint32_t* src = PR + (g * 9 + t9) * 33;
-                const bool r0 = (c_pm_terms[t9][1] >> L) & 1, r1 = (c_pm_terms[t9][2] >> L) & 1, r2 = (c_pm_terms[t9][3] >> L) & 1;
-                if (r0) { for (int j = 0; j < 32; j++) acc[j] ^= src[j]; }
-                if (r1) { for (int j = 0; j < 32; j++) s1[j] ^= src[j]; }
-                if (r2) { for (int j = 0; j < 32; j++) s2[j] ^= src[j]; }
+                const uint32_t* src = PR + (g * 9 + t9) * 3 * 33 + lane;
+                if ((c_pm_terms[t9][1] >> L) & 1) acc ^= src[0];
+                if ((c_pm_terms[t9][2] >> L) & 1) acc ^= src[33];
+                if ((c_pm_terms[t9][3] >> L) & 1) acc ^= src[66];
             }
-            bs_mul_v31(s1, t);
-#pragma unroll
-            for (int j = 0; j < 32; j++) acc[j] ^= t[j];
-            bs_mul_v31sq(s2, t);
-            uint32_t* sc = PL + it * 33;   // (the operand planes are dead: the products have read them)
-#pragma unroll
-            for (int j = 0; j < 32; j++) sc[j] = acc[j] ^ t[j];
-        }
-        __syncthreads();
-        for (uint32_t it = warp; it < GC * 4; it += nwarp) {   // back to elements: a warp transpose per item
-            const uint32_t g = it >> 2, L = it & 3;
             uint32_t* dst = sm_limb<CL>(AL, L, q, N) + (int)((g0 + g) << 5) + dsh;
-            dst[lane] = warp_transpose32(PL[it * 33 + lane], lane);
+            dst[lane] = warp_transpose32(acc, lane);
         }
         sm_sync<CL>();   // every result limb delivered
         SM_T(9);
@@ -582,7 +647,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small(SmallParams p) {
         if (p.split[2]) {   // the inverted low block, window by window on my segment (every limb I hold)
             for (uint32_t l = 0; l < LPC; l++)
                 sm_low_block<uint32_t, true>(AL + l * N, sbase, sbase + seg, p.kw[2], p.ops_i, p.ntop[2], p.nlow[2],
-                                             l * (seg >> p.kw[2]), nthr >> 5);
+                                             l * (p.kw[2] == 4 ? ((seg >> 4) + 31) >> 5 : seg >> p.kw[2]), nthr >> 5);
             __syncthreads();
         }
         if constexpr (QB > 0) {
