@@ -57,6 +57,48 @@ struct ChunkSweeps {
     uint8_t lg[BITCHUNK_MAXSW];
     int n, cw;                        // sweeps; words per chunk (2^(C-6))
 };
+// sweeps [k0, k1) of a chunk held in shared memory (a barrier after each sweep or in-word run)
+__device__ __forceinline__ void chunk_sweeps(uint64_t* T, uint32_t cw, const ChunkSweeps& sw, int k0, int k1) {
+    for (int k = k0; k < k1; k++) {
+        const int lg = sw.lg[k];
+        const uint32_t d = sw.d[k];
+        if (lg <= 6) {
+            // a run of consecutive in-word sweeps: each thread applies all of them to its own words in
+            // registers (no word is read by another thread), with one barrier after the run
+            int kr = k + 1;
+            while (kr < k1 && sw.lg[kr] <= 6) kr++;
+            for (uint32_t w = threadIdx.x; w < cw; w += blockDim.x) {
+                uint64_t x = T[w];
+                for (int q = k; q < kr; q++) x ^= (x >> sw.d[q]) & sw.pmask[q];
+                T[w] = x;
+            }
+            k = kr - 1;
+        } else {
+            const uint32_t tlo = sw.tlo[k], thi = sw.thi[k], len = 1u << lg, wps = len >> 6, tw0 = tlo >> 6;
+            const uint32_t ntw = ((thi + 63) >> 6) - tw0, total = (cw / wps) * ntw;
+            uint64_t nv[4];
+            uint32_t nwd[4];
+            int cnt = 0;
+            // read phase (all sources first: a target word may be another thread's source word)
+            for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
+                const uint32_t seg = t / ntw, w = seg * wps + tw0 + (t - seg * ntw);
+                const uint32_t o = (w << 6) & (len - 1);
+                const uint32_t lo = tlo > o ? tlo - o : 0, hi = thi < o + 64 ? thi - o : 64;
+                if (lo >= hi) continue;
+                const uint64_t mask = (hi >= 64 ? ~0ull : ((1ull << hi) - 1)) & ~((1ull << lo) - 1);
+                const uint32_t sp = (w << 6) + d, w0 = sp >> 6, sh = sp & 63;
+                uint64_t src = T[w0] >> sh;
+                if (sh && w0 + 1 < cw) src |= T[w0 + 1] << (64 - sh);
+                nv[cnt] = T[w] ^ (src & mask);
+                nwd[cnt++] = w;
+            }
+            __syncthreads();
+            for (int q = 0; q < cnt; q++) T[nwd[q]] = nv[q];
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void __launch_bounds__(256) k_bitcvt_chunk(uint64_t* __restrict__ G, uint64_t nchunks, ChunkSweeps sw) {
     __shared__ uint64_t T[1024];
     const uint32_t cw = (uint32_t)sw.cw;
@@ -65,45 +107,86 @@ __global__ void __launch_bounds__(256) k_bitcvt_chunk(uint64_t* __restrict__ G, 
         __syncthreads();
         for (uint32_t w = threadIdx.x; w < cw; w += blockDim.x) T[w] = g[w];
         __syncthreads();
-        for (int k = 0; k < sw.n; k++) {
-            const int lg = sw.lg[k];
-            const uint32_t d = sw.d[k];
-            if (lg <= 6) {
-                // a run of consecutive in-word sweeps: each thread applies all of them to its own words in
-                // registers (no word is read by another thread), with one barrier after the run
-                int k1 = k + 1;
-                while (k1 < sw.n && sw.lg[k1] <= 6) k1++;
-                for (uint32_t w = threadIdx.x; w < cw; w += blockDim.x) {
-                    uint64_t x = T[w];
-                    for (int q = k; q < k1; q++) x ^= (x >> sw.d[q]) & sw.pmask[q];
-                    T[w] = x;
-                }
-                k = k1 - 1;
-            } else {
-                const uint32_t tlo = sw.tlo[k], thi = sw.thi[k], len = 1u << lg, wps = len >> 6, tw0 = tlo >> 6;
-                const uint32_t ntw = ((thi + 63) >> 6) - tw0, total = (cw / wps) * ntw;
-                uint64_t nv[4];
-                uint32_t nwd[4];
-                int cnt = 0;
-                // read phase (all sources first: a target word may be another thread's source word)
-                for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
-                    const uint32_t seg = t / ntw, w = seg * wps + tw0 + (t - seg * ntw);
-                    const uint32_t o = (w << 6) & (len - 1);
-                    const uint32_t lo = tlo > o ? tlo - o : 0, hi = thi < o + 64 ? thi - o : 64;
-                    if (lo >= hi) continue;
-                    const uint64_t mask = (hi >= 64 ? ~0ull : ((1ull << hi) - 1)) & ~((1ull << lo) - 1);
-                    const uint32_t sp = (w << 6) + d, w0 = sp >> 6, sh = sp & 63;
-                    uint64_t src = T[w0] >> sh;
-                    if (sh && w0 + 1 < cw) src |= T[w0 + 1] << (64 - sh);
-                    nv[cnt] = T[w] ^ (src & mask);
-                    nwd[cnt++] = w;
-                }
-                __syncthreads();
-                for (int q = 0; q < cnt; q++) T[nwd[q]] = nv[q];
+        chunk_sweeps(T, cw, sw, 0, sw.n);
+        for (uint32_t w = threadIdx.x; w < cw; w += blockDim.x) g[w] = T[w];
+    }
+}
+
+// ---- 2^16-bit chunks (C = 16, the c4a / c4b case) with their inner blocks in registers.  bit_ops(16) =
+// [levels 16..9, K = 8][bit_ops(8, 8): levels 16..13 (K = 4), then bit_ops(4, 12), bit_ops(4, 8)]
+// [bit_ops(8, 0)].  bit_ops(4, 12) and bit_ops(4, 8) are the 16-unit network of cvt_ops(4) (cvt16_regs,
+// small.cuh: the same steps, its last two in the other order -- they act on disjoint index bits and commute,
+// R26) on 16 words at stride 64 and at stride 4; bit_ops(8, 0) acts inside every 256-bit window (4 words): one
+// thread applies its 12 steps to a window as 256-bit shift-mask-XOR operations with compile-time constants.
+// The top run and levels 16..13 stay shared-memory sweeps (ChunkSweeps, 24 of them).
+constexpr uint64_t bw_mask(int lg, int K, bool A, int wi) {   // word wi of the step's target mask in 256 bits
+    uint64_t m = 0;
+    for (int b = 0; b < 64; b++) {
+        const int t = (wi * 64 + b) & ((1 << lg) - 1), h = 1 << (lg - 1), u = h >> K;
+        if (A ? (t >= h && t < h + u) : (t >= u && t < h)) m |= 1ull << b;
+    }
+    return m;
+}
+template <int LG, int K, bool A>
+__device__ __forceinline__ void bw_sweep(uint64_t* x) {   // x ^= (x >> d) & mask on 256 bits
+    constexpr int d = (1 << (LG - 1)) - ((1 << (LG - 1)) >> K), q = d >> 6, r = d & 63;
+    uint64_t y[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        uint64_t v = i + q < 4 ? x[i + q] >> r : 0ull;
+        if (r && i + q + 1 < 4) v |= x[i + q + 1] << (64 - r);
+        y[i] = v;
+    }
+    x[0] ^= y[0] & bw_mask(LG, K, A, 0);
+    x[1] ^= y[1] & bw_mask(LG, K, A, 1);
+    x[2] ^= y[2] & bw_mask(LG, K, A, 2);
+    x[3] ^= y[3] & bw_mask(LG, K, A, 3);
+}
+template <int LG, int K, bool INV>
+__device__ __forceinline__ void bw_step(uint64_t* x) {
+    bw_sweep<LG, K, !INV>(x);
+    bw_sweep<LG, K, INV>(x);
+}
+// bit_ops(8, 0) in the paper's order: (8,4) (7,4) (6,4) (5,4) (8,2) (7,2) (8,1) (6,1) (4,2) (3,2) (4,1) (2,1)
+template <bool INV>
+__device__ __forceinline__ void bw_cvt256(uint64_t* x) {
+    if (!INV) {
+        bw_step<8, 4, false>(x); bw_step<7, 4, false>(x); bw_step<6, 4, false>(x); bw_step<5, 4, false>(x);
+        bw_step<8, 2, false>(x); bw_step<7, 2, false>(x); bw_step<8, 1, false>(x); bw_step<6, 1, false>(x);
+        bw_step<4, 2, false>(x); bw_step<3, 2, false>(x); bw_step<4, 1, false>(x); bw_step<2, 1, false>(x);
+    } else {
+        bw_step<2, 1, true>(x); bw_step<4, 1, true>(x); bw_step<3, 2, true>(x); bw_step<4, 2, true>(x);
+        bw_step<6, 1, true>(x); bw_step<8, 1, true>(x); bw_step<7, 2, true>(x); bw_step<8, 2, true>(x);
+        bw_step<5, 4, true>(x); bw_step<6, 4, true>(x); bw_step<7, 4, true>(x); bw_step<8, 4, true>(x);
+    }
+}
+template <bool INV>
+__global__ void __launch_bounds__(256) k_bitcvt_chunk16(uint64_t* __restrict__ G, uint64_t nchunks, ChunkSweeps sw) {
+    __shared__ uint64_t T[1024];
+    const uint32_t tid = threadIdx.x;
+    for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        uint64_t* g = G + ch * 1024;
+        __syncthreads();
+        for (uint32_t w = tid; w < 1024; w += blockDim.x) T[w] = g[w];
+        __syncthreads();
+        if (!INV) chunk_sweeps(T, 1024, sw, 0, sw.n);   // levels 16..9 and 16..13
+        for (int ph = 0; ph < 3; ph++) {
+            // forward: bit_ops(4, 12), bit_ops(4, 8), bit_ops(8, 0); inverse: the reverse
+            const int f = INV ? 2 - ph : ph;
+            if (f == 0) { if (tid < 64) cvt16_pass<uint64_t, INV>(T, tid, 64); }
+            else if (f == 1) { if (tid < 64) cvt16_pass<uint64_t, INV>(T, (tid >> 2) * 64 + (tid & 3), 4); }
+            else {
+                uint64_t x[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) x[i] = T[tid * 4 + i];
+                bw_cvt256<INV>(x);
+#pragma unroll
+                for (int i = 0; i < 4; i++) T[tid * 4 + i] = x[i];
             }
             __syncthreads();
         }
-        for (uint32_t w = threadIdx.x; w < cw; w += blockDim.x) g[w] = T[w];
+        if (INV) chunk_sweeps(T, 1024, sw, 0, sw.n);
+        for (uint32_t w = tid; w < 1024; w += blockDim.x) g[w] = T[w];
     }
 }
 
@@ -151,6 +234,22 @@ static gf2x_status run_bitcvt(uint64_t* G, int M, bool inverse, int smc, cudaStr
     auto run_chunks = [&]() -> gf2x_status {
         std::vector<CvtOp> inner;
         bit_ops(C, 0, inner);
+        // C = 16: only the top run and levels 16..13 as sweeps, the rest in registers (k_bitcvt_chunk16); the
+        // kernel's fixed inner lists are checked against bit_ops here
+        const bool c16 = C == 16 && !env_flag_now("GF2X_BITCVT_NOREG");
+        if (c16) {
+            std::vector<CvtOp> hi, lo, want;
+            bit_ops(4, 12, hi);
+            bit_ops(4, 8, hi);
+            bit_ops(8, 0, lo);
+            const int ref[12][2] = {{8, 4}, {7, 4}, {6, 4}, {5, 4}, {8, 2}, {7, 2}, {8, 1}, {6, 1}, {4, 2}, {3, 2}, {4, 1}, {2, 1}};
+            bool ok = inner.size() == 12 + hi.size() + lo.size() && lo.size() == 12;
+            for (size_t i = 0; ok && i < hi.size(); i++)
+                ok = inner[12 + i].lg == hi[i].lg && inner[12 + i].K == hi[i].K && hi[i].K <= 2;
+            for (int i = 0; ok && i < 12; i++) ok = lo[i].lg == ref[i][0] && lo[i].K == ref[i][1] && inner[12 + hi.size() + i].lg == lo[i].lg;
+            if (!ok) return fail(GF2X_EINVAL, "bit-level chunk: unexpected inner op list");
+            inner.resize(12);   // levels 16..9 (K = 8) and 16..13 (K = 4)
+        }
         if (inverse) std::reverse(inner.begin(), inner.end());
         ChunkSweeps cs;
         cs.n = 0;
@@ -161,7 +260,9 @@ static gf2x_status run_bitcvt(uint64_t* G, int M, bool inverse, int smc, cudaStr
         }
         const uint64_t nchunks = (1ull << (M - 6)) >> (C - 6);
         ProfScope ps("k_bitcvt_chunk", 16.0 * (double)(1ull << (M - 6)), st);
-        k_bitcvt_chunk<<<grid_for(nchunks, 1, smc, 8), 256, 0, st>>>(G, nchunks, cs);
+        if (c16 && inverse) k_bitcvt_chunk16<true><<<grid_for(nchunks, 1, smc, 8), 256, 0, st>>>(G, nchunks, cs);
+        else if (c16) k_bitcvt_chunk16<false><<<grid_for(nchunks, 1, smc, 8), 256, 0, st>>>(G, nchunks, cs);
+        else k_bitcvt_chunk<<<grid_for(nchunks, 1, smc, 8), 256, 0, st>>>(G, nchunks, cs);
         return check_launch("bit-level chunk");
     };
     gf2x_status s0;

@@ -146,10 +146,11 @@ np.save(sys.argv[2], d.cpu().view(torch.int64).numpy())
 """
 
 
-@pytest.mark.parametrize("env", ["GF2X_BITCVT_SWEEPS", "GF2X_BITCVT_NOCHUNK"])
+@pytest.mark.parametrize("env", ["GF2X_BITCVT_SWEEPS", "GF2X_BITCVT_NOCHUNK", "GF2X_BITCVT_NOREG"])
 @pytest.mark.parametrize("M", [9, 20])
 def test_bit_basis_cvt_sweeps_only_variant(M, env, tmp_path):
-    # GF2X_BITCVT_SWEEPS=1: no word-level passes; GF2X_BITCVT_NOCHUNK=1: no shared-memory chunk pass; same result
+    # GF2X_BITCVT_SWEEPS=1: no word-level passes; GF2X_BITCVT_NOCHUNK=1: no shared-memory chunk pass;
+    # GF2X_BITCVT_NOREG=1: 2^16-bit chunks with every step swept (no register passes); same result
     import os
     import subprocess
     import sys
