@@ -1434,13 +1434,16 @@ static int small_cluster(const Plan& P) {
 // (ktw words each, 16-byte multiples): K_b = c v_b for each local layer and block, c = s_k(block base) the XOR
 // of S[k][j] over the base's bits (layer_const), computed on the host once per device and (m, QB) like the
 // App. C constants (frob.cuh); the kernel copies its segment's table with cp.async instead of building it.
-static gf2x_status get_small_kt(DeviceState* ds, int m, int QB, const uint32_t** out, uint32_t* ktw) {
+// (*out = nullptr when the table is not built yet and `build` is false: the kernel then builds its own)
+static gf2x_status get_small_kt(DeviceState* ds, int m, int QB, bool build, const uint32_t** out, uint32_t* ktw) {
     const int mloc = m - QB;
     *ktw = (kt_off(m, mloc, mloc) + 3) & ~3u;
     std::lock_guard<std::mutex> lk(g_mu);
     const int key = m * 4 + QB;
     auto it = ds->small_kt.find(key);
     if (it != ds->small_kt.end()) { *out = it->second; return GF2X_OK; }
+    *out = nullptr;
+    if (!build) return GF2X_OK;
     const uint32_t seg = 1u << mloc, QC = 1u << QB;
     std::vector<uint32_t> h((size_t)QC * *ktw, 0u);
     for (uint32_t q = 0; q < QC; q++)
@@ -1530,7 +1533,10 @@ static gf2x_status run_small(const uint64_t* a, uint64_t a_bits, const uint64_t*
     sp.ktg = nullptr;
     sp.ktw = 0;
     if (sp.kt && !env_flag_now("GF2X_SMALL_KT_BUILD")) {   // (GF2X_SMALL_KT_BUILD=1: every CTA builds its table)
-        gf2x_status ks = get_small_kt(ds, P.m, small_qb(CL), &sp.ktg, &sp.ktw);
+        // (no allocation or copy while the stream is being captured into a graph: the kernel builds its table)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(st, &cs);
+        gf2x_status ks = get_small_kt(ds, P.m, small_qb(CL), cs == cudaStreamCaptureStatusNone, &sp.ktg, &sp.ktw);
         if (ks != GF2X_OK) return ks;
     }
     const size_t sm = (size_t)small_layout(P.m, CL, sp.kt != 0).total * 4;

@@ -79,3 +79,23 @@ def test_capture_replay_batched_and_w128():
     for i in range(0, count, 7):
         assert np.array_equal(C[i], O.mul_karatsuba(A2[i], B2[i])), i
     assert np.array_equal(host(dw)[0], O.mul_karatsuba(a2, b2))
+
+
+@pytest.mark.parametrize("ab,bb", [(20000, 20001), (5000, 3000)])
+def test_capture_small_product_without_warmup(ab, bb):
+    """A fused small product (k_small) captured on its very first call: the per-device constant table is not
+    allocated during a capture (the kernel then builds its own), so the capture works either way."""
+    s = torch.cuda.Stream()
+    da, db = dev(operand(ab, seed=3)), dev(operand(bb, seed=4))
+    dc = torch.empty(G.nwords(ab) + G.nwords(bb), dtype=torch.uint64, device="cuda")
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        G.gf2x_mul(da, ab, db, bb, dc, stream=s)
+    for seed in (21, 22):
+        a, b = operand(ab, seed=seed), operand(bb, seed=seed + 100)
+        da.copy_(dev(a))
+        db.copy_(dev(b))
+        with torch.cuda.stream(s):
+            g.replay()
+        assert np.array_equal(host(dc), brute_mul_words(a, b)), seed
