@@ -157,6 +157,14 @@ gf2x_status gf2x_comm_check(gf2x_comm_t comm);
  * canonical no-swizzle K-major values 128 / 1024).  Profiled as "k_ipsi_tc". */
 gf2x_status gf2x_experiment_ipsi_tc(const void* P, uint64_t n, void* out, uint32_t lbo, uint32_t sbo, void* stream);
 
+/* Measured experiment, not the product path: the five innermost forward FFT_LCH layers
+ * (Alg. 1, layers k = 4 .. 0 of a 2^m-point transform, multipliers s_k(phi(b)) of the global block
+ * bases), in place on two device arrays A, B of 2^m TGF(2^128) elements (uint4, tower representation),
+ * 11 <= m <= 30.  variant 0: k_bottom's bit-sliced layers (the product path's formulation); variant 1: a
+ * warp-shuffle formulation (one element per lane, partner lane ^ 2^k).  Both give the same result.
+ * Stream-ordered; GF2X_EINVAL on bad arguments. */
+gf2x_status gf2x_experiment_fft_low(void* A, void* B, uint32_t m, int variant, void* stream);
+
 /* Host-mode communicator (no NCCL): the ranks' synchronisation goes through two caller-supplied HOST callbacks,
  * e.g. a torch.distributed gloo group.  `barrier(user)` returns when every rank has called it; `allgather(in,
  * out, bytes, user)` gathers `bytes` from every rank into out[rank * bytes].  Both return 0 on success.  All

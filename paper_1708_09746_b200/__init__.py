@@ -27,6 +27,7 @@ EXPORTS = [
     "gf2x_comm_peer_memory", "gf2x_mul_alg4", "gf2x_debug_stage_alg4", "gf2x_plan", "gf2x_basis_cvt_bits",
     "gf2x_mul_frob", "gf2x_comm_check", "gf2x_comm_wait", "gf2x_comm_abort", "gf2x_comm_init_host",
     "gf2x_experiment_ipsi_tc",
+    "gf2x_experiment_fft_low",
 ]
 
 
@@ -75,6 +76,9 @@ def load(path: str = LIB_PATH):
     L.gf2x_comm_init.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
     L.gf2x_comm_destroy.argtypes = [vp]
     L.gf2x_comm_peer_memory.argtypes = [vp]
+    if hasattr(L, "gf2x_experiment_fft_low"):
+        L.gf2x_experiment_fft_low.argtypes = [vp, vp, ctypes.c_uint32, i32, vp]
+        L.gf2x_experiment_fft_low.restype = i32
     if hasattr(L, "gf2x_experiment_ipsi_tc"):
         L.gf2x_experiment_ipsi_tc.argtypes = [vp, u64, vp, ctypes.c_uint32, ctypes.c_uint32, vp]
         L.gf2x_experiment_ipsi_tc.restype = i32
@@ -416,3 +420,9 @@ def profile_report():
 
 def version() -> str:
     return load().gf2x_version().decode()
+
+
+def experiment_fft_low(A, B, m: int, variant: int, stream=None):
+    """The five innermost forward FFT layers of a 2^m-point transform, in place on A and B ((2^m, 2) uint64
+    device tensors, tower elements): variant 0 bit-sliced (k_bottom), 1 warp-shuffle (DESIGN.md §7 experiment)."""
+    _check(load().gf2x_experiment_fft_low(_ptr(A), _ptr(B), m, variant, _stream_ptr(stream)))

@@ -1875,6 +1875,32 @@ gf2x_status gf2x_experiment_ipsi_tc(const void* P, uint64_t n, void* out, uint32
     return e == cudaSuccess ? GF2X_OK : fail(GF2X_ECUDA, std::string("ipsi tc launch: ") + cudaGetErrorString(e));
 }
 
+gf2x_status gf2x_experiment_fft_low(void* A, void* B, uint32_t m, int variant, void* stream) {
+    if (!A || !B || m < 11 || m > 30 || variant < 0 || variant > 1) return fail(GF2X_EINVAL, "fft_low experiment arguments");
+    int dev;
+    DeviceState* ds;
+    gf2x_status s = get_device(&dev, &ds);
+    if (s != GF2X_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint64_t n = 1ull << m;
+    if (variant == 0) {   // k_bottom's bit-sliced layers 4 .. 0 (forward only, both operands)
+        BottomParams bp;
+        bp.A = (uint4*)A; bp.B = (uint4*)B;
+        bp.total = n;
+        bp.ntiles = (n + (1ull << BT_BITS) - 1) >> BT_BITS;
+        bp.m = (int)m; bp.L = 5;
+        bp.map = IdxMap{0, 0, 0};
+        bp.mode = 1;
+        ProfScope ps("k_bottom<fwd, L=5>", 64.0 * n, st);
+        bottom_launch(bp, ds->sm_count, st);
+    } else {
+        ProfScope ps("k_fft_low_shfl", 64.0 * n, st);
+        k_fft_low_shfl<<<ds->sm_count * 4, SHFL_THREADS, 0, st>>>((uint4*)A, (uint4*)B, n);
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GF2X_OK : fail(GF2X_ECUDA, std::string("fft_low experiment: ") + cudaGetErrorString(e));
+}
+
 gf2x_status gf2x_comm_check(gf2x_comm_t comm) {
     if (!comm) return fail(GF2X_EINVAL, "null communicator");
     return comm_check(comm);

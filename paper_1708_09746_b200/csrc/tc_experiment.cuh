@@ -124,3 +124,53 @@ __global__ void __launch_bounds__(TC_THREADS, 4) k_ipsi_tc(const uint4* __restri
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
 }
+
+// ---------------------------------------------------------------------------------------------------------
+// Warp-shuffle formulation of the innermost forward FFT layers (k = 4 .. 0), a measured experiment (VERDICT
+// round 1 item 8 / DESIGN.md §7), against k_bottom's bit-sliced layers (`gf2x_experiment_fft_low`).
+// One TGF(2^128) element per lane (index bits [0, 5) = lane), so the layer-k partner is lane ^ 2^k (four
+// SHFL per butterfly side).  The multiplier s_k(phi(b)) of the pair's block base b splits by linearity into
+// C_hi = s_k(bits >= 5 of b) (warp-uniform: an M4R-4 table per warp and layer, 8 lookups per limb) and
+// c_lo = s_k(bits [k+1, 5) of b) < 2^(5-k) (lane-dependent: integer products on bytes, R25), the SURVEY's
+// "C_warp + c_lane" split.  Both lanes of a pair form x0 + c x1 (SIMT: the product is issued on both sides).
+#define SHFL_THREADS 256
+__global__ void __launch_bounds__(SHFL_THREADS) k_fft_low_shfl(uint4* __restrict__ A, uint4* __restrict__ B, uint64_t n) {
+    __shared__ __align__(16) uint32_t tabs[SHFL_THREADS / 32][128];   // one M4R-4 table per warp
+    __shared__ __align__(16) uint32_t KL[5][32][8];                    // c_lo v_b per layer and lane
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t i = threadIdx.x; i < 5 * 32; i += blockDim.x) {
+        const uint32_t k = i >> 5, l = i & 31;
+        uint32_t K[8];
+        sm_consts<8>(layer_const((int)k, (l >> (k + 1)) << (k + 1)), K);
+#pragma unroll
+        for (int b = 0; b < 8; b++) KL[k][l][b] = K[b];
+    }
+    __syncthreads();
+    const uint32_t tab_sa = (uint32_t)__cvta_generic_to_shared(tabs[warp]);
+    const uint64_t items = 2 * (n >> 5);
+    for (uint64_t it = blockIdx.x * (uint64_t)(SHFL_THREADS / 32) + warp; it < items; it += (uint64_t)gridDim.x * (SHFL_THREADS / 32)) {
+        uint4* X = it < (n >> 5) ? A : B;
+        const uint64_t i0 = (it % (n >> 5)) << 5;
+        uint4 x = X[i0 + lane];
+#pragma unroll 1
+        for (int k = 4; k >= 0; k--) {
+            __syncwarp();
+            if (lane < 8) build_tab_row(tabs[warp], layer_const(k, (uint32_t)i0), (int)lane, nullptr);
+            __syncwarp();
+            const uint32_t m = 1u << k;
+            const bool low = !(lane & m);
+            uint4 y;
+            y.x = __shfl_xor_sync(0xffffffffu, x.x, m); y.y = __shfl_xor_sync(0xffffffffu, x.y, m);
+            y.z = __shfl_xor_sync(0xffffffffu, x.z, m); y.w = __shfl_xor_sync(0xffffffffu, x.w, m);
+            const uint4 x1 = low ? y : x, x0 = low ? x : y;
+            const uint32_t* K = KL[k][lane];
+            uint4 x0n;
+            x0n.x = x0.x ^ m4r4_word_sa(tab_sa, x1.x) ^ smul<8>(x1.x, K);
+            x0n.y = x0.y ^ m4r4_word_sa(tab_sa, x1.y) ^ smul<8>(x1.y, K);
+            x0n.z = x0.z ^ m4r4_word_sa(tab_sa, x1.z) ^ smul<8>(x1.z, K);
+            x0n.w = x0.w ^ m4r4_word_sa(tab_sa, x1.w) ^ smul<8>(x1.w, K);
+            x = low ? x0n : make_uint4(x1.x ^ x0n.x, x1.y ^ x0n.y, x1.z ^ x0n.z, x1.w ^ x0n.w);
+        }
+        X[i0 + lane] = x;
+    }
+}
