@@ -257,6 +257,251 @@ __global__ void __launch_bounds__(RES_THREADS, 3) k_cvt_res(CvtResParams p) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// Seam pass (k_cvt_seam): a COMPLETE Taylor run (levels q .. K+1 of 2^q-unit chunks, Alg. 3 l.531 with
+// Alg. 2's steps) in its closed form, R27.  With M = 2^K - 1, B = q - K and the
+// residue classes c = 1 .. M (unit i = r M + c, row r; class M holds the units r M + M, i.e. the
+// nonzero multiples of M; unit 0 is never a target), the run maps class c's rows x to
+//     y[r] = XOR_{s superset of r} x[s]            for r <  c   (the superset-sum over the row bits)
+//     y[r] = XOR_{s superset of r-1} x[s+1]        for r >= c   (the same transform of the rows shifted by one)
+// (rows s run over 0 .. 2^B; a row beyond the chunk reads as 0).  For the classes c > 2^B of the top run
+// (all but the first 2^B) only the first line applies: that is k_cvt_top's "generic" case (R24).
+// Writing the class as (L = rows < c, U = rows >= c) and S = the superset-sum, the inverse run is
+//     x_U = T y_U (T = the shifted transform, an involution on U),  v = S(x_U on U, 0 on L),
+//     x_L = S(y_L on L, v on U) restricted to L                       (S_LL^-1 = S_LL, S_LL S_LU = S_LU S_UU).
+// Each S is separable over the row bits, so a tile (all 2^B + 1 rows of 32 / W consecutive classes, W 32-bit
+// words per unit: one 128-byte row, lane = word column) runs it in register phases of 4 row bits:
+// forward 2 phases (low bits of P = S x and Q = T x, then the high bits and the seam select), inverse 4.
+// Against k_cvt_res (one shared-memory sweep with a position test per step): the same HBM traffic and
+// 2-4 register phases instead of 2 (q - K) sweeps.  B in [5, 8] (rows <= 257).
+// ---------------------------------------------------------------------------------------------
+#define SEAM_THREADS 256   // 2 CTAs per SM, one tile prefetched each (measured: 5 stages at one 512-thread CTA per
+#define SEAM_NW (SEAM_THREADS / 32)   // SM 12 % slower; phase outputs stored straight to HBM 1.5x slower at u128)
+
+template <int N>
+__device__ __forceinline__ void seam_ss(uint32_t* v) {   // superset-sum over the log2(N) index bits
+#pragma unroll
+    for (int b = 1; b < N; b <<= 1)
+#pragma unroll
+        for (int t = 0; t < N; t++)
+            if (!(t & b)) v[t] ^= v[t | b];
+}
+
+template <typename T>
+__device__ __forceinline__ void seam_load_unit(T* dst, const T* src, bool ok) {
+    const uint32_t n = ok ? (uint32_t)sizeof(T) : 0u;   // src-size 0: zero fill (rows beyond the chunk)
+    if (sizeof(T) == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(n) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(n) : "memory");
+}
+
+// B = 4 + BH row bits; rows 0 .. 2^B (the last one only for classes c < 2^B)
+template <typename T, int BH>
+__global__ void __launch_bounds__(SEAM_THREADS, 2) k_cvt_seam(CvtResParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    constexpr int W = sizeof(T) / 4;        // words per unit
+    constexpr int C = 32 / W;               // classes per tile (one 128-byte row)
+    constexpr int L = 16, H = 1 << BH, NB = 4 + BH, NR = (1 << NB) + 1;
+    constexpr uint32_t BUF = (NR * 128 + 127) & ~127u;
+    constexpr int I1 = (H + SEAM_NW - 1) / SEAM_NW;   // phase-1 items (row groups) per warp
+    constexpr int I2 = L / SEAM_NW;                   // phase-2 items (low row index) per warp
+    T* data = reinterpret_cast<T*>(p.data);
+    const uint32_t M = (1u << p.K) - 1;
+    const uint32_t span = 1u << p.q;
+    const uint32_t nrb = (M + C - 1) / C;
+    const uint64_t ntiles = (p.units_per_pair >> p.q) * p.batch * nrb;
+    uint32_t* Qb = reinterpret_cast<uint32_t*>(smem_raw + 2 * BUF);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto prefetch = [&](uint64_t t, int b) {
+        const uint64_t chunk = t / nrb;
+        const uint32_t c0 = (uint32_t)(t - chunk * nrb) * C;
+        const T* dp = data + (chunk << p.q);
+        T* buf = reinterpret_cast<T*>(smem_raw + b * BUF);
+        for (uint32_t s = threadIdx.x; s < (uint32_t)NR * C; s += SEAM_THREADS) {
+            const uint32_t r = s / C, c = c0 + 1 + s % C, i = r * M + c;
+            const bool ok = c <= M && i < span;
+            seam_load_unit<T>(buf + s, dp + (ok ? i : 0), ok);
+        }
+    };
+    if (blockIdx.x < ntiles) prefetch(blockIdx.x, 0);
+    cp_async_commit();
+    int kb = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, kb++) {
+        if (t + gridDim.x < ntiles) prefetch(t + gridDim.x, (kb + 1) & 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        uint32_t* X = reinterpret_cast<uint32_t*>(smem_raw + (kb & 1) * BUF);
+        const uint64_t chunk = t / nrb;
+        const uint32_t c0 = (uint32_t)(t - chunk * nrb) * C;
+        const uint32_t c = c0 + 1 + lane / W;   // this lane's class (> M: an empty column, never stored)
+        if (!p.inverse) {
+            // phase 1: row groups g (rows L g .. L g + L): low bits of P = S x (in place) and Q = T x (Qb)
+            uint32_t v[I1][L + 1];
+#pragma unroll
+            for (int k = 0; k < I1; k++) {
+                const int g = warp + k * SEAM_NW;
+                if (g < H)
+#pragma unroll
+                    for (int u = 0; u <= L; u++) v[k][u] = X[(L * g + u) * 32 + lane];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < I1; k++) {
+                const int g = warp + k * SEAM_NW;
+                if (g < H) {
+                    uint32_t q[L];
+#pragma unroll
+                    for (int u = 0; u < L; u++) q[u] = v[k][u + 1];
+                    seam_ss<L>(v[k]);
+                    seam_ss<L>(q);
+#pragma unroll
+                    for (int u = 0; u < L; u++) {
+                        X[(L * g + u) * 32 + lane] = v[k][u];
+                        Qb[(L * g + u) * 32 + lane] = q[u];
+                    }
+                }
+            }
+            __syncthreads();
+            // phase 2: low index l (rows l + L h): high bits, the extra row 2^NB (a superset of row 0 only), the seam
+            uint32_t pv[I2][H], qv[I2][H];
+            const uint32_t xtra = X[(NR - 1) * 32 + lane];
+#pragma unroll
+            for (int k = 0; k < I2; k++) {
+                const int l = warp + k * SEAM_NW;
+#pragma unroll
+                for (int h = 0; h < H; h++) {
+                    pv[k][h] = X[(l + L * h) * 32 + lane];
+                    qv[k][h] = Qb[(l + L * h) * 32 + lane];
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < I2; k++) {
+                const int l = warp + k * SEAM_NW;
+                seam_ss<H>(pv[k]);
+                seam_ss<H>(qv[k]);
+                if (l == 0) pv[k][0] ^= xtra;
+#pragma unroll
+                for (int h = 0; h < H; h++) {
+                    const uint32_t r = l + L * h;
+                    if (r < c) X[r * 32 + lane] = pv[k][h];
+                    if (r + 1 >= c) X[(r + 1) * 32 + lane] = qv[k][h];
+                }
+            }
+        } else {
+            // phase 1: low bits of T y (rows 1 .. 2^NB shifted down by one) -> Qb
+            uint32_t v[I1][L];
+#pragma unroll
+            for (int k = 0; k < I1; k++) {
+                const int g = warp + k * SEAM_NW;
+                if (g < H) {
+#pragma unroll
+                    for (int u = 0; u < L; u++) v[k][u] = X[(L * g + u + 1) * 32 + lane];
+                    seam_ss<L>(v[k]);
+#pragma unroll
+                    for (int u = 0; u < L; u++) Qb[(L * g + u) * 32 + lane] = v[k][u];
+                }
+            }
+            __syncthreads();
+            // phase 2: high bits of T y -> x_U (rows r = w + 1 >= c, into X); then the high bits of
+            // S(x_U on U, 0 on L): the rows w + 1 of column l are column l + 1 (l = L - 1: column 0, one row group
+            // up; its row 0 is in L, and the extra row 2^NB is only its own superset)
+            uint32_t qv[I2][H];
+#pragma unroll
+            for (int k = 0; k < I2; k++) {
+                const int l = warp + k * SEAM_NW;
+#pragma unroll
+                for (int h = 0; h < H; h++) qv[k][h] = Qb[(l + L * h) * 32 + lane];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < I2; k++) {
+                const int l = warp + k * SEAM_NW;
+                seam_ss<H>(qv[k]);
+                uint32_t z[H];
+                if (l < L - 1) {
+#pragma unroll
+                    for (int h = 0; h < H; h++) {
+                        const uint32_t r = l + 1 + L * h;
+                        const bool up = r >= c;
+                        if (up) X[r * 32 + lane] = qv[k][h];
+                        z[h] = up ? qv[k][h] : 0u;
+                    }
+                    seam_ss<H>(z);
+#pragma unroll
+                    for (int h = 0; h < H; h++) Qb[(l + 1 + L * h) * 32 + lane] = z[h];
+                } else {
+                    z[0] = 0u;
+#pragma unroll
+                    for (int h = 0; h < H; h++) {
+                        const uint32_t r = L * (h + 1);
+                        const bool up = r >= c;
+                        if (up) X[r * 32 + lane] = qv[k][h];
+                        if (h + 1 < H) z[h + 1] = up ? qv[k][h] : 0u;
+                    }
+                    const uint32_t zn = (uint32_t)(NR - 1) >= c ? qv[k][H - 1] : 0u;
+                    seam_ss<H>(z);
+#pragma unroll
+                    for (int h = 0; h < H; h++) Qb[(L * h) * 32 + lane] = z[h];
+                    Qb[(NR - 1) * 32 + lane] = zn;
+                }
+            }
+            __syncthreads();
+            // phase 3: low bits of S -> v; w = (y on L, v on U); low bits of S w -> Qb (own rows)
+#pragma unroll
+            for (int k = 0; k < I1; k++) {
+                const int g = warp + k * SEAM_NW;
+                if (g < H) {
+                    uint32_t w[L];
+#pragma unroll
+                    for (int u = 0; u < L; u++) w[u] = Qb[(L * g + u) * 32 + lane];
+                    seam_ss<L>(w);
+#pragma unroll
+                    for (int u = 0; u < L; u++) {
+                        const uint32_t r = L * g + u;
+                        if (r < c) w[u] = X[r * 32 + lane];
+                    }
+                    seam_ss<L>(w);
+#pragma unroll
+                    for (int u = 0; u < L; u++) Qb[(L * g + u) * 32 + lane] = w[u];
+                }
+            }
+            __syncthreads();
+            // phase 4: high bits of S w (+ the extra row v[2^NB] = x_U[2^NB] into row 0) -> x_L
+            const uint32_t xtra = Qb[(NR - 1) * 32 + lane];
+#pragma unroll
+            for (int k = 0; k < I2; k++) {
+                const int l = warp + k * SEAM_NW;
+                uint32_t w[H];
+#pragma unroll
+                for (int h = 0; h < H; h++) w[h] = Qb[(l + L * h) * 32 + lane];
+                seam_ss<H>(w);
+                if (l == 0) w[0] ^= xtra;
+#pragma unroll
+                for (int h = 0; h < H; h++) {
+                    const uint32_t r = l + L * h;
+                    if (r < c) X[r * 32 + lane] = w[h];
+                }
+            }
+        }
+        __syncthreads();
+        // store the tile's units
+        {
+            const T* buf = reinterpret_cast<const T*>(X);
+            T* dp = data + (chunk << p.q);
+            for (uint32_t s = threadIdx.x; s < (uint32_t)NR * C; s += SEAM_THREADS) {
+                const uint32_t r = s / C, cc = c0 + 1 + s % C, i = r * M + cc;
+                if (cc <= M && i < span) dp[i] = buf[s];
+            }
+        }
+        __syncthreads();   // the buffer is refilled by the prefetch two tiles on; Qb is rewritten next tile
+    }
+    cp_async_wait<0>();
+}
+static size_t seam_smem() { return 3 * (size_t)((257 * 128 + 127) & ~127); }
+
+// ---------------------------------------------------------------------------------------------
 // Register-blocked pass for a run of Taylor steps with K <= 4 (windows of <= 5 index bits) whose
 // windows lie inside R <= 8 consecutive index bits [r_lo, r_lo + R) -- e.g. a whole CVT(8) node
 // (12 steps).  XORs act on whole elements, so each 32-bit limb is independent: in a phase a thread

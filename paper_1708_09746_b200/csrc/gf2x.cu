@@ -524,6 +524,10 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
 #undef RB_ATTR
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_res<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_res<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+#define SEAM_ATTR(T, BH) CUDA_TRY(cudaFuncSetAttribute(k_cvt_seam<T, BH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        SEAM_ATTR(uint64_t, 1) SEAM_ATTR(uint64_t, 2) SEAM_ATTR(uint64_t, 3) SEAM_ATTR(uint64_t, 4)
+        SEAM_ATTR(uint4, 1) SEAM_ATTR(uint4, 2) SEAM_ATTR(uint4, 3) SEAM_ATTR(uint4, 4)
+#undef SEAM_ATTR
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_top<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_top<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_slab<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -953,6 +957,13 @@ static bool slab_triple(const std::vector<CvtPass>& v, size_t i, int m) {
     if (!c.rb || c.rbp.r_lo != 8 || c.rbp.R != 8 || c.rbp.mode != 0 || c.rb_wb != 6) return false;
     return true;
 }
+// a residue pass that is a complete Taylor run (levels q .. K+1) with 5 <= B = q - K <= 8 row bits runs in
+// the closed form of R27 (k_cvt_seam)
+static bool seam_ok(const CvtPass& p) {
+    if (!p.res || p.ops.empty() || env_flag("GF2X_NO_SEAM")) return false;
+    const int K = p.ops[0].K, B = p.q - K;
+    return B >= 5 && B <= 8 && p.ops.front().lg == p.q && (int)p.ops.size() == B && p.ops.back().lg == K + 1;
+}
 static CvtResParams res_params(const CvtPass& p, void* data, uint64_t per, uint64_t batch, bool inverse) {
     CvtResParams prm;
     prm.data = data;
@@ -1131,6 +1142,18 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
                 case 4: k_cvt_rb<T, 4><<<g, RB_THREADS, sm, st>>>(prm); break;
                 case 5: k_cvt_rb<T, 5><<<g, RB_THREADS, sm, st>>>(prm); break;
                 default: k_cvt_rb<T, 6><<<g, RB_THREADS, sm, st>>>(prm); break;
+            }
+        } else if (p.res && seam_ok(p)) {
+            const CvtResParams prm = res_params(p, data, per, batch, inverse);
+            const uint64_t M = (1ull << prm.K) - 1, C = 32 / (sizeof(T) / 4);
+            const uint64_t ntiles = (per >> p.q) * batch * ((M + C - 1) / C);
+            ProfScope ps(sizeof(T) == 8 ? "k_cvt_seam<u64>" : "k_cvt_seam<u128>", 2.0 * per * batch * sizeof(T), st);
+            const int g = grid_for(ntiles, 1, sm_count, 2);
+            switch (p.q - prm.K) {
+                case 5: k_cvt_seam<T, 1><<<g, SEAM_THREADS, seam_smem(), st>>>(prm); break;
+                case 6: k_cvt_seam<T, 2><<<g, SEAM_THREADS, seam_smem(), st>>>(prm); break;
+                case 7: k_cvt_seam<T, 3><<<g, SEAM_THREADS, seam_smem(), st>>>(prm); break;
+                default: k_cvt_seam<T, 4><<<g, SEAM_THREADS, seam_smem(), st>>>(prm); break;
             }
         } else if (p.res) {
             CvtResParams prm;
