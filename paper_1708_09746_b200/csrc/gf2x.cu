@@ -211,13 +211,26 @@ __device__ __forceinline__ uint32_t ib_swz(uint32_t e) { return e ^ ((e >> 5) & 
 
 // halo (sharded multiply, batch 1): the tower element preceding P[0] globally (rank r-1's last one), or null
 // n_write: flat output words written (N batch when n_out = N; n_out <= N for a single product)
+// MC (R28): instead of InterleavedCombine, write D = lo64(C) ^ M hi64(C) in the NOVEL basis, where M is
+// the shift by one block written in that basis (multiplication by y = X_1):
+//     (M h)[j] = h[j-1] ^ [j odd] h[j] ^ [j even, j > 0] h[j + 2^ctz(j) - 1]      (j within its product)
+// so that iBasisCvt of the 64-bit D (in place, in `out`) is the product: half the conversion traffic of the
+// 128-bit iBasisCvt it replaces.  The partner of a tile-aligned j (ctz >= 12) lies in another tile (thread 0).
+__device__ __forceinline__ uint64_t ipsi_hi_global(const uint4 pv, const DevTables* tabs) {
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    const uint32_t w[4] = {pv.x, pv.y, pv.z, pv.w};
+    for (int L = 0; L < 4; L++)
+        for (int b = 0; b < 4; b++) acc = xor4(acc, tabs->ipsi[(L * 4 + b) * 256 + ((w[L] >> (8 * b)) & 255)]);
+    return ((uint64_t)acc.w << 32) | acc.z;   // (only the high half is needed)
+}
+template <bool MC>
 __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restrict__ P, const DevTables* tabs, uint64_t N,
                                                          uint64_t batch, uint64_t* __restrict__ out,
                                                          const uint4* __restrict__ halo, uint64_t n_write) {
     extern __shared__ __align__(1024) uint32_t ib_smem[];
     uint32_t* S = ib_smem;                    // [4][IB_TILE] limb planes (swizzled)
     uint32_t* H = ib_smem + 4 * IB_TILE;      // [2][IB_TILE] hi64 halves of every element (swizzled)
-    __shared__ uint64_t halo_hi;
+    __shared__ uint64_t halo_hi, far_hi;
     // the batch is one flat run of products (n_out = N): a tile covers IB_TILE consecutive elements, which
     // may span several small products; an element at a product boundary has no predecessor
     const uint64_t ntiles = (n_write + IB_TILE - 1) / IB_TILE;
@@ -242,15 +255,11 @@ __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restri
         // the element before the tile (its hi64 enters the tile's first output word)
         if (t == 0) {
             uint64_t hi = 0;
-            if ((w0 & (N - 1)) != 0 || halo) {   // N is a power of two
-                const uint4 pv = (w0 & (N - 1)) != 0 ? src[-1] : *halo;
-                uint4 acc = make_uint4(0, 0, 0, 0);
-                const uint32_t w[4] = {pv.x, pv.y, pv.z, pv.w};
-                for (int L = 0; L < 4; L++)
-                    for (int b = 0; b < 4; b++) acc = xor4(acc, tabs->ipsi[(L * 4 + b) * 256 + ((w[L] >> (8 * b)) & 255)]);
-                hi = ((uint64_t)acc.w << 32) | acc.z;   // (only the high half enters this tile)
-            }
+            const uint64_t jj = w0 & (N - 1);   // N is a power of two
+            if (jj != 0 || halo) hi = ipsi_hi_global(jj != 0 ? src[-1] : *halo, tabs);
             halo_hi = hi;
+            // MC: the tile's first word, if tile-aligned inside its product, also takes h[j + 2^ctz(j) - 1]
+            far_hi = (MC && jj != 0) ? ipsi_hi_global(src[(1ull << __ffsll((long long)jj) >> 1) - 1], tabs) : 0ull;
         }
         __syncthreads();
         // ---- my 32 elements: limb -> planes, in place
@@ -306,10 +315,19 @@ __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restri
 #pragma unroll
         for (int j = 0; j < 32; j++) {
             const uint32_t e = e0 + j;
+            const uint64_t jj = (w0 + e) & (N - 1);
             uint32_t plo, phi;
             if (e == 0) { plo = (uint32_t)halo_hi; phi = (uint32_t)(halo_hi >> 32); }
-            else if (((w0 + e) & (N - 1)) == 0) { plo = 0; phi = 0; }   // first word of a product
+            else if (jj == 0) { plo = 0; phi = 0; }   // first word of a product
             else { plo = H[ib_swz(e - 1)]; phi = H[IB_TILE + ib_swz(e - 1)]; }
+            if (MC && jj != 0) {
+                if (jj & 1) { plo ^= H[ib_swz(e)]; phi ^= H[IB_TILE + ib_swz(e)]; }
+                else if (e == 0) { plo ^= (uint32_t)far_hi; phi ^= (uint32_t)(far_hi >> 32); }
+                else {   // e != 0: ctz(jj) = ctz(e) < 12, the partner lies in this tile and product
+                    const uint32_t q = ib_swz(e + (e & (0u - e)) - 1);
+                    plo ^= H[q]; phi ^= H[IB_TILE + q];
+                }
+            }
             S[ib_swz(e)] = a0[j] ^ plo;
             S[IB_TILE + ib_swz(e)] = a1[j] ^ phi;
         }
@@ -538,7 +556,8 @@ static gf2x_status get_device(int* dev_out, DeviceState** st_out) {
         CUDA_TRY(cudaFuncSetAttribute(k_small<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         CUDA_TRY(cudaFuncSetAttribute(k_cvt_slab<uint4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CUDA_TRY(cudaFuncSetAttribute(k_ipsi_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_ipsi_bs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_ipsi_bs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_ipsi_bs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         st.tabs = d;
     }
     *dev_out = dev;
@@ -793,6 +812,7 @@ struct Plan {
     uint64_t a_bits = 0, b_bits = 0;
     int m, ma, mb;
     std::vector<CvtPass> cvt_a, cvt_b, icvt;
+    std::vector<CvtPass> icvt64;   // R28: iBasisCvt of the combined 64-bit sequence (mcomb_ok)
     std::vector<FftPass> fft;
     size_t off_sa, off_sb, off_wa, off_wb, bytes;
     // one product: BasisCvt split at 2^p + tail 2^j (R22); p < 0 = not split
@@ -840,6 +860,7 @@ static gf2x_status make_plan(uint64_t a_bits, uint64_t b_bits, int64_t batch, Pl
     P.cvt_a = plan_cvt(P.ma, 8);
     P.cvt_b = plan_cvt(P.mb, 8);
     P.icvt = plan_cvt(P.m, 16);
+    P.icvt64 = plan_cvt(P.m, 8);
     P.fft = plan_fft(P.m);
     if (P.batch == 1) {
         P.sa = plan_cvt_split(P.na, P.ma, 8);
@@ -876,13 +897,19 @@ static bool split_fused(const Plan& P) {
     const bool same = P.ma == P.mb && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8 && P.sa.p < 0 && P.sb.p < 0;
     return same && P.a_bits == P.b_bits && !P.cvt_a.empty() && top_rowbits(P.cvt_a[0], P.ma) >= 0 && !env_flag("GF2X_NO_FUSED_SPLIT");
 }
+// R28: InterleavedCombine before iBasisCvt (k_ipsi_bs<true>, then iBasisCvt of 64-bit words in the output
+// buffer): the output holds all N words of every product (n_out = N), no split conversion, whole ipsi tiles
+static bool mcomb_ok(const Plan& P) {
+    return P.na + P.nb == P.N && P.ic.p < 0 && (P.N * P.batch) % IB_TILE == 0 && !env_flag("GF2X_NO_MCOMB") &&
+           !env_flag("GF2X_NO_IPSI_BS");
+}
 static int small_cluster(const Plan& P);
 static int launches_of(const Plan& P) {
     if (small_cluster(P)) return 1;
     const bool same = P.ma == P.mb && P.off_sb == P.off_sa + (1ull << P.ma) * P.batch * 8 && P.sa.p < 0 && P.sb.p < 0;
     int n = split_fused(P) ? 0 : 2;  // prep a, b
     n += launches_of_split(P.sa, P.cvt_a, P.ma) + (same ? 0 : launches_of_split(P.sb, P.cvt_b, P.mb)) +
-         launches_of_split(P.ic, P.icvt, P.m);
+         (mcomb_ok(P) ? cvt_launches(P.icvt64, P.m) : launches_of_split(P.ic, P.icvt, P.m));
     const int nd = (int)P.fft.size() - 1;
     n += (same ? 1 : 2) * (nd ? nd : 1);      // forward a, b (or the changeRepr-only pass)
     n += 1;                      // fused bottom
@@ -1369,6 +1396,19 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         if ((s = launch_fft(P.fft[i], true, false, Wa, P.N, Wa, P, ds, st)) != GF2X_OK) return s;
     }
     if (stop_stage == 4) return GF2X_OK;
+    if (stop_stage == 0 && mcomb_ok(P)) {
+        // R28: changeRepr^-1 and the combine written in the novel basis (64-bit words, into the output), then
+        // iBasisCvt of those words in place: the product
+        {
+            const uint64_t n_write = P.N * P.batch;
+            ProfScope ps("k_ipsi_mcomb", 16.0 * n_write + 8.0 * n_write, st);
+            k_ipsi_bs<true><<<grid_for(n_write / IB_TILE, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(
+                Wa, ds->tabs, P.N, P.batch, c, nullptr, n_write);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("mcomb launch: ") + cudaGetErrorString(e));
+        }
+        return run_cvt<uint64_t>(P.icvt64, c, P.m, P.batch, true, smc, st);
+    }
     // iBasisCvt (tower); the novel coefficients beyond the product's length are zero (R22 split)
     if (P.ic.p >= 0) s = run_icvt_split(P.ic, Wa, smc, st);
     else s = run_cvt<uint4>(P.icvt, Wa, P.m, P.batch, true, smc, st);
@@ -1384,7 +1424,7 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         if (bs && !env_flag("GF2X_NO_IPSI_BS")) {
             const uint64_t n_write = n_out == P.N ? P.N * P.batch : n_out;
             ProfScope ps("k_ipsi_bs", 16.0 * n_write + 8.0 * total, st);
-            k_ipsi_bs<<<grid_for((n_write + IB_TILE - 1) / IB_TILE, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(
+            k_ipsi_bs<false><<<grid_for((n_write + IB_TILE - 1) / IB_TILE, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(
                 Wa, ds->tabs, P.N, P.batch, c, nullptr, n_write);
         } else {
             ProfScope ps("k_ipsi_combine", 16.0 * P.N * P.batch + 8.0 * total, st);

@@ -634,7 +634,7 @@ static gf2x_status run_sharded(const ShardGeom& S, ShardExec& X, DeviceState* ds
         const uint4* halo = r ? (const uint4*)R.buf[SB_HALO] : nullptr;
         if (Nloc % IB_TILE == 0) {
             ProfScope ps("k_ipsi_bs", 24.0 * Nloc, st);
-            k_ipsi_bs<<<grid_for(Nloc / IB_TILE, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>((const uint4*)R.buf[SB_W], ds->tabs,
+            k_ipsi_bs<false><<<grid_for(Nloc / IB_TILE, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>((const uint4*)R.buf[SB_W], ds->tabs,
                                                                                                  Nloc, 1, R.c_shard, halo, Nloc);
         } else {
             ProfScope ps("k_ipsi_combine", 24.0 * Nloc, st);

@@ -361,7 +361,7 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
     }
     if (n_out <= P.N && P.N % IB_TILE == 0 && !env_flag("GF2X_NO_IPSI_BS")) {
         ProfScope ps("k_ipsi_bs", 16.0 * n_out + 8.0 * n_out, st);
-        k_ipsi_bs<<<grid_for((n_out + IB_TILE - 1) / IB_TILE, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(Wa, ds->tabs, P.N,
+        k_ipsi_bs<false><<<grid_for((n_out + IB_TILE - 1) / IB_TILE, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(Wa, ds->tabs, P.N,
                                                                                                         1, c, nullptr, n_out);
     } else {
         ProfScope ps("k_ipsi_combine", 16.0 * P.N + 8.0 * n_out, st);

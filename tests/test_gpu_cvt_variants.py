@@ -5,7 +5,9 @@ process), against the oracle's Alg. 5 / Karatsuba on the same seeded operands:
   * GF2X_NO_CVT_TOP=1: the plain residue pass + k_prep;
   * GF2X_CVT_SLAB=1: the CVT(16) slab pass on thread-block clusters (measured slower; kept opt-in);
   * GF2X_NO_FUSED_SPLIT=1: k_cvt_top without the fused Split;
-  * GF2X_NO_RB_TMA=1: the register-blocked passes with cp.async tile loads instead of TMA (k_cvt_rb_tma)."""
+  * GF2X_NO_RB_TMA=1: the register-blocked passes with cp.async tile loads instead of TMA (k_cvt_rb_tma);
+  * GF2X_NO_MCOMB=1: iBasisCvt on the 128-bit tower elements followed by changeRepr^-1 + InterleavedCombine
+    (the default, R28, combines first in the novel basis and converts 64-bit words)."""
 import json
 import os
 import subprocess
@@ -57,7 +59,7 @@ def run_variant(env, sizes, tmp_path):
 
 
 @pytest.mark.parametrize("env", [{}, {"GF2X_NO_CVT_TOP": "1"}, {"GF2X_CVT_SLAB": "1"}, {"GF2X_NO_FUSED_SPLIT": "1"},
-                                 {"GF2X_NO_RB_TMA": "1"}])
+                                 {"GF2X_NO_RB_TMA": "1"}, {"GF2X_NO_MCOMB": "1"}])
 def test_cvt_variants_exact(env, tmp_path):
     res = run_variant(env, SIZES + BIG, tmp_path)
     for bits in SIZES + BIG:
@@ -67,10 +69,13 @@ def test_cvt_variants_exact(env, tmp_path):
         assert np.array_equal(got, want), (env, bits)
     k = set(res[1 << 24]["kernels"])
     if not env:
-        assert "k_cvt_top<u64>" in k and "k_cvt_top<u128>" in k and "k_prep" not in k
+        assert "k_cvt_top<u64>" in k and "k_ipsi_mcomb" in k and "k_prep" not in k
+        assert not any(x.endswith("<u128>") for x in k) and "k_ipsi_bs" not in k
+    if env.get("GF2X_NO_MCOMB"):
+        assert "k_cvt_top<u128>" in k and "k_ipsi_bs" in k and "k_ipsi_mcomb" not in k
     if env.get("GF2X_NO_CVT_TOP"):
         assert not any(x.startswith("k_cvt_top") for x in k) and "k_prep" in k
     if env.get("GF2X_CVT_SLAB"):
-        assert "k_cvt_slab<u64>" in k and "k_cvt_slab<u128>" in k
+        assert "k_cvt_slab<u64>" in k
     if env.get("GF2X_NO_FUSED_SPLIT"):
         assert "k_prep" in k and "k_cvt_top<u64>" in k
