@@ -15,6 +15,9 @@
 
 #define FFT_THREADS 256
 #define FFT_UNR 8
+#ifndef FFT_PSI_PF
+#define FFT_PSI_PF 1   // changeRepr pass: next tile's words loaded into registers during this tile's layers
+#endif
 #define BOT_B_MAX 6   // at most layers [0, 6) run in the fused bit-sliced bottom kernel (planner: 5)
 
 // ---------------------------------------------------------------------------------------------
@@ -305,6 +308,22 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     }
     int kt = 0;
     uint32_t tab_key = 0xFFFFFFFFu;
+    // PSI passes whose tile is one FFT_UNR-word batch per thread: the next tile's words are loaded into registers
+    // before this tile's layers (software pipelining; the pass has no room for a second tile buffer)
+    const bool psi_pf = PSI && FFT_PSI_PF && nslots == (uint32_t)FFT_UNR * blockDim.x;
+    uint64_t wn[FFT_UNR];
+    auto psi_load = [&](uint64_t tt, uint64_t* w) {
+        uint64_t pair; uint32_t base;
+        tile_geom(tt, pair, base);
+        const uint64_t* src = reinterpret_cast<const uint64_t*>(p.src) + pair * p.src_per;
+#pragma unroll
+        for (int u = 0; u < FFT_UNR; u++) {
+            const uint32_t s = threadIdx.x + u * blockDim.x;
+            const uint32_t g = base | (s & cmask) | ((s >> p.c) << p.k_lo);
+            w[u] = g < p.src_per ? src[g] : 0ull;
+        }
+    };
+    if (psi_pf && t_begin < t_end) psi_load(t_begin, wn);
     for (uint64_t t = t_begin; t < t_end; t++, kt++) {
         uint64_t pair;
         uint32_t base;
@@ -340,11 +359,16 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             const uint64_t* src = reinterpret_cast<const uint64_t*>(p.src) + pair * p.src_per;
             for (uint32_t s0 = threadIdx.x; s0 < nslots; s0 += FFT_UNR * blockDim.x) {
                 uint64_t w[FFT_UNR];
+                if (psi_pf) {
 #pragma unroll
-                for (int u = 0; u < FFT_UNR; u++) {
-                    const uint32_t s = s0 + u * blockDim.x;
-                    const uint32_t g = base | (s & cmask) | ((s >> p.c) << p.k_lo);
-                    w[u] = (s < nslots && g < p.src_per) ? src[g] : 0ull;
+                    for (int u = 0; u < FFT_UNR; u++) w[u] = wn[u];
+                } else {
+#pragma unroll
+                    for (int u = 0; u < FFT_UNR; u++) {
+                        const uint32_t s = s0 + u * blockDim.x;
+                        const uint32_t g = base | (s & cmask) | ((s >> p.c) << p.k_lo);
+                        w[u] = (s < nslots && g < p.src_per) ? src[g] : 0ull;
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < FFT_UNR; u++) {
@@ -361,6 +385,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             if (p.db) cp_async_wait<1>();   // this tile's copies have landed (the next tile's may be in flight)
             else cp_async_wait<0>();
         }
+        if (psi_pf && t + 1 < t_end) psi_load(t + 1, wn);   // in flight during this tile's layers
         __syncthreads();
         if (!INV && PSI && p.red_dst) fold_tile(base);
         // ---- layers, in groups of <= 3 (forward: from the top; inverse: from the bottom)

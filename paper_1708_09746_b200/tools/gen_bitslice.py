@@ -141,6 +141,40 @@ def bs_mul(P, a, b, l, leaf=1):
     return lo + hi
 
 
+def bs_mul_pair(P, a, b, c, l, leaf=1):
+    """a c and b c for one common multiplier c, emitted together: the c-side Karatsuba sums are formed once
+    and the two products interleave at every recursion level (independent instruction streams)."""
+    if l <= leaf:
+        return bs_mul(P, a, c, l, leaf), bs_mul(P, b, c, l, leaf)
+    h = 1 << (l - 1)
+    a0, a1, b0, b1, c0, c1 = a[:h], a[h:], b[:h], b[h:], c[:h], c[h:]
+    pa0, pb0 = bs_mul_pair(P, a0, b0, c0, l - 1, leaf)
+    pa2, pb2 = bs_mul_pair(P, a1, b1, c1, l - 1, leaf)
+    cs = [P.XOR(x, y) for x, y in zip(c0, c1)]
+    pa1, pb1 = bs_mul_pair(P, [P.XOR(x, y) for x, y in zip(a0, a1)], [P.XOR(x, y) for x, y in zip(b0, b1)], cs,
+                           l - 1, leaf)
+    out = []
+    for p0, p1, p2 in ((pa0, pa1, pa2), (pb0, pb1, pb2)):
+        p2c = apply_linmap(P, p2, linmap_matrix(1 << (h - 1), l - 1))
+        out.append([P.XOR(x, y) for x, y in zip(p0, p2c)] + [P.XOR(x, y) for x, y in zip(p1, p0)])
+    return out[0], out[1]
+
+
+def emit_mul_pair(fname, l):
+    P = Prog()
+    n = 1 << l
+    pre = ([f"const uint32_t A{i} = a[{i}];" for i in range(n)] + [f"const uint32_t B{i} = b[{i}];" for i in range(n)] +
+           [f"const uint32_t C{i} = c[{i}];" for i in range(n)])
+    ra, rb = bs_mul_pair(P, [f"A{i}" for i in range(n)], [f"B{i}" for i in range(n)], [f"C{i}" for i in range(n)], l)
+    body = pre + P.lines + [f"ra[{i}] = {ra[i]};" for i in range(n)] + [f"rb[{i}] = {rb[i]};" for i in range(n)]
+    src = (f"// two {n}-bit tower products a c, b c of 32 bit-sliced triples (common c): {P.ops['and']} AND, "
+           f"{P.ops['xor']} XOR\n"
+           f"GF2X_HD GF2X_INLINE void {fname}(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, "
+           f"const uint32_t* __restrict__ c, uint32_t* __restrict__ ra, uint32_t* __restrict__ rb) {{\n  "
+           + "\n  ".join(body) + "\n}\n")
+    return src, P.ops
+
+
 def emit_mul(fname, l):
     P = Prog()
     n = 1 << l
@@ -239,6 +273,9 @@ def main():
     parts.append(s)
     # products by a multiplier of a subfield (k_bottom layers whose multipliers are < 2^16 / < 2^8: Prop. 2,
     # each 16- / 8-bit block of the other factor is multiplied on its own)
+    sp, opsp = emit_mul_pair("bs_mul32x2", 5)
+    parts.append(sp)
+    print("bs_mul32x2 ops", opsp, file=sys.stderr)
     s16, ops16 = emit_mul("bs_mul16", 4)
     parts.append(s16)
     s8, ops8 = emit_mul("bs_mul8", 3)
