@@ -1123,7 +1123,10 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
         const int topB = top_rowbits(p, m);
         if (src && oi == 0 && (topB < 0 || inverse || sizeof(T) != 8))
             return fail(GF2X_EINVAL, "fused Split needs a top Taylor pass first");
-        if (topB >= 0) {
+        // a top run with 5..8 row bits and no fused Split: the seam form covers every class (k_cvt_top runs Alg. 2's
+        // sweeps on the first ~1.5 2^B classes)
+        const bool top_seam = topB >= 0 && !(src && oi == 0) && seam_ok(p) && env_flag("GF2X_TOP_SEAM");
+        if (topB >= 0 && !top_seam) {
             gf2x_status s = launch_cvt_top<T>(p, topB, data, m, batch, inverse, sm_count, st, oi == 0 ? src : nullptr);
             if (s != GF2X_OK) return s;
             continue;

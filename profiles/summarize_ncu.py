@@ -77,7 +77,11 @@ def main():
     def bname(k):
         if k in bmap:
             return bmap[k]
-        m = re.match(r"(k_cvt_(?:rb|res|tile|stream|top|slab))(?:_tma)?<(u64|u128)", k)
+        if k.startswith("k_ipsi_bs<1") or k.startswith("k_ipsi_bs<true"):
+            return "k_ipsi_mcomb"
+        if k.startswith("k_ipsi_bs"):
+            return "k_ipsi_bs"
+        m = re.match(r"(k_cvt_(?:rb|res|tile|stream|top|slab|seam))(?:_tma)?<(u64|u128)", k)
         if m:
             return f"{m.group(1)}<{m.group(2)}>"
         if k.startswith("k_bottom"):
