@@ -1399,7 +1399,7 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
         if ((s = launch_fft(P.fft[i], true, false, Wa, P.N, Wa, P, ds, st)) != GF2X_OK) return s;
     }
     if (stop_stage == 4) return GF2X_OK;
-    if (stop_stage == 0 && mcomb_ok(P)) {
+    if (stop_stage == 0 && mcomb_ok(P) && ((uintptr_t)c & 15) == 0) {   // (16-byte aligned: TMA / bulk copies in place)
         // R28: changeRepr^-1 and the combine written in the novel basis (64-bit words, into the output), then
         // iBasisCvt of those words in place: the product
         {

@@ -316,12 +316,16 @@ __global__ void __launch_bounds__(W2_THREADS) k_psi256_bs(const uint4* __restric
 #define IB2_GROUPS 4
 #define IB2_THREADS (IB2_GROUPS * W2_THREADS)
 #define IB2_SMEM (12 * W2_TILE * 4)
+// MC (R28 on 128-bit blocks): out block j = lo128(C_j) ^ (M hi128(C))[j] in the novel basis,
+// (M h)[j] = h[j-1] ^ [j odd] h[j] ^ [j even, j > 0] h[j + 2^ctz(j) - 1], for the 128-bit iBasisCvt that follows
+template <bool MC>
 __global__ void __launch_bounds__(IB2_THREADS, 1) k_ipsi256_bs(const uint4* __restrict__ W, uint64_t N, uint64_t batch,
                                                              const DevTables256* __restrict__ T, uint64_t* __restrict__ out) {
     extern __shared__ __align__(1024) uint32_t w2_smem[];
     uint32_t* In = w2_smem;                  // [8][W2_TILE] limb planes; afterwards [4][W2_TILE] output halves
     uint32_t* H = w2_smem + 8 * W2_TILE;     // [4][W2_TILE] hi pairs (4,5), (6,7) of every element
     __shared__ uint4 Hp;                     // predecessor's C hi128 (limbs 4..7)
+    __shared__ uint4 Hf;                     // MC: the tile-aligned first block's far partner's hi128
     const uint64_t plane = batch * N, ntiles = plane / W2_TILE;
     const uint32_t t = threadIdx.x, g = t / W2_THREADS, e0 = 32 * (t % W2_THREADS);
     const int O = g == 0 ? 4 : (g == 1 ? 6 : (g == 2 ? 0 : 2));
@@ -340,6 +344,12 @@ __global__ void __launch_bounds__(IB2_THREADS, 1) k_ipsi256_bs(const uint4* __re
             uint4 rlo = make_uint4(0, 0, 0, 0), rhi = rlo;
             if (i0 != 0) ipsi256_apply(T->ipsi, lo[-1], hi[-1], rlo, rhi);   // (L1-cached global tables)
             Hp = rhi;
+            uint4 flo = make_uint4(0, 0, 0, 0), fhi = flo;
+            if (MC && i0 != 0) {
+                const uint64_t d = (1ull << __ffsll((long long)i0) >> 1) - 1;   // 2^ctz(i0) - 1
+                ipsi256_apply(T->ipsi, lo[d], hi[d], flo, fhi);
+            }
+            Hf = fhi;
         }
         __syncthreads();
         // limbs 2g, 2g + 1 of my column: elements -> planes, in place
@@ -372,12 +382,21 @@ __global__ void __launch_bounds__(IB2_THREADS, 1) k_ipsi256_bs(const uint4* __re
         if (O < 4) {    // word 2e (O = 0: limbs 0,1 ^ C_(e-1) limbs 4,5) or 2e + 1 (O = 2: limbs 2,3 ^ limbs 6,7)
             const uint32_t* h = H + O * W2_TILE;
             const uint32_t* hp = reinterpret_cast<const uint32_t*>(&Hp) + O;
+            const uint32_t* hf = reinterpret_cast<const uint32_t*>(&Hf) + O;
             uint32_t* o = In + O * W2_TILE;
 #pragma unroll
             for (int j = 0; j < 32; j++) {
                 const uint32_t e = e0 + j;
-                const uint32_t p0 = e ? h[w2_swz(e - 1)] : hp[0];
-                const uint32_t p1 = e ? h[W2_TILE + w2_swz(e - 1)] : hp[1];
+                uint32_t p0 = e ? h[w2_swz(e - 1)] : hp[0];
+                uint32_t p1 = e ? h[W2_TILE + w2_swz(e - 1)] : hp[1];
+                if (MC && (i0 | e) != 0) {   // (tiles never straddle products: j = i0 + e)
+                    if (e & 1) { p0 ^= h[w2_swz(e)]; p1 ^= h[W2_TILE + w2_swz(e)]; }
+                    else if (e == 0) { p0 ^= hf[0]; p1 ^= hf[1]; }
+                    else {
+                        const uint32_t q = w2_swz(e + (e & (0u - e)) - 1);
+                        p0 ^= h[q]; p1 ^= h[W2_TILE + q];
+                    }
+                }
                 o[w2_swz(e)] = a0[j] ^ p0;
                 o[W2_TILE + w2_swz(e)] = a1[j] ^ p1;
             }
@@ -444,7 +463,8 @@ static gf2x_status get_tables256(DeviceState* ds, DevTables256** out) {
         delete h;
         if (e != cudaSuccess) { cudaFree(d); return fail(GF2X_ECUDA, cudaGetErrorString(e)); }
         CUDA_TRY(cudaFuncSetAttribute(k_w128_post, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_ipsi256_bs, cudaFuncAttributeMaxDynamicSharedMemorySize, IB2_SMEM));
+        CUDA_TRY(cudaFuncSetAttribute(k_ipsi256_bs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, IB2_SMEM));
+        CUDA_TRY(cudaFuncSetAttribute(k_ipsi256_bs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, IB2_SMEM));
         ds->tabs256 = d;
     }
     *out = ds->tabs256;
@@ -466,6 +486,11 @@ static void bottom_run(uint4* A, uint4* B, uint64_t total, int m, int L, int mod
 
 // stop_stage: 0 = product; 1 = after changeRepr, 2 = after FFT_LCH, 3 = after pointmul, 5 = after
 // iBasisCvt (operand a's planes left in Wa)
+// R28 for w = 128: the product fills all N blocks, whole bit-sliced tiles, a 16-byte aligned output
+static bool w128_mcomb(const PlanW128& P, const uint64_t* c, int stop_stage) {
+    return stop_stage == 0 && P.N % W2_TILE == 0 && P.na + P.nb == 2 * P.N && ((uintptr_t)c & 15) == 0 &&
+           !env_flag("GF2X_NO_W2_BS") && !env_flag("GF2X_NO_MCOMB");
+}
 static gf2x_status run_pipeline_w128(const uint64_t* a, uint64_t a_bits, const uint64_t* b, uint64_t b_bits, uint64_t* c,
                                      const PlanW128& P, void* ws, DeviceState* ds, cudaStream_t st, int stop_stage) {
     DevTables256* T256;
@@ -550,13 +575,23 @@ static gf2x_status run_pipeline_w128(const uint64_t* a, uint64_t a_bits, const u
     bottom_run(Wa, Wa, 2 * plane, P.m, L, 4, smc, st);
     for (size_t i = ndirect; i-- > 0;)
         if ((s = launch_fft(P.fft[i], true, false, Wa, P.N, Wa, Pf, ds, st)) != GF2X_OK) return s;
+    // R28: the combine in the novel basis into the output, then iBasisCvt of those 128-bit blocks in place (one plane
+    // instead of two)
+    if (w128_mcomb(P, c, stop_stage)) {
+        {
+            ProfScope ps("k_ipsi256_mcomb", 32.0 * plane + 16.0 * plane, st);
+            k_ipsi256_bs<true><<<grid_for(plane / W2_TILE, 1, smc, 2), IB2_THREADS, IB2_SMEM, st>>>(Wa, P.N, B, T256, c);
+        }
+        if ((s = check_launch("ipsi256 mcomb")) != GF2X_OK) return s;
+        return run_cvt<uint4>(P.icvt, reinterpret_cast<uint4*>(c), P.m, B, true, smc, st);
+    }
     // iBasisCvt on both planes
     if ((s = run_cvt<uint4>(P.icvt, Wa, P.m, 2 * B, true, smc, st)) != GF2X_OK) return s;
     if (stop_stage == 5) return GF2X_OK;
     // changeRepr^-1 + InterleavedCombine
     if (w2bs && P.na + P.nb == 2 * P.N) {
         ProfScope ps("k_ipsi256_bs", 32.0 * plane + 16.0 * plane, st);
-        k_ipsi256_bs<<<grid_for(plane / W2_TILE, 1, smc, 2), IB2_THREADS, IB2_SMEM, st>>>(Wa, P.N, B, T256, c);
+        k_ipsi256_bs<false><<<grid_for(plane / W2_TILE, 1, smc, 2), IB2_THREADS, IB2_SMEM, st>>>(Wa, P.N, B, T256, c);
     } else {
         const uint64_t n_out = P.na + P.nb, nblk = (n_out + 1) / 2;
         const uint64_t ctas = (nblk + IPSI256_THREADS - 1) / IPSI256_THREADS * B;
