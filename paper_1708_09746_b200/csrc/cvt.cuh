@@ -317,8 +317,10 @@ __global__ void __launch_bounds__(SEAM_THREADS, 2) k_cvt_seam(CvtResParams p) {
         const uint32_t c0 = (uint32_t)(t - chunk * nrb) * C;
         const T* dp = data + (chunk << p.q);
         T* buf = reinterpret_cast<T*>(smem_raw + b * BUF);
-        for (uint32_t s = threadIdx.x; s < (uint32_t)NR * C; s += SEAM_THREADS) {
-            const uint32_t r = s / C, c = c0 + 1 + s % C, i = r * M + c;
+        // SEAM_THREADS is a multiple of C: a thread keeps its class, its row advances by SEAM_THREADS / C
+        const uint32_t c = c0 + 1 + threadIdx.x % C, di = (SEAM_THREADS / C) * M;
+        uint32_t i = (threadIdx.x / C) * M + c;
+        for (uint32_t s = threadIdx.x; s < (uint32_t)NR * C; s += SEAM_THREADS, i += di) {
             const bool ok = c <= M && i < span;
             seam_load_unit<T>(buf + s, dp + (ok ? i : 0), ok);
         }
@@ -490,9 +492,10 @@ __global__ void __launch_bounds__(SEAM_THREADS, 2) k_cvt_seam(CvtResParams p) {
         {
             const T* buf = reinterpret_cast<const T*>(X);
             T* dp = data + (chunk << p.q);
-            for (uint32_t s = threadIdx.x; s < (uint32_t)NR * C; s += SEAM_THREADS) {
-                const uint32_t r = s / C, cc = c0 + 1 + s % C, i = r * M + cc;
-                if (cc <= M && i < span) dp[i] = buf[s];
+            const uint32_t cc = c0 + 1 + threadIdx.x % C, di = (SEAM_THREADS / C) * M;
+            if (cc <= M) {
+                uint32_t i = (threadIdx.x / C) * M + cc;
+                for (uint32_t s = threadIdx.x; s < (uint32_t)NR * C && i < span; s += SEAM_THREADS, i += di) dp[i] = buf[s];
             }
         }
         __syncthreads();   // the buffer is refilled by the prefetch two tiles on; Qb is rewritten next tile
@@ -832,10 +835,13 @@ __global__ void __launch_bounds__(TOP_THREADS, 2) k_cvt_top(CvtTopParams p) {
         const uint32_t c0 = (uint32_t)(t - pair * nrb) << p.C_log;
         T* dp = data + pair * p.units_per_pair;
         const uint64_t* sp = fuse ? (pair < p.batch0 ? p.src0 + pair * p.nsrc : p.src1 + (pair - p.batch0) * p.nsrc) : nullptr;
-        for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
-            const uint32_t r = s >> p.C_log, c = c0 + (s & (C - 1));
-            const uint32_t i = r * M + c;
-            if (c >= M || i >= span) continue;
+        // blockDim is a multiple of C: a thread keeps its class, its row advances by blockDim / C (units i by that
+        // times M; rows only grow, so the first one past the chunk ends the loop)
+        const uint32_t c = c0 + (threadIdx.x & (C - 1));
+        if (c >= M) return;
+        const uint32_t di = (blockDim.x >> p.C_log) * M;
+        uint32_t i = (threadIdx.x >> p.C_log) * M + c;
+        for (uint32_t s = threadIdx.x; s < nslots && i < span; s += blockDim.x, i += di) {
             if (fuse) {
                 const uint32_t n = (uint64_t)i < p.nsrc ? 8u : 0u;   // src-size 0: zero fill (words >= nsrc)
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(buf + s)),
@@ -899,10 +905,13 @@ __global__ void __launch_bounds__(TOP_THREADS, 2) k_cvt_top(CvtTopParams p) {
             }
         }
         T* dp = data + pair * p.units_per_pair;
-        for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) {
-            const uint32_t r = s >> p.C_log, c = c0 + (s & (C - 1));
-            const uint32_t i = r * M + c;
-            if (c < M && i < span) dp[i] = tile[s];
+        {
+            const uint32_t c = c0 + (threadIdx.x & (C - 1));
+            if (c < M) {
+                const uint32_t di = (blockDim.x >> p.C_log) * M;
+                uint32_t i = (threadIdx.x >> p.C_log) * M + c;
+                for (uint32_t s = threadIdx.x; s < nslots && i < span; s += blockDim.x, i += di) dp[i] = tile[s];
+            }
         }
         __syncthreads();
     }
