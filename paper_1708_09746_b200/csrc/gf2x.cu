@@ -258,8 +258,11 @@ __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restri
             const uint64_t jj = w0 & (N - 1);   // N is a power of two
             if (jj != 0 || halo) hi = ipsi_hi_global(jj != 0 ? src[-1] : *halo, tabs);
             halo_hi = hi;
-            // MC: the tile's first word, if tile-aligned inside its product, also takes h[j + 2^ctz(j) - 1]
-            far_hi = (MC && jj != 0) ? ipsi_hi_global(src[(1ull << __ffsll((long long)jj) >> 1) - 1], tabs) : 0ull;
+        }
+        if (MC && t == 32) {   // (another warp, so that the two table walks overlap)
+            // the tile's first word, if tile-aligned inside its product, also takes h[j + 2^ctz(j) - 1]
+            const uint64_t jj = w0 & (N - 1);
+            far_hi = jj != 0 ? ipsi_hi_global(src[(1ull << __ffsll((long long)jj) >> 1) - 1], tabs) : 0ull;
         }
         __syncthreads();
         // ---- my 32 elements: limb -> planes, in place
