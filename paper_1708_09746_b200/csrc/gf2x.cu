@@ -226,7 +226,8 @@ __device__ __forceinline__ uint64_t ipsi_hi_global(const uint4 pv, const DevTabl
 template <bool MC>
 __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restrict__ P, const DevTables* tabs, uint64_t N,
                                                          uint64_t batch, uint64_t* __restrict__ out,
-                                                         const uint4* __restrict__ halo, uint64_t n_write) {
+                                                         const uint4* __restrict__ halo, uint64_t n_write,
+                                                         uint64_t n_valid = ~0ull) {   // elements >= n_valid read as 0
     extern __shared__ __align__(1024) uint32_t ib_smem[];
     uint32_t* S = ib_smem;                    // [4][IB_TILE] limb planes (swizzled)
     uint32_t* H = ib_smem + 4 * IB_TILE;      // [2][IB_TILE] hi64 halves of every element (swizzled)
@@ -245,7 +246,8 @@ __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restri
         for (uint32_t e0 = t; e0 < IB_TILE; e0 += 16 * IB_THREADS) {
             uint4 v[16];
 #pragma unroll
-            for (int u = 0; u < 16; u++) v[u] = src[e0 + u * IB_THREADS];
+            for (int u = 0; u < 16; u++)
+                v[u] = w0 + e0 + u * IB_THREADS < n_valid ? src[e0 + u * IB_THREADS] : make_uint4(0, 0, 0, 0);
 #pragma unroll
             for (int u = 0; u < 16; u++) {
                 const uint32_t q = ib_swz(e0 + u * IB_THREADS);
@@ -262,7 +264,8 @@ __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restri
         if (MC && t == 32) {   // (another warp, so that the two table walks overlap)
             // the tile's first word, if tile-aligned inside its product, also takes h[j + 2^ctz(j) - 1]
             const uint64_t jj = w0 & (N - 1);
-            far_hi = jj != 0 ? ipsi_hi_global(src[(1ull << __ffsll((long long)jj) >> 1) - 1], tabs) : 0ull;
+            const uint64_t d = (1ull << __ffsll((long long)jj) >> 1) - 1;   // 2^ctz(jj) - 1
+            far_hi = (jj != 0 && w0 + d < n_valid) ? ipsi_hi_global(src[d], tabs) : 0ull;
         }
         __syncthreads();
         // ---- my 32 elements: limb -> planes, in place
@@ -1272,11 +1275,12 @@ static gf2x_status run_cvt_fwd_split(const CvtSplit& S, uint64_t* data, uint64_t
     return run_cvt<uint64_t>(S.hi, data + (1ull << S.p), S.j, 1, false, smc, st);
 }
 // inverse per R22: iBasisCvt_p(g_lo) + s_p(x) iBasisCvt_j(g_hi) (g vanishes from 2^p + 2^j up: the product's length)
-static gf2x_status run_icvt_split(const CvtSplit& S, uint4* data, int smc, cudaStream_t st) {
+template <typename T>
+static gf2x_status run_icvt_split(const CvtSplit& S, T* data, int smc, cudaStream_t st) {
     gf2x_status s;
-    if ((s = run_cvt<uint4>(S.lo, data, S.p, 1, true, smc, st)) != GF2X_OK) return s;
-    if ((s = run_cvt<uint4>(S.hi, data + (1ull << S.p), S.j, 1, true, smc, st)) != GF2X_OK) return s;
-    return launch_shift_xor<uint4>(data, S.p, 1ull << S.j, smc, st);
+    if ((s = run_cvt<T>(S.lo, data, S.p, 1, true, smc, st)) != GF2X_OK) return s;
+    if ((s = run_cvt<T>(S.hi, data + (1ull << S.p), S.j, 1, true, smc, st)) != GF2X_OK) return s;
+    return launch_shift_xor<T>(data, S.p, 1ull << S.j, smc, st);
 }
 
 static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* src, uint64_t src_per, uint4* dst,

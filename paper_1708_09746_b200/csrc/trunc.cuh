@@ -169,6 +169,10 @@ static bool trunc_fuse(const std::vector<FftPass>& fl, const TruncGeom& T) {
     return !env_flag("GF2X_TRUNC_LAYERED") && !env_flag("GF2X_TRUNC_NOFUSE") && fl.size() > 1 && fl[0].c == 5 &&
            fl[0].k_hi - fl[0].k_lo == 6 && fl[0].k_hi == T.m - 1 && T.j <= fl[0].k_lo;
 }
+// R28 on the truncated path (one product): the output words fit N, whole bit-sliced tiles
+static bool trunc_mcomb(const Plan& P) {
+    return P.na + P.nb <= P.N && P.N % IB_TILE == 0 && !env_flag("GF2X_NO_MCOMB") && !env_flag("GF2X_NO_IPSI_BS");
+}
 // kernel launches of one truncated multiply (the default variant)
 static int launches_of_trunc(const Plan& P, const TruncGeom& T) {
     const std::vector<FftPass> fl = plan_fft(T.m - 1), fu = plan_fft(T.j);
@@ -181,7 +185,12 @@ static int launches_of_trunc(const Plan& P, const TruncGeom& T) {
     n += 3 * ((int)fu.size() - 1) + 1;                                     // upper
     n += 2 * nred + 1;                                                     // Reduce (forward, g_lo), g_hi combine
     n += (P.na > T.H) + (P.nb > T.H);                                      // operand tails past H
-    n += launches_of_split(P.ic, P.icvt, P.m) + 1;                              // iBasisCvt, changeRepr^-1 + combine
+    if (trunc_mcomb(P)) {   // R28: changeRepr^-1 + combine, then the 64-bit iBasisCvt
+        const uint64_t n_out = P.na + P.nb;
+        n += 1 + launches_of_split(plan_cvt_split(n_out, P.m, 8), P.icvt64, P.m);
+    } else {
+        n += launches_of_split(P.ic, P.icvt, P.m) + 1;                          // iBasisCvt, changeRepr^-1 + combine
+    }
     return n;
 }
 
@@ -350,6 +359,25 @@ static gf2x_status run_pipeline_trunc(const uint64_t* a, uint64_t a_bits, const 
     }
     const uint64_t n_out = P.na + P.nb;
     if ((s = check_launch("trunc combine")) != GF2X_OK) return s;
+    if (trunc_mcomb(P)) {
+        // R28: changeRepr^-1 and the combine written in the novel basis (the coefficients g_k, k >= H + U, are zero:
+        // read as 0, no clearing), then iBasisCvt of the n_out 64-bit words -- split at 2^p + 2^j (R22) as the
+        // 128-bit path would be -- in the output when the split's extent fits it, else in Wb (then copied)
+        const CvtSplit S64 = plan_cvt_split(n_out, P.m, 8);
+        const uint64_t extent = S64.p >= 0 ? (1ull << S64.p) + (1ull << S64.j) : P.N;
+        uint64_t* D = (extent <= n_out && ((uintptr_t)c & 15) == 0) ? c : reinterpret_cast<uint64_t*>(Wb);
+        if (D != c && extent > n_out) CUDA_TRY(cudaMemsetAsync(D + n_out, 0, (extent - n_out) * 8, st));
+        {
+            ProfScope ps("k_ipsi_mcomb", 16.0 * n_out + 8.0 * n_out, st);
+            k_ipsi_bs<true><<<grid_for((n_out + IB_TILE - 1) / IB_TILE, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(
+                Wa, ds->tabs, P.N, 1, D, nullptr, n_out, T.H + T.U);
+        }
+        if ((s = check_launch("trunc mcomb")) != GF2X_OK) return s;
+        s = S64.p >= 0 ? run_icvt_split<uint64_t>(S64, D, smc, st) : run_cvt<uint64_t>(P.icvt64, D, P.m, 1, true, smc, st);
+        if (s != GF2X_OK) return s;
+        if (D != c) CUDA_TRY(cudaMemcpyAsync(c, D, n_out * 8, cudaMemcpyDeviceToDevice, st));
+        return GF2X_OK;
+    }
     // iBasisCvt on the N coefficients (or split at H, R22: only units < n_out are read afterwards), then
     // changeRepr^-1 + InterleavedCombine (as the full path)
     if (P.ic.p >= 0) {
