@@ -52,6 +52,7 @@ struct BottomParams {
     int m, L, mode;      // mode bit0: forward layers (A and B), bit1: pointmul (A <- A B), bit2: inverse layers (A)
     IdxMap map;          // local -> global index for the multipliers (identity unless sharded;
                          // the bottom layers and position bits are always below map.pos)
+    int l2pf;            // bit 0: thread 0 prefetches the CTA's next tile of A (and B) into L2
 };
 
 // (group g of limb lb) -> plane block.  Blocks of groups 32..63 are stored with their low 5 bits
@@ -269,6 +270,13 @@ __global__ void __launch_bounds__(BT_THREADS, 2 / BT_TPC) k_bottom(BottomParams 
     // drops its stores (e0 >= total)
     for (uint64_t tb = (uint64_t)blockIdx.x * BT_TPC; tb < p.ntiles; tb += (uint64_t)gridDim.x * BT_TPC) {
         const uint64_t e0 = (tb + half) << BT_BITS;
+        if ((p.l2pf & 1) && tid == 0) {   // the CTA's next tile(s) into L2 while this one runs
+            const uint64_t n0 = (tb + (uint64_t)gridDim.x * BT_TPC) << BT_BITS;
+            if (n0 + ((uint64_t)BT_TPC << BT_BITS) <= total) {
+                bulk_prefetch_l2(p.A + n0, (uint32_t)(16u << BT_BITS) * BT_TPC);
+                if (p.mode & 3) bulk_prefetch_l2(p.B + n0, (uint32_t)(16u << BT_BITS) * BT_TPC);
+            }
+        }
         __syncthreads();
         for (int i = tid; i < L * 32; i += BT_HALF) UC[i] = bt_u(i >> 5, i & 31, e0, L, p.m, p.map);
         // ---- load + bit-slice both operands (warp = limb, lane = group)
@@ -379,9 +387,12 @@ __global__ void __launch_bounds__(BT_THREADS, 2 / BT_TPC) k_bottom(BottomParams 
 static size_t bottom_smem() { return (size_t)(BT_TPC * 2 * BT_REGION + 6 * 32 + BT_TPC * (6 * 32 + 4 * 64 * 33)) * 4; }
 
 static int grid_for(uint64_t items, int per_block, int sm_count, int occ);
+static int bottom_l2pf();
 static void bottom_launch(const BottomParams& bp, int smc, cudaStream_t st) {
     const bool subw = bp.m + bp.map.bits - (bp.L - 1) <= 16;   // the lowest layer's multipliers are < 2^16
     const int g = grid_for((bp.ntiles + BT_TPC - 1) / BT_TPC, 1, smc, 2 / BT_TPC);
-    if (subw) k_bottom<true><<<g, BT_THREADS, bottom_smem(), st>>>(bp);
-    else k_bottom<false><<<g, BT_THREADS, bottom_smem(), st>>>(bp);
+    BottomParams q = bp;
+    q.l2pf = bottom_l2pf();
+    if (subw) k_bottom<true><<<g, BT_THREADS, bottom_smem(), st>>>(q);
+    else k_bottom<false><<<g, BT_THREADS, bottom_smem(), st>>>(q);
 }

@@ -120,6 +120,7 @@ struct FftParams {
     uint4* red_dst;       // c = 5, R = 6, one product (truncated FFT, trunc.cuh): the changeRepr pass (its input)
     uint32_t red_c[6];    //   or an inverse pass (its output) also folds the tile's 6 index bits [k_lo, k_hi)
                           //   with the Reduce constants red_c[k - k_lo] into red_dst[base | col]
+    int st_tma;           // double-buffered non-PSI passes: tiles leave by one TMA tensor store (map over dst)
 };
 
 // x[u] ^= c x[u + HALF], u < HALF (one Reduce level in registers; tl = the M4R-4 table of c)
@@ -218,7 +219,7 @@ __device__ __forceinline__ void fft_group_any(int r, uint4* tile, uint32_t nslot
 #endif
 // ZS: the pass holds the top layer (k_hi = m), where the multiplier-0 blocks are a large share
 template <bool INV, bool PSI, bool ZS>
-__global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
+__global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p, const __grid_constant__ CUtensorMap tm) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int R = p.k_hi - p.k_lo;
     const uint32_t nslots = 1u << (p.c + R);
@@ -308,6 +309,12 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
     }
     int kt = 0;
     uint32_t tab_key = 0xFFFFFFFFu;
+    // TMA stores (p.st_tma, double-buffered non-PSI passes): thread 0 stores the finished tile with one 4-D tensor
+    // store (dims: the 2^c-unit column run, middle bits [c, k_lo), rows [k_lo, k_hi), the rest incl. pairs); the
+    // next tile's prefetch into the other buffer is issued after the first layer group, once that store has read
+    // it (cp.async.bulk.wait_group.read)
+    // (the single-buffered PSI pass: the next tile's changeRepr writes wait for the store to have read the tile)
+    const bool stm = p.st_tma && (PSI || p.db);
     // PSI passes whose tile is one FFT_UNR-word batch per thread: the next tile's words are loaded into registers
     // before this tile's layers (software pipelining; the pass has no room for a second tile buffer)
     const bool psi_pf = PSI && FFT_PSI_PF && nslots == (uint32_t)FFT_UNR * blockDim.x;
@@ -331,7 +338,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
         if (!PSI) {
             if (p.db) {
                 tile = reinterpret_cast<uint4*>(smem_raw + tile_off + (kt & 1) * tbytes);
-                if (t + 1 < t_end) prefetch(t + 1, tile_off + ((kt + 1) & 1) * tbytes);
+                if (!stm && t + 1 < t_end) prefetch(t + 1, tile_off + ((kt + 1) & 1) * tbytes);
             } else {
                 prefetch(t, tile_off);   // single buffer: this tile's copies, waited for below
             }
@@ -354,6 +361,10 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
         }
         tab_key = key;
         // ---- load
+        if (PSI && stm && kt > 0) {
+            if (threadIdx.x == 0) bulk_wait_read<0>();
+            __syncthreads();
+        }
         if (PSI) {
             // FFT_UNR loads in flight per thread, then changeRepr of each word (M4R-8, 8 lookups)
             const uint64_t* src = reinterpret_cast<const uint64_t*>(p.src) + pair * p.src_per;
@@ -389,13 +400,23 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
         __syncthreads();
         if (!INV && PSI && p.red_dst) fold_tile(base);
         // ---- layers, in groups of <= 3 (forward: from the top; inverse: from the bottom)
+        bool first = true;
+        auto after_group = [&]() {   // (stm) the previous store has read the other buffer: refill it
+            if (!PSI && stm && first && threadIdx.x == 0) bulk_wait_read<0>();
+            __syncthreads();
+            if (!PSI && stm && first) {
+                if (t + 1 < t_end) prefetch(t + 1, tile_off + ((kt + 1) & 1) * tbytes);
+                cp_async_commit();
+            }
+            first = false;
+        };
         if (!INV) {
             int top = p.k_hi;
             while (top > p.k_lo) {
                 const int r = (top - p.k_lo) >= 3 ? 3 : (top - p.k_lo);
                 const int ka = top - r;
                 fft_group_any<INV, ZS>(r, tile, nslots, p.c + ka - p.k_lo, ka, p, tabs_sa, zf, kbt);
-                __syncthreads();
+                after_group();
                 top = ka;
             }
         } else {
@@ -403,17 +424,28 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p) {
             while (bot < p.k_hi) {
                 const int r = (p.k_hi - bot) >= 3 ? 3 : (p.k_hi - bot);
                 fft_group_any<INV, ZS>(r, tile, nslots, p.c + bot - p.k_lo, bot, p, tabs_sa, zf, kbt);
-                __syncthreads();
+                after_group();
                 bot += r;
             }
         }
         if (INV && p.red_dst) fold_tile(base);
         // ---- store
+        if (stm) {
+            fence_proxy_async_smem();   // the layers' writes before the tensor store's reads
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const uint64_t tt = t - pair * tiles_per_pair;
+                tma_store_4d(&tm, 0, (int)(tt & ((1u << midbits) - 1)), 0, (int)(pair * (N >> p.k_hi) + (tt >> midbits)), tile);
+                bulk_commit();
+            }
+            continue;
+        }
         uint4* dst = p.dst + pair * N;
         for (uint32_t s = threadIdx.x; s < nslots; s += blockDim.x) dst[base | (s & cmask) | ((s >> p.c) << p.k_lo)] = tile[s];
         __syncthreads();
     }
     if (!PSI) cp_async_wait<0>();
+    if (stm && threadIdx.x == 0) bulk_wait<0>();
 }
 
 static size_t fft2_smem(int c, int R, bool psi, bool wt_shared, bool db, bool red = false) {

@@ -227,7 +227,8 @@ template <bool MC>
 __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restrict__ P, const DevTables* tabs, uint64_t N,
                                                          uint64_t batch, uint64_t* __restrict__ out,
                                                          const uint4* __restrict__ halo, uint64_t n_write,
-                                                         uint64_t n_valid = ~0ull) {   // elements >= n_valid read as 0
+                                                         uint64_t n_valid = ~0ull,   // elements >= n_valid read as 0
+                                                         int l2pf = 0) {             // L2 prefetch of the next tile
     extern __shared__ __align__(1024) uint32_t ib_smem[];
     uint32_t* S = ib_smem;                    // [4][IB_TILE] limb planes (swizzled)
     uint32_t* H = ib_smem + 4 * IB_TILE;      // [2][IB_TILE] hi64 halves of every element (swizzled)
@@ -240,6 +241,8 @@ __global__ void __launch_bounds__(IB_THREADS, 2) k_ipsi_bs(const uint4* __restri
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint64_t w0 = tile * IB_TILE;   // first element / word of the tile (flat)
         const uint4* src = P + w0;
+        if (l2pf && t == 0 && (tile + gridDim.x + 1) * IB_TILE <= n_valid && (tile + gridDim.x + 1) * IB_TILE <= n_write)
+            bulk_prefetch_l2(P + (tile + gridDim.x) * IB_TILE, IB_TILE * 16);   // the CTA's next tile into L2
         // ---- load (coalesced), limb-planar; 16 loads in flight per thread (the tile is not prefetched: a second
         // 64 KB buffer would halve the occupancy)
 #pragma unroll 1
@@ -1083,6 +1086,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encode_fn() {
     }
     return fn;
 }
+// L2 prefetch of the next tile (GF2X_L2PF bit 0: k_bottom, bit 1: k_ipsi_bs on the R28 path)
+static int bottom_l2pf() { static const int v = env_int("GF2X_L2PF", 0, 0, 3); return v & 1; }
+static int ipsi_l2pf() { static const int v = env_int("GF2X_L2PF", 0, 0, 3); return (v >> 1) & 1; }
 static bool rb_tma_enabled() { return !env_flag("GF2X_NO_RB_TMA"); }   // measured 5 % faster (c4b)
 // mode 0: dims (column run of 2^C units, middle bits [C, r_lo), rows [r_lo, r_lo + R), the rest incl. pairs),
 // box (2^C units, 1, 2^R, 1); units as 64-bit elements (u128: 2 per unit).  Mode 1 uses 1-D bulk copies.
@@ -1167,6 +1173,8 @@ static gf2x_status run_cvt(const std::vector<CvtPass>& passes, T* data, int m, u
             const int g = grid_for(ntiles, 1, sm_count, occ);
             CUtensorMap tm;
             if (rb_tma_enabled() && p.rb_wb == 6 && make_rb_tmap<T>(prm, &tm)) {
+                static const int st_tma = env_int("GF2X_RB_ST", 2, 0, 2);   // measured: 0.074 -> 0.068 ms per c4b pass
+                prm.st_tma = st_tma;
                 k_cvt_rb_tma<T, 6><<<g, RB_THREADS, sm, st>>>(prm, tm);
                 cudaError_t e = cudaGetLastError();
                 if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("cvt rb tma launch: ") + cudaGetErrorString(e));
@@ -1283,6 +1291,23 @@ static gf2x_status run_icvt_split(const CvtSplit& S, T* data, int smc, cudaStrea
     return launch_shift_xor<T>(data, S.p, 1ull << S.j, smc, st);
 }
 
+// tensor map over an FFT pass's output for its TMA tile stores (k_fft2, p.st_tma): tower elements as two 64-bit
+// elements; dims (the 2^c-unit column run, middle bits [c, k_lo), rows [k_lo, k_hi), the rest incl. pairs)
+static bool make_fft_tmap(const FftParams& q, uint64_t N, CUtensorMap* tm) {
+    auto fn = tmap_encode_fn();
+    if (!fn) return false;
+    const int R = q.k_hi - q.k_lo;
+    const uint64_t total = N * q.batch;
+    if (q.c > 7 || R > 8 || (reinterpret_cast<uintptr_t>(q.dst) & 15)) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)2 << q.c, (cuuint64_t)1 << (q.k_lo - q.c), (cuuint64_t)1 << R, (cuuint64_t)(total >> q.k_hi)};
+    cuuint64_t strides[3] = {((cuuint64_t)1 << q.c) * 16, ((cuuint64_t)1 << q.k_lo) * 16, ((cuuint64_t)1 << q.k_hi) * 16};
+    cuuint32_t box[4] = {(cuuint32_t)2 << q.c, 1, (cuuint32_t)1 << R, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, q.dst, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* src, uint64_t src_per, uint4* dst,
                               const Plan& P, DeviceState* ds, cudaStream_t st, int operands = 1, IdxMap map = {0, 0, 0},
                               uint4* red_dst = nullptr, const uint32_t* red_c = nullptr) {
@@ -1311,9 +1336,15 @@ static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* 
     // passes holding the top layer skip the multiplier-0 blocks (a third of their butterflies at 6 layers);
     // elsewhere the check costs more than it saves
     const bool zs = f.k_hi == P.m && !map.bits;
-    if (inv) { if (zs) k_fft2<true, false, true><<<grid, FFT_THREADS, sm, st>>>(prm); else k_fft2<true, false, false><<<grid, FFT_THREADS, sm, st>>>(prm); }
-    else if (psi) { if (zs) k_fft2<false, true, true><<<grid, FFT_THREADS, sm, st>>>(prm); else k_fft2<false, true, false><<<grid, FFT_THREADS, sm, st>>>(prm); }
-    else { if (zs) k_fft2<false, false, true><<<grid, FFT_THREADS, sm, st>>>(prm); else k_fft2<false, false, false><<<grid, FFT_THREADS, sm, st>>>(prm); }
+    CUtensorMap tm;
+    // TMA tile stores (k_fft2): 1 = double-buffered non-PSI passes (measured c4b 0.571 -> 0.534 ms forward,
+    // 0.284 -> 0.267 ms inverse per pass), 2 = also the changeRepr pass
+    static const int fft_st = env_int("GF2X_FFT_ST", 1, 0, 2);
+    prm.st_tma = (((fft_st >= 1 && !psi && prm.db) || (fft_st >= 2 && psi)) && make_fft_tmap(prm, P.N, &tm)) ? 1 : 0;
+    if (!prm.st_tma) memset(&tm, 0, sizeof(tm));
+    if (inv) { if (zs) k_fft2<true, false, true><<<grid, FFT_THREADS, sm, st>>>(prm, tm); else k_fft2<true, false, false><<<grid, FFT_THREADS, sm, st>>>(prm, tm); }
+    else if (psi) { if (zs) k_fft2<false, true, true><<<grid, FFT_THREADS, sm, st>>>(prm, tm); else k_fft2<false, true, false><<<grid, FFT_THREADS, sm, st>>>(prm, tm); }
+    else { if (zs) k_fft2<false, false, true><<<grid, FFT_THREADS, sm, st>>>(prm, tm); else k_fft2<false, false, false><<<grid, FFT_THREADS, sm, st>>>(prm, tm); }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("fft launch: ") + cudaGetErrorString(e));
     return GF2X_OK;
@@ -1413,7 +1444,7 @@ static gf2x_status run_pipeline(const uint64_t* a, uint64_t a_bits, const uint64
             const uint64_t n_write = P.N * P.batch;
             ProfScope ps("k_ipsi_mcomb", 16.0 * n_write + 8.0 * n_write, st);
             k_ipsi_bs<true><<<grid_for(n_write / IB_TILE, 1, smc, 2), IB_THREADS, 6 * IB_TILE * 4, st>>>(
-                Wa, ds->tabs, P.N, P.batch, c, nullptr, n_write);
+                Wa, ds->tabs, P.N, P.batch, c, nullptr, n_write, ~0ull, ipsi_l2pf());
             cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("mcomb launch: ") + cudaGetErrorString(e));
         }
