@@ -1087,8 +1087,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encode_fn() {
     return fn;
 }
 // L2 prefetch of the next tile (GF2X_L2PF bit 0: k_bottom, bit 1: k_ipsi_bs on the R28 path)
-static int bottom_l2pf() { static const int v = env_int("GF2X_L2PF", 0, 0, 3); return v & 1; }
-static int ipsi_l2pf() { static const int v = env_int("GF2X_L2PF", 0, 0, 3); return (v >> 1) & 1; }
+static int bottom_l2pf() { static const int v = env_int("GF2X_L2PF", 1, 0, 3); return v & 1; }   // c4b: 1.941 -> 1.927 ms
+static int ipsi_l2pf() { static const int v = env_int("GF2X_L2PF", 1, 0, 3); return (v >> 1) & 1; }   // (no change measured)
 static bool rb_tma_enabled() { return !env_flag("GF2X_NO_RB_TMA"); }   // measured 5 % faster (c4b)
 // mode 0: dims (column run of 2^C units, middle bits [C, r_lo), rows [r_lo, r_lo + R), the rest incl. pairs),
 // box (2^C units, 1, 2^R, 1); units as 64-bit elements (u128: 2 per unit).  Mode 1 uses 1-D bulk copies.
@@ -1293,17 +1293,18 @@ static gf2x_status run_icvt_split(const CvtSplit& S, T* data, int smc, cudaStrea
 
 // tensor map over an FFT pass's output for its TMA tile stores (k_fft2, p.st_tma): tower elements as two 64-bit
 // elements; dims (the 2^c-unit column run, middle bits [c, k_lo), rows [k_lo, k_hi), the rest incl. pairs)
-static bool make_fft_tmap(const FftParams& q, uint64_t N, CUtensorMap* tm) {
+static bool make_fft_tmap(const FftParams& q, uint64_t N, CUtensorMap* tm, const void* base = nullptr) {
     auto fn = tmap_encode_fn();
     if (!fn) return false;
     const int R = q.k_hi - q.k_lo;
     const uint64_t total = N * q.batch;
-    if (q.c > 7 || R > 8 || (reinterpret_cast<uintptr_t>(q.dst) & 15)) return false;
+    if (!base) base = q.dst;
+    if (q.c > 7 || R > 8 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
     cuuint64_t dims[4] = {(cuuint64_t)2 << q.c, (cuuint64_t)1 << (q.k_lo - q.c), (cuuint64_t)1 << R, (cuuint64_t)(total >> q.k_hi)};
     cuuint64_t strides[3] = {((cuuint64_t)1 << q.c) * 16, ((cuuint64_t)1 << q.k_lo) * 16, ((cuuint64_t)1 << q.k_hi) * 16};
     cuuint32_t box[4] = {(cuuint32_t)2 << q.c, 1, (cuuint32_t)1 << R, 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, q.dst, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -1342,9 +1343,13 @@ static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* 
     static const int fft_st = env_int("GF2X_FFT_ST", 1, 0, 2);
     prm.st_tma = (((fft_st >= 1 && !psi && prm.db) || (fft_st >= 2 && psi)) && make_fft_tmap(prm, P.N, &tm)) ? 1 : 0;
     if (!prm.st_tma) memset(&tm, 0, sizeof(tm));
-    if (inv) { if (zs) k_fft2<true, false, true><<<grid, FFT_THREADS, sm, st>>>(prm, tm); else k_fft2<true, false, false><<<grid, FFT_THREADS, sm, st>>>(prm, tm); }
-    else if (psi) { if (zs) k_fft2<false, true, true><<<grid, FFT_THREADS, sm, st>>>(prm, tm); else k_fft2<false, true, false><<<grid, FFT_THREADS, sm, st>>>(prm, tm); }
-    else { if (zs) k_fft2<false, false, true><<<grid, FFT_THREADS, sm, st>>>(prm, tm); else k_fft2<false, false, false><<<grid, FFT_THREADS, sm, st>>>(prm, tm); }
+    CUtensorMap tm_src;
+    static const int fft_ld = env_int("GF2X_FFT_LD", 0, 0, 1);
+    prm.ld_tma = (fft_ld && prm.st_tma && !psi && prm.db && make_fft_tmap(prm, P.N, &tm_src, src)) ? 1 : 0;
+    if (!prm.ld_tma) memset(&tm_src, 0, sizeof(tm_src));
+    if (inv) { if (zs) k_fft2<true, false, true><<<grid, FFT_THREADS, sm, st>>>(prm, tm, tm_src); else k_fft2<true, false, false><<<grid, FFT_THREADS, sm, st>>>(prm, tm, tm_src); }
+    else if (psi) { if (zs) k_fft2<false, true, true><<<grid, FFT_THREADS, sm, st>>>(prm, tm, tm_src); else k_fft2<false, true, false><<<grid, FFT_THREADS, sm, st>>>(prm, tm, tm_src); }
+    else { if (zs) k_fft2<false, false, true><<<grid, FFT_THREADS, sm, st>>>(prm, tm, tm_src); else k_fft2<false, false, false><<<grid, FFT_THREADS, sm, st>>>(prm, tm, tm_src); }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(GF2X_ECUDA, std::string("fft launch: ") + cudaGetErrorString(e));
     return GF2X_OK;
