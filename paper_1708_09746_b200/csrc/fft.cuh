@@ -121,6 +121,7 @@ struct FftParams {
     uint32_t red_c[6];    //   or an inverse pass (its output) also folds the tile's 6 index bits [k_lo, k_hi)
                           //   with the Reduce constants red_c[k - k_lo] into red_dst[base | col]
     int st_tma;           // double-buffered non-PSI passes: tiles leave by one TMA tensor store (map over dst)
+    int ld_tma;           // (with st_tma) and arrive by one TMA tensor load (map over src)
 };
 
 // x[u] ^= c x[u + HALF], u < HALF (one Reduce level in registers; tl = the M4R-4 table of c)
@@ -219,7 +220,9 @@ __device__ __forceinline__ void fft_group_any(int r, uint4* tile, uint32_t nslot
 #endif
 // ZS: the pass holds the top layer (k_hi = m), where the multiplier-0 blocks are a large share
 template <bool INV, bool PSI, bool ZS>
-__global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p, const __grid_constant__ CUtensorMap tm) {
+__global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p, const __grid_constant__ CUtensorMap tm,
+                                                                const __grid_constant__ CUtensorMap tm_src) {
+    __shared__ __align__(8) uint64_t fbars[2];   // (p.ld_tma) TMA tile loads, one mbarrier per buffer
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int R = p.k_hi - p.k_lo;
     const uint32_t nslots = 1u << (p.c + R);
@@ -273,6 +276,14 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p, con
         for (int q = 1; q < 6; q++) cst = l == q ? p.red_c[q] : cst;
         build_tab_row(rtab + 128 * l, cst, threadIdx.x & 7, p.tabs->wt);
     }
+    // TMA tile loads (p.ld_tma, with p.st_tma, double-buffered non-PSI passes): thread 0 loads a tile with one 4-D
+    // tensor load (the store's geometry over src), completing on the buffer's mbarrier
+    const bool ldm = !PSI && p.db && p.st_tma && p.ld_tma;
+    if (ldm && threadIdx.x == 0) {
+        mbar_init(&fbars[0], 1);
+        mbar_init(&fbars[1], 1);
+        mbar_fence_init();
+    }
     __syncthreads();   // the first tile's table build / load reads entries other warps wrote
 
     const uint64_t N = 1ull << p.m;
@@ -303,7 +314,17 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p, con
             cp_async16(buf + s, src + (base | (s & cmask) | ((s >> p.c) << p.k_lo)));
     };
     const uint32_t tbytes = nslots * 16;
-    if (!PSI && p.db) {
+    auto tma_prefetch = [&](uint64_t t, int b) {   // thread 0 only
+        uint64_t pair; uint32_t base;
+        tile_geom(t, pair, base);
+        const uint64_t tt = t - pair * tiles_per_pair;
+        mbar_arrive_expect_tx(&fbars[b], tbytes);
+        tma_load_4d(smem_raw + tile_off + b * tbytes, &tm_src, 0, (int)(tt & ((1u << midbits) - 1)), 0,
+                    (int)(pair * (N >> p.k_hi) + (tt >> midbits)), &fbars[b]);
+    };
+    if (ldm) {
+        if (threadIdx.x == 0 && t_begin < t_end) tma_prefetch(t_begin, 0);
+    } else if (!PSI && p.db) {
         if (t_begin < t_end) prefetch(t_begin, tile_off);
         cp_async_commit();
     }
@@ -342,7 +363,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p, con
             } else {
                 prefetch(t, tile_off);   // single buffer: this tile's copies, waited for below
             }
-            cp_async_commit();
+            if (!ldm) cp_async_commit();
         }
         // ---- tables of this tile's multipliers: id -> (layer kk, block blk); they depend on base >> k_hi only
         const uint32_t key = (uint32_t)((uint64_t)base >> p.k_hi);
@@ -393,7 +414,8 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p, con
                 }
             }
         } else {
-            if (p.db) cp_async_wait<1>();   // this tile's copies have landed (the next tile's may be in flight)
+            if (ldm) mbar_wait(&fbars[kt & 1], (uint32_t)(kt >> 1) & 1);
+            else if (p.db) cp_async_wait<1>();   // this tile's copies have landed (the next tile's may be in flight)
             else cp_async_wait<0>();
         }
         if (psi_pf && t + 1 < t_end) psi_load(t + 1, wn);   // in flight during this tile's layers
@@ -402,9 +424,12 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p, con
         // ---- layers, in groups of <= 3 (forward: from the top; inverse: from the bottom)
         bool first = true;
         auto after_group = [&]() {   // (stm) the previous store has read the other buffer: refill it
-            if (!PSI && stm && first && threadIdx.x == 0) bulk_wait_read<0>();
+            if (!PSI && stm && first && threadIdx.x == 0) {
+                bulk_wait_read<0>();
+                if (ldm && t + 1 < t_end) tma_prefetch(t + 1, (kt + 1) & 1);
+            }
             __syncthreads();
-            if (!PSI && stm && first) {
+            if (!PSI && stm && first && !ldm) {
                 if (t + 1 < t_end) prefetch(t + 1, tile_off + ((kt + 1) & 1) * tbytes);
                 cp_async_commit();
             }
