@@ -338,7 +338,8 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p, con
     const bool stm = p.st_tma && (PSI || p.db);
     // PSI passes whose tile is one FFT_UNR-word batch per thread: the next tile's words are loaded into registers
     // before this tile's layers (software pipelining; the pass has no room for a second tile buffer)
-    const bool psi_pf = PSI && FFT_PSI_PF && nslots == (uint32_t)FFT_UNR * blockDim.x;
+    // (also tiles of fewer slots, e.g. one 2^9-point product of a batch: nslots / threads words per thread)
+    const bool psi_pf = PSI && FFT_PSI_PF && nslots <= (uint32_t)FFT_UNR * blockDim.x && nslots % blockDim.x == 0;
     uint64_t wn[FFT_UNR];
     auto psi_load = [&](uint64_t tt, uint64_t* w) {
         uint64_t pair; uint32_t base;
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(FFT_THREADS, FFT_MINB) k_fft2(FftParams p, con
         for (int u = 0; u < FFT_UNR; u++) {
             const uint32_t s = threadIdx.x + u * blockDim.x;
             const uint32_t g = base | (s & cmask) | ((s >> p.c) << p.k_lo);
-            w[u] = g < p.src_per ? src[g] : 0ull;
+            w[u] = (s < nslots && g < p.src_per) ? src[g] : 0ull;
         }
     };
     if (psi_pf && t_begin < t_end) psi_load(t_begin, wn);

@@ -1339,12 +1339,13 @@ static gf2x_status launch_fft(const FftPass& f, bool inv, bool psi, const void* 
     const bool zs = f.k_hi == P.m && !map.bits;
     CUtensorMap tm;
     // TMA tile stores (k_fft2): 1 = double-buffered non-PSI passes (measured c4b 0.571 -> 0.534 ms forward,
-    // 0.284 -> 0.267 ms inverse per pass), 2 = also the changeRepr pass
-    static const int fft_st = env_int("GF2X_FFT_ST", 1, 0, 2);
+    // 0.284 -> 0.267 ms inverse per pass), 2 = also the changeRepr pass (0.604 -> 0.583 ms)
+    static const int fft_st = env_int("GF2X_FFT_ST", 2, 0, 2);
     prm.st_tma = (((fft_st >= 1 && !psi && prm.db) || (fft_st >= 2 && psi)) && make_fft_tmap(prm, P.N, &tm)) ? 1 : 0;
     if (!prm.st_tma) memset(&tm, 0, sizeof(tm));
     CUtensorMap tm_src;
-    static const int fft_ld = env_int("GF2X_FFT_LD", 0, 0, 1);
+    // TMA tile loads (with the stores; non-PSI passes): c4b forward 0.532 -> 0.514 ms, inverse 0.258 -> 0.248 ms
+    static const int fft_ld = env_int("GF2X_FFT_LD", 1, 0, 1);
     prm.ld_tma = (fft_ld && prm.st_tma && !psi && prm.db && make_fft_tmap(prm, P.N, &tm_src, src)) ? 1 : 0;
     if (!prm.ld_tma) memset(&tm_src, 0, sizeof(tm_src));
     if (inv) { if (zs) k_fft2<true, false, true><<<grid, FFT_THREADS, sm, st>>>(prm, tm, tm_src); else k_fft2<true, false, false><<<grid, FFT_THREADS, sm, st>>>(prm, tm, tm_src); }
