@@ -46,6 +46,29 @@ def test_library_is_sm100a_only(lib):
     assert "sm_90" not in out and "sm_80" not in out
 
 
+def test_hot_kernels_keep_their_tma_and_cluster_instructions(lib):
+    """SASS of the shipped library (profiles/round2_s4_sass_tma.md): the FFT table passes and the CVT(8) node pass
+    move their tiles with TMA tensor loads / stores on mbarriers, the small-product kernel uses cluster barriers."""
+    from paper_1708_09746_b200 import build
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", build.LIB], capture_output=True, text=True).stdout
+    per, fn = {}, None
+    for line in sass.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            fn = m.group(1)
+            continue
+        for mn in ("UTMALDG", "UTMASTG", "SYNCS", "UCGABAR_ARV"):
+            if fn and mn in line:
+                per.setdefault(fn, set()).add(mn)
+    fft = [k for k in per if k.startswith("_Z6k_fft2")]
+    assert fft and all("UTMASTG" in per[k] for k in fft)
+    assert any({"UTMALDG", "SYNCS"} <= per[k] for k in fft)
+    rb = [k for k in per if k.startswith("_Z12k_cvt_rb_tma")]
+    assert rb and all({"UTMALDG", "UTMASTG", "SYNCS"} <= per[k] for k in rb)
+    small = [k for k in per if k.startswith("_Z7k_small")]
+    assert small and all("UCGABAR_ARV" in per[k] for k in small)
+
+
 def test_host_only_queries(lib):
     import paper_1708_09746_b200 as G
     assert G.version().startswith("gf2x-b200")
