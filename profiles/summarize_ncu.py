@@ -1,6 +1,6 @@
 """Summarise ncu outputs into profiles/ (tracked).
 
-python profiles/summarize_ncu.py <launches.csv> <full.ncu-rep> <tag> <config> ["<launch-list command>"] [multiplies]
+python profiles/summarize_ncu.py <launches.csv> <full.ncu-rep | raw-page.csv> <tag> <config> ["<launch-list command>"] [multiplies]
 writes profiles/<tag>_launches.md, profiles/<tag>_kernels.md and updates profiles/ncu_traffic.json
 (per-kernel-class DRAM bytes per launch, read by bench.py as roofline.traffic).
 """
@@ -99,7 +99,10 @@ def main():
     allt[cfg]["__step_launches"] = sum(c[0] for c in cls.values()) / nmul
     json.dump(allt, open(tj, "w"), indent=1)
     # full capture
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):   # the raw page already exported on the GPU box (`ncu -i … --page raw --csv`)
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, data = rows[0], rows[2:]
     keys = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "DRAM read"),
